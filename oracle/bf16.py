@@ -1,0 +1,31 @@
+"""Round-to-nearest-even fp32 -> bfloat16 (value returned as float32).
+
+Mixed precision keeps a half-precision copy theta16 of the fp32 weights
+(PAPER.md:193-206); on B200 the half format is bfloat16 (reading D-31) and
+theta16 = RNE(theta32) after every optimizer bucket (reading D-15).
+Pinned by tests/test_oracle_misc.py (0.1 -> 0.10009765625, 1/3 ->
+0.333984375, ties-to-even cases, NaN/Inf passthrough, torch cast cross-check).
+"""
+import numpy as np
+
+
+def round_bf16(x) -> np.ndarray:
+    """RNE of float32 values to bf16, returned as float32 arrays."""
+    f = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    bits = f.view(np.uint32).astype(np.uint64)
+    # round-to-nearest-even on the low 16 bits
+    lsb = (bits >> np.uint64(16)) & np.uint64(1)
+    rounded = (bits + np.uint64(0x7FFF) + lsb) & np.uint64(0xFFFF0000)
+    out = rounded.astype(np.uint32)
+    nan = np.isnan(f)
+    out = np.where(nan, (f.view(np.uint32) | np.uint32(0x00400000)) & np.uint32(0xFFFF0000), out)
+    return out.astype(np.uint32).view(np.float32)
+
+
+def to_bf16_bits(x) -> np.ndarray:
+    """uint16 bit patterns of RNE(x)."""
+    return (round_bf16(x).view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+
+
+def from_bf16_bits(b) -> np.ndarray:
+    return (np.asarray(b, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)

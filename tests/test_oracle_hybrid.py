@@ -1,0 +1,88 @@
+"""Pins for oracle/hybrid.py (Alg. 1 + Alg. 2; SURVEY.md §8(c.3) pins 7 and 10).
+
+The hybrid step is an exact reformulation of full-batch training: the
+pipelined, microbatched, data-parallel loss and gradients must equal the
+plain sequential full-batch ones (brute force, fp64 rel <= 1e-12)."""
+import numpy as np
+import pytest
+
+from oracle import hybrid, model
+from synth import init_params, markov_tokens
+
+TINY = model.GPTConfig(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256)
+TINY4 = model.GPTConfig(n_layers=4, hidden=32, heads=2, seq_len=16, vocab=64)
+
+
+def p64(cfg):
+    p = init_params(cfg.n_layers, cfg.hidden, cfg.seq_len, cfg.vocab, seed=42, parity=True)
+    return {k: v.astype(np.float64) for k, v in p.items()}
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+_REF = {}
+
+
+def reference(cfg, B):
+    key = (cfg, B)
+    if key not in _REF:
+        p = p64(cfg)
+        tok = markov_tokens(B, cfg.seq_len, cfg.vocab, seed=7)
+        _REF[key] = (p, tok, model.full_batch_loss_and_grads(p, cfg, tok))
+    return _REF[key]
+
+
+@pytest.mark.parametrize("cfg,gi", [(TINY, 1), (TINY, 2), (TINY4, 4)])
+@pytest.mark.parametrize("gd", [1, 2])
+@pytest.mark.parametrize("bm", [1, 2, 4])
+def test_pipelined_equals_sequential(cfg, gi, gd, bm):
+    B = 8
+    p, tok, (loss_ref, g_ref) = reference(cfg, B)
+    loss, g = hybrid.hybrid_step(p, cfg, tok, gi, gd, bm)
+    assert abs(loss - loss_ref) <= 1e-12 * abs(loss_ref)
+    assert set(g) == set(g_ref)
+    for k in g_ref:
+        assert rel(g[k], g_ref[k]) <= 1e-12, k
+
+
+def test_dp_identity_and_sum():
+    """Pin 10: G_data = 1 is the identity; the column sum over replicas equals
+    the full-batch gradient."""
+    cfg = TINY
+    p, tok, (loss_ref, g_ref) = reference(cfg, 8)
+    l1, g1 = hybrid.hybrid_step(p, cfg, tok, 1, 1, 8)
+    for k in g_ref:
+        assert np.array_equal(g1[k], g_ref[k])
+    # manual replica sum
+    half = [hybrid.hybrid_step(p, cfg, tok[j * 4:(j + 1) * 4], 1, 1, 4)[1] for j in range(2)]
+    l2, g2 = hybrid.hybrid_step(p, cfg, tok, 1, 2, 4)
+    for k in g_ref:
+        # halves were normalised by M_total = 1 each; the full batch by M_total = 2
+        assert rel(g2[k], (half[0][k] + half[1][k]) / 2) <= 1e-13
+        assert rel(g2[k], g_ref[k]) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_schedule_timing_does_not_change_numerics(seed):
+    """Random action costs reorder the schedule; accumulation order stays
+    ascending per stage, so gradients are bit-identical (D-19)."""
+    cfg = TINY4
+    p, tok, _ = reference(cfg, 8)
+    l0, g0 = hybrid.hybrid_step(p, cfg, tok, 4, 1, 1)
+    l1, g1 = hybrid.hybrid_step(p, cfg, tok, 4, 1, 1, seed=seed)
+    l2, g2 = hybrid.hybrid_step(p, cfg, tok, 4, 1, 1, policy="arrival", seed=seed)
+    assert l0 == l1 == l2
+    for k in g0:
+        assert np.array_equal(g0[k], g1[k]) and np.array_equal(g0[k], g2[k])
+
+
+def test_validation_errors():
+    p, tok, _ = reference(TINY, 8)
+    with pytest.raises(hybrid.ConfigError, match="NonDivisibleLayers"):
+        hybrid.hybrid_step(p, TINY, tok, 3, 1, 1)
+    with pytest.raises(hybrid.ConfigError, match="NonDivisibleBatch"):
+        hybrid.hybrid_step(p, TINY, tok, 1, 3, 1)
+    with pytest.raises(hybrid.ConfigError, match="NonDivisibleBatch"):
+        hybrid.hybrid_step(p, TINY, tok, 1, 2, 3)
