@@ -1,0 +1,205 @@
+/* axonn.h — C-ABI of the B200-native AxoNN hybrid training step.
+ *
+ * The library implements ONE thing: the data-parallel hot path of AxoNN
+ * (arXiv 2110.13005, /root/reference/PAPER.md), i.e. Alg. 1 `train` /
+ * `data_parallel_step` with the Alg. 2 message-driven
+ * inter-layer step, the data-parallel gradient all-reduce
+ * and the bucketed, host-offloaded optimizer with
+ * all-reduce/optimizer overlap — for a GPT-style
+ * transformer (readings D-1..D-9 in DESIGN.md §2).
+ *
+ * Conventions (all calls):
+ *  - every call returns an axonn_status; no exception crosses the ABI;
+ *  - one context per process / GPU; calls are not thread-safe; every call
+ *    makes the context's device current;
+ *  - the library owns the device memory, pinned host memory, CUDA streams,
+ *    events and NCCL communicators it creates; caller pointers are borrowed
+ *    for the duration of the call only;
+ *  - CUDA and NCCL errors are sticky: after one, only axonn_last_error and
+ *    axonn_free are valid on that context;
+ *  - there is no CPU fallback: without a usable sm_100a device axonn_init
+ *    fails with AXONN_ERR_CUDA.
+ */
+#ifndef AXONN_H
+#define AXONN_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define AXONN_API __attribute__((visibility("default")))
+#else
+#define AXONN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct axonn_ctx axonn_ctx;
+
+typedef enum {
+  AXONN_OK = 0,
+  AXONN_ERR_INVALID_ARG = -1,          /* bad pointer / size / hyperparameter */
+  AXONN_ERR_GRID_MISMATCH = -2,        /* world_size != g_inter * g_data */
+  AXONN_ERR_NONDIVISIBLE_LAYERS = -3,  /* g_inter does not divide n_layers */
+  AXONN_ERR_NONDIVISIBLE_BATCH = -4,   /* g_data * microbatch does not divide batch */
+  AXONN_ERR_OOM = -5,
+  AXONN_ERR_CUDA = -6,
+  AXONN_ERR_NCCL = -7,
+  AXONN_ERR_STATE = -8,                /* call out of order (e.g. optimizer_step without run_batch) */
+  AXONN_ERR_NONFINITE = -9,            /* non-finite gradient: step skipped, t not incremented */
+  AXONN_ERR_TIMEOUT = -10              /* scheduler watchdog: no message progress */
+} axonn_status;
+
+/* GPT shape (layers, hidden size, heads; seq and vocab PAPER.md:839-840). */
+typedef struct {
+  int n_layers, hidden, heads, seq_len, vocab;
+  uint64_t init_seed;   /* weights N(0,0.02) (D-22) generated on device; overwrite with axonn_write_tensor */
+} axonn_model_cfg;
+
+/* Optimizer and memory-optimisation knobs. */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;  /* paper: 1e-3, 0.9, 0.999, (1e-8, D-13), 0.01 */
+  float loss_scale;                           /* S (D-11); 1 for bf16 */
+  int offload;                                /* 1: fp32 theta + Adam state in pinned host memory */
+  int64_t bucket_elems;                       /* bsize in elements (D-16); paper 4M */
+  int coarsen_k;                              /* all-reduce chunk = k * bsize elements; paper 4 */
+  int pipeline_limit;                         /* 0 -> G_inter */
+} axonn_opt_cfg;
+
+/* Process placement in the G_inter x G_data grid: world_rank = j * G_inter + i
+ * (i = stage, j = replica, reading D-29).  nccl_id: 128-byte ncclUniqueId made
+ * by rank 0 with axonn_get_unique_id and broadcast by the caller (the Python
+ * binding uses torch.distributed for that; PyTorch is plumbing only).
+ * Ignored when world_size == 1. */
+typedef struct {
+  int world_rank, world_size;
+  const void* nccl_id;
+  int device;   /* CUDA ordinal */
+} axonn_dist;
+
+/* Tensor kinds for inspection (canonical oracle layout, fp32 on the host). */
+typedef enum {
+  AXONN_T_PARAM16 = 0,   /* theta16 (bf16 on device)                                   */
+  AXONN_T_GRAD = 1,      /* reduced half-precision gradient (bf16), input of the optimizer */
+  AXONN_T_MASTER = 2,    /* fp32 master theta (device or pinned host)                  */
+  AXONN_T_ADAM_M = 3,
+  AXONN_T_ADAM_V = 4,
+  AXONN_T_GRAD32 = 5     /* fp32 accumulation buffer (D-20)                            */
+} axonn_which;
+
+/* Writes rank 0's 128-byte ncclUniqueId into out. */
+AXONN_API axonn_status axonn_get_unique_id(void* out128);
+
+/* Alg. 1 l.2: validate, instantiate the nn_shard of g^{i,j},
+ * allocate theta16 and the gradient buffers on the device and theta32/m/v on
+ * the device or in pinned host memory (offload), build NCCL communicators
+ * (column all-reduce group, neighbour links).  Collective over all ranks.
+ * *out = NULL on error.  Errors: GRID_MISMATCH, NONDIVISIBLE_LAYERS,
+ * INVALID_ARG, OOM, CUDA, NCCL. */
+AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch, const axonn_model_cfg* model,
+                        const axonn_opt_cfg* opt, const axonn_dist* dist, axonn_ctx** out);
+
+/* Alg. 1 l.4-6: one data_parallel_step.  Collective (SPMD).
+ * tokens: host int32 [batch][seq_len + 1], the FULL batch (inputs = [:, :s],
+ * labels = [:, 1:]); replica j uses rows [j*batch/G_data, (j+1)*batch/G_data).
+ * Runs Alg. 2 to completion on this rank, then the half-precision gradient
+ * all-reduce over the column (chunked).  *loss_out (may be
+ * NULL) = batch-mean token cross entropy, unscaled, identical on all ranks.
+ * Errors: NONDIVISIBLE_BATCH, STATE (two run_batch without optimizer_step),
+ * TIMEOUT, CUDA, NCCL. */
+AXONN_API axonn_status axonn_run_batch(axonn_ctx* ctx, const int32_t* tokens, int batch, float* loss_out);
+
+/* Same as axonn_run_batch with this replica's shard already resident on the
+ * device: d_tokens = device int32 [batch/G_data][seq_len + 1]. */
+AXONN_API axonn_status axonn_run_batch_device(axonn_ctx* ctx, const int32_t* d_tokens, int batch,
+                                    float* loss_out);
+
+/* Alg. 1 l.7 "run the optimizer": AdamW on every parameter of
+ * this stage, bucket by bucket, each bucket's update
+ * enqueued as soon as its all-reduce chunk completes;
+ * refreshes theta16 = RNE(theta32).  Collective.  Errors: STATE, NONFINITE,
+ * CUDA, NCCL. */
+AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* ctx);
+
+/* Synchronise and release everything the context owns. */
+AXONN_API void axonn_free(axonn_ctx* ctx);
+
+AXONN_API const char* axonn_last_error(const axonn_ctx* ctx);
+
+/* Inspection (parity harness): tensors of THIS stage in canonical order
+ * (oracle layout: linear weights [out, in] row-major, QKV rows q|k|v). */
+AXONN_API int axonn_num_tensors(const axonn_ctx* ctx);
+AXONN_API axonn_status axonn_tensor_info(const axonn_ctx* ctx, int idx, char name[64], int64_t shape[2],
+                               int64_t* numel);
+/* Synchronising fp32 copies; host buffers hold numel floats.  Writing
+ * AXONN_T_GRAD for every tensor marks the gradients reduced, so
+ * axonn_optimizer_step can run without run_batch (values are rounded to bf16).
+ * Writing AXONN_T_MASTER also refreshes theta16 = RNE(theta32). */
+AXONN_API axonn_status axonn_read_tensor(axonn_ctx* ctx, int which, int idx, float* host_dst);
+AXONN_API axonn_status axonn_write_tensor(axonn_ctx* ctx, int which, int idx, const float* host_src);
+
+/* Statistics of the last batch; see AXONN_STAT_* for the index meaning. */
+enum {
+  AXONN_STAT_T_BATCH_MS = 0,      /* run_batch wall time (host)                 */
+  AXONN_STAT_T_OPT_MS = 1,        /* optimizer_step wall time                   */
+  AXONN_STAT_GEMM_MS = 2,         /* sum of K1 launch durations (profiling on)  */
+  AXONN_STAT_GEMM_FLOP = 3,       /* algorithmic FLOPs of those launches        */
+  AXONN_STAT_GEMM_LAUNCHES = 4,
+  AXONN_STAT_KERNEL_LAUNCHES = 5, /* all own kernels launched in the last batch+step */
+  AXONN_STAT_ADAM_MS = 6,         /* sum of K9 launch durations (profiling on)  */
+  AXONN_STAT_ADAM_BYTES = 7,
+  AXONN_STAT_P2P_BYTES = 8,
+  AXONN_STAT_ALLREDUCE_BYTES = 9,
+  AXONN_STAT_H2D_BYTES = 10,
+  AXONN_STAT_D2H_BYTES = 11,
+  AXONN_STAT_COUNT = 12
+};
+AXONN_API axonn_status axonn_stats(const axonn_ctx* ctx, double* out, int n);
+/* 1: bracket every K1/K9 launch with CUDA events on its stream (for the
+ * roofline numbers in bench.py); 0: off (default). */
+AXONN_API axonn_status axonn_set_profiling(axonn_ctx* ctx, int on);
+
+/* ---------------------------------------------------------------------------
+ * Kernel-level entry points (device pointers; enqueue on `stream`, a
+ * cudaStream_t or NULL for the legacy stream).  Used by the kernel parity
+ * tests and microbenchmarks.  Return 0 on success, < 0 on a bad argument or
+ * launch failure.
+ * ------------------------------------------------------------------------- */
+
+/* K1: C[z] = epilogue(alpha * A[z] * B[z]^T), bf16 in, fp32 TMEM accumulation.
+ * A: a_mn = 0 -> [M][lda] (K contiguous), a_mn = 1 -> [K][lda] (M contiguous).
+ * B: b_mn = 0 -> [N][ldb], b_mn = 1 -> [K][ldb].  Batch z in [0, Z):
+ * z1 = z % Z1, z2 = z / Z1, element offsets z1*s1 + z2*s2.  Leading
+ * dimensions and batch strides must be multiples of 8 elements and bases
+ * 16-byte aligned (TMA).  epi: 0 bf16 (+bias[N], +resid), 1 bias + GeLU
+ * (stores pre-activation to aux), 2 multiply by GeLU'(aux), 3 fp32
+ * (accumulate = 1 adds into C).  causal: 0 none, 1 skip tiles above the
+ * diagonal, 2 k < m0 + 128, 3 k >= m0.  col_group_in/out: column remap
+ * c -> (c / in) * out + c % in (0 = identity); n_valid: columns >= n_valid are
+ * not stored (0 = N). */
+typedef struct {
+  int M, N, K, Z, Z1;
+  const void* A; int64_t lda, a_s1, a_s2; int a_mn;
+  const void* B; int64_t ldb, b_s1, b_s2; int b_mn;
+  void* C; int64_t ldc, c_s1, c_s2;
+  int epi, causal, accumulate, col_group_in, col_group_out, n_valid;
+  const void* bias; const void* resid; int64_t ld_resid; void* aux; int64_t ld_aux;
+  float alpha;
+  int max_ctas;
+} axonn_gemm_args;
+AXONN_API int axonn_k_gemm(const axonn_gemm_args* args, void* stream);
+
+/* K9: fused AdamW over n elements (reading D-14 op order, IEEE round-to-nearest,
+ * no FMA contraction).  g16: bf16 gradients; theta/m/v fp32 (in place);
+ * theta16: bf16 out = RNE(theta).  Scalars as produced by the host in double
+ * and rounded once to fp32: decay = 1 - lr*wd, b1, omb1 = 1 - b1, b2,
+ * omb2 = 1 - b2, step = lr / (1 - b1^t), bc2_sqrt = sqrt(1 - b2^t), eps,
+ * inv_scale = 1 / S. */
+AXONN_API int axonn_k_adamw(int64_t n, const void* g16, float* theta, float* m, float* v, void* theta16,
+                  const float scalars[9], void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AXONN_H */

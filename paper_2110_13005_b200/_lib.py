@@ -1,0 +1,91 @@
+"""ctypes binding of libaxonn.so (include/axonn.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; there is
+no Python or CPU fallback.  If the shared library is missing or cannot be
+loaded this module raises immediately."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libaxonn.so")
+
+_lib = None
+
+
+class GemmArgs(C.Structure):
+    _fields_ = [("M", C.c_int), ("N", C.c_int), ("K", C.c_int), ("Z", C.c_int), ("Z1", C.c_int),
+                ("A", C.c_void_p), ("lda", C.c_int64), ("a_s1", C.c_int64), ("a_s2", C.c_int64),
+                ("a_mn", C.c_int),
+                ("B", C.c_void_p), ("ldb", C.c_int64), ("b_s1", C.c_int64), ("b_s2", C.c_int64),
+                ("b_mn", C.c_int),
+                ("C", C.c_void_p), ("ldc", C.c_int64), ("c_s1", C.c_int64), ("c_s2", C.c_int64),
+                ("epi", C.c_int), ("causal", C.c_int), ("accumulate", C.c_int),
+                ("col_group_in", C.c_int), ("col_group_out", C.c_int), ("n_valid", C.c_int),
+                ("bias", C.c_void_p), ("resid", C.c_void_p), ("ld_resid", C.c_int64),
+                ("aux", C.c_void_p), ("ld_aux", C.c_int64),
+                ("alpha", C.c_float), ("max_ctas", C.c_int)]
+
+
+class ModelCfg(C.Structure):
+    _fields_ = [("n_layers", C.c_int), ("hidden", C.c_int), ("heads", C.c_int),
+                ("seq_len", C.c_int), ("vocab", C.c_int), ("init_seed", C.c_uint64)]
+
+
+class OptCfg(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("weight_decay", C.c_float), ("loss_scale", C.c_float), ("offload", C.c_int),
+                ("bucket_elems", C.c_int64), ("coarsen_k", C.c_int), ("pipeline_limit", C.c_int)]
+
+
+class Dist(C.Structure):
+    _fields_ = [("world_rank", C.c_int), ("world_size", C.c_int), ("nccl_id", C.c_void_p),
+                ("device", C.c_int)]
+
+
+def _declare(lib):
+    P, I, I64, F = C.c_void_p, C.c_int, C.c_int64, C.c_float
+    sig = {
+        "axonn_get_unique_id": (I, [P]),
+        "axonn_init": (I, [I, I, I, C.POINTER(ModelCfg), C.POINTER(OptCfg), C.POINTER(Dist),
+                           C.POINTER(C.c_void_p)]),
+        "axonn_run_batch": (I, [P, P, I, C.POINTER(F)]),
+        "axonn_run_batch_device": (I, [P, P, I, C.POINTER(F)]),
+        "axonn_optimizer_step": (I, [P]),
+        "axonn_free": (None, [P]),
+        "axonn_last_error": (C.c_char_p, [P]),
+        "axonn_num_tensors": (I, [P]),
+        "axonn_tensor_info": (I, [P, I, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+        "axonn_read_tensor": (I, [P, I, I, P]),
+        "axonn_write_tensor": (I, [P, I, I, P]),
+        "axonn_stats": (I, [P, C.POINTER(C.c_double), I]),
+        "axonn_set_profiling": (I, [P, I]),
+        "axonn_k_gemm": (I, [C.POINTER(GemmArgs), P]),
+        "axonn_k_adamw": (I, [I64, P, P, P, P, P, C.POINTER(F), P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name, None)
+        if fn is None:
+            continue
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def load():
+    """Load (building first if needed) the in-tree libaxonn.so."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            from . import build
+            build.build()
+        _lib = _declare(C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL))
+    return _lib
+
+
+def exported_symbols():
+    """Names declared with AXONN_API in include/axonn.h."""
+    import re
+    hdr = os.path.join(os.path.dirname(HERE), "include", "axonn.h")
+    return re.findall(r"AXONN_API\s+[\w\s\*]+?\b(axonn_\w+)\(", open(hdr).read())

@@ -1,0 +1,27 @@
+// Kernel-level C-ABI entry points (include/axonn.h, "Kernel-level entry points").
+#include <cstring>
+
+#include "../../include/axonn.h"
+#include "kernels.h"
+
+extern "C" int axonn_k_gemm(const axonn_gemm_args* a, void* stream) {
+  if (!a) return -1;
+  axonn::GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.M = a->M; g.N = a->N; g.K = a->K; g.Z = a->Z; g.Z1 = a->Z1;
+  g.A = a->A; g.lda = a->lda; g.a_s1 = a->a_s1; g.a_s2 = a->a_s2; g.a_mn = a->a_mn;
+  g.B = a->B; g.ldb = a->ldb; g.b_s1 = a->b_s1; g.b_s2 = a->b_s2; g.b_mn = a->b_mn;
+  g.C = a->C; g.ldc = a->ldc; g.c_s1 = a->c_s1; g.c_s2 = a->c_s2;
+  g.epi = a->epi; g.causal = a->causal; g.accumulate = a->accumulate;
+  g.col_group_in = a->col_group_in; g.col_group_out = a->col_group_out; g.n_valid = a->n_valid;
+  g.bias = a->bias; g.resid = a->resid; g.ld_resid = a->ld_resid;
+  g.aux = a->aux; g.ld_aux = a->ld_aux; g.alpha = a->alpha; g.max_ctas = a->max_ctas;
+  return axonn::gemm_launch(g, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int axonn_k_adamw(int64_t n, const void* g16, float* theta, float* m, float* v,
+                             void* theta16, const float scalars[9], void* stream) {
+  if (!g16 || !theta || !m || !v || !theta16 || !scalars || n < 0) return -1;
+  return axonn::adamw_launch(n, g16, theta, m, v, theta16, scalars,
+                             reinterpret_cast<cudaStream_t>(stream));
+}

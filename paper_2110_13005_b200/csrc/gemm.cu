@@ -1,0 +1,390 @@
+// K1: persistent, warp-specialised bf16 GEMM on tcgen05 tensor cores (sm_100a).
+//
+//   C[z] (epilogue)= A[z] (M x K) * B[z] (N x K)^T       fp32 accumulation in TMEM
+//
+// Every contraction of the transformer layer ("transformer
+// kernel") runs through this kernel:
+// forward X W^T (A, B K-major), dgrad dY W (B MN-major), wgrad dY^T X (A and
+// B MN-major) and the batched attention products (4-D TMA maps over
+// (sample, head)).  Layout of one CTA (192 threads, 1 CTA / SM):
+//   warp 0      TMA producer  (cp.async.bulk.tensor, SWIZZLE_128B, OOB zero fill)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  epilogue: tcgen05.ld -> registers -> fused epilogue -> global
+// smem ring of 4 stages (A 128x64 + B BNx64 bf16), TMEM double-buffered
+// accumulators (2 x BN fp32 columns) so the epilogue of tile i overlaps the
+// MMAs of tile i+1.  Tiles are walked persistently (tile = blockIdx.x +
+// k*gridDim.x, M fastest so B tiles are shared through L2).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdio>
+#include <cstring>
+
+#include "ptx.cuh"
+#include "kernels.h"
+
+namespace axonn {
+
+constexpr int BM = 128, BK = 64, STAGES = 4;
+
+struct GemmParams {
+  int M, N, K, Z, Z1;
+  int a_mn, b_mn, causal, epi, accumulate;
+  int col_group_in, col_group_out, n_valid;
+  void* C;
+  long long ldc, c_s1, c_s2;
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* resid;
+  long long ld_resid;
+  __nv_bfloat16* aux;
+  long long ld_aux;
+  float alpha;
+  int num_m, num_n, total;
+};
+
+__device__ __forceinline__ bool tile_coords(const GemmParams& p, int BN, int t, int& z, int& m0,
+                                            int& n0, int& kb0, int& kb1) {
+  int per = p.num_m * p.num_n;
+  z = t / per;
+  int r = t - z * per;
+  int nb = r / p.num_m;
+  int mb = r - nb * p.num_m;
+  m0 = mb * BM;
+  n0 = nb * BN;
+  int lo = 0, hi = p.K;
+  if (p.causal == 1 && n0 > m0 + BM - 1) return false;   // scores tile above the diagonal
+  if (p.causal == 2) hi = min(p.K, m0 + BM);             // keys <= last query of the tile
+  if (p.causal == 3) lo = m0;                            // queries >= first key of the tile
+  kb0 = lo / BK;
+  kb1 = (hi + BK - 1) / BK;
+  return kb1 > kb0;
+}
+
+__device__ __forceinline__ float gelu_f(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  return 0.5f * x * (1.0f + tanhf(c * (x + a * x * x * x)));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  float t = tanhf(c * (x + a * x * x * x));
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * c * (1.0f + 3.0f * a * x * x);
+}
+
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int row, int col0,
+                                               const uint32_t (&r)[32]) {
+  if (row >= p.M) return;
+  const int z1 = z % p.Z1, z2 = z / p.Z1;
+  const int lim = min(p.n_valid, p.N);
+  const int ncols = min(32, lim - col0);
+  if (ncols <= 0) return;
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+
+  if (p.epi == EPI_F32) {
+    float* C = reinterpret_cast<float*>(p.C) + z2 * p.c_s2 + z1 * p.c_s1 + row * p.ldc + col0;
+    if (ncols == 32 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) {
+      float4* C4 = reinterpret_cast<float4*>(C);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        if (p.accumulate) {
+          float4 c = C4[i];
+          o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+        }
+        C4[i] = o;
+      }
+    } else {
+      for (int i = 0; i < ncols; ++i) C[i] = p.accumulate ? C[i] + v[i] : v[i];
+    }
+    return;
+  }
+  if (p.bias) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < ncols) v[i] += __bfloat162float(p.bias[col0 + i]);
+  }
+  if (p.epi == EPI_BIAS_GELU) {
+    __nv_bfloat16* aux = p.aux + row * p.ld_aux + col0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (i < ncols) {
+        __nv_bfloat16 pre = __float2bfloat16_rn(v[i]);
+        aux[i] = pre;
+        v[i] = gelu_f(__bfloat162float(pre));
+      }
+    }
+  } else if (p.epi == EPI_DGELU) {
+    const __nv_bfloat16* aux = p.aux + row * p.ld_aux + col0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < ncols) v[i] *= gelu_grad_f(__bfloat162float(aux[i]));
+  }
+  if (p.resid) {
+    const __nv_bfloat16* rs = p.resid + row * p.ld_resid + col0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < ncols) v[i] += __bfloat162float(rs[i]);
+  }
+  __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C) + z2 * p.c_s2 + z1 * p.c_s1 + row * p.ldc;
+  if (p.col_group_in == 0) {
+    __nv_bfloat16* dst = C + col0;
+    if (ncols == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
+        uint4 o;
+        o.x = *reinterpret_cast<uint32_t*>(&h0);
+        o.y = *reinterpret_cast<uint32_t*>(&h1);
+        o.z = *reinterpret_cast<uint32_t*>(&h2);
+        o.w = *reinterpret_cast<uint32_t*>(&h3);
+        d4[i] = o;
+      }
+    } else {
+      for (int i = 0; i < ncols; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+    }
+  } else {
+    for (int i = 0; i < ncols; ++i) {
+      int c = col0 + i;
+      int dc = (c / p.col_group_in) * p.col_group_out + (c % p.col_group_in);
+      C[dc] = __float2bfloat16_rn(v[i]);
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap mapA,
+                      const __grid_constant__ CUtensorMap mapB, const GemmParams p) {
+  constexpr int A_BYTES = BM * BK * 2;
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapA);
+    tma_prefetch_desc(&mapB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
+        int z, m0, n0, kb0, kb1;
+        if (!tile_coords(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+        const int z1 = z % p.Z1, z2 = z / p.Z1;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t* sA = smem + stage * STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          const int k0 = kb * BK;
+          if (!p.a_mn) {
+            tma_load_4d(sA, &mapA, &full[stage], k0, m0, z1, z2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_4d(sA + j * 8192, &mapA, &full[stage], m0 + 64 * j, k0, z1, z2);
+          }
+          if (!p.b_mn) {
+            tma_load_4d(sB, &mapB, &full[stage], k0, n0, z1, z2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_4d(sB + j * 8192, &mapB, &full[stage], n0 + 64 * j, k0, z1, z2);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(BM, BN, p.a_mn, p.b_mn);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
+        int z, m0, n0, kb0, kb1;
+        if (!tile_coords(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t b_base = a_base + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad = p.a_mn ? umma_desc_sw128(a_base + k * 2048, 8192, 1024)
+                                 : umma_desc_sw128(a_base + k * 32, 16, 1024);
+            uint64_t bd = p.b_mn ? umma_desc_sw128(b_base + k * 2048, 8192, 1024)
+                                 : umma_desc_sw128(b_base + k * 32, 16, 1024);
+            mma_bf16_ss(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+        ++it;
+      }
+    }
+  } else {
+    const int q = warp & 3;   // TMEM lane quarter this warp may access
+    int it = 0;
+    for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
+      int z, m0, n0, kb0, kb1;
+      if (!tile_coords(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      for (int c = 0; c < BN; c += 32) {
+        if (n0 + c >= p.N) break;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c, r);
+        epilogue_chunk(p, z, row, n0 + c, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      ++it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t get_encoder() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(ptr);
+  }
+  return fn;
+}
+
+// 4-D bf16 map (inner, outer, z1, z2); strides in elements; box (64, box_outer, 1, 1).
+static int make_map(CUtensorMap* map, const void* base, long long inner, long long outer,
+                    long long ld, int Z1, long long s1, int Z2, long long s2, int box_outer) {
+  PFN_encodeTiled_t enc = get_encoder();
+  if (!enc) return -1;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 2) % 16) return -2;
+  cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)Z1, (cuuint64_t)Z2};
+  long long st1 = Z1 > 1 ? s1 : ld * outer;
+  long long st2 = Z2 > 1 ? s2 : st1 * Z1;
+  if ((st1 * 2) % 16 || (st2 * 2) % 16) return -2;
+  cuuint64_t strides[3] = {(cuuint64_t)(ld * 2), (cuuint64_t)(st1 * 2), (cuuint64_t)(st2 * 2)};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_outer, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -3;
+}
+
+static int g_num_sms = 0;
+
+template <int BN>
+static int launch_bn(const GemmArgs& g, cudaStream_t st) {
+  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM) != cudaSuccess)
+      return -10;
+    attr_set = true;
+  }
+  CUtensorMap ma, mb;
+  int Z2 = g.Z / g.Z1;
+  int rc;
+  if (!g.a_mn)
+    rc = make_map(&ma, g.A, g.K, g.M, g.lda, g.Z1, g.a_s1, Z2, g.a_s2, BM);
+  else
+    rc = make_map(&ma, g.A, g.M, g.K, g.lda, g.Z1, g.a_s1, Z2, g.a_s2, 64);
+  if (rc) return rc;
+  if (!g.b_mn)
+    rc = make_map(&mb, g.B, g.K, g.N, g.ldb, g.Z1, g.b_s1, Z2, g.b_s2, BN);
+  else
+    rc = make_map(&mb, g.B, g.N, g.K, g.ldb, g.Z1, g.b_s1, Z2, g.b_s2, 64);
+  if (rc) return rc;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.M = g.M; p.N = g.N; p.K = g.K; p.Z = g.Z; p.Z1 = g.Z1;
+  p.a_mn = g.a_mn; p.b_mn = g.b_mn; p.causal = g.causal; p.epi = g.epi;
+  p.accumulate = g.accumulate;
+  p.col_group_in = g.col_group_in; p.col_group_out = g.col_group_out;
+  p.n_valid = g.n_valid > 0 ? g.n_valid : g.N;
+  p.C = g.C; p.ldc = g.ldc; p.c_s1 = g.c_s1; p.c_s2 = g.c_s2;
+  p.bias = reinterpret_cast<const __nv_bfloat16*>(g.bias);
+  p.resid = reinterpret_cast<const __nv_bfloat16*>(g.resid);
+  p.ld_resid = g.ld_resid;
+  p.aux = reinterpret_cast<__nv_bfloat16*>(g.aux);
+  p.ld_aux = g.ld_aux;
+  p.alpha = g.alpha;
+  p.num_m = (g.M + BM - 1) / BM;
+  p.num_n = (g.N + BN - 1) / BN;
+  p.total = p.num_m * p.num_n * g.Z;
+  if (g_num_sms == 0) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int grid = p.total < g_num_sms ? p.total : g_num_sms;
+  if (g.max_ctas > 0 && grid > g.max_ctas) grid = g.max_ctas;
+  gemm_bf16_tcgen05<BN><<<grid, 192, SMEM, st>>>(ma, mb, p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int gemm_launch(const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.Z <= 0 || g.Z1 <= 0 || g.Z % g.Z1) return -1;
+  if (g.N <= 128) return launch_bn<128>(g, st);
+  return launch_bn<256>(g, st);
+}
+
+}  // namespace axonn

@@ -1,0 +1,59 @@
+// Internal launcher declarations for the sm_100a kernels (not part of the C-ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace axonn {
+
+enum Epi { EPI_BF16 = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3 };
+
+struct GemmArgs {
+  int M, N, K;          // per-batch GEMM: C[M,N] = A[M,K] * B[N,K]^T
+  int Z, Z1;            // batch count; z1 = z % Z1, z2 = z / Z1 index the 4-D TMA maps
+  const void* A;        // bf16; K-major: [M][lda] ; MN-major (a_mn=1): [K][lda]
+  long long lda, a_s1, a_s2;
+  int a_mn;
+  const void* B;        // bf16; K-major: [N][ldb] ; MN-major (b_mn=1): [K][ldb]
+  long long ldb, b_s1, b_s2;
+  int b_mn;
+  void* C;              // bf16 or fp32 (EPI_F32)
+  long long ldc, c_s1, c_s2;
+  int epi, causal, accumulate;
+  int col_group_in, col_group_out, n_valid;
+  const void* bias;     // bf16 [N]
+  const void* resid;    // bf16 [M][ld_resid]
+  long long ld_resid;
+  void* aux;            // bf16 [M][ld_aux]: GeLU pre-activation (stored by BIAS_GELU, read by DGELU)
+  long long ld_aux;
+  float alpha;
+  int max_ctas;
+};
+
+int gemm_launch(const GemmArgs& g, cudaStream_t st);
+int adamw_launch(long long n, const void* g16, float* theta, float* m, float* v, void* theta16,
+                 const float* scalars9, cudaStream_t st);
+
+// ops.cu
+int embed_fwd(const int32_t* tok, long long tok_ld, int b, int s, int h, const void* etok,
+              const void* epos, void* out, cudaStream_t st);
+int embed_bwd(const int32_t* tok, long long tok_ld, int b, int s, int h, int vocab, const void* dx,
+              float* detok, float* dpos, cudaStream_t st);
+int ln_fwd(const void* x, int rows, int h, const void* g, const void* b, void* y, float* mean,
+           float* rstd, cudaStream_t st);
+int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int h,
+           const void* g, const void* dres, void* dx, cudaStream_t st);
+int colsum_chunks(int rows);
+int colsum(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int n,
+           float* workspace, float* out_b, float* out_g, int accumulate, cudaStream_t st);
+int softmax_fwd(const float* S, long long nrows, int s, void* P, cudaStream_t st);
+int softmax_bwd(const void* P, const float* dP, long long nrows, int s, float scale, void* dS,
+                cudaStream_t st);
+int xent(void* z, const int32_t* labels, long long lab_ld, int rows, int s, int V, float coef,
+         float* row_loss, cudaStream_t st);
+int reduce_sum(const float* x, int n, float scale, double* out, cudaStream_t st);
+int cast_f32_bf16(const float* in, void* out, long long n, cudaStream_t st);
+int cast_bf16_f32(const void* in, float* out, long long n, cudaStream_t st);
+int init_normal(void* out, float* master, long long n, uint64_t seed, float mean, float stdv,
+                cudaStream_t st);
+
+}  // namespace axonn

@@ -1,0 +1,571 @@
+// HBM-bound kernels of the stage forward/backward:
+// embedding gather / deterministic scatter-add, LayerNorm forward/backward
+// (warp per row, 16-byte vectors, warp-shuffle reductions, fp32 statistics),
+// column reductions for bias / LN parameter gradients (two-stage, fixed
+// order => bitwise reproducible), causal softmax forward/backward over
+// attention score rows, fused LM-head cross entropy (loss pre-divided by the
+// number of microbatches), fp32 -> bf16 gradient cast.
+// Readings: D-5 tanh GeLU (fused in the GEMM epilogue), D-6 LN eps 1e-5 with
+// biased variance, D-7 scale 1/sqrt(d), D-8 causal mask, D-9 loss
+// normalisation.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cfloat>
+
+#include "kernels.h"
+
+namespace axonn {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+static int g_sms_ops = 0;
+static int num_sms() {
+  if (!g_sms_ops) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms_ops, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_sms_ops;
+}
+static inline int ok() { return cudaGetLastError() == cudaSuccess ? 0 : -11; }
+
+// ------------------------------------------------------------------ embedding
+// x0[t] = E_tok[tok[t]] + E_pos[t % s]   (D-1: learned token + position embeddings)
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, long long tok_ld, int s, int rows,
+                                 int h, const __nv_bfloat16* __restrict__ etok,
+                                 const __nv_bfloat16* __restrict__ epos,
+                                 __nv_bfloat16* __restrict__ out) {
+  const int warps = blockDim.x / 32;
+  const int row = blockIdx.x * warps + threadIdx.x / 32;
+  if (row >= rows) return;
+  const int lane = threadIdx.x % 32;
+  const int b = row / s, t = row % s;
+  const int id = tok[b * tok_ld + t];
+  const __nv_bfloat16* e = etok + (long long)id * h;
+  const __nv_bfloat16* p = epos + (long long)t * h;
+  __nv_bfloat16* o = out + (long long)row * h;
+  for (int c = lane * 8; c < h; c += 256) {
+    float a[8], bb[8];
+    load8(e + c, a);
+    load8(p + c, bb);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] += bb[i];
+    store8(o + c, a);
+  }
+}
+
+int embed_fwd(const int32_t* tok, long long tok_ld, int b, int s, int h, const void* etok,
+              const void* epos, void* out, cudaStream_t st) {
+  int rows = b * s;
+  embed_fwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>(
+      tok, tok_ld, s, rows, h, (const __nv_bfloat16*)etok, (const __nv_bfloat16*)epos,
+      (__nv_bfloat16*)out);
+  return ok();
+}
+
+// dE_tok[v] += sum_{t: tok[t] = v} dx[t], in ascending t: every block owns a
+// range of 32 vocabulary rows and scans all tokens in order (deterministic, no
+// atomics, no sort).  dE_pos[t] += sum_b dx[b, t] (fixed b order).
+constexpr int EMB_VROWS = 32;
+__global__ void embed_bwd_tok_kernel(const int32_t* __restrict__ tok, long long tok_ld, int b, int s,
+                                     int h, int vocab, const __nv_bfloat16* __restrict__ dx,
+                                     float* __restrict__ detok) {
+  const int v0 = blockIdx.x * EMB_VROWS;
+  const int ncol_chunks = h / 8;
+  __shared__ int hits[1024];
+  __shared__ int nhits;
+  const int rows = b * s;
+  for (int base = 0; base < rows; base += 1024) {
+    if (threadIdx.x == 0) nhits = 0;
+    __syncthreads();
+    // ordered compaction of matching token positions in [base, base+1024)
+    for (int i0 = 0; i0 < 1024; i0 += blockDim.x) {
+      int i = base + i0 + threadIdx.x;
+      bool hit = false;
+      if (i0 + threadIdx.x < 1024 && i < rows) {
+        int id = tok[(i / s) * tok_ld + (i % s)];
+        hit = id >= v0 && id < v0 + EMB_VROWS;
+      }
+      unsigned m = __ballot_sync(0xffffffffu, hit);
+      // block-wide ordered prefix: warps in order
+      __shared__ int wcount[32];
+      int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+      if (lane == 0) wcount[warp] = __popc(m);
+      __syncthreads();
+      if (hit) {
+        int off = nhits;
+        for (int w = 0; w < warp; ++w) off += wcount[w];
+        off += __popc(m & ((1u << lane) - 1));
+        hits[off] = i;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < (int)(blockDim.x / 32); ++w) tot += wcount[w];
+        nhits += tot;
+      }
+      __syncthreads();
+    }
+    const int n = nhits;
+    for (int c = threadIdx.x; c < ncol_chunks; c += blockDim.x) {
+      for (int k = 0; k < n; ++k) {
+        int i = hits[k];
+        int id = tok[(i / s) * tok_ld + (i % s)];
+        float g[8];
+        load8(dx + (long long)i * h + c * 8, g);
+        float* d = detok + (long long)id * h + c * 8;
+        float4 d0 = reinterpret_cast<float4*>(d)[0];
+        float4 d1 = reinterpret_cast<float4*>(d)[1];
+        d0.x += g[0]; d0.y += g[1]; d0.z += g[2]; d0.w += g[3];
+        d1.x += g[4]; d1.y += g[5]; d1.z += g[6]; d1.w += g[7];
+        reinterpret_cast<float4*>(d)[0] = d0;
+        reinterpret_cast<float4*>(d)[1] = d1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void embed_bwd_pos_kernel(int b, int s, int h, const __nv_bfloat16* __restrict__ dx,
+                                     float* __restrict__ dpos) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;   // over s*h/2 pairs
+  long long n = (long long)s * h / 2;
+  if (idx >= n) return;
+  int t = (int)(idx / (h / 2));
+  int c = (int)(idx % (h / 2)) * 2;
+  float a = 0.f, bsum = 0.f;
+  for (int bi = 0; bi < b; ++bi) {
+    float2 v = __bfloat1622float2(
+        *reinterpret_cast<const __nv_bfloat162*>(dx + ((long long)bi * s + t) * h + c));
+    a += v.x;
+    bsum += v.y;
+  }
+  float2* d = reinterpret_cast<float2*>(dpos + (long long)t * h + c);
+  float2 o = *d;
+  o.x += a;
+  o.y += bsum;
+  *d = o;
+}
+
+int embed_bwd(const int32_t* tok, long long tok_ld, int b, int s, int h, int vocab, const void* dx,
+              float* detok, float* dpos, cudaStream_t st) {
+  int blocks = (vocab + EMB_VROWS - 1) / EMB_VROWS;
+  embed_bwd_tok_kernel<<<blocks, 256, 0, st>>>(tok, tok_ld, b, s, h, vocab,
+                                               (const __nv_bfloat16*)dx, detok);
+  long long pairs = (long long)s * h / 2;
+  embed_bwd_pos_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(
+      b, s, h, (const __nv_bfloat16*)dx, dpos);
+  return ok();
+}
+
+// ------------------------------------------------------------------ LayerNorm
+// y = (x - mean) * rstd * g + b, two-pass statistics in fp32 (D-6).  Warp per row.
+__global__ void ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int rows, int h,
+                              const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ bta,
+                              __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                              float* __restrict__ rstd_out) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (row >= rows) return;
+  const int lane = threadIdx.x % 32;
+  const __nv_bfloat16* xr = x + (long long)row * h;
+  float s = 0.f;
+  for (int c = lane * 8; c < h; c += 256) {
+    float f[8];
+    load8(xr + c, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += f[i];
+  }
+  const float mean = warp_sum(s) / h;
+  float v = 0.f;
+  for (int c = lane * 8; c < h; c += 256) {
+    float f[8];
+    load8(xr + c, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float d = f[i] - mean;
+      v += d * d;
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(v) / h + 1e-5f);
+  __nv_bfloat16* yr = y + (long long)row * h;
+  for (int c = lane * 8; c < h; c += 256) {
+    float f[8], gg[8], bb[8];
+    load8(xr + c, f);
+    load8(g + c, gg);
+    load8(bta + c, bb);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = (f[i] - mean) * rstd * gg[i] + bb[i];
+    store8(yr + c, f);
+  }
+  if (lane == 0) {
+    mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+int ln_fwd(const void* x, int rows, int h, const void* g, const void* b, void* y, float* mean,
+           float* rstd, cudaStream_t st) {
+  ln_fwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)x, rows, h,
+                                                (const __nv_bfloat16*)g, (const __nv_bfloat16*)b,
+                                                (__nv_bfloat16*)y, mean, rstd);
+  return ok();
+}
+
+// dx = dres + rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)),  dxhat = dy * g
+__global__ void ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                              const float* __restrict__ mean, const float* __restrict__ rstd, int rows,
+                              int h, const __nv_bfloat16* __restrict__ g,
+                              const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (row >= rows) return;
+  const int lane = threadIdx.x % 32;
+  const float mu = mean[row], rs = rstd[row];
+  const __nv_bfloat16* xr = x + (long long)row * h;
+  const __nv_bfloat16* dyr = dy + (long long)row * h;
+  float s1 = 0.f, s2 = 0.f;
+  for (int c = lane * 8; c < h; c += 256) {
+    float xf[8], df[8], gf[8];
+    load8(xr + c, xf);
+    load8(dyr + c, df);
+    load8(g + c, gf);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float dxh = df[i] * gf[i];
+      float xh = (xf[i] - mu) * rs;
+      s1 += dxh;
+      s2 += dxh * xh;
+    }
+  }
+  s1 = warp_sum(s1) / h;
+  s2 = warp_sum(s2) / h;
+  __nv_bfloat16* o = dx + (long long)row * h;
+  const __nv_bfloat16* rr = dres ? dres + (long long)row * h : nullptr;
+  for (int c = lane * 8; c < h; c += 256) {
+    float xf[8], df[8], gf[8], rf[8];
+    load8(xr + c, xf);
+    load8(dyr + c, df);
+    load8(g + c, gf);
+    if (rr) load8(rr + c, rf);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float xh = (xf[i] - mu) * rs;
+      float v = rs * (df[i] * gf[i] - s1 - xh * s2);
+      rf[i] = rr ? rf[i] + v : v;
+    }
+    store8(o + c, rf);
+  }
+}
+
+int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int h,
+           const void* g, const void* dres, void* dx, cudaStream_t st) {
+  ln_bwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean, rstd, rows, h,
+      (const __nv_bfloat16*)g, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx);
+  return ok();
+}
+
+// ------------------------------------------------------------------ column reductions
+// Stage 1: part_b[r][c] = sum_{rows in chunk r} dy[row][c];
+//          part_g[r][c] = sum dy * xhat  (xhat from x, mean, rstd) when x != null.
+// Block = 256 threads = 8 row lanes x 32 column-pair lanes -> 64 columns.
+constexpr int CR_ROWCHUNK = 128;
+__global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                                      const float* __restrict__ mean, const float* __restrict__ rstd,
+                                      int rows, int n, float* __restrict__ part_b,
+                                      float* __restrict__ part_g) {
+  const int cl = threadIdx.x % 32, rl = threadIdx.x / 32;
+  const int c = blockIdx.x * 64 + cl * 2;
+  const int r0 = blockIdx.y * CR_ROWCHUNK;
+  const int r1 = min(rows, r0 + CR_ROWCHUNK);
+  float sb0 = 0.f, sb1 = 0.f, sg0 = 0.f, sg1 = 0.f;
+  if (c < n) {
+    for (int r = r0 + rl; r < r1; r += 8) {
+      float2 d = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy + (long long)r * n + c));
+      sb0 += d.x;
+      sb1 += d.y;
+      if (x) {
+        float2 xv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + (long long)r * n + c));
+        float mu = mean[r], rs = rstd[r];
+        sg0 += d.x * ((xv.x - mu) * rs);
+        sg1 += d.y * ((xv.y - mu) * rs);
+      }
+    }
+  }
+  __shared__ float sh[4][8][33];
+  sh[0][rl][cl] = sb0;
+  sh[1][rl][cl] = sb1;
+  sh[2][rl][cl] = sg0;
+  sh[3][rl][cl] = sg1;
+  __syncthreads();
+  if (rl < 4 && c < n) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += sh[rl][k][cl];
+    int col = c + (rl & 1);
+    if (rl < 2)
+      part_b[(long long)blockIdx.y * n + col] = acc;
+    else if (x)
+      part_g[(long long)blockIdx.y * n + col] = acc;
+  }
+}
+
+// Stage 2: out[c] (+)= sum_r part[r][c] in ascending r.
+__global__ void colsum_final_kernel(const float* __restrict__ part, int nchunks, int n,
+                                    float* __restrict__ out, int accumulate) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  float acc = 0.f;
+  for (int r = 0; r < nchunks; ++r) acc += part[(long long)r * n + c];
+  out[c] = accumulate ? out[c] + acc : acc;
+}
+
+int colsum_chunks(int rows) { return (rows + CR_ROWCHUNK - 1) / CR_ROWCHUNK; }
+
+int colsum(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int n,
+           float* workspace, float* out_b, float* out_g, int accumulate, cudaStream_t st) {
+  int nch = colsum_chunks(rows);
+  float* part_b = workspace;
+  float* part_g = workspace + (long long)nch * n;
+  dim3 grid((n + 63) / 64, nch);
+  colsum_partial_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                                              mean, rstd, rows, n, part_b, part_g);
+  colsum_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(part_b, nch, n, out_b, accumulate);
+  if (x) colsum_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(part_g, nch, n, out_g, accumulate);
+  return ok();
+}
+
+// ------------------------------------------------------------------ attention softmax
+// Row q of S (fp32, already scaled by 1/sqrt(d)): P[q, k] = exp(S - max) / sum for
+// k <= q, 0 for k > q (D-8).  One warp per row; rows of length s.
+__global__ void softmax_fwd_kernel(const float* __restrict__ S, long long nrows, int s,
+                                   __nv_bfloat16* __restrict__ P) {
+  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (row >= nrows) return;
+  const int lane = threadIdx.x % 32;
+  const int q = (int)(row % s);
+  const float* sr = S + row * s;
+  float mx = -FLT_MAX;
+  for (int k = lane; k <= q; k += 32) mx = fmaxf(mx, sr[k]);
+  mx = warp_max(mx);
+  float sum = 0.f;
+  for (int k = lane; k <= q; k += 32) sum += __expf(sr[k] - mx);
+  sum = warp_sum(sum);
+  const float inv = 1.f / sum;
+  __nv_bfloat16* pr = P + row * s;
+  for (int k = lane * 2; k < s; k += 64) {
+    float a = k <= q ? __expf(sr[k] - mx) * inv : 0.f;
+    float b = k + 1 <= q ? __expf(sr[k + 1] - mx) * inv : 0.f;
+    *reinterpret_cast<__nv_bfloat162*>(pr + k) = __floats2bfloat162_rn(a, b);
+  }
+}
+
+int softmax_fwd(const float* S, long long nrows, int s, void* P, cudaStream_t st) {
+  unsigned blocks = (unsigned)((nrows + 7) / 8);
+  softmax_fwd_kernel<<<blocks, 256, 0, st>>>(S, nrows, s, (__nv_bfloat16*)P);
+  return ok();
+}
+
+// dS[q, k] = scale * P[q, k] * (dP[q, k] - sum_k' P[q, k'] dP[q, k']), zero for k > q.
+__global__ void softmax_bwd_kernel(const __nv_bfloat16* __restrict__ P, const float* __restrict__ dP,
+                                   long long nrows, int s, float scale,
+                                   __nv_bfloat16* __restrict__ dS) {
+  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (row >= nrows) return;
+  const int lane = threadIdx.x % 32;
+  const int q = (int)(row % s);
+  const __nv_bfloat16* pr = P + row * s;
+  const float* dr = dP + row * s;
+  float dot = 0.f;
+  for (int k = lane; k <= q; k += 32) dot += __bfloat162float(pr[k]) * dr[k];
+  dot = warp_sum(dot);
+  __nv_bfloat16* o = dS + row * s;
+  for (int k = lane * 2; k < s; k += 64) {
+    float a = k <= q ? scale * __bfloat162float(pr[k]) * (dr[k] - dot) : 0.f;
+    float b = k + 1 <= q ? scale * __bfloat162float(pr[k + 1]) * (dr[k + 1] - dot) : 0.f;
+    *reinterpret_cast<__nv_bfloat162*>(o + k) = __floats2bfloat162_rn(a, b);
+  }
+}
+
+int softmax_bwd(const void* P, const float* dP, long long nrows, int s, float scale, void* dS,
+                cudaStream_t st) {
+  unsigned blocks = (unsigned)((nrows + 7) / 8);
+  softmax_bwd_kernel<<<blocks, 256, 0, st>>>((const __nv_bfloat16*)P, dP, nrows, s, scale,
+                                             (__nv_bfloat16*)dS);
+  return ok();
+}
+
+// ------------------------------------------------------------------ cross entropy
+// Per row of logits z [V] (bf16): lse = log sum exp z; ce = lse - z_y;
+// dz = coef * (softmax(z) - onehot(y)) written in place (bf16);
+// row_loss[row] = ce (fp32, unscaled).  coef = S / (M_total * tokens_in_microbatch) (D-9).
+__global__ void xent_kernel(__nv_bfloat16* __restrict__ z, const int32_t* __restrict__ labels,
+                            long long lab_ld, int s, int V, float coef, float* __restrict__ row_loss) {
+  const int row = blockIdx.x;
+  __nv_bfloat16* zr = z + (long long)row * V;
+  const int y = labels[(row / s) * lab_ld + (row % s)];
+  float mx = -FLT_MAX, sum = 0.f;
+  for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
+    float f[8];
+    load8(zr + c, f);
+    float lm = f[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) lm = fmaxf(lm, f[i]);
+    if (lm > mx) {
+      sum *= __expf(mx - lm);
+      mx = lm;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sum += __expf(f[i] - mx);
+  }
+  // block reduce of (max, sum)
+  __shared__ float smx[32], ssum[32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float wm = warp_max(mx);
+  sum *= __expf(mx - wm);
+  float ws = warp_sum(sum);
+  if (lane == 0) { smx[warp] = wm; ssum[warp] = ws; }
+  __syncthreads();
+  const int nw = blockDim.x / 32;
+  float gm = -FLT_MAX;
+  for (int w = 0; w < nw; ++w) gm = fmaxf(gm, smx[w]);
+  float gs = 0.f;
+  for (int w = 0; w < nw; ++w) gs += ssum[w] * __expf(smx[w] - gm);
+  const float lse = logf(gs) + gm;
+  const float zy = __bfloat162float(zr[y]);
+  __syncthreads();
+  for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
+    float f[8];
+    load8(zr + c, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float p = __expf(f[i] - lse);
+      f[i] = coef * (p - ((c + i) == y ? 1.f : 0.f));
+    }
+    store8(zr + c, f);
+  }
+  if (threadIdx.x == 0) row_loss[row] = lse - zy;
+}
+
+int xent(void* z, const int32_t* labels, long long lab_ld, int rows, int s, int V, float coef,
+         float* row_loss, cudaStream_t st) {
+  if (V % 8) return -2;
+  xent_kernel<<<rows, 512, 0, st>>>((__nv_bfloat16*)z, labels, lab_ld, s, V, coef, row_loss);
+  return ok();
+}
+
+// sum of n fp32 values in a fixed order (single block), out[slot] (+)= sum * scale
+__global__ void reduce_sum_kernel(const float* __restrict__ x, int n, float scale,
+                                  double* __restrict__ out) {
+  __shared__ double sh[1024];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out += sh[0] * scale;
+}
+
+int reduce_sum(const float* x, int n, float scale, double* out, cudaStream_t st) {
+  reduce_sum_kernel<<<1, 1024, 0, st>>>(x, n, scale, out);
+  return ok();
+}
+
+// ------------------------------------------------------------------ casts
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                     long long n) {
+  long long nv = n / 4;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    float4 v = reinterpret_cast<const float4*>(in)[i];
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    reinterpret_cast<uint2*>(out)[i] = u;
+  }
+  for (long long i = nv * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+int cast_f32_bf16(const float* in, void* out, long long n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  long long blocks = (n / 4 + 255) / 256;
+  long long cap = (long long)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  cast_f32_bf16_kernel<<<(unsigned)blocks, 256, 0, st>>>(in, (__nv_bfloat16*)out, n);
+  return ok();
+}
+
+__global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ in, float* __restrict__ out,
+                                     long long n) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __bfloat162float(in[i]);
+}
+int cast_bf16_f32(const void* in, float* out, long long n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  cast_bf16_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((const __nv_bfloat16*)in, out, n);
+  return ok();
+}
+
+// deterministic N(0, std) init, truncated to bf16-representable values (D-15, D-22):
+// Box-Muller on a counter-based splitmix64 stream.
+__device__ __forceinline__ uint64_t smix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void init_normal_kernel(__nv_bfloat16* __restrict__ out, float* __restrict__ master,
+                                   long long n, uint64_t seed, float mean, float stdv) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t a = smix(seed * 0x100000001B3ull + 2 * i), b = smix(seed * 0x100000001B3ull + 2 * i + 1);
+  float u1 = ((a >> 40) + 1) * (1.0f / 16777217.0f), u2 = (b >> 40) * (1.0f / 16777216.0f);
+  float z = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+  float v = mean + stdv * z;
+  uint32_t bits = __float_as_uint(v) & 0xFFFF0000u;
+  float tv = __uint_as_float(bits);
+  out[i] = __float2bfloat16_rn(tv);
+  if (master) master[i] = tv;
+}
+int init_normal(void* out, float* master, long long n, uint64_t seed, float mean, float stdv,
+                cudaStream_t st) {
+  if (n <= 0) return 0;
+  init_normal_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((__nv_bfloat16*)out, master, n,
+                                                                  seed, mean, stdv);
+  return ok();
+}
+
+}  // namespace axonn

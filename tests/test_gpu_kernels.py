@@ -1,0 +1,212 @@
+"""Kernel-level parity (T2): K1 tcgen05 GEMM and K9 AdamW through the C-ABI.
+
+References: numpy fp64 products of the SAME bf16-rounded inputs (a matmul is a
+library primitive, ③) and the fp32 oracle AdamW (bit-exact by design, D-14)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2110_13005_b200 import _lib
+    return _lib.load()
+
+
+def torch():
+    import torch as t
+    return t
+
+
+def dev_bf16(x):
+    t = torch()
+    return t.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(t.bfloat16).cuda()
+
+
+def host(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def gemm(lib, **kw):
+    from paper_2110_13005_b200._lib import GemmArgs
+    a = GemmArgs()
+    defaults = dict(Z=1, Z1=1, a_s1=0, a_s2=0, b_s1=0, b_s2=0, c_s1=0, c_s2=0, alpha=1.0)
+    defaults.update(kw)
+    for k, v in defaults.items():
+        if hasattr(v, "data_ptr"):
+            v = v.data_ptr()
+        setattr(a, k, v)
+    rc = lib.axonn_k_gemm(C.byref(a), None)
+    assert rc == 0, rc
+    torch().cuda.synchronize()
+
+
+def rel(x, ref):
+    return np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-30)
+
+
+def cos(x, ref):
+    return float((x * ref).sum() / (np.linalg.norm(x) * np.linalg.norm(ref) + 1e-300))
+
+
+RNG = np.random.default_rng(1234)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 200), (1024, 768, 1024),
+                                   (4096, 2048, 2048), (77, 16, 8)])
+def test_gemm_forward_bias_resid(lib, M, N, K):
+    t = torch()
+    A = dev_bf16(RNG.standard_normal((M, K)))
+    B = dev_bf16(RNG.standard_normal((N, K)) * 0.05)
+    bias = dev_bf16(RNG.standard_normal(N))
+    res = dev_bf16(RNG.standard_normal((M, N)))
+    Cd = t.empty((M, N), dtype=t.bfloat16, device="cuda")
+    gemm(lib, M=M, N=N, K=K, A=A, lda=K, a_mn=0, B=B, ldb=K, b_mn=0, C=Cd, ldc=N, epi=0,
+         bias=bias, resid=res, ld_resid=N)
+    ref = host(A) @ host(B).T + host(bias) + host(res)
+    out = host(Cd)
+    assert rel(out, ref) < 1e-2 and cos(out, ref) > 0.9999
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 200, 384), (4096, 2048, 8192), (130, 72, 64)])
+def test_gemm_dgrad_b_mn_major(lib, M, N, K):
+    """dX = dY W: B stored [K][N] (MN-major)."""
+    t = torch()
+    A = dev_bf16(RNG.standard_normal((M, K)))
+    W = dev_bf16(RNG.standard_normal((K, N)) * 0.05)
+    Cd = t.empty((M, N), dtype=t.bfloat16, device="cuda")
+    gemm(lib, M=M, N=N, K=K, A=A, lda=K, a_mn=0, B=W, ldb=N, b_mn=1, C=Cd, ldc=N, epi=0)
+    ref = host(A) @ host(W)
+    out = host(Cd)
+    assert rel(out, ref) < 1e-2 and cos(out, ref) > 0.9999
+
+
+@pytest.mark.parametrize("M,N,K", [(192, 320, 500), (2048, 8192, 4096), (64, 136, 40)])
+def test_gemm_wgrad_both_mn_major_f32_accumulate(lib, M, N, K):
+    """dW (+)= dY^T X: A stored [K][M], B stored [K][N]; fp32 output, accumulate."""
+    t = torch()
+    dY = dev_bf16(RNG.standard_normal((K, M)))
+    X = dev_bf16(RNG.standard_normal((K, N)))
+    Cd = t.zeros((M, N), dtype=t.float32, device="cuda")
+    for acc in (0, 1):
+        gemm(lib, M=M, N=N, K=K, A=dY, lda=M, a_mn=1, B=X, ldb=N, b_mn=1, C=Cd, ldc=N, epi=3,
+             accumulate=acc)
+    ref = 2 * host(dY).T @ host(X)
+    out = Cd.cpu().numpy().astype(np.float64)
+    assert rel(out, ref) < 1e-5
+
+
+def test_gemm_gelu_and_dgelu(lib):
+    t = torch()
+    M, N, K = 256, 512, 192
+    A = dev_bf16(RNG.standard_normal((M, K)))
+    B = dev_bf16(RNG.standard_normal((N, K)) * 0.1)
+    bias = dev_bf16(RNG.standard_normal(N) * 0.1)
+    out = t.empty((M, N), dtype=t.bfloat16, device="cuda")
+    pre = t.empty((M, N), dtype=t.bfloat16, device="cuda")
+    gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=out, ldc=N, epi=1, bias=bias, aux=pre,
+         ld_aux=N)
+    pre_ref = host(A) @ host(B).T + host(bias)
+    assert rel(host(pre), pre_ref) < 1e-2
+    p = host(pre)
+    c = 0.7978845608028654
+    gelu = 0.5 * p * (1 + np.tanh(c * (p + 0.044715 * p ** 3)))
+    assert rel(host(out), gelu) < 1e-2
+    # DGELU: out2 = (A B^T) * gelu'(pre)
+    out2 = t.empty((M, N), dtype=t.bfloat16, device="cuda")
+    gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=out2, ldc=N, epi=2, aux=pre, ld_aux=N)
+    th = np.tanh(c * (p + 0.044715 * p ** 3))
+    dg = 0.5 * (1 + th) + 0.5 * p * (1 - th * th) * c * (1 + 3 * 0.044715 * p * p)
+    ref2 = (host(A) @ host(B).T) * dg
+    assert rel(host(out2), ref2) < 1e-2
+
+
+def test_gemm_batched_attention_shapes(lib):
+    """S = Q K^T over (sample, head) from the packed [b*s, 3h] QKV layout via
+    4-D TMA maps; causal modes 1 (skip upper tiles), 2 (k < m0+128), 3 (k >= m0)."""
+    t = torch()
+    b, s, a, d = 2, 384, 3, 64
+    h = a * d
+    qkv = dev_bf16(RNG.standard_normal((b * s, 3 * h)))
+    Q = host(qkv)[:, :h].reshape(b, s, a, d).transpose(0, 2, 1, 3)
+    Kt = host(qkv)[:, h:2 * h].reshape(b, s, a, d).transpose(0, 2, 1, 3)
+    S = t.full((b, a, s, s), float("nan"), dtype=t.float32, device="cuda")
+    gemm(lib, M=s, N=s, K=d, Z=b * a, Z1=a,
+         A=qkv, lda=3 * h, a_s1=d, a_s2=s * 3 * h, a_mn=0,
+         B=qkv[:, h:], ldb=3 * h, b_s1=d, b_s2=s * 3 * h, b_mn=0,
+         C=S, ldc=s, c_s1=s * s, c_s2=a * s * s, epi=3, causal=1, alpha=0.5)
+    ref = 0.5 * Q @ Kt.transpose(0, 1, 3, 2)
+    got = S.cpu().numpy()
+    low = np.tril(np.ones((s, s), dtype=bool))
+    assert rel(got[..., low], ref[..., low]) < 1e-5
+    # PV: O[q, e] = sum_{k <= q-block} P[q, k] V[k, e] with P lower-triangular
+    P = np.tril(RNG.standard_normal((b, a, s, s)))
+    Pd = dev_bf16(P)
+    O = t.zeros((b * s, h), dtype=t.bfloat16, device="cuda")
+    gemm(lib, M=s, N=d, K=s, Z=b * a, Z1=a,
+         A=Pd, lda=s, a_s1=s * s, a_s2=a * s * s, a_mn=0,
+         B=qkv[:, 2 * h:], ldb=3 * h, b_s1=d, b_s2=s * 3 * h, b_mn=1,
+         C=O, ldc=h, c_s1=d, c_s2=s * h, epi=0, causal=2)
+    V = host(qkv)[:, 2 * h:].reshape(b, s, a, d).transpose(0, 2, 1, 3)
+    refO = (host(Pd) @ V).transpose(0, 2, 1, 3).reshape(b * s, h)
+    assert rel(host(O), refO) < 1e-2
+    # dK = dS^T Q with dS lower-triangular: A = dS^T (MN-major), B = Q^T (MN-major), causal 3
+    dK = t.zeros((b * s, h), dtype=t.bfloat16, device="cuda")
+    gemm(lib, M=s, N=d, K=s, Z=b * a, Z1=a,
+         A=Pd, lda=s, a_s1=s * s, a_s2=a * s * s, a_mn=1,
+         B=qkv, ldb=3 * h, b_s1=d, b_s2=s * 3 * h, b_mn=1,
+         C=dK, ldc=h, c_s1=d, c_s2=s * h, epi=0, causal=3)
+    refK = (host(Pd).transpose(0, 1, 3, 2) @ Q).transpose(0, 2, 1, 3).reshape(b * s, h)
+    assert rel(host(dK), refK) < 1e-2
+
+
+def test_gemm_column_remap_and_nvalid(lib):
+    """Columns c -> (c / 5) * 8 + c % 5 (head padding layout); n_valid cut."""
+    t = torch()
+    M, N, K = 130, 40, 64
+    A = dev_bf16(RNG.standard_normal((M, K)))
+    B = dev_bf16(RNG.standard_normal((N, K)))
+    Cd = t.zeros((M, 64), dtype=t.bfloat16, device="cuda")
+    gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=Cd, ldc=64, epi=0, col_group_in=5,
+         col_group_out=8)
+    ref = host(A) @ host(B).T
+    out = host(Cd)
+    for c in range(N):
+        dc = (c // 5) * 8 + c % 5
+        assert rel(out[:, dc], ref[:, c]) < 1e-2
+    pad = [dc for dc in range(64) if dc % 8 >= 5]
+    assert np.all(out[:, pad] == 0)
+    Cd2 = t.zeros((M, N), dtype=t.bfloat16, device="cuda")
+    gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=Cd2, ldc=N, epi=0, n_valid=37)
+    o2 = host(Cd2)
+    assert np.all(o2[:, 37:] == 0) and rel(o2[:, :37], ref[:, :37]) < 1e-2
+
+
+@pytest.mark.parametrize("n", [1, 7, 4096, (1 << 20) + 3])
+def test_adamw_bit_exact_vs_oracle(lib, n):
+    """K9 vs oracle AdamW (fp32, D-14 op order): bit-identical theta, m, v, theta16."""
+    t = torch()
+    from oracle import adamw
+    from synth import adam_test_state
+    theta, m, v, g = adam_test_state(n, seed=n)
+    sc = adamw.step_scalars(3)
+    scal = np.array([sc[k] for k in ("decay", "b1", "omb1", "b2", "omb2", "step", "bc2_sqrt",
+                                     "eps", "inv_scale")], dtype=np.float32)
+    dth = t.from_numpy(theta.copy()).cuda()
+    dm = t.from_numpy(m.copy()).cuda()
+    dv = t.from_numpy(v.copy()).cuda()
+    dg = t.from_numpy(g).to(t.bfloat16).cuda()
+    d16 = t.empty(n, dtype=t.bfloat16, device="cuda")
+    rc = lib.axonn_k_adamw(n, dg.data_ptr(), dth.data_ptr(), dm.data_ptr(), dv.data_ptr(),
+                           d16.data_ptr(), scal.ctypes.data_as(C.POINTER(C.c_float)), None)
+    assert rc == 0
+    t.cuda.synchronize()
+    th_r, m_r, v_r = theta.copy(), m.copy(), v.copy()
+    t16 = adamw.adamw_step_fp32(th_r, m_r, v_r, g, sc)
+    assert np.array_equal(dth.cpu().numpy().view(np.uint32), th_r.view(np.uint32))
+    assert np.array_equal(dm.cpu().numpy().view(np.uint32), m_r.view(np.uint32))
+    assert np.array_equal(dv.cpu().numpy().view(np.uint32), v_r.view(np.uint32))
+    assert np.array_equal(d16.float().cpu().numpy().view(np.uint32), t16.view(np.uint32))
