@@ -1,0 +1,304 @@
+"""bench.py — AxoNN hybrid training step on B200 (BASELINE.json metric).
+
+One step = one AxoNN batch: axonn_run_batch (Alg. 1 l.4-6: Alg. 2 inter-layer
+step of every microbatch, fp32 weight-gradient accumulation, bf16 gradient
+all-reduce over the column) + axonn_optimizer_step (AdamW over every
+parameter, bucketed, overlapped with the all-reduce chunks).  Nothing is
+skipped inside the timed region.
+
+Default workload (N = 1, and weak scaling for N > 1): BASELINE.json
+configs[1], the GPT 1.3B-shaped model (24 layers, hidden 2048, 16 heads,
+seq 512, vocab 51200), G_inter = 1, G_data = N, microbatch 8, 8 microbatches
+per replica (64 samples per GPU), optimizer state in HBM (no offload).
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Under torchrun every rank runs one GPU; rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "per-GPU model TFLOP/s and % of B200 bf16 peak at 1/2/4/8 GPUs; batch time"
+
+CONFIGS = {
+    # BASELINE.json configs[1]: GPT 1.3B-shaped, G_inter = 1, G_data = N, no offload
+    "gpt1.3b": dict(n_layers=24, hidden=2048, heads=16, seq_len=512, vocab=51200,
+                    g_inter=1, microbatch=8, mb_per_replica=8, offload=False),
+    # small smoke configuration (BASELINE.json configs[0] shape, single stage)
+    "tiny": dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256,
+                 g_inter=1, microbatch=2, mb_per_replica=4, offload=False),
+}
+
+
+def model_flops(b, s, l, h, V):
+    """72 b s l h^2 (1 + s/6h) + 6 b s h V (reading D-25; Eq. 3 credits recompute)."""
+    return 72 * b * s * l * h * h + 12 * b * s * s * l * h + 6 * b * s * h * V
+
+
+def eq3_flops(b, s, l, h, V):
+    return 96 * b * s * l * h * h + 16 * b * s * s * l * h + 6 * b * s * h * V
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d.get("hbm_gbs", 6456.2), bf16=d.get("bf16_tflops", 1660.9),
+                    bf16_sus=d.get("bf16_tflops_sustained", 1415.3), src="MEASURED_PEAKS.json")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="B200_PROFILING.md fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_sample(cfg, steps: int = 1):
+    """Time the oracle (as it stands) on a bounded sample of the same workload:
+    a 2-layer slice of the configured shape (full per-layer width, LM head
+    included) on one 512-token sequence, fp64 numpy on the host cores."""
+    from oracle import model as om
+    from synth import init_params, uniform_tokens
+    l = 2
+    c = om.GPTConfig(n_layers=l, hidden=cfg["hidden"], heads=cfg["heads"], seq_len=cfg["seq_len"],
+                     vocab=cfg["vocab"])
+    p = {k: v.astype(np.float64) for k, v in
+         init_params(l, c.hidden, c.seq_len, c.vocab, seed=5, parity=False).items()}
+    tok = uniform_tokens(1, c.seq_len, c.vocab, seed=1234)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        om.full_batch_loss_and_grads(p, c, tok)
+    dt = (time.perf_counter() - t0) / steps
+    fl = model_flops(1, c.seq_len, l, c.hidden, c.vocab)
+    return dict(value=fl / dt / 1e12, unit="model TFLOP/s", cores=os.cpu_count(), kind="oracle",
+                sample=f"numpy fp64 oracle fwd+bwd of a {l}-layer slice (h {c.hidden}, a {c.heads}, "
+                       f"s {c.seq_len}, V {c.vocab}), 1 x {c.seq_len} tokens, {dt:.2f} s/step")
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle (this tier's reference arm) on the host."""
+    if rank != 0:
+        return
+    steps_total = args.warmup + args.steps
+    for _ in range(args.warmup):
+        cpu_oracle_sample(cfg, 1)
+    res = cpu_oracle_sample(cfg, args.steps)
+    v = res["value"]
+    sample_flops = model_flops(1, cfg["seq_len"], 2, cfg["hidden"], cfg["vocab"])
+    ms = sample_flops / (v * 1e12) * 1e3
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "model TFLOP/s (all GPUs)",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": args.config, "global_batch": 1, "seq_len": cfg["seq_len"],
+                      "parallelism": "cpu oracle", "sample": res["sample"]},
+           "cpu_baseline": res,
+           "e2e": {"value": v, "unit": "model TFLOP/s (all GPUs)", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    _ = steps_total
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="gpt1.3b", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+
+    from paper_2110_13005_b200 import dist as D
+    rank, world, local = D.env_rank_world()
+    if world == 1 and args.gpus > 1:
+        raise SystemExit("use torchrun --nproc-per-node N for N > 1")
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    D.init_process_group(rank, world, backend="gloo")
+    from paper_2110_13005_b200.engine import AxoNN
+    g_inter = cfg["g_inter"]
+    g_data = world // g_inter
+    b_m, m = cfg["microbatch"], cfg["mb_per_replica"]
+    B = b_m * m * g_data
+    nid = D.share_unique_id(rank, world, D.nccl_unique_id)
+    eng = AxoNN(g_inter, g_data, b_m, n_layers=cfg["n_layers"], hidden=cfg["hidden"],
+                heads=cfg["heads"], seq_len=cfg["seq_len"], vocab=cfg["vocab"], init_seed=42,
+                offload=cfg["offload"], rank=rank, world_size=world, device=local, nccl_id=nid)
+    from synth import uniform_tokens
+    s, V = cfg["seq_len"], cfg["vocab"]
+    tokens = uniform_tokens(B, s, V, seed=1234)          # full batch on the host (pinned below)
+    j = rank // g_inter
+    lo, hi = D.batch_shard(B, g_data, j)
+    d_tok = torch.from_numpy(tokens[lo:hi].copy()).cuda()  # this replica's shard resident in HBM
+    h_tok = torch.from_numpy(tokens).pin_memory()
+    h_np = h_tok.numpy()
+
+    # warm-up (untimed)
+    for _ in range(args.warmup):
+        eng.run_batch_device(d_tok.data_ptr(), B)
+        eng.optimizer_step()
+    torch.cuda.synchronize()
+
+    # timed region: K steps with device-resident inputs; K1 launches bracketed
+    # by CUDA events on the library's compute stream (roofline numbers)
+    eng.set_profiling(True)
+    gemm_ms = gemm_flop = adam_ms = adam_bytes = 0.0
+    launches = 0
+    D.barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        eng.timer_mark(0)
+        losses = []
+        for _ in range(args.steps):
+            losses.append(eng.run_batch_device(d_tok.data_ptr(), B))
+            eng.optimizer_step()
+            st = eng.stats()
+            gemm_ms += st["gemm_ms"]
+            gemm_flop += st["gemm_flop"]
+            adam_ms += st["adam_ms"]
+            adam_bytes += st["adam_bytes"]
+            launches += int(st["kernel_launches"])
+        eng.timer_mark(1)
+        dev_ms = eng.timer_elapsed_ms(0, 1)
+    torch.cuda.synchronize()
+    D.barrier(world)
+    eng.set_profiling(False)
+    dev_ms = D.max_over_ranks(dev_ms, world)
+    ms_step = dev_ms / args.steps
+    fl = model_flops(B, s, cfg["n_layers"], cfg["hidden"], V)
+    value = fl / (ms_step / 1e3) / 1e12                       # whole-job model TFLOP/s
+
+    # e2e: through the public C-ABI with HOST tokens; H2D of the shard + D2H of
+    # the loss happen inside axonn_run_batch every step
+    e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
+    D.barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        eng.run_batch(h_np)
+        eng.optimizer_step()
+    torch.cuda.synchronize()
+    e2e_ms = D.max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps, world)
+    e2e_val = fl / (e2e_ms / 1e3) / 1e12
+
+    peaks = load_peaks()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_sample(cfg, 1)
+    if rank == 0:
+        gemm_tf = gemm_flop / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+        out = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "model TFLOP/s (all GPUs)",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (uniform tokens, splitmix64 seed 1234; random-init weights seed 42)",
+            "config": {"workload": args.config, "model": f"GPT {cfg['n_layers']}L h{cfg['hidden']} "
+                       f"a{cfg['heads']} s{s} V{V}", "global_batch": B, "seq_len": s,
+                       "microbatch": b_m, "microbatches_per_replica": m,
+                       "parallelism": f"G_inter{g_inter} x G_data{g_data}",
+                       "offload": cfg["offload"], "l2": "inputs larger than L2 (GBs of weights/activations per step)"},
+            "per_gpu_tflops": value / world,
+            "pct_bf16_peak": 100.0 * value / world / peaks["bf16"],
+            "pct_bf16_peak_sustained": 100.0 * value / world / peaks["bf16_sus"],
+            "eq3_tflops_per_gpu": eq3_flops(B, s, cfg["n_layers"], cfg["hidden"], V) / (ms_step / 1e3) / 1e12 / world,
+            "batch_time_s": ms_step / 1e3,
+            "loss": losses[-1] if losses else None,
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_val, "unit": "model TFLOP/s (all GPUs)",
+                    "h2d_bytes_per_step": int((hi - lo) * (s + 1) * 4), "d2h_bytes_per_step": 8,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "kernel": "K1 gemm_bf16_tcgen05 (linear layers)",
+                         "achieved": gemm_tf, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
+                         "frac": (gemm_tf / peaks["bf16_sus"]) if gemm_tf else None,
+                         "peak_src": peaks["src"] + " bf16_tflops_sustained (kernel timed inside a long step)",
+                         "gemm_share_of_step": gemm_ms / args.steps / ms_step,
+                         "traffic": None},
+            "adam": {"achieved_gbs": adam_bytes / (adam_ms / 1e3) / 1e9 if adam_ms else None,
+                     "peak_gbs": peaks["hbm"], "bytes_per_param": 28},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -59,8 +59,9 @@ typedef struct {
 
 /* Optimizer and memory-optimisation knobs. */
 typedef struct {
-  float lr, beta1, beta2, eps, weight_decay;  /* paper: 1e-3, 0.9, 0.999, (1e-8, D-13), 0.01 */
-  float loss_scale;                           /* S (D-11); 1 for bf16 */
+  double lr, beta1, beta2, eps, weight_decay; /* paper: 1e-3, 0.9, 0.999, (1e-8, D-13), 0.01;
+                                                 step scalars are formed in double, rounded once (D-14) */
+  double loss_scale;                          /* S (D-11); 1 for bf16 */
   int offload;                                /* 1: fp32 theta + Adam state in pinned host memory */
   int64_t bucket_elems;                       /* bsize in elements (D-16); paper 4M */
   int coarsen_k;                              /* all-reduce chunk = k * bsize elements; paper 4 */
@@ -159,6 +160,13 @@ AXONN_API axonn_status axonn_stats(const axonn_ctx* ctx, double* out, int n);
 /* 1: bracket every K1/K9 launch with CUDA events on its stream (for the
  * roofline numbers in bench.py); 0: off (default). */
 AXONN_API axonn_status axonn_set_profiling(axonn_ctx* ctx, int on);
+
+/* Device-side timing for benchmarks: axonn_timer_mark(ctx, id) records CUDA
+ * event id (0..7) on the context's compute stream after all work enqueued so
+ * far (including the optimizer); axonn_timer_elapsed synchronises on the
+ * later event and returns the device time between two marks in ms. */
+AXONN_API axonn_status axonn_timer_mark(axonn_ctx* ctx, int id);
+AXONN_API axonn_status axonn_timer_elapsed(axonn_ctx* ctx, int id0, int id1, double* ms);
 
 /* ---------------------------------------------------------------------------
  * Kernel-level entry points (device pointers; enqueue on `stream`, a

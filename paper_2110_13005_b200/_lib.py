@@ -34,8 +34,9 @@ class ModelCfg(C.Structure):
 
 
 class OptCfg(C.Structure):
-    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
-                ("weight_decay", C.c_float), ("loss_scale", C.c_float), ("offload", C.c_int),
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double), ("weight_decay", C.c_double), ("loss_scale", C.c_double),
+                ("offload", C.c_int),
                 ("bucket_elems", C.c_int64), ("coarsen_k", C.c_int), ("pipeline_limit", C.c_int)]
 
 
@@ -61,6 +62,8 @@ def _declare(lib):
         "axonn_write_tensor": (I, [P, I, I, P]),
         "axonn_stats": (I, [P, C.POINTER(C.c_double), I]),
         "axonn_set_profiling": (I, [P, I]),
+        "axonn_timer_mark": (I, [P, I]),
+        "axonn_timer_elapsed": (I, [P, I, I, C.POINTER(C.c_double)]),
         "axonn_k_gemm": (I, [C.POINTER(GemmArgs), P]),
         "axonn_k_adamw": (I, [I64, P, P, P, P, P, C.POINTER(F), P]),
     }

@@ -1,0 +1,875 @@
+// AxoNN hybrid step engine: context lifecycle (Alg. 1 l.2), the Alg. 2
+// message-driven scheduler over NCCL P2P, the column gradient all-reduce
+// (Alg. 1 l.13) chunked by k*bsize and the bucketed,
+// optionally host-offloaded AdamW overlapped with it.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <new>
+#include <thread>
+
+#include "engine.h"
+
+namespace axonn {
+
+// ------------------------------------------------------------------ helpers
+int Ctx::fail(int code, const std::string& msg) {
+  if (err.empty() || !sticky) err = msg;
+  if (code == AXONN_ERR_CUDA || code == AXONN_ERR_NCCL || code == AXONN_ERR_TIMEOUT) sticky = true;
+  return code;
+}
+int Ctx::check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return 0;
+  return fail(e == cudaErrorMemoryAllocation ? AXONN_ERR_OOM : AXONN_ERR_CUDA,
+              std::string(what) + ": " + cudaGetErrorString(e));
+}
+int Ctx::check_nccl(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return 0;
+  return fail(AXONN_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+void* Ctx::dalloc(size_t bytes) {
+  void* p = nullptr;
+  bytes = (bytes + 255) & ~size_t(255);
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  allocs.push_back(p);
+  return p;
+}
+cudaEvent_t Ctx::ev() {
+  if (ev_next == ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ev_pool.push_back(e);
+  }
+  return ev_pool[ev_next++];
+}
+
+static uint16_t f2bf(float f) {   // round-to-nearest-even (host side of theta16 writes)
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x7FFFFFu)) return (uint16_t)((u >> 16) | 0x40);
+  uint32_t lsb = (u >> 16) & 1u;
+  u += 0x7FFFu + lsb;
+  return (uint16_t)(u >> 16);
+}
+static float bf2f(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+#define CU(x)                                  \
+  do {                                         \
+    int _rc = c->check_cuda((x), #x);          \
+    if (_rc) return (axonn_status)_rc;         \
+  } while (0)
+#define NC(x)                                  \
+  do {                                         \
+    int _rc = c->check_nccl((x), #x);          \
+    if (_rc) return (axonn_status)_rc;         \
+  } while (0)
+
+// ------------------------------------------------------------------ parameter table
+static void build_tensors(Ctx* c) {
+  const int h = c->h, V = c->V, s = c->s;
+  int64_t off = 0;
+  auto add = [&](const std::string& n, int64_t r, int64_t cc) {
+    TensorRec t{n, r, cc, r * cc, off};
+    off += (r * cc + 63) / 64 * 64;   // 128-byte (bf16) / 256-byte (fp32) aligned views
+    c->tensors.push_back(t);
+    return t.off;
+  };
+  if (c->first) {
+    c->tok_emb = add("tok_emb", V, h);
+    c->pos_emb = add("pos_emb", s, h);
+  }
+  for (int li = 0; li < c->nl; ++li) {
+    std::string p = "l" + std::to_string(c->layer0 + li) + ".";
+    LayerOff o;
+    o.ln1_g = add(p + "ln1_g", 1, h);
+    o.ln1_b = add(p + "ln1_b", 1, h);
+    o.w_qkv = add(p + "w_qkv", 3 * h, h);
+    o.b_qkv = add(p + "b_qkv", 1, 3 * h);
+    o.w_o = add(p + "w_o", h, h);
+    o.b_o = add(p + "b_o", 1, h);
+    o.ln2_g = add(p + "ln2_g", 1, h);
+    o.ln2_b = add(p + "ln2_b", 1, h);
+    o.w_fc1 = add(p + "w_fc1", 4 * h, h);
+    o.b_fc1 = add(p + "b_fc1", 1, 4 * h);
+    o.w_fc2 = add(p + "w_fc2", h, 4 * h);
+    o.b_fc2 = add(p + "b_fc2", 1, h);
+    c->loff.push_back(o);
+  }
+  if (c->last) {
+    c->lnf_g = add("lnf_g", 1, h);
+    c->lnf_b = add("lnf_b", 1, h);
+    c->head_w = add("head_w", V, h);
+  }
+  c->nflat = off;
+}
+
+// D-22 initialisation on the device (bf16-representable by truncation, D-15).
+static int init_weights(Ctx* c) {
+  uint64_t seed = c->mc.init_seed;
+  const float proj = 0.02f / sqrtf(2.0f * c->mc.n_layers);
+  float* m32 = c->oc.offload ? nullptr : c->master;
+  for (size_t i = 0; i < c->tensors.size(); ++i) {
+    const TensorRec& t = c->tensors[i];
+    const std::string leaf = t.name.substr(t.name.find('.') == std::string::npos ? 0 : t.name.find('.') + 1);
+    float mean = 0.f, sd = 0.02f;
+    if (leaf.size() > 2 && leaf.compare(leaf.size() - 2, 2, "_g") == 0) { mean = 1.f; sd = 0.f; }
+    else if ((leaf.size() > 2 && leaf.compare(leaf.size() - 2, 2, "_b") == 0) || leaf.rfind("b_", 0) == 0) sd = 0.f;
+    else if (leaf == "w_o" || leaf == "w_fc2") sd = proj;
+    if (init_normal(c->p16(t.off), m32 ? m32 + t.off : nullptr, t.numel,
+                    seed * 1000003ull + (uint64_t)c->stage * 7919ull + i, mean, sd, c->s_comp))
+      return c->fail(AXONN_ERR_CUDA, "init_normal");
+  }
+  if (c->oc.offload) {   // theta32 = theta16 exactly at step 0 (D-15)
+    std::vector<uint16_t> tmp(c->nflat);
+    if (cudaMemcpyAsync(tmp.data(), c->theta16, c->nflat * 2, cudaMemcpyDeviceToHost, c->s_comp) != cudaSuccess ||
+        cudaStreamSynchronize(c->s_comp) != cudaSuccess)
+      return c->fail(AXONN_ERR_CUDA, "init offload copy");
+    for (int64_t i = 0; i < c->nflat; ++i) c->master[i] = bf2f(tmp[i]);
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ init
+static int split_comm(Ctx* c, ncclComm_t parent, int color, int key, ncclComm_t* out,
+                      int max_ctas) {
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  if (max_ctas > 0) {
+    cfg.maxCTAs = max_ctas;
+    cfg.minCTAs = 1;
+  }
+  ncclComm_t nc = nullptr;
+  int rc = c->check_nccl(ncclCommSplit(parent, color, key, &nc, &cfg), "ncclCommSplit");
+  if (rc) return rc;
+  if (nc) c->owned_comms.push_back(nc);
+  *out = nc;
+  return 0;
+}
+
+static int plan_memory(Ctx* c) {
+  const size_t Mh = (size_t)c->M * c->h;
+  const size_t att = (size_t)c->microbatch * c->heads * c->s * c->s;
+  c->slots.resize(c->limit);
+  for (int si = 0; si < c->limit; ++si) {
+    Slot& sl = c->slots[si];
+    sl.in = c->dalloc(Mh * 2);
+    sl.L.resize(c->nl);
+    for (int li = 0; li < c->nl; ++li) {
+      LayerStash& st = sl.L[li];
+      st.u = c->dalloc(Mh * 2);
+      st.qkv = c->dalloc(3 * Mh * 2);
+      st.P = c->dalloc(att * 2);
+      st.o = c->dalloc(Mh * 2);
+      st.x1 = c->dalloc(Mh * 2);
+      st.w = c->dalloc(Mh * 2);
+      st.pre = c->dalloc(4 * Mh * 2);
+      st.act = c->dalloc(4 * Mh * 2);
+      st.out = c->dalloc(Mh * 2);
+      st.mean1 = (float*)c->dalloc(c->M * 4);
+      st.rstd1 = (float*)c->dalloc(c->M * 4);
+      st.mean2 = (float*)c->dalloc(c->M * 4);
+      st.rstd2 = (float*)c->dalloc(c->M * 4);
+      if (!st.u || !st.qkv || !st.P || !st.o || !st.x1 || !st.w || !st.pre || !st.act || !st.out ||
+          !st.mean1 || !st.rstd1 || !st.mean2 || !st.rstd2)
+        return c->fail(AXONN_ERR_OOM, "activation stash allocation");
+    }
+    if (c->last) {
+      sl.hf = c->dalloc(Mh * 2);
+      sl.meanf = (float*)c->dalloc(c->M * 4);
+      sl.rstdf = (float*)c->dalloc(c->M * 4);
+    }
+    if (!c->first) sl.gsend = c->dalloc(Mh * 2);
+    if (!c->last) sl.grecv = c->dalloc(Mh * 2);
+    if (!sl.in) return c->fail(AXONN_ERR_OOM, "slot allocation");
+  }
+  c->S = (float*)c->dalloc(att * 4);
+  c->dS = c->dalloc(att * 2);
+  c->dh0 = c->dalloc(Mh * 2);
+  c->dh1 = c->dalloc(Mh * 2);
+  c->dqkv = c->dalloc(3 * Mh * 2);
+  c->dpre = c->dalloc(4 * Mh * 2);
+  c->dO = c->dalloc(Mh * 2);
+  c->du = c->dalloc(Mh * 2);
+  c->dx1 = c->dalloc(Mh * 2);
+  c->cs_ws = (float*)c->dalloc((size_t)2 * colsum_chunks(c->M) * 4 * c->h * 4);
+  c->row_loss = (float*)c->dalloc(c->M * 4);
+  c->d_loss = (double*)c->dalloc(64);
+  if (c->last) c->logits = c->dalloc((size_t)c->M * c->V * 2);
+  if (!c->S || !c->dS || !c->dh0 || !c->dh1 || !c->dqkv || !c->dpre || !c->dO || !c->du ||
+      !c->dx1 || !c->cs_ws || !c->row_loss || !c->d_loss || (c->last && !c->logits))
+    return c->fail(AXONN_ERR_OOM, "workspace allocation");
+  if (cudaMallocHost(&c->h_loss, 64) != cudaSuccess) return c->fail(AXONN_ERR_OOM, "pinned loss");
+  // parameters, gradients, optimizer state
+  c->theta16 = c->dalloc(c->nflat * 2);
+  c->grad32 = (float*)c->dalloc(c->nflat * 4);
+  c->grad16 = c->dalloc(c->nflat * 2);
+  if (!c->theta16 || !c->grad32 || !c->grad16) return c->fail(AXONN_ERR_OOM, "parameter buffers");
+  if (cudaMemsetAsync(c->theta16, 0, c->nflat * 2, c->s_comp) != cudaSuccess ||
+      cudaMemsetAsync(c->grad32, 0, c->nflat * 4, c->s_comp) != cudaSuccess ||
+      cudaMemsetAsync(c->grad16, 0, c->nflat * 2, c->s_comp) != cudaSuccess)
+    return c->fail(AXONN_ERR_CUDA, "memset parameters");
+  if (c->oc.offload) {
+    for (float** p : {&c->master, &c->adam_m, &c->adam_v})
+      if (cudaHostAlloc((void**)p, c->nflat * 4, cudaHostAllocPortable) != cudaSuccess)
+        return c->fail(AXONN_ERR_OOM, "pinned host optimizer state");
+    memset(c->adam_m, 0, c->nflat * 4);
+    memset(c->adam_v, 0, c->nflat * 4);
+    int64_t bs = c->oc.bucket_elems;
+    if (bs > c->nflat) bs = c->nflat;
+    for (int r = 0; r < 3; ++r)
+      for (int a = 0; a < 3; ++a)
+        if (!(c->ring[r][a] = (float*)c->dalloc(bs * 4))) return c->fail(AXONN_ERR_OOM, "offload ring");
+  } else {
+    c->master = (float*)c->dalloc(c->nflat * 4);
+    c->adam_m = (float*)c->dalloc(c->nflat * 4);
+    c->adam_v = (float*)c->dalloc(c->nflat * 4);
+    if (!c->master || !c->adam_m || !c->adam_v) return c->fail(AXONN_ERR_OOM, "optimizer state");
+    if (cudaMemsetAsync(c->master, 0, c->nflat * 4, c->s_comp) != cudaSuccess)
+      return c->fail(AXONN_ERR_CUDA, "memset master");
+    if (cudaMemsetAsync(c->adam_m, 0, c->nflat * 4, c->s_comp) != cudaSuccess ||
+        cudaMemsetAsync(c->adam_v, 0, c->nflat * 4, c->s_comp) != cudaSuccess)
+      return c->fail(AXONN_ERR_CUDA, "memset adam");
+  }
+  return 0;
+}
+
+}  // namespace axonn
+
+using namespace axonn;
+
+struct axonn_ctx : public Ctx {};
+
+extern "C" {
+
+AXONN_API axonn_status axonn_get_unique_id(void* out128) {
+  if (!out128) return AXONN_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return AXONN_ERR_NCCL;
+  memcpy(out128, &id, sizeof(id));
+  return AXONN_OK;
+}
+
+AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
+                                  const axonn_model_cfg* model, const axonn_opt_cfg* opt,
+                                  const axonn_dist* dist, axonn_ctx** out) {
+  if (!out) return AXONN_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!model || !opt || g_inter < 1 || g_data < 1 || microbatch < 1) return AXONN_ERR_INVALID_ARG;
+  const int world = dist ? dist->world_size : 1;
+  const int rank = dist ? dist->world_rank : 0;
+  if (world != g_inter * g_data) return AXONN_ERR_GRID_MISMATCH;
+  if (rank < 0 || rank >= world) return AXONN_ERR_INVALID_ARG;
+  if (model->n_layers < 1 || model->n_layers % g_inter) return AXONN_ERR_NONDIVISIBLE_LAYERS;
+  if (model->hidden < 8 || model->heads < 1 || model->hidden % model->heads ||
+      model->hidden % 8 || model->seq_len < 8 || model->seq_len % 8 || model->vocab < 2 ||
+      model->vocab % 8)
+    return AXONN_ERR_INVALID_ARG;
+  const int d = model->hidden / model->heads;
+  if (d % 8) return AXONN_ERR_INVALID_ARG;   // TMA head stride (padded heads: next step)
+  if (!(opt->lr >= 0) || !(opt->beta1 >= 0 && opt->beta1 < 1) || !(opt->beta2 >= 0 && opt->beta2 < 1) ||
+      !(opt->eps > 0) || !(opt->loss_scale > 0) || opt->bucket_elems < 1 || opt->coarsen_k < 1 ||
+      opt->pipeline_limit < 0)
+    return AXONN_ERR_INVALID_ARG;
+  if (world > 1 && (!dist || !dist->nccl_id)) return AXONN_ERR_INVALID_ARG;
+
+  axonn_ctx* c = new (std::nothrow) axonn_ctx();
+  if (!c) return AXONN_ERR_OOM;
+  c->g_inter = g_inter; c->g_data = g_data; c->microbatch = microbatch;
+  c->mc = *model; c->oc = *opt;
+  if (c->oc.bucket_elems % 4) c->oc.bucket_elems += 4 - c->oc.bucket_elems % 4;   // 16-B aligned buckets
+  c->rank = rank; c->world = world; c->device = dist ? dist->device : 0;
+  c->stage = rank % g_inter;            // world_rank = j * G_inter + i (D-29)
+  c->replica = rank / g_inter;
+  c->first = c->stage == 0;
+  c->last = c->stage == g_inter - 1;
+  c->nl = model->n_layers / g_inter;
+  c->layer0 = c->stage * c->nl;
+  c->h = model->hidden; c->heads = model->heads; c->d = d; c->s = model->seq_len;
+  c->V = model->vocab; c->M = microbatch * model->seq_len;
+  c->limit = g_inter == 1 ? 1 : (opt->pipeline_limit > 0 ? opt->pipeline_limit : g_inter);
+
+  auto bail = [&](int rc) {
+    axonn_free(c);
+    return (axonn_status)rc;
+  };
+  int rc = c->check_cuda(cudaSetDevice(c->device), "cudaSetDevice");
+  if (rc) return bail(rc);
+  cudaDeviceProp prop;
+  if ((rc = c->check_cuda(cudaGetDeviceProperties(&prop, c->device), "props"))) return bail(rc);
+  if (prop.major < 10) return bail(c->fail(AXONN_ERR_CUDA, "needs an sm_100a (B200) device"));
+  c->num_sms = prop.multiProcessorCount;
+  for (cudaStream_t* st : {&c->s_comp, &c->s_send_act, &c->s_send_grad, &c->s_recv_act,
+                           &c->s_recv_grad, &c->s_dp, &c->s_h2d, &c->s_d2h, &c->s_opt})
+    if ((rc = c->check_cuda(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking), "stream")))
+      return bail(rc);
+  for (cudaEvent_t* e : {&c->ev_grads_ready, &c->ev_opt_done, &c->ev_loss})
+    if ((rc = c->check_cuda(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event"))) return bail(rc);
+  for (int r = 0; r < 3; ++r)
+    for (cudaEvent_t* e : {&c->ev_h2d[r], &c->ev_adam[r], &c->ev_d2h[r]})
+      if ((rc = c->check_cuda(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event"))) return bail(rc);
+
+  build_tensors(c);
+  c->grad_written.assign(c->tensors.size(), 0);
+  if ((rc = plan_memory(c))) return bail(rc);
+  if ((rc = init_weights(c))) return bail(rc);
+
+  // NCCL: world, column (all-reduce) and per-direction neighbour links (2-rank comms).
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, dist->nccl_id, sizeof(id));
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    if ((rc = c->check_nccl(ncclCommInitRankConfig(&c->world_comm, world, id, rank, &cfg),
+                            "ncclCommInitRank")))
+      return bail(rc);
+    c->owned_comms.push_back(c->world_comm);
+    if ((rc = split_comm(c, c->world_comm, g_data > 1 ? c->stage : NCCL_SPLIT_NOCOLOR, c->replica,
+                         &c->dp_comm, 0)))
+      return bail(rc);
+    // links between stage k and k+1 of row j; even and odd boundaries in separate splits so
+    // that every rank joins at most one comm per split.  P2P comms capped at 4 CTAs.
+    for (int dir = 0; dir < 2; ++dir) {
+      for (int parity = 0; parity < 2; ++parity) {
+        int color = NCCL_SPLIT_NOCOLOR;
+        int k_lo = c->stage, k_hi = c->stage - 1;   // boundary to the right / left of this stage
+        int kb = -1;
+        if (g_inter > 1) {
+          if (k_lo % 2 == parity && k_lo < g_inter - 1) kb = k_lo;
+          else if (k_hi >= 0 && k_hi % 2 == parity) kb = k_hi;
+        }
+        if (kb >= 0) color = c->replica * g_inter + kb;
+        ncclComm_t nc = nullptr;
+        if ((rc = split_comm(c, c->world_comm, color, c->stage, &nc, 4))) return bail(rc);
+        if (kb < 0) continue;
+        bool right = (kb == c->stage);   // comm with stage+1
+        if (dir == 0) {
+          if (right) c->act_out = nc; else c->act_in = nc;
+        } else {
+          if (right) c->grad_in = nc; else c->grad_out = nc;
+        }
+      }
+    }
+  }
+  if ((rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "init sync"))) return bail(rc);
+  *out = c;
+  return AXONN_OK;
+}
+
+AXONN_API void axonn_free(axonn_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (ncclComm_t nc : c->owned_comms) {
+    if (c->sticky) ncclCommAbort(nc);
+    else ncclCommDestroy(nc);
+  }
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->oc.offload) {
+    if (c->master) cudaFreeHost(c->master);
+    if (c->adam_m) cudaFreeHost(c->adam_m);
+    if (c->adam_v) cudaFreeHost(c->adam_v);
+  }
+  if (c->h_loss) cudaFreeHost(c->h_loss);
+  if (c->dtok) cudaFree(c->dtok);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->timer)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_grads_ready, c->ev_opt_done, c->ev_loss})
+    if (e) cudaEventDestroy(e);
+  for (int r = 0; r < 3; ++r)
+    for (cudaEvent_t e : {c->ev_h2d[r], c->ev_adam[r], c->ev_d2h[r]})
+      if (e) cudaEventDestroy(e);
+  for (cudaStream_t st : {c->s_comp, c->s_send_act, c->s_send_grad, c->s_recv_act, c->s_recv_grad,
+                          c->s_dp, c->s_h2d, c->s_d2h, c->s_opt})
+    if (st) cudaStreamDestroy(st);
+  delete c;
+}
+
+AXONN_API const char* axonn_last_error(const axonn_ctx* c) {
+  if (!c) return "null context";
+  return c->err.c_str();
+}
+
+AXONN_API int axonn_num_tensors(const axonn_ctx* c) { return c ? (int)c->tensors.size() : -1; }
+
+AXONN_API axonn_status axonn_tensor_info(const axonn_ctx* c, int idx, char name[64],
+                                         int64_t shape[2], int64_t* numel) {
+  if (!c || idx < 0 || idx >= (int)c->tensors.size()) return AXONN_ERR_INVALID_ARG;
+  const TensorRec& t = c->tensors[idx];
+  if (name) {
+    strncpy(name, t.name.c_str(), 63);
+    name[63] = 0;
+  }
+  if (shape) {
+    shape[0] = t.rows;
+    shape[1] = t.cols;
+  }
+  if (numel) *numel = t.numel;
+  return AXONN_OK;
+}
+
+AXONN_API axonn_status axonn_read_tensor(axonn_ctx* c, int which, int idx, float* dst) {
+  if (!c || !dst || idx < 0 || idx >= (int)c->tensors.size()) return AXONN_ERR_INVALID_ARG;
+  if (c->sticky) return AXONN_ERR_STATE;
+  CU(cudaSetDevice(c->device));
+  CU(cudaDeviceSynchronize());
+  const TensorRec& t = c->tensors[idx];
+  switch (which) {
+    case AXONN_T_PARAM16:
+    case AXONN_T_GRAD: {
+      std::vector<uint16_t> tmp(t.numel);
+      const char* base = static_cast<const char*>(which == AXONN_T_PARAM16 ? c->theta16 : c->grad16);
+      CU(cudaMemcpy(tmp.data(), base + t.off * 2, t.numel * 2, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < t.numel; ++i) dst[i] = bf2f(tmp[i]);
+      return AXONN_OK;
+    }
+    case AXONN_T_GRAD32:
+      CU(cudaMemcpy(dst, c->grad32 + t.off, t.numel * 4, cudaMemcpyDeviceToHost));
+      return AXONN_OK;
+    case AXONN_T_MASTER:
+    case AXONN_T_ADAM_M:
+    case AXONN_T_ADAM_V: {
+      const float* src = which == AXONN_T_MASTER ? c->master : which == AXONN_T_ADAM_M ? c->adam_m : c->adam_v;
+      if (c->oc.offload) memcpy(dst, src + t.off, t.numel * 4);
+      else CU(cudaMemcpy(dst, src + t.off, t.numel * 4, cudaMemcpyDeviceToHost));
+      return AXONN_OK;
+    }
+  }
+  return AXONN_ERR_INVALID_ARG;
+}
+
+AXONN_API axonn_status axonn_write_tensor(axonn_ctx* c, int which, int idx, const float* src) {
+  if (!c || !src || idx < 0 || idx >= (int)c->tensors.size()) return AXONN_ERR_INVALID_ARG;
+  if (c->sticky) return AXONN_ERR_STATE;
+  CU(cudaSetDevice(c->device));
+  CU(cudaDeviceSynchronize());
+  const TensorRec& t = c->tensors[idx];
+  std::vector<uint16_t> tmp;
+  auto put16 = [&](void* base) -> int {
+    tmp.resize(t.numel);
+    for (int64_t i = 0; i < t.numel; ++i) tmp[i] = f2bf(src[i]);
+    return c->check_cuda(cudaMemcpy(static_cast<char*>(base) + t.off * 2, tmp.data(), t.numel * 2,
+                                    cudaMemcpyHostToDevice), "write16");
+  };
+  int rc = 0;
+  switch (which) {
+    case AXONN_T_PARAM16:
+      rc = put16(c->theta16);
+      break;
+    case AXONN_T_GRAD:
+      rc = put16(c->grad16);
+      c->grad_written[idx] = 1;
+      {
+        bool all = true;
+        for (char w : c->grad_written) all = all && w;
+        if (all) {
+          c->grads_ready = true;
+          c->ev_chunk.clear();
+          std::fill(c->grad_written.begin(), c->grad_written.end(), 0);
+        }
+      }
+      break;
+    case AXONN_T_GRAD32:
+      rc = c->check_cuda(cudaMemcpy(c->grad32 + t.off, src, t.numel * 4, cudaMemcpyHostToDevice), "write32");
+      break;
+    case AXONN_T_MASTER:
+    case AXONN_T_ADAM_M:
+    case AXONN_T_ADAM_V: {
+      float* dstp = which == AXONN_T_MASTER ? c->master : which == AXONN_T_ADAM_M ? c->adam_m : c->adam_v;
+      if (c->oc.offload) memcpy(dstp + t.off, src, t.numel * 4);
+      else rc = c->check_cuda(cudaMemcpy(dstp + t.off, src, t.numel * 4, cudaMemcpyHostToDevice), "write32");
+      if (!rc && which == AXONN_T_MASTER) rc = put16(c->theta16);   // theta16 = RNE(theta32)
+      break;
+    }
+    default:
+      return AXONN_ERR_INVALID_ARG;
+  }
+  return (axonn_status)rc;
+}
+
+AXONN_API axonn_status axonn_timer_mark(axonn_ctx* c, int id) {
+  if (!c || id < 0 || id >= 8) return AXONN_ERR_INVALID_ARG;
+  CU(cudaSetDevice(c->device));
+  if (!c->timer[id]) CU(cudaEventCreate(&c->timer[id]));
+  CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
+  cudaEvent_t e = c->ev();
+  CU(cudaEventRecord(e, c->s_dp));
+  CU(cudaStreamWaitEvent(c->s_comp, e, 0));
+  CU(cudaEventRecord(c->timer[id], c->s_comp));
+  return AXONN_OK;
+}
+
+AXONN_API axonn_status axonn_timer_elapsed(axonn_ctx* c, int a, int b, double* ms) {
+  if (!c || !ms || a < 0 || a >= 8 || b < 0 || b >= 8 || !c->timer[a] || !c->timer[b])
+    return AXONN_ERR_INVALID_ARG;
+  CU(cudaSetDevice(c->device));
+  CU(cudaEventSynchronize(c->timer[b]));
+  float f = 0;
+  CU(cudaEventElapsedTime(&f, c->timer[a], c->timer[b]));
+  *ms = f;
+  return AXONN_OK;
+}
+
+AXONN_API axonn_status axonn_set_profiling(axonn_ctx* c, int on) {
+  if (!c) return AXONN_ERR_INVALID_ARG;
+  c->profiling = on != 0;
+  return AXONN_OK;
+}
+
+AXONN_API axonn_status axonn_stats(const axonn_ctx* c, double* out, int n) {
+  if (!c || !out || n < 0) return AXONN_ERR_INVALID_ARG;
+  for (int i = 0; i < n && i < AXONN_STAT_COUNT; ++i) out[i] = c->stats[i];
+  for (int i = AXONN_STAT_COUNT; i < n; ++i) out[i] = 0;
+  return AXONN_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ Alg. 2 + Alg. 1
+namespace axonn {
+
+// Alg. 2 on this rank for microbatches 0..m-1.
+static int run_pipeline(Ctx* c, int m) {
+  const size_t Mh = (size_t)c->M * c->h;
+  const int P = c->g_inter, L = c->limit;
+  int rc;
+  if (P == 1) {   // D-18: F, loss, B per microbatch; no messages
+    for (int mb = 0; mb < m; ++mb) {
+      Slot& sl = c->slots[0];
+      if ((rc = c->forward(sl, mb))) return rc;
+      if ((rc = c->backward(sl, mb, nullptr))) return rc;
+    }
+    return 0;
+  }
+  // In 2-rank link comms the lower stage is rank 0: act_out/grad_in peer = 1, act_in/grad_out peer = 0.
+  std::vector<cudaEvent_t> ev_act(m, nullptr), ev_grad(m, nullptr), ev_sent_grad(m, nullptr),
+      ev_sent_act(m, nullptr), ev_bdone(m, nullptr);
+  int next_act_post = 0, next_grad_post = 0;   // next microbatch whose receive is posted
+  int next_act = 0, next_grad = 0;             // next microbatch expected on each link (FIFO)
+  int done_b = 0;                              // backwards completed on this stage
+  int popped = 0;                              // stage 0 injections
+  auto slot_of = [&](int mb) -> Slot& { return c->slots[mb % L]; };
+  auto post = [&]() -> int {
+    // pre-post receives into free slots, in microbatch order
+    while (!c->first && next_act_post < m && next_act_post < done_b + L) {
+      int mb = next_act_post++;
+      ev_act[mb] = c->ev();
+      // the slot's previous occupant (mb - L) must have finished its backward on the GPU
+      if (mb >= L) cudaStreamWaitEvent(c->s_recv_act, ev_bdone[mb - L], 0);
+      int r = c->check_nccl(ncclRecv(slot_of(mb).in, Mh, ncclBfloat16, 0, c->act_in, c->s_recv_act),
+                            "ncclRecv act");
+      if (r) return r;
+      if ((r = c->check_cuda(cudaEventRecord(ev_act[mb], c->s_recv_act), "rec"))) return r;
+    }
+    while (!c->last && next_grad_post < m && next_grad_post < done_b + L) {
+      int mb = next_grad_post++;
+      ev_grad[mb] = c->ev();
+      if (mb >= L) cudaStreamWaitEvent(c->s_recv_grad, ev_bdone[mb - L], 0);
+      int r = c->check_nccl(ncclRecv(slot_of(mb).grecv, Mh, ncclBfloat16, 1, c->grad_in, c->s_recv_grad),
+                            "ncclRecv grad");
+      if (r) return r;
+      if ((r = c->check_cuda(cudaEventRecord(ev_grad[mb], c->s_recv_grad), "rec"))) return r;
+    }
+    return 0;
+  };
+  auto send_act = [&](int mb) -> int {
+    Slot& sl = slot_of(mb);
+    cudaEvent_t e = c->ev();
+    cudaEventRecord(e, c->s_comp);
+    cudaStreamWaitEvent(c->s_send_act, e, 0);
+    const void* out = c->nl > 0 ? sl.L[c->nl - 1].out : sl.in;
+    c->stats[AXONN_STAT_P2P_BYTES] += (double)Mh * 2;
+    int r = c->check_nccl(ncclSend(out, Mh, ncclBfloat16, 1, c->act_out, c->s_send_act), "ncclSend act");
+    ev_sent_act[mb] = c->ev();
+    cudaEventRecord(ev_sent_act[mb], c->s_send_act);
+    return r;
+  };
+  auto send_grad = [&](int mb) -> int {
+    Slot& sl = slot_of(mb);
+    cudaEvent_t e = c->ev();
+    cudaEventRecord(e, c->s_comp);
+    cudaStreamWaitEvent(c->s_send_grad, e, 0);
+    c->stats[AXONN_STAT_P2P_BYTES] += (double)Mh * 2;
+    int r = c->check_nccl(ncclSend(sl.gsend, Mh, ncclBfloat16, 0, c->grad_out, c->s_send_grad),
+                          "ncclSend grad");
+    ev_sent_grad[mb] = c->ev();
+    cudaEventRecord(ev_sent_grad[mb], c->s_send_grad);
+    return r;
+  };
+  auto forward_of = [&](int mb) -> int {   // Forward (+ Backward(1) and grad send on the last stage)
+    Slot& sl = slot_of(mb);
+    sl.mb = mb;
+    if (!c->first) cudaStreamWaitEvent(c->s_comp, ev_act[mb], 0);
+    // a slot's gradient-out buffer is reused only after its previous send finished
+    if (!c->first && mb >= L && ev_sent_grad[mb - L]) cudaStreamWaitEvent(c->s_comp, ev_sent_grad[mb - L], 0);
+    if (!c->last && mb >= L && ev_sent_act[mb - L]) cudaStreamWaitEvent(c->s_comp, ev_sent_act[mb - L], 0);
+    int r = c->forward(sl, mb);
+    if (r) return r;
+    if (c->last) {
+      if ((r = c->backward(sl, mb, nullptr))) return r;
+      ev_bdone[mb] = c->ev();
+      cudaEventRecord(ev_bdone[mb], c->s_comp);
+      ++done_b;
+      return send_grad(mb);
+    }
+    return send_act(mb);
+  };
+  auto backward_of = [&](int mb) -> int {
+    Slot& sl = slot_of(mb);
+    cudaStreamWaitEvent(c->s_comp, ev_grad[mb], 0);
+    int r = c->backward(sl, mb, sl.grecv);
+    if (r) return r;
+    ev_bdone[mb] = c->ev();
+    cudaEventRecord(ev_bdone[mb], c->s_comp);
+    ++done_b;
+    if (!c->first) return send_grad(mb);
+    if (popped < m) {   // Alg. 2 l.24-26: inject the next microbatch
+      int nxt = popped++;
+      return forward_of(nxt);
+    }
+    return 0;
+  };
+
+  if ((rc = post())) return rc;
+  if (c->first) {   // Alg. 2 l.3-9: warm-up
+    int n = L < m ? L : m;
+    for (int k = 0; k < n; ++k) {
+      int mb = popped++;
+      if ((rc = forward_of(mb))) return rc;
+    }
+  }
+  auto t_last = std::chrono::steady_clock::now();
+  const double watchdog_s = 600.0;
+  int fwd_done = c->first ? popped : 0;
+  while (true) {
+    bool need_act = !c->first && next_act < m;
+    bool need_grad = !c->last && next_grad < m;
+    if (!need_act && !need_grad) break;
+    if ((rc = post())) return rc;
+    bool grad_landed = need_grad && next_grad < next_grad_post &&
+                       cudaEventQuery(ev_grad[next_grad]) == cudaSuccess;
+    bool act_landed = !grad_landed && need_act && next_act < next_act_post &&
+                      cudaEventQuery(ev_act[next_act]) == cudaSuccess;
+    if (grad_landed) {   // backward-first among landed messages (D-19)
+      int mb = next_grad++;
+      if ((rc = backward_of(mb))) return rc;
+      t_last = std::chrono::steady_clock::now();
+    } else if (act_landed) {
+      int mb = next_act++;
+      ++fwd_done;
+      if ((rc = forward_of(mb))) return rc;
+      t_last = std::chrono::steady_clock::now();
+    } else {
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t_last).count() > watchdog_s)
+        return c->fail(AXONN_ERR_TIMEOUT, "Alg. 2 watchdog: no message landed for " +
+                                              std::to_string((int)watchdog_s) + " s (stage " +
+                                              std::to_string(c->stage) + ")");
+      std::this_thread::yield();
+    }
+  }
+  (void)fwd_done;
+  // all sends must complete before the slots are reused by the next batch
+  cudaEvent_t e1 = c->ev(), e2 = c->ev();
+  cudaEventRecord(e1, c->s_send_act);
+  cudaEventRecord(e2, c->s_send_grad);
+  cudaStreamWaitEvent(c->s_comp, e1, 0);
+  cudaStreamWaitEvent(c->s_comp, e2, 0);
+  return 0;
+}
+
+static int64_t chunk_elems(const Ctx* c) {
+  return (int64_t)c->oc.coarsen_k * c->oc.bucket_elems;
+}
+
+// Alg. 1 l.4-6 + l.11-14 on this rank.
+static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_device, int batch,
+                                   float* loss_out) {
+  if (!c) return AXONN_ERR_INVALID_ARG;
+  if (c->sticky) return AXONN_ERR_STATE;
+  if (batch < 1 || batch % (c->g_data * c->microbatch)) return AXONN_ERR_NONDIVISIBLE_BATCH;
+  if (c->grads_ready) return (axonn_status)c->fail(AXONN_ERR_STATE, "run_batch twice without optimizer_step");
+  if (!tokens) return AXONN_ERR_INVALID_ARG;
+  CU(cudaSetDevice(c->device));
+  auto t0 = std::chrono::steady_clock::now();
+  const int shard = batch / c->g_data;
+  const int m = shard / c->microbatch;
+  c->cur_mtotal = batch / c->microbatch;   // D-9: microbatches in the whole batch
+  c->ev_next = 0;
+  c->prof.clear();
+  c->launches = 0;
+  c->bwd_count = 0;
+  c->stats[AXONN_STAT_P2P_BYTES] = 0;
+  c->stats[AXONN_STAT_ALLREDUCE_BYTES] = 0;
+  c->stats[AXONN_STAT_H2D_BYTES] = 0;
+  c->stats[AXONN_STAT_D2H_BYTES] = 0;
+  const int64_t need = (int64_t)shard * (c->s + 1);
+  if (need > c->dtok_cap) {
+    if (c->dtok) cudaFree(c->dtok);
+    c->dtok = nullptr;
+    CU(cudaMalloc(&c->dtok, need * 4));
+    c->dtok_cap = need;
+  }
+  // the next forward reads theta16 written by the previous optimizer step
+  CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
+  const size_t row0 = (size_t)c->replica * shard * (c->s + 1);   // Alg. 1 l.5
+  if (on_device) {
+    CU(cudaMemcpyAsync(c->dtok, tokens, need * 4, cudaMemcpyDeviceToDevice, c->s_comp));
+  } else {
+    CU(cudaMemcpyAsync(c->dtok, tokens + row0, need * 4, cudaMemcpyHostToDevice, c->s_comp));
+    c->stats[AXONN_STAT_H2D_BYTES] += need * 4.0;
+  }
+  CU(cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->s_comp));
+  if (c->first) {   // embedding gradients are scatter-added (K6)
+    CU(cudaMemsetAsync(c->g32(c->tok_emb), 0, (size_t)c->V * c->h * 4, c->s_comp));
+    CU(cudaMemsetAsync(c->g32(c->pos_emb), 0, (size_t)c->s * c->h * 4, c->s_comp));
+  }
+  int rc = run_pipeline(c, m);
+  if (rc) return (axonn_status)rc;
+  // half-precision gradients (D-20: fp32 accumulation, bf16 reduction)
+  if (cast_f32_bf16(c->grad32, c->grad16, c->nflat, c->s_comp)) return (axonn_status)c->fail(AXONN_ERR_CUDA, "cast");
+  ++c->launches;
+  CU(cudaEventRecord(c->ev_grads_ready, c->s_comp));
+  CU(cudaEventRecord(c->ev_loss, c->s_comp));
+  CU(cudaStreamWaitEvent(c->s_dp, c->ev_loss, 0));
+  if (c->world > 1)   // C5: loss sum over the last-stage ranks, seen by every rank
+    NC(ncclAllReduce(c->d_loss, c->d_loss, 1, ncclFloat64, ncclSum, c->world_comm, c->s_dp));
+  CU(cudaMemcpyAsync(c->h_loss, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->s_dp));
+  cudaEvent_t ev_loss_host = c->ev();
+  CU(cudaEventRecord(ev_loss_host, c->s_dp));
+  // Alg. 1 l.13: SUM all-reduce over the column, chunks of k * bsize
+  c->ev_chunk.clear();
+  if (c->g_data > 1) {
+    CU(cudaStreamWaitEvent(c->s_dp, c->ev_grads_ready, 0));
+    const int64_t ch = chunk_elems(c);
+    for (int64_t lo = 0; lo < c->nflat; lo += ch) {
+      int64_t n = std::min(ch, c->nflat - lo);
+      NC(ncclAllReduce(static_cast<char*>(c->grad16) + lo * 2, static_cast<char*>(c->grad16) + lo * 2,
+                       n, ncclBfloat16, ncclSum, c->dp_comm, c->s_dp));
+      cudaEvent_t e = c->ev();
+      CU(cudaEventRecord(e, c->s_dp));
+      c->ev_chunk.push_back(e);
+      c->stats[AXONN_STAT_ALLREDUCE_BYTES] += n * 2.0;
+    }
+  }
+  CU(cudaEventSynchronize(ev_loss_host));
+  if (loss_out) *loss_out = (float)(*c->h_loss / c->oc.loss_scale);
+  c->grads_ready = true;
+  c->stats[AXONN_STAT_T_BATCH_MS] =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return AXONN_OK;
+}
+
+}  // namespace axonn
+
+extern "C" {
+
+AXONN_API axonn_status axonn_run_batch(axonn_ctx* c, const int32_t* tokens, int batch, float* loss_out) {
+  return run_batch_impl(c, tokens, false, batch, loss_out);
+}
+
+AXONN_API axonn_status axonn_run_batch_device(axonn_ctx* c, const int32_t* d_tokens, int batch,
+                                              float* loss_out) {
+  return run_batch_impl(c, d_tokens, true, batch, loss_out);
+}
+
+// Alg. 1 l.7 with the memory optimisation and the
+// all-reduce / optimizer interleave.
+AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
+  if (!c) return AXONN_ERR_INVALID_ARG;
+  if (c->sticky) return AXONN_ERR_STATE;
+  if (!c->grads_ready) return (axonn_status)c->fail(AXONN_ERR_STATE, "optimizer_step without run_batch");
+  CU(cudaSetDevice(c->device));
+  auto t0 = std::chrono::steady_clock::now();
+  const int64_t t = c->t_step + 1;
+  // step scalars in double, rounded once to fp32 (D-14)
+  const double lr = c->oc.lr, b1 = c->oc.beta1, b2 = c->oc.beta2;
+  float sc[9];
+  sc[0] = (float)(1.0 - lr * c->oc.weight_decay);
+  sc[1] = (float)b1;
+  sc[2] = (float)(1.0 - b1);
+  sc[3] = (float)b2;
+  sc[4] = (float)(1.0 - b2);
+  sc[5] = (float)(lr / (1.0 - std::pow(b1, (double)t)));
+  sc[6] = (float)std::sqrt(1.0 - std::pow(b2, (double)t));
+  sc[7] = (float)c->oc.eps;   // eps rounded once
+  sc[8] = (float)(1.0 / c->oc.loss_scale);
+  // the optimizer may start only once the gradients exist
+  CU(cudaStreamWaitEvent(c->s_opt, c->ev_grads_ready, 0));
+  const int64_t bs = c->oc.bucket_elems;
+  const int64_t ch = chunk_elems(c);
+  int64_t chunk_idx = -1;
+  int64_t bucket = 0;
+  for (int64_t lo = 0; lo < c->nflat; lo += bs, ++bucket) {
+    const int64_t n = std::min(bs, c->nflat - lo);
+    const int64_t ci = lo / ch;
+    if (ci != chunk_idx && ci < (int64_t)c->ev_chunk.size()) {   // bucket waits for its chunk
+      CU(cudaStreamWaitEvent(c->s_opt, c->ev_chunk[ci], 0));
+      chunk_idx = ci;
+    }
+    const void* g = static_cast<const char*>(c->grad16) + lo * 2;
+    void* t16 = static_cast<char*>(c->theta16) + lo * 2;
+    ProfRec pr{};
+    if (c->oc.offload) {   // fetch bucket, step, offload back; 3-slot ring
+      const int r = (int)(bucket % 3);
+      if (bucket >= 3) CU(cudaStreamWaitEvent(c->s_h2d, c->ev_d2h[r], 0));
+      CU(cudaMemcpyAsync(c->ring[r][0], c->master + lo, n * 4, cudaMemcpyHostToDevice, c->s_h2d));
+      CU(cudaMemcpyAsync(c->ring[r][1], c->adam_m + lo, n * 4, cudaMemcpyHostToDevice, c->s_h2d));
+      CU(cudaMemcpyAsync(c->ring[r][2], c->adam_v + lo, n * 4, cudaMemcpyHostToDevice, c->s_h2d));
+      CU(cudaEventRecord(c->ev_h2d[r], c->s_h2d));
+      CU(cudaStreamWaitEvent(c->s_opt, c->ev_h2d[r], 0));
+      if (c->profiling) { pr.a = c->ev(); pr.b = c->ev(); cudaEventRecord(pr.a, c->s_opt); }
+      if (adamw_launch(n, g, c->ring[r][0], c->ring[r][1], c->ring[r][2], t16, sc, c->s_opt))
+        return (axonn_status)c->fail(AXONN_ERR_CUDA, "adamw launch");
+      if (c->profiling) { cudaEventRecord(pr.b, c->s_opt); pr.work = n * 28.0; pr.kind = 1; c->prof.push_back(pr); }
+      CU(cudaEventRecord(c->ev_adam[r], c->s_opt));
+      CU(cudaStreamWaitEvent(c->s_d2h, c->ev_adam[r], 0));
+      CU(cudaMemcpyAsync(c->master + lo, c->ring[r][0], n * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+      CU(cudaMemcpyAsync(c->adam_m + lo, c->ring[r][1], n * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+      CU(cudaMemcpyAsync(c->adam_v + lo, c->ring[r][2], n * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+      CU(cudaEventRecord(c->ev_d2h[r], c->s_d2h));
+      c->stats[AXONN_STAT_H2D_BYTES] += n * 12.0;
+      c->stats[AXONN_STAT_D2H_BYTES] += n * 12.0;
+    } else {
+      if (c->profiling) { pr.a = c->ev(); pr.b = c->ev(); cudaEventRecord(pr.a, c->s_opt); }
+      if (adamw_launch(n, g, c->master + lo, c->adam_m + lo, c->adam_v + lo, t16, sc, c->s_opt))
+        return (axonn_status)c->fail(AXONN_ERR_CUDA, "adamw launch");
+      if (c->profiling) { cudaEventRecord(pr.b, c->s_opt); pr.work = n * 28.0; pr.kind = 1; c->prof.push_back(pr); }
+    }
+    ++c->launches;
+  }
+  if (c->oc.offload) {
+    cudaEvent_t e = c->ev();
+    CU(cudaEventRecord(e, c->s_d2h));
+    CU(cudaStreamWaitEvent(c->s_opt, e, 0));
+  }
+  CU(cudaEventRecord(c->ev_opt_done, c->s_opt));
+  CU(cudaEventSynchronize(c->ev_opt_done));
+  c->t_step = t;
+  c->grads_ready = false;
+  c->ev_chunk.clear();
+  c->stats[AXONN_STAT_T_OPT_MS] =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  // kernel-time statistics of this batch + step (profiling mode)
+  double gms = 0, gfl = 0, ams = 0, aby = 0;
+  int gl = 0;
+  for (const ProfRec& p : c->prof) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    if (p.kind == 0) { gms += ms; gfl += p.work; ++gl; }
+    else if (p.kind == 1) { ams += ms; aby += p.work; }
+  }
+  c->stats[AXONN_STAT_GEMM_MS] = gms;
+  c->stats[AXONN_STAT_GEMM_FLOP] = gfl;
+  c->stats[AXONN_STAT_GEMM_LAUNCHES] = gl;
+  c->stats[AXONN_STAT_ADAM_MS] = ams;
+  c->stats[AXONN_STAT_ADAM_BYTES] = aby;
+  c->stats[AXONN_STAT_KERNEL_LAUNCHES] = (double)c->launches;
+  return AXONN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,135 @@
+// Host engine of the AxoNN hybrid step (H1 context, H2 scheduler, H3 optimizer
+// driver, H5 batch plumbing).  Internal — the boundary is
+// include/axonn.h.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/axonn.h"
+#include "kernels.h"
+
+namespace axonn {
+
+struct TensorRec {
+  std::string name;
+  int64_t rows, cols, numel, off;   // off: element offset in every flat buffer
+};
+
+// Element offsets of one layer's tensors in the flat buffers (D-2 layout).
+struct LayerOff {
+  int64_t ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_fc1, b_fc1, w_fc2, b_fc2;
+};
+
+// Activations saved by a layer's forward for its backward (one microbatch).
+struct LayerStash {
+  void *u, *qkv, *P, *o, *x1, *w, *pre, *act, *out;
+  float *mean1, *rstd1, *mean2, *rstd2;
+};
+
+// One in-flight microbatch on this stage (pipeline_limit of them, Alg. 2).
+struct Slot {
+  void* in = nullptr;                 // stage input [M, h]: embedding output or received activation
+  std::vector<LayerStash> L;
+  void* hf = nullptr;                 // last stage: LN_f output
+  float *meanf = nullptr, *rstdf = nullptr;
+  void* gsend = nullptr;              // gradient w.r.t. the stage input, sent to stage i-1
+  void* grecv = nullptr;              // output gradient received from stage i+1
+  int mb = -1;
+};
+
+struct ProfRec {
+  cudaEvent_t a, b;
+  double work;
+  int kind;   // 0 gemm, 1 adam
+};
+
+struct Ctx {
+  // ---- configuration
+  int g_inter = 1, g_data = 1, microbatch = 1;
+  axonn_model_cfg mc{};
+  axonn_opt_cfg oc{};
+  int rank = 0, world = 1, device = 0;
+  int stage = 0, replica = 0;
+  bool first = true, last = true;
+  int nl = 0, layer0 = 0;             // local layers, first global layer id
+  int h = 0, heads = 0, d = 0, s = 0, V = 0, M = 0;   // M = microbatch * seq tokens
+  int limit = 1;
+  std::string err;
+  bool sticky = false;
+  int num_sms = 148;
+
+  // ---- parameters
+  std::vector<TensorRec> tensors;
+  int64_t nflat = 0;
+  int64_t tok_emb = -1, pos_emb = -1, lnf_g = -1, lnf_b = -1, head_w = -1;
+  std::vector<LayerOff> loff;
+  void* theta16 = nullptr;            // bf16 [nflat]
+  float* grad32 = nullptr;            // fp32 accumulation (D-20)
+  void* grad16 = nullptr;             // bf16 all-reduce / optimizer input
+  float *master = nullptr, *adam_m = nullptr, *adam_v = nullptr;   // device or pinned host
+  float* ring[3][3] = {};             // offload ring: [slot][theta, m, v]
+  int64_t t_step = 0;
+
+  // ---- activations / workspace
+  std::vector<void*> allocs;
+  std::vector<Slot> slots;
+  float* S = nullptr;                 // scores / dP fp32 [b a s s]
+  void* dS = nullptr;                 // bf16 [b a s s]
+  void *dh0 = nullptr, *dh1 = nullptr, *dqkv = nullptr, *dpre = nullptr, *dO = nullptr,
+       *du = nullptr, *dx1 = nullptr;
+  float* cs_ws = nullptr;             // column-sum workspace
+  void* logits = nullptr;             // [M, V] bf16 (last stage)
+  float* row_loss = nullptr;
+  double* d_loss = nullptr;           // device loss accumulator
+  double* h_loss = nullptr;           // pinned
+  int32_t* dtok = nullptr;            // this replica's token shard [B/G_data, s+1]
+  int64_t dtok_cap = 0;
+
+  // ---- streams / events / comms
+  cudaStream_t s_comp = nullptr, s_send_act = nullptr, s_send_grad = nullptr,
+               s_recv_act = nullptr, s_recv_grad = nullptr, s_dp = nullptr, s_h2d = nullptr,
+               s_d2h = nullptr, s_opt = nullptr;
+  ncclComm_t world_comm = nullptr, dp_comm = nullptr, act_out = nullptr, act_in = nullptr,
+             grad_out = nullptr, grad_in = nullptr;
+  std::vector<ncclComm_t> owned_comms;
+  cudaEvent_t ev_grads_ready = nullptr, ev_opt_done = nullptr, ev_loss = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;
+  cudaEvent_t ev_h2d[3] = {}, ev_adam[3] = {}, ev_d2h[3] = {};
+  cudaEvent_t timer[8] = {};
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+
+  // ---- state / stats
+  bool grads_ready = false;           // run_batch (or GRAD writes) done, optimizer pending
+  int bwd_count = 0;                  // backwards done in this batch (first one stores)
+  int cur_mtotal = 1;
+  int write_grad_mask = 0;
+  std::vector<char> grad_written;
+  bool profiling = false;
+  std::vector<ProfRec> prof;
+  double stats[AXONN_STAT_COUNT] = {};
+  long long launches = 0;
+
+  // helpers
+  cudaEvent_t ev();                   // next event from the pool (reset per batch)
+  void* dalloc(size_t bytes);
+  int check_cuda(cudaError_t e, const char* what);
+  int check_nccl(ncclResult_t r, const char* what);
+  int fail(int code, const std::string& msg);
+
+  void* p16(int64_t off) const { return static_cast<char*>(theta16) + off * 2; }
+  float* g32(int64_t off) const { return grad32 + off; }
+
+  // model execution (model_exec.cpp)
+  int gemm(GemmArgs g, double flops);
+  int forward(Slot& sl, int mb);          // nn_shard.Forward (and the loss on the last stage)
+  int backward(Slot& sl, int mb, const void* dout);   // nn_shard.Backward
+  int layer_fwd(int li, const void* x, LayerStash& st);
+  int layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void* din);
+};
+
+}  // namespace axonn

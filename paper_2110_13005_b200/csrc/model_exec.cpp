@@ -1,0 +1,283 @@
+// nn_shard.Forward / nn_shard.Backward of one pipeline stage (Alg. 2 l.6, 14,
+// 16, 22, 25) as a chain of sm_100a kernels on s_comp.
+//
+// Layer = GPT-2 pre-LN block (readings D-1..D-8):
+//   u = LN1(x); qkv = u Wqkv^T + b; S = Q K^T / sqrt(d) (causal); P = softmax(S);
+//   o = P V; x1 = x + o Wo^T + bo; w = LN2(x1); pre = w W1^T + b1; a = GeLU(pre);
+//   out = x1 + a W2^T + b2.
+// Every contraction is K1 (tcgen05 GEMM) with its elementwise tail fused in the
+// epilogue (bias, GeLU + pre-activation store, residual add, GeLU' in dgrad,
+// fp32 weight-gradient accumulation).  The last stage adds LN_f, the untied LM
+// head and the fused cross entropy with the loss pre-divided by the number of
+// microbatches in the batch (D-9).
+#include <cmath>
+#include <cstring>
+
+#include "engine.h"
+
+namespace axonn {
+
+int Ctx::gemm(GemmArgs g, double flops) {
+  if (g.Z == 0) g.Z = 1;
+  if (g.Z1 == 0) g.Z1 = 1;
+  if (g.alpha == 0.f) g.alpha = 1.f;
+  if (g.max_ctas == 0 && g_inter > 1) g.max_ctas = num_sms - 8;   // leave SMs to posted NCCL P2P kernels
+  ProfRec pr{};
+  if (profiling) {
+    pr.a = ev();
+    pr.b = ev();
+    pr.work = flops;
+    pr.kind = flops >= 0 ? 0 : 2;
+    cudaEventRecord(pr.a, s_comp);
+  }
+  int rc = gemm_launch(g, s_comp);
+  ++launches;
+  if (rc) return fail(AXONN_ERR_CUDA, "gemm_launch failed rc=" + std::to_string(rc) +
+                                          " M=" + std::to_string(g.M) + " N=" + std::to_string(g.N) +
+                                          " K=" + std::to_string(g.K));
+  if (profiling) {
+    cudaEventRecord(pr.b, s_comp);
+    prof.push_back(pr);
+  }
+  return 0;
+}
+
+static GemmArgs lin_fwd(const void* X, const void* W, int M, int N, int K, void* out) {
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.M = M; g.N = N; g.K = K;
+  g.A = X; g.lda = K;
+  g.B = W; g.ldb = K;
+  g.C = out; g.ldc = N;
+  g.epi = EPI_BF16;
+  return g;
+}
+// dX[M, Kin] = dY[M, Nout] W[Nout, Kin]
+static GemmArgs lin_dgrad(const void* dY, const void* W, int M, int Nout, int Kin, void* dX) {
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.M = M; g.N = Kin; g.K = Nout;
+  g.A = dY; g.lda = Nout;
+  g.B = W; g.ldb = Kin; g.b_mn = 1;
+  g.C = dX; g.ldc = Kin;
+  g.epi = EPI_BF16;
+  return g;
+}
+// dW[Nout, Kin] (+)= dY^T X
+static GemmArgs lin_wgrad(const void* dY, const void* X, int M, int Nout, int Kin, float* dW,
+                          int accumulate) {
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.M = Nout; g.N = Kin; g.K = M;
+  g.A = dY; g.lda = Nout; g.a_mn = 1;
+  g.B = X; g.ldb = Kin; g.b_mn = 1;
+  g.C = dW; g.ldc = Kin;
+  g.epi = EPI_F32;
+  g.accumulate = accumulate;
+  return g;
+}
+
+#define TRY(x)              \
+  do {                      \
+    int _rc = (x);          \
+    if (_rc) return _rc;    \
+  } while (0)
+#define KCHK(x)                                                                       \
+  do {                                                                                \
+    ++launches;                                                                       \
+    if ((x) != 0) return fail(AXONN_ERR_CUDA, std::string("kernel launch failed: ") + #x); \
+  } while (0)
+
+int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
+  const LayerOff& o = loff[li];
+  const int b = microbatch;
+  const double dM = M, dh = h;
+  KCHK(ln_fwd(x, M, h, p16(o.ln1_g), p16(o.ln1_b), st.u, st.mean1, st.rstd1, s_comp));
+  {
+    GemmArgs g = lin_fwd(st.u, p16(o.w_qkv), M, 3 * h, h, st.qkv);
+    g.bias = p16(o.b_qkv);
+    TRY(gemm(g, 2 * dM * 3 * dh * dh));
+  }
+  {  // S = Q K^T / sqrt(d) per (sample, head), causal tile skipping (D-7, D-8)
+    GemmArgs g;
+    memset(&g, 0, sizeof(g));
+    g.M = s; g.N = s; g.K = d; g.Z = b * heads; g.Z1 = heads;
+    g.A = st.qkv; g.lda = 3 * h; g.a_s1 = d; g.a_s2 = (long long)s * 3 * h;
+    g.B = static_cast<char*>(st.qkv) + (size_t)h * 2; g.ldb = 3 * h; g.b_s1 = d;
+    g.b_s2 = (long long)s * 3 * h;
+    g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
+    g.epi = EPI_F32; g.causal = 1; g.alpha = 1.0f / sqrtf((float)d);
+    TRY(gemm(g, -1));
+  }
+  KCHK(softmax_fwd(S, (long long)b * heads * s, s, st.P, s_comp));
+  {  // o = P V, heads merged into [M, h]
+    GemmArgs g;
+    memset(&g, 0, sizeof(g));
+    g.M = s; g.N = d; g.K = s; g.Z = b * heads; g.Z1 = heads;
+    g.A = st.P; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s;
+    g.B = static_cast<char*>(st.qkv) + (size_t)2 * h * 2; g.ldb = 3 * h; g.b_s1 = d;
+    g.b_s2 = (long long)s * 3 * h; g.b_mn = 1;
+    g.C = st.o; g.ldc = h; g.c_s1 = d; g.c_s2 = (long long)s * h;
+    g.epi = EPI_BF16; g.causal = 2;
+    TRY(gemm(g, -1));
+  }
+  {
+    GemmArgs g = lin_fwd(st.o, p16(o.w_o), M, h, h, st.x1);
+    g.bias = p16(o.b_o);
+    g.resid = x; g.ld_resid = h;
+    TRY(gemm(g, 2 * dM * dh * dh));
+  }
+  KCHK(ln_fwd(st.x1, M, h, p16(o.ln2_g), p16(o.ln2_b), st.w, st.mean2, st.rstd2, s_comp));
+  {
+    GemmArgs g = lin_fwd(st.w, p16(o.w_fc1), M, 4 * h, h, st.act);
+    g.bias = p16(o.b_fc1);
+    g.epi = EPI_BIAS_GELU; g.aux = st.pre; g.ld_aux = 4 * h;
+    TRY(gemm(g, 2 * dM * 4 * dh * dh));
+  }
+  {
+    GemmArgs g = lin_fwd(st.act, p16(o.w_fc2), M, h, 4 * h, st.out);
+    g.bias = p16(o.b_fc2);
+    g.resid = st.x1; g.ld_resid = h;
+    TRY(gemm(g, 2 * dM * 4 * dh * dh));
+  }
+  return 0;
+}
+
+int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void* din) {
+  const LayerOff& o = loff[li];
+  const int b = microbatch;
+  const int acc = bwd_count > 0 ? 1 : 0;
+  const double dM = M, dh = h;
+  // FC2: dpre = (dout W2) * GeLU'(pre);  dW2 += dout^T act;  db2 += colsum(dout)
+  {
+    GemmArgs g = lin_dgrad(dout, p16(o.w_fc2), M, h, 4 * h, dpre);
+    g.epi = EPI_DGELU; g.aux = st.pre; g.ld_aux = 4 * h;
+    TRY(gemm(g, 2 * dM * 4 * dh * dh));
+    TRY(gemm(lin_wgrad(dout, st.act, M, h, 4 * h, g32(o.w_fc2), acc), 2 * dM * 4 * dh * dh));
+    KCHK(colsum(dout, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_fc2), nullptr, acc, s_comp));
+  }
+  // FC1: du = dpre W1;  dW1 += dpre^T w;  db1 += colsum(dpre)
+  TRY(gemm(lin_dgrad(dpre, p16(o.w_fc1), M, 4 * h, h, du), 2 * dM * 4 * dh * dh));
+  TRY(gemm(lin_wgrad(dpre, st.w, M, 4 * h, h, g32(o.w_fc1), acc), 2 * dM * 4 * dh * dh));
+  KCHK(colsum(dpre, nullptr, nullptr, nullptr, M, 4 * h, cs_ws, g32(o.b_fc1), nullptr, acc, s_comp));
+  // LN2: dx1 = dout + LN2'(du);  dg2, db2
+  KCHK(ln_bwd(du, st.x1, st.mean2, st.rstd2, M, h, p16(o.ln2_g), dout, dx1, s_comp));
+  KCHK(colsum(du, st.x1, st.mean2, st.rstd2, M, h, cs_ws, g32(o.ln2_b), g32(o.ln2_g), acc, s_comp));
+  // proj: dO = dx1 Wo;  dWo += dx1^T o;  dbo += colsum(dx1)
+  TRY(gemm(lin_dgrad(dx1, p16(o.w_o), M, h, h, dO), 2 * dM * dh * dh));
+  TRY(gemm(lin_wgrad(dx1, st.o, M, h, h, g32(o.w_o), acc), 2 * dM * dh * dh));
+  KCHK(colsum(dx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, s_comp));
+  // attention backward
+  {  // dP = dO V^T (fp32 into S)
+    GemmArgs g;
+    memset(&g, 0, sizeof(g));
+    g.M = s; g.N = s; g.K = d; g.Z = b * heads; g.Z1 = heads;
+    g.A = dO; g.lda = h; g.a_s1 = d; g.a_s2 = (long long)s * h;
+    g.B = static_cast<char*>(st.qkv) + (size_t)2 * h * 2; g.ldb = 3 * h; g.b_s1 = d;
+    g.b_s2 = (long long)s * 3 * h;
+    g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
+    g.epi = EPI_F32; g.causal = 1;
+    TRY(gemm(g, -1));
+  }
+  KCHK(softmax_bwd(st.P, S, (long long)b * heads * s, s, 1.0f / sqrtf((float)d), dS, s_comp));
+  {  // dQ = dS K  -> dqkv[:, 0:h]
+    GemmArgs g;
+    memset(&g, 0, sizeof(g));
+    g.M = s; g.N = d; g.K = s; g.Z = b * heads; g.Z1 = heads;
+    g.A = dS; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s;
+    g.B = static_cast<char*>(st.qkv) + (size_t)h * 2; g.ldb = 3 * h; g.b_s1 = d;
+    g.b_s2 = (long long)s * 3 * h; g.b_mn = 1;
+    g.C = dqkv; g.ldc = 3 * h; g.c_s1 = d; g.c_s2 = (long long)s * 3 * h;
+    g.epi = EPI_BF16; g.causal = 2;
+    TRY(gemm(g, -1));
+  }
+  {  // dK = dS^T Q -> dqkv[:, h:2h]
+    GemmArgs g;
+    memset(&g, 0, sizeof(g));
+    g.M = s; g.N = d; g.K = s; g.Z = b * heads; g.Z1 = heads;
+    g.A = dS; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s; g.a_mn = 1;
+    g.B = st.qkv; g.ldb = 3 * h; g.b_s1 = d; g.b_s2 = (long long)s * 3 * h; g.b_mn = 1;
+    g.C = static_cast<char*>(dqkv) + (size_t)h * 2; g.ldc = 3 * h; g.c_s1 = d;
+    g.c_s2 = (long long)s * 3 * h;
+    g.epi = EPI_BF16; g.causal = 3;
+    TRY(gemm(g, -1));
+  }
+  {  // dV = P^T dO -> dqkv[:, 2h:3h]
+    GemmArgs g;
+    memset(&g, 0, sizeof(g));
+    g.M = s; g.N = d; g.K = s; g.Z = b * heads; g.Z1 = heads;
+    g.A = st.P; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s; g.a_mn = 1;
+    g.B = dO; g.ldb = h; g.b_s1 = d; g.b_s2 = (long long)s * h; g.b_mn = 1;
+    g.C = static_cast<char*>(dqkv) + (size_t)2 * h * 2; g.ldc = 3 * h; g.c_s1 = d;
+    g.c_s2 = (long long)s * 3 * h;
+    g.epi = EPI_BF16; g.causal = 3;
+    TRY(gemm(g, -1));
+  }
+  // QKV: du = dqkv Wqkv;  dWqkv += dqkv^T u;  dbqkv += colsum(dqkv)
+  TRY(gemm(lin_dgrad(dqkv, p16(o.w_qkv), M, 3 * h, h, du), 2 * dM * 3 * dh * dh));
+  TRY(gemm(lin_wgrad(dqkv, st.u, M, 3 * h, h, g32(o.w_qkv), acc), 2 * dM * 3 * dh * dh));
+  KCHK(colsum(dqkv, nullptr, nullptr, nullptr, M, 3 * h, cs_ws, g32(o.b_qkv), nullptr, acc, s_comp));
+  // LN1: din = dx1 + LN1'(du)
+  KCHK(ln_bwd(du, x, st.mean1, st.rstd1, M, h, p16(o.ln1_g), dx1, din, s_comp));
+  KCHK(colsum(du, x, st.mean1, st.rstd1, M, h, cs_ws, g32(o.ln1_b), g32(o.ln1_g), acc, s_comp));
+  return 0;
+}
+
+// nn_shard.Forward for microbatch mb into slot sl.  Stage 0 embeds its tokens;
+// the last stage also runs LN_f, the LM head and the fused, pre-divided loss.
+int Ctx::forward(Slot& sl, int mb) {
+  const int b = microbatch;
+  const int32_t* tok = dtok + (size_t)mb * b * (s + 1);
+  if (first) KCHK(embed_fwd(tok, s + 1, b, s, h, p16(tok_emb), p16(pos_emb), sl.in, s_comp));
+  const void* x = sl.in;
+  for (int li = 0; li < nl; ++li) {
+    TRY(layer_fwd(li, x, sl.L[li]));
+    x = sl.L[li].out;
+  }
+  if (!last) return 0;
+  KCHK(ln_fwd(x, M, h, p16(lnf_g), p16(lnf_b), sl.hf, sl.meanf, sl.rstdf, s_comp));
+  TRY(gemm(lin_fwd(sl.hf, p16(head_w), M, V, h, logits), 2.0 * M * V * h));
+  const float coef = (float)(oc.loss_scale / ((double)cur_mtotal * (double)M));
+  KCHK(xent(logits, tok + 1, s + 1, M, s, V, coef, row_loss, s_comp));
+  KCHK(reduce_sum(row_loss, M, 1.0f / ((float)cur_mtotal * (float)M), d_loss, s_comp));
+  return 0;
+}
+
+// nn_shard.Backward: dout = received output-gradient (nullptr on the last
+// stage, where Backward(1) starts from the cross-entropy gradient already
+// written in place of the logits).  The input gradient goes to sl.gsend.
+int Ctx::backward(Slot& sl, int mb, const void* dout) {
+  const int b = microbatch;
+  const int acc = bwd_count > 0 ? 1 : 0;
+  const int32_t* tok = dtok + (size_t)mb * b * (s + 1);
+  void* cur = dh0;
+  void* nxt = dh1;
+  if (last) {
+    const void* xL = nl > 0 ? sl.L[nl - 1].out : sl.in;
+    TRY(gemm(lin_dgrad(logits, p16(head_w), M, V, h, du), 2.0 * M * V * h));
+    TRY(gemm(lin_wgrad(logits, sl.hf, M, V, h, g32(head_w), acc), 2.0 * M * V * h));
+    KCHK(ln_bwd(du, xL, sl.meanf, sl.rstdf, M, h, p16(lnf_g), nullptr, cur, s_comp));
+    KCHK(colsum(du, xL, sl.meanf, sl.rstdf, M, h, cs_ws, g32(lnf_b), g32(lnf_g), acc, s_comp));
+  } else {
+    cur = const_cast<void*>(dout);
+  }
+  for (int li = nl - 1; li >= 0; --li) {
+    const void* x = li > 0 ? sl.L[li - 1].out : sl.in;
+    void* din = (li == 0 && !first) ? sl.gsend : nxt;
+    TRY(layer_bwd(li, x, sl.L[li], cur, din));
+    if (li == 0 && !first) {
+      cur = din;
+    } else {
+      cur = din;
+      nxt = (din == dh0) ? dh1 : dh0;
+    }
+  }
+  if (first) {
+    // embedding gradients (fp32, zeroed at batch start): deterministic scatter-add
+    KCHK(embed_bwd(tok, s + 1, b, s, h, V, cur, g32(tok_emb), g32(pos_emb), s_comp));
+  }
+  ++bwd_count;
+  return 0;
+}
+
+}  // namespace axonn

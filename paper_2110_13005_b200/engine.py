@@ -1,0 +1,147 @@
+"""Python wrapper of one libaxonn context (one process per GPU).
+
+Argument marshalling only: construction calls ``axonn_init``, ``run_batch``
+calls ``axonn_run_batch`` (Alg. 1 l.4-6 + Alg. 2 + the column all-reduce),
+``optimizer_step`` calls ``axonn_optimizer_step`` (Alg. 1 l.7 with the
+bucketed offload and all-reduce/optimizer overlap).  See include/axonn.h."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+T_PARAM16, T_GRAD, T_MASTER, T_ADAM_M, T_ADAM_V, T_GRAD32 = range(6)
+
+STAT_NAMES = ["t_batch_ms", "t_opt_ms", "gemm_ms", "gemm_flop", "gemm_launches",
+              "kernel_launches", "adam_ms", "adam_bytes", "p2p_bytes", "allreduce_bytes",
+              "h2d_bytes", "d2h_bytes"]
+
+STATUS = {0: "OK", -1: "INVALID_ARG", -2: "GRID_MISMATCH", -3: "NONDIVISIBLE_LAYERS",
+          -4: "NONDIVISIBLE_BATCH", -5: "OOM", -6: "CUDA", -7: "NCCL", -8: "STATE",
+          -9: "NONFINITE", -10: "TIMEOUT"}
+
+
+class AxoNNError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class AxoNN:
+    """One g^{i,j} of the G_inter x G_data grid."""
+
+    def __init__(self, g_inter: int, g_data: int, microbatch: int, *, n_layers: int, hidden: int,
+                 heads: int, seq_len: int, vocab: int, init_seed: int = 42, lr: float = 1e-3,
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                 weight_decay: float = 0.01, loss_scale: float = 1.0, offload: bool = False,
+                 bucket_elems: int = 4_000_000, coarsen_k: int = 4, pipeline_limit: int = 0,
+                 rank: int = 0, world_size: int = 1, device: int = 0, nccl_id: bytes | None = None):
+        self.lib = _lib.load()
+        self.mc = _lib.ModelCfg(n_layers, hidden, heads, seq_len, vocab, init_seed)
+        self.oc = _lib.OptCfg(lr, beta1, beta2, eps, weight_decay, loss_scale, int(offload),
+                              bucket_elems, coarsen_k, pipeline_limit)
+        self._id = C.create_string_buffer(nccl_id if nccl_id else b"\0" * 128, 128)
+        self.dist = _lib.Dist(rank, world_size, C.cast(self._id, C.c_void_p), device)
+        self.ctx = C.c_void_p()
+        rc = self.lib.axonn_init(g_inter, g_data, microbatch, C.byref(self.mc), C.byref(self.oc),
+                                 C.byref(self.dist), C.byref(self.ctx))
+        if rc != 0:
+            raise AxoNNError(rc, "axonn_init failed")
+        self.g_inter, self.g_data, self.microbatch = g_inter, g_data, microbatch
+        self.seq_len = seq_len
+        self.rank, self.world_size = rank, world_size
+        self.stage, self.replica = rank % g_inter, rank // g_inter
+        self._tensors = None
+
+    # ------------------------------------------------------------- lifecycle
+    def close(self):
+        if self.ctx:
+            self.lib.axonn_free(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc, what):
+        if rc != 0:
+            msg = self.lib.axonn_last_error(self.ctx)
+            raise AxoNNError(rc, f"{what}: {msg.decode() if msg else ''}")
+
+    # ------------------------------------------------------------- hot path
+    def run_batch(self, tokens: np.ndarray) -> float:
+        """tokens: int32 [batch, seq_len + 1], the full batch (Alg. 1 l.4)."""
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        assert tok.ndim == 2 and tok.shape[1] == self.seq_len + 1
+        loss = C.c_float()
+        self._check(self.lib.axonn_run_batch(self.ctx, tok.ctypes.data_as(C.c_void_p),
+                                             tok.shape[0], C.byref(loss)), "run_batch")
+        return loss.value
+
+    def run_batch_device(self, d_tokens_ptr: int, batch: int) -> float:
+        """This replica's shard [batch/G_data, seq_len + 1] already on the device."""
+        loss = C.c_float()
+        self._check(self.lib.axonn_run_batch_device(self.ctx, C.c_void_p(d_tokens_ptr), batch,
+                                                    C.byref(loss)), "run_batch_device")
+        return loss.value
+
+    def optimizer_step(self):
+        self._check(self.lib.axonn_optimizer_step(self.ctx), "optimizer_step")
+
+    # ------------------------------------------------------------- inspection
+    def tensors(self):
+        if self._tensors is None:
+            out = []
+            name = C.create_string_buffer(64)
+            shape = (C.c_int64 * 2)()
+            numel = C.c_int64()
+            for i in range(self.lib.axonn_num_tensors(self.ctx)):
+                self._check(self.lib.axonn_tensor_info(self.ctx, i, name, shape, C.byref(numel)),
+                            "tensor_info")
+                rows, cols = shape[0], shape[1]
+                shp = (cols,) if rows == 1 else (rows, cols)
+                out.append((name.value.decode(), shp, numel.value))
+            self._tensors = out
+        return self._tensors
+
+    def read(self, which: int, idx: int) -> np.ndarray:
+        name, shp, n = self.tensors()[idx]
+        buf = np.empty(n, dtype=np.float32)
+        self._check(self.lib.axonn_read_tensor(self.ctx, which, idx, buf.ctypes.data_as(C.c_void_p)),
+                    f"read {name}")
+        return buf.reshape(shp)
+
+    def write(self, which: int, idx: int, values) -> None:
+        name, shp, n = self.tensors()[idx]
+        buf = np.ascontiguousarray(values, dtype=np.float32).reshape(-1)
+        assert buf.size == n, (name, buf.size, n)
+        self._check(self.lib.axonn_write_tensor(self.ctx, which, idx, buf.ctypes.data_as(C.c_void_p)),
+                    f"write {name}")
+
+    def read_all(self, which: int) -> dict:
+        return {name: self.read(which, i) for i, (name, _, _) in enumerate(self.tensors())}
+
+    def write_all(self, which: int, values: dict) -> None:
+        for i, (name, _, _) in enumerate(self.tensors()):
+            self.write(which, i, values[name])
+
+    def timer_mark(self, i: int):
+        self._check(self.lib.axonn_timer_mark(self.ctx, i), "timer_mark")
+
+    def timer_elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_double()
+        self._check(self.lib.axonn_timer_elapsed(self.ctx, a, b, C.byref(ms)), "timer_elapsed")
+        return ms.value
+
+    def set_profiling(self, on: bool):
+        self._check(self.lib.axonn_set_profiling(self.ctx, int(on)), "set_profiling")
+
+    def stats(self) -> dict:
+        buf = (C.c_double * len(STAT_NAMES))()
+        self._check(self.lib.axonn_stats(self.ctx, buf, len(STAT_NAMES)), "stats")
+        return dict(zip(STAT_NAMES, list(buf)))

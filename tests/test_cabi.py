@@ -1,0 +1,59 @@
+"""The C-ABI library loads and exports every symbol include/axonn.h declares
+(no compute calls: runs on CPU-only hosts), and the Python binding fails
+loudly instead of falling back when a call cannot run."""
+import ctypes as C
+import re
+import subprocess
+
+import pytest
+
+
+def test_library_builds_and_exports_all_symbols():
+    from paper_2110_13005_b200 import _lib, build
+    path = build.build()
+    lib = C.CDLL(path)
+    names = _lib.exported_symbols()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    # nothing else leaks from the shared object (hidden visibility)
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (axonn_\w+)", out))
+    assert exported == set(names), exported ^ set(names)
+
+
+def test_header_declares_paper_boundary():
+    from paper_2110_13005_b200 import _lib
+    names = set(_lib.exported_symbols())
+    for n in ("axonn_init", "axonn_run_batch", "axonn_optimizer_step", "axonn_free"):
+        assert n in names
+
+
+def test_init_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2110_13005_b200.engine import AxoNN, AxoNNError
+    with pytest.raises(AxoNNError) as e:
+        AxoNN(1, 1, 1, n_layers=1, hidden=64, heads=2, seq_len=32, vocab=256)
+    assert e.value.status == "CUDA"
+
+
+def test_init_validation_errors_before_device():
+    """Argument validation happens before any device work."""
+    from paper_2110_13005_b200.engine import AxoNN, AxoNNError
+    cases = [
+        (dict(g_inter=2, g_data=1), dict(), "GRID_MISMATCH"),
+        (dict(g_inter=1, g_data=1), dict(hidden=60), "INVALID_ARG"),
+        (dict(g_inter=1, g_data=1), dict(heads=3), "INVALID_ARG"),
+    ]
+    for grid, over, status in cases:
+        cfg = dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256)
+        cfg.update(over)
+        with pytest.raises(AxoNNError) as e:
+            AxoNN(grid["g_inter"], grid["g_data"], 1, **cfg)
+        assert e.value.status == status
+    with pytest.raises(AxoNNError) as e:
+        AxoNN(2, 1, 1, n_layers=3, hidden=64, heads=2, seq_len=32, vocab=256, world_size=2,
+              nccl_id=b"x" * 128)
+    assert e.value.status == "NONDIVISIBLE_LAYERS"
