@@ -118,36 +118,43 @@ class ClockSampler:
 
 def cpu_oracle_sample(cfg, steps: int = 1):
     """Time the oracle (as it stands) on a bounded sample of the same workload:
-    a 2-layer slice of the configured shape (full per-layer width, LM head
-    included) on one 512-token sequence, fp64 numpy on the host cores."""
+    one transformer layer of the configured shape as a middle pipeline stage
+    (nn_shard.Forward + Backward, no embedding / head) on one full-length
+    sequence, fp64 numpy on the host cores.  Unit: model TFLOP/s of that layer
+    (72 s h^2 (1 + s/6h) per sequence)."""
     from oracle import model as om
-    from synth import init_params, uniform_tokens
-    l = 2
-    c = om.GPTConfig(n_layers=l, hidden=cfg["hidden"], heads=cfg["heads"], seq_len=cfg["seq_len"],
+    from synth import init_params
+    c = om.GPTConfig(n_layers=3, hidden=cfg["hidden"], heads=cfg["heads"], seq_len=cfg["seq_len"],
                      vocab=cfg["vocab"])
-    p = {k: v.astype(np.float64) for k, v in
-         init_params(l, c.hidden, c.seq_len, c.vocab, seed=5, parity=False).items()}
-    tok = uniform_tokens(1, c.seq_len, c.vocab, seed=1234)
+    names = om.layer_names(1)
+    rng = np.random.default_rng(5)
+    full = init_params(1, c.hidden, c.seq_len, 8, seed=5, parity=False)
+    p = {n.replace("l0.", "l1."): v.astype(np.float64) for n, v in full.items() if n.startswith("l0.")}
+    assert set(p) == set(names)
+    x = rng.standard_normal((1, c.seq_len, c.hidden))
+    dy = rng.standard_normal((1, c.seq_len, c.hidden)) * 1e-3
     t0 = time.perf_counter()
     for _ in range(steps):
-        om.full_batch_loss_and_grads(p, c, tok)
+        out, cache = om.stage_forward(p, c, 1, 3, x)
+        om.stage_backward(p, c, 1, 3, cache, dy)
     dt = (time.perf_counter() - t0) / steps
-    fl = model_flops(1, c.seq_len, l, c.hidden, c.vocab)
+    fl = 72 * c.seq_len * c.hidden ** 2 + 12 * c.seq_len ** 2 * c.hidden
     return dict(value=fl / dt / 1e12, unit="model TFLOP/s", cores=os.cpu_count(), kind="oracle",
-                sample=f"numpy fp64 oracle fwd+bwd of a {l}-layer slice (h {c.hidden}, a {c.heads}, "
-                       f"s {c.seq_len}, V {c.vocab}), 1 x {c.seq_len} tokens, {dt:.2f} s/step")
+                sample=f"numpy fp64 oracle nn_shard Forward+Backward of one layer (h {c.hidden}, "
+                       f"a {c.heads}, s {c.seq_len}) on 1 x {c.seq_len} tokens, {dt:.2f} s/step")
 
 
 def run_reference(args, cfg, rank, world):
     """--impl reference: the oracle (this tier's reference arm) on the host."""
     if rank != 0:
         return
-    steps_total = args.warmup + args.steps
-    for _ in range(args.warmup):
+    # bounded: one warm-up sample and at most 4 timed samples (a few minutes on 16 cores)
+    steps_total = min(args.warmup, 1) + min(args.steps, 4)
+    if args.warmup:
         cpu_oracle_sample(cfg, 1)
-    res = cpu_oracle_sample(cfg, args.steps)
+    res = cpu_oracle_sample(cfg, min(args.steps, 4))
     v = res["value"]
-    sample_flops = model_flops(1, cfg["seq_len"], 2, cfg["hidden"], cfg["vocab"])
+    sample_flops = 72 * cfg["seq_len"] * cfg["hidden"] ** 2 + 12 * cfg["seq_len"] ** 2 * cfg["hidden"]
     ms = sample_flops / (v * 1e12) * 1e3
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "model TFLOP/s (all GPUs)",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -171,8 +178,11 @@ def main():
     ap.add_argument("--config", default="gpt1.3b", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--layers", type=int, default=None, help="override n_layers (profiling runs only)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
+    if args.layers:
+        cfg["n_layers"] = args.layers
 
     from paper_2110_13005_b200 import dist as D
     rank, world, local = D.env_rank_world()

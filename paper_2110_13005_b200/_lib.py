@@ -25,7 +25,7 @@ class GemmArgs(C.Structure):
                 ("col_group_in", C.c_int), ("col_group_out", C.c_int), ("n_valid", C.c_int),
                 ("bias", C.c_void_p), ("resid", C.c_void_p), ("ld_resid", C.c_int64),
                 ("aux", C.c_void_p), ("ld_aux", C.c_int64),
-                ("alpha", C.c_float), ("max_ctas", C.c_int)]
+                ("alpha", C.c_float), ("max_ctas", C.c_int), ("variant", C.c_int)]
 
 
 class ModelCfg(C.Structure):

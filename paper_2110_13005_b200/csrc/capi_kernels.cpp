@@ -16,6 +16,7 @@ extern "C" int axonn_k_gemm(const axonn_gemm_args* a, void* stream) {
   g.col_group_in = a->col_group_in; g.col_group_out = a->col_group_out; g.n_valid = a->n_valid;
   g.bias = a->bias; g.resid = a->resid; g.ld_resid = a->ld_resid;
   g.aux = a->aux; g.ld_aux = a->ld_aux; g.alpha = a->alpha; g.max_ctas = a->max_ctas;
+  g.variant = a->variant;
   return axonn::gemm_launch(g, reinterpret_cast<cudaStream_t>(stream));
 }
 

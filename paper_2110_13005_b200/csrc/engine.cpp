@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <new>
@@ -163,7 +164,9 @@ static int plan_memory(Ctx* c) {
     for (int li = 0; li < c->nl; ++li) {
       LayerStash& st = sl.L[li];
       st.u = c->dalloc(Mh * 2);
-      st.qkv = c->dalloc(3 * Mh * 2);
+      st.qkv = c->dalloc((size_t)c->M * c->lq * 2);
+      if (st.qkv && c->dp != c->d && cudaMemset(st.qkv, 0, (size_t)c->M * c->lq * 2) != cudaSuccess)
+        return c->fail(AXONN_ERR_CUDA, "memset qkv padding");
       st.P = c->dalloc(att * 2);
       st.o = c->dalloc(Mh * 2);
       st.x1 = c->dalloc(Mh * 2);
@@ -194,7 +197,9 @@ static int plan_memory(Ctx* c) {
   c->dh1 = c->dalloc(Mh * 2);
   c->dqkv = c->dalloc(3 * Mh * 2);
   c->dpre = c->dalloc(4 * Mh * 2);
-  c->dO = c->dalloc(Mh * 2);
+  c->dO = c->dalloc((size_t)c->M * c->heads * c->dp * 2);
+  if (c->dO && cudaMemset(c->dO, 0, (size_t)c->M * c->heads * c->dp * 2) != cudaSuccess)
+    return c->fail(AXONN_ERR_CUDA, "memset dO");
   c->du = c->dalloc(Mh * 2);
   c->dx1 = c->dalloc(Mh * 2);
   c->cs_ws = (float*)c->dalloc((size_t)2 * colsum_chunks(c->M) * 4 * c->h * 4);
@@ -271,7 +276,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
       model->vocab % 8)
     return AXONN_ERR_INVALID_ARG;
   const int d = model->hidden / model->heads;
-  if (d % 8) return AXONN_ERR_INVALID_ARG;   // TMA head stride (padded heads: next step)
+  if (d < 2) return AXONN_ERR_INVALID_ARG;
   if (!(opt->lr >= 0) || !(opt->beta1 >= 0 && opt->beta1 < 1) || !(opt->beta2 >= 0 && opt->beta2 < 1) ||
       !(opt->eps > 0) || !(opt->loss_scale > 0) || opt->bucket_elems < 1 || opt->coarsen_k < 1 ||
       opt->pipeline_limit < 0)
@@ -292,6 +297,8 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   c->layer0 = c->stage * c->nl;
   c->h = model->hidden; c->heads = model->heads; c->d = d; c->s = model->seq_len;
   c->V = model->vocab; c->M = microbatch * model->seq_len;
+  c->dp = (d + 7) / 8 * 8;            // e.g. 12B: d = 188 -> 192 (D-7: scale stays 1/sqrt(188))
+  c->lq = 3LL * c->heads * c->dp;
   c->limit = g_inter == 1 ? 1 : (opt->pipeline_limit > 0 ? opt->pipeline_limit : g_inter);
 
   auto bail = [&](int rc) {
@@ -352,6 +359,29 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
         } else {
           if (right) c->grad_in = nc; else c->grad_out = nc;
         }
+      }
+    }
+  }
+  // NCCL connects P2P peers lazily and the first call on a link blocks on the host until
+  // the peer also reaches it; in Alg. 2 the peer only does so after a message arrives, so
+  // connect every link now, in ascending boundary order (no cycle: rank i finishes
+  // boundary i-1 before boundary i).
+  if (world > 1 && g_inter > 1) {
+    void* tmp = c->dalloc(256);
+    if (!tmp) return bail(c->fail(AXONN_ERR_OOM, "link warm-up buffer"));
+    for (int k = 0; k < g_inter - 1; ++k) {
+      if (k == c->stage - 1) {   // boundary (i-1, i): receive activation, send gradient
+        if ((rc = c->check_nccl(ncclRecv(tmp, 8, ncclBfloat16, 0, c->act_in, c->s_comp), "warm recv")) ||
+            (rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "warm sync")) ||
+            (rc = c->check_nccl(ncclSend(tmp, 8, ncclBfloat16, 0, c->grad_out, c->s_comp), "warm send")) ||
+            (rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "warm sync")))
+          return bail(rc);
+      } else if (k == c->stage) {   // boundary (i, i+1): send activation, receive gradient
+        if ((rc = c->check_nccl(ncclSend(tmp, 8, ncclBfloat16, 1, c->act_out, c->s_comp), "warm send")) ||
+            (rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "warm sync")) ||
+            (rc = c->check_nccl(ncclRecv(tmp, 8, ncclBfloat16, 1, c->grad_in, c->s_comp), "warm recv")) ||
+            (rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "warm sync")))
+          return bail(rc);
       }
     }
   }
@@ -644,7 +674,8 @@ static int run_pipeline(Ctx* c, int m) {
     }
   }
   auto t_last = std::chrono::steady_clock::now();
-  const double watchdog_s = 600.0;
+  const char* wd_env = getenv("AXONN_WATCHDOG_S");   // no message progress -> AXONN_ERR_TIMEOUT
+  const double watchdog_s = wd_env ? atof(wd_env) : 600.0;
   int fwd_done = c->first ? popped : 0;
   while (true) {
     bool need_act = !c->first && next_act < m;

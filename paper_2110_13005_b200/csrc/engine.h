@@ -57,6 +57,8 @@ struct Ctx {
   bool first = true, last = true;
   int nl = 0, layer0 = 0;             // local layers, first global layer id
   int h = 0, heads = 0, d = 0, s = 0, V = 0, M = 0;   // M = microbatch * seq tokens
+  int dp = 0;                         // head dim padded to a multiple of 8 (16-B TMA strides)
+  long long lq = 0;                   // row stride of the packed qkv buffer = 3 * heads * dp
   int limit = 1;
   std::string err;
   bool sticky = false;

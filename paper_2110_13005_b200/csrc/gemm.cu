@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "ptx.cuh"
@@ -42,6 +43,7 @@ struct GemmParams {
   int num_m, num_n, total;
 };
 
+template <int TBM = BM>
 __device__ __forceinline__ bool tile_coords(const GemmParams& p, int BN, int t, int& z, int& m0,
                                             int& n0, int& kb0, int& kb1) {
   int per = p.num_m * p.num_n;
@@ -49,11 +51,11 @@ __device__ __forceinline__ bool tile_coords(const GemmParams& p, int BN, int t, 
   int r = t - z * per;
   int nb = r / p.num_m;
   int mb = r - nb * p.num_m;
-  m0 = mb * BM;
+  m0 = mb * TBM;
   n0 = nb * BN;
   int lo = 0, hi = p.K;
-  if (p.causal == 1 && n0 > m0 + BM - 1) return false;   // scores tile above the diagonal
-  if (p.causal == 2) hi = min(p.K, m0 + BM);             // keys <= last query of the tile
+  if (p.causal == 1 && n0 > m0 + TBM - 1) return false;  // scores tile above the diagonal
+  if (p.causal == 2) hi = min(p.K, m0 + TBM);            // keys <= last query of the tile
   if (p.causal == 3) lo = m0;                            // queries >= first key of the tile
   kb0 = lo / BK;
   kb1 = (hi + BK - 1) / BK;
@@ -289,6 +291,154 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair version
+// cta_group::2: a cluster of 2 CTAs (one TPC) computes a 256 x 256 tile.  Each CTA
+// stages its 128 rows of A and its 128 rows (N/2) of B; the leader's single thread
+// issues M=256 N=256 K=16 MMAs reading both CTAs' shared memory, accumulating
+// 128 lanes x 256 fp32 columns in each CTA's TMEM (double-buffered: 512 columns).
+// Per-SM smem traffic per MMA is half the 1-CTA 128x256 tile's.
+constexpr int STAGES2 = 6;
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap mapA,
+                           const __grid_constant__ CUtensorMap mapB, const GemmParams p) {
+  constexpr int TBM = 2 * BM;                 // 256 rows per pair
+  constexpr int A_BYTES = BM * BK * 2;        // this CTA's 128 rows
+  constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's BN/2 rows
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE_BYTES);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tfull = empty + STAGES2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapA);
+    tma_prefetch_desc(&mapB);
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<TMEM_COLS>(tmem_holder);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < p.total; t += npairs) {
+        int z, m0, n0, kb0, kb1;
+        if (!tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+        const int z1 = z % p.Z1, z2 = z / p.Z1;
+        const int am = m0 + (int)rank * BM;
+        const int bn = n0 + (int)rank * (BN / 2);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          uint8_t* sA = smem + stage * STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          const int k0 = kb * BK;
+          if (!p.a_mn) {
+            tma_load_4d_pair(sA, &mapA, &full[stage], k0, am, z1, z2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_4d_pair(sA + j * 8192, &mapA, &full[stage], am + 64 * j, k0, z1, z2);
+          }
+          if (!p.b_mn) {
+            tma_load_4d_pair(sB, &mapB, &full[stage], k0, bn, z1, z2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 128; ++j)
+              tma_load_4d_pair(sB + j * 8192, &mapB, &full[stage], bn + 64 * j, k0, z1, z2);
+          }
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(TBM, BN, p.a_mn, p.b_mn);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < p.total; t += npairs) {
+        int z, m0, n0, kb0, kb1;
+        if (!tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t b_base = a_base + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad = p.a_mn ? umma_desc_sw128(a_base + k * 2048, 8192, 1024)
+                                 : umma_desc_sw128(a_base + k * 32, 16, 1024);
+            uint64_t bd = p.b_mn ? umma_desc_sw128(b_base + k * 2048, 8192, 1024)
+                                 : umma_desc_sw128(b_base + k * 32, 16, 1024);
+            mma_bf16_ss_pair(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit_pair(&empty[stage]);
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_pair(&tfull[acc]);
+        ++it;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    int it = 0;
+    for (int t = pair; t < p.total; t += npairs) {
+      int z, m0, n0, kb0, kb1;
+      if (!tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + (int)rank * BM + q * 32 + lane;
+      for (int c = 0; c < BN; c += 32) {
+        if (n0 + c >= p.N) break;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c, r);
+        epilogue_chunk(p, z, row, n0 + c, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      ++it;
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                       const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -330,30 +480,7 @@ static int make_map(CUtensorMap* map, const void* base, long long inner, long lo
 
 static int g_num_sms = 0;
 
-template <int BN>
-static int launch_bn(const GemmArgs& g, cudaStream_t st) {
-  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM) != cudaSuccess)
-      return -10;
-    attr_set = true;
-  }
-  CUtensorMap ma, mb;
-  int Z2 = g.Z / g.Z1;
-  int rc;
-  if (!g.a_mn)
-    rc = make_map(&ma, g.A, g.K, g.M, g.lda, g.Z1, g.a_s1, Z2, g.a_s2, BM);
-  else
-    rc = make_map(&ma, g.A, g.M, g.K, g.lda, g.Z1, g.a_s1, Z2, g.a_s2, 64);
-  if (rc) return rc;
-  if (!g.b_mn)
-    rc = make_map(&mb, g.B, g.K, g.N, g.ldb, g.Z1, g.b_s1, Z2, g.b_s2, BN);
-  else
-    rc = make_map(&mb, g.B, g.N, g.K, g.ldb, g.Z1, g.b_s1, Z2, g.b_s2, 64);
-  if (rc) return rc;
-  GemmParams p;
+static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
   memset(&p, 0, sizeof(p));
   p.M = g.M; p.N = g.N; p.K = g.K; p.Z = g.Z; p.Z1 = g.Z1;
   p.a_mn = g.a_mn; p.b_mn = g.b_mn; p.causal = g.causal; p.epi = g.epi;
@@ -367,24 +494,86 @@ static int launch_bn(const GemmArgs& g, cudaStream_t st) {
   p.aux = reinterpret_cast<__nv_bfloat16*>(g.aux);
   p.ld_aux = g.ld_aux;
   p.alpha = g.alpha;
-  p.num_m = (g.M + BM - 1) / BM;
-  p.num_n = (g.N + BN - 1) / BN;
+  p.num_m = (g.M + tbm - 1) / tbm;
+  p.num_n = (g.N + bn - 1) / bn;
   p.total = p.num_m * p.num_n * g.Z;
   if (g_num_sms == 0) {
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
+}
+
+// A box rows a_rows (K-major) / B box rows b_rows (K-major); MN-major boxes are 64 x 64.
+static int make_maps(CUtensorMap& ma, CUtensorMap& mb, const GemmArgs& g, int a_rows, int b_rows) {
+  int Z2 = g.Z / g.Z1;
+  int rc;
+  if (!g.a_mn)
+    rc = make_map(&ma, g.A, g.K, g.M, g.lda, g.Z1, g.a_s1, Z2, g.a_s2, a_rows);
+  else
+    rc = make_map(&ma, g.A, g.M, g.K, g.lda, g.Z1, g.a_s1, Z2, g.a_s2, 64);
+  if (rc) return rc;
+  if (!g.b_mn)
+    rc = make_map(&mb, g.B, g.K, g.N, g.ldb, g.Z1, g.b_s1, Z2, g.b_s2, b_rows);
+  else
+    rc = make_map(&mb, g.B, g.N, g.K, g.ldb, g.Z1, g.b_s1, Z2, g.b_s2, 64);
+  return rc;
+}
+
+template <int BN>
+static int launch_bn(const GemmArgs& g, cudaStream_t st) {
+  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM) != cudaSuccess)
+      return -10;
+    attr_set = true;
+  }
+  CUtensorMap ma, mb;
+  int rc = make_maps(ma, mb, g, BM, BN);
+  if (rc) return rc;
+  GemmParams p;
+  fill_params(p, g, BM, BN);
   int grid = p.total < g_num_sms ? p.total : g_num_sms;
   if (g.max_ctas > 0 && grid > g.max_ctas) grid = g.max_ctas;
   gemm_bf16_tcgen05<BN><<<grid, 192, SMEM, st>>>(ma, mb, p);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
+template <int BN>
+static int launch_pair(const GemmArgs& g, cudaStream_t st) {
+  constexpr int SMEM = STAGES2 * (BM * BK * 2 + (BN / 2) * BK * 2) + 1024 + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+      return -10;
+    attr_set = true;
+  }
+  CUtensorMap ma, mb;
+  int rc = make_maps(ma, mb, g, BM, BN / 2);
+  if (rc) return rc;
+  GemmParams p;
+  fill_params(p, g, 2 * BM, BN);
+  int pairs_avail = g_num_sms / 2;
+  if (g.max_ctas > 0 && pairs_avail > g.max_ctas / 2) pairs_avail = g.max_ctas / 2;
+  int pairs = p.total < pairs_avail ? p.total : pairs_avail;
+  gemm_bf16_tcgen05_pair<BN><<<2 * pairs, 192, SMEM, st>>>(ma, mb, p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+static int g_pair_mode = -1;   // AXONN_GEMM_PAIR=0 disables the CTA-pair kernel
+
 int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.Z <= 0 || g.Z1 <= 0 || g.Z % g.Z1) return -1;
-  if (g.N <= 128) return launch_bn<128>(g, st);
-  return launch_bn<256>(g, st);
+  if (g_pair_mode < 0) {
+    const char* e = getenv("AXONN_GEMM_PAIR");
+    g_pair_mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (g.variant == 1 || (g.variant == 0 && (g.N <= 128 || !g_pair_mode || g.M <= 128)))
+    return g.N <= 128 ? launch_bn<128>(g, st) : launch_bn<256>(g, st);
+  return launch_pair<256>(g, st);
 }
 
 }  // namespace axonn

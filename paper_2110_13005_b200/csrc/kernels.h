@@ -27,6 +27,7 @@ struct GemmArgs {
   long long ld_aux;
   float alpha;
   int max_ctas;
+  int variant;          // 0 auto, 1 single CTA, 2 CTA pair
 };
 
 int gemm_launch(const GemmArgs& g, cudaStream_t st);

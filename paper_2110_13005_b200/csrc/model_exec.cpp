@@ -96,15 +96,17 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
   {
     GemmArgs g = lin_fwd(st.u, p16(o.w_qkv), M, 3 * h, h, st.qkv);
     g.bias = p16(o.b_qkv);
+    g.ldc = lq;   // packed [M, 3, heads, dp]: heads padded to dp (TMA strides, D-7)
+    if (dp != d) { g.col_group_in = d; g.col_group_out = dp; }
     TRY(gemm(g, 2 * dM * 3 * dh * dh));
   }
   {  // S = Q K^T / sqrt(d) per (sample, head), causal tile skipping (D-7, D-8)
     GemmArgs g;
     memset(&g, 0, sizeof(g));
-    g.M = s; g.N = s; g.K = d; g.Z = b * heads; g.Z1 = heads;
-    g.A = st.qkv; g.lda = 3 * h; g.a_s1 = d; g.a_s2 = (long long)s * 3 * h;
-    g.B = static_cast<char*>(st.qkv) + (size_t)h * 2; g.ldb = 3 * h; g.b_s1 = d;
-    g.b_s2 = (long long)s * 3 * h;
+    g.M = s; g.N = s; g.K = dp; g.Z = b * heads; g.Z1 = heads;
+    g.A = st.qkv; g.lda = lq; g.a_s1 = dp; g.a_s2 = (long long)s * lq;
+    g.B = static_cast<char*>(st.qkv) + (size_t)heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
+    g.b_s2 = (long long)s * lq;
     g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
     g.epi = EPI_F32; g.causal = 1; g.alpha = 1.0f / sqrtf((float)d);
     TRY(gemm(g, -1));
@@ -113,10 +115,10 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
   {  // o = P V, heads merged into [M, h]
     GemmArgs g;
     memset(&g, 0, sizeof(g));
-    g.M = s; g.N = d; g.K = s; g.Z = b * heads; g.Z1 = heads;
+    g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
     g.A = st.P; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s;
-    g.B = static_cast<char*>(st.qkv) + (size_t)2 * h * 2; g.ldb = 3 * h; g.b_s1 = d;
-    g.b_s2 = (long long)s * 3 * h; g.b_mn = 1;
+    g.B = static_cast<char*>(st.qkv) + (size_t)2 * heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
+    g.b_s2 = (long long)s * lq; g.b_mn = 1;
     g.C = st.o; g.ldc = h; g.c_s1 = d; g.c_s2 = (long long)s * h;
     g.epi = EPI_BF16; g.causal = 2;
     TRY(gemm(g, -1));
@@ -164,17 +166,22 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   KCHK(ln_bwd(du, st.x1, st.mean2, st.rstd2, M, h, p16(o.ln2_g), dout, dx1, s_comp));
   KCHK(colsum(du, st.x1, st.mean2, st.rstd2, M, h, cs_ws, g32(o.ln2_b), g32(o.ln2_g), acc, s_comp));
   // proj: dO = dx1 Wo;  dWo += dx1^T o;  dbo += colsum(dx1)
-  TRY(gemm(lin_dgrad(dx1, p16(o.w_o), M, h, h, dO), 2 * dM * dh * dh));
+  {
+    GemmArgs g = lin_dgrad(dx1, p16(o.w_o), M, h, h, dO);
+    g.ldc = (long long)heads * dp;   // dO per head, padded like q/k/v
+    if (dp != d) { g.col_group_in = d; g.col_group_out = dp; }
+    TRY(gemm(g, 2 * dM * dh * dh));
+  }
   TRY(gemm(lin_wgrad(dx1, st.o, M, h, h, g32(o.w_o), acc), 2 * dM * dh * dh));
   KCHK(colsum(dx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, s_comp));
   // attention backward
   {  // dP = dO V^T (fp32 into S)
     GemmArgs g;
     memset(&g, 0, sizeof(g));
-    g.M = s; g.N = s; g.K = d; g.Z = b * heads; g.Z1 = heads;
-    g.A = dO; g.lda = h; g.a_s1 = d; g.a_s2 = (long long)s * h;
-    g.B = static_cast<char*>(st.qkv) + (size_t)2 * h * 2; g.ldb = 3 * h; g.b_s1 = d;
-    g.b_s2 = (long long)s * 3 * h;
+    g.M = s; g.N = s; g.K = dp; g.Z = b * heads; g.Z1 = heads;
+    g.A = dO; g.lda = (long long)heads * dp; g.a_s1 = dp; g.a_s2 = (long long)s * heads * dp;
+    g.B = static_cast<char*>(st.qkv) + (size_t)2 * heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
+    g.b_s2 = (long long)s * lq;
     g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
     g.epi = EPI_F32; g.causal = 1;
     TRY(gemm(g, -1));
@@ -183,10 +190,10 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   {  // dQ = dS K  -> dqkv[:, 0:h]
     GemmArgs g;
     memset(&g, 0, sizeof(g));
-    g.M = s; g.N = d; g.K = s; g.Z = b * heads; g.Z1 = heads;
+    g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
     g.A = dS; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s;
-    g.B = static_cast<char*>(st.qkv) + (size_t)h * 2; g.ldb = 3 * h; g.b_s1 = d;
-    g.b_s2 = (long long)s * 3 * h; g.b_mn = 1;
+    g.B = static_cast<char*>(st.qkv) + (size_t)heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
+    g.b_s2 = (long long)s * lq; g.b_mn = 1;
     g.C = dqkv; g.ldc = 3 * h; g.c_s1 = d; g.c_s2 = (long long)s * 3 * h;
     g.epi = EPI_BF16; g.causal = 2;
     TRY(gemm(g, -1));
@@ -194,9 +201,9 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   {  // dK = dS^T Q -> dqkv[:, h:2h]
     GemmArgs g;
     memset(&g, 0, sizeof(g));
-    g.M = s; g.N = d; g.K = s; g.Z = b * heads; g.Z1 = heads;
+    g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
     g.A = dS; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s; g.a_mn = 1;
-    g.B = st.qkv; g.ldb = 3 * h; g.b_s1 = d; g.b_s2 = (long long)s * 3 * h; g.b_mn = 1;
+    g.B = st.qkv; g.ldb = lq; g.b_s1 = dp; g.b_s2 = (long long)s * lq; g.b_mn = 1;
     g.C = static_cast<char*>(dqkv) + (size_t)h * 2; g.ldc = 3 * h; g.c_s1 = d;
     g.c_s2 = (long long)s * 3 * h;
     g.epi = EPI_BF16; g.causal = 3;
@@ -205,9 +212,10 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   {  // dV = P^T dO -> dqkv[:, 2h:3h]
     GemmArgs g;
     memset(&g, 0, sizeof(g));
-    g.M = s; g.N = d; g.K = s; g.Z = b * heads; g.Z1 = heads;
+    g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
     g.A = st.P; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s; g.a_mn = 1;
-    g.B = dO; g.ldb = h; g.b_s1 = d; g.b_s2 = (long long)s * h; g.b_mn = 1;
+    g.B = dO; g.ldb = (long long)heads * dp; g.b_s1 = dp; g.b_s2 = (long long)s * heads * dp;
+    g.b_mn = 1;
     g.C = static_cast<char*>(dqkv) + (size_t)2 * h * 2; g.ldc = 3 * h; g.c_s1 = d;
     g.c_s2 = (long long)s * 3 * h;
     g.epi = EPI_BF16; g.causal = 3;

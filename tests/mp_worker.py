@@ -1,0 +1,62 @@
+"""Worker for the multi-GPU parity tests (launched by torchrun, one rank per GPU).
+
+Writes the seeded parity weights of its stage, runs batches through the C-ABI
+and dumps losses / gradients / updated weights to <out>/rank<r>.npz."""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--g-inter", type=int, required=True)
+    ap.add_argument("--g-data", type=int, required=True)
+    ap.add_argument("--mb", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--cfg", default="tiny")
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--offload", type=int, default=0)
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args()
+    import torch
+    from paper_2110_13005_b200 import dist as D
+    from paper_2110_13005_b200.engine import T_GRAD, T_GRAD32, T_MASTER, AxoNN
+    from synth import init_params, markov_tokens
+    cfgs = {"tiny": dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256),
+            "tiny4": dict(n_layers=4, hidden=64, heads=2, seq_len=32, vocab=256),
+            "mini": dict(n_layers=4, hidden=256, heads=4, seq_len=128, vocab=1024)}
+    cfg = cfgs[a.cfg]
+    rank, world, local = D.env_rank_world()
+    torch.cuda.set_device(local)
+    D.init_process_group(rank, world)
+    nid = D.share_unique_id(rank, world, D.nccl_unique_id)
+    eng = AxoNN(a.g_inter, a.g_data, a.mb, **cfg, rank=rank, world_size=world, device=local,
+                nccl_id=nid, offload=bool(a.offload), bucket_elems=5000, coarsen_k=2)
+    params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=42)
+    names = [n for n, _, _ in eng.tensors()]
+    eng.write_all(T_MASTER, {n: params[n] for n in names})
+    out = {}
+    for step in range(a.steps):
+        tok = markov_tokens(a.batch, cfg["seq_len"], cfg["vocab"], seed=7 + step)
+        loss = eng.run_batch(tok)
+        out[f"loss{step}"] = np.array(loss)
+        if step == 0:
+            for n, v in eng.read_all(T_GRAD32).items():
+                out["g32." + n] = v
+            for n, v in eng.read_all(T_GRAD).items():
+                out["g16." + n] = v
+        eng.optimizer_step()
+    for n, v in eng.read_all(T_MASTER).items():
+        out["theta." + n] = v
+    np.savez(os.path.join(a.out, f"rank{rank}.npz"), **out)
+    D.barrier(world)
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -55,9 +55,13 @@ def cos(x, ref):
 RNG = np.random.default_rng(1234)
 
 
+VARIANTS = pytest.mark.parametrize("variant", [1, 2])
+
+
+@VARIANTS
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 200), (1024, 768, 1024),
-                                   (4096, 2048, 2048), (77, 16, 8)])
-def test_gemm_forward_bias_resid(lib, M, N, K):
+                                   (4096, 2048, 2048), (77, 16, 8), (640, 384, 72)])
+def test_gemm_forward_bias_resid(lib, M, N, K, variant):
     t = torch()
     A = dev_bf16(RNG.standard_normal((M, K)))
     B = dev_bf16(RNG.standard_normal((N, K)) * 0.05)
@@ -65,27 +69,32 @@ def test_gemm_forward_bias_resid(lib, M, N, K):
     res = dev_bf16(RNG.standard_normal((M, N)))
     Cd = t.empty((M, N), dtype=t.bfloat16, device="cuda")
     gemm(lib, M=M, N=N, K=K, A=A, lda=K, a_mn=0, B=B, ldb=K, b_mn=0, C=Cd, ldc=N, epi=0,
-         bias=bias, resid=res, ld_resid=N)
+         bias=bias, resid=res, ld_resid=N, variant=variant)
     ref = host(A) @ host(B).T + host(bias) + host(res)
     out = host(Cd)
     assert rel(out, ref) < 1e-2 and cos(out, ref) > 0.9999
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 200, 384), (4096, 2048, 8192), (130, 72, 64)])
-def test_gemm_dgrad_b_mn_major(lib, M, N, K):
+@VARIANTS
+@pytest.mark.parametrize("M,N,K", [(256, 200, 384), (4096, 2048, 8192), (130, 72, 64),
+                                   (520, 328, 136)])
+def test_gemm_dgrad_b_mn_major(lib, M, N, K, variant):
     """dX = dY W: B stored [K][N] (MN-major)."""
     t = torch()
     A = dev_bf16(RNG.standard_normal((M, K)))
     W = dev_bf16(RNG.standard_normal((K, N)) * 0.05)
     Cd = t.empty((M, N), dtype=t.bfloat16, device="cuda")
-    gemm(lib, M=M, N=N, K=K, A=A, lda=K, a_mn=0, B=W, ldb=N, b_mn=1, C=Cd, ldc=N, epi=0)
+    gemm(lib, M=M, N=N, K=K, A=A, lda=K, a_mn=0, B=W, ldb=N, b_mn=1, C=Cd, ldc=N, epi=0,
+         variant=variant)
     ref = host(A) @ host(W)
     out = host(Cd)
     assert rel(out, ref) < 1e-2 and cos(out, ref) > 0.9999
 
 
-@pytest.mark.parametrize("M,N,K", [(192, 320, 500), (2048, 8192, 4096), (64, 136, 40)])
-def test_gemm_wgrad_both_mn_major_f32_accumulate(lib, M, N, K):
+@VARIANTS
+@pytest.mark.parametrize("M,N,K", [(192, 320, 500), (2048, 8192, 4096), (64, 136, 40),
+                                   (392, 264, 128)])
+def test_gemm_wgrad_both_mn_major_f32_accumulate(lib, M, N, K, variant):
     """dW (+)= dY^T X: A stored [K][M], B stored [K][N]; fp32 output, accumulate."""
     t = torch()
     dY = dev_bf16(RNG.standard_normal((K, M)))
@@ -93,13 +102,14 @@ def test_gemm_wgrad_both_mn_major_f32_accumulate(lib, M, N, K):
     Cd = t.zeros((M, N), dtype=t.float32, device="cuda")
     for acc in (0, 1):
         gemm(lib, M=M, N=N, K=K, A=dY, lda=M, a_mn=1, B=X, ldb=N, b_mn=1, C=Cd, ldc=N, epi=3,
-             accumulate=acc)
+             accumulate=acc, variant=variant)
     ref = 2 * host(dY).T @ host(X)
     out = Cd.cpu().numpy().astype(np.float64)
     assert rel(out, ref) < 1e-5
 
 
-def test_gemm_gelu_and_dgelu(lib):
+@VARIANTS
+def test_gemm_gelu_and_dgelu(lib, variant):
     t = torch()
     M, N, K = 256, 512, 192
     A = dev_bf16(RNG.standard_normal((M, K)))
@@ -108,7 +118,7 @@ def test_gemm_gelu_and_dgelu(lib):
     out = t.empty((M, N), dtype=t.bfloat16, device="cuda")
     pre = t.empty((M, N), dtype=t.bfloat16, device="cuda")
     gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=out, ldc=N, epi=1, bias=bias, aux=pre,
-         ld_aux=N)
+         ld_aux=N, variant=variant)
     pre_ref = host(A) @ host(B).T + host(bias)
     assert rel(host(pre), pre_ref) < 1e-2
     p = host(pre)
@@ -117,14 +127,16 @@ def test_gemm_gelu_and_dgelu(lib):
     assert rel(host(out), gelu) < 1e-2
     # DGELU: out2 = (A B^T) * gelu'(pre)
     out2 = t.empty((M, N), dtype=t.bfloat16, device="cuda")
-    gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=out2, ldc=N, epi=2, aux=pre, ld_aux=N)
+    gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=out2, ldc=N, epi=2, aux=pre, ld_aux=N,
+         variant=variant)
     th = np.tanh(c * (p + 0.044715 * p ** 3))
     dg = 0.5 * (1 + th) + 0.5 * p * (1 - th * th) * c * (1 + 3 * 0.044715 * p * p)
     ref2 = (host(A) @ host(B).T) * dg
     assert rel(host(out2), ref2) < 1e-2
 
 
-def test_gemm_batched_attention_shapes(lib):
+@VARIANTS
+def test_gemm_batched_attention_shapes(lib, variant):
     """S = Q K^T over (sample, head) from the packed [b*s, 3h] QKV layout via
     4-D TMA maps; causal modes 1 (skip upper tiles), 2 (k < m0+128), 3 (k >= m0)."""
     t = torch()
@@ -137,7 +149,7 @@ def test_gemm_batched_attention_shapes(lib):
     gemm(lib, M=s, N=s, K=d, Z=b * a, Z1=a,
          A=qkv, lda=3 * h, a_s1=d, a_s2=s * 3 * h, a_mn=0,
          B=qkv[:, h:], ldb=3 * h, b_s1=d, b_s2=s * 3 * h, b_mn=0,
-         C=S, ldc=s, c_s1=s * s, c_s2=a * s * s, epi=3, causal=1, alpha=0.5)
+         C=S, ldc=s, c_s1=s * s, c_s2=a * s * s, epi=3, causal=1, alpha=0.5, variant=variant)
     ref = 0.5 * Q @ Kt.transpose(0, 1, 3, 2)
     got = S.cpu().numpy()
     low = np.tril(np.ones((s, s), dtype=bool))

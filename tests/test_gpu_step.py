@@ -35,7 +35,12 @@ def oracle_grads(params32, cfg, tokens):
     return model.full_batch_loss_and_grads(p, c, tokens)
 
 
-@pytest.mark.parametrize("cfg,B,mb", [(TINY, 8, 2), (TINY, 8, 8), (MINI, 16, 2)])
+PAD10 = dict(n_layers=2, hidden=80, heads=8, seq_len=32, vocab=256)     # d = 10 -> padded 16
+PAD188 = dict(n_layers=1, hidden=376, heads=2, seq_len=64, vocab=512)   # the 12B head dim d = 188
+
+
+@pytest.mark.parametrize("cfg,B,mb", [(TINY, 8, 2), (TINY, 8, 8), (MINI, 16, 2), (PAD10, 8, 2),
+                                      (PAD188, 4, 2)])
 def test_step_loss_and_grads_vs_oracle(cfg, B, mb):
     from paper_2110_13005_b200.engine import T_GRAD32, T_MASTER
     eng = make(cfg, mb=mb)
