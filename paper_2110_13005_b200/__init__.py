@@ -7,4 +7,14 @@ on CUDA streams and events, NCCL P2P and all-reduce over NVLink, and the
 bucketed pinned-host optimizer.  This package is a thin binding:
 ``_lib`` (ctypes marshalling), ``engine`` (Python wrapper of a context) and
 ``dist`` (torch.distributed bootstrap of the NCCL unique id)."""
-from ._lib import load  # noqa: F401
+import os as _os
+
+# Alg. 2 pre-posts receives (PAPER.md:499-501): a pending ncclRecv kernel spins until its
+# message lands.  With more streams than CUDA hardware work queues (default 8) a later
+# kernel of another stream can be queued behind it and never start.  Give every
+# library stream its own queue; must be set before the process creates its CUDA context.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# libaxonn force-loads its kernels in axonn_init; eager loading also covers torch's.
+_os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
+from ._lib import load  # noqa: E402,F401

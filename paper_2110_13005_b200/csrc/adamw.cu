@@ -99,3 +99,10 @@ int adamw_launch(long long n, const void* g16, float* theta, float* m, float* v,
 }
 
 }  // namespace axonn
+
+namespace axonn {
+int preload_adamw() {   // see preload_ops (ops.cu)
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)adamw_kernel) == cudaSuccess ? 0 : -1;
+}
+}  // namespace axonn

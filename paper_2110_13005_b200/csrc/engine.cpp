@@ -311,6 +311,11 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   if ((rc = c->check_cuda(cudaGetDeviceProperties(&prop, c->device), "props"))) return bail(rc);
   if (prop.major < 10) return bail(c->fail(AXONN_ERR_CUDA, "needs an sm_100a (B200) device"));
   c->num_sms = prop.multiProcessorCount;
+  // CUDA lazy loading would load a kernel's module at its first launch and wait for the
+  // device's running kernels — including a pre-posted ncclRecv spinning until the peer
+  // sends, which the peer only does after our launch: load everything now.
+  if (preload_gemm() || preload_ops() || preload_adamw())
+    return bail(c->fail(AXONN_ERR_CUDA, "kernel preload failed"));
   for (cudaStream_t* st : {&c->s_comp, &c->s_send_act, &c->s_send_grad, &c->s_recv_act,
                            &c->s_recv_grad, &c->s_dp, &c->s_h2d, &c->s_d2h, &c->s_opt})
     if ((rc = c->check_cuda(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking), "stream")))
@@ -696,10 +701,19 @@ static int run_pipeline(Ctx* c, int m) {
       if ((rc = forward_of(mb))) return rc;
       t_last = std::chrono::steady_clock::now();
     } else {
-      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t_last).count() > watchdog_s)
-        return c->fail(AXONN_ERR_TIMEOUT, "Alg. 2 watchdog: no message landed for " +
-                                              std::to_string((int)watchdog_s) + " s (stage " +
-                                              std::to_string(c->stage) + ")");
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t_last).count() > watchdog_s) {
+        auto busy = [](cudaStream_t st) { return cudaStreamQuery(st) == cudaErrorNotReady ? "busy" : "idle"; };
+        char buf[512];
+        snprintf(buf, sizeof(buf),
+                 "Alg. 2 watchdog: no message landed for %d s (stage %d): posted act %d grad %d, "
+                 "consumed act %d grad %d, backwards %d, injected %d; streams comp %s send_act %s "
+                 "send_grad %s recv_act %s recv_grad %s",
+                 (int)watchdog_s, c->stage, next_act_post, next_grad_post, next_act, next_grad,
+                 done_b, popped, busy(c->s_comp), busy(c->s_send_act), busy(c->s_send_grad),
+                 busy(c->s_recv_act), busy(c->s_recv_grad));
+        fprintf(stderr, "[axonn rank %d] %s\n", c->rank, buf);
+        return c->fail(AXONN_ERR_TIMEOUT, buf);
+      }
       std::this_thread::yield();
     }
   }

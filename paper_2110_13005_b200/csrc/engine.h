@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -128,6 +129,14 @@ struct Ctx {
 
   // model execution (model_exec.cpp)
   int gemm(GemmArgs g, double flops);
+  int softmax_mode = -1;              // AXONN_FUSED_SOFTMAX=0 -> separate softmax kernels
+  bool fused_softmax() {
+    if (softmax_mode < 0) {
+      const char* e = getenv("AXONN_FUSED_SOFTMAX");
+      softmax_mode = (e && e[0] == '0') ? 0 : 1;
+    }
+    return softmax_mode && s <= 512 && s % 32 == 0;
+  }
   int forward(Slot& sl, int mb);          // nn_shard.Forward (and the loss on the last stage)
   int backward(Slot& sl, int mb, const void* dout);   // nn_shard.Backward
   int layer_fwd(int li, const void* x, LayerStash& st);

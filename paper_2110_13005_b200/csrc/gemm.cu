@@ -439,6 +439,228 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   }
 }
 
+// ------------------------------------------------------------------ row-softmax variant
+// Attention scores with the causal softmax (or its backward) fused into the epilogue:
+// one tile = 128 query rows x ALL keys (N <= 512: two N=256 MMAs filling the 512 TMEM
+// columns), so every epilogue thread owns a complete score row in TMEM.
+//   EPI_SOFTMAX     : C = P = softmax_k<=q(alpha * Q K^T)        (bf16, zeros for k > q)
+//   EPI_SOFTMAX_BWD : C = dS = alpha * P * (dP - sum_k P dP)     (acc = dP = dO V^T, P = aux)
+// Removes the fp32 score round trip and the separate softmax kernels (D-7, D-8).
+constexpr int RS_STAGES = 2;
+__global__ void __launch_bounds__(192, 1)
+    gemm_rowsoftmax(const __grid_constant__ CUtensorMap mapA,
+                    const __grid_constant__ CUtensorMap mapB, const GemmParams p) {
+  constexpr int A_BYTES = BM * BK * 2;
+  constexpr int HALF_BYTES = 256 * BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + 2 * HALF_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RS_STAGES * STAGE_BYTES);
+  uint64_t* empty = full + RS_STAGES;
+  uint64_t* tfull = empty + RS_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapA);
+    tma_prefetch_desc(&mapB);
+    for (int s = 0; s < RS_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int nkb = (p.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
+        const int z = t / p.num_m, m0 = (t % p.num_m) * BM;
+        const int z1 = z % p.Z1, z2 = z / p.Z1;
+        const int kv = min(p.N, m0 + BM);
+        const int nh = kv > 256 ? 2 : 1;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], A_BYTES + nh * HALF_BYTES);
+          uint8_t* sA = smem + stage * STAGE_BYTES;
+          tma_load_4d(sA, &mapA, &full[stage], kb * BK, m0, z1, z2);
+          for (int hh = 0; hh < nh; ++hh)
+            tma_load_4d(sA + A_BYTES + hh * HALF_BYTES, &mapB, &full[stage], kb * BK, 256 * hh, z1, z2);
+          if (++stage == RS_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(BM, 256, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
+        const int m0 = (t % p.num_m) * BM;
+        const int kv = min(p.N, m0 + BM);
+        const int nh = kv > 256 ? 2 : 1;
+        mbar_wait(tempty, (it & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smem + stage * STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
+            for (int hh = 0; hh < nh; ++hh) {
+              uint64_t bd = umma_desc_sw128(a_base + A_BYTES + hh * HALF_BYTES + k * 32, 16, 1024);
+              mma_bf16_ss(tmem_base + 256 * hh, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == RS_STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(tfull);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    int it = 0;
+    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
+      const int z = t / p.num_m, m0 = (t % p.num_m) * BM;
+      const int z1 = z % p.Z1, z2 = z / p.Z1;
+      const int kv = min(p.N, m0 + BM);
+      const int row = m0 + q * 32 + lane;
+      const bool live = row < p.M;
+      const long long off = z2 * p.c_s2 + z1 * p.c_s1 + (long long)row * p.ldc;
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + off;
+      const __nv_bfloat16* Pin = p.aux + off;
+      mbar_wait(tfull, it & 1);
+      tc_fence_after();
+      uint32_t r[32];
+      if (p.epi == EPI_SOFTMAX) {
+        float mx = -3.0e38f;
+        for (int c0 = 0; c0 < kv; c0 += 32) {
+          tmem_ld32(trow + c0, r);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c0 + i <= row) mx = fmaxf(mx, __uint_as_float(r[i]) * p.alpha);
+        }
+        float sum = 0.f;
+        for (int c0 = 0; c0 < kv; c0 += 32) {
+          tmem_ld32(trow + c0, r);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c0 + i <= row) sum += __expf(__uint_as_float(r[i]) * p.alpha - mx);
+        }
+        const float inv = 1.f / sum;
+        for (int c0 = 0; c0 < p.N; c0 += 32) {
+          float v[32];
+          if (c0 < kv) {
+            tmem_ld32(trow + c0, r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              v[i] = (c0 + i <= row) ? __expf(__uint_as_float(r[i]) * p.alpha - mx) * inv : 0.f;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+          if (live) {
+            uint4* d4 = reinterpret_cast<uint4*>(out + c0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
+              __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
+              __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
+              uint4 o;
+              o.x = *reinterpret_cast<uint32_t*>(&h0);
+              o.y = *reinterpret_cast<uint32_t*>(&h1);
+              o.z = *reinterpret_cast<uint32_t*>(&h2);
+              o.w = *reinterpret_cast<uint32_t*>(&h3);
+              d4[i] = o;
+            }
+          }
+        }
+      } else {   // EPI_SOFTMAX_BWD
+        float dot = 0.f;
+        for (int c0 = 0; c0 < kv; c0 += 32) {
+          tmem_ld32(trow + c0, r);
+          if (live) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              uint4 pv = *reinterpret_cast<const uint4*>(Pin + c0 + i);
+              const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&pv);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                float2 pf = __bfloat1622float2(ph[j]);
+                if (c0 + i + 2 * j <= row) dot += pf.x * __uint_as_float(r[i + 2 * j]);
+                if (c0 + i + 2 * j + 1 <= row) dot += pf.y * __uint_as_float(r[i + 2 * j + 1]);
+              }
+            }
+          }
+        }
+        for (int c0 = 0; c0 < p.N; c0 += 32) {
+          float v[32];
+          if (c0 < kv) {
+            tmem_ld32(trow + c0, r);
+            if (live) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 8) {
+                uint4 pv = *reinterpret_cast<const uint4*>(Pin + c0 + i);
+                const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&pv);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  float2 pf = __bfloat1622float2(ph[j]);
+                  v[i + 2 * j] = (c0 + i + 2 * j <= row)
+                                     ? p.alpha * pf.x * (__uint_as_float(r[i + 2 * j]) - dot) : 0.f;
+                  v[i + 2 * j + 1] = (c0 + i + 2 * j + 1 <= row)
+                                         ? p.alpha * pf.y * (__uint_as_float(r[i + 2 * j + 1]) - dot) : 0.f;
+                }
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+          if (live) {
+            uint4* d4 = reinterpret_cast<uint4*>(out + c0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
+              __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
+              __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
+              uint4 o;
+              o.x = *reinterpret_cast<uint32_t*>(&h0);
+              o.y = *reinterpret_cast<uint32_t*>(&h1);
+              o.z = *reinterpret_cast<uint32_t*>(&h2);
+              o.w = *reinterpret_cast<uint32_t*>(&h3);
+              d4[i] = o;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                       const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -563,6 +785,30 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
+static int launch_rowsoftmax(const GemmArgs& g, cudaStream_t st) {
+  constexpr int SMEM = RS_STAGES * (BM * BK * 2 + 2 * 256 * BK * 2) + 1024 + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_rowsoftmax, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
+        cudaSuccess)
+      return -10;
+    attr_set = true;
+  }
+  if (g.N > 512 || g.N % 32 || g.a_mn || g.b_mn || (g.ldc % 8) || (g.c_s1 % 8) || (g.c_s2 % 8))
+    return -1;
+  CUtensorMap ma, mb;
+  int rc = make_maps(ma, mb, g, BM, 256);
+  if (rc) return rc;
+  GemmParams p;
+  fill_params(p, g, BM, 512);
+  p.num_n = 1;
+  p.total = p.num_m * g.Z;
+  int grid = p.total < g_num_sms ? p.total : g_num_sms;
+  if (g.max_ctas > 0 && grid > g.max_ctas) grid = g.max_ctas;
+  gemm_rowsoftmax<<<grid, 192, SMEM, st>>>(ma, mb, p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
 static int g_pair_mode = -1;   // AXONN_GEMM_PAIR=0 disables the CTA-pair kernel
 
 int gemm_launch(const GemmArgs& g, cudaStream_t st) {
@@ -571,9 +817,21 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
     const char* e = getenv("AXONN_GEMM_PAIR");
     g_pair_mode = (e && e[0] == '0') ? 0 : 1;
   }
+  if (g.epi == EPI_SOFTMAX || g.epi == EPI_SOFTMAX_BWD) return launch_rowsoftmax(g, st);
   if (g.variant == 1 || (g.variant == 0 && (g.N <= 128 || !g_pair_mode || g.M <= 128)))
     return g.N <= 128 ? launch_bn<128>(g, st) : launch_bn<256>(g, st);
   return launch_pair<256>(g, st);
 }
 
+}  // namespace axonn
+
+namespace axonn {
+int preload_gemm() {   // see preload_ops (ops.cu)
+  cudaFuncAttributes a;
+  const void* fns[] = {(const void*)gemm_bf16_tcgen05<128>, (const void*)gemm_bf16_tcgen05<256>,
+                       (const void*)gemm_bf16_tcgen05_pair<256>, (const void*)gemm_rowsoftmax};
+  for (const void* f : fns)
+    if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
+  return 0;
+}
 }  // namespace axonn

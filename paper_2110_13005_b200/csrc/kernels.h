@@ -5,7 +5,11 @@
 
 namespace axonn {
 
-enum Epi { EPI_BF16 = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3 };
+enum Epi {
+  EPI_BF16 = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3,
+  EPI_SOFTMAX = 4,       // causal row softmax of alpha * acc -> bf16 P (N <= 512, full rows per tile)
+  EPI_SOFTMAX_BWD = 5    // dS = alpha * P * (acc - rowsum(P * acc)), P read from aux
+};
 
 struct GemmArgs {
   int M, N, K;          // per-batch GEMM: C[M,N] = A[M,K] * B[N,K]^T
@@ -31,6 +35,9 @@ struct GemmArgs {
 };
 
 int gemm_launch(const GemmArgs& g, cudaStream_t st);
+int preload_gemm();    // force-load kernels (no lazy module load behind a spinning NCCL kernel)
+int preload_ops();
+int preload_adamw();
 int adamw_launch(long long n, const void* g16, float* theta, float* m, float* v, void* theta16,
                  const float* scalars9, cudaStream_t st);
 

@@ -109,9 +109,15 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
     g.b_s2 = (long long)s * lq;
     g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
     g.epi = EPI_F32; g.causal = 1; g.alpha = 1.0f / sqrtf((float)d);
-    TRY(gemm(g, -1));
+    if (fused_softmax()) {   // softmax in the epilogue: P straight from TMEM
+      g.C = st.P;
+      g.epi = EPI_SOFTMAX;
+      TRY(gemm(g, -1));
+    } else {
+      TRY(gemm(g, -1));
+      KCHK(softmax_fwd(S, (long long)b * heads * s, s, st.P, s_comp));
+    }
   }
-  KCHK(softmax_fwd(S, (long long)b * heads * s, s, st.P, s_comp));
   {  // o = P V, heads merged into [M, h]
     GemmArgs g;
     memset(&g, 0, sizeof(g));
@@ -184,9 +190,17 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
     g.b_s2 = (long long)s * lq;
     g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
     g.epi = EPI_F32; g.causal = 1;
-    TRY(gemm(g, -1));
+    if (fused_softmax()) {   // dS = P * (dP - rowsum(P dP)) / sqrt(d) in the epilogue
+      g.C = dS;
+      g.epi = EPI_SOFTMAX_BWD;
+      g.aux = st.P;
+      g.alpha = 1.0f / sqrtf((float)d);
+      TRY(gemm(g, -1));
+    } else {
+      TRY(gemm(g, -1));
+      KCHK(softmax_bwd(st.P, S, (long long)b * heads * s, s, 1.0f / sqrtf((float)d), dS, s_comp));
+    }
   }
-  KCHK(softmax_bwd(st.P, S, (long long)b * heads * s, s, 1.0f / sqrtf((float)d), dS, s_comp));
   {  // dQ = dS K  -> dqkv[:, 0:h]
     GemmArgs g;
     memset(&g, 0, sizeof(g));

@@ -569,3 +569,22 @@ int init_normal(void* out, float* master, long long n, uint64_t seed, float mean
 }
 
 }  // namespace axonn
+
+namespace axonn {
+// Force-load every kernel of this module now (CUDA lazy loading would otherwise load a
+// module at its first launch, which waits for running kernels — e.g. a pre-posted
+// ncclRecv spinning until the peer's message arrives — and deadlocks Alg. 2).
+int preload_ops() {
+  cudaFuncAttributes a;
+  const void* fns[] = {(const void*)embed_fwd_kernel, (const void*)embed_bwd_tok_kernel,
+                       (const void*)embed_bwd_pos_kernel, (const void*)ln_fwd_kernel,
+                       (const void*)ln_bwd_kernel, (const void*)colsum_partial_kernel,
+                       (const void*)colsum_final_kernel, (const void*)softmax_fwd_kernel,
+                       (const void*)softmax_bwd_kernel, (const void*)xent_kernel,
+                       (const void*)reduce_sum_kernel, (const void*)cast_f32_bf16_kernel,
+                       (const void*)cast_bf16_f32_kernel, (const void*)init_normal_kernel};
+  for (const void* f : fns)
+    if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
+  return 0;
+}
+}  // namespace axonn

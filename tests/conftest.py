@@ -4,6 +4,7 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")   # see paper_2110_13005_b200/__init__.py
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

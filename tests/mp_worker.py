@@ -10,6 +10,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")   # before any CUDA context
 
 
 def main():
@@ -32,6 +33,8 @@ def main():
             "mini": dict(n_layers=4, hidden=256, heads=4, seq_len=128, vocab=1024)}
     cfg = cfgs[a.cfg]
     rank, world, local = D.env_rank_world()
+    if "AXONN_WATCHDOG_S" in os.environ:   # stagger so every rank reports its own state
+        os.environ["AXONN_WATCHDOG_S"] = str(float(os.environ["AXONN_WATCHDOG_S"]) + 15 * rank)
     torch.cuda.set_device(local)
     D.init_process_group(rank, world)
     nid = D.share_unique_id(rank, world, D.nccl_unique_id)

@@ -175,6 +175,48 @@ def test_gemm_batched_attention_shapes(lib, variant):
     assert rel(host(dK), refK) < 1e-2
 
 
+@pytest.mark.parametrize("s,d", [(384, 64), (320, 128), (512, 128), (64, 24)])
+def test_gemm_rowsoftmax_epilogues(lib, s, d):
+    """Epilogue 4: P = causal softmax(alpha Q K^T) straight from a full-row TMEM tile;
+    epilogue 5: dS = alpha P (dP - rowsum(P dP)) with dP = dO V^T (D-7, D-8)."""
+    t = torch()
+    b, a = 2, 3
+    h = a * d
+    alpha = 1.0 / np.sqrt(d)
+    qkv = dev_bf16(RNG.standard_normal((b * s, 3 * h)))
+    Pd = t.full((b, a, s, s), float("nan"), dtype=t.bfloat16, device="cuda")
+    gemm(lib, M=s, N=s, K=d, Z=b * a, Z1=a,
+         A=qkv, lda=3 * h, a_s1=d, a_s2=s * 3 * h,
+         B=qkv[:, h:], ldb=3 * h, b_s1=d, b_s2=s * 3 * h,
+         C=Pd, ldc=s, c_s1=s * s, c_s2=a * s * s, epi=4, causal=1, alpha=alpha)
+    hq = host(qkv)
+    Q = hq[:, :h].reshape(b, s, a, d).transpose(0, 2, 1, 3)
+    K = hq[:, h:2 * h].reshape(b, s, a, d).transpose(0, 2, 1, 3)
+    sc = alpha * Q @ K.transpose(0, 1, 3, 2)
+    mask = np.triu(np.ones((s, s), dtype=bool), 1)
+    sc = np.where(mask, -np.inf, sc)
+    P = np.exp(sc - sc.max(-1, keepdims=True))
+    P /= P.sum(-1, keepdims=True)
+    got = host(Pd)
+    assert np.all(got[..., mask] == 0)
+    assert rel(got, P) < 1e-2
+    # backward: dP = dO V^T with dO random; dS vs reference from the GPU's own P
+    dO = dev_bf16(RNG.standard_normal((b * s, h)))
+    dS = t.full((b, a, s, s), float("nan"), dtype=t.bfloat16, device="cuda")
+    gemm(lib, M=s, N=s, K=d, Z=b * a, Z1=a,
+         A=dO, lda=h, a_s1=d, a_s2=s * h,
+         B=qkv[:, 2 * h:], ldb=3 * h, b_s1=d, b_s2=s * 3 * h,
+         C=dS, ldc=s, c_s1=s * s, c_s2=a * s * s, epi=5, causal=1, alpha=alpha, aux=Pd)
+    V = hq[:, 2 * h:].reshape(b, s, a, d).transpose(0, 2, 1, 3)
+    dOh = host(dO).reshape(b, s, a, d).transpose(0, 2, 1, 3)
+    dPr = dOh @ V.transpose(0, 1, 3, 2)
+    Pg = got
+    ref = alpha * Pg * (dPr - (Pg * dPr).sum(-1, keepdims=True))
+    g2 = host(dS)
+    assert np.all(g2[..., mask] == 0)
+    assert rel(g2, ref) < 2e-2
+
+
 def test_gemm_column_remap_and_nvalid(lib):
     """Columns c -> (c / 5) * 8 + c % 5 (head padding layout); n_valid cut."""
     t = torch()
