@@ -40,6 +40,15 @@ CONFIGS = {
     # small smoke configuration (BASELINE.json configs[0] shape, single stage)
     "tiny": dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256,
                  g_inter=1, microbatch=2, mb_per_replica=4, offload=False),
+    # BASELINE.json configs[2] proxy: the paper's 12B layer shape (Table I),
+    # 12 layers per stage as in the 4 x 2 grid, G_inter = N (pipeline), microbatch 8
+    # (Table II), bucketed CPU-offloaded Adam (bsize 4M, k 4)
+    "gpt12b-pipe": dict(layers_per_stage=12, hidden=4512, heads=24, seq_len=512, vocab=51200,
+                        g_inter="N", microbatch=8, mb_per_replica=16, offload=True),
+    # BASELINE.json configs[3] proxy: the 24B layer shape (d = 176), 6 layers per stage as in
+    # 8 x 1, microbatch 4, offload on
+    "gpt24b-pipe": dict(layers_per_stage=6, hidden=6336, heads=36, seq_len=512, vocab=51200,
+                        g_inter="N", microbatch=4, mb_per_replica=32, offload=True),
 }
 
 
@@ -180,10 +189,19 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--layers", type=int, default=None, help="override n_layers (profiling runs only)")
+    ap.add_argument("--mb-per-replica", type=int, default=None, help="microbatches per replica (m)")
+    ap.add_argument("--offload", type=int, default=None, help="1/0: override the config's offload")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.layers:
         cfg["n_layers"] = args.layers
+    if args.mb_per_replica:
+        cfg["mb_per_replica"] = args.mb_per_replica
+    if args.offload is not None:
+        cfg["offload"] = bool(args.offload)
+    if cfg.get("g_inter") == "N":   # pipeline proxies: one stage per GPU
+        cfg["g_inter"] = int(os.environ.get("WORLD_SIZE", "1"))
+        cfg.setdefault("n_layers", cfg["layers_per_stage"] * cfg["g_inter"])
 
     from paper_2110_13005_b200 import dist as D
     rank, world, local = D.env_rank_world()
@@ -301,7 +319,10 @@ def main():
                          "achieved": gemm_tf, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
                          "frac": (gemm_tf / peaks["bf16_sus"]) if gemm_tf else None,
                          "peak_src": peaks["src"] + " bf16_tflops_sustained (kernel timed inside a long step)",
-                         "gemm_share_of_step": gemm_ms / args.steps / ms_step,
+                         # events bracket the K1 launches of the LAST microbatch of every
+                         # timed step (same shapes each microbatch); share scaled by m
+                         "events": "K1 launches of the last microbatch of each timed step",
+                         "gemm_share_of_step": gemm_ms * m / args.steps / ms_step,
                          "traffic": None},
             "adam": {"achieved_gbs": adam_bytes / (adam_ms / 1e3) / 1e9 if adam_ms else None,
                      "peak_gbs": peaks["hbm"], "bytes_per_param": 28},

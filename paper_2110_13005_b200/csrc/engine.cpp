@@ -744,6 +744,7 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   const int shard = batch / c->g_data;
   const int m = shard / c->microbatch;
   c->cur_mtotal = batch / c->microbatch;   // D-9: microbatches in the whole batch
+  c->cur_m = m;
   c->ev_next = 0;
   c->prof.clear();
   c->launches = 0;

@@ -110,6 +110,8 @@ struct Ctx {
   bool grads_ready = false;           // run_batch (or GRAD writes) done, optimizer pending
   int bwd_count = 0;                  // backwards done in this batch (first one stores)
   int cur_mtotal = 1;
+  int cur_m = 1;                      // microbatches of this replica in the current batch
+  bool prof_mb = false;               // profile the launches of the current microbatch
   int write_grad_mask = 0;
   std::vector<char> grad_written;
   bool profiling = false;

@@ -27,6 +27,10 @@
 namespace axonn {
 
 constexpr int BM = 128, BK = 64, STAGES = 4;
+// 8 epilogue warps: two per TMEM lane quarter, each draining half of the tile's columns, so
+// the fp32 read-modify-write (wgrad) and GeLU epilogues keep enough loads in flight.
+constexpr int EPI_WARPS = 8;
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
 struct GemmParams {
   int M, N, K, Z, Z1;
@@ -159,7 +163,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
 }
 
 template <int BN>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap mapA,
                       const __grid_constant__ CUtensorMap mapB, const GemmParams p) {
   constexpr int A_BYTES = BM * BK * 2;
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], EPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -261,7 +265,9 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    const int q = warp & 3;   // TMEM lane quarter this warp may access
+    const int q = warp & 3;                     // TMEM lane quarter this warp may access
+    const int cpart = (warp - 2) / 4;           // which column slice of the tile
+    constexpr int CW = BN / (EPI_WARPS / 4);    // columns per epilogue warp
     int it = 0;
     for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
       int z, m0, n0, kb0, kb1;
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = cpart * CW; c < (cpart + 1) * CW; c += 32) {
         if (n0 + c >= p.N) break;
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c, r);
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(192, 1)
 // Per-SM smem traffic per MMA is half the 1-CTA 128x256 tile's.
 constexpr int STAGES2 = 6;
 template <int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap mapA,
                            const __grid_constant__ CUtensorMap mapB, const GemmParams p) {
   constexpr int TBM = 2 * BM;                 // 256 rows per pair
@@ -328,7 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[a], 2 * EPI_WARPS);   // epilogue warps of both CTAs
     }
     fence_barrier_init();
   }
@@ -408,6 +414,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
   } else {
     const int q = warp & 3;
+    const int cpart = (warp - 2) / 4;
+    constexpr int CW = BN / (EPI_WARPS / 4);
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
     int it = 0;
@@ -419,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + (int)rank * BM + q * 32 + lane;
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = cpart * CW; c < (cpart + 1) * CW; c += 32) {
         if (n0 + c >= p.N) break;
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c, r);
@@ -759,7 +767,7 @@ static int launch_bn(const GemmArgs& g, cudaStream_t st) {
   fill_params(p, g, BM, BN);
   int grid = p.total < g_num_sms ? p.total : g_num_sms;
   if (g.max_ctas > 0 && grid > g.max_ctas) grid = g.max_ctas;
-  gemm_bf16_tcgen05<BN><<<grid, 192, SMEM, st>>>(ma, mb, p);
+  gemm_bf16_tcgen05<BN><<<grid, GEMM_THREADS, SMEM, st>>>(ma, mb, p);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
@@ -781,7 +789,7 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
   int pairs_avail = g_num_sms / 2;
   if (g.max_ctas > 0 && pairs_avail > g.max_ctas / 2) pairs_avail = g.max_ctas / 2;
   int pairs = p.total < pairs_avail ? p.total : pairs_avail;
-  gemm_bf16_tcgen05_pair<BN><<<2 * pairs, 192, SMEM, st>>>(ma, mb, p);
+  gemm_bf16_tcgen05_pair<BN><<<2 * pairs, GEMM_THREADS, SMEM, st>>>(ma, mb, p);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

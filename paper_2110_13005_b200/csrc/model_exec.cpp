@@ -23,7 +23,7 @@ int Ctx::gemm(GemmArgs g, double flops) {
   if (g.alpha == 0.f) g.alpha = 1.f;
   if (g.max_ctas == 0 && g_inter > 1) g.max_ctas = num_sms - 8;   // leave SMs to posted NCCL P2P kernels
   ProfRec pr{};
-  if (profiling) {
+  if (prof_mb) {
     pr.a = ev();
     pr.b = ev();
     pr.work = flops;
@@ -35,7 +35,7 @@ int Ctx::gemm(GemmArgs g, double flops) {
   if (rc) return fail(AXONN_ERR_CUDA, "gemm_launch failed rc=" + std::to_string(rc) +
                                           " M=" + std::to_string(g.M) + " N=" + std::to_string(g.N) +
                                           " K=" + std::to_string(g.K));
-  if (profiling) {
+  if (prof_mb) {
     cudaEventRecord(pr.b, s_comp);
     prof.push_back(pr);
   }
@@ -248,6 +248,10 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
 // nn_shard.Forward for microbatch mb into slot sl.  Stage 0 embeds its tokens;
 // the last stage also runs LN_f, the LM head and the fused, pre-divided loss.
 int Ctx::forward(Slot& sl, int mb) {
+  // K1 launches are bracketed by CUDA events only for the last microbatch of the
+  // batch (every microbatch runs the same GEMM shapes; bracketing all of them would
+  // perturb the timed step by several percent).
+  prof_mb = profiling && mb == cur_m - 1;
   const int b = microbatch;
   const int32_t* tok = dtok + (size_t)mb * b * (s + 1);
   if (first) KCHK(embed_fwd(tok, s + 1, b, s, h, p16(tok_emb), p16(pos_emb), sl.in, s_comp));
@@ -269,6 +273,7 @@ int Ctx::forward(Slot& sl, int mb) {
 // stage, where Backward(1) starts from the cross-entropy gradient already
 // written in place of the logits).  The input gradient goes to sl.gsend.
 int Ctx::backward(Slot& sl, int mb, const void* dout) {
+  prof_mb = profiling && mb == cur_m - 1;
   const int b = microbatch;
   const int acc = bwd_count > 0 ? 1 : 0;
   const int32_t* tok = dtok + (size_t)mb * b * (s + 1);

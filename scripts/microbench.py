@@ -82,6 +82,19 @@ def gemm_sweep(variants=(0, 1, 2)):
         else:
             ref = lambda: torch.matmul(A.t(), B)
         res["cublas_tflops"] = fl / time_cuda(ref) / 1e9
+        if kind == "fwd" and name in ("fc1", "proj"):   # the step's fused epilogues
+            bias = torch.randn(N, device="cuda", dtype=torch.bfloat16)
+            aux = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            g = _lib.GemmArgs()
+            g.M, g.N, g.K, g.Z, g.Z1 = M, N, K, 1, 1
+            g.A, g.lda, g.B, g.ldb, g.C, g.ldc = A.data_ptr(), K, B.data_ptr(), K, Cb.data_ptr(), N
+            g.alpha, g.bias = 1.0, bias.data_ptr()
+            if name == "fc1":
+                g.epi, g.aux, g.ld_aux = 1, aux.data_ptr(), N        # bias + GeLU (+ pre store)
+            else:
+                g.epi, g.resid, g.ld_resid = 0, aux.data_ptr(), N    # bias + residual
+            res["ours_fused_epilogue_tflops"] = fl / time_cuda(
+                lambda: lib.axonn_k_gemm(C.byref(g), C.c_void_p(st))) / 1e9
         out.append(res)
         print(json.dumps(res), flush=True)
         del A, B, Cb
