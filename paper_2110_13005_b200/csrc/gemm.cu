@@ -66,14 +66,40 @@ __device__ __forceinline__ bool tile_coords(const GemmParams& p, int BN, int t, 
   return kb1 > kb0;
 }
 
-__device__ __forceinline__ float gelu_f(float x) {
+// tanh on the SFU (MUFU.TANH, rel. error ~2^-11: below the bf16 rounding of the output)
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_f(float x) {   // D-5 tanh GeLU
   const float c = 0.7978845608028654f, a = 0.044715f;
-  return 0.5f * x * (1.0f + tanhf(c * (x + a * x * x * x)));
+  return 0.5f * x * (1.0f + tanh_fast(c * (x + a * x * x * x)));
 }
 __device__ __forceinline__ float gelu_grad_f(float x) {
   const float c = 0.7978845608028654f, a = 0.044715f;
-  float t = tanhf(c * (x + a * x * x * x));
+  float t = tanh_fast(c * (x + a * x * x * x));
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * c * (1.0f + 3.0f * a * x * x);
+}
+__device__ __forceinline__ void ld8_bf16(const __nv_bfloat16* p, float* f) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void st8_bf16(__nv_bfloat16* p, const float* f) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ bool al16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
 }
 
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int row, int col0,
@@ -104,6 +130,43 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
       for (int i = 0; i < ncols; ++i) C[i] = p.accumulate ? C[i] + v[i] : v[i];
     }
     return;
+  }
+  {  // fast path: full 32-column chunk, every operand 16-byte aligned -> 16-byte accesses only
+    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.C) + z2 * p.c_s2 + z1 * p.c_s1 +
+                         row * p.ldc + col0;
+    __nv_bfloat16* auxp = p.aux ? p.aux + row * p.ld_aux + col0 : nullptr;
+    const __nv_bfloat16* rsp = p.resid ? p.resid + row * p.ld_resid + col0 : nullptr;
+    const __nv_bfloat16* bp = p.bias ? p.bias + col0 : nullptr;
+    if (ncols == 32 && p.col_group_in == 0 && al16(dst) && (!auxp || al16(auxp)) &&
+        (!rsp || al16(rsp)) && (!bp || al16(bp))) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float* w = v + 8 * j;
+        float t[8];
+        if (bp) {
+          ld8_bf16(bp + 8 * j, t);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) w[i] += t[i];
+        }
+        if (p.epi == EPI_BIAS_GELU) {
+          st8_bf16(auxp + 8 * j, w);              // pre-activation (bf16) for the backward
+#pragma unroll
+          for (int i = 0; i < 8; ++i)             // GeLU of the same rounded value
+            w[i] = gelu_f(__bfloat162float(__float2bfloat16_rn(w[i])));
+        } else if (p.epi == EPI_DGELU) {
+          ld8_bf16(auxp + 8 * j, t);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) w[i] *= gelu_grad_f(t[i]);
+        }
+        if (rsp) {
+          ld8_bf16(rsp + 8 * j, t);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) w[i] += t[i];
+        }
+        st8_bf16(dst + 8 * j, w);
+      }
+      return;
+    }
   }
   if (p.bias) {
 #pragma unroll
@@ -455,7 +518,182 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 //   EPI_SOFTMAX_BWD : C = dS = alpha * P * (dP - sum_k P dP)     (acc = dP = dO V^T, P = aux)
 // Removes the fp32 score round trip and the separate softmax kernels (D-7, D-8).
 constexpr int RS_STAGES = 2;
-__global__ void __launch_bounds__(192, 1)
+constexpr int RS_THREADS = 64 + 32 * 8;                 // 8 epilogue warps
+constexpr int RS_EPI_SMEM = 3 * 2 * 128 * 4 + 8 * 4096;  // partial max/sum/dot + staging
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Epilogue of gemm_rowsoftmax: warp pair (q, half) owns TMEM lane quarter q (32 score rows)
+// and key columns [256 half, 256 half + 256).  Row statistics are combined across the pair
+// through shared memory; P / dS rows leave (and P rows arrive) through a per-warp swizzled
+// 32 x 64 bf16 staging tile so every global access is a coalesced 128-byte row segment.
+__device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_t tmem_base,
+                                                    uint64_t* tfull, uint64_t* tempty,
+                                                    uint8_t* scratch, int warp, int lane) {
+  const int q = warp & 3, half = (warp - 2) >> 2;
+  const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+  float* red_max = reinterpret_cast<float*>(scratch);      // [2][128]
+  float* red_sum = red_max + 256;
+  float* red_dot = red_sum + 256;
+  uint4* stg = reinterpret_cast<uint4*>(scratch + 3 * 2 * 128 * 4) + (warp - 2) * 256;   // 32 x 8
+  const int rl = q * 32 + lane;                            // row within the 128-row tile
+  const bool fwd = p.epi == EPI_SOFTMAX;
+  int it = 0;
+  for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
+    const int z = t / p.num_m, m0 = (t % p.num_m) * BM;
+    const int z1 = z % p.Z1, z2 = z / p.Z1;
+    const int kv = min(p.N, m0 + BM);
+    const int row = m0 + rl;
+    const long long base = z2 * p.c_s2 + z1 * p.c_s1;
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + base;
+    const __nv_bfloat16* Pin = p.aux + base;
+    const int c_lo = half * 256;
+    const int c_hi = min(kv, c_lo + 256);                    // my columns holding scores
+    const int c_end = min(p.N, c_lo + 256);                  // my columns to write
+    mbar_wait(tfull, it & 1);
+    tc_fence_after();
+    uint32_t r[32];
+    // coalesced load of P rows [m0 + 32 q, +32) x [g0, g0 + 64) into the staging tile
+    auto stage_P = [&](int g0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = i * 4 + lane / 8, ch = lane % 8;
+        const int gr = m0 + q * 32 + rr;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (gr < p.M) v = *reinterpret_cast<const uint4*>(Pin + (long long)gr * p.ldc + g0 + ch * 8);
+        stg[rr * 8 + (ch ^ (rr & 7))] = v;
+      }
+      __syncwarp();
+    };
+    // coalesced store of the staging tile to out rows [m0 + 32 q, +32) x [g0, g0 + 64)
+    auto flush = [&](int g0) {
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = i * 4 + lane / 8, ch = lane % 8;
+        const int gr = m0 + q * 32 + rr;
+        if (gr < p.M)
+          *reinterpret_cast<uint4*>(out + (long long)gr * p.ldc + g0 + ch * 8) = stg[rr * 8 + (ch ^ (rr & 7))];
+      }
+      __syncwarp();
+    };
+    auto put_row = [&](int j, const float* v8) {   // this thread's row, 16-byte chunk j
+      uint4 u;
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(v8[2 * i], v8[2 * i + 1]);
+      stg[lane * 8 + (j ^ (lane & 7))] = u;
+    };
+    auto get_row = [&](int j, float* v8) {
+      uint4 u = stg[lane * 8 + (j ^ (lane & 7))];
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float2 f = __bfloat1622float2(h2[i]);
+        v8[2 * i] = f.x;
+        v8[2 * i + 1] = f.y;
+      }
+    };
+    if (fwd) {
+      float mx = -3.0e38f;
+      for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
+        tmem_ld32(trow + c0, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c0 + i <= row) mx = fmaxf(mx, __uint_as_float(r[i]) * p.alpha);
+      }
+      red_max[half * 128 + rl] = mx;
+      named_bar(1 + q, 64);
+      mx = fmaxf(red_max[rl], red_max[128 + rl]);
+      float sum = 0.f;
+      for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
+        tmem_ld32(trow + c0, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c0 + i <= row) sum += __expf(__uint_as_float(r[i]) * p.alpha - mx);
+      }
+      red_sum[half * 128 + rl] = sum;
+      named_bar(1 + q, 64);
+      const float inv = 1.f / (red_sum[rl] + red_sum[128 + rl]);
+      for (int g0 = c_lo; g0 < c_end; g0 += 64) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int c0 = g0 + 32 * hh;
+          float v[32];
+          if (c0 < c_hi) {
+            tmem_ld32(trow + c0, r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              v[i] = (c0 + i <= row) ? __expf(__uint_as_float(r[i]) * p.alpha - mx) * inv : 0.f;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) put_row(4 * hh + j, v + 8 * j);
+        }
+        flush(g0);
+      }
+    } else {   // EPI_SOFTMAX_BWD: dS = alpha * P * (dP - rowsum(P dP))
+      float dot = 0.f;
+      for (int g0 = c_lo; g0 < c_hi; g0 += 64) {
+        stage_P(g0);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int c0 = g0 + 32 * hh;
+          if (c0 < c_hi) {
+            tmem_ld32(trow + c0, r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float pv[8];
+              get_row(4 * hh + j, pv);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (c0 + 8 * j + i <= row) dot += pv[i] * __uint_as_float(r[8 * j + i]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      red_dot[half * 128 + rl] = dot;
+      named_bar(1 + q, 64);
+      dot = red_dot[rl] + red_dot[128 + rl];
+      for (int g0 = c_lo; g0 < c_end; g0 += 64) {
+        if (g0 < c_hi) stage_P(g0);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int c0 = g0 + 32 * hh;
+          float v[32];
+          if (c0 < c_hi) {
+            tmem_ld32(trow + c0, r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float pv[8];
+              get_row(4 * hh + j, pv);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                v[8 * j + i] = (c0 + 8 * j + i <= row)
+                                   ? p.alpha * pv[i] * (__uint_as_float(r[8 * j + i]) - dot) : 0.f;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+          __syncwarp();   // everyone has read its P chunk before it is overwritten
+#pragma unroll
+          for (int j = 0; j < 4; ++j) put_row(4 * hh + j, v + 8 * j);
+        }
+        flush(g0);
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tempty);
+  }
+}
+__global__ void __launch_bounds__(RS_THREADS, 1)
     gemm_rowsoftmax(const __grid_constant__ CUtensorMap mapA,
                     const __grid_constant__ CUtensorMap mapB, const GemmParams p) {
   constexpr int A_BYTES = BM * BK * 2;
@@ -477,7 +715,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    mbar_init(tempty, 8);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_holder);
@@ -537,6 +775,11 @@ __global__ void __launch_bounds__(192, 1)
         mma_commit(tfull);
       }
     }
+  } else {
+    rowsoftmax_epilogue(p, tmem_base, tfull, tempty, reinterpret_cast<uint8_t*>(tmem_holder + 4),
+                        warp, lane);
+  }
+#if 0   // previous 4-warp row-per-thread epilogue (kept for reference, not compiled)
   } else {
     const int q = warp & 3;
     const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
@@ -661,6 +904,7 @@ __global__ void __launch_bounds__(192, 1)
       if (lane == 0) mbar_arrive(tempty);
     }
   }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -794,7 +1038,7 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
 }
 
 static int launch_rowsoftmax(const GemmArgs& g, cudaStream_t st) {
-  constexpr int SMEM = RS_STAGES * (BM * BK * 2 + 2 * 256 * BK * 2) + 1024 + 256;
+  constexpr int SMEM = RS_STAGES * (BM * BK * 2 + 2 * 256 * BK * 2) + 1024 + 256 + RS_EPI_SMEM;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(gemm_rowsoftmax, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
@@ -813,7 +1057,7 @@ static int launch_rowsoftmax(const GemmArgs& g, cudaStream_t st) {
   p.total = p.num_m * g.Z;
   int grid = p.total < g_num_sms ? p.total : g_num_sms;
   if (g.max_ctas > 0 && grid > g.max_ctas) grid = g.max_ctas;
-  gemm_rowsoftmax<<<grid, 192, SMEM, st>>>(ma, mb, p);
+  gemm_rowsoftmax<<<grid, RS_THREADS, SMEM, st>>>(ma, mb, p);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

@@ -37,7 +37,7 @@ def time_cuda(fn, iters=10, warm=3):
     return tot / iters
 
 
-def gemm_sweep(variants=(0, 1, 2)):
+def gemm_sweep(variants=(0, 1, 2), only=None, iters=10):
     import torch
     from paper_2110_13005_b200 import _lib
     lib = _lib.load()
@@ -49,6 +49,8 @@ def gemm_sweep(variants=(0, 1, 2)):
             shapes.append((tag, name, "wgrad", N, K, M))
         shapes.append((tag, "head", "fwd", M, 51200, h))
     out = []
+    if only:
+        shapes = [s for s in shapes if f"{s[0]} {s[1]} {s[2]}" == only]
     for tag, name, kind, M, N, K in shapes:
         # operands in the layouts the step uses
         A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16) if kind != "wgrad" else \
@@ -73,7 +75,7 @@ def gemm_sweep(variants=(0, 1, 2)):
             def run(g=g):
                 rc = lib.axonn_k_gemm(C.byref(g), C.c_void_p(st))
                 assert rc == 0, rc
-            ms = time_cuda(run)
+            ms = time_cuda(run, iters=iters, warm=min(3, iters))
             res[f"ours_v{v}_tflops"] = fl / ms / 1e9
         if kind == "fwd":
             ref = lambda: torch.matmul(A, B.t())
@@ -81,7 +83,7 @@ def gemm_sweep(variants=(0, 1, 2)):
             ref = lambda: torch.matmul(A, B)
         else:
             ref = lambda: torch.matmul(A.t(), B)
-        res["cublas_tflops"] = fl / time_cuda(ref) / 1e9
+        res["cublas_tflops"] = fl / time_cuda(ref, iters=iters, warm=min(3, iters)) / 1e9
         if kind == "fwd" and name in ("fc1", "proj"):   # the step's fused epilogues
             bias = torch.randn(N, device="cuda", dtype=torch.bfloat16)
             aux = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
@@ -148,8 +150,11 @@ def adam_sweep():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--what", default="gemm,adam")
+    ap.add_argument("--only", default=None, help='one shape, e.g. "1.3B fc1 fwd"')
+    ap.add_argument("--variants", default="0,1,2")
+    ap.add_argument("--iters", type=int, default=10)
     a = ap.parse_args()
     if "gemm" in a.what:
-        gemm_sweep()
+        gemm_sweep(tuple(int(v) for v in a.variants.split(",")), a.only, a.iters)
     if "adam" in a.what:
         adam_sweep()
