@@ -242,6 +242,7 @@ def main():
     # by CUDA events on the library's compute stream (roofline numbers)
     eng.set_profiling(True)
     gemm_ms = gemm_flop = adam_ms = adam_bytes = 0.0
+    breakdown = {}
     launches = 0
     D.barrier(world)
     torch.cuda.synchronize()
@@ -257,6 +258,11 @@ def main():
             adam_ms += st["adam_ms"]
             adam_bytes += st["adam_bytes"]
             launches += int(st["kernel_launches"])
+            for k, (kms, kw, kn) in eng.profile().items():
+                acc = breakdown.setdefault(k, [0.0, 0.0, 0])
+                acc[0] += kms
+                acc[1] += kw
+                acc[2] += kn
         eng.timer_mark(1)
         dev_ms = eng.timer_elapsed_ms(0, 1)
     torch.cuda.synchronize()
@@ -327,6 +333,13 @@ def main():
             "adam": {"achieved_gbs": adam_bytes / (adam_ms / 1e3) / 1e9 if adam_ms else None,
                      "peak_gbs": peaks["hbm"], "bytes_per_param": 28},
             "cpu_baseline": cpu,
+            # per-shape K1 timing (last microbatch of each timed step): ms/launch, TFLOP/s
+            "gemm_breakdown": {k: {"ms_per_launch": v[0] / max(v[2], 1),
+                                   ("tflops" if k != "adamw" else "GB/s"):
+                                       v[1] / (v[0] / 1e3) / (1e12 if k != "adamw" else 1e9)
+                                       if v[0] > 0 else None,
+                                   "launches": v[2]}
+                               for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])},
         }
         print(json.dumps(out), flush=True)
     eng.close()

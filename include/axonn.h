@@ -157,8 +157,13 @@ enum {
   AXONN_STAT_COUNT = 12
 };
 AXONN_API axonn_status axonn_stats(const axonn_ctx* ctx, double* out, int n);
-/* 1: bracket every K1/K9 launch with CUDA events on its stream (for the
- * roofline numbers in bench.py); 0: off (default). */
+/* Per-shape timing of the last profiled batch + step as a JSON object
+ * {"fwd|dgrad|wgrad|attn MxNxK zZ epiE": [ms, flop, launches], "adamw": [ms, bytes, n]}.
+ * Copies at most n-1 characters into buf (NUL-terminated); returns the full length. */
+AXONN_API int axonn_profile_json(const axonn_ctx* ctx, char* buf, int n);
+/* 1: bracket the K1 launches of the last microbatch of each batch and every K9
+ * launch with CUDA events on their streams (roofline numbers in bench.py);
+ * 0: off (default). */
 AXONN_API axonn_status axonn_set_profiling(axonn_ctx* ctx, int on);
 
 /* Device-side timing for benchmarks: axonn_timer_mark(ctx, id) records CUDA

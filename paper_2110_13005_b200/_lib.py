@@ -62,6 +62,7 @@ def _declare(lib):
         "axonn_write_tensor": (I, [P, I, I, P]),
         "axonn_stats": (I, [P, C.POINTER(C.c_double), I]),
         "axonn_set_profiling": (I, [P, I]),
+        "axonn_profile_json": (I, [P, C.c_char_p, I]),
         "axonn_timer_mark": (I, [P, I]),
         "axonn_timer_elapsed": (I, [P, I, I, C.POINTER(C.c_double)]),
         "axonn_k_gemm": (I, [C.POINTER(GemmArgs), P]),

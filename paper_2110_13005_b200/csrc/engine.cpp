@@ -9,6 +9,7 @@
 #include <cstring>
 #include <deque>
 #include <new>
+#include <map>
 #include <thread>
 
 #include "engine.h"
@@ -550,6 +551,17 @@ AXONN_API axonn_status axonn_timer_elapsed(axonn_ctx* c, int a, int b, double* m
   return AXONN_OK;
 }
 
+AXONN_API int axonn_profile_json(const axonn_ctx* c, char* buf, int n) {
+  if (!c) return -1;
+  const int len = (int)c->prof_json.size();
+  if (buf && n > 0) {
+    int k = len < n - 1 ? len : n - 1;
+    memcpy(buf, c->prof_json.data(), k);
+    buf[k] = 0;
+  }
+  return len;
+}
+
 AXONN_API axonn_status axonn_set_profiling(axonn_ctx* c, int on) {
   if (!c) return AXONN_ERR_INVALID_ARG;
   c->profiling = on != 0;
@@ -915,6 +927,25 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
   c->stats[AXONN_STAT_ADAM_MS] = ams;
   c->stats[AXONN_STAT_ADAM_BYTES] = aby;
   c->stats[AXONN_STAT_KERNEL_LAUNCHES] = (double)c->launches;
+  if (!c->prof.empty()) {   // per-shape breakdown: {"key": [ms, work, launches], ...}
+    std::map<std::string, double[3]> agg;
+    for (const ProfRec& p : c->prof) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, p.a, p.b);
+      const std::string k = p.kind == 1 ? "adamw" : p.key;
+      agg[k][0] += ms;
+      agg[k][1] += p.work;
+      agg[k][2] += 1;
+    }
+    std::string js = "{";
+    for (auto& kv : agg) {
+      char buf[192];
+      snprintf(buf, sizeof(buf), "%s\"%s\": [%.6f, %.6e, %d]", js.size() > 1 ? ", " : "",
+               kv.first.c_str(), kv.second[0], kv.second[1], (int)kv.second[2]);
+      js += buf;
+    }
+    c->prof_json = js + "}";
+  }
   return AXONN_OK;
 }
 

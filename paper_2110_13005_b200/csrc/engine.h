@@ -45,7 +45,8 @@ struct Slot {
 struct ProfRec {
   cudaEvent_t a, b;
   double work;
-  int kind;   // 0 gemm, 1 adam
+  int kind;   // 0 linear-layer GEMM, 1 adam, 2 attention GEMM
+  std::string key;   // "fwd|dgrad|wgrad|attn MxNxK epi"
 };
 
 struct Ctx {
@@ -117,6 +118,7 @@ struct Ctx {
   bool profiling = false;
   std::vector<ProfRec> prof;
   double stats[AXONN_STAT_COUNT] = {};
+  std::string prof_json = "{}";       // per-shape K1 / K9 timing of the last profiled step
   long long launches = 0;
 
   // helpers

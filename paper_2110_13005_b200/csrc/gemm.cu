@@ -562,7 +562,8 @@ __device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_
         const int rr = i * 4 + lane / 8, ch = lane % 8;
         const int gr = m0 + q * 32 + rr;
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (gr < p.M) v = *reinterpret_cast<const uint4*>(Pin + (long long)gr * p.ldc + g0 + ch * 8);
+        if (gr < p.M && g0 + ch * 8 < p.N)
+          v = *reinterpret_cast<const uint4*>(Pin + (long long)gr * p.ldc + g0 + ch * 8);
         stg[rr * 8 + (ch ^ (rr & 7))] = v;
       }
       __syncwarp();
@@ -574,7 +575,7 @@ __device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_
       for (int i = 0; i < 8; ++i) {
         const int rr = i * 4 + lane / 8, ch = lane % 8;
         const int gr = m0 + q * 32 + rr;
-        if (gr < p.M)
+        if (gr < p.M && g0 + ch * 8 < p.N)   // rows shorter than a 64-column group
           *reinterpret_cast<uint4*>(out + (long long)gr * p.ldc + g0 + ch * 8) = stg[rr * 8 + (ch ^ (rr & 7))];
       }
       __syncwarp();

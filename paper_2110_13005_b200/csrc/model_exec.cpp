@@ -11,6 +11,7 @@
 // head and the fused cross entropy with the loss pre-divided by the number of
 // microbatches in the batch (D-9).
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 
 #include "engine.h"
@@ -26,8 +27,12 @@ int Ctx::gemm(GemmArgs g, double flops) {
   if (prof_mb) {
     pr.a = ev();
     pr.b = ev();
-    pr.work = flops;
+    pr.work = flops >= 0 ? flops : 2.0 * g.M * g.N * g.K * g.Z;
     pr.kind = flops >= 0 ? 0 : 2;
+    const char* kind = flops < 0 ? "attn" : (g.a_mn && g.b_mn) ? "wgrad" : g.b_mn ? "dgrad" : "fwd";
+    char key[96];
+    snprintf(key, sizeof(key), "%s %dx%dx%d z%d epi%d", kind, g.M, g.N, g.K, g.Z, g.epi);
+    pr.key = key;
     cudaEventRecord(pr.a, s_comp);
   }
   int rc = gemm_launch(g, s_comp);

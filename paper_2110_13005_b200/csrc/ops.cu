@@ -349,8 +349,83 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int nchunks,
 
 int colsum_chunks(int rows) { return (rows + CR_ROWCHUNK - 1) / CR_ROWCHUNK; }
 
+// Single-pass column sums: a block owns 32 columns (4 groups of 8, 16-byte loads) and all
+// rows, split over 64 row lanes; partials are combined in shared memory in a fixed order
+// (bitwise reproducible).  out_b[c] (+)= sum_r dy[r][c];  out_g[c] (+)= sum_r dy * xhat.
+__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                     const __nv_bfloat16* __restrict__ x,
+                                                     const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, int rows,
+                                                     int n, float* __restrict__ out_b,
+                                                     float* __restrict__ out_g, int accumulate) {
+  const int cg = threadIdx.x & 3, rl = threadIdx.x >> 2;   // 4 column groups x 64 row lanes
+  const int c = blockIdx.x * 32 + cg * 8;
+  float sb[8], sg[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sb[i] = sg[i] = 0.f;
+  if (c < n) {
+    int r = rl;
+    for (; r + 3 * 64 < rows; r += 4 * 64) {   // 4 independent 16-byte loads in flight
+      float d[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load8(dy + (long long)(r + u * 64) * n + c, d[u]);
+      if (x) {
+        float xv[4][8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) load8(x + (long long)(r + u * 64) * n + c, xv[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float mu = mean[r + u * 64], rs = rstd[r + u * 64];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) sg[i] += d[u][i] * ((xv[u][i] - mu) * rs);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sb[i] += d[u][i];
+    }
+    for (; r < rows; r += 64) {
+      float d[8];
+      load8(dy + (long long)r * n + c, d);
+      if (x) {
+        float xv[8];
+        load8(x + (long long)r * n + c, xv);
+        const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sg[i] += d[i] * ((xv[i] - mu) * rs);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sb[i] += d[i];
+    }
+  }
+  __shared__ float sh[2][64][33];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    sh[0][rl][cg * 8 + i] = sb[i];
+    sh[1][rl][cg * 8 + i] = sg[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int which = threadIdx.x >> 5, col = threadIdx.x & 31;
+    const int gc = blockIdx.x * 32 + col;
+    if (gc < n && (which == 0 || x)) {
+      float acc = 0.f;
+      for (int k = 0; k < 64; ++k) acc += sh[which][k][col];
+      float* o = which == 0 ? out_b : out_g;
+      o[gc] = accumulate ? o[gc] + acc : acc;
+    }
+  }
+}
+
 int colsum(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int n,
            float* workspace, float* out_b, float* out_g, int accumulate, cudaStream_t st) {
+  if (n % 8 == 0) {
+    (void)workspace;
+    colsum_kernel<<<(n + 31) / 32, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                                                 mean, rstd, rows, n, out_b, out_g, accumulate);
+    return ok();
+  }
   int nch = colsum_chunks(rows);
   float* part_b = workspace;
   float* part_g = workspace + (long long)nch * n;
@@ -579,7 +654,8 @@ int preload_ops() {
   const void* fns[] = {(const void*)embed_fwd_kernel, (const void*)embed_bwd_tok_kernel,
                        (const void*)embed_bwd_pos_kernel, (const void*)ln_fwd_kernel,
                        (const void*)ln_bwd_kernel, (const void*)colsum_partial_kernel,
-                       (const void*)colsum_final_kernel, (const void*)softmax_fwd_kernel,
+                       (const void*)colsum_final_kernel, (const void*)colsum_kernel,
+                       (const void*)softmax_fwd_kernel,
                        (const void*)softmax_bwd_kernel, (const void*)xent_kernel,
                        (const void*)reduce_sum_kernel, (const void*)cast_f32_bf16_kernel,
                        (const void*)cast_bf16_f32_kernel, (const void*)init_normal_kernel};

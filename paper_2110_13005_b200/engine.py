@@ -138,6 +138,14 @@ class AxoNN:
         self._check(self.lib.axonn_timer_elapsed(self.ctx, a, b, C.byref(ms)), "timer_elapsed")
         return ms.value
 
+    def profile(self) -> dict:
+        """Per-shape K1/K9 timing of the last profiled batch: key -> (ms, work, launches)."""
+        import json
+        n = self.lib.axonn_profile_json(self.ctx, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        self.lib.axonn_profile_json(self.ctx, buf, n + 1)
+        return json.loads(buf.value.decode() or "{}")
+
     def set_profiling(self, on: bool):
         self._check(self.lib.axonn_set_profiling(self.ctx, int(on)), "set_profiling")
 

@@ -175,7 +175,7 @@ def test_gemm_batched_attention_shapes(lib, variant):
     assert rel(host(dK), refK) < 1e-2
 
 
-@pytest.mark.parametrize("s,d", [(384, 64), (320, 128), (512, 128), (64, 24)])
+@pytest.mark.parametrize("s,d", [(384, 64), (320, 128), (512, 128), (64, 24), (32, 32), (96, 16)])
 def test_gemm_rowsoftmax_epilogues(lib, s, d):
     """Epilogue 4: P = causal softmax(alpha Q K^T) straight from a full-row TMEM tile;
     epilogue 5: dS = alpha P (dP - rowsum(P dP)) with dP = dO V^T (D-7, D-8)."""
