@@ -534,10 +534,15 @@ __device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_
                                                     uint8_t* scratch, int warp, int lane) {
   const int q = warp & 3, half = (warp - 2) >> 2;
   const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-  float* red_max = reinterpret_cast<float*>(scratch);      // [2][128]
-  float* red_sum = red_max + 256;
-  float* red_dot = red_sum + 256;
-  uint4* stg = reinterpret_cast<uint4*>(scratch + 3 * 2 * 128 * 4) + (warp - 2) * 256;   // 32 x 8
+  // static __shared__ so the compiler emits STS/LDS (a pointer laundered through integer
+  // arithmetic on the dynamic smem base turns into slow generic ST.E/LD.E)
+  __shared__ float red_s[3 * 2 * 128];
+  __shared__ uint4 stg_s[8 * 256];
+  (void)scratch;
+  float* red_max = red_s;                                  // [2][128]
+  float* red_sum = red_s + 256;
+  float* red_dot = red_s + 512;
+  uint4* stg = stg_s + (warp - 2) * 256;                   // 32 rows x 8 x 16 B per warp
   const int rl = q * 32 + lane;                            // row within the 128-row tile
   const bool fwd = p.epi == EPI_SOFTMAX;
   int it = 0;
@@ -1039,7 +1044,8 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
 }
 
 static int launch_rowsoftmax(const GemmArgs& g, cudaStream_t st) {
-  constexpr int SMEM = RS_STAGES * (BM * BK * 2 + 2 * 256 * BK * 2) + 1024 + 256 + RS_EPI_SMEM;
+  // dynamic part only; the epilogue's RS_EPI_SMEM bytes are static __shared__
+  constexpr int SMEM = RS_STAGES * (BM * BK * 2 + 2 * 256 * BK * 2) + 1024 + 256;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(gemm_rowsoftmax, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
@@ -1071,6 +1077,9 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
     g_pair_mode = (e && e[0] == '0') ? 0 : 1;
   }
   if (g.epi == EPI_SOFTMAX || g.epi == EPI_SOFTMAX_BWD) return launch_rowsoftmax(g, st);
+  // narrow outputs (attention P V, dQ, dK, dV: N = head dim): 256 x 128 pair tiles halve the
+  // per-SM A traffic of 128 x 128 single-CTA tiles
+  if (g.N <= 128 && g.M >= 256 && g_pair_mode && g.variant != 1) return launch_pair<128>(g, st);
   if (g.variant == 1 || (g.variant == 0 && (g.N <= 128 || !g_pair_mode || g.M <= 128)))
     return g.N <= 128 ? launch_bn<128>(g, st) : launch_bn<256>(g, st);
   return launch_pair<256>(g, st);
@@ -1082,7 +1091,8 @@ namespace axonn {
 int preload_gemm() {   // see preload_ops (ops.cu)
   cudaFuncAttributes a;
   const void* fns[] = {(const void*)gemm_bf16_tcgen05<128>, (const void*)gemm_bf16_tcgen05<256>,
-                       (const void*)gemm_bf16_tcgen05_pair<256>, (const void*)gemm_rowsoftmax};
+                       (const void*)gemm_bf16_tcgen05_pair<256>,
+                       (const void*)gemm_bf16_tcgen05_pair<128>, (const void*)gemm_rowsoftmax};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
   return 0;

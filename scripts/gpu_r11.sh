@@ -1,0 +1,8 @@
+set -x; mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()"
+timeout 600 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_step.py -q -m gpu -x > gpurun_out/gpu_tests.log 2>&1; echo "exit $?" >> gpurun_out/gpu_tests.log
+tail -2 gpurun_out/gpu_tests.log
+timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_1p3b.log 2>&1; echo "exit $?" >> gpurun_out/bench_1p3b.log
+CMD="python bench.py --layers 4 --steps 1 --warmup 1 --e2e-steps 1 --no-cpu-baseline"
+timeout 300 $CMD > gpurun_out/prof_plain.log 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_rowsoftmax -s 4 -c 2 -o gpurun_out/rowsoftmax_full $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu exit $?"
