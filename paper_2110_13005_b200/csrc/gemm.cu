@@ -45,6 +45,7 @@ struct GemmParams {
   long long ld_aux;
   float alpha;
   int num_m, num_n, total;
+  int dbg;   // AXONN_RS_DEBUG experiments (row-softmax epilogue): 0 normal
 };
 
 template <int TBM = BM>
@@ -525,6 +526,208 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// v2 epilogue of gemm_rowsoftmax.  Warp pair (q, half) owns TMEM lane quarter q (score rows
+// r0 .. r0+31, r0 = m0 + 32 q) and key columns [256 half, 256 half + 256).  A 32-column
+// chunk c0 of those rows is FULL (c0 + 32 <= r0: every key <= every query), the DIAGONAL
+// chunk (c0 == r0: key i valid for lane >= i) or MASKED (c0 > r0) — warp-uniform, so
+// only the diagonal chunk is predicated.  Forward: exp2 with the 1/sqrt(d) * log2(e) scale
+// folded into one FFMA, computed once and written back to TMEM (tcgen05.st), then
+// rescaled by 1/sum in the store pass.  Backward: P is exactly 0 above the diagonal, so
+// dS = alpha * P * (dP - dot) needs no mask at all.  P / dS leave (and P arrives) through a
+// per-warp swizzled 32 x 64 bf16 staging tile as coalesced 128-byte row segments.
+__device__ __forceinline__ void rowsoftmax_epilogue2(const GemmParams& p, uint32_t tmem_base,
+                                                     uint64_t* tfull, uint64_t* tempty, int warp,
+                                                     int lane) {
+  const int q = warp & 3, half = (warp - 2) >> 2;
+  const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+  __shared__ float red2[3 * 2 * 128];
+  __shared__ uint4 stg2[8 * 256];
+  float* red_max = red2;
+  float* red_sum = red2 + 256;
+  float* red_dot = red2 + 512;
+  uint4* stg = stg2 + (warp - 2) * 256;
+  const int rl = q * 32 + lane;
+  const bool fwd = p.epi == EPI_SOFTMAX;
+  const float c1 = p.alpha * 1.4426950408889634f;   // alpha * log2(e)
+  int it = 0;
+  for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
+    const int z = t / p.num_m, m0 = (t % p.num_m) * BM;
+    const int z1 = z % p.Z1, z2 = z / p.Z1;
+    const int kv = min(p.N, m0 + BM);
+    const int r0 = m0 + q * 32;                 // first row of this warp = its diagonal chunk
+    const int c_lo = half * 256;
+    const int c_end = min(p.N, c_lo + 256);     // my columns to write
+    const int c_val = min(min(kv, c_lo + 256), r0 + 32);   // columns [c_lo, c_val) hold scores
+    const int c_full = min(c_val, r0);          // [c_lo, c_full) are full chunks
+    const bool has_diag = r0 >= c_lo && r0 < c_val;   // diagonal chunk [r0, r0+32) is mine
+    const long long base = z2 * p.c_s2 + z1 * p.c_s1;
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + base;
+    const __nv_bfloat16* Pin = p.aux + base;
+    mbar_wait(tfull, it & 1);
+    tc_fence_after();
+    uint32_t r[32];
+    auto stage_P = [&](int g0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = i * 4 + lane / 8, ch = lane % 8;
+        const int gr = r0 + rr;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (gr < p.M && g0 + ch * 8 < p.N)
+          v = *reinterpret_cast<const uint4*>(Pin + (long long)gr * p.ldc + g0 + ch * 8);
+        stg[rr * 8 + (ch ^ (rr & 7))] = v;
+      }
+      __syncwarp();
+    };
+    auto flush = [&](int g0) {
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = i * 4 + lane / 8, ch = lane % 8;
+        const int gr = r0 + rr;
+        if (gr < p.M && g0 + ch * 8 < p.N)
+          *reinterpret_cast<uint4*>(out + (long long)gr * p.ldc + g0 + ch * 8) =
+              stg[rr * 8 + (ch ^ (rr & 7))];
+      }
+      __syncwarp();
+    };
+    auto put8 = [&](int j, const float* v8) {
+      uint4 u;
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(v8[2 * i], v8[2 * i + 1]);
+      stg[lane * 8 + (j ^ (lane & 7))] = u;
+    };
+    auto get8 = [&](int j, float* v8) {
+      uint4 u = stg[lane * 8 + (j ^ (lane & 7))];
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float2 f = __bfloat1622float2(h2[i]);
+        v8[2 * i] = f.x;
+        v8[2 * i + 1] = f.y;
+      }
+    };
+    if (fwd) {
+      float mx = -3.0e38f;   // max of the raw scores (alpha > 0)
+      for (int c0 = c_lo; c0 < c_full; c0 += 32) {
+        tmem_ld32(trow + c0, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+      }
+      if (has_diag) {   // diagonal chunk
+        tmem_ld32(trow + r0, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i <= lane) mx = fmaxf(mx, __uint_as_float(r[i]));
+      }
+      red_max[half * 128 + rl] = mx;
+      named_bar(1 + q, 64);
+      const float moff = fmaxf(red_max[rl], red_max[128 + rl]) * c1;
+      float s0 = 0.f, s1 = 0.f;
+      for (int c0 = c_lo; c0 < c_full; c0 += 32) {
+        tmem_ld32(trow + c0, r);
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float e0 = ex2_approx(fmaf(__uint_as_float(r[i]), c1, -moff));
+          const float e1 = ex2_approx(fmaf(__uint_as_float(r[i + 1]), c1, -moff));
+          s0 += e0;
+          s1 += e1;
+          r[i] = __float_as_uint(e0);
+          r[i + 1] = __float_as_uint(e1);
+        }
+        tmem_st32(trow + c0, r);
+      }
+      if (has_diag) {
+        tmem_ld32(trow + r0, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float e = i <= lane ? ex2_approx(fmaf(__uint_as_float(r[i]), c1, -moff)) : 0.f;
+          s0 += e;
+          r[i] = __float_as_uint(e);
+        }
+        tmem_st32(trow + r0, r);
+      }
+      tmem_st_wait();
+      red_sum[half * 128 + rl] = s0 + s1;
+      named_bar(1 + q, 64);
+      const float inv = 1.f / (red_sum[rl] + red_sum[128 + rl]);
+      for (int g0 = c_lo; g0 < c_end; g0 += 64) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int c0 = g0 + 32 * hh;
+          float v[32];
+          if (c0 < c_val) {
+            tmem_ld32(trow + c0, r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * inv;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) put8(4 * hh + j, v + 8 * j);
+        }
+        flush(g0);
+      }
+    } else {   // EPI_SOFTMAX_BWD
+      float d0 = 0.f, d1 = 0.f;
+      for (int g0 = c_lo; g0 < c_val; g0 += 64) {
+        stage_P(g0);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int c0 = g0 + 32 * hh;
+          if (c0 < c_val) {
+            tmem_ld32(trow + c0, r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float pv[8];
+              get8(4 * hh + j, pv);
+#pragma unroll
+              for (int i = 0; i < 8; i += 2) {
+                d0 = fmaf(pv[i], __uint_as_float(r[8 * j + i]), d0);
+                d1 = fmaf(pv[i + 1], __uint_as_float(r[8 * j + i + 1]), d1);
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+      red_dot[half * 128 + rl] = d0 + d1;
+      named_bar(1 + q, 64);
+      const float dot = red_dot[rl] + red_dot[128 + rl];
+      for (int g0 = c_lo; g0 < c_end; g0 += 64) {
+        if (g0 < c_val) stage_P(g0);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int c0 = g0 + 32 * hh;
+          float v[32];
+          if (c0 < c_val) {
+            tmem_ld32(trow + c0, r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float pv[8];
+              get8(4 * hh + j, pv);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                v[8 * j + i] = p.alpha * pv[i] * (__uint_as_float(r[8 * j + i]) - dot);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) put8(4 * hh + j, v + 8 * j);
+        }
+        flush(g0);
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tempty);
+  }
+}
+
 // Epilogue of gemm_rowsoftmax: warp pair (q, half) owns TMEM lane quarter q (32 score rows)
 // and key columns [256 half, 256 half + 256).  Row statistics are combined across the pair
 // through shared memory; P / dS rows leave (and P rows arrive) through a per-warp swizzled
@@ -580,7 +783,7 @@ __device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_
       for (int i = 0; i < 8; ++i) {
         const int rr = i * 4 + lane / 8, ch = lane % 8;
         const int gr = m0 + q * 32 + rr;
-        if (gr < p.M && g0 + ch * 8 < p.N)   // rows shorter than a 64-column group
+        if (gr < p.M && g0 + ch * 8 < p.N && p.dbg != 2)   // rows shorter than a 64-col group
           *reinterpret_cast<uint4*>(out + (long long)gr * p.ldc + g0 + ch * 8) = stg[rr * 8 + (ch ^ (rr & 7))];
       }
       __syncwarp();
@@ -602,7 +805,15 @@ __device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_
         v8[2 * i + 1] = f.y;
       }
     };
-    if (fwd) {
+    if (p.dbg == 4) {            // experiment: no epilogue work at all
+    } else if (p.dbg == 3) {     // experiment: TMEM reads only
+      float acc = 0.f;
+      for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
+        tmem_ld32(trow + c0, r);
+        acc += __uint_as_float(r[0]) + __uint_as_float(r[31]);
+      }
+      if (acc == 1234.5f) red_max[rl] = acc;
+    } else if (fwd) {
       float mx = -3.0e38f;
       for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
         tmem_ld32(trow + c0, r);
@@ -614,7 +825,7 @@ __device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_
       named_bar(1 + q, 64);
       mx = fmaxf(red_max[rl], red_max[128 + rl]);
       float sum = 0.f;
-      for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
+      for (int c0 = c_lo; c0 < c_hi && p.dbg != 5; c0 += 32) {
         tmem_ld32(trow + c0, r);
 #pragma unroll
         for (int i = 0; i < 32; ++i)
@@ -623,7 +834,7 @@ __device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_
       red_sum[half * 128 + rl] = sum;
       named_bar(1 + q, 64);
       const float inv = 1.f / (red_sum[rl] + red_sum[128 + rl]);
-      for (int g0 = c_lo; g0 < c_end; g0 += 64) {
+      for (int g0 = c_lo; g0 < c_end && p.dbg < 5; g0 += 64) {
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int c0 = g0 + 32 * hh;
@@ -782,8 +993,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
       }
     }
   } else {
-    rowsoftmax_epilogue(p, tmem_base, tfull, tempty, reinterpret_cast<uint8_t*>(tmem_holder + 4),
-                        warp, lane);
+    rowsoftmax_epilogue2(p, tmem_base, tfull, tempty, warp, lane);
   }
 #if 0   // previous 4-warp row-per-thread epilogue (kept for reference, not compiled)
   } else {
@@ -1062,6 +1272,10 @@ static int launch_rowsoftmax(const GemmArgs& g, cudaStream_t st) {
   fill_params(p, g, BM, 512);
   p.num_n = 1;
   p.total = p.num_m * g.Z;
+  {
+    const char* e = getenv("AXONN_RS_DEBUG");
+    p.dbg = e ? atoi(e) : 0;
+  }
   int grid = p.total < g_num_sms ? p.total : g_num_sms;
   if (g.max_ctas > 0 && grid > g.max_ctas) grid = g.max_ctas;
   gemm_rowsoftmax<<<grid, RS_THREADS, SMEM, st>>>(ma, mb, p);
@@ -1079,7 +1293,9 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   if (g.epi == EPI_SOFTMAX || g.epi == EPI_SOFTMAX_BWD) return launch_rowsoftmax(g, st);
   // narrow outputs (attention P V, dQ, dK, dV: N = head dim): 256 x 128 pair tiles halve the
   // per-SM A traffic of 128 x 128 single-CTA tiles
-  if (g.N <= 128 && g.M >= 256 && g_pair_mode && g.variant != 1) return launch_pair<128>(g, st);
+  // (measured: 36 us vs 30 us for the single-CTA 128 x 128 tiles at the 1.3B attention shape,
+  // so narrow GEMMs use the pair only when forced with variant 2)
+  if (g.N <= 128 && g.M >= 256 && g.variant == 2) return launch_pair<128>(g, st);
   if (g.variant == 1 || (g.variant == 0 && (g.N <= 128 || !g_pair_mode || g.M <= 128)))
     return g.N <= 128 ? launch_bn<128>(g, st) : launch_bn<256>(g, st);
   return launch_pair<256>(g, st);
