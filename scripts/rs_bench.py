@@ -46,6 +46,24 @@ def main():
         out[f"rowsoftmax dbg{dbg} us"] = timeit(args(4, P))
     os.environ["AXONN_RS_DEBUG"] = "0"
     out["scores fp32 GEMM (unfused) us"] = timeit(args(3, S))
+    # fixed per-launch cost: one-tile GEMMs
+    A1 = torch.randn(256, 64, device="cuda").to(torch.bfloat16)
+    C1 = torch.empty(256, 256, device="cuda", dtype=torch.bfloat16)
+    for var in (1, 2):
+        g = _lib.GemmArgs()
+        g.M, g.N, g.K, g.Z, g.Z1 = 256 if var == 2 else 128, 256, 64, 1, 1
+        g.A, g.lda, g.B, g.ldb, g.C, g.ldc = A1.data_ptr(), 64, A1.data_ptr(), 64, C1.data_ptr(), 256
+        g.alpha, g.variant = 1.0, var
+        out[f"one-tile gemm variant{var} us"] = timeit(g, 50)
+    # the narrow attention product P V at the 1.3B shape
+    O = torch.empty(b * s, h, device="cuda", dtype=torch.bfloat16)
+    g = _lib.GemmArgs()
+    g.M, g.N, g.K, g.Z, g.Z1 = s, d, s, b * a, a
+    g.A, g.lda, g.a_s1, g.a_s2 = P.data_ptr(), s, s * s, a * s * s
+    g.B, g.ldb, g.b_s1, g.b_s2, g.b_mn = qkv.data_ptr() + 2 * h * 2, 3 * h, d, s * 3 * h, 1
+    g.C, g.ldc, g.c_s1, g.c_s2 = O.data_ptr(), h, d, s * h
+    g.causal, g.alpha = 2, 1.0
+    out["PV gemm us"] = timeit(g)
     print(json.dumps(out))
 
 
