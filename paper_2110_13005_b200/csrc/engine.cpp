@@ -318,7 +318,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   if (preload_gemm() || preload_ops() || preload_adamw())
     return bail(c->fail(AXONN_ERR_CUDA, "kernel preload failed"));
   for (cudaStream_t* st : {&c->s_comp, &c->s_send_act, &c->s_send_grad, &c->s_recv_act,
-                           &c->s_recv_grad, &c->s_dp, &c->s_h2d, &c->s_d2h, &c->s_opt})
+                           &c->s_recv_grad, &c->s_dp, &c->s_h2d, &c->s_d2h, &c->s_opt, &c->s_wg})
     if ((rc = c->check_cuda(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking), "stream")))
       return bail(rc);
   for (cudaEvent_t* e : {&c->ev_grads_ready, &c->ev_opt_done, &c->ev_loss})
@@ -421,7 +421,7 @@ AXONN_API void axonn_free(axonn_ctx* c) {
     for (cudaEvent_t e : {c->ev_h2d[r], c->ev_adam[r], c->ev_d2h[r]})
       if (e) cudaEventDestroy(e);
   for (cudaStream_t st : {c->s_comp, c->s_send_act, c->s_send_grad, c->s_recv_act, c->s_recv_grad,
-                          c->s_dp, c->s_h2d, c->s_d2h, c->s_opt})
+                          c->s_dp, c->s_h2d, c->s_d2h, c->s_opt, c->s_wg})
     if (st) cudaStreamDestroy(st);
   delete c;
 }

@@ -97,6 +97,11 @@ struct Ctx {
   cudaStream_t s_comp = nullptr, s_send_act = nullptr, s_send_grad = nullptr,
                s_recv_act = nullptr, s_recv_grad = nullptr, s_dp = nullptr, s_h2d = nullptr,
                s_d2h = nullptr, s_opt = nullptr;
+  // weight-gradient side stream: dW GEMMs and bias column sums of the backward run here,
+  // concurrently with the data-gradient chain on s_comp (fills GEMM tail waves)
+  cudaStream_t s_wg = nullptr;
+  cudaStream_t gst = nullptr;         // stream the next gemm() launches on (s_comp default)
+  std::vector<std::pair<const void*, cudaEvent_t>> wg_reads;   // buffers s_wg still reads
   ncclComm_t world_comm = nullptr, dp_comm = nullptr, act_out = nullptr, act_in = nullptr,
              grad_out = nullptr, grad_in = nullptr;
   std::vector<ncclComm_t> owned_comms;
@@ -145,6 +150,10 @@ struct Ctx {
   int backward(Slot& sl, int mb, const void* dout);   // nn_shard.Backward
   int layer_fwd(int li, const void* x, LayerStash& st);
   int layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void* din);
+  void wg_fork();                       // s_wg waits for everything enqueued on s_comp so far
+  void wg_note(const void* buf);        // s_wg reads buf (recorded after its last enqueued read)
+  void wg_guard(const void* buf);       // s_comp waits before overwriting buf
+  void wg_join();                       // s_comp waits for all of s_wg
 };
 
 }  // namespace axonn

@@ -18,7 +18,31 @@
 
 namespace axonn {
 
+void Ctx::wg_fork() {
+  cudaEvent_t e = ev();
+  cudaEventRecord(e, s_comp);
+  cudaStreamWaitEvent(s_wg, e, 0);
+}
+void Ctx::wg_note(const void* buf) {
+  cudaEvent_t e = ev();
+  cudaEventRecord(e, s_wg);
+  for (auto& pr : wg_reads)
+    if (pr.first == buf) { pr.second = e; return; }
+  wg_reads.emplace_back(buf, e);
+}
+void Ctx::wg_guard(const void* buf) {
+  for (auto& pr : wg_reads)
+    if (pr.first == buf) cudaStreamWaitEvent(s_comp, pr.second, 0);
+}
+void Ctx::wg_join() {
+  cudaEvent_t e = ev();
+  cudaEventRecord(e, s_wg);
+  cudaStreamWaitEvent(s_comp, e, 0);
+  wg_reads.clear();
+}
+
 int Ctx::gemm(GemmArgs g, double flops) {
+  cudaStream_t st = gst ? gst : s_comp;
   if (g.Z == 0) g.Z = 1;
   if (g.Z1 == 0) g.Z1 = 1;
   if (g.alpha == 0.f) g.alpha = 1.f;
@@ -33,15 +57,15 @@ int Ctx::gemm(GemmArgs g, double flops) {
     char key[96];
     snprintf(key, sizeof(key), "%s %dx%dx%d z%d epi%d", kind, g.M, g.N, g.K, g.Z, g.epi);
     pr.key = key;
-    cudaEventRecord(pr.a, s_comp);
+    cudaEventRecord(pr.a, st);
   }
-  int rc = gemm_launch(g, s_comp);
+  int rc = gemm_launch(g, st);
   ++launches;
   if (rc) return fail(AXONN_ERR_CUDA, "gemm_launch failed rc=" + std::to_string(rc) +
                                           " M=" + std::to_string(g.M) + " N=" + std::to_string(g.N) +
                                           " K=" + std::to_string(g.K));
   if (prof_mb) {
-    cudaEventRecord(pr.b, s_comp);
+    cudaEventRecord(pr.b, st);
     prof.push_back(pr);
   }
   return 0;
@@ -161,30 +185,48 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   const int b = microbatch;
   const int acc = bwd_count > 0 ? 1 : 0;
   const double dM = M, dh = h;
+  // Weight gradients (dW GEMM + bias column sum) go to s_wg, concurrent with the
+  // data-gradient chain on s_comp; wg_guard() orders any later overwrite of a buffer
+  // s_wg still reads.
   // FC2: dpre = (dout W2) * GeLU'(pre);  dW2 += dout^T act;  db2 += colsum(dout)
+  wg_fork();
+  gst = s_wg;
+  TRY(gemm(lin_wgrad(dout, st.act, M, h, 4 * h, g32(o.w_fc2), acc), 2 * dM * 4 * dh * dh));
+  gst = s_comp;
+  KCHK(colsum(dout, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_fc2), nullptr, acc, s_wg));
+  wg_note(dout);
+  wg_guard(dpre);
   {
     GemmArgs g = lin_dgrad(dout, p16(o.w_fc2), M, h, 4 * h, dpre);
     g.epi = EPI_DGELU; g.aux = st.pre; g.ld_aux = 4 * h;
     TRY(gemm(g, 2 * dM * 4 * dh * dh));
-    TRY(gemm(lin_wgrad(dout, st.act, M, h, 4 * h, g32(o.w_fc2), acc), 2 * dM * 4 * dh * dh));
-    KCHK(colsum(dout, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_fc2), nullptr, acc, s_comp));
   }
   // FC1: du = dpre W1;  dW1 += dpre^T w;  db1 += colsum(dpre)
-  TRY(gemm(lin_dgrad(dpre, p16(o.w_fc1), M, 4 * h, h, du), 2 * dM * 4 * dh * dh));
+  wg_fork();
+  gst = s_wg;
   TRY(gemm(lin_wgrad(dpre, st.w, M, 4 * h, h, g32(o.w_fc1), acc), 2 * dM * 4 * dh * dh));
-  KCHK(colsum(dpre, nullptr, nullptr, nullptr, M, 4 * h, cs_ws, g32(o.b_fc1), nullptr, acc, s_comp));
+  gst = s_comp;
+  KCHK(colsum(dpre, nullptr, nullptr, nullptr, M, 4 * h, cs_ws, g32(o.b_fc1), nullptr, acc, s_wg));
+  wg_note(dpre);
+  TRY(gemm(lin_dgrad(dpre, p16(o.w_fc1), M, 4 * h, h, du), 2 * dM * 4 * dh * dh));
   // LN2: dx1 = dout + LN2'(du);  dg2, db2
+  wg_guard(dx1);
   KCHK(ln_bwd(du, st.x1, st.mean2, st.rstd2, M, h, p16(o.ln2_g), dout, dx1, s_comp));
   KCHK(colsum(du, st.x1, st.mean2, st.rstd2, M, h, cs_ws, g32(o.ln2_b), g32(o.ln2_g), acc, s_comp));
   // proj: dO = dx1 Wo;  dWo += dx1^T o;  dbo += colsum(dx1)
+  wg_fork();
+  gst = s_wg;
+  TRY(gemm(lin_wgrad(dx1, st.o, M, h, h, g32(o.w_o), acc), 2 * dM * dh * dh));
+  gst = s_comp;
+  KCHK(colsum(dx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, s_wg));
+  wg_note(dx1);
   {
     GemmArgs g = lin_dgrad(dx1, p16(o.w_o), M, h, h, dO);
     g.ldc = (long long)heads * dp;   // dO per head, padded like q/k/v
     if (dp != d) { g.col_group_in = d; g.col_group_out = dp; }
     TRY(gemm(g, 2 * dM * dh * dh));
   }
-  TRY(gemm(lin_wgrad(dx1, st.o, M, h, h, g32(o.w_o), acc), 2 * dM * dh * dh));
-  KCHK(colsum(dx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, s_comp));
+  wg_guard(dqkv);
   // attention backward
   {  // dP = dO V^T (fp32 into S)
     GemmArgs g;
@@ -241,10 +283,15 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
     TRY(gemm(g, -1));
   }
   // QKV: du = dqkv Wqkv;  dWqkv += dqkv^T u;  dbqkv += colsum(dqkv)
-  TRY(gemm(lin_dgrad(dqkv, p16(o.w_qkv), M, 3 * h, h, du), 2 * dM * 3 * dh * dh));
+  wg_fork();
+  gst = s_wg;
   TRY(gemm(lin_wgrad(dqkv, st.u, M, 3 * h, h, g32(o.w_qkv), acc), 2 * dM * 3 * dh * dh));
-  KCHK(colsum(dqkv, nullptr, nullptr, nullptr, M, 3 * h, cs_ws, g32(o.b_qkv), nullptr, acc, s_comp));
-  // LN1: din = dx1 + LN1'(du)
+  gst = s_comp;
+  KCHK(colsum(dqkv, nullptr, nullptr, nullptr, M, 3 * h, cs_ws, g32(o.b_qkv), nullptr, acc, s_wg));
+  wg_note(dqkv);
+  TRY(gemm(lin_dgrad(dqkv, p16(o.w_qkv), M, 3 * h, h, du), 2 * dM * 3 * dh * dh));
+  // LN1: din = dx1 + LN1'(du)   (din is the buffer the layer above read as dout)
+  wg_guard(din);
   KCHK(ln_bwd(du, x, st.mean1, st.rstd1, M, h, p16(o.ln1_g), dx1, din, s_comp));
   KCHK(colsum(du, x, st.mean1, st.rstd1, M, h, cs_ws, g32(o.ln1_b), g32(o.ln1_g), acc, s_comp));
   return 0;
@@ -286,8 +333,11 @@ int Ctx::backward(Slot& sl, int mb, const void* dout) {
   void* nxt = dh1;
   if (last) {
     const void* xL = nl > 0 ? sl.L[nl - 1].out : sl.in;
-    TRY(gemm(lin_dgrad(logits, p16(head_w), M, V, h, du), 2.0 * M * V * h));
+    wg_fork();
+    gst = s_wg;
     TRY(gemm(lin_wgrad(logits, sl.hf, M, V, h, g32(head_w), acc), 2.0 * M * V * h));
+    gst = s_comp;
+    TRY(gemm(lin_dgrad(logits, p16(head_w), M, V, h, du), 2.0 * M * V * h));
     KCHK(ln_bwd(du, xL, sl.meanf, sl.rstdf, M, h, p16(lnf_g), nullptr, cur, s_comp));
     KCHK(colsum(du, xL, sl.meanf, sl.rstdf, M, h, cs_ws, g32(lnf_b), g32(lnf_g), acc, s_comp));
   } else {
@@ -308,6 +358,7 @@ int Ctx::backward(Slot& sl, int mb, const void* dout) {
     // embedding gradients (fp32, zeroed at batch start): deterministic scatter-add
     KCHK(embed_bwd(tok, s + 1, b, s, h, V, cur, g32(tok_emb), g32(pos_emb), s_comp));
   }
+  wg_join();   // stash, logits and gradient buffers are reused by the next microbatch
   ++bwd_count;
   return 0;
 }
