@@ -154,6 +154,9 @@ struct Ctx {
   void wg_note(const void* buf);        // s_wg reads buf (recorded after its last enqueued read)
   void wg_guard(const void* buf);       // s_comp waits before overwriting buf
   void wg_join();                       // s_comp waits for all of s_wg
+  // the profiled microbatch runs its weight gradients in order on s_comp so the CUDA-event
+  // duration of every K1 launch is its own (overlapped launches would share the GPU)
+  cudaStream_t wgs() const { return prof_mb ? s_comp : s_wg; }
 };
 
 }  // namespace axonn

@@ -190,10 +190,10 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   // s_wg still reads.
   // FC2: dpre = (dout W2) * GeLU'(pre);  dW2 += dout^T act;  db2 += colsum(dout)
   wg_fork();
-  gst = s_wg;
+  gst = wgs();
   TRY(gemm(lin_wgrad(dout, st.act, M, h, 4 * h, g32(o.w_fc2), acc), 2 * dM * 4 * dh * dh));
   gst = s_comp;
-  KCHK(colsum(dout, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_fc2), nullptr, acc, s_wg));
+  KCHK(colsum(dout, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_fc2), nullptr, acc, wgs()));
   wg_note(dout);
   wg_guard(dpre);
   {
@@ -203,10 +203,10 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   }
   // FC1: du = dpre W1;  dW1 += dpre^T w;  db1 += colsum(dpre)
   wg_fork();
-  gst = s_wg;
+  gst = wgs();
   TRY(gemm(lin_wgrad(dpre, st.w, M, 4 * h, h, g32(o.w_fc1), acc), 2 * dM * 4 * dh * dh));
   gst = s_comp;
-  KCHK(colsum(dpre, nullptr, nullptr, nullptr, M, 4 * h, cs_ws, g32(o.b_fc1), nullptr, acc, s_wg));
+  KCHK(colsum(dpre, nullptr, nullptr, nullptr, M, 4 * h, cs_ws, g32(o.b_fc1), nullptr, acc, wgs()));
   wg_note(dpre);
   TRY(gemm(lin_dgrad(dpre, p16(o.w_fc1), M, 4 * h, h, du), 2 * dM * 4 * dh * dh));
   // LN2: dx1 = dout + LN2'(du);  dg2, db2
@@ -215,10 +215,10 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   KCHK(colsum(du, st.x1, st.mean2, st.rstd2, M, h, cs_ws, g32(o.ln2_b), g32(o.ln2_g), acc, s_comp));
   // proj: dO = dx1 Wo;  dWo += dx1^T o;  dbo += colsum(dx1)
   wg_fork();
-  gst = s_wg;
+  gst = wgs();
   TRY(gemm(lin_wgrad(dx1, st.o, M, h, h, g32(o.w_o), acc), 2 * dM * dh * dh));
   gst = s_comp;
-  KCHK(colsum(dx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, s_wg));
+  KCHK(colsum(dx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, wgs()));
   wg_note(dx1);
   {
     GemmArgs g = lin_dgrad(dx1, p16(o.w_o), M, h, h, dO);
@@ -284,10 +284,10 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   }
   // QKV: du = dqkv Wqkv;  dWqkv += dqkv^T u;  dbqkv += colsum(dqkv)
   wg_fork();
-  gst = s_wg;
+  gst = wgs();
   TRY(gemm(lin_wgrad(dqkv, st.u, M, 3 * h, h, g32(o.w_qkv), acc), 2 * dM * 3 * dh * dh));
   gst = s_comp;
-  KCHK(colsum(dqkv, nullptr, nullptr, nullptr, M, 3 * h, cs_ws, g32(o.b_qkv), nullptr, acc, s_wg));
+  KCHK(colsum(dqkv, nullptr, nullptr, nullptr, M, 3 * h, cs_ws, g32(o.b_qkv), nullptr, acc, wgs()));
   wg_note(dqkv);
   TRY(gemm(lin_dgrad(dqkv, p16(o.w_qkv), M, 3 * h, h, du), 2 * dM * 3 * dh * dh));
   // LN1: din = dx1 + LN1'(du)   (din is the buffer the layer above read as dout)
@@ -334,7 +334,7 @@ int Ctx::backward(Slot& sl, int mb, const void* dout) {
   if (last) {
     const void* xL = nl > 0 ? sl.L[nl - 1].out : sl.in;
     wg_fork();
-    gst = s_wg;
+    gst = wgs();
     TRY(gemm(lin_wgrad(logits, sl.hf, M, V, h, g32(head_w), acc), 2.0 * M * V * h));
     gst = s_comp;
     TRY(gemm(lin_dgrad(logits, p16(head_w), M, V, h, du), 2.0 * M * V * h));
