@@ -367,11 +367,57 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // issues M=256 N=256 K=16 MMAs reading both CTAs' shared memory, accumulating
 // 128 lanes x 256 fp32 columns in each CTA's TMEM (double-buffered: 512 columns).
 // Per-SM smem traffic per MMA is half the 1-CTA 128x256 tile's.
+//
+// TE (TMA epilogue): each epilogue warp drains its 32 rows x 128 columns through two
+// 4 KB SWIZZLE_128B staging boxes in shared memory and writes them with TMA stores
+// (bf16) or TMA reduce-adds performed in L2 (fp32 weight-gradient accumulation, D-20),
+// so no thread issues a strided global access; residual / GeLU pre-activation inputs
+// arrive the same way (TMA loads into the staging boxes, prefetched before the tile's
+// accumulator is ready).
 constexpr int STAGES2 = 6;
-template <int BN>
+constexpr int STAGES2_TE = 5;
+constexpr int TE_BOX = 4096;                       // 32 rows x 128 B
+constexpr int TE_SMEM = EPI_WARPS * 2 * TE_BOX;    // two boxes per epilogue warp
+
+__device__ __forceinline__ void ld8_bias(const __nv_bfloat16* bias, int col, int N, float* f) {
+  if (col + 8 <= N) {
+    uint4 u = __ldg(reinterpret_cast<const uint4*>(bias + col));
+    const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 t = __bfloat1622float2(hh[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = col + i < N ? __bfloat162float(bias[col + i]) : 0.f;
+  }
+}
+__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
+  const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(hh[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  uint4 u;
+  __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) hh[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+
+template <int BN, bool TE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap mapA,
-                           const __grid_constant__ CUtensorMap mapB, const GemmParams p) {
+                           const __grid_constant__ CUtensorMap mapB, const GemmParams p,
+                           const __grid_constant__ CUtensorMap mapC,
+                           const __grid_constant__ CUtensorMap mapX) {
+  constexpr int NST = TE ? STAGES2_TE : STAGES2;
   constexpr int TBM = 2 * BM;                 // 256 rows per pair
   constexpr int A_BYTES = BM * BK * 2;        // this CTA's 128 rows
   constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's BN/2 rows
@@ -379,11 +425,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   constexpr uint32_t TMEM_COLS = 2 * BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE_BYTES);
-  uint64_t* empty = full + STAGES2;
-  uint64_t* tfull = empty + STAGES2;
+  uint8_t* stg_all = smem + NST * STAGE_BYTES;          // TE staging boxes (1024-aligned)
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg_all + (TE ? TE_SMEM : 0));
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ebar = tempty + 2;                          // TE: one input barrier per epilogue warp
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ebar + EPI_WARPS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_ctarank();
@@ -392,7 +440,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapA);
     tma_prefetch_desc(&mapB);
-    for (int s = 0; s < STAGES2; ++s) {
+    if (TE) {
+      tma_prefetch_desc(&mapC);
+      tma_prefetch_desc(&mapX);
+    }
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -400,6 +452,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * EPI_WARPS);   // epilogue warps of both CTAs
     }
+    for (int w = 0; w < EPI_WARPS; ++w) mbar_init(&ebar[w], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_pair<TMEM_COLS>(tmem_holder);
@@ -438,7 +491,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             for (int j = 0; j < BN / 128; ++j)
               tma_load_4d_pair(sB + j * 8192, &mapB, &full[stage], bn + 64 * j, k0, z1, z2);
           }
-          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -470,13 +523,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             mma_bf16_ss_pair(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           mma_commit_pair(&empty[stage]);
-          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         mma_commit_pair(&tfull[acc]);
         ++it;
       }
     }
-  } else {
+  } else if (!TE) {
     const int q = warp & 3;
     const int cpart = (warp - 2) / 4;
     constexpr int CW = BN / (EPI_WARPS / 4);
@@ -502,6 +555,145 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
       ++it;
     }
+  } else {
+    // ---------------- TMA epilogue: warp (q, cpart) owns rows [32 q, +32) x columns
+    // [cpart * BN/2, +BN/2) of this CTA's 128 x BN accumulator.
+    const int q = warp & 3, cpart = (warp - 2) / 4, wi = warp - 2;
+    constexpr int CW = BN / 2;
+    static_assert(CW == 128 || CW == 64, "TE epilogue: 64 or 128 columns per warp");
+    uint8_t* box0 = stg_all + wi * 2 * TE_BOX;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    const bool f32 = p.epi == EPI_F32;
+    const bool gelu = p.epi == EPI_BIAS_GELU;
+    const bool has_in = p.epi == EPI_DGELU || (p.epi == EPI_BF16 && p.resid != nullptr);
+    const int sw = lane & 7;
+    uint8_t* my_row0 = box0 + lane * 128;
+    uint32_t ephase = 0;
+    int it = 0;
+    for (int t = pair; t < p.total; t += npairs) {
+      int z, m0, n0, kb0, kb1;
+      if (!tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int row0 = m0 + (int)rank * BM + q * 32;
+      const int cb = n0 + cpart * CW;
+      if (has_in && lane == 0) {   // residual / pre-activation boxes, before the accumulator
+        bulk_wait_read<0>();
+        mbar_arrive_expect_tx(&ebar[wi], (CW / 64) * TE_BOX);
+#pragma unroll
+        for (int g = 0; g < CW / 64; ++g) tma_load_2d(box0 + g * TE_BOX, &mapX, &ebar[wi], cb + 64 * g, row0);
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + cpart * CW;
+      if (f32) {
+#pragma unroll 1
+        for (int g = 0; g < CW / 32; ++g) {   // 32 fp32 columns = one 128-byte box row
+          uint32_t r[32];
+          tmem_ld32(tb + 32 * g, r);
+          if (g == CW / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+          }
+          uint8_t* row = my_row0 + (g & 1) * TE_BOX;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 o = make_float4(__uint_as_float(r[4 * j]) * p.alpha, __uint_as_float(r[4 * j + 1]) * p.alpha,
+                                   __uint_as_float(r[4 * j + 2]) * p.alpha, __uint_as_float(r[4 * j + 3]) * p.alpha);
+            *reinterpret_cast<float4*>(row + ((j ^ sw) << 4)) = o;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (p.accumulate) tma_reduce_add_2d(&mapC, box0 + (g & 1) * TE_BOX, cb + 32 * g, row0);
+            else tma_store_2d(&mapC, box0 + (g & 1) * TE_BOX, cb + 32 * g, row0);
+            bulk_commit();
+          }
+        }
+      } else {
+        if (has_in) {
+          mbar_wait(&ebar[wi], ephase);
+          ephase ^= 1;
+        }
+#pragma unroll 1
+        for (int g = 0; g < CW / 64; ++g) {   // 64 bf16 columns = one 128-byte box row
+          uint32_t r0[32], r1[32];
+          tmem_ld32_nowait(tb + 64 * g, r0);
+          tmem_ld32_nowait(tb + 64 * g + 32, r1);
+          tmem_ld_wait();
+          if (g == CW / 64 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+          }
+          // gelu: pre -> box 0, act -> box 1 (ring of two commits); else box g (in place)
+          uint8_t* rowA = my_row0 + (gelu ? 0 : g) * TE_BOX;
+          uint8_t* rowB = my_row0 + TE_BOX;
+          if (!has_in) {   // gelu rewrites both boxes; otherwise the other box may be in flight
+            if (lane == 0) {
+              if (gelu) bulk_wait_read<0>();
+              else bulk_wait_read<1>();
+            }
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              v[i] = __uint_as_float(j < 4 ? r0[8 * j + i] : r1[8 * (j - 4) + i]) * p.alpha;
+            const int col = cb + 64 * g + 8 * j;
+            if (p.bias) {
+              float b8[8];
+              ld8_bias(p.bias, col, p.N, b8);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] += b8[i];
+            }
+            uint4* slot = reinterpret_cast<uint4*>(rowA + ((j ^ sw) << 4));
+            if (gelu) {
+              const uint4 pre = pack8(v);
+              *slot = pre;
+              unpack8(pre, v);   // GeLU of the same rounded value
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = gelu_f(v[i]);
+              *reinterpret_cast<uint4*>(rowB + ((j ^ sw) << 4)) = pack8(v);
+            } else {
+              float in8[8];
+              if (has_in) {
+                unpack8(*slot, in8);
+                if (p.epi == EPI_DGELU) {
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_f(in8[i]);
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) v[i] += in8[i];
+                }
+              }
+              *slot = pack8(v);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (gelu) {
+              tma_store_2d(&mapX, box0, cb + 64 * g, row0);            // pre-activation
+              bulk_commit();
+              tma_store_2d(&mapC, box0 + TE_BOX, cb + 64 * g, row0);   // GeLU
+              bulk_commit();
+            } else {
+              tma_store_2d(&mapC, box0 + g * TE_BOX, cb + 64 * g, row0);
+              bulk_commit();
+            }
+          }
+        }
+      }
+      ++it;
+    }
+    if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   cluster_sync();
@@ -1231,25 +1423,75 @@ static int launch_bn(const GemmArgs& g, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
-template <int BN>
+// 2-D map over a row-major [rows][ld] matrix for the TMA epilogue: box = 32 rows x 128 B
+// (64 bf16 or 32 fp32 columns), SWIZZLE_128B to match the staging layout.
+static int make_map_epi(CUtensorMap* map, const void* base, long long cols, long long rows,
+                        long long ld, bool f32) {
+  PFN_encodeTiled_t enc = get_encoder();
+  if (!enc) return -1;
+  const int es = f32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * es) % 16) return -2;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / es), 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -3;
+}
+
+static bool al16h(const void* p, long long ld, int es) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * es) % 16 == 0;
+}
+
+// The TMA epilogue covers the linear layers: one batch, no column remap, every output
+// column valid, 16-byte aligned bases and row pitches.
+static bool te_eligible(const GemmArgs& g) {
+  if (g.Z != 1 || g.col_group_in != 0 || (g.n_valid > 0 && g.n_valid < g.N)) return false;
+  if (g.epi == EPI_F32) return al16h(g.C, g.ldc, 4);
+  if (g.epi != EPI_BF16 && g.epi != EPI_BIAS_GELU && g.epi != EPI_DGELU) return false;
+  if (!al16h(g.C, g.ldc, 2)) return false;
+  if (g.bias && (reinterpret_cast<uintptr_t>(g.bias) & 15)) return false;
+  if ((g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) && !al16h(g.aux, g.ld_aux, 2)) return false;
+  if (g.epi == EPI_BF16 && g.resid && !al16h(g.resid, g.ld_resid, 2)) return false;
+  if ((g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) && g.resid) return false;
+  return true;
+}
+
+static int g_te_mode = -1;   // AXONN_GEMM_TE=0 disables the TMA epilogue
+
+template <int BN, bool TE>
 static int launch_pair(const GemmArgs& g, cudaStream_t st) {
-  constexpr int SMEM = STAGES2 * (BM * BK * 2 + (BN / 2) * BK * 2) + 1024 + 256;
+  constexpr int NST = TE ? STAGES2_TE : STAGES2;
+  constexpr int SMEM = NST * (BM * BK * 2 + (BN / 2) * BK * 2) + (TE ? TE_SMEM : 0) + 1024 + 256;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN>,
+    if (cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, TE>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
       return -10;
     attr_set = true;
   }
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc, mx;
   int rc = make_maps(ma, mb, g, BM, BN / 2);
   if (rc) return rc;
+  memset(&mc, 0, sizeof(mc));
+  memset(&mx, 0, sizeof(mx));
+  if (TE) {
+    rc = make_map_epi(&mc, g.C, g.N, g.M, g.ldc, g.epi == EPI_F32);
+    if (!rc && (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU))
+      rc = make_map_epi(&mx, g.aux, g.N, g.M, g.ld_aux, false);
+    else if (!rc && g.resid)
+      rc = make_map_epi(&mx, g.resid, g.N, g.M, g.ld_resid, false);
+    if (rc) return rc;
+  }
   GemmParams p;
   fill_params(p, g, 2 * BM, BN);
   int pairs_avail = g_num_sms / 2;
   if (g.max_ctas > 0 && pairs_avail > g.max_ctas / 2) pairs_avail = g.max_ctas / 2;
   int pairs = p.total < pairs_avail ? p.total : pairs_avail;
-  gemm_bf16_tcgen05_pair<BN><<<2 * pairs, GEMM_THREADS, SMEM, st>>>(ma, mb, p);
+  gemm_bf16_tcgen05_pair<BN, TE><<<2 * pairs, GEMM_THREADS, SMEM, st>>>(ma, mb, p, mc, mx);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
@@ -1295,10 +1537,15 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   // per-SM A traffic of 128 x 128 single-CTA tiles
   // (measured: 36 us vs 30 us for the single-CTA 128 x 128 tiles at the 1.3B attention shape,
   // so narrow GEMMs use the pair only when forced with variant 2)
-  if (g.N <= 128 && g.M >= 256 && g.variant == 2) return launch_pair<128>(g, st);
+  if (g_te_mode < 0) {
+    const char* e = getenv("AXONN_GEMM_TE");
+    g_te_mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (g.N <= 128 && g.M >= 256 && g.variant == 2) return launch_pair<128, false>(g, st);
   if (g.variant == 1 || (g.variant == 0 && (g.N <= 128 || !g_pair_mode || g.M <= 128)))
     return g.N <= 128 ? launch_bn<128>(g, st) : launch_bn<256>(g, st);
-  return launch_pair<256>(g, st);
+  if (g_te_mode && g.variant != 3 && te_eligible(g)) return launch_pair<256, true>(g, st);
+  return launch_pair<256, false>(g, st);
 }
 
 }  // namespace axonn
@@ -1307,8 +1554,9 @@ namespace axonn {
 int preload_gemm() {   // see preload_ops (ops.cu)
   cudaFuncAttributes a;
   const void* fns[] = {(const void*)gemm_bf16_tcgen05<128>, (const void*)gemm_bf16_tcgen05<256>,
-                       (const void*)gemm_bf16_tcgen05_pair<256>,
-                       (const void*)gemm_bf16_tcgen05_pair<128>, (const void*)gemm_rowsoftmax};
+                       (const void*)gemm_bf16_tcgen05_pair<256, false>,
+                       (const void*)gemm_bf16_tcgen05_pair<256, true>,
+                       (const void*)gemm_bf16_tcgen05_pair<128, false>, (const void*)gemm_rowsoftmax};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
   return 0;

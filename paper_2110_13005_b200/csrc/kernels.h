@@ -31,7 +31,7 @@ struct GemmArgs {
   long long ld_aux;
   float alpha;
   int max_ctas;
-  int variant;          // 0 auto, 1 single CTA, 2 CTA pair
+  int variant;          // 0 auto, 1 single CTA, 2 CTA pair (TMA epilogue when eligible), 3 CTA pair, thread-store epilogue
 };
 
 int gemm_launch(const GemmArgs& g, cudaStream_t st);
