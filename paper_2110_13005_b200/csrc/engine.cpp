@@ -203,12 +203,19 @@ static int plan_memory(Ctx* c) {
     return c->fail(AXONN_ERR_CUDA, "memset dO");
   c->du = c->dalloc(Mh * 2);
   c->dx1 = c->dalloc(Mh * 2);
-  c->cs_ws = (float*)c->dalloc((size_t)2 * colsum_chunks(c->M) * 4 * c->h * 4);
+  // column-sum workspaces (tickets + partials): one for the bias sums on s_wg, one for the
+  // LayerNorm parameter sums on s_comp (the two streams run concurrently)
+  const size_t cs_bytes = 4096 + (size_t)2 * colsum_chunks(c->M) * 4 * c->h * 4;
+  c->cs_ws = (float*)c->dalloc(cs_bytes);
+  c->cs_ws_ln = (float*)c->dalloc(cs_bytes);
+  if (c->cs_ws && c->cs_ws_ln &&
+      (cudaMemset(c->cs_ws, 0, 4096) != cudaSuccess || cudaMemset(c->cs_ws_ln, 0, 4096) != cudaSuccess))
+    return c->fail(AXONN_ERR_CUDA, "memset colsum tickets");
   c->row_loss = (float*)c->dalloc(c->M * 4);
   c->d_loss = (double*)c->dalloc(64);
   if (c->last) c->logits = c->dalloc((size_t)c->M * c->V * 2);
   if (!c->S || !c->dS || !c->dh0 || !c->dh1 || !c->dqkv || !c->dpre || !c->dO || !c->du ||
-      !c->dx1 || !c->cs_ws || !c->row_loss || !c->d_loss || (c->last && !c->logits))
+      !c->dx1 || !c->cs_ws || !c->cs_ws_ln || !c->row_loss || !c->d_loss || (c->last && !c->logits))
     return c->fail(AXONN_ERR_OOM, "workspace allocation");
   if (cudaMallocHost(&c->h_loss, 64) != cudaSuccess) return c->fail(AXONN_ERR_OOM, "pinned loss");
   // parameters, gradients, optimizer state

@@ -85,7 +85,8 @@ struct Ctx {
   void* dS = nullptr;                 // bf16 [b a s s]
   void *dh0 = nullptr, *dh1 = nullptr, *dqkv = nullptr, *dpre = nullptr, *dO = nullptr,
        *du = nullptr, *dx1 = nullptr;
-  float* cs_ws = nullptr;             // column-sum workspace
+  float* cs_ws = nullptr;             // column-sum workspace (bias sums, s_wg)
+  float* cs_ws_ln = nullptr;          // column-sum workspace (LayerNorm sums, s_comp)
   void* logits = nullptr;             // [M, V] bf16 (last stage)
   float* row_loss = nullptr;
   double* d_loss = nullptr;           // device loss accumulator

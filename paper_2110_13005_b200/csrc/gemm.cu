@@ -473,6 +473,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const int bn = n0 + (int)rank * (BN / 2);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (p.dbg == 7) {   // experiment: no operand traffic (MMA on stale smem)
+            if (leader) mbar_arrive(&full[stage]);
+            if (++stage == NST) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
           uint8_t* sA = smem + stage * STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
@@ -587,7 +592,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + cpart * CW;
-      if (f32) {
+      if (p.dbg == 8) {   // experiment: no epilogue work
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      } else if (f32) {
 #pragma unroll 1
         for (int g = 0; g < CW / 32; ++g) {   // 32 fp32 columns = one 128-byte box row
           uint32_t r[32];
@@ -1488,6 +1497,14 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
   }
   GemmParams p;
   fill_params(p, g, 2 * BM, BN);
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("AXONN_GEMM_DBG");
+      dbg = e ? atoi(e) : 0;
+    }
+    p.dbg = dbg;
+  }
   int pairs_avail = g_num_sms / 2;
   if (g.max_ctas > 0 && pairs_avail > g.max_ctas / 2) pairs_avail = g.max_ctas / 2;
   int pairs = p.total < pairs_avail ? p.total : pairs_avail;

@@ -418,17 +418,112 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
   }
 }
 
+// Column sums over a 2-D grid: block (bx, by) sums rows [256 by, +256) of columns
+// [64 bx, +64) (8 column groups x 16-byte loads = 128 contiguous bytes per row, 32 row
+// lanes), writes its partial, and the LAST block of each column slab (atomic ticket)
+// adds the partials in ascending row-chunk order -> one launch, bitwise reproducible.
+// workspace: [0, 4 KB) zero-initialised tickets, then 2 x R x n fp32 partials.
+constexpr int CS2_ROWS = 256;
+__global__ void __launch_bounds__(256) colsum2_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                      const __nv_bfloat16* __restrict__ x,
+                                                      const float* __restrict__ mean,
+                                                      const float* __restrict__ rstd, int rows,
+                                                      int n, float* __restrict__ part,
+                                                      unsigned* __restrict__ ticket,
+                                                      float* __restrict__ out_b,
+                                                      float* __restrict__ out_g, int accumulate) {
+  const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
+  const int c = blockIdx.x * 64 + cg * 8;
+  const int r0 = blockIdx.y * CS2_ROWS, r1 = min(rows, r0 + CS2_ROWS);
+  const int R = gridDim.y;
+  float sb[8], sg[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sb[i] = sg[i] = 0.f;
+  if (c < n) {
+    int r = r0 + rl;
+    for (; r + 3 * 32 < r1; r += 4 * 32) {
+      float d[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load8(dy + (long long)(r + u * 32) * n + c, d[u]);
+      if (x) {
+        float xv[4][8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) load8(x + (long long)(r + u * 32) * n + c, xv[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float mu = mean[r + u * 32], rs = rstd[r + u * 32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) sg[i] += d[u][i] * ((xv[u][i] - mu) * rs);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sb[i] += d[u][i];
+    }
+    for (; r < r1; r += 32) {
+      float d[8];
+      load8(dy + (long long)r * n + c, d);
+      if (x) {
+        float xv[8];
+        load8(x + (long long)r * n + c, xv);
+        const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sg[i] += d[i] * ((xv[i] - mu) * rs);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sb[i] += d[i];
+    }
+  }
+  __shared__ float sh[2][32][65];
+  __shared__ unsigned last;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    sh[0][rl][cg * 8 + i] = sb[i];
+    sh[1][rl][cg * 8 + i] = sg[i];
+  }
+  __syncthreads();
+  const int which = threadIdx.x >> 6, col = threadIdx.x & 63;   // threads 0..127
+  const int gc = blockIdx.x * 64 + col;
+  const bool act = threadIdx.x < 128 && gc < n && (which == 0 || x);
+  float acc = 0.f;
+  if (act) {
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) acc += sh[which][k][col];
+  }
+  float* o = which == 0 ? out_b : out_g;
+  if (R == 1) {
+    if (act) o[gc] = accumulate ? o[gc] + acc : acc;
+    return;
+  }
+  if (act) part[((long long)which * R + blockIdx.y) * n + gc] = acc;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&ticket[blockIdx.x], 1u) == (unsigned)(R - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (act) {
+    float s = 0.f;
+    for (int k = 0; k < R; ++k) s += __ldcg(&part[((long long)which * R + k) * n + gc]);
+    o[gc] = accumulate ? o[gc] + s : s;
+  }
+  if (threadIdx.x == 0) ticket[blockIdx.x] = 0;
+}
+
 int colsum(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int n,
            float* workspace, float* out_b, float* out_g, int accumulate, cudaStream_t st) {
-  if (n % 8 == 0) {
-    (void)workspace;
-    colsum_kernel<<<(n + 31) / 32, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
-                                                 mean, rstd, rows, n, out_b, out_g, accumulate);
+  if (n % 8 == 0 && (n + 63) / 64 <= 1024) {
+    dim3 grid((n + 63) / 64, (rows + CS2_ROWS - 1) / CS2_ROWS);
+    unsigned* ticket = reinterpret_cast<unsigned*>(workspace);
+    float* part = workspace + 1024;
+    colsum2_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean,
+                                         rstd, rows, n, part, ticket, out_b, out_g, accumulate);
     return ok();
   }
   int nch = colsum_chunks(rows);
-  float* part_b = workspace;
-  float* part_g = workspace + (long long)nch * n;
+  float* part_b = workspace + 1024;
+  float* part_g = part_b + (long long)nch * n;
   dim3 grid((n + 63) / 64, nch);
   colsum_partial_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
                                               mean, rstd, rows, n, part_b, part_g);
@@ -654,7 +749,7 @@ int preload_ops() {
   const void* fns[] = {(const void*)embed_fwd_kernel, (const void*)embed_bwd_tok_kernel,
                        (const void*)embed_bwd_pos_kernel, (const void*)ln_fwd_kernel,
                        (const void*)ln_bwd_kernel, (const void*)colsum_partial_kernel,
-                       (const void*)colsum_final_kernel, (const void*)colsum_kernel,
+                       (const void*)colsum_final_kernel, (const void*)colsum_kernel, (const void*)colsum2_kernel,
                        (const void*)softmax_fwd_kernel,
                        (const void*)softmax_bwd_kernel, (const void*)xent_kernel,
                        (const void*)reduce_sum_kernel, (const void*)cast_f32_bf16_kernel,

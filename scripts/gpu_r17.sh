@@ -1,0 +1,6 @@
+set -x; mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()"
+timeout 600 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_step.py -q -m gpu -x > gpurun_out/gpu_tests.log 2>&1; echo "exit $?" >> gpurun_out/gpu_tests.log
+tail -3 gpurun_out/gpu_tests.log
+for d in 0 7 8; do for s in "fc1 fwd plain" "fc1 dgrad" "fc2 wgrad"; do AXONN_GEMM_DBG=$d DIAG_ONLY="$s" timeout 120 python scripts/diag_sustained.py >> gpurun_out/diag_dbg$d.jsonl 2>>gpurun_out/diag_dbg.err; done; done
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_1p3b.log 2>&1; echo "exit $?" >> gpurun_out/bench_1p3b.log
