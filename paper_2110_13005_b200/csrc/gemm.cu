@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {   // whole warp runs the loop; one elected lane issues the TMA copies
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
@@ -272,31 +272,40 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int z1 = z % p.Z1, z2 = z / p.Z1;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          uint8_t* sA = smem + stage * STAGE_BYTES;
-          uint8_t* sB = sA + A_BYTES;
-          const int k0 = kb * BK;
-          if (!p.a_mn) {
-            tma_load_4d(sA, &mapA, &full[stage], k0, m0, z1, z2);
-          } else {
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            uint8_t* sA = smem + stage * STAGE_BYTES;
+            uint8_t* sB = sA + A_BYTES;
+            const int k0 = kb * BK;
+            if (!p.a_mn) {
+              tma_load_4d(sA, &mapA, &full[stage], k0, m0, z1, z2);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_4d(sA + j * 8192, &mapA, &full[stage], m0 + 64 * j, k0, z1, z2);
-          }
-          if (!p.b_mn) {
-            tma_load_4d(sB, &mapB, &full[stage], k0, n0, z1, z2);
-          } else {
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_4d(sA + j * 8192, &mapA, &full[stage], m0 + 64 * j, k0, z1, z2);
+            }
+            if (!p.b_mn) {
+              tma_load_4d(sB, &mapB, &full[stage], k0, n0, z1, z2);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_4d(sB + j * 8192, &mapB, &full[stage], n0 + 64 * j, k0, z1, z2);
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_4d(sB + j * 8192, &mapB, &full[stage], n0 + 64 * j, k0, z1, z2);
+            }
           }
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // whole warp runs the loop; one elected lane issues the MMAs
       const uint32_t idesc = umma_idesc_bf16(BM, BN, p.a_mn, p.b_mn);
+      const uint32_t s0 = smem_u32(smem);
+      const uint64_t a_d0 = p.a_mn ? umma_desc_sw128(s0, 8192, 1024) : umma_desc_sw128(s0, 16, 1024);
+      const uint64_t b_d0 = p.b_mn ? umma_desc_sw128(s0 + A_BYTES, 8192, 1024)
+                                   : umma_desc_sw128(s0 + A_BYTES, 16, 1024);
+      const uint64_t a_k = p.a_mn ? (2048 >> 4) : (32 >> 4);
+      const uint64_t b_k = p.b_mn ? (2048 >> 4) : (32 >> 4);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -311,20 +320,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(smem + stage * STAGE_BYTES);
-          const uint32_t b_base = a_base + A_BYTES;
+          const uint64_t so = (uint64_t)((stage * STAGE_BYTES) >> 4);
+          const uint64_t ad = a_d0 + so, bd = b_d0 + so;
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            uint64_t ad = p.a_mn ? umma_desc_sw128(a_base + k * 2048, 8192, 1024)
-                                 : umma_desc_sw128(a_base + k * 32, 16, 1024);
-            uint64_t bd = p.b_mn ? umma_desc_sw128(b_base + k * 2048, 8192, 1024)
-                                 : umma_desc_sw128(b_base + k * 32, 16, 1024);
-            mma_bf16_ss(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_ss(tmem_d, ad + k * a_k, bd + k * b_k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            mma_commit(&empty[stage]);
           }
-          mma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);
+        if (elect_one()) mma_commit(&tfull[acc]);
+        __syncwarp();
         ++it;
       }
     }
@@ -462,7 +470,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {   // whole warp runs the loop; one elected lane issues the TMA copies
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < p.total; t += npairs) {
@@ -473,36 +481,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const int bn = n0 + (int)rank * (BN / 2);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (p.dbg == 7) {   // experiment: no operand traffic (MMA on stale smem)
-            if (leader) mbar_arrive(&full[stage]);
-            if (++stage == NST) { stage = 0; phase ^= 1; }
-            continue;
-          }
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
-          uint8_t* sA = smem + stage * STAGE_BYTES;
-          uint8_t* sB = sA + A_BYTES;
-          const int k0 = kb * BK;
-          if (!p.a_mn) {
-            tma_load_4d_pair(sA, &mapA, &full[stage], k0, am, z1, z2);
-          } else {
+          if (elect_one()) {
+            if (p.dbg == 7) {   // experiment: no operand traffic (MMA on stale smem)
+              if (leader) mbar_arrive(&full[stage]);
+            } else {
+              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+              uint8_t* sA = smem + stage * STAGE_BYTES;
+              uint8_t* sB = sA + A_BYTES;
+              const int k0 = kb * BK;
+              if (!p.a_mn) {
+                tma_load_4d_pair(sA, &mapA, &full[stage], k0, am, z1, z2);
+              } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_4d_pair(sA + j * 8192, &mapA, &full[stage], am + 64 * j, k0, z1, z2);
-          }
-          if (!p.b_mn) {
-            tma_load_4d_pair(sB, &mapB, &full[stage], k0, bn, z1, z2);
-          } else {
+                for (int j = 0; j < BM / 64; ++j)
+                  tma_load_4d_pair(sA + j * 8192, &mapA, &full[stage], am + 64 * j, k0, z1, z2);
+              }
+              if (!p.b_mn) {
+                tma_load_4d_pair(sB, &mapB, &full[stage], k0, bn, z1, z2);
+              } else {
 #pragma unroll
-            for (int j = 0; j < BN / 128; ++j)
-              tma_load_4d_pair(sB + j * 8192, &mapB, &full[stage], bn + 64 * j, k0, z1, z2);
+                for (int j = 0; j < BN / 128; ++j)
+                  tma_load_4d_pair(sB + j * 8192, &mapB, &full[stage], bn + 64 * j, k0, z1, z2);
+              }
+            }
           }
+          __syncwarp();
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {   // whole warp runs the loop; one elected lane issues (uniform registers)
       const uint32_t idesc = umma_idesc_bf16(TBM, BN, p.a_mn, p.b_mn);
+      // descriptors of stage 0 and the per-stage / per-k16 increments (address field = addr >> 4)
+      const uint32_t s0 = smem_u32(smem);
+      const uint64_t a_d0 = p.a_mn ? umma_desc_sw128(s0, 8192, 1024) : umma_desc_sw128(s0, 16, 1024);
+      const uint64_t b_d0 = p.b_mn ? umma_desc_sw128(s0 + A_BYTES, 8192, 1024)
+                                   : umma_desc_sw128(s0 + A_BYTES, 16, 1024);
+      const uint64_t a_k = p.a_mn ? (2048 >> 4) : (32 >> 4);
+      const uint64_t b_k = p.b_mn ? (2048 >> 4) : (32 >> 4);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -517,20 +534,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(smem + stage * STAGE_BYTES);
-          const uint32_t b_base = a_base + A_BYTES;
+          const uint64_t so = (uint64_t)((stage * STAGE_BYTES) >> 4);
+          const uint64_t ad = a_d0 + so, bd = b_d0 + so;
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            uint64_t ad = p.a_mn ? umma_desc_sw128(a_base + k * 2048, 8192, 1024)
-                                 : umma_desc_sw128(a_base + k * 32, 16, 1024);
-            uint64_t bd = p.b_mn ? umma_desc_sw128(b_base + k * 2048, 8192, 1024)
-                                 : umma_desc_sw128(b_base + k * 32, 16, 1024);
-            mma_bf16_ss_pair(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_ss_pair(tmem_d, ad + k * a_k, bd + k * b_k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            mma_commit_pair(&empty[stage]);
           }
-          mma_commit_pair(&empty[stage]);
+          __syncwarp();
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
-        mma_commit_pair(&tfull[acc]);
+        if (elect_one()) mma_commit_pair(&tfull[acc]);
+        __syncwarp();
         ++it;
       }
     }
@@ -1144,7 +1160,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
   const int nkb = (p.K + BK - 1) / BK;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {   // whole warp; elected lane issues
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
@@ -1154,18 +1170,22 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
         const int nh = kv > 256 ? 2 : 1;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], A_BYTES + nh * HALF_BYTES);
-          uint8_t* sA = smem + stage * STAGE_BYTES;
-          tma_load_4d(sA, &mapA, &full[stage], kb * BK, m0, z1, z2);
-          for (int hh = 0; hh < nh; ++hh)
-            tma_load_4d(sA + A_BYTES + hh * HALF_BYTES, &mapB, &full[stage], kb * BK, 256 * hh, z1, z2);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&full[stage], A_BYTES + nh * HALF_BYTES);
+            uint8_t* sA = smem + stage * STAGE_BYTES;
+            tma_load_4d(sA, &mapA, &full[stage], kb * BK, m0, z1, z2);
+            for (int hh = 0; hh < nh; ++hh)
+              tma_load_4d(sA + A_BYTES + hh * HALF_BYTES, &mapB, &full[stage], kb * BK, 256 * hh, z1, z2);
+          }
+          __syncwarp();
           if (++stage == RS_STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // whole warp; elected lane issues
       const uint32_t idesc = umma_idesc_bf16(BM, 256, 0, 0);
+      const uint64_t d0 = umma_desc_sw128(smem_u32(smem), 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -1178,19 +1198,22 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(smem + stage * STAGE_BYTES);
+          const uint64_t ad = d0 + (uint64_t)((stage * STAGE_BYTES) >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
-            for (int hh = 0; hh < nh; ++hh) {
-              uint64_t bd = umma_desc_sw128(a_base + A_BYTES + hh * HALF_BYTES + k * 32, 16, 1024);
-              mma_bf16_ss(tmem_base + 256 * hh, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              for (int hh = 0; hh < nh; ++hh) {
+                const uint64_t bd = ad + (uint64_t)((A_BYTES + hh * HALF_BYTES) >> 4);
+                mma_bf16_ss(tmem_base + 256 * hh, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              }
             }
+            mma_commit(&empty[stage]);
           }
-          mma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == RS_STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(tfull);
+        if (elect_one()) mma_commit(tfull);
+        __syncwarp();
       }
     }
   } else {

@@ -263,3 +263,17 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 }  // namespace axonn
+
+namespace axonn {
+// one lane of a converged warp (elect.sync): keeps the warp's values in uniform registers so
+// tcgen05 / TMA issue needs no per-instruction waterfall loop
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+}  // namespace axonn
