@@ -213,6 +213,28 @@ AXONN_API int axonn_k_gemm(const axonn_gemm_args* args, void* stream);
 AXONN_API int axonn_k_adamw(int64_t n, const void* g16, float* theta, float* m, float* v, void* theta16,
                   const float scalars[9], void* stream);
 
+/* K2: fused causal self-attention forward over one microbatch ("transformer
+ * kernel", SURVEY.md §8(a) A2 "causal MHA"; readings D-7 scale alpha = 1/sqrt(d), D-8 causal).
+ * qkv: bf16 [b*s][lq], lq = 3*heads*dp; Q of head n at columns [n*dp, n*dp+d), K at
+ * heads*dp + n*dp, V at 2*heads*dp + n*dp (pad columns d..dp-1 must be zero).
+ * o: bf16 [b*s][ldo], head n written to columns [n*d, (n+1)*d).
+ * lse: fp32 [b*heads*s] (index (sample*heads + head)*s + query): log2-domain row normaliser
+ * max_k(alpha*log2(e)*S) + log2(sum_k exp2(...)), consumed by the backward.
+ * Limits: s <= 512, dp even and dp <= 256, d even.  Device pointers; no allocation;
+ * returns 0 or a negative code (invalid shape / launch failure). */
+AXONN_API int axonn_k_attn_fwd(const void* qkv, int64_t lq, int b, int heads, int s, int d, int dp,
+                               float alpha, void* o, int64_t ldo, float* lse, void* stream);
+
+/* K2 backward (same passage and readings).  From dO (bf16 [b*s][heads*dp], head n at n*dp,
+ * pad columns zero), the forward's o and lse and the same qkv, writes into dqkv (bf16
+ * [b*s][ldq]): dQ at columns [n*d, ...), dK at h + n*d, dV at 2h + n*d (h = heads*d), with
+ * dS = alpha * P * (dP - D), D_i = dO_i . o_i.  P is recomputed from S and lse (never stored);
+ * every output element has one writer (no atomics: bitwise reproducible).  dbuf: fp32
+ * workspace of b*heads*s elements (receives D).  Same limits as axonn_k_attn_fwd. */
+AXONN_API int axonn_k_attn_bwd(const void* qkv, int64_t lq, const void* dO, const void* o, int64_t ldo,
+                               const float* lse, float* dbuf, int b, int heads, int s, int d, int dp,
+                               float alpha, void* dqkv, int64_t ldq, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,8 @@ def _declare(lib):
         "axonn_timer_elapsed": (I, [P, I, I, C.POINTER(C.c_double)]),
         "axonn_k_gemm": (I, [C.POINTER(GemmArgs), P]),
         "axonn_k_adamw": (I, [I64, P, P, P, P, P, C.POINTER(F), P]),
+        "axonn_k_attn_fwd": (I, [P, I64, I, I, I, I, I, F, P, I64, P, P]),
+        "axonn_k_attn_bwd": (I, [P, I64, P, P, I64, P, P, I, I, I, I, I, F, P, I64, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name, None)

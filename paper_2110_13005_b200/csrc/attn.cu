@@ -1,0 +1,733 @@
+// Fused causal self-attention on tcgen05 (sm_100a) for the stage forward (SURVEY.md §8(a) A2:
+// "causal MHA"; readings D-7 scale 1/sqrt(d), D-8 causal mask).
+//
+// One CTA tile = 128 queries of one (sample, head); all keys of the tile (kv <= 512) fit in
+// TMEM, so the softmax is exact (no online rescaling):
+//   1. S = Q K^T                     SS-MMA into TMEM columns [0, 512)      (fp32)
+//   2. softmax rows in the epilogue:  e = exp2(alpha log2e S - m), P = bf16(e) written BACK into
+//      TMEM (packed bf16 pairs: keys [0,256) -> columns [0,128), keys [256,512) -> [384,512))
+//   3. O = P V                       TS-MMA (A = P from TMEM, B = V from smem) into [128, 128+NV)
+//   4. O / sum -> bf16 -> o[token][head * d + j]; lse2 = m + log2(sum) per row for the backward.
+// Neither S nor P touches HBM.  Warp roles (320 threads, 1 CTA / SM, persistent over tiles):
+//   warp 0 TMA producer (Q, K, then V blocks through a 2-stage ring), warp 1 MMA issuer,
+//   warps 2..9 epilogue: warp pair (q, half) owns TMEM lane quarter q (32 query rows) and the
+//   key half [256 half, 256 half + 256).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace axonn {
+
+namespace {
+
+constexpr int QT = 128;                 // queries per tile
+constexpr int KB = 64;                  // head-dim block of the S = Q K^T mainloop
+constexpr int ATT_STAGES = 2;
+constexpr int Q_BYTES = QT * KB * 2;    // 16 KB
+constexpr int KH_BYTES = 256 * KB * 2;  // 32 KB (one key half)
+constexpr int ATT_STAGE = Q_BYTES + 2 * KH_BYTES;   // 80 KB: Q + K, or one V block (<= 32 KB)
+constexpr int ATT_THREADS = 64 + 8 * 32;
+
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// 32 lanes x 16 columns (32-bit) register -> TMEM
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void nbar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// TMEM column holding the packed P pair of key `key` (two keys per 32-bit column)
+__device__ __forceinline__ uint32_t p_col(int key) {
+  return key < 256 ? (uint32_t)(key >> 1) : (uint32_t)(256 + (key >> 1));
+}
+
+struct AttnParams {
+  int s, heads, d, nv, num_m, total;
+  float c1;               // alpha * log2(e)
+  __nv_bfloat16* o;
+  long long ldo;
+  float* lse;
+};
+
+__global__ void __launch_bounds__(ATT_THREADS, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
+                    const __grid_constant__ CUtensorMap mapV, const AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ATT_STAGES * ATT_STAGE);
+  uint64_t* empty = full + ATT_STAGES;
+  uint64_t* s_full = empty + ATT_STAGES;
+  uint64_t* p_ready = s_full + 1;
+  uint64_t* o_full = p_ready + 1;
+  uint64_t* t_free = o_full + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_free + 1);
+  __shared__ float red[2][2][128];          // [max|sum][half][row]
+  __shared__ uint4 stg_all[8][32 * 4];      // per epilogue warp: 32 rows x 32 bf16
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nkd = (p.nv + KB - 1) / KB;     // head-dim blocks (dp <= nv, OOB zero-filled)
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapQ);
+    tma_prefetch_desc(&mapK);
+    tma_prefetch_desc(&mapV);
+    for (int i = 0; i < ATT_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(o_full, 1);
+    mbar_init(p_ready, 8);
+    mbar_init(t_free, 8);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
+      const int z = t / p.num_m, m0 = (p.num_m - 1 - t % p.num_m) * QT;
+      const int z1 = z % p.heads, z2 = z / p.heads;
+      const int kv = min(p.s, m0 + QT);
+      const int nh = kv > 256 ? 2 : 1;
+      for (int kb = 0; kb < nkd; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&full[stage], Q_BYTES + nh * KH_BYTES);
+          uint8_t* sQ = smem + stage * ATT_STAGE;
+          tma_load_4d(sQ, &mapQ, &full[stage], kb * KB, m0, z1, z2);
+          for (int hh = 0; hh < nh; ++hh)
+            tma_load_4d(sQ + Q_BYTES + hh * KH_BYTES, &mapK, &full[stage], kb * KB, 256 * hh, z1, z2);
+        }
+        __syncwarp();
+        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
+      }
+      const int nvb = (kv + 63) / 64;
+      for (int j = 0; j < nvb; ++j) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&full[stage], (p.nv / 64) * 8192);
+          uint8_t* sV = smem + stage * ATT_STAGE;
+          for (int c = 0; c < p.nv / 64; ++c)
+            tma_load_4d(sV + c * 8192, &mapV, &full[stage], 64 * c, 64 * j, z1, z2);
+        }
+        __syncwarp();
+        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idS = umma_idesc_bf16(QT, 256, 0, 0);
+    const uint32_t idO = umma_idesc_bf16(QT, p.nv, 0, 1);
+    const uint64_t d0 = umma_desc_sw128(smem_u32(smem), 16, 1024);          // K-major (Q, K)
+    const uint64_t v0 = umma_desc_sw128(smem_u32(smem), 8192, 1024);        // MN-major (V)
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
+      const int m0 = (p.num_m - 1 - t % p.num_m) * QT;
+      const int kv = min(p.s, m0 + QT);
+      const int nh = kv > 256 ? 2 : 1;
+      mbar_wait(t_free, (it & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkd; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint64_t ad = d0 + (uint64_t)((stage * ATT_STAGE) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < KB / 16; ++k)
+            for (int hh = 0; hh < nh; ++hh)
+              mma_bf16_ss(tmem + 256 * hh, ad + 2 * k, ad + ((Q_BYTES + hh * KH_BYTES) >> 4) + 2 * k,
+                          idS, (kb > 0 || k > 0) ? 1u : 0u);
+          mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (elect_one()) mma_commit(s_full);
+      __syncwarp();
+      mbar_wait(p_ready, it & 1);
+      tc_fence_after();
+      const int nvb = (kv + 63) / 64;
+      for (int j = 0; j < nvb; ++j) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint64_t vd = v0 + (uint64_t)((stage * ATT_STAGE) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_bf16_ts(tmem + 128, tmem + p_col(64 * j + 16 * k), vd + k * (2048 >> 4), idO,
+                        (j > 0 || k > 0) ? 1u : 0u);
+          mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (elect_one()) mma_commit(o_full);
+      __syncwarp();
+    }
+  } else {
+    const int q = warp & 3, half = (warp - 2) >> 2, wi = warp - 2;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const int rl = q * 32 + lane;
+    uint4* stg = stg_all[wi];
+    int it = 0;
+    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
+      const int z = t / p.num_m, m0 = (p.num_m - 1 - t % p.num_m) * QT;
+      const int z1 = z % p.heads, z2 = z / p.heads;
+      const int kv = min(p.s, m0 + QT);
+      const int kv64 = (kv + 63) / 64 * 64;
+      const int r0 = m0 + q * 32;                                 // first query row of the warp
+      const int c_lo = half * 256;
+      const int c_end = min(kv64, c_lo + 256);                    // P columns to write
+      const int c_val = min(min(kv, c_lo + 256), r0 + 32);        // columns holding scores
+      const int c_full = min(c_val, r0);                          // full chunks below
+      const bool has_diag = r0 >= c_lo && r0 < c_val;
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      uint32_t r[32];
+      // pass 1: row max of the raw scores (alpha > 0)
+      float mx = -3.0e38f;
+      for (int c0 = c_lo; c0 < c_full; c0 += 32) {
+        tmem_ld32(trow + c0, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+      }
+      if (has_diag) {
+        tmem_ld32(trow + r0, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i <= lane) mx = fmaxf(mx, __uint_as_float(r[i]));
+      }
+      red[0][half][rl] = mx;
+      nbar(1 + q, 64);
+      const float moff = fmaxf(red[0][0][rl], red[0][1][rl]) * p.c1;
+      // pass 2: e = exp2(c1 S - moff); P = bf16(e) into TMEM (half 1 walks downwards so its
+      // packed columns never overwrite unread scores); zeros above the diagonal up to kv64
+      float s0 = 0.f, s1 = 0.f;
+      const int nch = (c_end - c_lo + 31) / 32;
+      for (int ci = 0; ci < nch; ++ci) {
+        const int c0 = half ? c_lo + 32 * (nch - 1 - ci) : c_lo + 32 * ci;
+        uint32_t pk[16];
+        if (c0 < c_full || (has_diag && c0 == r0)) {
+          tmem_ld32(trow + c0, r);
+          const bool diag = c0 == r0;
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float e0 = ex2_approx(fmaf(__uint_as_float(r[i]), p.c1, -moff));
+            float e1 = ex2_approx(fmaf(__uint_as_float(r[i + 1]), p.c1, -moff));
+            if (diag) {
+              e0 = i <= lane ? e0 : 0.f;
+              e1 = i + 1 <= lane ? e1 : 0.f;
+            }
+            s0 += e0;
+            s1 += e1;
+            pk[i / 2] = pack_bf16(e0, e1);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = 0u;
+        }
+        tmem_st16(trow + p_col(c0), pk);
+      }
+      red[1][half][rl] = s0 + s1;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_ready);
+      nbar(1 + q, 64);
+      const float sum = red[1][0][rl] + red[1][1][rl];
+      const float inv = 1.f / sum;
+      const int row = r0 + lane;
+      if (half == 0 && row < p.s) p.lse[(long long)z * p.s + row] = moff + __log2f(sum);
+      // O = P V: this warp drains O columns [half * nv/2, +nv/2), scaled by 1/sum
+      mbar_wait(o_full, it & 1);
+      tc_fence_after();
+      const int ncol = p.nv / 2;
+      __nv_bfloat16* obase = p.o + ((long long)z2 * p.s) * p.ldo + (long long)z1 * p.d;
+      for (int cc = 0; cc < ncol; cc += 32) {
+        const int oc = half * ncol + cc;                          // head-dim column
+        tmem_ld32(trow + 128 + oc, r);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 u;
+          u.x = pack_bf16(__uint_as_float(r[8 * j + 0]) * inv, __uint_as_float(r[8 * j + 1]) * inv);
+          u.y = pack_bf16(__uint_as_float(r[8 * j + 2]) * inv, __uint_as_float(r[8 * j + 3]) * inv);
+          u.z = pack_bf16(__uint_as_float(r[8 * j + 4]) * inv, __uint_as_float(r[8 * j + 5]) * inv);
+          u.w = pack_bf16(__uint_as_float(r[8 * j + 6]) * inv, __uint_as_float(r[8 * j + 7]) * inv);
+          stg[lane * 4 + (j ^ (lane & 3))] = u;
+        }
+        __syncwarp();
+        // 8 rows x 64 B per instruction: lane -> (row i * 8 + lane / 4, 16-byte chunk lane % 4)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = i * 8 + lane / 4, ch = lane & 3;
+          const int gr = r0 + rr;
+          const int col = oc + ch * 8;
+          if (gr < p.s && col < p.d) {
+            const uint4 v = stg[rr * 4 + (ch ^ (rr & 3))];
+            __nv_bfloat16* dst = obase + (long long)gr * p.ldo + col;
+            if ((p.d & 7) == 0) {
+              *reinterpret_cast<uint4*>(dst) = v;
+            } else {   // unaligned head width (d = 188, 176): bf16 pairs
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (col + 2 * e < p.d) *reinterpret_cast<uint32_t*>(dst + 2 * e) = w[e];
+            }
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(t_free);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ------------------------------------------------------------------ backward
+// dS = alpha * P * (dP - D),  D_i = sum_j P_ij dP_ij = dO_i . O_i (computed by attn_bwd_d),
+// P recomputed from S and the forward's lse2 (never stored).  Two kernels of one template:
+//   KA (rows = 128 keys n): for every query block m >= n:  X = K_n Q_m^T, Y = V_n dO_m^T
+//       -> P^T, dS^T packed bf16 in TMEM ->  dV_n += P^T dO_m,  dK_n += dS^T Q_m   (TS-MMAs)
+//   !KA (rows = 128 queries m): for every key block n <= m: X = Q_m K_n^T, Y = dO_m V_n^T
+//       -> dS packed in TMEM -> dQ_m += dS K_n
+// so every gradient element has exactly one writer (deterministic, no atomics).  The row
+// operands (F1, F2) stay in smem for the whole unit; the column operands (G1, G2) stream
+// through a ring.  One smem copy of each operand serves both the K-major (X, Y) and the
+// MN-major (accumulation) descriptor.  4 epilogue warps: thread = TMEM lane = tile row.
+struct AttnBwdParams {
+  int s, heads, d, nv, qb, nq, nk, total, stages;
+  float c1, alpha;
+  const float* lse;
+  const float* D;
+  __nv_bfloat16* dq;   // dqkv base; dQ at column z1*d, dK at h + z1*d, dV at 2h + z1*d
+  long long ldq;
+  int h;
+};
+
+constexpr int BWD_THREADS = 64 + 4 * 32;
+
+__device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
+                                          int nv, int rows, int row0, int z1, int z2) {
+  // [rows x nv] operand: d-chunk c (64 columns) at c * rows * 128, 64-row boxes
+  for (int c = 0; c < nv / 64; ++c)
+    for (int rb = 0; rb < rows / 64; ++rb)
+      tma_load_4d(dst + c * rows * 128 + rb * 8192, map, bar, 64 * c, row0 + 64 * rb, z1, z2);
+}
+
+template <bool KA>
+__global__ void __launch_bounds__(BWD_THREADS, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
+                    const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapO,
+                    const AttnBwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int FR = 128;                        // rows of the unit tile
+  const int GR = KA ? p.qb : 128;            // rows of one streamed block
+  const int f_bytes = p.nv * FR * 2;         // one row operand
+  const int g_bytes = p.nv * GR * 2;         // one streamed operand
+  uint8_t* sF = smem;                        // F1, F2
+  uint8_t* sG = smem + 2 * f_bytes;          // ring: stage i holds G1, G2
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sG + p.stages * 2 * g_bytes);
+  uint64_t* f_full = bars;
+  uint64_t* f_empty = bars + 1;
+  uint64_t* xy_full = bars + 2;
+  uint64_t* pd_ready = bars + 3;
+  uint64_t* acc_done = bars + 4;
+  uint64_t* acc_full = bars + 5;
+  uint64_t* acc_free = bars + 6;
+  uint64_t* g_full = bars + 8;
+  uint64_t* g_empty = g_full + 4;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(g_empty + 4);
+  __shared__ float sL[128], sD[128];
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int NX = KA ? p.qb : 128;            // columns of X / Y
+  const uint32_t colY = NX;                  // TMEM: X [0, NX), Y [NX, 2NX), acc_a, acc_b
+  const uint32_t colA = 2 * NX, colB = 2 * NX + (KA ? p.nv : 0);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapQ);
+    tma_prefetch_desc(&mapK);
+    tma_prefetch_desc(&mapV);
+    tma_prefetch_desc(&mapO);
+    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], i == 3 || i == 6 ? 4 : 1);
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(&g_full[i], 1);
+      mbar_init(&g_empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  // unit t -> (z, tile): KA: key tile n ascending (most query blocks first); else query tile
+  // m descending (most key blocks first)
+  auto unit = [&](int t, int& z, int& r0, int& i0, int& ni) {
+    const int per = KA ? p.nk : p.nq;
+    z = t / per;
+    const int k = t % per;
+    if (KA) {
+      r0 = k * 128;                     // keys [r0, r0 + 128)
+      i0 = r0 / p.qb;                   // first query block touching the diagonal
+      ni = (p.s + p.qb - 1) / p.qb - i0;
+    } else {
+      const int m = per - 1 - k;
+      r0 = m * 128;                     // queries [r0, r0 + 128)
+      i0 = 0;
+      ni = m + 1;                       // key blocks 0..m
+    }
+  };
+
+  if (warp == 0) {
+    int stage = 0;
+    uint32_t phase = 0;
+    int u = 0;
+    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++u) {
+      int z, r0, i0, ni;
+      unit(t, z, r0, i0, ni);
+      const int z1 = z % p.heads, z2 = z / p.heads;
+      mbar_wait(f_empty, (u & 1) ^ 1);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(f_full, 2 * f_bytes);
+        load_rows(sF, KA ? &mapK : &mapQ, f_full, p.nv, FR, r0, z1, z2);
+        load_rows(sF + f_bytes, KA ? &mapV : &mapO, f_full, p.nv, FR, r0, z1, z2);
+      }
+      __syncwarp();
+      for (int it = 0; it < ni; ++it) {
+        const int g0 = (i0 + it) * GR;
+        mbar_wait(&g_empty[stage], phase ^ 1);
+        if (elect_one()) {
+          uint8_t* g = sG + stage * 2 * g_bytes;
+          mbar_arrive_expect_tx(&g_full[stage], 2 * g_bytes);
+          load_rows(g, KA ? &mapQ : &mapK, &g_full[stage], p.nv, GR, g0, z1, z2);
+          load_rows(g + g_bytes, KA ? &mapO : &mapV, &g_full[stage], p.nv, GR, g0, z1, z2);
+        }
+        __syncwarp();
+        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idXY = umma_idesc_bf16(128, NX, 0, 0);
+    const uint32_t idAcc = umma_idesc_bf16(128, p.nv, 0, 1);
+    const uint32_t sF0 = smem_u32(sF), sG0 = smem_u32(sG);
+    int stage = 0;
+    uint32_t phase = 0;
+    int u = 0, g_it = 0, nacc = 0;
+    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++u) {
+      int z, r0, i0, ni;
+      unit(t, z, r0, i0, ni);
+      mbar_wait(f_full, u & 1);
+      tc_fence_after();
+      for (int it = 0; it < ni; ++it, ++g_it) {
+        mbar_wait(&g_full[stage], phase);
+        if (nacc > 0) mbar_wait(acc_done, (nacc - 1) & 1);   // previous TS-MMAs read X / Y
+        tc_fence_after();
+        const uint32_t g1 = sG0 + stage * 2 * g_bytes, g2 = g1 + g_bytes;
+        if (elect_one()) {
+          for (int c = 0; c < p.nv / 64; ++c) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t acc = (c > 0 || k > 0) ? 1u : 0u;
+              mma_bf16_ss(tmem, umma_desc_sw128(sF0 + c * FR * 128 + 32 * k, 16, 1024),
+                          umma_desc_sw128(g1 + c * GR * 128 + 32 * k, 16, 1024), idXY, acc);
+              mma_bf16_ss(tmem + colY, umma_desc_sw128(sF0 + f_bytes + c * FR * 128 + 32 * k, 16, 1024),
+                          umma_desc_sw128(g2 + c * GR * 128 + 32 * k, 16, 1024), idXY, acc);
+            }
+          }
+          mma_commit(xy_full);
+          if (it == ni - 1) mma_commit(f_empty);
+        }
+        __syncwarp();
+        mbar_wait(pd_ready, g_it & 1);
+        if (it == 0) mbar_wait(acc_free, (u & 1) ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          // accumulate over the GR rows of this block: A = packed P^T / dS (TMEM), B = G MN-major
+          for (int k = 0; k < GR / 16; ++k) {
+            const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
+            if (KA)
+              mma_bf16_ts(tmem + colA, tmem + 8 * k, umma_desc_sw128(g2 + 2048 * k, GR * 128, 1024),
+                          idAcc, acc);
+            mma_bf16_ts(tmem + colB, tmem + colY + 8 * k, umma_desc_sw128(g1 + 2048 * k, GR * 128, 1024),
+                        idAcc, acc);
+          }
+          mma_commit(&g_empty[stage]);
+          mma_commit(acc_done);
+          if (it == ni - 1) mma_commit(acc_full);
+        }
+        __syncwarp();
+        ++nacc;
+        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    const int q = warp & 3;                   // TMEM lane quarter this warp may access
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    int u = 0, g_it = 0;
+    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++u) {
+      int z, r0, i0, ni;
+      unit(t, z, r0, i0, ni);
+      const int z1 = z % p.heads, z2 = z / p.heads;
+      const int row = r0 + q * 32 + lane;     // key (KA) or query (!KA) index
+      const float* lse = p.lse + (long long)z * p.s;
+      const float* Dz = p.D + (long long)z * p.s;
+      float Lr = 0.f, Dr = 0.f;
+      if (!KA && row < p.s) {
+        Lr = lse[row];
+        Dr = Dz[row];
+      }
+      for (int it = 0; it < ni; ++it, ++g_it) {
+        const int g0 = (i0 + it) * GR;        // first query (KA) or key (!KA) of the block
+        if (KA) {
+          const int tid = threadIdx.x - 64;
+          if (tid < GR) {
+            const int i = g0 + tid;
+            sL[tid] = i < p.s ? lse[i] : 0.f;
+            sD[tid] = i < p.s ? Dz[i] : 0.f;
+          }
+          nbar(1, 128);
+        }
+        mbar_wait(xy_full, g_it & 1);
+        tc_fence_after();
+        for (int c0 = 0; c0 < NX; c0 += 32) {
+          uint32_t x[32], y[32];
+          tmem_ld32_nowait(trow + c0, x);
+          tmem_ld32_nowait(trow + colY + c0, y);
+          tmem_ld_wait();
+          uint32_t pp[16], pd[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float P2[2], S2[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = g0 + c0 + i + e;
+              float L, Dv;
+              bool ok;
+              if (KA) {   // row = key, col = query
+                L = sL[c0 + i + e];
+                Dv = sD[c0 + i + e];
+                ok = col >= row && col < p.s;
+              } else {    // row = query, col = key
+                L = Lr;
+                Dv = Dr;
+                ok = col <= row;
+              }
+              const float P = ok ? ex2_approx(fmaf(__uint_as_float(x[i + e]), p.c1, -L)) : 0.f;
+              P2[e] = P;
+              S2[e] = P * (__uint_as_float(y[i + e]) - Dv) * p.alpha;
+            }
+            pp[i / 2] = pack_bf16(P2[0], P2[1]);
+            pd[i / 2] = pack_bf16(S2[0], S2[1]);
+          }
+          if (KA) tmem_st16(trow + c0 / 2, pp);
+          tmem_st16(trow + colY + c0 / 2, pd);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pd_ready);
+        if (KA) nbar(1, 128);                 // sL / sD are rewritten by the next block
+      }
+      // drain the accumulators of the unit: KA -> dV (acc_a), dK (acc_b); else dQ (acc_b)
+      mbar_wait(acc_full, u & 1);
+      tc_fence_after();
+      __nv_bfloat16* base = p.dq + (long long)z2 * p.s * p.ldq + (long long)z1 * p.d;
+      for (int which = KA ? 0 : 1; which < 2; ++which) {
+        const uint32_t ca = which == 0 ? colA : colB;
+        __nv_bfloat16* dst = base + (KA ? (which == 0 ? 2 * p.h : p.h) : 0) + (long long)row * p.ldq;
+        for (int c0 = 0; c0 < p.nv; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(trow + ca + c0, r);
+          if (row < p.s) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const int col = c0 + i;
+              if (col < p.d)
+                *reinterpret_cast<uint32_t*>(dst + col) =
+                    pack_bf16(__uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_free);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// D[z * s + i] = sum_j dO[i, head, j] * O[i, head * d + j]   (fp32), one warp per (token, head)
+__global__ void attn_bwd_d_kernel(const __nv_bfloat16* __restrict__ dO, long long ld_do, int dp,
+                                  const __nv_bfloat16* __restrict__ O, long long ld_o, int d,
+                                  int s, int heads, long long ntok, float* __restrict__ D) {
+  const long long w = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= ntok * heads) return;
+  const long long tok = w / heads;
+  const int hd = (int)(w % heads);
+  const __nv_bfloat16* a = dO + tok * ld_do + (long long)hd * dp;
+  const __nv_bfloat16* b = O + tok * ld_o + (long long)hd * d;
+  float acc = 0.f;
+  for (int j = 2 * lane; j < d; j += 64) {
+    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + j));
+    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(b + j));
+    acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    const long long sample = tok / s, i = tok % s;
+    D[(sample * heads + hd) * s + i] = acc;
+  }
+}
+
+}  // namespace
+
+int attn_fwd(const void* qkv, long long lq, int b, int heads, int s, int d, int dp, float alpha,
+             void* o, long long ldo, float* lse, cudaStream_t st) {
+  if (s <= 0 || s > 512 || d <= 0 || dp < d || dp % 2 || (d & 1)) return -1;
+  const int nv = (dp + 63) / 64 * 64;
+  if (nv > 256) return -1;
+  constexpr int SMEM = ATT_STAGES * ATT_STAGE + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
+        cudaSuccess)
+      return -10;
+    attr = true;
+  }
+  const char* base = static_cast<const char*>(qkv);
+  CUtensorMap mq, mk, mv;
+  const long long s2 = (long long)s * lq;
+  int rc = make_tmap_4d(&mq, base, dp, s, lq, heads, dp, b, s2, QT);
+  if (!rc) rc = make_tmap_4d(&mk, base + (size_t)heads * dp * 2, dp, s, lq, heads, dp, b, s2, 256);
+  if (!rc) rc = make_tmap_4d(&mv, base + (size_t)2 * heads * dp * 2, dp, s, lq, heads, dp, b, s2, 64);
+  if (rc) return rc;
+  AttnParams p;
+  p.s = s;
+  p.heads = heads;
+  p.d = d;
+  p.nv = nv;
+  p.num_m = (s + QT - 1) / QT;
+  p.total = p.num_m * b * heads;
+  p.c1 = alpha * 1.4426950408889634f;
+  p.o = static_cast<__nv_bfloat16*>(o);
+  p.ldo = ldo;
+  p.lse = lse;
+  int nsm = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = p.total < nsm ? p.total : nsm;
+  attn_fwd_kernel<<<grid, ATT_THREADS, SMEM, st>>>(mq, mk, mv, p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long long ldo,
+             const float* lse, float* Dbuf, int b, int heads, int s, int d, int dp, float alpha,
+             void* dqkv, long long ldq, cudaStream_t st) {
+  if (s <= 0 || s > 512 || d <= 0 || dp < d || dp % 2 || (d & 1) || (ldq & 1)) return -1;
+  const int nv = (dp + 63) / 64 * 64;
+  if (nv > 256) return -1;
+  const long long ntok = (long long)b * s;
+  {
+    const int wpb = 8;
+    const long long nw = ntok * heads;
+    attn_bwd_d_kernel<<<(unsigned)((nw + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(dO), (long long)heads * dp, dp,
+        static_cast<const __nv_bfloat16*>(o), ldo, d, s, heads, ntok, Dbuf);
+  }
+  const char* base = static_cast<const char*>(qkv);
+  CUtensorMap mq, mk, mv, mo;
+  const long long s2 = (long long)s * lq;
+  int rc = make_tmap_4d(&mq, base, dp, s, lq, heads, dp, b, s2, 64);
+  if (!rc) rc = make_tmap_4d(&mk, base + (size_t)heads * dp * 2, dp, s, lq, heads, dp, b, s2, 64);
+  if (!rc) rc = make_tmap_4d(&mv, base + (size_t)2 * heads * dp * 2, dp, s, lq, heads, dp, b, s2, 64);
+  if (!rc) rc = make_tmap_4d(&mo, dO, dp, s, (long long)heads * dp, heads, dp, b,
+                             (long long)s * heads * dp, 64);
+  if (rc) return rc;
+  int nsm = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  AttnBwdParams p;
+  p.s = s; p.heads = heads; p.d = d; p.nv = nv;
+  p.qb = nv <= 128 ? 128 : 64;
+  p.nq = (s + 127) / 128;
+  p.nk = (s + 127) / 128;
+  p.c1 = alpha * 1.4426950408889634f;
+  p.alpha = alpha;
+  p.lse = lse;
+  p.D = Dbuf;
+  p.dq = static_cast<__nv_bfloat16*>(dqkv);
+  p.ldq = ldq;
+  p.h = heads * d;
+  const int max_smem = 227 * 1024 - 2048 - 1024;
+  for (int ka = 1; ka >= 0; --ka) {
+    const int GR = ka ? p.qb : 128;
+    const int f_bytes = nv * 128 * 2, g_bytes = nv * GR * 2;
+    int stages = 2;
+    while (stages > 1 && 2 * f_bytes + stages * 2 * g_bytes > max_smem) --stages;
+    if (2 * f_bytes + stages * 2 * g_bytes > max_smem) return -1;
+    p.stages = stages;
+    p.total = b * heads * (ka ? p.nk : p.nq);
+    const int smem = 2 * f_bytes + stages * 2 * g_bytes + 1024 + 256;
+    void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, AttnBwdParams) =
+        ka ? attn_bwd_kernel<true> : attn_bwd_kernel<false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return -10;
+    const int grid = p.total < nsm ? p.total : nsm;
+    kern<<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mo, p);
+    if (cudaGetLastError() != cudaSuccess) return -11;
+  }
+  return 0;
+}
+
+int preload_attn() {
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, attn_fwd_kernel) != cudaSuccess) return -1;
+  if (cudaFuncGetAttributes(&a, attn_bwd_kernel<true>) != cudaSuccess) return -1;
+  if (cudaFuncGetAttributes(&a, attn_bwd_kernel<false>) != cudaSuccess) return -1;
+  return cudaFuncGetAttributes(&a, attn_bwd_d_kernel) == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace axonn

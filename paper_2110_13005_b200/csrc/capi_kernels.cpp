@@ -26,3 +26,18 @@ extern "C" int axonn_k_adamw(int64_t n, const void* g16, float* theta, float* m,
   return axonn::adamw_launch(n, g16, theta, m, v, theta16, scalars,
                              reinterpret_cast<cudaStream_t>(stream));
 }
+
+extern "C" int axonn_k_attn_fwd(const void* qkv, int64_t lq, int b, int heads, int s, int d, int dp,
+                                float alpha, void* o, int64_t ldo, float* lse, void* stream) {
+  if (!qkv || !o || !lse) return -1;
+  return axonn::attn_fwd(qkv, lq, b, heads, s, d, dp, alpha, o, ldo, lse,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int axonn_k_attn_bwd(const void* qkv, int64_t lq, const void* dO, const void* o, int64_t ldo,
+                                const float* lse, float* dbuf, int b, int heads, int s, int d, int dp,
+                                float alpha, void* dqkv, int64_t ldq, void* stream) {
+  if (!qkv || !dO || !o || !lse || !dbuf || !dqkv) return -1;
+  return axonn::attn_bwd(qkv, lq, dO, o, ldo, lse, dbuf, b, heads, s, d, dp, alpha, dqkv, ldq,
+                         reinterpret_cast<cudaStream_t>(stream));
+}

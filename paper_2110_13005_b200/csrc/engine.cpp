@@ -322,7 +322,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   // CUDA lazy loading would load a kernel's module at its first launch and wait for the
   // device's running kernels — including a pre-posted ncclRecv spinning until the peer
   // sends, which the peer only does after our launch: load everything now.
-  if (preload_gemm() || preload_ops() || preload_adamw())
+  if (preload_gemm() || preload_ops() || preload_adamw() || preload_attn())
     return bail(c->fail(AXONN_ERR_CUDA, "kernel preload failed"));
   for (cudaStream_t* st : {&c->s_comp, &c->s_send_act, &c->s_send_grad, &c->s_recv_act,
                            &c->s_recv_grad, &c->s_dp, &c->s_h2d, &c->s_d2h, &c->s_opt, &c->s_wg})

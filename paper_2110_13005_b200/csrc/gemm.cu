@@ -272,7 +272,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int z1 = z % p.Z1, z2 = z / p.Z1;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (elect_one()) {
+          if (p.dbg == 7) {
+            if (elect_one()) mbar_arrive(&full[stage]);
+          } else if (elect_one()) {
             mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
             uint8_t* sA = smem + stage * STAGE_BYTES;
             uint8_t* sB = sA + A_BYTES;
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
-      for (int c = cpart * CW; c < (cpart + 1) * CW; c += 32) {
+      for (int c = cpart * CW; c < (cpart + 1) * CW && p.dbg != 8; c += 32) {
         if (n0 + c >= p.N) break;
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c, r);
@@ -1392,6 +1394,12 @@ static int make_map(CUtensorMap* map, const void* base, long long inner, long lo
   return r == CUDA_SUCCESS ? 0 : -3;
 }
 
+// exported for the fused attention kernels (attn.cu)
+int make_tmap_4d(CUtensorMap* map, const void* base, long long inner, long long outer,
+                 long long ld, int Z1, long long s1, int Z2, long long s2, int box_outer) {
+  return make_map(map, base, inner, outer, ld, Z1, s1, Z2, s2, box_outer);
+}
+
 static int g_num_sms = 0;
 
 static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
@@ -1449,6 +1457,14 @@ static int launch_bn(const GemmArgs& g, cudaStream_t st) {
   if (rc) return rc;
   GemmParams p;
   fill_params(p, g, BM, BN);
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("AXONN_GEMM_DBG");
+      dbg = e ? atoi(e) : 0;
+    }
+    p.dbg = dbg;
+  }
   int grid = p.total < g_num_sms ? p.total : g_num_sms;
   if (g.max_ctas > 0 && grid > g.max_ctas) grid = g.max_ctas;
   gemm_bf16_tcgen05<BN><<<grid, GEMM_THREADS, SMEM, st>>>(ma, mb, p);

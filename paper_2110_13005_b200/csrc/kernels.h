@@ -1,6 +1,7 @@
 // Internal launcher declarations for the sm_100a kernels (not part of the C-ABI).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace axonn {
@@ -35,6 +36,22 @@ struct GemmArgs {
 };
 
 int gemm_launch(const GemmArgs& g, cudaStream_t st);
+// 4-D bf16 TMA map (inner, outer, z1, z2), strides in elements, box (64, box_outer), SWIZZLE_128B
+int make_tmap_4d(CUtensorMap* map, const void* base, long long inner, long long outer,
+                 long long ld, int Z1, long long s1, int Z2, long long s2, int box_outer);
+
+// attn.cu: fused causal attention over the packed [tokens, 3, heads, dp] QKV buffer (s <= 512).
+// Forward: o = softmax_causal(alpha Q K^T) V written to o[token][head * d + j] (j < d), and the
+// per-row log2-domain normaliser lse2 = max(alpha log2e S) + log2(sum) to lse[z * s + row].
+int attn_fwd(const void* qkv, long long lq, int b, int heads, int s, int d, int dp, float alpha,
+             void* o, long long ldo, float* lse, cudaStream_t st);
+// Backward: dqkv[:, 0:h) = dQ, [h, 2h) = dK, [2h, 3h) = dV (head n at n*d; ld = ldq), from dO
+// (bf16 [tokens][heads*dp], padded like q) and the forward's o / lse.  Dbuf: fp32 [b*heads*s]
+// workspace (D_i = dO_i . O_i).  P is recomputed from S and lse (never stored).
+int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long long ldo,
+             const float* lse, float* Dbuf, int b, int heads, int s, int d, int dp, float alpha,
+             void* dqkv, long long ldq, cudaStream_t st);
+int preload_attn();
 int preload_gemm();    // force-load kernels (no lazy module load behind a spinning NCCL kernel)
 int preload_ops();
 int preload_adamw();
