@@ -320,16 +320,19 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 // ------------------------------------------------------------------ backward
 // dS = alpha * P * (dP - D),  D_i = sum_j P_ij dP_ij = dO_i . O_i (computed by attn_bwd_d),
 // P recomputed from S and the forward's lse2 (never stored).  Two kernels of one template:
-//   KA (rows = 128 keys n): for every query block m >= n:  X = K_n Q_m^T, Y = V_n dO_m^T
-//       -> P^T, dS^T packed bf16 in TMEM ->  dV_n += P^T dO_m,  dK_n += dS^T Q_m   (TS-MMAs)
-//   !KA (rows = 128 queries m): for every key block n <= m: X = Q_m K_n^T, Y = dO_m V_n^T
-//       -> dS packed in TMEM -> dQ_m += dS K_n
+//   KA (rows = 128 keys n): for every 64-query block m with queries >= keys:
+//       X = K_n Q_m^T, Y = V_n dO_m^T -> P^T, dS^T packed bf16 in TMEM
+//       -> dV_n += P^T dO_m,  dK_n += dS^T Q_m                                   (TS-MMAs)
+//   !KA (rows = 128 queries m): for every 64-key block n <= m:
+//       X = Q_m K_n^T, Y = dO_m V_n^T -> dS packed in TMEM -> dQ_m += dS K_n
 // so every gradient element has exactly one writer (deterministic, no atomics).  The row
-// operands (F1, F2) stay in smem for the whole unit; the column operands (G1, G2) stream
-// through a ring.  One smem copy of each operand serves both the K-major (X, Y) and the
-// MN-major (accumulation) descriptor.  4 epilogue warps: thread = TMEM lane = tile row.
+// operands (F1, F2) stay in smem for the unit; the 64-row column operands (G1, G2) stream
+// through a ring, and one smem copy of each serves both the K-major (X, Y) and the MN-major
+// (accumulation) descriptor.  X / Y are double-buffered in TMEM when the accumulators leave
+// room, so the epilogue of block i overlaps the MMAs of block i+1.  8 epilogue warps:
+// warp (q, half) owns TMEM lanes [32 q, +32) and block columns [32 half, +32).
 struct AttnBwdParams {
-  int s, heads, d, nv, qb, nq, nk, total, stages;
+  int s, heads, d, nv, nq, nk, total, stages, nbuf;
   float c1, alpha;
   const float* lse;
   const float* D;
@@ -338,7 +341,8 @@ struct AttnBwdParams {
   int h;
 };
 
-constexpr int BWD_THREADS = 64 + 4 * 32;
+constexpr int BWD_THREADS = 64 + 8 * 32;
+constexpr int GRB = 64;   // rows of one streamed block (queries for KA, keys for !KA)
 
 __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
                                           int nv, int rows, int row0, int z1, int z2) {
@@ -348,6 +352,42 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, 
       tma_load_4d(dst + c * rows * 128 + rb * 8192, map, bar, 64 * c, row0 + 64 * rb, z1, z2);
 }
 
+// 32 rows x 32 bf16 (this warp's chunk, row = lane) -> global rows r0.., columns col0..
+// (only col < dvalid), through a swizzled 2 KB staging tile: 8 rows x 64 B per instruction
+__device__ __forceinline__ void store_chunk32(uint4* stg, int lane, const uint32_t (&r)[32],
+                                              float scale, __nv_bfloat16* gbase, long long ld,
+                                              int r0, int rows_valid, int col0, int dvalid) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 u;
+    u.x = pack_bf16(__uint_as_float(r[8 * j + 0]) * scale, __uint_as_float(r[8 * j + 1]) * scale);
+    u.y = pack_bf16(__uint_as_float(r[8 * j + 2]) * scale, __uint_as_float(r[8 * j + 3]) * scale);
+    u.z = pack_bf16(__uint_as_float(r[8 * j + 4]) * scale, __uint_as_float(r[8 * j + 5]) * scale);
+    u.w = pack_bf16(__uint_as_float(r[8 * j + 6]) * scale, __uint_as_float(r[8 * j + 7]) * scale);
+    stg[lane * 4 + (j ^ (lane & 3))] = u;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rr = i * 8 + lane / 4, ch = lane & 3;
+    const int gr = r0 + rr;
+    const int col = col0 + ch * 8;
+    if (gr < rows_valid && col < dvalid) {
+      const uint4 v = stg[rr * 4 + (ch ^ (rr & 3))];
+      __nv_bfloat16* dst = gbase + (long long)gr * ld + col;
+      if ((dvalid & 7) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        *reinterpret_cast<uint4*>(dst) = v;
+      } else {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (col + 2 * e < dvalid) *reinterpret_cast<uint32_t*>(dst + 2 * e) = w[e];
+      }
+    }
+  }
+  __syncwarp();
+}
+
 template <bool KA>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
@@ -355,8 +395,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                     const AttnBwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int FR = 128;                        // rows of the unit tile
-  const int GR = KA ? p.qb : 128;            // rows of one streamed block
+  constexpr int FR = 128, GR = GRB;
   const int f_bytes = p.nv * FR * 2;         // one row operand
   const int g_bytes = p.nv * GR * 2;         // one streamed operand
   uint8_t* sF = smem;                        // F1, F2
@@ -364,30 +403,26 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sG + p.stages * 2 * g_bytes);
   uint64_t* f_full = bars;
   uint64_t* f_empty = bars + 1;
-  uint64_t* xy_full = bars + 2;
-  uint64_t* pd_ready = bars + 3;
-  uint64_t* acc_done = bars + 4;
-  uint64_t* acc_full = bars + 5;
-  uint64_t* acc_free = bars + 6;
-  uint64_t* g_full = bars + 8;
-  uint64_t* g_empty = g_full + 4;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(g_empty + 4);
-  __shared__ float sL[128], sD[128];
+  uint64_t* acc_full = bars + 2;
+  uint64_t* acc_free = bars + 3;             // 8 arrivals
+  uint64_t* xy_full = bars + 4;              // [2]
+  uint64_t* pd_ready = bars + 6;             // [2], 8 arrivals
+  uint64_t* acc_done = bars + 8;             // [2]
+  uint64_t* g_full = bars + 10;              // [4]
+  uint64_t* g_empty = bars + 14;             // [4]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 18);
+  __shared__ float sL[2][GR], sD[2][GR];
+  __shared__ uint4 stg_all[8][32 * 4];
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int NX = KA ? p.qb : 128;            // columns of X / Y
-  const uint32_t colY = NX;                  // TMEM: X [0, NX), Y [NX, 2NX), acc_a, acc_b
-  const uint32_t colA = 2 * NX, colB = 2 * NX + (KA ? p.nv : 0);
+  // TMEM: buffer b: X [128 b, +64), Y [128 b + 64, +64); accumulators after the buffers
+  const uint32_t colA = 128 * p.nbuf, colB = colA + (KA ? p.nv : 0);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapQ);
     tma_prefetch_desc(&mapK);
     tma_prefetch_desc(&mapV);
     tma_prefetch_desc(&mapO);
-    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], i == 3 || i == 6 ? 4 : 1);
-    for (int i = 0; i < p.stages; ++i) {
-      mbar_init(&g_full[i], 1);
-      mbar_init(&g_empty[i], 1);
-    }
+    for (int i = 0; i < 18; ++i) mbar_init(&bars[i], (i == 3 || i == 6 || i == 7) ? 8 : 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_holder);
@@ -403,13 +438,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const int k = t % per;
     if (KA) {
       r0 = k * 128;                     // keys [r0, r0 + 128)
-      i0 = r0 / p.qb;                   // first query block touching the diagonal
-      ni = (p.s + p.qb - 1) / p.qb - i0;
+      i0 = r0 / GR;                     // first query block touching the diagonal
+      ni = (p.s + GR - 1) / GR - i0;
     } else {
       const int m = per - 1 - k;
       r0 = m * 128;                     // queries [r0, r0 + 128)
       i0 = 0;
-      ni = m + 1;                       // key blocks 0..m
+      ni = min((p.s + GR - 1) / GR, (r0 + 128) / GR);   // key blocks with keys <= last query
     }
   };
 
@@ -442,63 +477,88 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    const uint32_t idXY = umma_idesc_bf16(128, NX, 0, 0);
+    const uint32_t idXY = umma_idesc_bf16(128, GR, 0, 0);
     const uint32_t idAcc = umma_idesc_bf16(128, p.nv, 0, 1);
     const uint32_t sF0 = smem_u32(sF), sG0 = smem_u32(sG);
-    int stage = 0;
-    uint32_t phase = 0;
-    int u = 0, g_it = 0, nacc = 0;
+    int g = 0;                        // global block counter (stage / buffer / parity source)
+    uint32_t accd_ph[2] = {0, 0};     // acc_done uses per buffer
+    int accd_n[2] = {0, 0};
+    int u = 0;
+    auto issue_xy = [&](int gi) {     // X, Y of global block gi into buffer gi % nbuf
+      const int b = gi % p.nbuf, stg = gi % p.stages;
+      mbar_wait(&g_full[stg], (uint32_t)((gi / p.stages) & 1));
+      if (accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);   // last TS-MMA read of b
+      tc_fence_after();
+      const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
+      if (elect_one()) {
+        for (int c = 0; c < p.nv / 64; ++c) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t acc = (c > 0 || k > 0) ? 1u : 0u;
+            mma_bf16_ss(tmem + 128 * b, umma_desc_sw128(sF0 + c * FR * 128 + 32 * k, 16, 1024),
+                        umma_desc_sw128(g1 + c * GR * 128 + 32 * k, 16, 1024), idXY, acc);
+            mma_bf16_ss(tmem + 128 * b + 64,
+                        umma_desc_sw128(sF0 + f_bytes + c * FR * 128 + 32 * k, 16, 1024),
+                        umma_desc_sw128(g2 + c * GR * 128 + 32 * k, 16, 1024), idXY, acc);
+          }
+        }
+        mma_commit(&xy_full[b]);
+      }
+      __syncwarp();
+    };
     for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++u) {
       int z, r0, i0, ni;
       unit(t, z, r0, i0, ni);
       mbar_wait(f_full, u & 1);
       tc_fence_after();
-      for (int it = 0; it < ni; ++it, ++g_it) {
-        mbar_wait(&g_full[stage], phase);
-        if (nacc > 0) mbar_wait(acc_done, (nacc - 1) & 1);   // previous TS-MMAs read X / Y
-        tc_fence_after();
-        const uint32_t g1 = sG0 + stage * 2 * g_bytes, g2 = g1 + g_bytes;
-        if (elect_one()) {
-          for (int c = 0; c < p.nv / 64; ++c) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t acc = (c > 0 || k > 0) ? 1u : 0u;
-              mma_bf16_ss(tmem, umma_desc_sw128(sF0 + c * FR * 128 + 32 * k, 16, 1024),
-                          umma_desc_sw128(g1 + c * GR * 128 + 32 * k, 16, 1024), idXY, acc);
-              mma_bf16_ss(tmem + colY, umma_desc_sw128(sF0 + f_bytes + c * FR * 128 + 32 * k, 16, 1024),
-                          umma_desc_sw128(g2 + c * GR * 128 + 32 * k, 16, 1024), idXY, acc);
-            }
-          }
-          mma_commit(xy_full);
-          if (it == ni - 1) mma_commit(f_empty);
+      const int g_first = g;
+      issue_xy(g);
+      if (ni == 1 && elect_one()) mma_commit(f_empty);
+      __syncwarp();
+      for (int it = 0; it < ni; ++it, ++g) {
+        const int b = g % p.nbuf, stg = g % p.stages;
+        if (p.nbuf == 2 && it + 1 < ni) {
+          issue_xy(g + 1);
+          if (it + 2 == ni && elect_one()) mma_commit(f_empty);
+          __syncwarp();
         }
-        __syncwarp();
-        mbar_wait(pd_ready, g_it & 1);
+        mbar_wait(&pd_ready[b], (uint32_t)(((g - (p.nbuf == 2 ? 0 : 0)) / p.nbuf) & 1));
         if (it == 0) mbar_wait(acc_free, (u & 1) ^ 1);
         tc_fence_after();
+        const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
         if (elect_one()) {
-          // accumulate over the GR rows of this block: A = packed P^T / dS (TMEM), B = G MN-major
+          // accumulate over the 64 rows of this block: A = packed P^T / dS (TMEM; columns of
+          // the two 32-wide halves at +0 and +32), B = G operand MN-major
+#pragma unroll
           for (int k = 0; k < GR / 16; ++k) {
             const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
+            const uint32_t pc = 128 * b + (k >> 1) * 32 + (k & 1) * 8;
             if (KA)
-              mma_bf16_ts(tmem + colA, tmem + 8 * k, umma_desc_sw128(g2 + 2048 * k, GR * 128, 1024),
+              mma_bf16_ts(tmem + colA, tmem + pc, umma_desc_sw128(g2 + 2048 * k, GR * 128, 1024),
                           idAcc, acc);
-            mma_bf16_ts(tmem + colB, tmem + colY + 8 * k, umma_desc_sw128(g1 + 2048 * k, GR * 128, 1024),
+            mma_bf16_ts(tmem + colB, tmem + pc + 64, umma_desc_sw128(g1 + 2048 * k, GR * 128, 1024),
                         idAcc, acc);
           }
-          mma_commit(&g_empty[stage]);
-          mma_commit(acc_done);
+          mma_commit(&g_empty[stg]);
+          mma_commit(&acc_done[b]);
           if (it == ni - 1) mma_commit(acc_full);
         }
         __syncwarp();
-        ++nacc;
-        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        accd_ph[b] ^= 1;
+        ++accd_n[b];
+        if (p.nbuf == 1 && it + 1 < ni) {
+          issue_xy(g + 1);
+          if (it + 2 == ni && elect_one()) mma_commit(f_empty);
+          __syncwarp();
+        }
       }
+      (void)g_first;
     }
   } else {
-    const int q = warp & 3;                   // TMEM lane quarter this warp may access
+    const int q = warp & 3, half = (warp - 2) >> 2, wi = warp - 2;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    int u = 0, g_it = 0;
+    uint4* stg = stg_all[wi];
+    int u = 0, g = 0;
     for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++u) {
       int z, r0, i0, ni;
       unit(t, z, r0, i0, ni);
@@ -511,77 +571,71 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         Lr = lse[row];
         Dr = Dz[row];
       }
-      for (int it = 0; it < ni; ++it, ++g_it) {
+      for (int it = 0; it < ni; ++it, ++g) {
+        const int b = g % p.nbuf;
         const int g0 = (i0 + it) * GR;        // first query (KA) or key (!KA) of the block
+        const int sb = g & 1;
         if (KA) {
           const int tid = threadIdx.x - 64;
           if (tid < GR) {
             const int i = g0 + tid;
-            sL[tid] = i < p.s ? lse[i] : 0.f;
-            sD[tid] = i < p.s ? Dz[i] : 0.f;
+            sL[sb][tid] = i < p.s ? lse[i] : 0.f;
+            sD[sb][tid] = i < p.s ? Dz[i] : 0.f;
           }
-          nbar(1, 128);
+          nbar(1, 256);
         }
-        mbar_wait(xy_full, g_it & 1);
+        mbar_wait(&xy_full[b], (uint32_t)((g / p.nbuf) & 1));
         tc_fence_after();
-        for (int c0 = 0; c0 < NX; c0 += 32) {
-          uint32_t x[32], y[32];
-          tmem_ld32_nowait(trow + c0, x);
-          tmem_ld32_nowait(trow + colY + c0, y);
-          tmem_ld_wait();
-          uint32_t pp[16], pd[16];
+        const int c0 = 32 * half;             // this warp's 32 block columns
+        uint32_t x[32], y[32];
+        tmem_ld32_nowait(trow + 128 * b + c0, x);
+        tmem_ld32_nowait(trow + 128 * b + 64 + c0, y);
+        tmem_ld_wait();
+        uint32_t pp[16], pd[16];
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            float P2[2], S2[2];
+        for (int i = 0; i < 32; i += 2) {
+          float P2[2], S2[2];
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int col = g0 + c0 + i + e;
-              float L, Dv;
-              bool ok;
-              if (KA) {   // row = key, col = query
-                L = sL[c0 + i + e];
-                Dv = sD[c0 + i + e];
-                ok = col >= row && col < p.s;
-              } else {    // row = query, col = key
-                L = Lr;
-                Dv = Dr;
-                ok = col <= row;
-              }
-              const float P = ok ? ex2_approx(fmaf(__uint_as_float(x[i + e]), p.c1, -L)) : 0.f;
-              P2[e] = P;
-              S2[e] = P * (__uint_as_float(y[i + e]) - Dv) * p.alpha;
+          for (int e = 0; e < 2; ++e) {
+            const int col = g0 + c0 + i + e;
+            float L, Dv;
+            bool ok;
+            if (KA) {   // row = key, col = query
+              L = sL[sb][c0 + i + e];
+              Dv = sD[sb][c0 + i + e];
+              ok = col >= row && col < p.s;
+            } else {    // row = query, col = key
+              L = Lr;
+              Dv = Dr;
+              ok = col <= row;
             }
-            pp[i / 2] = pack_bf16(P2[0], P2[1]);
-            pd[i / 2] = pack_bf16(S2[0], S2[1]);
+            const float P = ok ? ex2_approx(fmaf(__uint_as_float(x[i + e]), p.c1, -L)) : 0.f;
+            P2[e] = P;
+            S2[e] = P * (__uint_as_float(y[i + e]) - Dv) * p.alpha;
           }
-          if (KA) tmem_st16(trow + c0 / 2, pp);
-          tmem_st16(trow + colY + c0 / 2, pd);
+          pp[i / 2] = pack_bf16(P2[0], P2[1]);
+          pd[i / 2] = pack_bf16(S2[0], S2[1]);
         }
+        if (KA) tmem_st16(trow + 128 * b + c0, pp);
+        tmem_st16(trow + 128 * b + 64 + c0, pd);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(pd_ready);
-        if (KA) nbar(1, 128);                 // sL / sD are rewritten by the next block
+        if (lane == 0) mbar_arrive(&pd_ready[b]);
       }
       // drain the accumulators of the unit: KA -> dV (acc_a), dK (acc_b); else dQ (acc_b)
       mbar_wait(acc_full, u & 1);
       tc_fence_after();
       __nv_bfloat16* base = p.dq + (long long)z2 * p.s * p.ldq + (long long)z1 * p.d;
+      const int r0w = r0 + q * 32;
       for (int which = KA ? 0 : 1; which < 2; ++which) {
         const uint32_t ca = which == 0 ? colA : colB;
-        __nv_bfloat16* dst = base + (KA ? (which == 0 ? 2 * p.h : p.h) : 0) + (long long)row * p.ldq;
-        for (int c0 = 0; c0 < p.nv; c0 += 32) {
+        __nv_bfloat16* gb = base + (KA ? (which == 0 ? 2 * p.h : p.h) : 0);
+        for (int cc = 0; cc < p.nv / 2; cc += 32) {
+          const int oc = half * (p.nv / 2) + cc;
           uint32_t r[32];
-          tmem_ld32(trow + ca + c0, r);
-          if (row < p.s) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              const int col = c0 + i;
-              if (col < p.d)
-                *reinterpret_cast<uint32_t*>(dst + col) =
-                    pack_bf16(__uint_as_float(r[i]), __uint_as_float(r[i + 1]));
-            }
-          }
+          tmem_ld32(trow + ca + oc, r);
+          store_chunk32(stg, lane, r, 1.f, gb, p.ldq, r0w, p.s, oc, p.d);
         }
       }
       tc_fence_before();
@@ -691,7 +745,6 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   AttnBwdParams p;
   p.s = s; p.heads = heads; p.d = d; p.nv = nv;
-  p.qb = nv <= 128 ? 128 : 64;
   p.nq = (s + 127) / 128;
   p.nk = (s + 127) / 128;
   p.c1 = alpha * 1.4426950408889634f;
@@ -701,14 +754,16 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   p.dq = static_cast<__nv_bfloat16*>(dqkv);
   p.ldq = ldq;
   p.h = heads * d;
-  const int max_smem = 227 * 1024 - 2048 - 1024;
+  const int max_smem = 227 * 1024 - 1024 - 256 - 18 * 1024;   // dynamic budget beside static
   for (int ka = 1; ka >= 0; --ka) {
-    const int GR = ka ? p.qb : 128;
-    const int f_bytes = nv * 128 * 2, g_bytes = nv * GR * 2;
-    int stages = 2;
-    while (stages > 1 && 2 * f_bytes + stages * 2 * g_bytes > max_smem) --stages;
+    const int f_bytes = nv * 128 * 2, g_bytes = nv * GRB * 2;
+    int stages = 4;
+    while (stages > 2 && 2 * f_bytes + stages * 2 * g_bytes > max_smem) --stages;
     if (2 * f_bytes + stages * 2 * g_bytes > max_smem) return -1;
     p.stages = stages;
+    // X / Y double buffer (256 TMEM columns) when the accumulators fit beside it
+    p.nbuf = (256 + (ka ? 2 * nv : nv) <= 512) ? 2 : 1;
+    if (128 * p.nbuf + (ka ? 2 * nv : nv) > 512) return -1;
     p.total = b * heads * (ka ? p.nk : p.nq);
     const int smem = 2 * f_bytes + stages * 2 * g_bytes + 1024 + 256;
     void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, AttnBwdParams) =

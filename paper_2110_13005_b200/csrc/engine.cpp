@@ -168,7 +168,10 @@ static int plan_memory(Ctx* c) {
       st.qkv = c->dalloc((size_t)c->M * c->lq * 2);
       if (st.qkv && c->dp != c->d && cudaMemset(st.qkv, 0, (size_t)c->M * c->lq * 2) != cudaSuccess)
         return c->fail(AXONN_ERR_CUDA, "memset qkv padding");
-      st.P = c->dalloc(att * 2);
+      if (c->flash_attn())
+        st.lse = (float*)c->dalloc((size_t)c->microbatch * c->heads * c->s * 4);
+      else
+        st.P = c->dalloc(att * 2);
       st.o = c->dalloc(Mh * 2);
       st.x1 = c->dalloc(Mh * 2);
       st.w = c->dalloc(Mh * 2);
@@ -179,7 +182,7 @@ static int plan_memory(Ctx* c) {
       st.rstd1 = (float*)c->dalloc(c->M * 4);
       st.mean2 = (float*)c->dalloc(c->M * 4);
       st.rstd2 = (float*)c->dalloc(c->M * 4);
-      if (!st.u || !st.qkv || !st.P || !st.o || !st.x1 || !st.w || !st.pre || !st.act || !st.out ||
+      if (!st.u || !st.qkv || !(st.P || st.lse) || !st.o || !st.x1 || !st.w || !st.pre || !st.act || !st.out ||
           !st.mean1 || !st.rstd1 || !st.mean2 || !st.rstd2)
         return c->fail(AXONN_ERR_OOM, "activation stash allocation");
     }
@@ -192,8 +195,13 @@ static int plan_memory(Ctx* c) {
     if (!c->last) sl.grecv = c->dalloc(Mh * 2);
     if (!sl.in) return c->fail(AXONN_ERR_OOM, "slot allocation");
   }
-  c->S = (float*)c->dalloc(att * 4);
-  c->dS = c->dalloc(att * 2);
+  if (c->flash_attn()) {   // S, P, dS never materialised
+    c->attn_D = (float*)c->dalloc((size_t)c->microbatch * c->heads * c->s * 4);
+    if (!c->attn_D) return c->fail(AXONN_ERR_OOM, "attention workspace");
+  } else {
+    c->S = (float*)c->dalloc(att * 4);
+    c->dS = c->dalloc(att * 2);
+  }
   c->dh0 = c->dalloc(Mh * 2);
   c->dh1 = c->dalloc(Mh * 2);
   c->dqkv = c->dalloc(3 * Mh * 2);
@@ -214,7 +222,7 @@ static int plan_memory(Ctx* c) {
   c->row_loss = (float*)c->dalloc(c->M * 4);
   c->d_loss = (double*)c->dalloc(64);
   if (c->last) c->logits = c->dalloc((size_t)c->M * c->V * 2);
-  if (!c->S || !c->dS || !c->dh0 || !c->dh1 || !c->dqkv || !c->dpre || !c->dO || !c->du ||
+  if ((!c->flash_attn() && (!c->S || !c->dS)) || !c->dh0 || !c->dh1 || !c->dqkv || !c->dpre || !c->dO || !c->du ||
       !c->dx1 || !c->cs_ws || !c->cs_ws_ln || !c->row_loss || !c->d_loss || (c->last && !c->logits))
     return c->fail(AXONN_ERR_OOM, "workspace allocation");
   if (cudaMallocHost(&c->h_loss, 64) != cudaSuccess) return c->fail(AXONN_ERR_OOM, "pinned loss");

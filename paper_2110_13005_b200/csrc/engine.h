@@ -29,6 +29,7 @@ struct LayerOff {
 struct LayerStash {
   void *u, *qkv, *P, *o, *x1, *w, *pre, *act, *out;
   float *mean1, *rstd1, *mean2, *rstd2;
+  float* lse = nullptr;               // fused attention: log2-domain row normaliser [b*heads*s]
 };
 
 // One in-flight microbatch on this stage (pipeline_limit of them, Alg. 2).
@@ -147,6 +148,16 @@ struct Ctx {
     }
     return softmax_mode && s <= 512 && s % 32 == 0;
   }
+  int flash_mode = -1;                // AXONN_FLASH_ATTN=0 -> GEMM + row-softmax attention path
+  bool flash_attn() {
+    if (flash_mode < 0) {
+      const char* e = getenv("AXONN_FLASH_ATTN");
+      flash_mode = (e && e[0] == '0') ? 0 : 1;
+    }
+    return flash_mode && s <= 512 && d % 2 == 0 && ((dp + 63) / 64) * 64 <= 256;
+  }
+  float* attn_D = nullptr;            // fused attention backward workspace (D = dO . O)
+  int attn_call(bool fwd, LayerStash& st);   // K2 launch (+ profiling events)
   int forward(Slot& sl, int mb);          // nn_shard.Forward (and the loss on the last stage)
   int backward(Slot& sl, int mb, const void* dout);   // nn_shard.Backward
   int layer_fwd(int li, const void* x, LayerStash& st);

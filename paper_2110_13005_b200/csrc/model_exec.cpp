@@ -71,6 +71,32 @@ int Ctx::gemm(GemmArgs g, double flops) {
   return 0;
 }
 
+int Ctx::attn_call(bool fwd, LayerStash& st) {
+  const int b = microbatch;
+  const float alpha = 1.0f / sqrtf((float)d);
+  ProfRec pr{};
+  if (prof_mb) {
+    pr.a = ev();
+    pr.b = ev();
+    // executed (causal) FLOPs: fwd Q K^T + P V, bwd recomputed S + dP + 3 accumulations
+    const double half = 2.0 * b * heads * (double)s * s * dp / 2;
+    pr.work = fwd ? 2 * half : 5 * half;
+    pr.kind = 2;
+    pr.key = fwd ? "attn_fwd (fused)" : "attn_bwd (fused)";
+    cudaEventRecord(pr.a, s_comp);
+  }
+  int rc = fwd ? attn_fwd(st.qkv, lq, b, heads, s, d, dp, alpha, st.o, h, st.lse, s_comp)
+               : attn_bwd(st.qkv, lq, dO, st.o, h, st.lse, attn_D, b, heads, s, d, dp, alpha, dqkv,
+                          3LL * h, s_comp);
+  launches += fwd ? 1 : 3;
+  if (rc) return fail(AXONN_ERR_CUDA, std::string("attention kernel failed rc=") + std::to_string(rc));
+  if (prof_mb) {
+    cudaEventRecord(pr.b, s_comp);
+    prof.push_back(pr);
+  }
+  return 0;
+}
+
 static GemmArgs lin_fwd(const void* X, const void* W, int M, int N, int K, void* out) {
   GemmArgs g;
   memset(&g, 0, sizeof(g));
@@ -129,34 +155,38 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
     if (dp != d) { g.col_group_in = d; g.col_group_out = dp; }
     TRY(gemm(g, 2 * dM * 3 * dh * dh));
   }
-  {  // S = Q K^T / sqrt(d) per (sample, head), causal tile skipping (D-7, D-8)
-    GemmArgs g;
-    memset(&g, 0, sizeof(g));
-    g.M = s; g.N = s; g.K = dp; g.Z = b * heads; g.Z1 = heads;
-    g.A = st.qkv; g.lda = lq; g.a_s1 = dp; g.a_s2 = (long long)s * lq;
-    g.B = static_cast<char*>(st.qkv) + (size_t)heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
-    g.b_s2 = (long long)s * lq;
-    g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
-    g.epi = EPI_F32; g.causal = 1; g.alpha = 1.0f / sqrtf((float)d);
-    if (fused_softmax()) {   // softmax in the epilogue: P straight from TMEM
-      g.C = st.P;
-      g.epi = EPI_SOFTMAX;
-      TRY(gemm(g, -1));
-    } else {
-      TRY(gemm(g, -1));
-      KCHK(softmax_fwd(S, (long long)b * heads * s, s, st.P, s_comp));
+  if (flash_attn()) {   // K2: o = softmax_causal(Q K^T / sqrt(d)) V, S and P stay in TMEM
+    TRY(attn_call(true, st));
+  } else {
+    {  // S = Q K^T / sqrt(d) per (sample, head), causal tile skipping (D-7, D-8)
+      GemmArgs g;
+      memset(&g, 0, sizeof(g));
+      g.M = s; g.N = s; g.K = dp; g.Z = b * heads; g.Z1 = heads;
+      g.A = st.qkv; g.lda = lq; g.a_s1 = dp; g.a_s2 = (long long)s * lq;
+      g.B = static_cast<char*>(st.qkv) + (size_t)heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
+      g.b_s2 = (long long)s * lq;
+      g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
+      g.epi = EPI_F32; g.causal = 1; g.alpha = 1.0f / sqrtf((float)d);
+      if (fused_softmax()) {   // softmax in the epilogue: P straight from TMEM
+        g.C = st.P;
+        g.epi = EPI_SOFTMAX;
+        TRY(gemm(g, -1));
+      } else {
+        TRY(gemm(g, -1));
+        KCHK(softmax_fwd(S, (long long)b * heads * s, s, st.P, s_comp));
+      }
     }
-  }
-  {  // o = P V, heads merged into [M, h]
-    GemmArgs g;
-    memset(&g, 0, sizeof(g));
-    g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
-    g.A = st.P; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s;
-    g.B = static_cast<char*>(st.qkv) + (size_t)2 * heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
-    g.b_s2 = (long long)s * lq; g.b_mn = 1;
-    g.C = st.o; g.ldc = h; g.c_s1 = d; g.c_s2 = (long long)s * h;
-    g.epi = EPI_BF16; g.causal = 2;
-    TRY(gemm(g, -1));
+    {  // o = P V, heads merged into [M, h]
+      GemmArgs g;
+      memset(&g, 0, sizeof(g));
+      g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
+      g.A = st.P; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s;
+      g.B = static_cast<char*>(st.qkv) + (size_t)2 * heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
+      g.b_s2 = (long long)s * lq; g.b_mn = 1;
+      g.C = st.o; g.ldc = h; g.c_s1 = d; g.c_s2 = (long long)s * h;
+      g.epi = EPI_BF16; g.causal = 2;
+      TRY(gemm(g, -1));
+    }
   }
   {
     GemmArgs g = lin_fwd(st.o, p16(o.w_o), M, h, h, st.x1);
@@ -228,59 +258,63 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   }
   wg_guard(dqkv);
   // attention backward
-  {  // dP = dO V^T (fp32 into S)
-    GemmArgs g;
-    memset(&g, 0, sizeof(g));
-    g.M = s; g.N = s; g.K = dp; g.Z = b * heads; g.Z1 = heads;
-    g.A = dO; g.lda = (long long)heads * dp; g.a_s1 = dp; g.a_s2 = (long long)s * heads * dp;
-    g.B = static_cast<char*>(st.qkv) + (size_t)2 * heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
-    g.b_s2 = (long long)s * lq;
-    g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
-    g.epi = EPI_F32; g.causal = 1;
-    if (fused_softmax()) {   // dS = P * (dP - rowsum(P dP)) / sqrt(d) in the epilogue
-      g.C = dS;
-      g.epi = EPI_SOFTMAX_BWD;
-      g.aux = st.P;
-      g.alpha = 1.0f / sqrtf((float)d);
-      TRY(gemm(g, -1));
-    } else {
-      TRY(gemm(g, -1));
-      KCHK(softmax_bwd(st.P, S, (long long)b * heads * s, s, 1.0f / sqrtf((float)d), dS, s_comp));
+  if (flash_attn()) {   // K2 backward: dQ, dK, dV straight into dqkv (P recomputed)
+    TRY(attn_call(false, st));
+  } else {
+    {  // dP = dO V^T (fp32 into S)
+      GemmArgs g;
+      memset(&g, 0, sizeof(g));
+      g.M = s; g.N = s; g.K = dp; g.Z = b * heads; g.Z1 = heads;
+      g.A = dO; g.lda = (long long)heads * dp; g.a_s1 = dp; g.a_s2 = (long long)s * heads * dp;
+      g.B = static_cast<char*>(st.qkv) + (size_t)2 * heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
+      g.b_s2 = (long long)s * lq;
+      g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
+      g.epi = EPI_F32; g.causal = 1;
+      if (fused_softmax()) {   // dS = P * (dP - rowsum(P dP)) / sqrt(d) in the epilogue
+        g.C = dS;
+        g.epi = EPI_SOFTMAX_BWD;
+        g.aux = st.P;
+        g.alpha = 1.0f / sqrtf((float)d);
+        TRY(gemm(g, -1));
+      } else {
+        TRY(gemm(g, -1));
+        KCHK(softmax_bwd(st.P, S, (long long)b * heads * s, s, 1.0f / sqrtf((float)d), dS, s_comp));
+      }
     }
-  }
-  {  // dQ = dS K  -> dqkv[:, 0:h]
-    GemmArgs g;
-    memset(&g, 0, sizeof(g));
-    g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
-    g.A = dS; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s;
-    g.B = static_cast<char*>(st.qkv) + (size_t)heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
-    g.b_s2 = (long long)s * lq; g.b_mn = 1;
-    g.C = dqkv; g.ldc = 3 * h; g.c_s1 = d; g.c_s2 = (long long)s * 3 * h;
-    g.epi = EPI_BF16; g.causal = 2;
-    TRY(gemm(g, -1));
-  }
-  {  // dK = dS^T Q -> dqkv[:, h:2h]
-    GemmArgs g;
-    memset(&g, 0, sizeof(g));
-    g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
-    g.A = dS; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s; g.a_mn = 1;
-    g.B = st.qkv; g.ldb = lq; g.b_s1 = dp; g.b_s2 = (long long)s * lq; g.b_mn = 1;
-    g.C = static_cast<char*>(dqkv) + (size_t)h * 2; g.ldc = 3 * h; g.c_s1 = d;
-    g.c_s2 = (long long)s * 3 * h;
-    g.epi = EPI_BF16; g.causal = 3;
-    TRY(gemm(g, -1));
-  }
-  {  // dV = P^T dO -> dqkv[:, 2h:3h]
-    GemmArgs g;
-    memset(&g, 0, sizeof(g));
-    g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
-    g.A = st.P; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s; g.a_mn = 1;
-    g.B = dO; g.ldb = (long long)heads * dp; g.b_s1 = dp; g.b_s2 = (long long)s * heads * dp;
-    g.b_mn = 1;
-    g.C = static_cast<char*>(dqkv) + (size_t)2 * h * 2; g.ldc = 3 * h; g.c_s1 = d;
-    g.c_s2 = (long long)s * 3 * h;
-    g.epi = EPI_BF16; g.causal = 3;
-    TRY(gemm(g, -1));
+    {  // dQ = dS K  -> dqkv[:, 0:h]
+      GemmArgs g;
+      memset(&g, 0, sizeof(g));
+      g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
+      g.A = dS; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s;
+      g.B = static_cast<char*>(st.qkv) + (size_t)heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
+      g.b_s2 = (long long)s * lq; g.b_mn = 1;
+      g.C = dqkv; g.ldc = 3 * h; g.c_s1 = d; g.c_s2 = (long long)s * 3 * h;
+      g.epi = EPI_BF16; g.causal = 2;
+      TRY(gemm(g, -1));
+    }
+    {  // dK = dS^T Q -> dqkv[:, h:2h]
+      GemmArgs g;
+      memset(&g, 0, sizeof(g));
+      g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
+      g.A = dS; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s; g.a_mn = 1;
+      g.B = st.qkv; g.ldb = lq; g.b_s1 = dp; g.b_s2 = (long long)s * lq; g.b_mn = 1;
+      g.C = static_cast<char*>(dqkv) + (size_t)h * 2; g.ldc = 3 * h; g.c_s1 = d;
+      g.c_s2 = (long long)s * 3 * h;
+      g.epi = EPI_BF16; g.causal = 3;
+      TRY(gemm(g, -1));
+    }
+    {  // dV = P^T dO -> dqkv[:, 2h:3h]
+      GemmArgs g;
+      memset(&g, 0, sizeof(g));
+      g.M = s; g.N = dp; g.K = s; g.Z = b * heads; g.Z1 = heads; g.n_valid = d;
+      g.A = st.P; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)heads * s * s; g.a_mn = 1;
+      g.B = dO; g.ldb = (long long)heads * dp; g.b_s1 = dp; g.b_s2 = (long long)s * heads * dp;
+      g.b_mn = 1;
+      g.C = static_cast<char*>(dqkv) + (size_t)2 * h * 2; g.ldc = 3 * h; g.c_s1 = d;
+      g.c_s2 = (long long)s * 3 * h;
+      g.epi = EPI_BF16; g.causal = 3;
+      TRY(gemm(g, -1));
+    }
   }
   // QKV: du = dqkv Wqkv;  dWqkv += dqkv^T u;  dbqkv += colsum(dqkv)
   wg_fork();
