@@ -62,6 +62,14 @@ __device__ __forceinline__ uint32_t p_col(int key) {
   return key < 256 ? (uint32_t)(key >> 1) : (uint32_t)(256 + (key >> 1));
 }
 
+// Static "snake" schedule over work-sorted units: unit list ordered heaviest tile first
+// (all (sample, head) of the heaviest causal tile, then the next), dealt to the CTAs
+// boustrophedon (round r forward when r is even, backward when odd) so per-CTA work stays
+// within one unit of the mean even though causal tiles differ 4x in cost.
+__device__ __forceinline__ int snake_unit(int r) {
+  return r * (int)gridDim.x + ((r & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
+}
+
 struct AttnParams {
   int s, heads, d, nv, num_m, total;
   float c1;               // alpha * log2(e)
@@ -110,8 +118,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
-      const int z = t / p.num_m, m0 = (p.num_m - 1 - t % p.num_m) * QT;
+    for (int rnd = 0;; ++rnd) {
+      const int t = snake_unit(rnd);
+      if (t >= p.total) break;
+      const int nz = p.total / p.num_m;
+      const int z = t % nz, m0 = (p.num_m - 1 - t / nz) * QT;
       const int z1 = z % p.heads, z2 = z / p.heads;
       const int kv = min(p.s, m0 + QT);
       const int nh = kv > 256 ? 2 : 1;
@@ -148,8 +159,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
-      const int m0 = (p.num_m - 1 - t % p.num_m) * QT;
+    for (int rnd = 0;; ++rnd, ++it) {
+      const int t = snake_unit(rnd);
+      if (t >= p.total) break;
+      const int nz = p.total / p.num_m;
+      const int m0 = (p.num_m - 1 - t / nz) * QT;
       const int kv = min(p.s, m0 + QT);
       const int nh = kv > 256 ? 2 : 1;
       mbar_wait(t_free, (it & 1) ^ 1);
@@ -197,8 +211,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     const int rl = q * 32 + lane;
     uint4* stg = stg_all[wi];
     int it = 0;
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
-      const int z = t / p.num_m, m0 = (p.num_m - 1 - t % p.num_m) * QT;
+    for (int rnd = 0;; ++rnd, ++it) {
+      const int t = snake_unit(rnd);
+      if (t >= p.total) break;
+      const int nz = p.total / p.num_m;
+      const int z = t % nz, m0 = (p.num_m - 1 - t / nz) * QT;
       const int z1 = z % p.heads, z2 = z / p.heads;
       const int kv = min(p.s, m0 + QT);
       const int kv64 = (kv + 63) / 64 * 64;
@@ -434,8 +451,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   // m descending (most key blocks first)
   auto unit = [&](int t, int& z, int& r0, int& i0, int& ni) {
     const int per = KA ? p.nk : p.nq;
-    z = t / per;
-    const int k = t % per;
+    const int nz = p.total / per;
+    z = t % nz;
+    const int k = t / nz;                // heaviest tiles first (snake_unit deals them)
     if (KA) {
       r0 = k * 128;                     // keys [r0, r0 + 128)
       i0 = r0 / GR;                     // first query block touching the diagonal
@@ -452,7 +470,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int u = 0;
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++u) {
+    for (int rnd = 0;; ++rnd, ++u) {
+      const int t = snake_unit(rnd);
+      if (t >= p.total) break;
       int z, r0, i0, ni;
       unit(t, z, r0, i0, ni);
       const int z1 = z % p.heads, z2 = z / p.heads;
@@ -506,7 +526,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       __syncwarp();
     };
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++u) {
+    for (int rnd = 0;; ++rnd, ++u) {
+      const int t = snake_unit(rnd);
+      if (t >= p.total) break;
       int z, r0, i0, ni;
       unit(t, z, r0, i0, ni);
       mbar_wait(f_full, u & 1);
@@ -559,7 +581,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
     uint4* stg = stg_all[wi];
     int u = 0, g = 0;
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++u) {
+    for (int rnd = 0;; ++rnd, ++u) {
+      const int t = snake_unit(rnd);
+      if (t >= p.total) break;
       int z, r0, i0, ni;
       unit(t, z, r0, i0, ni);
       const int z1 = z % p.heads, z2 = z / p.heads;
@@ -651,26 +675,41 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   }
 }
 
-// D[z * s + i] = sum_j dO[i, head, j] * O[i, head * d + j]   (fp32), one warp per (token, head)
+// D[z * s + i] = sum_j dO[i, head, j] * O[i, head * d + j]   (fp32); 16 lanes per (token, head),
+// 8 elements per lane per step (16-byte loads when the head width allows)
 __global__ void attn_bwd_d_kernel(const __nv_bfloat16* __restrict__ dO, long long ld_do, int dp,
                                   const __nv_bfloat16* __restrict__ O, long long ld_o, int d,
                                   int s, int heads, long long ntok, float* __restrict__ D) {
-  const long long w = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 16;
+  const int l = threadIdx.x & 15;
   if (w >= ntok * heads) return;
   const long long tok = w / heads;
   const int hd = (int)(w % heads);
   const __nv_bfloat16* a = dO + tok * ld_do + (long long)hd * dp;
   const __nv_bfloat16* b = O + tok * ld_o + (long long)hd * d;
   float acc = 0.f;
-  for (int j = 2 * lane; j < d; j += 64) {
-    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + j));
-    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(b + j));
-    acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+  if ((d & 7) == 0 && (dp & 7) == 0) {
+    for (int j = 8 * l; j < d; j += 128) {
+      const uint4 x = *reinterpret_cast<const uint4*>(a + j);
+      const uint4 y = *reinterpret_cast<const uint4*>(b + j);
+      const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&x);
+      const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 xf = __bfloat1622float2(xh[e]), yf = __bfloat1622float2(yh[e]);
+        acc = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, acc));
+      }
+    }
+  } else {
+    for (int j = 2 * l; j < d; j += 32) {
+      const float2 xf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + j));
+      const float2 yf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(b + j));
+      acc = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, acc));
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) {
+  for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (l == 0) {
     const long long sample = tok / s, i = tok % s;
     D[(sample * heads + hd) * s + i] = acc;
   }
@@ -725,9 +764,8 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   if (nv > 256) return -1;
   const long long ntok = (long long)b * s;
   {
-    const int wpb = 8;
-    const long long nw = ntok * heads;
-    attn_bwd_d_kernel<<<(unsigned)((nw + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
+    const long long nthreads = ntok * heads * 16;
+    attn_bwd_d_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(dO), (long long)heads * dp, dp,
         static_cast<const __nv_bfloat16*>(o), ldo, d, s, heads, ntok, Dbuf);
   }
