@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -350,6 +351,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 // warp (q, half) owns TMEM lanes [32 q, +32) and block columns [32 half, +32).
 struct AttnBwdParams {
   int s, heads, d, nv, nq, nk, total, stages, nbuf;
+  int nfb, nab;        // row-operand smem buffers, accumulator TMEM buffers (1 or 2 each)
+  int dbg;             // AXONN_ATTN_DBG experiments: 1 no epilogue math, 2 no accumulation MMAs
   float c1, alpha;
   const float* lse;
   const float* D;
@@ -415,31 +418,32 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   constexpr int FR = 128, GR = GRB;
   const int f_bytes = p.nv * FR * 2;         // one row operand
   const int g_bytes = p.nv * GR * 2;         // one streamed operand
-  uint8_t* sF = smem;                        // F1, F2
-  uint8_t* sG = smem + 2 * f_bytes;          // ring: stage i holds G1, G2
+  uint8_t* sF = smem;                        // [nfb] x (F1, F2)
+  uint8_t* sG = smem + p.nfb * 2 * f_bytes;  // ring: stage i holds G1, G2
   uint64_t* bars = reinterpret_cast<uint64_t*>(sG + p.stages * 2 * g_bytes);
-  uint64_t* f_full = bars;
-  uint64_t* f_empty = bars + 1;
-  uint64_t* acc_full = bars + 2;
-  uint64_t* acc_free = bars + 3;             // 8 arrivals
-  uint64_t* xy_full = bars + 4;              // [2]
-  uint64_t* pd_ready = bars + 6;             // [2], 8 arrivals
-  uint64_t* acc_done = bars + 8;             // [2]
-  uint64_t* g_full = bars + 10;              // [4]
-  uint64_t* g_empty = bars + 14;             // [4]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* f_full = bars;                   // [2]
+  uint64_t* f_empty = bars + 2;              // [2]
+  uint64_t* acc_full = bars + 4;             // [2]
+  uint64_t* acc_free = bars + 6;             // [2], 8 arrivals
+  uint64_t* xy_full = bars + 8;              // [2]
+  uint64_t* pd_ready = bars + 10;            // [2], 8 arrivals
+  uint64_t* acc_done = bars + 12;            // [2]
+  uint64_t* g_full = bars + 14;              // [4]
+  uint64_t* g_empty = bars + 18;             // [4]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 22);
   __shared__ float sL[2][GR], sD[2][GR];
   __shared__ uint4 stg_all[8][32 * 4];
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // TMEM: buffer b: X [128 b, +64), Y [128 b + 64, +64); accumulators after the buffers
-  const uint32_t colA = 128 * p.nbuf, colB = colA + (KA ? p.nv : 0);
+  // accumulator buffer ab: colA(ab) = 128 nbuf + ab * (KA ? 2 nv : nv), colB = colA + (KA ? nv : 0)
+  const uint32_t acc_w = KA ? 2 * p.nv : p.nv;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapQ);
     tma_prefetch_desc(&mapK);
     tma_prefetch_desc(&mapV);
     tma_prefetch_desc(&mapO);
-    for (int i = 0; i < 18; ++i) mbar_init(&bars[i], (i == 3 || i == 6 || i == 7) ? 8 : 1);
+    for (int i = 0; i < 22; ++i) mbar_init(&bars[i], (i == 6 || i == 7 || i == 10 || i == 11) ? 8 : 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_holder);
@@ -476,11 +480,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       int z, r0, i0, ni;
       unit(t, z, r0, i0, ni);
       const int z1 = z % p.heads, z2 = z / p.heads;
-      mbar_wait(f_empty, (u & 1) ^ 1);
+      const int fb = u % p.nfb;
+      mbar_wait(&f_empty[fb], (uint32_t)(((u / p.nfb) & 1) ^ 1));
       if (elect_one()) {
-        mbar_arrive_expect_tx(f_full, 2 * f_bytes);
-        load_rows(sF, KA ? &mapK : &mapQ, f_full, p.nv, FR, r0, z1, z2);
-        load_rows(sF + f_bytes, KA ? &mapV : &mapO, f_full, p.nv, FR, r0, z1, z2);
+        uint8_t* f = sF + fb * 2 * f_bytes;
+        mbar_arrive_expect_tx(&f_full[fb], 2 * f_bytes);
+        load_rows(f, KA ? &mapK : &mapQ, &f_full[fb], p.nv, FR, r0, z1, z2);
+        load_rows(f + f_bytes, KA ? &mapV : &mapO, &f_full[fb], p.nv, FR, r0, z1, z2);
       }
       __syncwarp();
       for (int it = 0; it < ni; ++it) {
@@ -499,11 +505,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   } else if (warp == 1) {
     const uint32_t idXY = umma_idesc_bf16(128, GR, 0, 0);
     const uint32_t idAcc = umma_idesc_bf16(128, p.nv, 0, 1);
-    const uint32_t sF0 = smem_u32(sF), sG0 = smem_u32(sG);
+    const uint32_t sG0 = smem_u32(sG);
     int g = 0;                        // global block counter (stage / buffer / parity source)
     uint32_t accd_ph[2] = {0, 0};     // acc_done uses per buffer
     int accd_n[2] = {0, 0};
     int u = 0;
+    uint32_t sF0 = 0;                 // current unit's row operands
     auto issue_xy = [&](int gi) {     // X, Y of global block gi into buffer gi % nbuf
       const int b = gi % p.nbuf, stg = gi % p.stages;
       mbar_wait(&g_full[stg], (uint32_t)((gi / p.stages) & 1));
@@ -531,24 +538,32 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (t >= p.total) break;
       int z, r0, i0, ni;
       unit(t, z, r0, i0, ni);
-      mbar_wait(f_full, u & 1);
+      const int fb = u % p.nfb, ab = u % p.nab;
+      const uint32_t colA = 128 * p.nbuf + ab * acc_w, colB = colA + (KA ? p.nv : 0);
+      mbar_wait(&f_full[fb], (uint32_t)((u / p.nfb) & 1));
       tc_fence_after();
+      sF0 = smem_u32(sF + fb * 2 * f_bytes);
       const int g_first = g;
       issue_xy(g);
-      if (ni == 1 && elect_one()) mma_commit(f_empty);
+      if (ni == 1 && elect_one()) mma_commit(&f_empty[fb]);
       __syncwarp();
       for (int it = 0; it < ni; ++it, ++g) {
         const int b = g % p.nbuf, stg = g % p.stages;
         if (p.nbuf == 2 && it + 1 < ni) {
           issue_xy(g + 1);
-          if (it + 2 == ni && elect_one()) mma_commit(f_empty);
+          if (it + 2 == ni && elect_one()) mma_commit(&f_empty[fb]);
           __syncwarp();
         }
         mbar_wait(&pd_ready[b], (uint32_t)(((g - (p.nbuf == 2 ? 0 : 0)) / p.nbuf) & 1));
-        if (it == 0) mbar_wait(acc_free, (u & 1) ^ 1);
+        if (it == 0) mbar_wait(&acc_free[ab], (uint32_t)(((u / p.nab) & 1) ^ 1));
         tc_fence_after();
         const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
         if (elect_one()) {
+          if (p.dbg == 2) {
+            mma_commit(&g_empty[stg]);
+            mma_commit(&acc_done[b]);
+            if (it == ni - 1) mma_commit(&acc_full[ab]);
+          } else {
           // accumulate over the 64 rows of this block: A = packed P^T / dS (TMEM; columns of
           // the two 32-wide halves at +0 and +32), B = G operand MN-major
 #pragma unroll
@@ -563,14 +578,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           }
           mma_commit(&g_empty[stg]);
           mma_commit(&acc_done[b]);
-          if (it == ni - 1) mma_commit(acc_full);
+          if (it == ni - 1) mma_commit(&acc_full[ab]);
+          }
         }
         __syncwarp();
         accd_ph[b] ^= 1;
         ++accd_n[b];
         if (p.nbuf == 1 && it + 1 < ni) {
           issue_xy(g + 1);
-          if (it + 2 == ni && elect_one()) mma_commit(f_empty);
+          if (it + 2 == ni && elect_one()) mma_commit(&f_empty[fb]);
           __syncwarp();
         }
       }
@@ -610,6 +626,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
         mbar_wait(&xy_full[b], (uint32_t)((g / p.nbuf) & 1));
         tc_fence_after();
+        if (p.dbg == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&pd_ready[b]);
+          continue;
+        }
         const int c0 = 32 * half;             // this warp's 32 block columns
         uint32_t x[32], y[32];
         tmem_ld32_nowait(trow + 128 * b + c0, x);
@@ -648,7 +670,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         if (lane == 0) mbar_arrive(&pd_ready[b]);
       }
       // drain the accumulators of the unit: KA -> dV (acc_a), dK (acc_b); else dQ (acc_b)
-      mbar_wait(acc_full, u & 1);
+      const int ab = u % p.nab;
+      const uint32_t colA = 128 * p.nbuf + ab * acc_w, colB = colA + (KA ? p.nv : 0);
+      mbar_wait(&acc_full[ab], (uint32_t)((u / p.nab) & 1));
       tc_fence_after();
       __nv_bfloat16* base = p.dq + (long long)z2 * p.s * p.ldq + (long long)z1 * p.d;
       const int r0w = r0 + q * 32;
@@ -664,7 +688,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(acc_free);
+      if (lane == 0) mbar_arrive(&acc_free[ab]);
     }
   }
   tc_fence_before();
@@ -792,18 +816,37 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   p.dq = static_cast<__nv_bfloat16*>(dqkv);
   p.ldq = ldq;
   p.h = heads * d;
+  {
+    const char* e = getenv("AXONN_ATTN_DBG");
+    p.dbg = e ? atoi(e) : 0;
+  }
   const int max_smem = 227 * 1024 - 1024 - 256 - 18 * 1024;   // dynamic budget beside static
   for (int ka = 1; ka >= 0; --ka) {
     const int f_bytes = nv * 128 * 2, g_bytes = nv * GRB * 2;
+    // prefer: double row-operand buffer (next unit's loads overlap this unit), then ring depth
+    static int nfb_env = -1;
+    if (nfb_env < 0) {
+      const char* e = getenv("AXONN_ATTN_NFB");
+      nfb_env = e ? atoi(e) : 1;
+    }
+    p.nfb = nfb_env == 2 ? 2 : 1;
     int stages = 4;
-    while (stages > 2 && 2 * f_bytes + stages * 2 * g_bytes > max_smem) --stages;
-    if (2 * f_bytes + stages * 2 * g_bytes > max_smem) return -1;
+    while (stages > 2 && p.nfb * 2 * f_bytes + stages * 2 * g_bytes > max_smem) --stages;
+    if (p.nfb * 2 * f_bytes + stages * 2 * g_bytes > max_smem) {
+      p.nfb = 1;
+      stages = 4;
+      while (stages > 2 && 2 * f_bytes + stages * 2 * g_bytes > max_smem) --stages;
+    }
+    if (p.nfb * 2 * f_bytes + stages * 2 * g_bytes > max_smem) return -1;
     p.stages = stages;
-    // X / Y double buffer (256 TMEM columns) when the accumulators fit beside it
-    p.nbuf = (256 + (ka ? 2 * nv : nv) <= 512) ? 2 : 1;
-    if (128 * p.nbuf + (ka ? 2 * nv : nv) > 512) return -1;
+    // X / Y double buffer (256 TMEM columns) when the accumulators fit beside it; then
+    // double-buffered accumulators (the drain of unit u overlaps unit u+1)
+    const int accw = ka ? 2 * nv : nv;
+    p.nbuf = (256 + accw <= 512) ? 2 : 1;
+    if (128 * p.nbuf + accw > 512) return -1;
+    p.nab = (128 * p.nbuf + 2 * accw <= 512) ? 2 : 1;
     p.total = b * heads * (ka ? p.nk : p.nq);
-    const int smem = 2 * f_bytes + stages * 2 * g_bytes + 1024 + 256;
+    const int smem = p.nfb * 2 * f_bytes + stages * 2 * g_bytes + 1024 + 256;
     void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, AttnBwdParams) =
         ka ? attn_bwd_kernel<true> : attn_bwd_kernel<false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)

@@ -13,7 +13,10 @@ def main():
     from paper_2110_13005_b200 import _lib
     lib = _lib.load()
     st = torch.cuda.current_stream().cuda_stream
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     for tag, b, heads, s, d, dp in (("1.3B", 8, 16, 512, 128, 128), ("12B", 8, 24, 512, 188, 192)):
+        if only and tag != only:
+            continue
         lq = 3 * heads * dp
         qkv = (torch.randn(b * s, lq, device="cuda") * 0.5).to(torch.bfloat16)
         o = torch.empty(b * s, heads * d, device="cuda", dtype=torch.bfloat16)
@@ -24,11 +27,11 @@ def main():
             assert lib.axonn_k_attn_fwd(C.c_void_p(qkv.data_ptr()), lq, b, heads, s, d, dp, C.c_float(alpha),
                                         C.c_void_p(o.data_ptr()), heads * d, C.c_void_p(lse.data_ptr()),
                                         C.c_void_p(st)) == 0
-        for _ in range(5):
+        for _ in range(1 if only else 5):
             fwd()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n = 50
+        n = 3 if only else 50
         e0.record()
         for _ in range(n):
             fwd()
@@ -47,7 +50,7 @@ def main():
             assert lib.axonn_k_attn_bwd(P(qkv.data_ptr()), lq, P(dO.data_ptr()), P(o.data_ptr()), heads * d,
                                         P(lse.data_ptr()), P(dbuf.data_ptr()), b, heads, s, d, dp,
                                         C.c_float(alpha), P(dqkv.data_ptr()), 3 * heads * d, P(st)) == 0
-        for _ in range(5):
+        for _ in range(1 if only else 5):
             bwd()
         torch.cuda.synchronize()
         e0.record()
