@@ -41,10 +41,10 @@ CONFIGS = {
     "tiny": dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256,
                  g_inter=1, microbatch=2, mb_per_replica=4, offload=False),
     # BASELINE.json configs[2] proxy: the paper's 12B layer shape (Table I),
-    # 12 layers per stage as in the 4 x 2 grid, G_inter = N (pipeline), microbatch 8
+    # 12 layers per stage as in the 4 x 2 grid, G_inter = N (pipeline), microbatch 8, m = 64 per replica
     # (Table II), bucketed CPU-offloaded Adam (bsize 4M, k 4)
     "gpt12b-pipe": dict(layers_per_stage=12, hidden=4512, heads=24, seq_len=512, vocab=51200,
-                        g_inter="N", microbatch=8, mb_per_replica=16, offload=True),
+                        g_inter="N", microbatch=8, mb_per_replica=64, offload=True),
     # BASELINE.json configs[3] proxy: the 24B layer shape (d = 176), 6 layers per stage as in
     # 8 x 1, microbatch 4, offload on
     "gpt24b-pipe": dict(layers_per_stage=6, hidden=6336, heads=36, seq_len=512, vocab=51200,

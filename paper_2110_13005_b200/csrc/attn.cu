@@ -517,6 +517,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);   // last TS-MMA read of b
       tc_fence_after();
       const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
+      if (p.dbg == 4) {   // experiment: no X / Y MMAs
+        if (elect_one()) mma_commit(&xy_full[b]);
+        __syncwarp();
+        return;
+      }
       if (elect_one()) {
         for (int c = 0; c < p.nv / 64; ++c) {
 #pragma unroll
@@ -559,7 +564,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tc_fence_after();
         const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
         if (elect_one()) {
-          if (p.dbg == 2) {
+          if (p.dbg >= 2) {
             mma_commit(&g_empty[stg]);
             mma_commit(&acc_done[b]);
             if (it == ni - 1) mma_commit(&acc_full[ab]);
@@ -626,7 +631,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
         mbar_wait(&xy_full[b], (uint32_t)((g / p.nbuf) & 1));
         tc_fence_after();
-        if (p.dbg == 1) {
+        if (p.dbg == 1 || p.dbg == 3 || p.dbg == 4) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&pd_ready[b]);
