@@ -66,6 +66,11 @@ typedef struct {
   int64_t bucket_elems;                       /* bsize in elements (D-16); paper 4M */
   int coarsen_k;                              /* all-reduce chunk = k * bsize elements; paper 4 */
   int pipeline_limit;                         /* 0 -> G_inter */
+  int overlap_next_batch;                     /* 1: axonn_optimizer_step returns once every bucket is
+                                                 enqueued; the next axonn_run_batch starts at once and
+                                                 each layer's forward waits only for the buckets that
+                                                 hold its parameters (results are identical; reading
+                                                 D-32).  0: the step completes before returning. */
 } axonn_opt_cfg;
 
 /* Process placement in the G_inter x G_data grid: world_rank = j * G_inter + i

@@ -37,7 +37,8 @@ class OptCfg(C.Structure):
     _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
                 ("eps", C.c_double), ("weight_decay", C.c_double), ("loss_scale", C.c_double),
                 ("offload", C.c_int),
-                ("bucket_elems", C.c_int64), ("coarsen_k", C.c_int), ("pipeline_limit", C.c_int)]
+                ("bucket_elems", C.c_int64), ("coarsen_k", C.c_int), ("pipeline_limit", C.c_int),
+                ("overlap_next_batch", C.c_int)]
 
 
 class Dist(C.Structure):

@@ -2,6 +2,7 @@
 // message-driven scheduler over NCCL P2P, the column gradient all-reduce
 // (Alg. 1 l.13) chunked by k*bsize and the bucketed,
 // optionally host-offloaded AdamW overlapped with it.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -45,6 +46,15 @@ cudaEvent_t Ctx::ev() {
     ev_pool.push_back(e);
   }
   return ev_pool[ev_next++];
+}
+
+cudaEvent_t Ctx::ev_opt() {
+  if (ev_next_opt == ev_pool_opt.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ev_pool_opt.push_back(e);
+  }
+  return ev_pool_opt[ev_next_opt++];
 }
 
 static uint16_t f2bf(float f) {   // round-to-nearest-even (host side of theta16 writes)
@@ -428,6 +438,8 @@ AXONN_API void axonn_free(axonn_ctx* c) {
   if (c->h_loss) cudaFreeHost(c->h_loss);
   if (c->dtok) cudaFree(c->dtok);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_pool_opt) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_bucket) cudaEventDestroy(e);
   for (cudaEvent_t e : c->timer)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {c->ev_grads_ready, c->ev_opt_done, c->ev_loss})
@@ -787,8 +799,9 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
     CU(cudaMalloc(&c->dtok, need * 4));
     c->dtok_cap = need;
   }
-  // the next forward reads theta16 written by the previous optimizer step
-  CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
+  // the next forward reads theta16 written by the previous optimizer step: all of it, or
+  // (overlap_next_batch) per layer as its buckets complete (Ctx::wait_params)
+  if (!c->opt_pending) CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
   const size_t row0 = (size_t)c->replica * shard * (c->s + 1);   // Alg. 1 l.5
   if (on_device) {
     CU(cudaMemcpyAsync(c->dtok, tokens, need * 4, cudaMemcpyDeviceToDevice, c->s_comp));
@@ -803,6 +816,8 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   }
   int rc = run_pipeline(c, m);
   if (rc) return (axonn_status)rc;
+  // grad16 is still read by a pending optimizer step until it completes
+  if (c->opt_pending) CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
   // half-precision gradients (D-20: fp32 accumulation, bf16 reduction)
   if (cast_f32_bf16(c->grad32, c->grad16, c->nflat, c->s_comp)) return (axonn_status)c->fail(AXONN_ERR_CUDA, "cast");
   ++c->launches;
@@ -832,6 +847,11 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   CU(cudaEventSynchronize(ev_loss_host));
   if (loss_out) *loss_out = (float)(*c->h_loss / c->oc.loss_scale);
   c->grads_ready = true;
+  if (c->opt_pending) {   // the previous step has completed (the cast above waited for it)
+    c->opt_pending = false;
+    c->collect_stats();
+    c->prof_opt.clear();
+  }
   c->stats[AXONN_STAT_T_BATCH_MS] =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return AXONN_OK;
@@ -877,6 +897,16 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
   const int64_t ch = chunk_elems(c);
   int64_t chunk_idx = -1;
   int64_t bucket = 0;
+  const bool overlap = c->oc.overlap_next_batch != 0;
+  c->ev_next_opt = 0;
+  if (overlap) {
+    const size_t nb = (size_t)((c->nflat + bs - 1) / bs);
+    while (c->ev_bucket.size() < nb) {
+      cudaEvent_t e;
+      CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->ev_bucket.push_back(e);
+    }
+  }
   for (int64_t lo = 0; lo < c->nflat; lo += bs, ++bucket) {
     const int64_t n = std::min(bs, c->nflat - lo);
     const int64_t ci = lo / ch;
@@ -895,11 +925,12 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
       CU(cudaMemcpyAsync(c->ring[r][2], c->adam_v + lo, n * 4, cudaMemcpyHostToDevice, c->s_h2d));
       CU(cudaEventRecord(c->ev_h2d[r], c->s_h2d));
       CU(cudaStreamWaitEvent(c->s_opt, c->ev_h2d[r], 0));
-      if (c->profiling) { pr.a = c->ev(); pr.b = c->ev(); cudaEventRecord(pr.a, c->s_opt); }
+      if (c->profiling) { pr.a = c->ev_opt(); pr.b = c->ev_opt(); cudaEventRecord(pr.a, c->s_opt); }
       if (adamw_launch(n, g, c->ring[r][0], c->ring[r][1], c->ring[r][2], t16, sc, c->s_opt))
         return (axonn_status)c->fail(AXONN_ERR_CUDA, "adamw launch");
       if (c->profiling) { cudaEventRecord(pr.b, c->s_opt); pr.work = n * 28.0; pr.kind = 1; c->prof.push_back(pr); }
       CU(cudaEventRecord(c->ev_adam[r], c->s_opt));
+      if (overlap) CU(cudaEventRecord(c->ev_bucket[bucket], c->s_opt));
       CU(cudaStreamWaitEvent(c->s_d2h, c->ev_adam[r], 0));
       CU(cudaMemcpyAsync(c->master + lo, c->ring[r][0], n * 4, cudaMemcpyDeviceToHost, c->s_d2h));
       CU(cudaMemcpyAsync(c->adam_m + lo, c->ring[r][1], n * 4, cudaMemcpyDeviceToHost, c->s_d2h));
@@ -908,10 +939,11 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
       c->stats[AXONN_STAT_H2D_BYTES] += n * 12.0;
       c->stats[AXONN_STAT_D2H_BYTES] += n * 12.0;
     } else {
-      if (c->profiling) { pr.a = c->ev(); pr.b = c->ev(); cudaEventRecord(pr.a, c->s_opt); }
+      if (c->profiling) { pr.a = c->ev_opt(); pr.b = c->ev_opt(); cudaEventRecord(pr.a, c->s_opt); }
       if (adamw_launch(n, g, c->master + lo, c->adam_m + lo, c->adam_v + lo, t16, sc, c->s_opt))
         return (axonn_status)c->fail(AXONN_ERR_CUDA, "adamw launch");
       if (c->profiling) { cudaEventRecord(pr.b, c->s_opt); pr.work = n * 28.0; pr.kind = 1; c->prof.push_back(pr); }
+      if (overlap) CU(cudaEventRecord(c->ev_bucket[bucket], c->s_opt));
     }
     ++c->launches;
   }
@@ -921,16 +953,49 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
     CU(cudaStreamWaitEvent(c->s_opt, e, 0));
   }
   CU(cudaEventRecord(c->ev_opt_done, c->s_opt));
-  CU(cudaEventSynchronize(c->ev_opt_done));
   c->t_step = t;
   c->grads_ready = false;
   c->ev_chunk.clear();
+  if (overlap) {   // returns now; the next run_batch waits per layer (reading D-32)
+    for (ProfRec& p : c->prof)
+      if (p.kind == 1) c->prof_opt.push_back(p);
+    c->prof.erase(std::remove_if(c->prof.begin(), c->prof.end(),
+                                 [](const ProfRec& p) { return p.kind == 1; }),
+                  c->prof.end());
+    c->opt_pending = true;
+    c->stats[AXONN_STAT_T_OPT_MS] =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return AXONN_OK;
+  }
+  CU(cudaEventSynchronize(c->ev_opt_done));
   c->stats[AXONN_STAT_T_OPT_MS] =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  c->collect_stats();
+  return AXONN_OK;
+}
+
+}  // extern "C"
+
+namespace axonn {
+
+void Ctx::wait_params(int64_t off_end) {
+  if (!opt_pending || ev_bucket.empty()) return;
+  const int64_t bs = oc.bucket_elems;
+  int64_t b = (off_end - 1) / bs;
+  if (b >= (int64_t)ev_bucket.size()) b = (int64_t)ev_bucket.size() - 1;
+  cudaStreamWaitEvent(s_comp, ev_bucket[b], 0);
+}
+
+// kernel-time statistics (profiling mode) of the records of this batch and of the optimizer
+// step they belong with; every record's events have completed when this runs
+void Ctx::collect_stats() {
+  Ctx* c = this;
   // kernel-time statistics of this batch + step (profiling mode)
   double gms = 0, gfl = 0, ams = 0, aby = 0;
   int gl = 0;
-  for (const ProfRec& p : c->prof) {
+  std::vector<ProfRec> all(c->prof);
+  all.insert(all.end(), c->prof_opt.begin(), c->prof_opt.end());
+  for (const ProfRec& p : all) {
     float ms = 0;
     cudaEventElapsedTime(&ms, p.a, p.b);
     if (p.kind == 0) { gms += ms; gfl += p.work; ++gl; }
@@ -942,9 +1007,9 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
   c->stats[AXONN_STAT_ADAM_MS] = ams;
   c->stats[AXONN_STAT_ADAM_BYTES] = aby;
   c->stats[AXONN_STAT_KERNEL_LAUNCHES] = (double)c->launches;
-  if (!c->prof.empty()) {   // per-shape breakdown: {"key": [ms, work, launches], ...}
+  if (!all.empty()) {   // per-shape breakdown: {"key": [ms, work, launches], ...}
     std::map<std::string, double[3]> agg;
-    for (const ProfRec& p : c->prof) {
+    for (const ProfRec& p : all) {
       float ms = 0;
       cudaEventElapsedTime(&ms, p.a, p.b);
       const std::string k = p.kind == 1 ? "adamw" : p.key;
@@ -961,7 +1026,10 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
     }
     c->prof_json = js + "}";
   }
-  return AXONN_OK;
 }
+
+}  // namespace axonn
+
+extern "C" {
 
 }  // extern "C"

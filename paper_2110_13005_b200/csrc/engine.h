@@ -124,12 +124,21 @@ struct Ctx {
   std::vector<char> grad_written;
   bool profiling = false;
   std::vector<ProfRec> prof;
+  // optimizer / next-batch overlap (overlap_next_batch, reading D-32)
+  bool opt_pending = false;           // an optimizer step is still running on s_opt
+  std::vector<cudaEvent_t> ev_bucket; // K9 of bucket b done (theta16 of the bucket written)
+  std::vector<ProfRec> prof_opt;      // AdamW records of the pending step
+  void wait_params(int64_t off_end);  // s_comp waits until theta16[0, off_end) is updated
+  void collect_stats();               // kernel-time statistics from completed records
   double stats[AXONN_STAT_COUNT] = {};
   std::string prof_json = "{}";       // per-shape K1 / K9 timing of the last profiled step
   long long launches = 0;
 
   // helpers
   cudaEvent_t ev();                   // next event from the pool (reset per batch)
+  std::vector<cudaEvent_t> ev_pool_opt;   // optimizer-step events (reset per step: they must
+  size_t ev_next_opt = 0;                 // outlive the overlapped next batch)
+  cudaEvent_t ev_opt();
   void* dalloc(size_t bytes);
   int check_cuda(cudaError_t e, const char* what);
   int check_nccl(ncclResult_t r, const char* what);
@@ -161,6 +170,9 @@ struct Ctx {
   int forward(Slot& sl, int mb);          // nn_shard.Forward (and the loss on the last stage)
   int backward(Slot& sl, int mb, const void* dout);   // nn_shard.Backward
   int layer_fwd(int li, const void* x, LayerStash& st);
+  int64_t layer_end(int li) const {   // one past the last flat element of layer li
+    return loff[li].b_fc2 + ((int64_t)h + 63) / 64 * 64;
+  }
   int layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void* din);
   void wg_fork();                       // s_wg waits for everything enqueued on s_comp so far
   void wg_note(const void* buf);        // s_wg reads buf (recorded after its last enqueued read)

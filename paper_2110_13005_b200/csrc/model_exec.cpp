@@ -340,13 +340,18 @@ int Ctx::forward(Slot& sl, int mb) {
   prof_mb = profiling && mb == cur_m - 1;
   const int b = microbatch;
   const int32_t* tok = dtok + (size_t)mb * b * (s + 1);
-  if (first) KCHK(embed_fwd(tok, s + 1, b, s, h, p16(tok_emb), p16(pos_emb), sl.in, s_comp));
+  if (first) {
+    wait_params(pos_emb + ((int64_t)s * h + 63) / 64 * 64);   // overlapped optimizer step (D-32)
+    KCHK(embed_fwd(tok, s + 1, b, s, h, p16(tok_emb), p16(pos_emb), sl.in, s_comp));
+  }
   const void* x = sl.in;
   for (int li = 0; li < nl; ++li) {
+    wait_params(layer_end(li));
     TRY(layer_fwd(li, x, sl.L[li]));
     x = sl.L[li].out;
   }
   if (!last) return 0;
+  wait_params(nflat);
   KCHK(ln_fwd(x, M, h, p16(lnf_g), p16(lnf_b), sl.hf, sl.meanf, sl.rstdf, s_comp));
   TRY(gemm(lin_fwd(sl.hf, p16(head_w), M, V, h, logits), 2.0 * M * V * h));
   const float coef = (float)(oc.loss_scale / ((double)cur_mtotal * (double)M));

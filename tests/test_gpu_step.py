@@ -167,3 +167,28 @@ def test_state_and_validation_errors():
     assert e.value.status == "STATE"
     eng.optimizer_step()
     eng.close()
+
+
+@pytest.mark.parametrize("offload", [0, 1])
+def test_overlapped_optimizer_equals_synchronous_bitwise(offload):
+    """Reading D-32: overlapping optimizer step t with batch t+1 (each layer's forward waits
+    only for the buckets holding its parameters) changes no value: losses, theta32, v and
+    theta16 after 3 steps are bitwise those of the synchronous schedule."""
+    from paper_2110_13005_b200.engine import T_ADAM_V, T_MASTER, T_PARAM16
+    cfg = MINI
+    params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=11)
+    tok = markov_tokens(16, cfg["seq_len"], cfg["vocab"], seed=5)
+    res = []
+    for ov in (False, True):
+        eng = make(cfg, offload=bool(offload), bucket_elems=40000, coarsen_k=2, overlap_next_batch=ov)
+        eng.write_all(T_MASTER, params)
+        losses = []
+        for _ in range(3):
+            losses.append(eng.run_batch(tok))
+            eng.optimizer_step()
+        res.append((losses, eng.read_all(T_MASTER), eng.read_all(T_ADAM_V), eng.read_all(T_PARAM16)))
+        eng.close()
+    assert res[0][0] == res[1][0]
+    for a, b in zip(res[0][1:], res[1][1:]):
+        for k in a:
+            assert np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)), k
