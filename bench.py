@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--layers", type=int, default=None, help="override n_layers (profiling runs only)")
     ap.add_argument("--mb-per-replica", type=int, default=None, help="microbatches per replica (m)")
     ap.add_argument("--offload", type=int, default=None, help="1/0: override the config's offload")
+    ap.add_argument("--g-inter", type=int, default=None,
+                    help="pipeline stages (pipeline configs; G_data = N / G_inter)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.layers:
@@ -199,8 +201,8 @@ def main():
         cfg["mb_per_replica"] = args.mb_per_replica
     if args.offload is not None:
         cfg["offload"] = bool(args.offload)
-    if cfg.get("g_inter") == "N":   # pipeline proxies: one stage per GPU
-        cfg["g_inter"] = int(os.environ.get("WORLD_SIZE", "1"))
+    if cfg.get("g_inter") == "N":   # pipeline proxies: one stage per GPU unless --g-inter
+        cfg["g_inter"] = args.g_inter or int(os.environ.get("WORLD_SIZE", "1"))
         cfg.setdefault("n_layers", cfg["layers_per_stage"] * cfg["g_inter"])
 
     from paper_2110_13005_b200 import dist as D
