@@ -126,6 +126,23 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def k1_traffic(cfg):
+    """roofline.traffic: DRAM bytes per K1 launch from the committed `ncu --set full` capture of
+    one layer's linear-layer GEMMs (profiles/r1/k1_traffic.json, scripts/ncu_traffic.py), beside
+    the algorithmic bytes per launch of the same launches (operands read once, outputs written
+    once).  null when no capture matches this model width."""
+    p = os.path.join(ROOT, "profiles", "r1", "k1_traffic.json")
+    if not os.path.exists(p):
+        return {"traffic": None}
+    d = json.load(open(p))
+    if d.get("hidden") != cfg["hidden"]:
+        return {"traffic": None}
+    return {"traffic": d["dram_bytes_per_launch_avg"],
+            "traffic_algorithmic": d.get("algorithmic_bytes_per_launch_avg"),
+            "traffic_unit": "bytes per K1 launch (average over one layer's 13 linear GEMMs)",
+            "traffic_src": "profiles/r1/k1_traffic.json (ncu --set full)"}
+
+
 def cpu_oracle_sample(cfg, steps: int = 1):
     """Time the oracle (as it stands) on a bounded sample of the same workload:
     one transformer layer of the configured shape as a middle pipeline stage
@@ -331,7 +348,7 @@ def main():
                          # timed step (same shapes each microbatch); share scaled by m
                          "events": "K1 launches of the last microbatch of each timed step",
                          "gemm_share_of_step": gemm_ms * m / args.steps / ms_step,
-                         "traffic": None},
+                         **k1_traffic(cfg)},
             "adam": {"achieved_gbs": adam_bytes / (adam_ms / 1e3) / 1e9 if adam_ms else None,
                      "peak_gbs": peaks["hbm"], "bytes_per_param": 28},
             "cpu_baseline": cpu,

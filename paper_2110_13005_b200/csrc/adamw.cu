@@ -39,11 +39,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(long long n, const __nv_bflo
                                                     AdamScalars s) {
   const long long nvec = n / 4;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
-    float4 th = reinterpret_cast<const float4*>(theta)[i];
-    float4 mm = reinterpret_cast<const float4*>(m)[i];
-    float4 vv = reinterpret_cast<const float4*>(v)[i];
-    uint2 graw = reinterpret_cast<const uint2*>(g16)[i];
+  auto step4 = [&](long long i, float4 th, float4 mm, float4 vv, uint2 graw) {
     __nv_bfloat162 g01 = *reinterpret_cast<__nv_bfloat162*>(&graw.x);
     __nv_bfloat162 g23 = *reinterpret_cast<__nv_bfloat162*>(&graw.y);
     __nv_bfloat16 o[4];
@@ -60,7 +56,25 @@ __global__ void __launch_bounds__(256) adamw_kernel(long long n, const __nv_bflo
     out.x = *reinterpret_cast<uint32_t*>(&p01);
     out.y = *reinterpret_cast<uint32_t*>(&p23);
     reinterpret_cast<uint2*>(theta16)[i] = out;
+  };
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // two independent vectors per iteration: all eight loads in flight before the math
+  for (; i + stride < nvec; i += 2 * stride) {
+    const long long j = i + stride;
+    const float4 th0 = __ldcs(reinterpret_cast<const float4*>(theta) + i);
+    const float4 th1 = __ldcs(reinterpret_cast<const float4*>(theta) + j);
+    const float4 m0 = __ldcs(reinterpret_cast<const float4*>(m) + i);
+    const float4 m1 = __ldcs(reinterpret_cast<const float4*>(m) + j);
+    const float4 v0 = __ldcs(reinterpret_cast<const float4*>(v) + i);
+    const float4 v1 = __ldcs(reinterpret_cast<const float4*>(v) + j);
+    const uint2 g0 = __ldcs(reinterpret_cast<const uint2*>(g16) + i);
+    const uint2 g1 = __ldcs(reinterpret_cast<const uint2*>(g16) + j);
+    step4(i, th0, m0, v0, g0);
+    step4(j, th1, m1, v1, g1);
   }
+  for (; i < nvec; i += stride)
+    step4(i, reinterpret_cast<const float4*>(theta)[i], reinterpret_cast<const float4*>(m)[i],
+          reinterpret_cast<const float4*>(v)[i], reinterpret_cast<const uint2*>(g16)[i]);
   // ragged tail (n % 4)
   for (long long i = nvec * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     float th = theta[i], mm = m[i], vv = v[i];
