@@ -46,7 +46,17 @@ struct GemmParams {
   float alpha;
   int num_m, num_n, total;
   int dbg;   // AXONN_RS_DEBUG experiments (row-softmax epilogue): 0 normal
+  // hybrid stream-K schedule of the pair kernel (sk = 1): the first sk_dp tiles are dealt
+  // data-parallel, the remaining tiles' k-blocks are split into equal contiguous ranges of
+  // sk_L iterations per pair; a tile cut between pairs is finished (in fixed order) by the
+  // pair holding its k-block 0 from the fp32 partials the others leave in sk_ws
+  int sk, sk_dp, sk_L, kbt;
+  float* sk_ws;
+  unsigned* sk_flag;
+  unsigned sk_epoch;
 };
+
+
 
 template <int TBM = BM>
 __device__ __forceinline__ bool tile_coords(const GemmParams& p, int BN, int t, int& z, int& m0,
@@ -65,6 +75,125 @@ __device__ __forceinline__ bool tile_coords(const GemmParams& p, int BN, int t, 
   kb0 = lo / BK;
   kb1 = (hi + BK - 1) / BK;
   return kb1 > kb0;
+}
+
+// Work units of one CTA pair: (tile, k-block range, role).  role 0 whole tile, 1 partial
+// (k-blocks after the first of its tile: written to the pair's workspace slot), 2 finisher
+// (holds k-block 0 of a cut tile: adds the partials of pairs first_prod..last_prod).
+struct PairUnits {
+  int pair, npairs, i, nfull, it, it1;
+  __device__ __forceinline__ PairUnits(const GemmParams& p, int pr, int np) : pair(pr), npairs(np) {
+    i = 0;
+    if (p.sk) {
+      nfull = p.sk_dp / np;
+      const int I = (p.total - p.sk_dp) * p.kbt;
+      it = min(pr * p.sk_L, I);
+      it1 = min(it + p.sk_L, I);
+    } else {
+      nfull = 0;
+      it = it1 = 0;
+    }
+  }
+  template <int TBM>
+  __device__ __forceinline__ bool next(const GemmParams& p, int BN, int& t, int& z, int& m0, int& n0,
+                                       int& kb0, int& kb1, int& role, int& last_prod) {
+    role = 0;
+    last_prod = -1;
+    if (!p.sk) {
+      for (;;) {
+        t = pair + i * npairs;
+        ++i;
+        if (t >= p.total) return false;
+        if (tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) return true;
+      }
+    }
+    if (i < nfull) {
+      t = pair + i * npairs;
+      ++i;
+      tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1);
+      return true;
+    }
+    if (it >= it1) return false;
+    const int ts = it / p.kbt;
+    t = p.sk_dp + ts;
+    tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1);
+    kb0 = it % p.kbt;
+    kb1 = min(p.kbt, kb0 + (it1 - it));
+    it += kb1 - kb0;
+    if (kb0 > 0) {
+      role = 1;
+    } else if (kb1 < p.kbt) {
+      role = 2;
+      last_prod = ((ts + 1) * p.kbt - 1) / p.sk_L;
+    }
+    return true;
+  }
+};
+
+__device__ __forceinline__ void st_release_u32(unsigned* a, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+
+// Stream-K fixup by one epilogue warp on its 32 rows x ncol columns of the accumulator at
+// TMEM address tb (lane base already applied).  role 1: store the partial to this pair's
+// slot and publish it; role 2: wait for the partials of pairs pair+1..last_prod and add them
+// (ascending pair order: deterministic) into TMEM before the regular epilogue runs.
+template <int BN>
+__device__ __forceinline__ void sk_fixup(const GemmParams& p, int role, int pair, int last_prod,
+                                         uint32_t rank, int wi, int rloc, int col0, int ncol,
+                                         uint32_t tb, int lane) {
+  auto slot_row = [&](int pr) {
+    return p.sk_ws + ((size_t)(pr * 2 + (int)rank) * 128 + rloc) * BN + col0;
+  };
+  if (role == 1) {
+    float* w = slot_row(pair);
+    for (int c = 0; c < ncol; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tb + c, r);
+      float4* w4 = reinterpret_cast<float4*>(w + c);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        __stcg(w4 + j, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release_u32(p.sk_flag + (pair * 2 + (int)rank) * 8 + wi, p.sk_epoch);
+    return;
+  }
+  for (int pr = pair + 1; pr <= last_prod; ++pr) {
+    if (lane == 0)
+      while (ld_acquire_u32(p.sk_flag + (pr * 2 + (int)rank) * 8 + wi) != p.sk_epoch) {
+      }
+    __syncwarp();
+  }
+  for (int c = 0; c < ncol; c += 32) {
+    uint32_t r[32];
+    tmem_ld32(tb + c, r);
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+    for (int pr = pair + 1; pr <= last_prod; ++pr) {
+      const float4* w4 = reinterpret_cast<const float4*>(slot_row(pr) + c);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 a = __ldcg(w4 + j);
+        v[4 * j] += a.x;
+        v[4 * j + 1] += a.y;
+        v[4 * j + 2] += a.z;
+        v[4 * j + 3] += a.w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i]);
+    tmem_st32(tb + c, r);
+  }
+  tmem_st_wait();
 }
 
 // tanh on the SFU (MUFU.TANH, rel. error ~2^-11: below the bf16 rounding of the output)
@@ -475,9 +604,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     {   // whole warp runs the loop; one elected lane issues the TMA copies
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < p.total; t += npairs) {
-        int z, m0, n0, kb0, kb1;
-        if (!tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+      PairUnits pu(p, pair, npairs);
+      int t, z, m0, n0, kb0, kb1, role, last_prod;
+      while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
         const int z1 = z % p.Z1, z2 = z / p.Z1;
         const int am = m0 + (int)rank * BM;
         const int bn = n0 + (int)rank * (BN / 2);
@@ -525,9 +654,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = pair; t < p.total; t += npairs) {
-        int z, m0, n0, kb0, kb1;
-        if (!tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+      PairUnits pu(p, pair, npairs);
+      int t, z, m0, n0, kb0, kb1, role, last_prod;
+      while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -559,13 +688,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
     int it = 0;
-    for (int t = pair; t < p.total; t += npairs) {
-      int z, m0, n0, kb0, kb1;
-      if (!tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+    PairUnits pu(p, pair, npairs);
+    int t, z, m0, n0, kb0, kb1, role, last_prod;
+    while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (role) {
+        sk_fixup<BN>(p, role, pair, last_prod, rank, warp - 2, q * 32 + lane, cpart * CW, CW,
+                     tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + cpart * CW, lane);
+        if (role == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+          ++it;
+          continue;
+        }
+      }
       const int row = m0 + (int)rank * BM + q * 32 + lane;
       for (int c = cpart * CW; c < (cpart + 1) * CW; c += 32) {
         if (n0 + c >= p.N) break;
@@ -594,13 +734,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     uint8_t* my_row0 = box0 + lane * 128;
     uint32_t ephase = 0;
     int it = 0;
-    for (int t = pair; t < p.total; t += npairs) {
-      int z, m0, n0, kb0, kb1;
-      if (!tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) continue;
+    PairUnits pu(p, pair, npairs);
+    int t, z, m0, n0, kb0, kb1, role, last_prod;
+    while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int row0 = m0 + (int)rank * BM + q * 32;
       const int cb = n0 + cpart * CW;
+      if (role == 1) {   // stream-K partial: no epilogue, publish the fp32 partial
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        sk_fixup<BN>(p, 1, pair, last_prod, rank, wi, q * 32 + lane, cpart * CW, CW,
+                     tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + cpart * CW, lane);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+        ++it;
+        continue;
+      }
       if (has_in && lane == 0) {   // residual / pre-activation boxes, before the accumulator
         bulk_wait_read<0>();
         mbar_arrive_expect_tx(&ebar[wi], (CW / 64) * TE_BOX);
@@ -610,6 +761,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + cpart * CW;
+      if (role == 2) sk_fixup<BN>(p, 2, pair, last_prod, rank, wi, q * 32 + lane, cpart * CW, CW, tb, lane);
       if (p.dbg == 8) {   // experiment: no epilogue work
         tc_fence_before();
         __syncwarp();
@@ -1509,6 +1661,29 @@ static bool te_eligible(const GemmArgs& g) {
 }
 
 static int g_te_mode = -1;   // AXONN_GEMM_TE=0 disables the TMA epilogue
+static int g_sk_mode = -1;   // AXONN_GEMM_SK=0 disables the stream-K schedule
+
+// Stream-K workspaces, one per concurrently launching stream (s_comp and s_wg run GEMMs at
+// the same time): fp32 [74 pairs][2 CTAs][128 x 256] partials + per-warp flags.
+constexpr int SK_SLOTS = 4;
+static float* g_sk_ws[SK_SLOTS] = {};
+static unsigned* g_sk_flag[SK_SLOTS] = {};
+static unsigned g_sk_epoch[SK_SLOTS] = {};
+static cudaStream_t g_sk_stream[SK_SLOTS] = {};
+static int sk_slot(cudaStream_t st) {
+  for (int i = 0; i < SK_SLOTS; ++i)
+    if (g_sk_ws[i] && g_sk_stream[i] == st) return i;
+  for (int i = 0; i < SK_SLOTS; ++i)
+    if (!g_sk_ws[i]) {
+      const size_t ws = (size_t)80 * 2 * 128 * 256 * 4;
+      if (cudaMalloc(&g_sk_ws[i], ws) != cudaSuccess) return -1;
+      if (cudaMalloc(&g_sk_flag[i], 80 * 2 * 8 * 4) != cudaSuccess) return -1;
+      if (cudaMemset(g_sk_flag[i], 0, 80 * 2 * 8 * 4) != cudaSuccess) return -1;
+      g_sk_stream[i] = st;
+      return i;
+    }
+  return -1;
+}
 
 template <int BN, bool TE>
 static int launch_pair(const GemmArgs& g, cudaStream_t st) {
@@ -1547,6 +1722,28 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
   int pairs_avail = g_num_sms / 2;
   if (g.max_ctas > 0 && pairs_avail > g.max_ctas / 2) pairs_avail = g.max_ctas / 2;
   int pairs = p.total < pairs_avail ? p.total : pairs_avail;
+  // hybrid stream-K when the last wave of whole tiles would leave pairs idle (T % P != 0,
+  // few waves); all but one full wave stay data-parallel
+  p.kbt = (g.K + BK - 1) / BK;
+  if (g_sk_mode < 0) {
+    const char* e = getenv("AXONN_GEMM_SK");
+    g_sk_mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  const int T = p.total, P = pairs_avail;
+  if (g_sk_mode && !g.no_sk && g.causal == 0 && g.Z == 1 && T % P != 0 && T < 6 * P && p.kbt >= 8 &&
+      P <= 80 && p.dbg == 0) {
+    const int slot = sk_slot(st);
+    if (slot >= 0) {
+      p.sk = 1;
+      p.sk_dp = T >= P ? (T / P - 1) * P : 0;
+      const int I = (T - p.sk_dp) * p.kbt;
+      p.sk_L = (I + P - 1) / P;
+      p.sk_ws = g_sk_ws[slot];
+      p.sk_flag = g_sk_flag[slot];
+      p.sk_epoch = ++g_sk_epoch[slot];
+      pairs = P;
+    }
+  }
   gemm_bf16_tcgen05_pair<BN, TE><<<2 * pairs, GEMM_THREADS, SMEM, st>>>(ma, mb, p, mc, mx);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }

@@ -33,6 +33,8 @@ struct GemmArgs {
   float alpha;
   int max_ctas;
   int variant;          // 0 auto, 1 single CTA, 2 CTA pair (TMA epilogue when eligible), 3 CTA pair, thread-store epilogue
+  int no_sk;            // 1: never use the stream-K schedule (launches that may run concurrently
+                        // with another spinning kernel: its cross-pair waits need co-residency)
 };
 
 int gemm_launch(const GemmArgs& g, cudaStream_t st);

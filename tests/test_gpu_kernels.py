@@ -264,3 +264,49 @@ def test_adamw_bit_exact_vs_oracle(lib, n):
     assert np.array_equal(dm.cpu().numpy().view(np.uint32), m_r.view(np.uint32))
     assert np.array_equal(dv.cpu().numpy().view(np.uint32), v_r.view(np.uint32))
     assert np.array_equal(d16.float().cpu().numpy().view(np.uint32), t16.view(np.uint32))
+
+
+@pytest.mark.parametrize("M,N,K,epi", [(1024, 1536, 1024, 1), (1000, 1000, 1000, 0), (1024, 1536, 1024, 2),
+                                       (4096, 2048, 2048, 0), (2048, 2048, 4096, 3)])
+def test_gemm_stream_k_fixup(lib, M, N, K, epi):
+    """Shapes whose tile count is not a multiple of the 74 CTA pairs run the hybrid stream-K
+    schedule (tiles cut across pairs, fp32 partials added by the pair holding k-block 0 in
+    fixed order): values vs the definition, and bitwise run-to-run."""
+    t = torch()
+    A = dev_bf16(RNG.standard_normal((M, K)) * 0.5)
+    B = dev_bf16(RNG.standard_normal((N, K)) * 0.05)
+    bias = dev_bf16(RNG.standard_normal(N) * 0.1)
+    aux = dev_bf16(RNG.standard_normal((M, N)))
+    outs = []
+    for _ in range(2):
+        if epi == 3:
+            Cd = t.zeros((M, N), dtype=t.float32, device="cuda")
+            gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=Cd, ldc=N, epi=3, accumulate=1)
+        elif epi == 1:
+            Cd = t.empty((M, N), dtype=t.bfloat16, device="cuda")
+            pre = t.empty((M, N), dtype=t.bfloat16, device="cuda")
+            gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=Cd, ldc=N, epi=1, bias=bias, aux=pre, ld_aux=N)
+        elif epi == 2:
+            Cd = t.empty((M, N), dtype=t.bfloat16, device="cuda")
+            gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=Cd, ldc=N, epi=2, aux=aux, ld_aux=N)
+        else:
+            Cd = t.empty((M, N), dtype=t.bfloat16, device="cuda")
+            gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=Cd, ldc=N, epi=0, bias=bias, resid=aux,
+                 ld_resid=N)
+        outs.append(Cd.clone())
+    assert t.equal(outs[0], outs[1])
+    acc = host(A) @ host(B).T
+    c = 0.7978845608028654
+    if epi == 3:
+        ref = acc
+    elif epi == 1:
+        p = acc + host(bias)
+        ref = 0.5 * p * (1 + np.tanh(c * (p + 0.044715 * p ** 3)))
+    elif epi == 2:
+        a = host(aux)
+        th = np.tanh(c * (a + 0.044715 * a ** 3))
+        ref = acc * (0.5 * (1 + th) + 0.5 * a * (1 - th * th) * c * (1 + 3 * 0.044715 * a * a))
+    else:
+        ref = acc + host(bias) + host(aux)
+    out = outs[0].float().cpu().numpy().astype(np.float64)
+    assert rel(out, ref) < (1e-5 if epi == 3 else 1e-2)
