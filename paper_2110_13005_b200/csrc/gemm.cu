@@ -1661,7 +1661,12 @@ static bool te_eligible(const GemmArgs& g) {
 }
 
 static int g_te_mode = -1;   // AXONN_GEMM_TE=0 disables the TMA epilogue
-static int g_sk_mode = -1;   // AXONN_GEMM_SK=0 disables the stream-K schedule
+// AXONN_GEMM_SK=1 enables the hybrid stream-K schedule.  Off by default: measured slower on
+// every layer shape (proj fwd 37.8 -> 53.2 us, FC1 dgrad 119.8 -> 148.5 us,
+// profiles/r1/diag_stream_k.jsonl) — the data-parallel order keeps the pairs that share an
+// operand panel on the same k-block at the same time (L2 serves them together), and the
+// GEMMs are L2 -> SM bound; pieces starting mid-tile lose that alignment.
+static int g_sk_mode = -1;
 
 // Stream-K workspaces, one per concurrently launching stream (s_comp and s_wg run GEMMs at
 // the same time): fp32 [74 pairs][2 CTAs][128 x 256] partials + per-warp flags.
@@ -1727,7 +1732,7 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
   p.kbt = (g.K + BK - 1) / BK;
   if (g_sk_mode < 0) {
     const char* e = getenv("AXONN_GEMM_SK");
-    g_sk_mode = (e && e[0] == '0') ? 0 : 1;
+    g_sk_mode = (e && e[0] == '1') ? 1 : 0;
   }
   const int T = p.total, P = pairs_avail;
   if (g_sk_mode && !g.no_sk && g.causal == 0 && g.Z == 1 && T % P != 0 && T < 6 * P && p.kbt >= 8 &&

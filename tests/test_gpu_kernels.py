@@ -267,11 +267,13 @@ def test_adamw_bit_exact_vs_oracle(lib, n):
 
 
 @pytest.mark.parametrize("M,N,K,epi", [(1024, 1536, 1024, 1), (1000, 1000, 1000, 0), (1024, 1536, 1024, 2),
-                                       (4096, 2048, 2048, 0), (2048, 2048, 4096, 3)])
+                                       (4096, 2048, 2048, 0), (2048, 2048, 4096, 3), (256, 256, 1024, 0),
+                                       (256, 256, 1024, 3)])
 def test_gemm_stream_k_fixup(lib, M, N, K, epi):
     """Shapes whose tile count is not a multiple of the 74 CTA pairs run the hybrid stream-K
-    schedule (tiles cut across pairs, fp32 partials added by the pair holding k-block 0 in
-    fixed order): values vs the definition, and bitwise run-to-run."""
+    schedule when AXONN_GEMM_SK=1 (tiles cut across pairs, fp32 partials added by the pair
+    holding k-block 0 in fixed order): values vs the definition, and bitwise run-to-run.
+    Without the variable the same shapes exercise the data-parallel schedule."""
     t = torch()
     A = dev_bf16(RNG.standard_normal((M, K)) * 0.5)
     B = dev_bf16(RNG.standard_normal((N, K)) * 0.05)

@@ -188,7 +188,7 @@ def test_overlapped_optimizer_equals_synchronous_bitwise(offload):
             eng.optimizer_step()
         res.append((losses, eng.read_all(T_MASTER), eng.read_all(T_ADAM_V), eng.read_all(T_PARAM16)))
         eng.close()
-    assert res[0][0] == res[1][0]
+    assert res[0][0] == res[1][0], (res[0][0], res[1][0])
     for a, b in zip(res[0][1:], res[1][1:]):
         for k in a:
             assert np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)), k
