@@ -307,7 +307,7 @@ def main():
 
     peaks = load_peaks()
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:   # the CPU baseline is an N = 1 figure
         cpu = cpu_oracle_sample(cfg, 1)
     if rank == 0:
         gemm_tf = gemm_flop / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None

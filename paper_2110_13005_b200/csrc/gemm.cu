@@ -556,12 +556,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                            const __grid_constant__ CUtensorMap mapB, const GemmParams p,
                            const __grid_constant__ CUtensorMap mapC,
                            const __grid_constant__ CUtensorMap mapX) {
-  constexpr int NST = TE ? STAGES2_TE : STAGES2;
+  // BN = 512: two N = 256 MMAs per k-step into one 512-column accumulator (no TMEM double
+  // buffer); per SM 48 KB of operands per 1024 MMA cycles instead of 32 KB per 512
+  constexpr int NST = TE ? (BN == 512 ? 3 : STAGES2_TE) : (BN == 512 ? 4 : STAGES2);
+  constexpr int NH = BN > 256 ? BN / 256 : 1;  // N = 256 MMAs per k-step
   constexpr int TBM = 2 * BM;                 // 256 rows per pair
   constexpr int A_BYTES = BM * BK * 2;        // this CTA's 128 rows
-  constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's BN/2 rows
+  constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's BN/2 rows (NH chunks of 128)
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = 2 * BN;
+  constexpr uint32_t TMEM_COLS = (2 * BN <= 512) ? 2 * BN : BN;
+  constexpr int NACC = TMEM_COLS / BN;        // accumulator buffers
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stg_all = smem + NST * STAGE_BYTES;          // TE staging boxes (1024-aligned)
@@ -609,7 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
         const int z1 = z % p.Z1, z2 = z / p.Z1;
         const int am = m0 + (int)rank * BM;
-        const int bn = n0 + (int)rank * (BN / 2);
+        const int bn = n0 + (int)rank * 128;   // this CTA's 128 B rows of each 256-wide N chunk
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (elect_one()) {
@@ -627,12 +631,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                 for (int j = 0; j < BM / 64; ++j)
                   tma_load_4d_pair(sA + j * 8192, &mapA, &full[stage], am + 64 * j, k0, z1, z2);
               }
-              if (!p.b_mn) {
-                tma_load_4d_pair(sB, &mapB, &full[stage], k0, bn, z1, z2);
-              } else {
 #pragma unroll
-                for (int j = 0; j < BN / 128; ++j)
-                  tma_load_4d_pair(sB + j * 8192, &mapB, &full[stage], bn + 64 * j, k0, z1, z2);
+              for (int h = 0; h < NH; ++h) {
+                const int bnh = bn + 256 * h;
+                if (!p.b_mn) {
+                  tma_load_4d_pair(sB + h * 16384, &mapB, &full[stage], k0, bnh, z1, z2);
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 2; ++j)
+                    tma_load_4d_pair(sB + h * 16384 + j * 8192, &mapB, &full[stage], bnh + 64 * j, k0, z1, z2);
+                }
               }
             }
           }
@@ -643,7 +651,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (leader) {   // whole warp runs the loop; one elected lane issues (uniform registers)
-      const uint32_t idesc = umma_idesc_bf16(TBM, BN, p.a_mn, p.b_mn);
+      const uint32_t idesc = umma_idesc_bf16(TBM, BN > 256 ? 256 : BN, p.a_mn, p.b_mn);
       // descriptors of stage 0 and the per-stage / per-k16 increments (address field = addr >> 4)
       const uint32_t s0 = smem_u32(smem);
       const uint64_t a_d0 = p.a_mn ? umma_desc_sw128(s0, 8192, 1024) : umma_desc_sw128(s0, 16, 1024);
@@ -657,8 +665,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       PairUnits pu(p, pair, npairs);
       int t, z, m0, n0, kb0, kb1, role, last_prod;
       while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+        const int acc = NACC == 2 ? (it & 1) : 0;
+        const uint32_t acc_phase = NACC == 2 ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
@@ -670,7 +678,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              mma_bf16_ss_pair(tmem_d, ad + k * a_k, bd + k * b_k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+#pragma unroll
+              for (int h = 0; h < NH; ++h)
+                mma_bf16_ss_pair(tmem_d + 256 * h, ad + k * a_k, bd + (uint64_t)(h * (16384 >> 4)) + k * b_k,
+                                 idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             mma_commit_pair(&empty[stage]);
           }
           __syncwarp();
@@ -691,8 +702,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     PairUnits pu(p, pair, npairs);
     int t, z, m0, n0, kb0, kb1, role, last_prod;
     while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = NACC == 2 ? (it & 1) : 0;
+      const uint32_t acc_phase = NACC == 2 ? ((it >> 1) & 1) : (it & 1);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (role) {
@@ -723,7 +734,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     // [cpart * BN/2, +BN/2) of this CTA's 128 x BN accumulator.
     const int q = warp & 3, cpart = (warp - 2) / 4, wi = warp - 2;
     constexpr int CW = BN / 2;
-    static_assert(CW == 128 || CW == 64, "TE epilogue: 64 or 128 columns per warp");
+    static_assert(CW == 256 || CW == 128 || CW == 64, "TE epilogue: 64..256 columns per warp");
     uint8_t* box0 = stg_all + wi * 2 * TE_BOX;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
@@ -737,8 +748,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     PairUnits pu(p, pair, npairs);
     int t, z, m0, n0, kb0, kb1, role, last_prod;
     while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = NACC == 2 ? (it & 1) : 0;
+      const uint32_t acc_phase = NACC == 2 ? ((it >> 1) & 1) : (it & 1);
       const int row0 = m0 + (int)rank * BM + q * 32;
       const int cb = n0 + cpart * CW;
       if (role == 1) {   // stream-K partial: no epilogue, publish the fp32 partial
@@ -810,7 +821,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
           }
           // gelu: pre -> box 0, act -> box 1 (ring of two commits); else box g (in place)
-          uint8_t* rowA = my_row0 + (gelu ? 0 : g) * TE_BOX;
+          uint8_t* rowA = my_row0 + (gelu ? 0 : (g & 1)) * TE_BOX;
           uint8_t* rowB = my_row0 + TE_BOX;
           if (!has_in) {   // gelu rewrites both boxes; otherwise the other box may be in flight
             if (lane == 0) {
@@ -864,7 +875,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
               tma_store_2d(&mapC, box0 + TE_BOX, cb + 64 * g, row0);   // GeLU
               bulk_commit();
             } else {
-              tma_store_2d(&mapC, box0 + g * TE_BOX, cb + 64 * g, row0);
+              tma_store_2d(&mapC, box0 + (g & 1) * TE_BOX, cb + 64 * g, row0);
               bulk_commit();
             }
           }
@@ -1661,6 +1672,7 @@ static bool te_eligible(const GemmArgs& g) {
 }
 
 static int g_te_mode = -1;   // AXONN_GEMM_TE=0 disables the TMA epilogue
+static int g_bn512 = -1;     // AXONN_GEMM_BN512=1: 256 x 512 pair tiles where eligible
 // AXONN_GEMM_SK=1 enables the hybrid stream-K schedule.  Off by default: measured slower on
 // every layer shape (proj fwd 37.8 -> 53.2 us, FC1 dgrad 119.8 -> 148.5 us,
 // profiles/r1/diag_stream_k.jsonl) — the data-parallel order keeps the pairs that share an
@@ -1692,7 +1704,7 @@ static int sk_slot(cudaStream_t st) {
 
 template <int BN, bool TE>
 static int launch_pair(const GemmArgs& g, cudaStream_t st) {
-  constexpr int NST = TE ? STAGES2_TE : STAGES2;
+  constexpr int NST = TE ? (BN == 512 ? 3 : STAGES2_TE) : (BN == 512 ? 4 : STAGES2);
   constexpr int SMEM = NST * (BM * BK * 2 + (BN / 2) * BK * 2) + (TE ? TE_SMEM : 0) + 1024 + 256;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1702,7 +1714,7 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
     attr_set = true;
   }
   CUtensorMap ma, mb, mc, mx;
-  int rc = make_maps(ma, mb, g, BM, BN / 2);
+  int rc = make_maps(ma, mb, g, BM, 128);
   if (rc) return rc;
   memset(&mc, 0, sizeof(mc));
   memset(&mx, 0, sizeof(mx));
@@ -1802,6 +1814,14 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   if (g.N <= 128 && g.M >= 256 && g.variant == 2) return launch_pair<128, false>(g, st);
   if (g.variant == 1 || (g.variant == 0 && (g.N <= 128 || !g_pair_mode || g.M <= 128)))
     return g.N <= 128 ? launch_bn<128>(g, st) : launch_bn<256>(g, st);
+  if (g_bn512 < 0) {
+    const char* e = getenv("AXONN_GEMM_BN512");
+    g_bn512 = (e && e[0] == '1') ? 1 : 0;
+  }
+  // 256 x 512 pair tiles: epilogues without a tile-sized input (two staging boxes per warp)
+  if (g_te_mode && te_eligible(g) && (g.variant == 4 || (g.variant == 0 && g_bn512)) &&
+      g.N >= 2048 && !(g.epi == EPI_DGELU || (g.epi == EPI_BF16 && g.resid)))
+    return launch_pair<512, true>(g, st);
   if (g_te_mode && g.variant != 3 && te_eligible(g)) return launch_pair<256, true>(g, st);
   return launch_pair<256, false>(g, st);
 }
@@ -1814,6 +1834,7 @@ int preload_gemm() {   // see preload_ops (ops.cu)
   const void* fns[] = {(const void*)gemm_bf16_tcgen05<128>, (const void*)gemm_bf16_tcgen05<256>,
                        (const void*)gemm_bf16_tcgen05_pair<256, false>,
                        (const void*)gemm_bf16_tcgen05_pair<256, true>,
+                       (const void*)gemm_bf16_tcgen05_pair<512, true>,
                        (const void*)gemm_bf16_tcgen05_pair<128, false>, (const void*)gemm_rowsoftmax};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;

@@ -32,7 +32,7 @@ struct GemmArgs {
   long long ld_aux;
   float alpha;
   int max_ctas;
-  int variant;          // 0 auto, 1 single CTA, 2 CTA pair (TMA epilogue when eligible), 3 CTA pair, thread-store epilogue
+  int variant;          // 0 auto, 1 single CTA, 2 CTA pair (TMA epilogue when eligible), 3 CTA pair, thread-store epilogue, 4 pair 256x512
   int no_sk;            // 1: never use the stream-K schedule (launches that may run concurrently
                         // with another spinning kernel: its cross-pair waits need co-residency)
 };

@@ -79,6 +79,7 @@ def main():
         g.B, g.ldb, g.b_mn = B.data_ptr(), (K if kind == "fwd" else N), int(kind != "fwd")
         g.C, g.ldc = Cb.data_ptr(), N
         g.alpha = 1.0
+        g.variant = int(os.environ.get("DIAG_VARIANT", "0"))
         if epi == 3:
             g.epi, g.accumulate = 3, 1
         elif epi == 1:

@@ -103,6 +103,41 @@ def gemm_sweep(variants=(0, 1, 2), only=None, iters=10):
     return out
 
 
+def host_link_probe():
+    """Pinned host <-> HBM copy bandwidth (the offloaded optimizer's roofline, SURVEY.md
+    §8(d.3) A7): H2D alone, D2H alone, and both directions at once on two streams."""
+    import torch
+    n = 1 << 30
+    h1 = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d1 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    res = {}
+    for name, pairs in (("h2d", [(d1, h1, s1)]), ("d2h", [(h2, d2, s2)]),
+                        ("duplex", [(d1, h1, s1), (h2, d2, s2)])):
+        best = 0.0
+        for _ in range(3):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for dst, src, st in pairs:
+                st.wait_event(e0)
+                with torch.cuda.stream(st):
+                    dst.copy_(src, non_blocking=True)
+            for _, _, st in pairs:
+                torch.cuda.current_stream().wait_stream(st)
+            e1.record()
+            torch.cuda.synchronize()
+            gbs = len(pairs) * n / (e0.elapsed_time(e1) / 1e3) / 1e9
+            best = max(best, gbs)
+        res[name + "_GBps"] = best
+    r = {"kernel": "host link probe (pinned, 1 GiB)", **res}
+    print(json.dumps(r), flush=True)
+    return res
+
+
 def adam_sweep():
     import torch
     from paper_2110_13005_b200 import _lib
@@ -124,13 +159,14 @@ def adam_sweep():
     print(json.dumps(r), flush=True)
     del th, m, v, g, t16
     torch.cuda.empty_cache()
+    probe = host_link_probe()
     # engine-level offloaded optimizer step (pinned host theta/m/v, 3-slot ring)
     from paper_2110_13005_b200.engine import AxoNN
     from synth import uniform_tokens
     for bs in (1 << 20, 4_000_000, 16_000_000, 64_000_000):
         for off in (1, 0):
             eng = AxoNN(1, 1, 1, n_layers=2, hidden=2048, heads=16, seq_len=512, vocab=51200,
-                        offload=bool(off), bucket_elems=bs, coarsen_k=4)
+                        offload=bool(off), bucket_elems=bs, coarsen_k=4, overlap_next_batch=False)
             phi = sum(t[2] for t in eng.tensors())
             tok = uniform_tokens(1, 512, 51200)
             ts = []
@@ -143,6 +179,8 @@ def adam_sweep():
             r = {"kernel": "optimizer_step " + ("offload" if off else "in-HBM"), "bucket": bs,
                  "params": phi, "ms": ms, "GB/s": per * phi / ms / 1e6,
                  "bytes_per_param": per}
+            if off and probe:
+                r["frac_of_duplex_probe"] = per * phi / ms / 1e6 / probe["duplex_GBps"]
             print(json.dumps(r), flush=True)
             eng.close()
 

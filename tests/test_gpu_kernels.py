@@ -55,7 +55,7 @@ def cos(x, ref):
 RNG = np.random.default_rng(1234)
 
 
-VARIANTS = pytest.mark.parametrize("variant", [1, 2, 3])
+VARIANTS = pytest.mark.parametrize("variant", [1, 2, 3, 4])
 
 
 @VARIANTS
