@@ -705,42 +705,72 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 }
 
 // D[z * s + i] = sum_j dO[i, head, j] * O[i, head * d + j]   (fp32); 16 lanes per (token, head),
-// 8 elements per lane per step (16-byte loads when the head width allows)
+// DITEMS (token, head) items per 16-lane group with every load issued before the math
+constexpr int DITEMS = 4;
 __global__ void attn_bwd_d_kernel(const __nv_bfloat16* __restrict__ dO, long long ld_do, int dp,
                                   const __nv_bfloat16* __restrict__ O, long long ld_o, int d,
                                   int s, int heads, long long ntok, float* __restrict__ D) {
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 16;
+  const long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 16;
   const int l = threadIdx.x & 15;
-  if (w >= ntok * heads) return;
-  const long long tok = w / heads;
-  const int hd = (int)(w % heads);
-  const __nv_bfloat16* a = dO + tok * ld_do + (long long)hd * dp;
-  const __nv_bfloat16* b = O + tok * ld_o + (long long)hd * d;
-  float acc = 0.f;
-  if ((d & 7) == 0 && (dp & 7) == 0) {
-    for (int j = 8 * l; j < d; j += 128) {
-      const uint4 x = *reinterpret_cast<const uint4*>(a + j);
-      const uint4 y = *reinterpret_cast<const uint4*>(b + j);
-      const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&x);
-      const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&y);
+  const long long nitems = ntok * heads;
+  float acc[DITEMS];
+  if ((d & 7) == 0 && (dp & 7) == 0 && d <= 128) {
+    uint4 x[DITEMS], y[DITEMS];
+#pragma unroll
+    for (int u = 0; u < DITEMS; ++u) {
+      const long long w = grp * DITEMS + u;
+      const int j = 8 * l;
+      x[u] = y[u] = make_uint4(0, 0, 0, 0);
+      if (w < nitems && j < d) {
+        const long long tok = w / heads;
+        const int hd = (int)(w % heads);
+        x[u] = __ldg(reinterpret_cast<const uint4*>(dO + tok * ld_do + (long long)hd * dp + j));
+        y[u] = __ldg(reinterpret_cast<const uint4*>(O + tok * ld_o + (long long)hd * d + j));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < DITEMS; ++u) {
+      const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&x[u]);
+      const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&y[u]);
+      float a = 0.f;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 xf = __bfloat1622float2(xh[e]), yf = __bfloat1622float2(yh[e]);
-        acc = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, acc));
+        a = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, a));
       }
+      acc[u] = a;
     }
   } else {
-    for (int j = 2 * l; j < d; j += 32) {
-      const float2 xf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + j));
-      const float2 yf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(b + j));
-      acc = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, acc));
+#pragma unroll
+    for (int u = 0; u < DITEMS; ++u) {
+      const long long w = grp * DITEMS + u;
+      float a = 0.f;
+      if (w < nitems) {
+        const long long tok = w / heads;
+        const int hd = (int)(w % heads);
+        const __nv_bfloat16* xa = dO + tok * ld_do + (long long)hd * dp;
+        const __nv_bfloat16* ya = O + tok * ld_o + (long long)hd * d;
+        for (int j = 2 * l; j < d; j += 32) {
+          const float2 xf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(xa + j));
+          const float2 yf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(ya + j));
+          a = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, a));
+        }
+      }
+      acc[u] = a;
     }
   }
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (l == 0) {
-    const long long sample = tok / s, i = tok % s;
-    D[(sample * heads + hd) * s + i] = acc;
+  for (int u = 0; u < DITEMS; ++u) {
+    float a = acc[u];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    const long long w = grp * DITEMS + u;
+    if (l == 0 && w < nitems) {
+      const long long tok = w / heads;
+      const int hd = (int)(w % heads);
+      const long long sample = tok / s, i = tok % s;
+      D[(sample * heads + hd) * s + i] = a;
+    }
   }
 }
 
@@ -793,7 +823,7 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   if (nv > 256) return -1;
   const long long ntok = (long long)b * s;
   {
-    const long long nthreads = ntok * heads * 16;
+    const long long nthreads = (ntok * heads + DITEMS - 1) / DITEMS * 16;
     attn_bwd_d_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(dO), (long long)heads * dp, dp,
         static_cast<const __nv_bfloat16*>(o), ldo, d, s, heads, ntok, Dbuf);

@@ -51,6 +51,7 @@ struct GemmParams {
   // sk_L iterations per pair; a tile cut between pairs is finished (in fixed order) by the
   // pair holding its k-block 0 from the fp32 partials the others leave in sk_ws
   int sk, sk_dp, sk_L, kbt;
+  int raster_n;       // tile order: 1 = N fastest (see fill_params)
   float* sk_ws;
   unsigned* sk_flag;
   unsigned sk_epoch;
@@ -64,8 +65,14 @@ __device__ __forceinline__ bool tile_coords(const GemmParams& p, int BN, int t, 
   int per = p.num_m * p.num_n;
   z = t / per;
   int r = t - z * per;
-  int nb = r / p.num_m;
-  int mb = r - nb * p.num_m;
+  int nb, mb;
+  if (p.raster_n) {   // N fastest: concurrent tiles share the A panel (A >> L2, B small)
+    mb = r / p.num_n;
+    nb = r - mb * p.num_n;
+  } else {            // M fastest: concurrent tiles share the B panel
+    nb = r / p.num_m;
+    mb = r - nb * p.num_m;
+  }
   m0 = mb * TBM;
   n0 = nb * BN;
   int lo = 0, hi = p.K;
@@ -1582,6 +1589,14 @@ static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
   p.num_m = (g.M + tbm - 1) / tbm;
   p.num_n = (g.N + bn - 1) / bn;
   p.total = p.num_m * p.num_n * g.Z;
+  // M-fastest order re-reads A once per N column of tiles; when A is far larger than L2 and
+  // B is small (LM-head weight gradient: A = dlogits^T 419 MB, B = 16.8 MB: 4.5x the
+  // algorithmic DRAM bytes, profiles/r1/k1_traffic.json), walk N fastest so each A panel is
+  // read from DRAM once and B stays L2-resident
+  {
+    const double a_bytes = 2.0 * g.M * g.K, b_bytes = 2.0 * g.N * g.K;
+    p.raster_n = (g.Z == 1 && p.num_n > 1 && a_bytes > 96e6 && a_bytes > 4 * b_bytes) ? 1 : 0;
+  }
   if (g_num_sms == 0) {
     int dev;
     cudaGetDevice(&dev);

@@ -187,21 +187,8 @@ int embed_bwd(const int32_t* tok, long long tok_ld, int b, int s, int h, int voc
 }
 
 // ------------------------------------------------------------------ LayerNorm
-// y = (x - mean) * rstd * g + b, two-pass statistics in fp32 (D-6).  Warp per row; the row
-// is read from HBM once and kept in registers as packed bf16 (NCH 16-byte chunks per lane,
-// h <= 256 * NCH), so the variance and normalisation passes cost no extra traffic.
-__device__ __forceinline__ void unpack8f(const uint4& u, float (&f)[8]) {
-  const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float2 t = __bfloat1622float2(hh[i]);
-    f[2 * i] = t.x;
-    f[2 * i + 1] = t.y;
-  }
-}
-
-template <int NCH>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int rows, int h,
+// y = (x - mean) * rstd * g + b, two-pass statistics in fp32 (D-6).  Warp per row.
+__global__ void ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int rows, int h,
                               const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ bta,
                               __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
                               float* __restrict__ rstd_out) {
@@ -209,49 +196,34 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
   if (row >= rows) return;
   const int lane = threadIdx.x % 32;
   const __nv_bfloat16* xr = x + (long long)row * h;
-  uint4 xv[NCH];
-#pragma unroll
-  for (int k = 0; k < NCH; ++k) {
-    const int c = (k * 32 + lane) * 8;
-    xv[k] = c < h ? *reinterpret_cast<const uint4*>(xr + c) : make_uint4(0, 0, 0, 0);
-  }
   float s = 0.f;
-#pragma unroll
-  for (int k = 0; k < NCH; ++k) {
+  for (int c = lane * 8; c < h; c += 256) {
     float f[8];
-    unpack8f(xv[k], f);
+    load8(xr + c, f);
 #pragma unroll
     for (int i = 0; i < 8; ++i) s += f[i];
   }
   const float mean = warp_sum(s) / h;
   float v = 0.f;
+  for (int c = lane * 8; c < h; c += 256) {
+    float f[8];
+    load8(xr + c, f);
 #pragma unroll
-  for (int k = 0; k < NCH; ++k) {
-    const int c = (k * 32 + lane) * 8;
-    if (c < h) {
-      float f[8];
-      unpack8f(xv[k], f);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float d = f[i] - mean;
-        v += d * d;
-      }
+    for (int i = 0; i < 8; ++i) {
+      float d = f[i] - mean;
+      v += d * d;
     }
   }
   const float rstd = rsqrtf(warp_sum(v) / h + 1e-5f);
   __nv_bfloat16* yr = y + (long long)row * h;
+  for (int c = lane * 8; c < h; c += 256) {
+    float f[8], gg[8], bb[8];
+    load8(xr + c, f);
+    load8(g + c, gg);
+    load8(bta + c, bb);
 #pragma unroll
-  for (int k = 0; k < NCH; ++k) {
-    const int c = (k * 32 + lane) * 8;
-    if (c < h) {
-      float f[8], gg[8], bb[8];
-      unpack8f(xv[k], f);
-      load8(g + c, gg);
-      load8(bta + c, bb);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) f[i] = (f[i] - mean) * rstd * gg[i] + bb[i];
-      store8(yr + c, f);
-    }
+    for (int i = 0; i < 8; ++i) f[i] = (f[i] - mean) * rstd * gg[i] + bb[i];
+    store8(yr + c, f);
   }
   if (lane == 0) {
     mean_out[row] = mean;
@@ -261,23 +233,14 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
 
 int ln_fwd(const void* x, int rows, int h, const void* g, const void* b, void* y, float* mean,
            float* rstd, cudaStream_t st) {
-  if (h % 8) return -1;
-  const unsigned grid = (rows + 7) / 8;
-  auto args = [&](auto kern) {
-    kern<<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, rows, h, (const __nv_bfloat16*)g,
-                               (const __nv_bfloat16*)b, (__nv_bfloat16*)y, mean, rstd);
-  };
-  if (h <= 256 * 4) args(ln_fwd_kernel<4>);
-  else if (h <= 256 * 8) args(ln_fwd_kernel<8>);
-  else if (h <= 256 * 16) args(ln_fwd_kernel<16>);
-  else if (h <= 256 * 32) args(ln_fwd_kernel<32>);
-  else return -1;
+  ln_fwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)x, rows, h,
+                                                (const __nv_bfloat16*)g, (const __nv_bfloat16*)b,
+                                                (__nv_bfloat16*)y, mean, rstd);
   return ok();
 }
 
 // dx = dres + rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)),  dxhat = dy * g
-template <int NCH>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+__global__ void ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                               const float* __restrict__ mean, const float* __restrict__ rstd, int rows,
                               int h, const __nv_bfloat16* __restrict__ g,
                               const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx) {
@@ -287,70 +250,45 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
   const float mu = mean[row], rs = rstd[row];
   const __nv_bfloat16* xr = x + (long long)row * h;
   const __nv_bfloat16* dyr = dy + (long long)row * h;
-  uint4 xv[NCH], dv[NCH];
-#pragma unroll
-  for (int k = 0; k < NCH; ++k) {
-    const int c = (k * 32 + lane) * 8;
-    const bool in = c < h;
-    xv[k] = in ? *reinterpret_cast<const uint4*>(xr + c) : make_uint4(0, 0, 0, 0);
-    dv[k] = in ? *reinterpret_cast<const uint4*>(dyr + c) : make_uint4(0, 0, 0, 0);
-  }
   float s1 = 0.f, s2 = 0.f;
+  for (int c = lane * 8; c < h; c += 256) {
+    float xf[8], df[8], gf[8];
+    load8(xr + c, xf);
+    load8(dyr + c, df);
+    load8(g + c, gf);
 #pragma unroll
-  for (int k = 0; k < NCH; ++k) {
-    const int c = (k * 32 + lane) * 8;
-    if (c < h) {
-      float xf[8], df[8], gf[8];
-      unpack8f(xv[k], xf);
-      unpack8f(dv[k], df);
-      load8(g + c, gf);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float dxh = df[i] * gf[i];
-        float xh = (xf[i] - mu) * rs;
-        s1 += dxh;
-        s2 += dxh * xh;
-      }
+    for (int i = 0; i < 8; ++i) {
+      float dxh = df[i] * gf[i];
+      float xh = (xf[i] - mu) * rs;
+      s1 += dxh;
+      s2 += dxh * xh;
     }
   }
   s1 = warp_sum(s1) / h;
   s2 = warp_sum(s2) / h;
   __nv_bfloat16* o = dx + (long long)row * h;
   const __nv_bfloat16* rr = dres ? dres + (long long)row * h : nullptr;
+  for (int c = lane * 8; c < h; c += 256) {
+    float xf[8], df[8], gf[8], rf[8];
+    load8(xr + c, xf);
+    load8(dyr + c, df);
+    load8(g + c, gf);
+    if (rr) load8(rr + c, rf);
 #pragma unroll
-  for (int k = 0; k < NCH; ++k) {
-    const int c = (k * 32 + lane) * 8;
-    if (c < h) {
-      float xf[8], df[8], gf[8], rf[8];
-      unpack8f(xv[k], xf);
-      unpack8f(dv[k], df);
-      load8(g + c, gf);
-      if (rr) load8(rr + c, rf);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float xh = (xf[i] - mu) * rs;
-        float v = rs * (df[i] * gf[i] - s1 - xh * s2);
-        rf[i] = rr ? rf[i] + v : v;
-      }
-      store8(o + c, rf);
+    for (int i = 0; i < 8; ++i) {
+      float xh = (xf[i] - mu) * rs;
+      float v = rs * (df[i] * gf[i] - s1 - xh * s2);
+      rf[i] = rr ? rf[i] + v : v;
     }
+    store8(o + c, rf);
   }
 }
 
 int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int h,
            const void* g, const void* dres, void* dx, cudaStream_t st) {
-  if (h % 8) return -1;
-  const unsigned grid = (rows + 7) / 8;
-  auto args = [&](auto kern) {
-    kern<<<grid, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean, rstd, rows,
-                               h, (const __nv_bfloat16*)g, (const __nv_bfloat16*)dres,
-                               (__nv_bfloat16*)dx);
-  };
-  if (h <= 256 * 4) args(ln_bwd_kernel<4>);
-  else if (h <= 256 * 8) args(ln_bwd_kernel<8>);
-  else if (h <= 256 * 16) args(ln_bwd_kernel<16>);
-  else if (h <= 256 * 32) args(ln_bwd_kernel<32>);
-  else return -1;
+  ln_bwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean, rstd, rows, h,
+      (const __nv_bfloat16*)g, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx);
   return ok();
 }
 
@@ -809,10 +747,8 @@ namespace axonn {
 int preload_ops() {
   cudaFuncAttributes a;
   const void* fns[] = {(const void*)embed_fwd_kernel, (const void*)embed_bwd_tok_kernel,
-                       (const void*)embed_bwd_pos_kernel, (const void*)ln_fwd_kernel<4>,
-                       (const void*)ln_fwd_kernel<8>, (const void*)ln_fwd_kernel<16>, (const void*)ln_fwd_kernel<32>,
-                       (const void*)ln_bwd_kernel<4>, (const void*)ln_bwd_kernel<8>, (const void*)ln_bwd_kernel<16>,
-                       (const void*)ln_bwd_kernel<32>, (const void*)colsum_partial_kernel,
+                       (const void*)embed_bwd_pos_kernel, (const void*)ln_fwd_kernel,
+                       (const void*)ln_bwd_kernel, (const void*)colsum_partial_kernel,
                        (const void*)colsum_final_kernel, (const void*)colsum_kernel, (const void*)colsum2_kernel,
                        (const void*)softmax_fwd_kernel,
                        (const void*)softmax_bwd_kernel, (const void*)xent_kernel,

@@ -10,7 +10,8 @@ import subprocess
 import sys
 
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1}
+         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1,
+         "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
 
 
 def main(rep, out):
