@@ -1591,11 +1591,11 @@ static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
   p.total = p.num_m * p.num_n * g.Z;
   // M-fastest order re-reads A once per N column of tiles; when A is far larger than L2 and
   // B is small (LM-head weight gradient: A = dlogits^T 419 MB, B = 16.8 MB: 4.5x the
-  // algorithmic DRAM bytes, profiles/r1/k1_traffic.json), walk N fastest so each A panel is
-  // read from DRAM once and B stays L2-resident
+  // algorithmic DRAM bytes; FC1 weight gradient 2x, profiles/r1/k1_traffic.json), walk N
+  // fastest so each A panel is read from DRAM once and B stays L2-resident
   {
     const double a_bytes = 2.0 * g.M * g.K, b_bytes = 2.0 * g.N * g.K;
-    p.raster_n = (g.Z == 1 && p.num_n > 1 && a_bytes > 96e6 && a_bytes > 4 * b_bytes) ? 1 : 0;
+    p.raster_n = (g.Z == 1 && p.num_n > 1 && a_bytes > 32e6 && a_bytes >= 3.5 * b_bytes) ? 1 : 0;
   }
   if (g_num_sms == 0) {
     int dev;
