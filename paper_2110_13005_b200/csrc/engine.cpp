@@ -223,7 +223,8 @@ static int plan_memory(Ctx* c) {
   c->dx1 = c->dalloc(Mh * 2);
   // column-sum workspaces (tickets + partials): one for the bias sums on s_wg, one for the
   // LayerNorm parameter sums on s_comp (the two streams run concurrently)
-  const size_t cs_bytes = 4096 + (size_t)2 * colsum_chunks(c->M) * 4 * c->h * 4;
+  const size_t cs_bytes = 4096 + std::max((size_t)2 * colsum_chunks(c->M) * 4 * c->h * 4,
+                                          (size_t)2 * ((c->M + 7) / 8) * c->h * 4);
   c->cs_ws = (float*)c->dalloc(cs_bytes);
   c->cs_ws_ln = (float*)c->dalloc(cs_bytes);
   if (c->cs_ws && c->cs_ws_ln &&
@@ -907,6 +908,7 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
       c->ev_bucket.push_back(e);
     }
   }
+  int64_t pend_lo = 0;   // in-HBM: first element not yet handed to a launch
   for (int64_t lo = 0; lo < c->nflat; lo += bs, ++bucket) {
     const int64_t n = std::min(bs, c->nflat - lo);
     const int64_t ci = lo / ch;
@@ -939,11 +941,27 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
       c->stats[AXONN_STAT_H2D_BYTES] += n * 12.0;
       c->stats[AXONN_STAT_D2H_BYTES] += n * 12.0;
     } else {
-      if (c->profiling) { pr.a = c->ev_opt(); pr.b = c->ev_opt(); cudaEventRecord(pr.a, c->s_opt); }
-      if (adamw_launch(n, g, c->master + lo, c->adam_m + lo, c->adam_v + lo, t16, sc, c->s_opt))
-        return (axonn_status)c->fail(AXONN_ERR_CUDA, "adamw launch");
-      if (c->profiling) { cudaEventRecord(pr.b, c->s_opt); pr.work = n * 28.0; pr.kind = 1; c->prof.push_back(pr); }
-      if (overlap) CU(cudaEventRecord(c->ev_bucket[bucket], c->s_opt));
+      // In HBM the bucket is only a scheduling unit: consecutive buckets that wait for the
+      // same all-reduce chunk (all of them when G_data = 1) run as one launch (same values;
+      // AdamW is elementwise), unless the next batch overlaps and needs per-bucket events.
+      const int64_t end = lo + n;
+      const bool chunk_ends = !c->ev_chunk.empty() && (end >= c->nflat || end / ch != ci);
+      if (overlap || end >= c->nflat || chunk_ends) {
+        const int64_t n2 = end - pend_lo;
+        const void* g2 = static_cast<const char*>(c->grad16) + pend_lo * 2;
+        void* t2 = static_cast<char*>(c->theta16) + pend_lo * 2;
+        if (c->profiling) { pr.a = c->ev_opt(); pr.b = c->ev_opt(); cudaEventRecord(pr.a, c->s_opt); }
+        if (adamw_launch(n2, g2, c->master + pend_lo, c->adam_m + pend_lo, c->adam_v + pend_lo, t2, sc,
+                         c->s_opt))
+          return (axonn_status)c->fail(AXONN_ERR_CUDA, "adamw launch");
+        if (c->profiling) { cudaEventRecord(pr.b, c->s_opt); pr.work = n2 * 28.0; pr.kind = 1; c->prof.push_back(pr); }
+        if (overlap) CU(cudaEventRecord(c->ev_bucket[bucket], c->s_opt));
+        pend_lo = end;
+        ++c->launches;
+      }
+      (void)g;
+      (void)t16;
+      continue;
     }
     ++c->launches;
   }
