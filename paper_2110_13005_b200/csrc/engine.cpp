@@ -224,7 +224,7 @@ static int plan_memory(Ctx* c) {
   // column-sum workspaces (tickets + partials): one for the bias sums on s_wg, one for the
   // LayerNorm parameter sums on s_comp (the two streams run concurrently)
   const size_t cs_bytes = 4096 + std::max((size_t)2 * colsum_chunks(c->M) * 4 * c->h * 4,
-                                          (size_t)2 * ((c->M + 7) / 8) * c->h * 4);
+                                          (size_t)2 * ((c->M + 7) / 8 + 32) * c->h * 4);
   c->cs_ws = (float*)c->dalloc(cs_bytes);
   c->cs_ws_ln = (float*)c->dalloc(cs_bytes);
   if (c->cs_ws && c->cs_ws_ln &&

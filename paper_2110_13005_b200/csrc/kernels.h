@@ -70,11 +70,6 @@ int ln_fwd(const void* x, int rows, int h, const void* g, const void* b, void* y
 int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int h,
            const void* g, const void* dres, void* dx, cudaStream_t st);
 int colsum_chunks(int rows);
-// LN backward fused with its parameter gradients (dbeta = sum dy, dgamma = sum dy * xhat);
-// workspace as colsum's (ticket at word 1023, partials after word 1024: 2 x ceil(rows/8) x h)
-int ln_bwd_colsum(const void* dy, const void* x, const float* mean, const float* rstd, int rows,
-                  int h, const void* g, const void* dres, void* dx, float* workspace,
-                  float* out_b, float* out_g, int accumulate, cudaStream_t st);
 int colsum(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int n,
            float* workspace, float* out_b, float* out_g, int accumulate, cudaStream_t st);
 int softmax_fwd(const float* S, long long nrows, int s, void* P, cudaStream_t st);

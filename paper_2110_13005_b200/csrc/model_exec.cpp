@@ -244,8 +244,8 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   TRY(gemm(lin_dgrad(dpre, p16(o.w_fc1), M, 4 * h, h, du), 2 * dM * 4 * dh * dh));
   // LN2: dx1 = dout + LN2'(du);  dg2, db2
   wg_guard(dx1);
-  KCHK(ln_bwd_colsum(du, st.x1, st.mean2, st.rstd2, M, h, p16(o.ln2_g), dout, dx1, cs_ws_ln,
-                     g32(o.ln2_b), g32(o.ln2_g), acc, s_comp));
+  KCHK(ln_bwd(du, st.x1, st.mean2, st.rstd2, M, h, p16(o.ln2_g), dout, dx1, s_comp));
+  KCHK(colsum(du, st.x1, st.mean2, st.rstd2, M, h, cs_ws_ln, g32(o.ln2_b), g32(o.ln2_g), acc, s_comp));
   // proj: dO = dx1 Wo;  dWo += dx1^T o;  dbo += colsum(dx1)
   wg_fork();
   gst = wgs();
@@ -329,8 +329,8 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   TRY(gemm(lin_dgrad(dqkv, p16(o.w_qkv), M, 3 * h, h, du), 2 * dM * 3 * dh * dh));
   // LN1: din = dx1 + LN1'(du)   (din is the buffer the layer above read as dout)
   wg_guard(din);
-  KCHK(ln_bwd_colsum(du, x, st.mean1, st.rstd1, M, h, p16(o.ln1_g), dx1, din, cs_ws_ln,
-                     g32(o.ln1_b), g32(o.ln1_g), acc, s_comp));
+  KCHK(ln_bwd(du, x, st.mean1, st.rstd1, M, h, p16(o.ln1_g), dx1, din, s_comp));
+  KCHK(colsum(du, x, st.mean1, st.rstd1, M, h, cs_ws_ln, g32(o.ln1_b), g32(o.ln1_g), acc, s_comp));
   return 0;
 }
 
@@ -380,8 +380,8 @@ int Ctx::backward(Slot& sl, int mb, const void* dout) {
     TRY(gemm(lin_wgrad(logits, sl.hf, M, V, h, g32(head_w), acc), 2.0 * M * V * h));
     gst = s_comp;
     TRY(gemm(lin_dgrad(logits, p16(head_w), M, V, h, du), 2.0 * M * V * h));
-    KCHK(ln_bwd_colsum(du, xL, sl.meanf, sl.rstdf, M, h, p16(lnf_g), nullptr, cur, cs_ws_ln,
-                       g32(lnf_b), g32(lnf_g), acc, s_comp));
+    KCHK(ln_bwd(du, xL, sl.meanf, sl.rstdf, M, h, p16(lnf_g), nullptr, cur, s_comp));
+    KCHK(colsum(du, xL, sl.meanf, sl.rstdf, M, h, cs_ws_ln, g32(lnf_b), g32(lnf_g), acc, s_comp));
   } else {
     cur = const_cast<void*>(dout);
   }

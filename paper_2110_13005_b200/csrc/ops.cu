@@ -292,163 +292,6 @@ int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, 
   return ok();
 }
 
-// ------------------------------------------------------------------ fused LayerNorm backward
-// One block owns LNB_ROWS consecutive rows; thread t owns columns {8 t + 2048 k}.  Per row the
-// two row reductions (sum dxhat, sum dxhat * xhat) go through a block reduction, dx is written,
-// and the LN parameter gradients dbeta = sum_r dy, dgamma = sum_r dy * xhat accumulate in
-// registers over the block's rows; block partials are then added in ascending block order
-// by the last block (ticket) -> bitwise reproducible, one launch, dy and x read once
-// (replaces ln_bwd + the LN column sums, which read them twice).
-constexpr int LNB_ROWS = 8;
-template <int LNB_MAXCH>   // h <= 2048 * LNB_MAXCH
-__global__ void __launch_bounds__(256) ln_bwd_fused_kernel(
-    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-    const float* __restrict__ mean, const float* __restrict__ rstd, int rows, int h,
-    const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ dres,
-    __nv_bfloat16* __restrict__ dx, float* __restrict__ part, unsigned* __restrict__ ticket,
-    float* __restrict__ out_b, float* __restrict__ out_g, int accumulate) {
-  const int t = threadIdx.x, warp = t / 32, lane = t % 32;
-  const int r0 = blockIdx.x * LNB_ROWS, r1 = min(rows, r0 + LNB_ROWS);
-  __shared__ float red[2][8][2];
-  __shared__ unsigned last;
-  float gg[LNB_MAXCH][8], ab[LNB_MAXCH][8], ag[LNB_MAXCH][8];
-#pragma unroll
-  for (int k = 0; k < LNB_MAXCH; ++k) {
-    const int c = 8 * t + 2048 * k;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ab[k][i] = ag[k][i] = 0.f;
-    if (c < h) load8(g + c, gg[k]);
-  }
-  const float inv_h = 1.0f / h;
-  // raw 16-byte chunks of the next row are loaded before the current row's reductions
-  uint4 nx[LNB_MAXCH], nd[LNB_MAXCH];
-  auto fetch = [&](int r) {
-#pragma unroll
-    for (int k = 0; k < LNB_MAXCH; ++k) {
-      const int c = 8 * t + 2048 * k;
-      if (r < r1 && c < h) {
-        nx[k] = __ldg(reinterpret_cast<const uint4*>(x + (long long)r * h + c));
-        nd[k] = __ldg(reinterpret_cast<const uint4*>(dy + (long long)r * h + c));
-      }
-    }
-  };
-  fetch(r0);
-  for (int r = r0; r < r1; ++r) {
-    const int par = (r - r0) & 1;
-    const float mu = mean[r], rs = rstd[r];
-    float xf[LNB_MAXCH][8], df[LNB_MAXCH][8];
-#pragma unroll
-    for (int k = 0; k < LNB_MAXCH; ++k) {
-      const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&nx[k]);
-      const __nv_bfloat162* dh = reinterpret_cast<const __nv_bfloat162*>(&nd[k]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 a = __bfloat1622float2(xh[i]), b = __bfloat1622float2(dh[i]);
-        xf[k][2 * i] = a.x;
-        xf[k][2 * i + 1] = a.y;
-        df[k][2 * i] = b.x;
-        df[k][2 * i + 1] = b.y;
-      }
-    }
-    fetch(r + 1);
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < LNB_MAXCH; ++k) {
-      const int c = 8 * t + 2048 * k;
-      if (c < h) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          xf[k][i] = (xf[k][i] - mu) * rs;           // xhat
-          const float dxh = df[k][i] * gg[k][i];
-          s1 += dxh;
-          s2 += dxh * xf[k][i];
-          ab[k][i] += df[k][i];
-          ag[k][i] += df[k][i] * xf[k][i];
-        }
-      }
-    }
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    if (lane == 0) {
-      red[par][warp][0] = s1;
-      red[par][warp][1] = s2;
-    }
-    __syncthreads();
-    s1 = 0.f;
-    s2 = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      s1 += red[par][w][0];
-      s2 += red[par][w][1];
-    }
-    s1 *= inv_h;
-    s2 *= inv_h;
-#pragma unroll
-    for (int k = 0; k < LNB_MAXCH; ++k) {
-      const int c = 8 * t + 2048 * k;
-      if (c < h) {
-        float o[8], rf[8];
-        if (dres) load8(dres + (long long)r * h + c, rf);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float v = rs * (df[k][i] * gg[k][i] - s1 - xf[k][i] * s2);
-          o[i] = dres ? rf[i] + v : v;
-        }
-        store8(dx + (long long)r * h + c, o);
-      }
-    }
-  }
-  // block partials -> part[blockIdx][2][h]; the last block reduces in block order
-  const int nb = gridDim.x;
-#pragma unroll
-  for (int k = 0; k < LNB_MAXCH; ++k) {
-    const int c = 8 * t + 2048 * k;
-    if (c < h) {
-      float* pb = part + ((long long)blockIdx.x * 2) * h + c;
-      float* pg = pb + h;
-#pragma unroll
-      for (int i = 0; i < 8; i += 4) {
-        __stcg(reinterpret_cast<float4*>(pb + i), make_float4(ab[k][i], ab[k][i + 1], ab[k][i + 2], ab[k][i + 3]));
-        __stcg(reinterpret_cast<float4*>(pg + i), make_float4(ag[k][i], ag[k][i + 1], ag[k][i + 2], ag[k][i + 3]));
-      }
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (t == 0) last = atomicAdd(ticket, 1u) == (unsigned)(nb - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int c = t; c < h; c += 256) {
-    float sb = 0.f, sg = 0.f;
-    for (int b = 0; b < nb; ++b) {
-      sb += __ldcg(part + ((long long)b * 2) * h + c);
-      sg += __ldcg(part + ((long long)b * 2 + 1) * h + c);
-    }
-    out_b[c] = accumulate ? out_b[c] + sb : sb;
-    out_g[c] = accumulate ? out_g[c] + sg : sg;
-  }
-  if (t == 0) *ticket = 0;
-}
-
-int ln_bwd_colsum(const void* dy, const void* x, const float* mean, const float* rstd, int rows,
-                  int h, const void* g, const void* dres, void* dx, float* workspace,
-                  float* out_b, float* out_g, int accumulate, cudaStream_t st) {
-  if (h % 8 || h > 2048 * 4) return -1;
-  const int nb = (rows + LNB_ROWS - 1) / LNB_ROWS;
-  unsigned* ticket = reinterpret_cast<unsigned*>(workspace) + 1023;   // own ticket slot
-  float* part = workspace + 1024;
-  auto go = [&](auto kern) {
-    kern<<<nb, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean, rstd, rows, h,
-                             (const __nv_bfloat16*)g, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx,
-                             part, ticket, out_b, out_g, accumulate);
-  };
-  if (h <= 2048) go(ln_bwd_fused_kernel<1>);
-  else if (h <= 4096) go(ln_bwd_fused_kernel<2>);
-  else go(ln_bwd_fused_kernel<4>);
-  return ok();
-}
-
 // ------------------------------------------------------------------ column reductions
 // Stage 1: part_b[r][c] = sum_{rows in chunk r} dy[row][c];
 //          part_g[r][c] = sum dy * xhat  (xhat from x, mean, rstd) when x != null.
@@ -662,7 +505,14 @@ __global__ void __launch_bounds__(256) colsum2_kernel(const __nv_bfloat16* __res
   __threadfence();
   if (act) {
     float s = 0.f;
-    for (int k = 0; k < R; ++k) s += __ldcg(&part[((long long)which * R + k) * n + gc]);
+    for (int k0 = 0; k0 < R; k0 += 16) {   // 16 independent loads, then ascending-order sums
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        v[i] = k0 + i < R ? __ldcg(&part[((long long)which * R + k0 + i) * n + gc]) : 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s += v[i];
+    }
     o[gc] = accumulate ? o[gc] + s : s;
   }
   if (threadIdx.x == 0) ticket[blockIdx.x] = 0;
@@ -905,8 +755,7 @@ int preload_ops() {
   cudaFuncAttributes a;
   const void* fns[] = {(const void*)embed_fwd_kernel, (const void*)embed_bwd_tok_kernel,
                        (const void*)embed_bwd_pos_kernel, (const void*)ln_fwd_kernel,
-                       (const void*)ln_bwd_kernel, (const void*)ln_bwd_fused_kernel<1>, (const void*)ln_bwd_fused_kernel<2>,
-                       (const void*)ln_bwd_fused_kernel<4>, (const void*)colsum_partial_kernel,
+                       (const void*)ln_bwd_kernel, (const void*)colsum_partial_kernel,
                        (const void*)colsum_final_kernel, (const void*)colsum_kernel, (const void*)colsum2_kernel,
                        (const void*)softmax_fwd_kernel,
                        (const void*)softmax_bwd_kernel, (const void*)xent_kernel,
