@@ -261,6 +261,7 @@ def main():
     # by CUDA events on the library's compute stream (roofline numbers)
     eng.set_profiling(True)
     gemm_ms = gemm_flop = adam_ms = adam_bytes = 0.0
+    ph = {"t_pipe_ms": 0.0, "t_busy_ms": 0.0, "t_allreduce_ms": 0.0, "t_opt_exposed_ms": 0.0}
     breakdown = {}
     launches = 0
     D.barrier(world)
@@ -277,6 +278,8 @@ def main():
             adam_ms += st["adam_ms"]
             adam_bytes += st["adam_bytes"]
             launches += int(st["kernel_launches"])
+            for k in ph:
+                ph[k] += st[k] / args.steps
             for k, (kms, kw, kn) in eng.profile().items():
                 acc = breakdown.setdefault(k, [0.0, 0.0, 0])
                 acc[0] += kms
@@ -288,6 +291,8 @@ def main():
     D.barrier(world)
     eng.set_profiling(False)
     dev_ms = D.max_over_ranks(dev_ms, world)
+    bubble = 1.0 - ph["t_busy_ms"] / ph["t_pipe_ms"] if ph["t_pipe_ms"] > 0 else 0.0
+    bubble_max = D.max_over_ranks(bubble, world)   # every rank joins the collective
     ms_step = dev_ms / args.steps
     fl = model_flops(B, s, cfg["n_layers"], cfg["hidden"], V)
     value = fl / (ms_step / 1e3) / 1e12                       # whole-job model TFLOP/s
@@ -335,6 +340,15 @@ def main():
             "eq3_tflops_per_gpu": eq3_flops(B, s, cfg["n_layers"], cfg["hidden"], V) / (ms_step / 1e3) / 1e12 / world,
             "batch_time_s": ms_step / 1e3,
             "loss": losses[-1] if losses else None,
+            # device-timed phases per step (CUDA events, rank 0; PAPER.md:704-708 phase bars):
+            # Alg. 2 phase, this stage's Forward/Backward busy time in it, the gradient cast +
+            # column all-reduce after it, optimizer time after the all-reduce
+            "phases": {"pipeline_ms": ph["t_pipe_ms"], "compute_busy_ms": ph["t_busy_ms"],
+                       "bubble_frac": bubble, "bubble_frac_max_over_ranks": bubble_max,
+                       "predicted_bubble_frac": (g_inter - 1) / (m + g_inter - 1),
+                       "allreduce_exposed_ms": ph["t_allreduce_ms"],
+                       "optimizer_exposed_ms": ph["t_opt_exposed_ms"],
+                       "note": "with overlap_next_batch (offload) the optimizer figure is the previous step's"},
             "clocks": clk.summary(),
             "e2e": {"value": e2e_val, "unit": "model TFLOP/s (all GPUs)",
                     "h2d_bytes_per_step": int((hi - lo) * (s + 1) * 4), "d2h_bytes_per_step": 8,

@@ -159,7 +159,12 @@ enum {
   AXONN_STAT_ALLREDUCE_BYTES = 9,
   AXONN_STAT_H2D_BYTES = 10,
   AXONN_STAT_D2H_BYTES = 11,
-  AXONN_STAT_COUNT = 12
+  /* device-timed phases (CUDA events; PAPER.md:704-708, 720-723 phase bars) */
+  AXONN_STAT_T_PIPE_MS = 12,      /* Alg. 2 phase: first forward issued .. last backward done   */
+  AXONN_STAT_T_BUSY_MS = 13,      /* sum of this stage's Forward/Backward spans in that phase   */
+  AXONN_STAT_T_ALLREDUCE_MS = 14, /* gradient cast + column all-reduce after the phase          */
+  AXONN_STAT_T_OPT_EXPOSED_MS = 15, /* optimizer time after the all-reduce (overlap: prev. step)*/
+  AXONN_STAT_COUNT = 16
 };
 AXONN_API axonn_status axonn_stats(const axonn_ctx* ctx, double* out, int n);
 /* Per-shape timing of the last profiled batch + step as a JSON object

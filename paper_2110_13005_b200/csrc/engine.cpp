@@ -441,6 +441,9 @@ AXONN_API void axonn_free(axonn_ctx* c) {
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_pool_opt) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_bucket) cudaEventDestroy(e);
+  for (auto& row : c->ph)
+    for (cudaEvent_t e : row)
+      if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->timer)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {c->ev_grads_ready, c->ev_opt_done, c->ev_loss})
@@ -815,14 +818,21 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
     CU(cudaMemsetAsync(c->g32(c->tok_emb), 0, (size_t)c->V * c->h * 4, c->s_comp));
     CU(cudaMemsetAsync(c->g32(c->pos_emb), 0, (size_t)c->s * c->h * 4, c->s_comp));
   }
+  const int par = (int)(c->t_step & 1);
+  for (int k = 0; k < 4; ++k)
+    if (!c->ph[par][k]) CU(cudaEventCreate(&c->ph[par][k]));
+  c->busy_ev.clear();
+  CU(cudaEventRecord(c->ph[par][0], c->s_comp));
   int rc = run_pipeline(c, m);
   if (rc) return (axonn_status)rc;
+  CU(cudaEventRecord(c->ph[par][1], c->s_comp));
   // grad16 is still read by a pending optimizer step until it completes
   if (c->opt_pending) CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
   // half-precision gradients (D-20: fp32 accumulation, bf16 reduction)
   if (cast_f32_bf16(c->grad32, c->grad16, c->nflat, c->s_comp)) return (axonn_status)c->fail(AXONN_ERR_CUDA, "cast");
   ++c->launches;
   CU(cudaEventRecord(c->ev_grads_ready, c->s_comp));
+  if (c->g_data == 1) CU(cudaEventRecord(c->ph[par][2], c->s_comp));
   CU(cudaEventRecord(c->ev_loss, c->s_comp));
   CU(cudaStreamWaitEvent(c->s_dp, c->ev_loss, 0));
   if (c->world > 1)   // C5: loss sum over the last-stage ranks, seen by every rank
@@ -844,14 +854,28 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
       c->ev_chunk.push_back(e);
       c->stats[AXONN_STAT_ALLREDUCE_BYTES] += n * 2.0;
     }
+    CU(cudaEventRecord(c->ph[par][2], c->s_dp));
   }
   CU(cudaEventSynchronize(ev_loss_host));
   if (loss_out) *loss_out = (float)(*c->h_loss / c->oc.loss_scale);
   c->grads_ready = true;
+  {   // device-timed phase of this batch (every s_comp event has completed: loss synced)
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ph[par][0], c->ph[par][1]);
+    c->stats[AXONN_STAT_T_PIPE_MS] = ms;
+    double busy = 0;
+    for (auto& pr : c->busy_ev) {
+      float b = 0;
+      cudaEventElapsedTime(&b, pr.first, pr.second);
+      busy += b;
+    }
+    c->stats[AXONN_STAT_T_BUSY_MS] = busy;
+  }
   if (c->opt_pending) {   // the previous step has completed (the cast above waited for it)
     c->opt_pending = false;
     c->collect_stats();
     c->prof_opt.clear();
+    c->phase_stats_ar_opt(par ^ 1);
   }
   c->stats[AXONN_STAT_T_BATCH_MS] =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -971,6 +995,9 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
     CU(cudaStreamWaitEvent(c->s_opt, e, 0));
   }
   CU(cudaEventRecord(c->ev_opt_done, c->s_opt));
+  const int par = (int)((t - 1) & 1);   // parity of the batch this step belongs to
+  if (c->ph[par][3] == nullptr) CU(cudaEventCreate(&c->ph[par][3]));
+  CU(cudaEventRecord(c->ph[par][3], c->s_opt));
   c->t_step = t;
   c->grads_ready = false;
   c->ev_chunk.clear();
@@ -989,12 +1016,22 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
   c->stats[AXONN_STAT_T_OPT_MS] =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   c->collect_stats();
+  c->phase_stats_ar_opt(par);
   return AXONN_OK;
 }
 
 }  // extern "C"
 
 namespace axonn {
+
+void Ctx::phase_stats_ar_opt(int par) {
+  if (!ph[par][1] || !ph[par][2] || !ph[par][3]) return;
+  float ar = 0, op = 0;
+  if (cudaEventElapsedTime(&ar, ph[par][1], ph[par][2]) != cudaSuccess) ar = 0;
+  if (cudaEventElapsedTime(&op, ph[par][2], ph[par][3]) != cudaSuccess) op = 0;
+  stats[AXONN_STAT_T_ALLREDUCE_MS] = ar;
+  stats[AXONN_STAT_T_OPT_EXPOSED_MS] = op > 0 ? op : 0;
+}
 
 void Ctx::wait_params(int64_t off_end) {
   if (!opt_pending || ev_bucket.empty()) return;

@@ -126,6 +126,11 @@ struct Ctx {
   std::vector<ProfRec> prof;
   // optimizer / next-batch overlap (overlap_next_batch, reading D-32)
   bool opt_pending = false;           // an optimizer step is still running on s_opt
+  // phase events per step parity: [0] phase start, [1] phase end (s_comp), [2] all-reduce
+  // done, [3] optimizer done; busy spans = (start, end) event pairs around Forward/Backward
+  cudaEvent_t ph[2][4] = {};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_ev;
+  void phase_stats_ar_opt(int par);
   std::vector<cudaEvent_t> ev_bucket; // K9 of bucket b done (theta16 of the bucket written)
   std::vector<ProfRec> prof_opt;      // AdamW records of the pending step
   void wait_params(int64_t off_end);  // s_comp waits until theta16[0, off_end) is updated
@@ -169,6 +174,8 @@ struct Ctx {
   int attn_call(bool fwd, LayerStash& st);   // K2 launch (+ profiling events)
   int forward(Slot& sl, int mb);          // nn_shard.Forward (and the loss on the last stage)
   int backward(Slot& sl, int mb, const void* dout);   // nn_shard.Backward
+  int forward_impl(Slot& sl, int mb);
+  int backward_impl(Slot& sl, int mb, const void* dout);
   int layer_fwd(int li, const void* x, LayerStash& st);
   int64_t layer_end(int li) const {   // one past the last flat element of layer li
     return loff[li].b_fc2 + ((int64_t)h + 63) / 64 * 64;

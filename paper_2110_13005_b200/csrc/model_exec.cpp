@@ -337,6 +337,15 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
 // nn_shard.Forward for microbatch mb into slot sl.  Stage 0 embeds its tokens;
 // the last stage also runs LN_f, the LM head and the fused, pre-divided loss.
 int Ctx::forward(Slot& sl, int mb) {
+  cudaEvent_t b0 = ev(), b1 = ev();   // busy span (after any message wait the caller enqueued)
+  cudaEventRecord(b0, s_comp);
+  const int rc = forward_impl(sl, mb);
+  cudaEventRecord(b1, s_comp);
+  busy_ev.emplace_back(b0, b1);
+  return rc;
+}
+
+int Ctx::forward_impl(Slot& sl, int mb) {
   // K1 launches are bracketed by CUDA events only for the last microbatch of the
   // batch (every microbatch runs the same GEMM shapes; bracketing all of them would
   // perturb the timed step by several percent).
@@ -367,6 +376,15 @@ int Ctx::forward(Slot& sl, int mb) {
 // stage, where Backward(1) starts from the cross-entropy gradient already
 // written in place of the logits).  The input gradient goes to sl.gsend.
 int Ctx::backward(Slot& sl, int mb, const void* dout) {
+  cudaEvent_t b0 = ev(), b1 = ev();
+  cudaEventRecord(b0, s_comp);
+  const int rc = backward_impl(sl, mb, dout);
+  cudaEventRecord(b1, s_comp);
+  busy_ev.emplace_back(b0, b1);
+  return rc;
+}
+
+int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
   prof_mb = profiling && mb == cur_m - 1;
   const int b = microbatch;
   const int acc = bwd_count > 0 ? 1 : 0;

@@ -16,7 +16,8 @@ T_PARAM16, T_GRAD, T_MASTER, T_ADAM_M, T_ADAM_V, T_GRAD32 = range(6)
 
 STAT_NAMES = ["t_batch_ms", "t_opt_ms", "gemm_ms", "gemm_flop", "gemm_launches",
               "kernel_launches", "adam_ms", "adam_bytes", "p2p_bytes", "allreduce_bytes",
-              "h2d_bytes", "d2h_bytes"]
+              "h2d_bytes", "d2h_bytes", "t_pipe_ms", "t_busy_ms", "t_allreduce_ms",
+              "t_opt_exposed_ms"]
 
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "GRID_MISMATCH", -3: "NONDIVISIBLE_LAYERS",
           -4: "NONDIVISIBLE_BATCH", -5: "OOM", -6: "CUDA", -7: "NCCL", -8: "STATE",
