@@ -1589,18 +1589,25 @@ static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
   p.num_m = (g.M + tbm - 1) / tbm;
   p.num_n = (g.N + bn - 1) / bn;
   p.total = p.num_m * p.num_n * g.Z;
-  // M-fastest order re-reads A once per N column of tiles; when A is far larger than L2 and
-  // B is small (LM-head weight gradient: A = dlogits^T 419 MB, B = 16.8 MB: 4.5x the
-  // algorithmic DRAM bytes; FC1 weight gradient 2x, profiles/r1/k1_traffic.json), walk N
-  // fastest so each A panel is read from DRAM once and B stays L2-resident
-  {
-    const double a_bytes = 2.0 * g.M * g.K, b_bytes = 2.0 * g.N * g.K;
-    p.raster_n = (g.Z == 1 && p.num_n > 1 && a_bytes > 32e6 && a_bytes >= 3.5 * b_bytes) ? 1 : 0;
-  }
   if (g_num_sms == 0) {
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // M-fastest order re-reads A once per N column of tiles; when A is far larger than L2 and
+  // B is small (LM-head weight gradient: A = dlogits^T 419 MB, B = 16.8 MB: 4.5x the
+  // algorithmic DRAM bytes; FC1 weight gradient 2x, profiles/r1/k1_traffic.json), walk N
+  // fastest so each A panel is read from DRAM once and B stays L2-resident
+  // General rule: an operand larger than ~L2/4 is re-read from DRAM once per wave of tiles
+  // that sweeps it; pick the order whose estimated DRAM bytes are smaller.
+  {
+    const double a_bytes = 2.0 * g.M * g.K, b_bytes = 2.0 * g.N * g.K;
+    const int units = tbm == 2 * BM ? g_num_sms / 2 : g_num_sms;   // pairs or CTAs
+    const double waves = (double)((p.total + units - 1) / units);
+    const double big = 32e6;
+    const double cost_m = (a_bytes > big ? a_bytes * waves : a_bytes) + b_bytes;
+    const double cost_n = (b_bytes > big ? b_bytes * waves : b_bytes) + a_bytes;
+    p.raster_n = (g.Z == 1 && p.num_n > 1 && cost_n < 0.9 * cost_m) ? 1 : 0;
   }
 }
 
