@@ -66,6 +66,11 @@ typedef struct {
   int64_t bucket_elems;                       /* bsize in elements (D-16); paper 4M */
   int coarsen_k;                              /* all-reduce chunk = k * bsize elements; paper 4 */
   int pipeline_limit;                         /* 0 -> G_inter */
+  int checkpoint_interval;                    /* activation checkpointing ac: 0 or 1
+                                                 off; -1 the paper's rule (factor of n_layers / G_inter
+                                                 closest to sqrt(n_layers)); k > 1 explicit, must divide
+                                                 the stage's layer count (else AXONN_ERR_INVALID_ARG,
+                                                 "BadCheckpointInterval").  Values are unchanged. */
   int overlap_next_batch;                     /* 1: axonn_optimizer_step returns once every bucket is
                                                  enqueued; the next axonn_run_batch starts at once and
                                                  each layer's forward waits only for the buckets that

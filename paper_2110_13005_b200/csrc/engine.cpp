@@ -164,37 +164,56 @@ static int split_comm(Ctx* c, ncclComm_t parent, int color, int key, ncclComm_t*
   return 0;
 }
 
+static int alloc_stash(Ctx* c, LayerStash& st) {
+  const size_t Mh = (size_t)c->M * c->h;
+  const size_t att = (size_t)c->microbatch * c->heads * c->s * c->s;
+  st.u = c->dalloc(Mh * 2);
+  st.qkv = c->dalloc((size_t)c->M * c->lq * 2);
+  if (st.qkv && c->dp != c->d && cudaMemset(st.qkv, 0, (size_t)c->M * c->lq * 2) != cudaSuccess)
+    return c->fail(AXONN_ERR_CUDA, "memset qkv padding");
+  if (c->flash_attn())
+    st.lse = (float*)c->dalloc((size_t)c->microbatch * c->heads * c->s * 4);
+  else
+    st.P = c->dalloc(att * 2);
+  st.o = c->dalloc(Mh * 2);
+  st.x1 = c->dalloc(Mh * 2);
+  st.w = c->dalloc(Mh * 2);
+  st.pre = c->dalloc(4 * Mh * 2);
+  st.act = c->dalloc(4 * Mh * 2);
+  st.out = c->dalloc(Mh * 2);
+  st.mean1 = (float*)c->dalloc(c->M * 4);
+  st.rstd1 = (float*)c->dalloc(c->M * 4);
+  st.mean2 = (float*)c->dalloc(c->M * 4);
+  st.rstd2 = (float*)c->dalloc(c->M * 4);
+  if (!st.u || !st.qkv || !(st.P || st.lse) || !st.o || !st.x1 || !st.w || !st.pre || !st.act ||
+      !st.out || !st.mean1 || !st.rstd1 || !st.mean2 || !st.rstd2)
+    return c->fail(AXONN_ERR_OOM, "activation stash allocation");
+  return 0;
+}
+
 static int plan_memory(Ctx* c) {
   const size_t Mh = (size_t)c->M * c->h;
   const size_t att = (size_t)c->microbatch * c->heads * c->s * c->s;
+  if (c->ac > 1) {
+    c->ck.resize(c->ac);
+    for (LayerStash& st : c->ck)
+      if (int r = alloc_stash(c, st)) return r;
+  }
   c->slots.resize(c->limit);
   for (int si = 0; si < c->limit; ++si) {
     Slot& sl = c->slots[si];
     sl.in = c->dalloc(Mh * 2);
-    sl.L.resize(c->nl);
-    for (int li = 0; li < c->nl; ++li) {
-      LayerStash& st = sl.L[li];
-      st.u = c->dalloc(Mh * 2);
-      st.qkv = c->dalloc((size_t)c->M * c->lq * 2);
-      if (st.qkv && c->dp != c->d && cudaMemset(st.qkv, 0, (size_t)c->M * c->lq * 2) != cudaSuccess)
-        return c->fail(AXONN_ERR_CUDA, "memset qkv padding");
-      if (c->flash_attn())
-        st.lse = (float*)c->dalloc((size_t)c->microbatch * c->heads * c->s * 4);
-      else
-        st.P = c->dalloc(att * 2);
-      st.o = c->dalloc(Mh * 2);
-      st.x1 = c->dalloc(Mh * 2);
-      st.w = c->dalloc(Mh * 2);
-      st.pre = c->dalloc(4 * Mh * 2);
-      st.act = c->dalloc(4 * Mh * 2);
-      st.out = c->dalloc(Mh * 2);
-      st.mean1 = (float*)c->dalloc(c->M * 4);
-      st.rstd1 = (float*)c->dalloc(c->M * 4);
-      st.mean2 = (float*)c->dalloc(c->M * 4);
-      st.rstd2 = (float*)c->dalloc(c->M * 4);
-      if (!st.u || !st.qkv || !(st.P || st.lse) || !st.o || !st.x1 || !st.w || !st.pre || !st.act || !st.out ||
-          !st.mean1 || !st.rstd1 || !st.mean2 || !st.rstd2)
-        return c->fail(AXONN_ERR_OOM, "activation stash allocation");
+    if (c->ac > 1) {   // checkpointing: segment inputs only; the stash is the shared scratch
+      sl.seg.assign(c->nl / c->ac + 1, nullptr);
+      sl.seg[0] = sl.in;
+      for (size_t j = 1; j < sl.seg.size(); ++j) {
+        sl.seg[j] = c->dalloc(Mh * 2);
+        if (!sl.seg[j]) return c->fail(AXONN_ERR_OOM, "checkpoint segment allocation");
+      }
+    } else {
+      sl.L.resize(c->nl);
+      for (int li = 0; li < c->nl; ++li)
+        if (int r = alloc_stash(c, sl.L[li])) return r;
     }
     if (c->last) {
       sl.hf = c->dalloc(Mh * 2);
@@ -309,6 +328,9 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
       opt->pipeline_limit < 0)
     return AXONN_ERR_INVALID_ARG;
   if (world > 1 && (!dist || !dist->nccl_id)) return AXONN_ERR_INVALID_ARG;
+  if (opt->checkpoint_interval < -1 ||   // BadCheckpointInterval: ac must divide N / G_inter
+      (opt->checkpoint_interval > 1 && (model->n_layers / g_inter) % opt->checkpoint_interval))
+    return AXONN_ERR_INVALID_ARG;
 
   axonn_ctx* c = new (std::nothrow) axonn_ctx();
   if (!c) return AXONN_ERR_OOM;
@@ -327,6 +349,15 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   c->dp = (d + 7) / 8 * 8;            // e.g. 12B: d = 188 -> 192 (D-7: scale stays 1/sqrt(188))
   c->lq = 3LL * c->heads * c->dp;
   c->limit = g_inter == 1 ? 1 : (opt->pipeline_limit > 0 ? opt->pipeline_limit : g_inter);
+  if (opt->checkpoint_interval == -1) {   // factor of N / G_inter closest to sqrt(N)
+    const double root = std::sqrt((double)model->n_layers);
+    int best = 1;
+    for (int a = 1; a <= c->nl; ++a)
+      if (c->nl % a == 0 && (std::fabs(a - root) < std::fabs(best - root))) best = a;
+    c->ac = best;
+  } else if (opt->checkpoint_interval > 1) {
+    c->ac = opt->checkpoint_interval;
+  }
 
   auto bail = [&](int rc) {
     axonn_free(c);
@@ -660,7 +691,7 @@ static int run_pipeline(Ctx* c, int m) {
     cudaEvent_t e = c->ev();
     cudaEventRecord(e, c->s_comp);
     cudaStreamWaitEvent(c->s_send_act, e, 0);
-    const void* out = c->nl > 0 ? sl.L[c->nl - 1].out : sl.in;
+    const void* out = c->stage_out(sl);
     c->stats[AXONN_STAT_P2P_BYTES] += (double)Mh * 2;
     int r = c->check_nccl(ncclSend(out, Mh, ncclBfloat16, 1, c->act_out, c->s_send_act), "ncclSend act");
     ev_sent_act[mb] = c->ev();

@@ -35,7 +35,8 @@ struct LayerStash {
 // One in-flight microbatch on this stage (pipeline_limit of them, Alg. 2).
 struct Slot {
   void* in = nullptr;                 // stage input [M, h]: embedding output or received activation
-  std::vector<LayerStash> L;
+  std::vector<LayerStash> L;          // full stash per layer (no checkpointing)
+  std::vector<void*> seg;             // checkpointing: input of segment j (seg[0] = in), seg[nl/ac] = stage output
   void* hf = nullptr;                 // last stage: LN_f output
   float *meanf = nullptr, *rstdf = nullptr;
   void* gsend = nullptr;              // gradient w.r.t. the stage input, sent to stage i-1
@@ -177,6 +178,15 @@ struct Ctx {
   int forward_impl(Slot& sl, int mb);
   int backward_impl(Slot& sl, int mb, const void* dout);
   int layer_fwd(int li, const void* x, LayerStash& st);
+  // activation checkpointing: with ac > 1 the layers share ac scratch
+  // stashes; a slot keeps only the segment inputs and the backward recomputes each segment
+  int ac = 1;
+  std::vector<LayerStash> ck;
+  LayerStash& stash(Slot& sl, int li) { return ac > 1 ? ck[li % ac] : sl.L[li]; }
+  const void* stage_out(const Slot& sl) const {
+    if (ac > 1) return sl.seg[nl / ac];
+    return nl > 0 ? sl.L[nl - 1].out : sl.in;
+  }
   int64_t layer_end(int li) const {   // one past the last flat element of layer li
     return loff[li].b_fc2 + ((int64_t)h + 63) / 64 * 64;
   }

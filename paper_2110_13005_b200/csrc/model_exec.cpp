@@ -359,8 +359,15 @@ int Ctx::forward_impl(Slot& sl, int mb) {
   const void* x = sl.in;
   for (int li = 0; li < nl; ++li) {
     wait_params(layer_end(li));
-    TRY(layer_fwd(li, x, sl.L[li]));
-    x = sl.L[li].out;
+    if (ac > 1) {   // the segment's last layer writes the kept segment boundary
+      LayerStash st = stash(sl, li);
+      if (li % ac == ac - 1) st.out = sl.seg[li / ac + 1];
+      TRY(layer_fwd(li, x, st));
+      x = st.out;
+    } else {
+      TRY(layer_fwd(li, x, sl.L[li]));
+      x = sl.L[li].out;
+    }
   }
   if (!last) return 0;
   wait_params(nflat);
@@ -392,7 +399,7 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
   void* cur = dh0;
   void* nxt = dh1;
   if (last) {
-    const void* xL = nl > 0 ? sl.L[nl - 1].out : sl.in;
+    const void* xL = stage_out(sl);
     wg_fork();
     gst = wgs();
     TRY(gemm(lin_wgrad(logits, sl.hf, M, V, h, g32(head_w), acc), 2.0 * M * V * h));
@@ -404,9 +411,23 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
     cur = const_cast<void*>(dout);
   }
   for (int li = nl - 1; li >= 0; --li) {
-    const void* x = li > 0 ? sl.L[li - 1].out : sl.in;
+    const void* x;
+    if (ac > 1) {
+      const int sg = li / ac;
+      if (li % ac == ac - 1) {   // recompute the segment's forward from its kept input
+        wg_join();                 // s_wg may still read the scratch stash of the segment above
+        const void* xr = sl.seg[sg];
+        for (int j = sg * ac; j <= li; ++j) {
+          TRY(layer_fwd(j, xr, stash(sl, j)));
+          xr = stash(sl, j).out;
+        }
+      }
+      x = li % ac == 0 ? sl.seg[sg] : stash(sl, li - 1).out;
+    } else {
+      x = li > 0 ? sl.L[li - 1].out : sl.in;
+    }
     void* din = (li == 0 && !first) ? sl.gsend : nxt;
-    TRY(layer_bwd(li, x, sl.L[li], cur, din));
+    TRY(layer_bwd(li, x, stash(sl, li), cur, din));
     if (li == 0 && !first) {
       cur = din;
     } else {

@@ -39,12 +39,12 @@ class AxoNN:
                  beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
                  weight_decay: float = 0.01, loss_scale: float = 1.0, offload: bool = False,
                  bucket_elems: int = 4_000_000, coarsen_k: int = 4, pipeline_limit: int = 0,
-                 overlap_next_batch: bool | None = None,
+                 overlap_next_batch: bool | None = None, checkpoint_interval: int = 0,
                  rank: int = 0, world_size: int = 1, device: int = 0, nccl_id: bytes | None = None):
         self.lib = _lib.load()
         self.mc = _lib.ModelCfg(n_layers, hidden, heads, seq_len, vocab, init_seed)
         self.oc = _lib.OptCfg(lr, beta1, beta2, eps, weight_decay, loss_scale, int(offload),
-                              bucket_elems, coarsen_k, pipeline_limit,
+                              bucket_elems, coarsen_k, pipeline_limit, checkpoint_interval,
                               # default: overlap when the optimizer is host-link bound (offload);
                               # in HBM the AdamW kernels only compete with the GEMMs for SMs
                               int(offload if overlap_next_batch is None else overlap_next_batch))

@@ -57,3 +57,11 @@ def test_init_validation_errors_before_device():
         AxoNN(2, 1, 1, n_layers=3, hidden=64, heads=2, seq_len=32, vocab=256, world_size=2,
               nccl_id=b"x" * 128)
     assert e.value.status == "NONDIVISIBLE_LAYERS"
+
+
+def test_bad_checkpoint_interval_rejected_before_device():
+    """BadCheckpointInterval: ac must divide the stage's layer count."""
+    from paper_2110_13005_b200.engine import AxoNN, AxoNNError
+    with pytest.raises(AxoNNError) as e:
+        AxoNN(1, 1, 1, n_layers=4, hidden=64, heads=2, seq_len=32, vocab=256, checkpoint_interval=3)
+    assert e.value.status == "INVALID_ARG"

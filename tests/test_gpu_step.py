@@ -192,3 +192,24 @@ def test_overlapped_optimizer_equals_synchronous_bitwise(offload):
     for a, b in zip(res[0][1:], res[1][1:]):
         for k in a:
             assert np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)), k
+
+
+@pytest.mark.parametrize("ac", [2, 4, -1])
+def test_activation_checkpointing_is_bitwise_neutral(ac):
+    """§8(f) N1: with checkpointing interval ac the backward recomputes each
+    segment's forward from its kept input; the recomputation is the same computation, so the
+    loss and every gradient equal those without checkpointing bit for bit."""
+    from paper_2110_13005_b200.engine import T_GRAD32, T_MASTER
+    cfg = MINI
+    params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=21)
+    tok = markov_tokens(16, cfg["seq_len"], cfg["vocab"], seed=4)
+    outs = []
+    for ck in (0, ac):
+        eng = make(cfg, checkpoint_interval=ck)
+        eng.write_all(T_MASTER, params)
+        loss = eng.run_batch(tok)
+        outs.append((loss, eng.read_all(T_GRAD32)))
+        eng.close()
+    assert outs[0][0] == outs[1][0]
+    for k in outs[0][1]:
+        assert np.array_equal(outs[0][1][k].view(np.uint32), outs[1][1][k].view(np.uint32)), k
