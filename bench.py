@@ -208,6 +208,8 @@ def main():
     ap.add_argument("--layers", type=int, default=None, help="override n_layers (profiling runs only)")
     ap.add_argument("--mb-per-replica", type=int, default=None, help="microbatches per replica (m)")
     ap.add_argument("--offload", type=int, default=None, help="1/0: override the config's offload")
+    ap.add_argument("--checkpoint-interval", type=int, default=0,
+                    help="activation checkpointing ac (PAPER.md:553-576): 0 off, -1 the paper's rule")
     ap.add_argument("--g-inter", type=int, default=None,
                     help="pipeline stages (pipeline configs; G_data = N / G_inter)")
     args = ap.parse_args()
@@ -241,7 +243,8 @@ def main():
     nid = D.share_unique_id(rank, world, D.nccl_unique_id)
     eng = AxoNN(g_inter, g_data, b_m, n_layers=cfg["n_layers"], hidden=cfg["hidden"],
                 heads=cfg["heads"], seq_len=cfg["seq_len"], vocab=cfg["vocab"], init_seed=42,
-                offload=cfg["offload"], rank=rank, world_size=world, device=local, nccl_id=nid)
+                offload=cfg["offload"], rank=rank, world_size=world, device=local, nccl_id=nid,
+                checkpoint_interval=args.checkpoint_interval)
     from synth import uniform_tokens
     s, V = cfg["seq_len"], cfg["vocab"]
     tokens = uniform_tokens(B, s, V, seed=1234)          # full batch on the host (pinned below)
@@ -338,8 +341,10 @@ def main():
                        f"a{cfg['heads']} s{s} V{V}", "global_batch": B, "seq_len": s,
                        "microbatch": b_m, "microbatches_per_replica": m,
                        "parallelism": f"G_inter{g_inter} x G_data{g_data}",
-                       "offload": cfg["offload"], "l2": "inputs larger than L2 (GBs of weights/activations per step)"},
+                       "offload": cfg["offload"], "checkpoint_interval": args.checkpoint_interval,
+                       "l2": "inputs larger than L2 (GBs of weights/activations per step)"},
             "per_gpu_tflops": value / world,
+            "device_mem_gib": torch.cuda.mem_get_info()[1] / 2**30 - torch.cuda.mem_get_info()[0] / 2**30,
             "pct_bf16_peak": 100.0 * value / world / peaks["bf16"],
             "pct_bf16_peak_sustained": 100.0 * value / world / peaks["bf16_sus"],
             "eq3_tflops_per_gpu": eq3_flops(B, s, cfg["n_layers"], cfg["hidden"], V) / (ms_step / 1e3) / 1e12 / world,
