@@ -414,7 +414,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
         }
         if (kb >= 0) color = c->replica * g_inter + kb;
         ncclComm_t nc = nullptr;
-        if ((rc = split_comm(c, c->world_comm, color, c->stage, &nc, 4))) return bail(rc);
+        if ((rc = split_comm(c, c->world_comm, color, c->stage, &nc, 1))) return bail(rc);
         if (kb < 0) continue;
         bool right = (kb == c->stage);   // comm with stage+1
         if (dir == 0) {

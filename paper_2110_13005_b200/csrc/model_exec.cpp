@@ -46,7 +46,8 @@ int Ctx::gemm(GemmArgs g, double flops) {
   if (g.Z == 0) g.Z = 1;
   if (g.Z1 == 0) g.Z1 = 1;
   if (g.alpha == 0.f) g.alpha = 1.f;
-  if (g.max_ctas == 0 && g_inter > 1) g.max_ctas = num_sms - 8;   // leave SMs to posted NCCL P2P kernels
+  // leave two TPCs to the posted one-CTA NCCL P2P kernels (receive act/grad, short sends)
+  if (g.max_ctas == 0 && g_inter > 1) g.max_ctas = num_sms - 4;
   // stream-K (cross-pair waits) only on s_comp: a weight-gradient GEMM on s_wg may hold SMs
   // concurrently, and two partially resident spinning kernels could starve each other
   if (st == s_wg) g.no_sk = 1;
