@@ -38,7 +38,7 @@ import math
 
 import numpy as np
 
-from .bf16 import round_bf16
+from .bf16 import round_half
 
 
 def step_scalars(t: int, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01,
@@ -56,15 +56,15 @@ def step_scalars(t: int, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay
     )
 
 
-def adamw_step_fp32(theta, m, v, g16, sc: dict):
-    """One AdamW step on float32 arrays (in place); returns theta16 (bf16 values as fp32)."""
+def adamw_step_fp32(theta, m, v, g16, sc: dict, half: str = "bf16"):
+    """One AdamW step on float32 arrays (in place); returns theta16 (RNE to ``half``, as fp32)."""
     g = g16.astype(np.float32) * sc["inv_scale"]
     theta *= sc["decay"]
     m[...] = sc["b1"] * m + sc["omb1"] * g
     v[...] = sc["b2"] * v + sc["omb2"] * (g * g)
     denom = np.sqrt(v) / sc["bc2_sqrt"] + sc["eps"]
     theta -= sc["step"] * (m / denom)
-    return round_bf16(theta)
+    return round_half(theta, half)
 
 
 def adamw_step_fp64(theta, m, v, g, t: int, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8,
@@ -78,7 +78,17 @@ def adamw_step_fp64(theta, m, v, g, t: int, lr=1e-3, beta1=0.9, beta2=0.999, eps
     return theta, m, v
 
 
-def adamw_bucketed_fp32(theta_host, m_host, v_host, g16_dev, sc: dict, bsize: int):
+def grads_finite(g16) -> bool:
+    """Overflow test of mixed precision with loss scaling (the loss is
+    multiplied by a large number so small gradients survive in half precision; an overflow
+    makes a gradient non-finite).  Reading D-12: when ANY gradient element of the whole
+    model (every stage, after the all-reduce) is inf or NaN the optimizer step is skipped:
+    theta, m, v and theta16 are left unchanged and the step counter t is not incremented."""
+    return bool(np.isfinite(np.asarray(g16, dtype=np.float32)).all())
+
+
+def adamw_bucketed_fp32(theta_host, m_host, v_host, g16_dev, sc: dict, bsize: int,
+                        half: str = "bf16"):
     """fetch a bucket of theta and s_opt, step it on reused
     scratch buffers, offload it back.  Returns theta16 for the whole vector."""
     n = theta_host.size
@@ -96,7 +106,7 @@ def adamw_bucketed_fp32(theta_host, m_host, v_host, g16_dev, sc: dict, bsize: in
         t[...] = theta_host[lo:hi]                 # H2D
         mm[...] = m_host[lo:hi]
         vv[...] = v_host[lo:hi]
-        theta16[lo:hi] = adamw_step_fp32(t, mm, vv, g16_dev[lo:hi], sc)
+        theta16[lo:hi] = adamw_step_fp32(t, mm, vv, g16_dev[lo:hi], sc, half)
         theta_host[lo:hi] = t                      # D2H
         m_host[lo:hi] = mm
         v_host[lo:hi] = vv

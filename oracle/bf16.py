@@ -29,3 +29,21 @@ def to_bf16_bits(x) -> np.ndarray:
 
 def from_bf16_bits(b) -> np.ndarray:
     return (np.asarray(b, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+def round_fp16(x) -> np.ndarray:
+    """RNE of float32 values to IEEE binary16 (the paper's V100 half format,
+    PAPER.md:202-206; reading D-31 variant N2), returned as float32.  Overflow
+    beyond 65504 (after rounding) gives +-inf, tiny values become subnormal.
+    Pinned by tests/test_oracle_misc.py (0.1 -> 0.0999755859375, 65520 -> inf,
+    2^-25 ties to 0, torch cast cross-check)."""
+    return np.asarray(x, dtype=np.float32).astype(np.float16).astype(np.float32)
+
+
+def round_half(x, half: str = "bf16") -> np.ndarray:
+    """RNE to the 16-bit format of theta16 / the gradients: 'bf16' or 'fp16'."""
+    if half == "bf16":
+        return round_bf16(x)
+    if half == "fp16":
+        return round_fp16(x)
+    raise ValueError(half)

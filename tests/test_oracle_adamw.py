@@ -102,3 +102,39 @@ def test_step_scalars_rounded_once():
     assert sc["step"] == np.float32(1e-3 / (1 - 0.9))
     assert sc["bc2_sqrt"] == np.float32(math.sqrt(1 - 0.999))
     assert sc["decay"] == np.float32(1 - 1e-5)
+
+
+def test_overflow_skip_rule():
+    """Reading D-12 (PAPER.md:198-201 loss scaling; SPEC.md:181 NonFiniteGradient): one inf or
+    NaN anywhere skips the step; finite gradients of any magnitude do not."""
+    g = np.zeros(1000, np.float32)
+    assert adamw.grads_finite(g)
+    g[17] = 65504.0
+    assert adamw.grads_finite(g)
+    for bad in (np.inf, -np.inf, np.nan):
+        h = g.copy()
+        h[999] = bad
+        assert not adamw.grads_finite(h)
+    # fp16 overflow of a sum of two finite values (what the column all-reduce can produce)
+    from oracle.bf16 import round_fp16
+    assert not adamw.grads_finite(round_fp16(np.float32(60000.0) + np.float32(60000.0)))
+
+
+def test_fp16_theta16_is_rne_fp16():
+    """N2: with half='fp16' theta16 = RNE_fp16(theta32) (PAPER.md:193-196), and theta32/m/v
+    are bit-identical to the bf16 run (the half format only changes theta16)."""
+    from oracle.bf16 import round_fp16
+    rng = np.random.default_rng(3)
+    th = (rng.standard_normal(4096) * 0.02).astype(np.float32)
+    m = (rng.standard_normal(4096) * 1e-3).astype(np.float32)
+    v = np.abs(rng.standard_normal(4096) * 1e-6).astype(np.float32)
+    g = round_fp16((rng.standard_normal(4096) * 1e-3).astype(np.float32))
+    sc = adamw.step_scalars(3, loss_scale=1024.0)
+    a = [th.copy(), m.copy(), v.copy()]
+    b = [th.copy(), m.copy(), v.copy()]
+    t16a = adamw.adamw_step_fp32(*a, g * 1024, sc, "fp16")
+    t16b = adamw.adamw_step_fp32(*b, g * 1024, sc, "bf16")
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    assert np.array_equal(t16a, round_fp16(a[0]))
+    assert not np.array_equal(t16a, t16b)

@@ -4,7 +4,7 @@ from fractions import Fraction
 import numpy as np
 
 from oracle import metrics
-from oracle.bf16 import from_bf16_bits, round_bf16, to_bf16_bits
+from oracle.bf16 import from_bf16_bits, round_bf16, round_fp16, to_bf16_bits
 
 
 def test_bf16_rne_values():
@@ -29,6 +29,28 @@ def test_bf16_vs_torch_cast():
     assert np.array_equal(round_bf16(x), ref)
     bits = to_bf16_bits(x)
     assert np.array_equal(from_bf16_bits(bits), ref)
+
+
+def test_fp16_rne_values():
+    """Pin 14 (fp16 part, N2): fp16(0.1) = 0.0999755859375; the largest finite value 65504;
+    65520 (halfway to 2^16) rounds to inf; 2^-25 is a tie between 0 and the smallest
+    subnormal 2^-24 -> 0 (even); 3*2^-25 -> 2^-23; ties to even at 1 + 2^-11."""
+    f = lambda x: float(round_fp16(np.float32(x))[()])
+    assert f(0.1) == 0.0999755859375
+    assert f(65504.0) == 65504.0 and f(65519.0) == 65504.0
+    assert np.isinf(f(65520.0)) and np.isinf(f(-1e6)) and f(-1e6) < 0
+    assert f(2.0 ** -25) == 0.0 and f(3 * 2.0 ** -25) == 2.0 ** -23 and f(2.0 ** -24) == 2.0 ** -24
+    assert f(1 + 2 ** -11) == 1.0 and f(1 + 3 * 2 ** -11) == 1 + 2 ** -9
+    assert np.isnan(f(np.nan))
+
+
+def test_fp16_vs_torch_cast():
+    """Cross-check against torch's float32 -> float16 cast (library routine)."""
+    import torch
+    rng = np.random.default_rng(1)
+    x = (rng.standard_normal(100000) * np.exp(rng.uniform(-25, 15, 100000))).astype(np.float32)
+    ref = torch.tensor(x).to(torch.float16).to(torch.float32).numpy()
+    assert np.array_equal(round_fp16(x), ref)
 
 
 def test_eq2():
