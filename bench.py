@@ -210,6 +210,10 @@ def main():
     ap.add_argument("--offload", type=int, default=None, help="1/0: override the config's offload")
     ap.add_argument("--checkpoint-interval", type=int, default=0,
                     help="activation checkpointing ac (PAPER.md:553-576): 0 off, -1 the paper's rule")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"],
+                    help="half format (library build); fp16 runs with a static loss scale (D-11)")
+    ap.add_argument("--loss-scale", type=float, default=None,
+                    help="static loss scale S (default 1 for bf16, 1024 for fp16)")
     ap.add_argument("--g-inter", type=int, default=None,
                     help="pipeline stages (pipeline configs; G_data = N / G_inter)")
     args = ap.parse_args()
@@ -244,7 +248,8 @@ def main():
     eng = AxoNN(g_inter, g_data, b_m, n_layers=cfg["n_layers"], hidden=cfg["hidden"],
                 heads=cfg["heads"], seq_len=cfg["seq_len"], vocab=cfg["vocab"], init_seed=42,
                 offload=cfg["offload"], rank=rank, world_size=world, device=local, nccl_id=nid,
-                checkpoint_interval=args.checkpoint_interval)
+                checkpoint_interval=args.checkpoint_interval, dtype=args.dtype,
+                loss_scale=args.loss_scale or (1024.0 if args.dtype == "fp16" else 1.0))
     from synth import uniform_tokens
     s, V = cfg["seq_len"], cfg["vocab"]
     tokens = uniform_tokens(B, s, V, seed=1234)          # full batch on the host (pinned below)
@@ -335,7 +340,7 @@ def main():
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "bf16",
+            "dtype": args.dtype,
             "data": "synthetic (uniform tokens, splitmix64 seed 1234; random-init weights seed 42)",
             "config": {"workload": args.config, "model": f"GPT {cfg['n_layers']}L h{cfg['hidden']} "
                        f"a{cfg['heads']} s{s} V{V}", "global_batch": B, "seq_len": s,

@@ -51,17 +51,30 @@ typedef enum {
   AXONN_ERR_TIMEOUT = -10              /* scheduler watchdog: no message progress */
 } axonn_status;
 
+/* Half-precision format of theta16, activations, messages and the all-reduce
+ * (PAPER.md:193-206 mixed precision).  bf16 is the B200 default (reading D-31);
+ * fp16 is the paper's own format and needs a loss scale (D-11) with the
+ * overflow skip of D-12.  The format is a build-time specialisation of every
+ * kernel: libaxonn.so computes in bf16, libaxonn_fp16.so in fp16, both export
+ * this same ABI (axonn_half_dtype says which). */
+typedef enum { AXONN_BF16 = 0, AXONN_FP16 = 1 } axonn_dtype;
+
 /* GPT shape (layers, hidden size, heads; seq and vocab PAPER.md:839-840). */
 typedef struct {
   int n_layers, hidden, heads, seq_len, vocab;
   uint64_t init_seed;   /* weights N(0,0.02) (D-22) generated on device; overwrite with axonn_write_tensor */
+  int dtype;            /* axonn_dtype; must equal axonn_half_dtype() of the loaded library,
+                           else axonn_init returns AXONN_ERR_INVALID_ARG */
 } axonn_model_cfg;
 
 /* Optimizer and memory-optimisation knobs. */
 typedef struct {
   double lr, beta1, beta2, eps, weight_decay; /* paper: 1e-3, 0.9, 0.999, (1e-8, D-13), 0.01;
                                                  step scalars are formed in double, rounded once (D-14) */
-  double loss_scale;                          /* S (D-11); 1 for bf16 */
+  double loss_scale;                          /* S (D-11): static; the loss (hence every gradient)
+                                                 is multiplied by S in the backward and K9 divides
+                                                 it out.  1 for bf16; fp16: a
+                                                 power of two such as 1024 */
   int offload;                                /* 1: fp32 theta + Adam state in pinned host memory */
   int64_t bucket_elems;                       /* bsize in elements (D-16); paper 4M */
   int coarsen_k;                              /* all-reduce chunk = k * bsize elements; paper 4 */
@@ -91,13 +104,16 @@ typedef struct {
 
 /* Tensor kinds for inspection (canonical oracle layout, fp32 on the host). */
 typedef enum {
-  AXONN_T_PARAM16 = 0,   /* theta16 (bf16 on device)                                   */
-  AXONN_T_GRAD = 1,      /* reduced half-precision gradient (bf16), input of the optimizer */
+  AXONN_T_PARAM16 = 0,   /* theta16 (bf16 / fp16 on device)                            */
+  AXONN_T_GRAD = 1,      /* reduced half-precision gradient (x S), input of the optimizer */
   AXONN_T_MASTER = 2,    /* fp32 master theta (device or pinned host)                  */
   AXONN_T_ADAM_M = 3,
   AXONN_T_ADAM_V = 4,
   AXONN_T_GRAD32 = 5     /* fp32 accumulation buffer (D-20)                            */
 } axonn_which;
+
+/* The half-precision format this library build computes in (axonn_dtype). */
+AXONN_API int axonn_half_dtype(void);
 
 /* Writes rank 0's 128-byte ncclUniqueId into out. */
 AXONN_API axonn_status axonn_get_unique_id(void* out128);
@@ -130,7 +146,14 @@ AXONN_API axonn_status axonn_run_batch_device(axonn_ctx* ctx, const int32_t* d_t
  * this stage, bucket by bucket, each bucket's update
  * enqueued as soon as its all-reduce chunk completes;
  * refreshes theta16 = RNE(theta32).  Collective.  Errors: STATE, NONFINITE,
- * CUDA, NCCL. */
+ * CUDA, NCCL.
+ * fp16 build (reading D-12): before any bucket is updated the reduced
+ * gradients of the stage are scanned for inf/NaN and the flag is MAX-reduced
+ * over all ranks; if set, no parameter or Adam state changes, t is not
+ * incremented and every rank returns AXONN_ERR_NONFINITE (not sticky: the
+ * context stays usable and the next call is axonn_run_batch).  This scan
+ * needs the whole all-reduce first, so the fp16 build gives up the
+ * chunk-by-chunk all-reduce/optimizer interleave. */
 AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* ctx);
 
 /* Synchronise and release everything the context owns. */
@@ -145,7 +168,7 @@ AXONN_API axonn_status axonn_tensor_info(const axonn_ctx* ctx, int idx, char nam
                                int64_t* numel);
 /* Synchronising fp32 copies; host buffers hold numel floats.  Writing
  * AXONN_T_GRAD for every tensor marks the gradients reduced, so
- * axonn_optimizer_step can run without run_batch (values are rounded to bf16).
+ * axonn_optimizer_step can run without run_batch (values are rounded to the half format).
  * Writing AXONN_T_MASTER also refreshes theta16 = RNE(theta32). */
 AXONN_API axonn_status axonn_read_tensor(axonn_ctx* ctx, int which, int idx, float* host_dst);
 AXONN_API axonn_status axonn_write_tensor(axonn_ctx* ctx, int which, int idx, const float* host_src);
@@ -190,7 +213,9 @@ AXONN_API axonn_status axonn_timer_elapsed(axonn_ctx* ctx, int id0, int id1, dou
 
 /* ---------------------------------------------------------------------------
  * Kernel-level entry points (device pointers; enqueue on `stream`, a
- * cudaStream_t or NULL for the legacy stream).  Used by the kernel parity
+ * cudaStream_t or NULL for the legacy stream).  "16-bit" below = the library's
+ * half format (bf16 in libaxonn.so, fp16 in libaxonn_fp16.so; the bf16 named in
+ * the comments reads as that format).  Used by the kernel parity
  * tests and microbenchmarks.  Return 0 on success, < 0 on a bad argument or
  * launch failure.
  * ------------------------------------------------------------------------- */

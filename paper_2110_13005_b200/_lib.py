@@ -1,4 +1,4 @@
-"""ctypes binding of libaxonn.so (include/axonn.h): argument marshalling only.
+"""ctypes binding of libaxonn.so / libaxonn_fp16.so (include/axonn.h): argument marshalling only.
 
 Every step of the hot path runs in the library's sm_100a kernels; there is
 no Python or CPU fallback.  If the shared library is missing or cannot be
@@ -10,8 +10,10 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libaxonn.so")
+LIB_PATHS = {"bf16": LIB_PATH, "fp16": os.path.join(HERE, "libaxonn_fp16.so")}
+DTYPES = {"bf16": 0, "fp16": 1}   # axonn_dtype
 
-_lib = None
+_libs: dict = {}
 
 
 class GemmArgs(C.Structure):
@@ -30,7 +32,8 @@ class GemmArgs(C.Structure):
 
 class ModelCfg(C.Structure):
     _fields_ = [("n_layers", C.c_int), ("hidden", C.c_int), ("heads", C.c_int),
-                ("seq_len", C.c_int), ("vocab", C.c_int), ("init_seed", C.c_uint64)]
+                ("seq_len", C.c_int), ("vocab", C.c_int), ("init_seed", C.c_uint64),
+                ("dtype", C.c_int)]
 
 
 class OptCfg(C.Structure):
@@ -49,6 +52,7 @@ class Dist(C.Structure):
 def _declare(lib):
     P, I, I64, F = C.c_void_p, C.c_int, C.c_int64, C.c_float
     sig = {
+        "axonn_half_dtype": (I, []),
         "axonn_get_unique_id": (I, [P]),
         "axonn_init": (I, [I, I, I, C.POINTER(ModelCfg), C.POINTER(OptCfg), C.POINTER(Dist),
                            C.POINTER(C.c_void_p)]),
@@ -80,15 +84,22 @@ def _declare(lib):
     return lib
 
 
-def load():
-    """Load (building first if needed) the in-tree libaxonn.so."""
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
+def load(dtype: str = "bf16"):
+    """Load (building first if needed) the in-tree library of the half format ``dtype``
+    ('bf16' -> libaxonn.so, 'fp16' -> libaxonn_fp16.so).  Both export the same symbols, so
+    the fp16 build is opened RTLD_LOCAL (and both are linked -Bsymbolic)."""
+    if dtype not in LIB_PATHS:
+        raise ValueError(f"dtype must be one of {list(LIB_PATHS)}")
+    if dtype not in _libs:
+        path = LIB_PATHS[dtype]
+        if not os.path.exists(path):
             from . import build
-            build.build()
-        _lib = _declare(C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL))
-    return _lib
+            build.build(dtypes=(dtype,))
+        lib = _declare(C.CDLL(path, mode=C.RTLD_GLOBAL if dtype == "bf16" else C.RTLD_LOCAL))
+        if lib.axonn_half_dtype() != DTYPES[dtype]:
+            raise RuntimeError(f"{path} reports half format {lib.axonn_half_dtype()}, expected {dtype}")
+        _libs[dtype] = lib
+    return _libs[dtype]
 
 
 def exported_symbols():

@@ -10,7 +10,7 @@
 // g16; write theta, m, v, theta16).  16-byte vector accesses, grid-stride
 // loop sized to a multiple of the SM count.
 #include <cuda_runtime.h>
-#include <cuda_bf16.h>
+#include "half.cuh"
 #include <cstdint>
 
 #include "kernels.h"
@@ -22,27 +22,27 @@ struct AdamScalars {
 };
 
 __device__ __forceinline__ void adam_one(float& th, float& m, float& v, float g16,
-                                         const AdamScalars& s, __nv_bfloat16& t16) {
+                                         const AdamScalars& s, hx& t16) {
   float g = __fmul_rn(g16, s.inv_scale);
   th = __fmul_rn(th, s.decay);
   m = __fadd_rn(__fmul_rn(s.b1, m), __fmul_rn(s.omb1, g));
   v = __fadd_rn(__fmul_rn(s.b2, v), __fmul_rn(s.omb2, __fmul_rn(g, g)));
   float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), s.bc2_sqrt), s.eps);
   th = __fsub_rn(th, __fmul_rn(s.step, __fdiv_rn(m, denom)));
-  t16 = __float2bfloat16_rn(th);
+  t16 = f2hx(th);
 }
 
-__global__ void __launch_bounds__(256) adamw_kernel(long long n, const __nv_bfloat16* __restrict__ g16,
+__global__ void __launch_bounds__(256) adamw_kernel(long long n, const hx* __restrict__ g16,
                                                     float* __restrict__ theta, float* __restrict__ m,
                                                     float* __restrict__ v,
-                                                    __nv_bfloat16* __restrict__ theta16,
+                                                    hx* __restrict__ theta16,
                                                     AdamScalars s) {
   const long long nvec = n / 4;
   const long long stride = (long long)gridDim.x * blockDim.x;
   auto step4 = [&](long long i, float4 th, float4 mm, float4 vv, uint2 graw) {
-    __nv_bfloat162 g01 = *reinterpret_cast<__nv_bfloat162*>(&graw.x);
-    __nv_bfloat162 g23 = *reinterpret_cast<__nv_bfloat162*>(&graw.y);
-    __nv_bfloat16 o[4];
+    hx2 g01 = *reinterpret_cast<hx2*>(&graw.x);
+    hx2 g23 = *reinterpret_cast<hx2*>(&graw.y);
+    hx o[4];
     adam_one(th.x, mm.x, vv.x, __low2float(g01), s, o[0]);
     adam_one(th.y, mm.y, vv.y, __high2float(g01), s, o[1]);
     adam_one(th.z, mm.z, vv.z, __low2float(g23), s, o[2]);
@@ -51,8 +51,8 @@ __global__ void __launch_bounds__(256) adamw_kernel(long long n, const __nv_bflo
     reinterpret_cast<float4*>(m)[i] = mm;
     reinterpret_cast<float4*>(v)[i] = vv;
     uint2 out;
-    __nv_bfloat162 p01 = __halves2bfloat162(o[0], o[1]);
-    __nv_bfloat162 p23 = __halves2bfloat162(o[2], o[3]);
+    hx2 p01 = hx2_pack(o[0], o[1]);
+    hx2 p23 = hx2_pack(o[2], o[3]);
     out.x = *reinterpret_cast<uint32_t*>(&p01);
     out.y = *reinterpret_cast<uint32_t*>(&p23);
     reinterpret_cast<uint2*>(theta16)[i] = out;
@@ -78,8 +78,8 @@ __global__ void __launch_bounds__(256) adamw_kernel(long long n, const __nv_bflo
   // ragged tail (n % 4)
   for (long long i = nvec * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     float th = theta[i], mm = m[i], vv = v[i];
-    __nv_bfloat16 o;
-    adam_one(th, mm, vv, __bfloat162float(g16[i]), s, o);
+    hx o;
+    adam_one(th, mm, vv, hx2f(g16[i]), s, o);
     theta[i] = th;
     m[i] = mm;
     v[i] = vv;
@@ -106,9 +106,9 @@ int adamw_launch(long long n, const void* g16, float* theta, float* m, float* v,
   long long blocks = (nvec + 255) / 256;
   long long cap = (long long)g_sms_adam * 8;   // 8 resident 256-thread CTAs per SM
   if (blocks > cap) blocks = cap;
-  adamw_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, reinterpret_cast<const __nv_bfloat16*>(g16),
+  adamw_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, reinterpret_cast<const hx*>(g16),
                                                  theta, m, v,
-                                                 reinterpret_cast<__nv_bfloat16*>(theta16), s);
+                                                 reinterpret_cast<hx*>(theta16), s);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

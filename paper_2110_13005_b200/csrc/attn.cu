@@ -14,7 +14,7 @@
 //   key half [256 half, 256 half + 256).
 #include <cuda.h>
 #include <cuda_runtime.h>
-#include <cuda_bf16.h>
+#include "half.cuh"
 #include <cstdint>
 #include <cstdlib>
 
@@ -33,7 +33,7 @@ constexpr int KH_BYTES = 256 * KB * 2;  // 32 KB (one key half)
 constexpr int ATT_STAGE = Q_BYTES + 2 * KH_BYTES;   // 80 KB: Q + K, or one V block (<= 32 KB)
 constexpr int ATT_THREADS = 64 + 8 * 32;
 
-__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -54,8 +54,8 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 __device__ __forceinline__ void nbar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+__device__ __forceinline__ uint32_t pack_hx2(float lo, float hi) {
+  hx2 v = f2hx2(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 // TMEM column holding the packed P pair of key `key` (two keys per 32-bit column)
@@ -74,7 +74,7 @@ __device__ __forceinline__ int snake_unit(int r) {
 struct AttnParams {
   int s, heads, d, nv, num_m, total;
   float c1;               // alpha * log2(e)
-  __nv_bfloat16* o;
+  hx* o;
   long long ldo;
   float* lse;
 };
@@ -153,8 +153,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    const uint32_t idS = umma_idesc_bf16(QT, 256, 0, 0);
-    const uint32_t idO = umma_idesc_bf16(QT, p.nv, 0, 1);
+    const uint32_t idS = umma_idesc_f16(QT, 256, 0, 0);
+    const uint32_t idO = umma_idesc_f16(QT, p.nv, 0, 1);
     const uint64_t d0 = umma_desc_sw128(smem_u32(smem), 16, 1024);          // K-major (Q, K)
     const uint64_t v0 = umma_desc_sw128(smem_u32(smem), 8192, 1024);        // MN-major (V)
     int stage = 0;
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < KB / 16; ++k)
             for (int hh = 0; hh < nh; ++hh)
-              mma_bf16_ss(tmem + 256 * hh, ad + 2 * k, ad + ((Q_BYTES + hh * KH_BYTES) >> 4) + 2 * k,
+              mma_f16_ss(tmem + 256 * hh, ad + 2 * k, ad + ((Q_BYTES + hh * KH_BYTES) >> 4) + 2 * k,
                           idS, (kb > 0 || k > 0) ? 1u : 0u);
           mma_commit(&empty[stage]);
         }
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_bf16_ts(tmem + 128, tmem + p_col(64 * j + 16 * k), vd + k * (2048 >> 4), idO,
+            mma_f16_ts(tmem + 128, tmem + p_col(64 * j + 16 * k), vd + k * (2048 >> 4), idO,
                         (j > 0 || k > 0) ? 1u : 0u);
           mma_commit(&empty[stage]);
         }
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             }
             s0 += e0;
             s1 += e1;
-            pk[i / 2] = pack_bf16(e0, e1);
+            pk[i / 2] = pack_hx2(e0, e1);
           }
         } else {
 #pragma unroll
@@ -287,17 +287,17 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       mbar_wait(o_full, it & 1);
       tc_fence_after();
       const int ncol = p.nv / 2;
-      __nv_bfloat16* obase = p.o + ((long long)z2 * p.s) * p.ldo + (long long)z1 * p.d;
+      hx* obase = p.o + ((long long)z2 * p.s) * p.ldo + (long long)z1 * p.d;
       for (int cc = 0; cc < ncol; cc += 32) {
         const int oc = half * ncol + cc;                          // head-dim column
         tmem_ld32(trow + 128 + oc, r);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           uint4 u;
-          u.x = pack_bf16(__uint_as_float(r[8 * j + 0]) * inv, __uint_as_float(r[8 * j + 1]) * inv);
-          u.y = pack_bf16(__uint_as_float(r[8 * j + 2]) * inv, __uint_as_float(r[8 * j + 3]) * inv);
-          u.z = pack_bf16(__uint_as_float(r[8 * j + 4]) * inv, __uint_as_float(r[8 * j + 5]) * inv);
-          u.w = pack_bf16(__uint_as_float(r[8 * j + 6]) * inv, __uint_as_float(r[8 * j + 7]) * inv);
+          u.x = pack_hx2(__uint_as_float(r[8 * j + 0]) * inv, __uint_as_float(r[8 * j + 1]) * inv);
+          u.y = pack_hx2(__uint_as_float(r[8 * j + 2]) * inv, __uint_as_float(r[8 * j + 3]) * inv);
+          u.z = pack_hx2(__uint_as_float(r[8 * j + 4]) * inv, __uint_as_float(r[8 * j + 5]) * inv);
+          u.w = pack_hx2(__uint_as_float(r[8 * j + 6]) * inv, __uint_as_float(r[8 * j + 7]) * inv);
           stg[lane * 4 + (j ^ (lane & 3))] = u;
         }
         __syncwarp();
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           const int col = oc + ch * 8;
           if (gr < p.s && col < p.d) {
             const uint4 v = stg[rr * 4 + (ch ^ (rr & 3))];
-            __nv_bfloat16* dst = obase + (long long)gr * p.ldo + col;
+            hx* dst = obase + (long long)gr * p.ldo + col;
             if ((p.d & 7) == 0) {
               *reinterpret_cast<uint4*>(dst) = v;
             } else {   // unaligned head width (d = 188, 176): bf16 pairs
@@ -356,7 +356,7 @@ struct AttnBwdParams {
   float c1, alpha;
   const float* lse;
   const float* D;
-  __nv_bfloat16* dq;   // dqkv base; dQ at column z1*d, dK at h + z1*d, dV at 2h + z1*d
+  hx* dq;   // dqkv base; dQ at column z1*d, dK at h + z1*d, dV at 2h + z1*d
   long long ldq;
   int h;
 };
@@ -375,15 +375,15 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, 
 // 32 rows x 32 bf16 (this warp's chunk, row = lane) -> global rows r0.., columns col0..
 // (only col < dvalid), through a swizzled 2 KB staging tile: 8 rows x 64 B per instruction
 __device__ __forceinline__ void store_chunk32(uint4* stg, int lane, const uint32_t (&r)[32],
-                                              float scale, __nv_bfloat16* gbase, long long ld,
+                                              float scale, hx* gbase, long long ld,
                                               int r0, int rows_valid, int col0, int dvalid) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     uint4 u;
-    u.x = pack_bf16(__uint_as_float(r[8 * j + 0]) * scale, __uint_as_float(r[8 * j + 1]) * scale);
-    u.y = pack_bf16(__uint_as_float(r[8 * j + 2]) * scale, __uint_as_float(r[8 * j + 3]) * scale);
-    u.z = pack_bf16(__uint_as_float(r[8 * j + 4]) * scale, __uint_as_float(r[8 * j + 5]) * scale);
-    u.w = pack_bf16(__uint_as_float(r[8 * j + 6]) * scale, __uint_as_float(r[8 * j + 7]) * scale);
+    u.x = pack_hx2(__uint_as_float(r[8 * j + 0]) * scale, __uint_as_float(r[8 * j + 1]) * scale);
+    u.y = pack_hx2(__uint_as_float(r[8 * j + 2]) * scale, __uint_as_float(r[8 * j + 3]) * scale);
+    u.z = pack_hx2(__uint_as_float(r[8 * j + 4]) * scale, __uint_as_float(r[8 * j + 5]) * scale);
+    u.w = pack_hx2(__uint_as_float(r[8 * j + 6]) * scale, __uint_as_float(r[8 * j + 7]) * scale);
     stg[lane * 4 + (j ^ (lane & 3))] = u;
   }
   __syncwarp();
@@ -394,7 +394,7 @@ __device__ __forceinline__ void store_chunk32(uint4* stg, int lane, const uint32
     const int col = col0 + ch * 8;
     if (gr < rows_valid && col < dvalid) {
       const uint4 v = stg[rr * 4 + (ch ^ (rr & 3))];
-      __nv_bfloat16* dst = gbase + (long long)gr * ld + col;
+      hx* dst = gbase + (long long)gr * ld + col;
       if ((dvalid & 7) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
         *reinterpret_cast<uint4*>(dst) = v;
       } else {
@@ -503,8 +503,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    const uint32_t idXY = umma_idesc_bf16(128, GR, 0, 0);
-    const uint32_t idAcc = umma_idesc_bf16(128, p.nv, 0, 1);
+    const uint32_t idXY = umma_idesc_f16(128, GR, 0, 0);
+    const uint32_t idAcc = umma_idesc_f16(128, p.nv, 0, 1);
     const uint32_t sG0 = smem_u32(sG);
     int g = 0;                        // global block counter (stage / buffer / parity source)
     uint32_t accd_ph[2] = {0, 0};     // acc_done uses per buffer
@@ -527,9 +527,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t acc = (c > 0 || k > 0) ? 1u : 0u;
-            mma_bf16_ss(tmem + 128 * b, umma_desc_sw128(sF0 + c * FR * 128 + 32 * k, 16, 1024),
+            mma_f16_ss(tmem + 128 * b, umma_desc_sw128(sF0 + c * FR * 128 + 32 * k, 16, 1024),
                         umma_desc_sw128(g1 + c * GR * 128 + 32 * k, 16, 1024), idXY, acc);
-            mma_bf16_ss(tmem + 128 * b + 64,
+            mma_f16_ss(tmem + 128 * b + 64,
                         umma_desc_sw128(sF0 + f_bytes + c * FR * 128 + 32 * k, 16, 1024),
                         umma_desc_sw128(g2 + c * GR * 128 + 32 * k, 16, 1024), idXY, acc);
           }
@@ -576,9 +576,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
             const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
             const uint32_t pc = 128 * b + (k >> 1) * 32 + (k & 1) * 8;
             if (KA)
-              mma_bf16_ts(tmem + colA, tmem + pc, umma_desc_sw128(g2 + 2048 * k, GR * 128, 1024),
+              mma_f16_ts(tmem + colA, tmem + pc, umma_desc_sw128(g2 + 2048 * k, GR * 128, 1024),
                           idAcc, acc);
-            mma_bf16_ts(tmem + colB, tmem + pc + 64, umma_desc_sw128(g1 + 2048 * k, GR * 128, 1024),
+            mma_f16_ts(tmem + colB, tmem + pc + 64, umma_desc_sw128(g1 + 2048 * k, GR * 128, 1024),
                         idAcc, acc);
           }
           mma_commit(&g_empty[stg]);
@@ -664,8 +664,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
             P2[e] = P;
             S2[e] = P * (__uint_as_float(y[i + e]) - Dv) * p.alpha;
           }
-          pp[i / 2] = pack_bf16(P2[0], P2[1]);
-          pd[i / 2] = pack_bf16(S2[0], S2[1]);
+          pp[i / 2] = pack_hx2(P2[0], P2[1]);
+          pd[i / 2] = pack_hx2(S2[0], S2[1]);
         }
         if (KA) tmem_st16(trow + 128 * b + c0, pp);
         tmem_st16(trow + 128 * b + 64 + c0, pd);
@@ -679,11 +679,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const uint32_t colA = 128 * p.nbuf + ab * acc_w, colB = colA + (KA ? p.nv : 0);
       mbar_wait(&acc_full[ab], (uint32_t)((u / p.nab) & 1));
       tc_fence_after();
-      __nv_bfloat16* base = p.dq + (long long)z2 * p.s * p.ldq + (long long)z1 * p.d;
+      hx* base = p.dq + (long long)z2 * p.s * p.ldq + (long long)z1 * p.d;
       const int r0w = r0 + q * 32;
       for (int which = KA ? 0 : 1; which < 2; ++which) {
         const uint32_t ca = which == 0 ? colA : colB;
-        __nv_bfloat16* gb = base + (KA ? (which == 0 ? 2 * p.h : p.h) : 0);
+        hx* gb = base + (KA ? (which == 0 ? 2 * p.h : p.h) : 0);
         for (int cc = 0; cc < p.nv / 2; cc += 32) {
           const int oc = half * (p.nv / 2) + cc;
           uint32_t r[32];
@@ -707,8 +707,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 // D[z * s + i] = sum_j dO[i, head, j] * O[i, head * d + j]   (fp32); 16 lanes per (token, head),
 // DITEMS (token, head) items per 16-lane group with every load issued before the math
 constexpr int DITEMS = 4;
-__global__ void attn_bwd_d_kernel(const __nv_bfloat16* __restrict__ dO, long long ld_do, int dp,
-                                  const __nv_bfloat16* __restrict__ O, long long ld_o, int d,
+__global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, int dp,
+                                  const hx* __restrict__ O, long long ld_o, int d,
                                   int s, int heads, long long ntok, float* __restrict__ D) {
   const long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 16;
   const int l = threadIdx.x & 15;
@@ -730,12 +730,12 @@ __global__ void attn_bwd_d_kernel(const __nv_bfloat16* __restrict__ dO, long lon
     }
 #pragma unroll
     for (int u = 0; u < DITEMS; ++u) {
-      const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&x[u]);
-      const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&y[u]);
+      const hx2* xh = reinterpret_cast<const hx2*>(&x[u]);
+      const hx2* yh = reinterpret_cast<const hx2*>(&y[u]);
       float a = 0.f;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float2 xf = __bfloat1622float2(xh[e]), yf = __bfloat1622float2(yh[e]);
+        const float2 xf = hx22f2(xh[e]), yf = hx22f2(yh[e]);
         a = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, a));
       }
       acc[u] = a;
@@ -748,11 +748,11 @@ __global__ void attn_bwd_d_kernel(const __nv_bfloat16* __restrict__ dO, long lon
       if (w < nitems) {
         const long long tok = w / heads;
         const int hd = (int)(w % heads);
-        const __nv_bfloat16* xa = dO + tok * ld_do + (long long)hd * dp;
-        const __nv_bfloat16* ya = O + tok * ld_o + (long long)hd * d;
+        const hx* xa = dO + tok * ld_do + (long long)hd * dp;
+        const hx* ya = O + tok * ld_o + (long long)hd * d;
         for (int j = 2 * l; j < d; j += 32) {
-          const float2 xf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(xa + j));
-          const float2 yf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(ya + j));
+          const float2 xf = hx22f2(*reinterpret_cast<const hx2*>(xa + j));
+          const float2 yf = hx22f2(*reinterpret_cast<const hx2*>(ya + j));
           a = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, a));
         }
       }
@@ -804,7 +804,7 @@ int attn_fwd(const void* qkv, long long lq, int b, int heads, int s, int d, int 
   p.num_m = (s + QT - 1) / QT;
   p.total = p.num_m * b * heads;
   p.c1 = alpha * 1.4426950408889634f;
-  p.o = static_cast<__nv_bfloat16*>(o);
+  p.o = static_cast<hx*>(o);
   p.ldo = ldo;
   p.lse = lse;
   int nsm = 0, dev = 0;
@@ -825,8 +825,8 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   {
     const long long nthreads = (ntok * heads + DITEMS - 1) / DITEMS * 16;
     attn_bwd_d_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(dO), (long long)heads * dp, dp,
-        static_cast<const __nv_bfloat16*>(o), ldo, d, s, heads, ntok, Dbuf);
+        static_cast<const hx*>(dO), (long long)heads * dp, dp,
+        static_cast<const hx*>(o), ldo, d, s, heads, ntok, Dbuf);
   }
   const char* base = static_cast<const char*>(qkv);
   CUtensorMap mq, mk, mv, mo;
@@ -848,7 +848,7 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   p.alpha = alpha;
   p.lse = lse;
   p.D = Dbuf;
-  p.dq = static_cast<__nv_bfloat16*>(dqkv);
+  p.dq = static_cast<hx*>(dqkv);
   p.ldq = ldq;
   p.h = heads * d;
   {

@@ -57,19 +57,18 @@ cudaEvent_t Ctx::ev_opt() {
   return ev_pool_opt[ev_next_opt++];
 }
 
-static uint16_t f2bf(float f) {   // round-to-nearest-even (host side of theta16 writes)
-  uint32_t u;
-  memcpy(&u, &f, 4);
-  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x7FFFFFu)) return (uint16_t)((u >> 16) | 0x40);
-  uint32_t lsb = (u >> 16) & 1u;
-  u += 0x7FFFu + lsb;
-  return (uint16_t)(u >> 16);
+// host side of the 16-bit reads / writes (theta16 and GRAD inspection): RNE to the library's
+// half format (half.cuh; the cuda_bf16 / cuda_fp16 conversions are host-callable)
+static uint16_t f2h16(float f) {
+  const hx h = f2hx(f);
+  uint16_t u;
+  memcpy(&u, &h, 2);
+  return u;
 }
-static float bf2f(uint16_t b) {
-  uint32_t u = (uint32_t)b << 16;
-  float f;
-  memcpy(&f, &u, 4);
-  return f;
+static float h162f(uint16_t b) {
+  hx h;
+  memcpy(&h, &b, 2);
+  return hx2f(h);
 }
 
 #define CU(x)                                  \
@@ -143,7 +142,7 @@ static int init_weights(Ctx* c) {
     if (cudaMemcpyAsync(tmp.data(), c->theta16, c->nflat * 2, cudaMemcpyDeviceToHost, c->s_comp) != cudaSuccess ||
         cudaStreamSynchronize(c->s_comp) != cudaSuccess)
       return c->fail(AXONN_ERR_CUDA, "init offload copy");
-    for (int64_t i = 0; i < c->nflat; ++i) c->master[i] = bf2f(tmp[i]);
+    for (int64_t i = 0; i < c->nflat; ++i) c->master[i] = h162f(tmp[i]);
   }
   return 0;
 }
@@ -256,6 +255,8 @@ static int plan_memory(Ctx* c) {
       !c->dx1 || !c->cs_ws || !c->cs_ws_ln || !c->row_loss || !c->d_loss || (c->last && !c->logits))
     return c->fail(AXONN_ERR_OOM, "workspace allocation");
   if (cudaMallocHost(&c->h_loss, 64) != cudaSuccess) return c->fail(AXONN_ERR_OOM, "pinned loss");
+  c->d_flag = reinterpret_cast<int*>(reinterpret_cast<char*>(c->d_loss) + 32);
+  c->h_flag = reinterpret_cast<int*>(reinterpret_cast<char*>(c->h_loss) + 32);
   // parameters, gradients, optimizer state
   c->theta16 = c->dalloc(c->nflat * 2);
   c->grad32 = (float*)c->dalloc(c->nflat * 4);
@@ -298,6 +299,8 @@ struct axonn_ctx : public Ctx {};
 
 extern "C" {
 
+AXONN_API int axonn_half_dtype(void) { return kHalfDtype; }
+
 AXONN_API axonn_status axonn_get_unique_id(void* out128) {
   if (!out128) return AXONN_ERR_INVALID_ARG;
   ncclUniqueId id;
@@ -312,6 +315,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   if (!out) return AXONN_ERR_INVALID_ARG;
   *out = nullptr;
   if (!model || !opt || g_inter < 1 || g_data < 1 || microbatch < 1) return AXONN_ERR_INVALID_ARG;
+  if (model->dtype != kHalfDtype) return AXONN_ERR_INVALID_ARG;   // other format: other library
   const int world = dist ? dist->world_size : 1;
   const int rank = dist ? dist->world_rank : 0;
   if (world != g_inter * g_data) return AXONN_ERR_GRID_MISMATCH;
@@ -434,15 +438,15 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
     if (!tmp) return bail(c->fail(AXONN_ERR_OOM, "link warm-up buffer"));
     for (int k = 0; k < g_inter - 1; ++k) {
       if (k == c->stage - 1) {   // boundary (i-1, i): receive activation, send gradient
-        if ((rc = c->check_nccl(ncclRecv(tmp, 8, ncclBfloat16, 0, c->act_in, c->s_comp), "warm recv")) ||
+        if ((rc = c->check_nccl(ncclRecv(tmp, 8, kNcclHalf, 0, c->act_in, c->s_comp), "warm recv")) ||
             (rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "warm sync")) ||
-            (rc = c->check_nccl(ncclSend(tmp, 8, ncclBfloat16, 0, c->grad_out, c->s_comp), "warm send")) ||
+            (rc = c->check_nccl(ncclSend(tmp, 8, kNcclHalf, 0, c->grad_out, c->s_comp), "warm send")) ||
             (rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "warm sync")))
           return bail(rc);
       } else if (k == c->stage) {   // boundary (i, i+1): send activation, receive gradient
-        if ((rc = c->check_nccl(ncclSend(tmp, 8, ncclBfloat16, 1, c->act_out, c->s_comp), "warm send")) ||
+        if ((rc = c->check_nccl(ncclSend(tmp, 8, kNcclHalf, 1, c->act_out, c->s_comp), "warm send")) ||
             (rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "warm sync")) ||
-            (rc = c->check_nccl(ncclRecv(tmp, 8, ncclBfloat16, 1, c->grad_in, c->s_comp), "warm recv")) ||
+            (rc = c->check_nccl(ncclRecv(tmp, 8, kNcclHalf, 1, c->grad_in, c->s_comp), "warm recv")) ||
             (rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "warm sync")))
           return bail(rc);
       }
@@ -523,7 +527,7 @@ AXONN_API axonn_status axonn_read_tensor(axonn_ctx* c, int which, int idx, float
       std::vector<uint16_t> tmp(t.numel);
       const char* base = static_cast<const char*>(which == AXONN_T_PARAM16 ? c->theta16 : c->grad16);
       CU(cudaMemcpy(tmp.data(), base + t.off * 2, t.numel * 2, cudaMemcpyDeviceToHost));
-      for (int64_t i = 0; i < t.numel; ++i) dst[i] = bf2f(tmp[i]);
+      for (int64_t i = 0; i < t.numel; ++i) dst[i] = h162f(tmp[i]);
       return AXONN_OK;
     }
     case AXONN_T_GRAD32:
@@ -550,7 +554,7 @@ AXONN_API axonn_status axonn_write_tensor(axonn_ctx* c, int which, int idx, cons
   std::vector<uint16_t> tmp;
   auto put16 = [&](void* base) -> int {
     tmp.resize(t.numel);
-    for (int64_t i = 0; i < t.numel; ++i) tmp[i] = f2bf(src[i]);
+    for (int64_t i = 0; i < t.numel; ++i) tmp[i] = f2h16(src[i]);
     return c->check_cuda(cudaMemcpy(static_cast<char*>(base) + t.off * 2, tmp.data(), t.numel * 2,
                                     cudaMemcpyHostToDevice), "write16");
   };
@@ -670,7 +674,7 @@ static int run_pipeline(Ctx* c, int m) {
       ev_act[mb] = c->ev();
       // the slot's previous occupant (mb - L) must have finished its backward on the GPU
       if (mb >= L) cudaStreamWaitEvent(c->s_recv_act, ev_bdone[mb - L], 0);
-      int r = c->check_nccl(ncclRecv(slot_of(mb).in, Mh, ncclBfloat16, 0, c->act_in, c->s_recv_act),
+      int r = c->check_nccl(ncclRecv(slot_of(mb).in, Mh, kNcclHalf, 0, c->act_in, c->s_recv_act),
                             "ncclRecv act");
       if (r) return r;
       if ((r = c->check_cuda(cudaEventRecord(ev_act[mb], c->s_recv_act), "rec"))) return r;
@@ -679,7 +683,7 @@ static int run_pipeline(Ctx* c, int m) {
       int mb = next_grad_post++;
       ev_grad[mb] = c->ev();
       if (mb >= L) cudaStreamWaitEvent(c->s_recv_grad, ev_bdone[mb - L], 0);
-      int r = c->check_nccl(ncclRecv(slot_of(mb).grecv, Mh, ncclBfloat16, 1, c->grad_in, c->s_recv_grad),
+      int r = c->check_nccl(ncclRecv(slot_of(mb).grecv, Mh, kNcclHalf, 1, c->grad_in, c->s_recv_grad),
                             "ncclRecv grad");
       if (r) return r;
       if ((r = c->check_cuda(cudaEventRecord(ev_grad[mb], c->s_recv_grad), "rec"))) return r;
@@ -693,7 +697,7 @@ static int run_pipeline(Ctx* c, int m) {
     cudaStreamWaitEvent(c->s_send_act, e, 0);
     const void* out = c->stage_out(sl);
     c->stats[AXONN_STAT_P2P_BYTES] += (double)Mh * 2;
-    int r = c->check_nccl(ncclSend(out, Mh, ncclBfloat16, 1, c->act_out, c->s_send_act), "ncclSend act");
+    int r = c->check_nccl(ncclSend(out, Mh, kNcclHalf, 1, c->act_out, c->s_send_act), "ncclSend act");
     ev_sent_act[mb] = c->ev();
     cudaEventRecord(ev_sent_act[mb], c->s_send_act);
     return r;
@@ -704,7 +708,7 @@ static int run_pipeline(Ctx* c, int m) {
     cudaEventRecord(e, c->s_comp);
     cudaStreamWaitEvent(c->s_send_grad, e, 0);
     c->stats[AXONN_STAT_P2P_BYTES] += (double)Mh * 2;
-    int r = c->check_nccl(ncclSend(sl.gsend, Mh, ncclBfloat16, 0, c->grad_out, c->s_send_grad),
+    int r = c->check_nccl(ncclSend(sl.gsend, Mh, kNcclHalf, 0, c->grad_out, c->s_send_grad),
                           "ncclSend grad");
     ev_sent_grad[mb] = c->ev();
     cudaEventRecord(ev_sent_grad[mb], c->s_send_grad);
@@ -860,7 +864,7 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   // grad16 is still read by a pending optimizer step until it completes
   if (c->opt_pending) CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
   // half-precision gradients (D-20: fp32 accumulation, bf16 reduction)
-  if (cast_f32_bf16(c->grad32, c->grad16, c->nflat, c->s_comp)) return (axonn_status)c->fail(AXONN_ERR_CUDA, "cast");
+  if (cast_f32_hx(c->grad32, c->grad16, c->nflat, c->s_comp)) return (axonn_status)c->fail(AXONN_ERR_CUDA, "cast");
   ++c->launches;
   CU(cudaEventRecord(c->ev_grads_ready, c->s_comp));
   if (c->g_data == 1) CU(cudaEventRecord(c->ph[par][2], c->s_comp));
@@ -879,7 +883,7 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
     for (int64_t lo = 0; lo < c->nflat; lo += ch) {
       int64_t n = std::min(ch, c->nflat - lo);
       NC(ncclAllReduce(static_cast<char*>(c->grad16) + lo * 2, static_cast<char*>(c->grad16) + lo * 2,
-                       n, ncclBfloat16, ncclSum, c->dp_comm, c->s_dp));
+                       n, kNcclHalf, ncclSum, c->dp_comm, c->s_dp));
       cudaEvent_t e = c->ev();
       CU(cudaEventRecord(e, c->s_dp));
       c->ev_chunk.push_back(e);
@@ -949,6 +953,30 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
   sc[8] = (float)(1.0 / c->oc.loss_scale);
   // the optimizer may start only once the gradients exist
   CU(cudaStreamWaitEvent(c->s_opt, c->ev_grads_ready, 0));
+  if (kHalfDtype == AXONN_FP16) {
+    // Reading D-12: skip the whole step if any reduced gradient of any stage overflowed.
+    // The flag needs the complete all-reduce (s_dp is past its last chunk), then one
+    // MAX over the world on s_dp (the stream of the other world-comm collective).
+    CU(cudaStreamWaitEvent(c->s_dp, c->ev_grads_ready, 0));
+    CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->s_dp));
+    if (nonfinite_scan(c->grad16, c->nflat, c->d_flag, c->s_dp))
+      return (axonn_status)c->fail(AXONN_ERR_CUDA, "nonfinite scan");
+    ++c->launches;
+    if (c->world > 1) NC(ncclAllReduce(c->d_flag, c->d_flag, 1, ncclInt32, ncclMax, c->world_comm, c->s_dp));
+    CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->s_dp));
+    cudaEvent_t e = c->ev();
+    CU(cudaEventRecord(e, c->s_dp));
+    CU(cudaEventSynchronize(e));
+    if (*c->h_flag) {   // nothing was updated; t stays; run_batch may follow
+      c->grads_ready = false;
+      c->ev_chunk.clear();
+      c->err = "non-finite gradient (fp16 overflow at loss scale " + std::to_string(c->oc.loss_scale) +
+               "): step skipped, t = " + std::to_string(c->t_step);
+      return AXONN_ERR_NONFINITE;
+    }
+    CU(cudaStreamWaitEvent(c->s_opt, e, 0));
+    c->ev_chunk.clear();   // every chunk is reduced: no per-bucket waits needed
+  }
   const int64_t bs = c->oc.bucket_elems;
   const int64_t ch = chunk_elems(c);
   int64_t chunk_idx = -1;

@@ -15,6 +15,12 @@
 
 namespace axonn {
 
+#ifdef AXONN_HALF_FP16
+constexpr ncclDataType_t kNcclHalf = ncclFloat16;
+#else
+constexpr ncclDataType_t kNcclHalf = ncclBfloat16;
+#endif
+
 struct TensorRec {
   std::string name;
   int64_t rows, cols, numel, off;   // off: element offset in every flat buffer
@@ -93,6 +99,8 @@ struct Ctx {
   float* row_loss = nullptr;
   double* d_loss = nullptr;           // device loss accumulator
   double* h_loss = nullptr;           // pinned
+  int* d_flag = nullptr;              // fp16 overflow flag (reading D-12), in d_loss's 64 B
+  int* h_flag = nullptr;              // pinned copy, in h_loss's 64 B
   int32_t* dtok = nullptr;            // this replica's token shard [B/G_data, s+1]
   int64_t dtok_cap = 0;
 

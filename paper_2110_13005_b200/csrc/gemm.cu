@@ -16,7 +16,7 @@
 // k*gridDim.x, M fastest so B tiles are shared through L2).
 #include <cuda.h>
 #include <cuda_runtime.h>
-#include <cuda_bf16.h>
+#include "half.cuh"
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -38,10 +38,10 @@ struct GemmParams {
   int col_group_in, col_group_out, n_valid;
   void* C;
   long long ldc, c_s1, c_s2;
-  const __nv_bfloat16* bias;
-  const __nv_bfloat16* resid;
+  const hx* bias;
+  const hx* resid;
   long long ld_resid;
-  __nv_bfloat16* aux;
+  hx* aux;
   long long ld_aux;
   float alpha;
   int num_m, num_n, total;
@@ -218,21 +218,21 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   float t = tanh_fast(c * (x + a * x * x * x));
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * c * (1.0f + 3.0f * a * x * x);
 }
-__device__ __forceinline__ void ld8_bf16(const __nv_bfloat16* p, float* f) {
+__device__ __forceinline__ void ld8_bf16(const hx* p, float* f) {
   uint4 u = *reinterpret_cast<const uint4*>(p);
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+  const hx2* h = reinterpret_cast<const hx2*>(&u);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    float2 t = __bfloat1622float2(h[i]);
+    float2 t = hx22f2(h[i]);
     f[2 * i] = t.x;
     f[2 * i + 1] = t.y;
   }
 }
-__device__ __forceinline__ void st8_bf16(__nv_bfloat16* p, const float* f) {
+__device__ __forceinline__ void st8_bf16(hx* p, const float* f) {
   uint4 u;
-  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+  hx2* h = reinterpret_cast<hx2*>(&u);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  for (int i = 0; i < 4; ++i) h[i] = f2hx2(f[2 * i], f[2 * i + 1]);
   *reinterpret_cast<uint4*>(p) = u;
 }
 __device__ __forceinline__ bool al16(const void* p) {
@@ -269,11 +269,11 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
     return;
   }
   {  // fast path: full 32-column chunk, every operand 16-byte aligned -> 16-byte accesses only
-    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.C) + z2 * p.c_s2 + z1 * p.c_s1 +
+    hx* dst = reinterpret_cast<hx*>(p.C) + z2 * p.c_s2 + z1 * p.c_s1 +
                          row * p.ldc + col0;
-    __nv_bfloat16* auxp = p.aux ? p.aux + row * p.ld_aux + col0 : nullptr;
-    const __nv_bfloat16* rsp = p.resid ? p.resid + row * p.ld_resid + col0 : nullptr;
-    const __nv_bfloat16* bp = p.bias ? p.bias + col0 : nullptr;
+    hx* auxp = p.aux ? p.aux + row * p.ld_aux + col0 : nullptr;
+    const hx* rsp = p.resid ? p.resid + row * p.ld_resid + col0 : nullptr;
+    const hx* bp = p.bias ? p.bias + col0 : nullptr;
     if (ncols == 32 && p.col_group_in == 0 && al16(dst) && (!auxp || al16(auxp)) &&
         (!rsp || al16(rsp)) && (!bp || al16(bp))) {
 #pragma unroll
@@ -289,7 +289,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
           st8_bf16(auxp + 8 * j, w);              // pre-activation (bf16) for the backward
 #pragma unroll
           for (int i = 0; i < 8; ++i)             // GeLU of the same rounded value
-            w[i] = gelu_f(__bfloat162float(__float2bfloat16_rn(w[i])));
+            w[i] = gelu_f(hx2f(f2hx(w[i])));
         } else if (p.epi == EPI_DGELU) {
           ld8_bf16(auxp + 8 * j, t);
 #pragma unroll
@@ -308,41 +308,41 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
   if (p.bias) {
 #pragma unroll
     for (int i = 0; i < 32; ++i)
-      if (i < ncols) v[i] += __bfloat162float(p.bias[col0 + i]);
+      if (i < ncols) v[i] += hx2f(p.bias[col0 + i]);
   }
   if (p.epi == EPI_BIAS_GELU) {
-    __nv_bfloat16* aux = p.aux + row * p.ld_aux + col0;
+    hx* aux = p.aux + row * p.ld_aux + col0;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       if (i < ncols) {
-        __nv_bfloat16 pre = __float2bfloat16_rn(v[i]);
+        hx pre = f2hx(v[i]);
         aux[i] = pre;
-        v[i] = gelu_f(__bfloat162float(pre));
+        v[i] = gelu_f(hx2f(pre));
       }
     }
   } else if (p.epi == EPI_DGELU) {
-    const __nv_bfloat16* aux = p.aux + row * p.ld_aux + col0;
+    const hx* aux = p.aux + row * p.ld_aux + col0;
 #pragma unroll
     for (int i = 0; i < 32; ++i)
-      if (i < ncols) v[i] *= gelu_grad_f(__bfloat162float(aux[i]));
+      if (i < ncols) v[i] *= gelu_grad_f(hx2f(aux[i]));
   }
   if (p.resid) {
-    const __nv_bfloat16* rs = p.resid + row * p.ld_resid + col0;
+    const hx* rs = p.resid + row * p.ld_resid + col0;
 #pragma unroll
     for (int i = 0; i < 32; ++i)
-      if (i < ncols) v[i] += __bfloat162float(rs[i]);
+      if (i < ncols) v[i] += hx2f(rs[i]);
   }
-  __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C) + z2 * p.c_s2 + z1 * p.c_s1 + row * p.ldc;
+  hx* C = reinterpret_cast<hx*>(p.C) + z2 * p.c_s2 + z1 * p.c_s1 + row * p.ldc;
   if (p.col_group_in == 0) {
-    __nv_bfloat16* dst = C + col0;
+    hx* dst = C + col0;
     if (ncols == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
       uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
-        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
-        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
+        hx2 h0 = f2hx2(v[8 * i + 0], v[8 * i + 1]);
+        hx2 h1 = f2hx2(v[8 * i + 2], v[8 * i + 3]);
+        hx2 h2 = f2hx2(v[8 * i + 4], v[8 * i + 5]);
+        hx2 h3 = f2hx2(v[8 * i + 6], v[8 * i + 7]);
         uint4 o;
         o.x = *reinterpret_cast<uint32_t*>(&h0);
         o.y = *reinterpret_cast<uint32_t*>(&h1);
@@ -351,13 +351,13 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
         d4[i] = o;
       }
     } else {
-      for (int i = 0; i < ncols; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+      for (int i = 0; i < ncols; ++i) dst[i] = f2hx(v[i]);
     }
   } else {
     for (int i = 0; i < ncols; ++i) {
       int c = col0 + i;
       int dc = (c / p.col_group_in) * p.col_group_out + (c % p.col_group_in);
-      C[dc] = __float2bfloat16_rn(v[i]);
+      C[dc] = f2hx(v[i]);
     }
   }
 }
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     {   // whole warp runs the loop; one elected lane issues the MMAs
-      const uint32_t idesc = umma_idesc_bf16(BM, BN, p.a_mn, p.b_mn);
+      const uint32_t idesc = umma_idesc_f16(BM, BN, p.a_mn, p.b_mn);
       const uint32_t s0 = smem_u32(smem);
       const uint64_t a_d0 = p.a_mn ? umma_desc_sw128(s0, 8192, 1024) : umma_desc_sw128(s0, 16, 1024);
       const uint64_t b_d0 = p.b_mn ? umma_desc_sw128(s0 + A_BYTES, 8192, 1024)
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              mma_bf16_ss(tmem_d, ad + k * a_k, bd + k * b_k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              mma_f16_ss(tmem_d, ad + k * a_k, bd + k * b_k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             mma_commit(&empty[stage]);
           }
           __syncwarp();
@@ -525,35 +525,35 @@ constexpr int STAGES2_TE = 5;
 constexpr int TE_BOX = 4096;                       // 32 rows x 128 B
 constexpr int TE_SMEM = EPI_WARPS * 2 * TE_BOX;    // two boxes per epilogue warp
 
-__device__ __forceinline__ void ld8_bias(const __nv_bfloat16* bias, int col, int N, float* f) {
+__device__ __forceinline__ void ld8_bias(const hx* bias, int col, int N, float* f) {
   if (col + 8 <= N) {
     uint4 u = __ldg(reinterpret_cast<const uint4*>(bias + col));
-    const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const hx2* hh = reinterpret_cast<const hx2*>(&u);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      float2 t = __bfloat1622float2(hh[i]);
+      float2 t = hx22f2(hh[i]);
       f[2 * i] = t.x;
       f[2 * i + 1] = t.y;
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) f[i] = col + i < N ? __bfloat162float(bias[col + i]) : 0.f;
+    for (int i = 0; i < 8; ++i) f[i] = col + i < N ? hx2f(bias[col + i]) : 0.f;
   }
 }
 __device__ __forceinline__ void unpack8(const uint4& u, float* f) {
-  const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+  const hx2* hh = reinterpret_cast<const hx2*>(&u);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    float2 t = __bfloat1622float2(hh[i]);
+    float2 t = hx22f2(hh[i]);
     f[2 * i] = t.x;
     f[2 * i + 1] = t.y;
   }
 }
 __device__ __forceinline__ uint4 pack8(const float* f) {
   uint4 u;
-  __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
+  hx2* hh = reinterpret_cast<hx2*>(&u);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) hh[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  for (int i = 0; i < 4; ++i) hh[i] = f2hx2(f[2 * i], f[2 * i + 1]);
   return u;
 }
 
@@ -658,7 +658,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (leader) {   // whole warp runs the loop; one elected lane issues (uniform registers)
-      const uint32_t idesc = umma_idesc_bf16(TBM, BN > 256 ? 256 : BN, p.a_mn, p.b_mn);
+      const uint32_t idesc = umma_idesc_f16(TBM, BN > 256 ? 256 : BN, p.a_mn, p.b_mn);
       // descriptors of stage 0 and the per-stage / per-k16 increments (address field = addr >> 4)
       const uint32_t s0 = smem_u32(smem);
       const uint64_t a_d0 = p.a_mn ? umma_desc_sw128(s0, 8192, 1024) : umma_desc_sw128(s0, 16, 1024);
@@ -687,7 +687,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             for (int k = 0; k < BK / 16; ++k)
 #pragma unroll
               for (int h = 0; h < NH; ++h)
-                mma_bf16_ss_pair(tmem_d + 256 * h, ad + k * a_k, bd + (uint64_t)(h * (16384 >> 4)) + k * b_k,
+                mma_f16_ss_pair(tmem_d + 256 * h, ad + k * a_k, bd + (uint64_t)(h * (16384 >> 4)) + k * b_k,
                                  idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             mma_commit_pair(&empty[stage]);
           }
@@ -747,7 +747,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
     const bool f32 = p.epi == EPI_F32;
     const bool gelu = p.epi == EPI_BIAS_GELU;
-    const bool has_in = p.epi == EPI_DGELU || (p.epi == EPI_BF16 && p.resid != nullptr);
+    const bool has_in = p.epi == EPI_DGELU || (p.epi == EPI_HALF && p.resid != nullptr);
     const int sw = lane & 7;
     uint8_t* my_row0 = box0 + lane * 128;
     uint32_t ephase = 0;
@@ -950,8 +950,8 @@ __device__ __forceinline__ void rowsoftmax_epilogue2(const GemmParams& p, uint32
     const int c_full = min(c_val, r0);          // [c_lo, c_full) are full chunks
     const bool has_diag = r0 >= c_lo && r0 < c_val;   // diagonal chunk [r0, r0+32) is mine
     const long long base = z2 * p.c_s2 + z1 * p.c_s1;
-    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + base;
-    const __nv_bfloat16* Pin = p.aux + base;
+    hx* out = reinterpret_cast<hx*>(p.C) + base;
+    const hx* Pin = p.aux + base;
     mbar_wait(tfull, it & 1);
     tc_fence_after();
     uint32_t r[32];
@@ -981,17 +981,17 @@ __device__ __forceinline__ void rowsoftmax_epilogue2(const GemmParams& p, uint32
     };
     auto put8 = [&](int j, const float* v8) {
       uint4 u;
-      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+      hx2* h2 = reinterpret_cast<hx2*>(&u);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(v8[2 * i], v8[2 * i + 1]);
+      for (int i = 0; i < 4; ++i) h2[i] = f2hx2(v8[2 * i], v8[2 * i + 1]);
       stg[lane * 8 + (j ^ (lane & 7))] = u;
     };
     auto get8 = [&](int j, float* v8) {
       uint4 u = stg[lane * 8 + (j ^ (lane & 7))];
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const hx2* h2 = reinterpret_cast<const hx2*>(&u);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        float2 f = __bfloat1622float2(h2[i]);
+        float2 f = hx22f2(h2[i]);
         v8[2 * i] = f.x;
         v8[2 * i + 1] = f.y;
       }
@@ -1144,8 +1144,8 @@ __device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_
     const int kv = min(p.N, m0 + BM);
     const int row = m0 + rl;
     const long long base = z2 * p.c_s2 + z1 * p.c_s1;
-    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + base;
-    const __nv_bfloat16* Pin = p.aux + base;
+    hx* out = reinterpret_cast<hx*>(p.C) + base;
+    const hx* Pin = p.aux + base;
     const int c_lo = half * 256;
     const int c_hi = min(kv, c_lo + 256);                    // my columns holding scores
     const int c_end = min(p.N, c_lo + 256);                  // my columns to write
@@ -1179,17 +1179,17 @@ __device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_
     };
     auto put_row = [&](int j, const float* v8) {   // this thread's row, 16-byte chunk j
       uint4 u;
-      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+      hx2* h2 = reinterpret_cast<hx2*>(&u);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(v8[2 * i], v8[2 * i + 1]);
+      for (int i = 0; i < 4; ++i) h2[i] = f2hx2(v8[2 * i], v8[2 * i + 1]);
       stg[lane * 8 + (j ^ (lane & 7))] = u;
     };
     auto get_row = [&](int j, float* v8) {
       uint4 u = stg[lane * 8 + (j ^ (lane & 7))];
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const hx2* h2 = reinterpret_cast<const hx2*>(&u);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        float2 f = __bfloat1622float2(h2[i]);
+        float2 f = hx22f2(h2[i]);
         v8[2 * i] = f.x;
         v8[2 * i + 1] = f.y;
       }
@@ -1356,7 +1356,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
     }
   } else if (warp == 1) {
     {   // whole warp; elected lane issues
-      const uint32_t idesc = umma_idesc_bf16(BM, 256, 0, 0);
+      const uint32_t idesc = umma_idesc_f16(BM, 256, 0, 0);
       const uint64_t d0 = umma_desc_sw128(smem_u32(smem), 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
@@ -1376,7 +1376,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
             for (int k = 0; k < BK / 16; ++k) {
               for (int hh = 0; hh < nh; ++hh) {
                 const uint64_t bd = ad + (uint64_t)((A_BYTES + hh * HALF_BYTES) >> 4);
-                mma_bf16_ss(tmem_base + 256 * hh, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                mma_f16_ss(tmem_base + 256 * hh, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
               }
             }
             mma_commit(&empty[stage]);
@@ -1403,8 +1403,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
       const int row = m0 + q * 32 + lane;
       const bool live = row < p.M;
       const long long off = z2 * p.c_s2 + z1 * p.c_s1 + (long long)row * p.ldc;
-      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + off;
-      const __nv_bfloat16* Pin = p.aux + off;
+      hx* out = reinterpret_cast<hx*>(p.C) + off;
+      const hx* Pin = p.aux + off;
       mbar_wait(tfull, it & 1);
       tc_fence_after();
       uint32_t r[32];
@@ -1439,10 +1439,10 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
             uint4* d4 = reinterpret_cast<uint4*>(out + c0);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
-              __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
-              __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
+              hx2 h0 = f2hx2(v[8 * i + 0], v[8 * i + 1]);
+              hx2 h1 = f2hx2(v[8 * i + 2], v[8 * i + 3]);
+              hx2 h2 = f2hx2(v[8 * i + 4], v[8 * i + 5]);
+              hx2 h3 = f2hx2(v[8 * i + 6], v[8 * i + 7]);
               uint4 o;
               o.x = *reinterpret_cast<uint32_t*>(&h0);
               o.y = *reinterpret_cast<uint32_t*>(&h1);
@@ -1460,10 +1460,10 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; i += 8) {
               uint4 pv = *reinterpret_cast<const uint4*>(Pin + c0 + i);
-              const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&pv);
+              const hx2* ph = reinterpret_cast<const hx2*>(&pv);
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                float2 pf = __bfloat1622float2(ph[j]);
+                float2 pf = hx22f2(ph[j]);
                 if (c0 + i + 2 * j <= row) dot += pf.x * __uint_as_float(r[i + 2 * j]);
                 if (c0 + i + 2 * j + 1 <= row) dot += pf.y * __uint_as_float(r[i + 2 * j + 1]);
               }
@@ -1478,10 +1478,10 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
 #pragma unroll
               for (int i = 0; i < 32; i += 8) {
                 uint4 pv = *reinterpret_cast<const uint4*>(Pin + c0 + i);
-                const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&pv);
+                const hx2* ph = reinterpret_cast<const hx2*>(&pv);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  float2 pf = __bfloat1622float2(ph[j]);
+                  float2 pf = hx22f2(ph[j]);
                   v[i + 2 * j] = (c0 + i + 2 * j <= row)
                                      ? p.alpha * pf.x * (__uint_as_float(r[i + 2 * j]) - dot) : 0.f;
                   v[i + 2 * j + 1] = (c0 + i + 2 * j + 1 <= row)
@@ -1497,10 +1497,10 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
             uint4* d4 = reinterpret_cast<uint4*>(out + c0);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
-              __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
-              __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
+              hx2 h0 = f2hx2(v[8 * i + 0], v[8 * i + 1]);
+              hx2 h1 = f2hx2(v[8 * i + 2], v[8 * i + 3]);
+              hx2 h2 = f2hx2(v[8 * i + 4], v[8 * i + 5]);
+              hx2 h3 = f2hx2(v[8 * i + 6], v[8 * i + 7]);
               uint4 o;
               o.x = *reinterpret_cast<uint32_t*>(&h0);
               o.y = *reinterpret_cast<uint32_t*>(&h1);
@@ -1558,7 +1558,7 @@ static int make_map(CUtensorMap* map, const void* base, long long inner, long lo
   cuuint64_t strides[3] = {(cuuint64_t)(ld * 2), (cuuint64_t)(st1 * 2), (cuuint64_t)(st2 * 2)};
   cuuint32_t box[4] = {64, (cuuint32_t)box_outer, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
+  CUresult r = enc(map, AXONN_TMA_HALF, 4, const_cast<void*>(base), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -3;
@@ -1580,10 +1580,10 @@ static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
   p.col_group_in = g.col_group_in; p.col_group_out = g.col_group_out;
   p.n_valid = g.n_valid > 0 ? g.n_valid : g.N;
   p.C = g.C; p.ldc = g.ldc; p.c_s1 = g.c_s1; p.c_s2 = g.c_s2;
-  p.bias = reinterpret_cast<const __nv_bfloat16*>(g.bias);
-  p.resid = reinterpret_cast<const __nv_bfloat16*>(g.resid);
+  p.bias = reinterpret_cast<const hx*>(g.bias);
+  p.resid = reinterpret_cast<const hx*>(g.resid);
   p.ld_resid = g.ld_resid;
-  p.aux = reinterpret_cast<__nv_bfloat16*>(g.aux);
+  p.aux = reinterpret_cast<hx*>(g.aux);
   p.ld_aux = g.ld_aux;
   p.alpha = g.alpha;
   p.num_m = (g.M + tbm - 1) / tbm;
@@ -1668,7 +1668,7 @@ static int make_map_epi(CUtensorMap* map, const void* base, long long cols, long
   cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
   cuuint32_t box[2] = {(cuuint32_t)(128 / es), 32};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : AXONN_TMA_HALF, 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1684,11 +1684,11 @@ static bool al16h(const void* p, long long ld, int es) {
 static bool te_eligible(const GemmArgs& g) {
   if (g.Z != 1 || g.col_group_in != 0 || (g.n_valid > 0 && g.n_valid < g.N)) return false;
   if (g.epi == EPI_F32) return al16h(g.C, g.ldc, 4);
-  if (g.epi != EPI_BF16 && g.epi != EPI_BIAS_GELU && g.epi != EPI_DGELU) return false;
+  if (g.epi != EPI_HALF && g.epi != EPI_BIAS_GELU && g.epi != EPI_DGELU) return false;
   if (!al16h(g.C, g.ldc, 2)) return false;
   if (g.bias && (reinterpret_cast<uintptr_t>(g.bias) & 15)) return false;
   if ((g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) && !al16h(g.aux, g.ld_aux, 2)) return false;
-  if (g.epi == EPI_BF16 && g.resid && !al16h(g.resid, g.ld_resid, 2)) return false;
+  if (g.epi == EPI_HALF && g.resid && !al16h(g.resid, g.ld_resid, 2)) return false;
   if ((g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) && g.resid) return false;
   return true;
 }
@@ -1842,7 +1842,7 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   }
   // 256 x 512 pair tiles: epilogues without a tile-sized input (two staging boxes per warp)
   if (g_te_mode && te_eligible(g) && (g.variant == 4 || (g.variant == 0 && g_bn512)) &&
-      g.N >= 2048 && !(g.epi == EPI_DGELU || (g.epi == EPI_BF16 && g.resid)))
+      g.N >= 2048 && !(g.epi == EPI_DGELU || (g.epi == EPI_HALF && g.resid)))
     return launch_pair<512, true>(g, st);
   if (g_te_mode && g.variant != 3 && te_eligible(g)) return launch_pair<256, true>(g, st);
   return launch_pair<256, false>(g, st);

@@ -4,10 +4,12 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include "half.cuh"
+
 namespace axonn {
 
 enum Epi {
-  EPI_BF16 = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3,
+  EPI_HALF = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3,
   EPI_SOFTMAX = 4,       // causal row softmax of alpha * acc -> bf16 P (N <= 512, full rows per tile)
   EPI_SOFTMAX_BWD = 5    // dS = alpha * P * (acc - rowsum(P * acc)), P read from aux
 };
@@ -78,8 +80,10 @@ int softmax_bwd(const void* P, const float* dP, long long nrows, int s, float sc
 int xent(void* z, const int32_t* labels, long long lab_ld, int rows, int s, int V, float coef,
          float* row_loss, cudaStream_t st);
 int reduce_sum(const float* x, int n, float scale, double* out, cudaStream_t st);
-int cast_f32_bf16(const float* in, void* out, long long n, cudaStream_t st);
-int cast_bf16_f32(const void* in, float* out, long long n, cudaStream_t st);
+int cast_f32_hx(const float* in, void* out, long long n, cudaStream_t st);
+// flag = 1 if any of the n 16-bit values is inf / NaN (flag is not cleared)
+int nonfinite_scan(const void* x, long long n, int* flag, cudaStream_t st);
+int cast_hx_f32(const void* in, float* out, long long n, cudaStream_t st);
 int init_normal(void* out, float* master, long long n, uint64_t seed, float mean, float stdv,
                 cudaStream_t st);
 

@@ -108,7 +108,7 @@ static GemmArgs lin_fwd(const void* X, const void* W, int M, int N, int K, void*
   g.A = X; g.lda = K;
   g.B = W; g.ldb = K;
   g.C = out; g.ldc = N;
-  g.epi = EPI_BF16;
+  g.epi = EPI_HALF;
   return g;
 }
 // dX[M, Kin] = dY[M, Nout] W[Nout, Kin]
@@ -119,7 +119,7 @@ static GemmArgs lin_dgrad(const void* dY, const void* W, int M, int Nout, int Ki
   g.A = dY; g.lda = Nout;
   g.B = W; g.ldb = Kin; g.b_mn = 1;
   g.C = dX; g.ldc = Kin;
-  g.epi = EPI_BF16;
+  g.epi = EPI_HALF;
   return g;
 }
 // dW[Nout, Kin] (+)= dY^T X
@@ -188,7 +188,7 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
       g.B = static_cast<char*>(st.qkv) + (size_t)2 * heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
       g.b_s2 = (long long)s * lq; g.b_mn = 1;
       g.C = st.o; g.ldc = h; g.c_s1 = d; g.c_s2 = (long long)s * h;
-      g.epi = EPI_BF16; g.causal = 2;
+      g.epi = EPI_HALF; g.causal = 2;
       TRY(gemm(g, -1));
     }
   }
@@ -293,7 +293,7 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
       g.B = static_cast<char*>(st.qkv) + (size_t)heads * dp * 2; g.ldb = lq; g.b_s1 = dp;
       g.b_s2 = (long long)s * lq; g.b_mn = 1;
       g.C = dqkv; g.ldc = 3 * h; g.c_s1 = d; g.c_s2 = (long long)s * 3 * h;
-      g.epi = EPI_BF16; g.causal = 2;
+      g.epi = EPI_HALF; g.causal = 2;
       TRY(gemm(g, -1));
     }
     {  // dK = dS^T Q -> dqkv[:, h:2h]
@@ -304,7 +304,7 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
       g.B = st.qkv; g.ldb = lq; g.b_s1 = dp; g.b_s2 = (long long)s * lq; g.b_mn = 1;
       g.C = static_cast<char*>(dqkv) + (size_t)h * 2; g.ldc = 3 * h; g.c_s1 = d;
       g.c_s2 = (long long)s * 3 * h;
-      g.epi = EPI_BF16; g.causal = 3;
+      g.epi = EPI_HALF; g.causal = 3;
       TRY(gemm(g, -1));
     }
     {  // dV = P^T dO -> dqkv[:, 2h:3h]
@@ -316,7 +316,7 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
       g.b_mn = 1;
       g.C = static_cast<char*>(dqkv) + (size_t)2 * h * 2; g.ldc = 3 * h; g.c_s1 = d;
       g.c_s2 = (long long)s * 3 * h;
-      g.epi = EPI_BF16; g.causal = 3;
+      g.epi = EPI_HALF; g.causal = 3;
       TRY(gemm(g, -1));
     }
   }

@@ -9,7 +9,7 @@
 // biased variance, D-7 scale 1/sqrt(d), D-8 causal mask, D-9 loss
 // normalisation.
 #include <cuda_runtime.h>
-#include <cuda_bf16.h>
+#include "half.cuh"
 #include <cstdint>
 #include <cfloat>
 
@@ -28,21 +28,21 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
+__device__ __forceinline__ void load8(const hx* p, float (&f)[8]) {
   uint4 u = *reinterpret_cast<const uint4*>(p);
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+  const hx2* h = reinterpret_cast<const hx2*>(&u);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    float2 t = __bfloat1622float2(h[i]);
+    float2 t = hx22f2(h[i]);
     f[2 * i] = t.x;
     f[2 * i + 1] = t.y;
   }
 }
-__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
+__device__ __forceinline__ void store8(hx* p, const float (&f)[8]) {
   uint4 u;
-  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+  hx2* h = reinterpret_cast<hx2*>(&u);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  for (int i = 0; i < 4; ++i) h[i] = f2hx2(f[2 * i], f[2 * i + 1]);
   *reinterpret_cast<uint4*>(p) = u;
 }
 
@@ -60,18 +60,18 @@ static inline int ok() { return cudaGetLastError() == cudaSuccess ? 0 : -11; }
 // ------------------------------------------------------------------ embedding
 // x0[t] = E_tok[tok[t]] + E_pos[t % s]   (D-1: learned token + position embeddings)
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, long long tok_ld, int s, int rows,
-                                 int h, const __nv_bfloat16* __restrict__ etok,
-                                 const __nv_bfloat16* __restrict__ epos,
-                                 __nv_bfloat16* __restrict__ out) {
+                                 int h, const hx* __restrict__ etok,
+                                 const hx* __restrict__ epos,
+                                 hx* __restrict__ out) {
   const int warps = blockDim.x / 32;
   const int row = blockIdx.x * warps + threadIdx.x / 32;
   if (row >= rows) return;
   const int lane = threadIdx.x % 32;
   const int b = row / s, t = row % s;
   const int id = tok[b * tok_ld + t];
-  const __nv_bfloat16* e = etok + (long long)id * h;
-  const __nv_bfloat16* p = epos + (long long)t * h;
-  __nv_bfloat16* o = out + (long long)row * h;
+  const hx* e = etok + (long long)id * h;
+  const hx* p = epos + (long long)t * h;
+  hx* o = out + (long long)row * h;
   for (int c = lane * 8; c < h; c += 256) {
     float a[8], bb[8];
     load8(e + c, a);
@@ -86,8 +86,8 @@ int embed_fwd(const int32_t* tok, long long tok_ld, int b, int s, int h, const v
               const void* epos, void* out, cudaStream_t st) {
   int rows = b * s;
   embed_fwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>(
-      tok, tok_ld, s, rows, h, (const __nv_bfloat16*)etok, (const __nv_bfloat16*)epos,
-      (__nv_bfloat16*)out);
+      tok, tok_ld, s, rows, h, (const hx*)etok, (const hx*)epos,
+      (hx*)out);
   return ok();
 }
 
@@ -96,7 +96,7 @@ int embed_fwd(const int32_t* tok, long long tok_ld, int b, int s, int h, const v
 // atomics, no sort).  dE_pos[t] += sum_b dx[b, t] (fixed b order).
 constexpr int EMB_VROWS = 32;
 __global__ void embed_bwd_tok_kernel(const int32_t* __restrict__ tok, long long tok_ld, int b, int s,
-                                     int h, int vocab, const __nv_bfloat16* __restrict__ dx,
+                                     int h, int vocab, const hx* __restrict__ dx,
                                      float* __restrict__ detok) {
   const int v0 = blockIdx.x * EMB_VROWS;
   const int ncol_chunks = h / 8;
@@ -154,7 +154,7 @@ __global__ void embed_bwd_tok_kernel(const int32_t* __restrict__ tok, long long 
   }
 }
 
-__global__ void embed_bwd_pos_kernel(int b, int s, int h, const __nv_bfloat16* __restrict__ dx,
+__global__ void embed_bwd_pos_kernel(int b, int s, int h, const hx* __restrict__ dx,
                                      float* __restrict__ dpos) {
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;   // over s*h/2 pairs
   long long n = (long long)s * h / 2;
@@ -163,8 +163,8 @@ __global__ void embed_bwd_pos_kernel(int b, int s, int h, const __nv_bfloat16* _
   int c = (int)(idx % (h / 2)) * 2;
   float a = 0.f, bsum = 0.f;
   for (int bi = 0; bi < b; ++bi) {
-    float2 v = __bfloat1622float2(
-        *reinterpret_cast<const __nv_bfloat162*>(dx + ((long long)bi * s + t) * h + c));
+    float2 v = hx22f2(
+        *reinterpret_cast<const hx2*>(dx + ((long long)bi * s + t) * h + c));
     a += v.x;
     bsum += v.y;
   }
@@ -179,23 +179,23 @@ int embed_bwd(const int32_t* tok, long long tok_ld, int b, int s, int h, int voc
               float* detok, float* dpos, cudaStream_t st) {
   int blocks = (vocab + EMB_VROWS - 1) / EMB_VROWS;
   embed_bwd_tok_kernel<<<blocks, 256, 0, st>>>(tok, tok_ld, b, s, h, vocab,
-                                               (const __nv_bfloat16*)dx, detok);
+                                               (const hx*)dx, detok);
   long long pairs = (long long)s * h / 2;
   embed_bwd_pos_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(
-      b, s, h, (const __nv_bfloat16*)dx, dpos);
+      b, s, h, (const hx*)dx, dpos);
   return ok();
 }
 
 // ------------------------------------------------------------------ LayerNorm
 // y = (x - mean) * rstd * g + b, two-pass statistics in fp32 (D-6).  Warp per row.
-__global__ void ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int rows, int h,
-                              const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ bta,
-                              __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+__global__ void ln_fwd_kernel(const hx* __restrict__ x, int rows, int h,
+                              const hx* __restrict__ g, const hx* __restrict__ bta,
+                              hx* __restrict__ y, float* __restrict__ mean_out,
                               float* __restrict__ rstd_out) {
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (row >= rows) return;
   const int lane = threadIdx.x % 32;
-  const __nv_bfloat16* xr = x + (long long)row * h;
+  const hx* xr = x + (long long)row * h;
   float s = 0.f;
   for (int c = lane * 8; c < h; c += 256) {
     float f[8];
@@ -215,7 +215,7 @@ __global__ void ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int rows, int
     }
   }
   const float rstd = rsqrtf(warp_sum(v) / h + 1e-5f);
-  __nv_bfloat16* yr = y + (long long)row * h;
+  hx* yr = y + (long long)row * h;
   for (int c = lane * 8; c < h; c += 256) {
     float f[8], gg[8], bb[8];
     load8(xr + c, f);
@@ -233,23 +233,23 @@ __global__ void ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int rows, int
 
 int ln_fwd(const void* x, int rows, int h, const void* g, const void* b, void* y, float* mean,
            float* rstd, cudaStream_t st) {
-  ln_fwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)x, rows, h,
-                                                (const __nv_bfloat16*)g, (const __nv_bfloat16*)b,
-                                                (__nv_bfloat16*)y, mean, rstd);
+  ln_fwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>((const hx*)x, rows, h,
+                                                (const hx*)g, (const hx*)b,
+                                                (hx*)y, mean, rstd);
   return ok();
 }
 
 // dx = dres + rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)),  dxhat = dy * g
-__global__ void ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+__global__ void ln_bwd_kernel(const hx* __restrict__ dy, const hx* __restrict__ x,
                               const float* __restrict__ mean, const float* __restrict__ rstd, int rows,
-                              int h, const __nv_bfloat16* __restrict__ g,
-                              const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx) {
+                              int h, const hx* __restrict__ g,
+                              const hx* __restrict__ dres, hx* __restrict__ dx) {
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (row >= rows) return;
   const int lane = threadIdx.x % 32;
   const float mu = mean[row], rs = rstd[row];
-  const __nv_bfloat16* xr = x + (long long)row * h;
-  const __nv_bfloat16* dyr = dy + (long long)row * h;
+  const hx* xr = x + (long long)row * h;
+  const hx* dyr = dy + (long long)row * h;
   float s1 = 0.f, s2 = 0.f;
   for (int c = lane * 8; c < h; c += 256) {
     float xf[8], df[8], gf[8];
@@ -266,8 +266,8 @@ __global__ void ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_b
   }
   s1 = warp_sum(s1) / h;
   s2 = warp_sum(s2) / h;
-  __nv_bfloat16* o = dx + (long long)row * h;
-  const __nv_bfloat16* rr = dres ? dres + (long long)row * h : nullptr;
+  hx* o = dx + (long long)row * h;
+  const hx* rr = dres ? dres + (long long)row * h : nullptr;
   for (int c = lane * 8; c < h; c += 256) {
     float xf[8], df[8], gf[8], rf[8];
     load8(xr + c, xf);
@@ -287,8 +287,8 @@ __global__ void ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_b
 int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int h,
            const void* g, const void* dres, void* dx, cudaStream_t st) {
   ln_bwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean, rstd, rows, h,
-      (const __nv_bfloat16*)g, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx);
+      (const hx*)dy, (const hx*)x, mean, rstd, rows, h,
+      (const hx*)g, (const hx*)dres, (hx*)dx);
   return ok();
 }
 
@@ -297,7 +297,7 @@ int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, 
 //          part_g[r][c] = sum dy * xhat  (xhat from x, mean, rstd) when x != null.
 // Block = 256 threads = 8 row lanes x 32 column-pair lanes -> 64 columns.
 constexpr int CR_ROWCHUNK = 128;
-__global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+__global__ void colsum_partial_kernel(const hx* __restrict__ dy, const hx* __restrict__ x,
                                       const float* __restrict__ mean, const float* __restrict__ rstd,
                                       int rows, int n, float* __restrict__ part_b,
                                       float* __restrict__ part_g) {
@@ -308,11 +308,11 @@ __global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ dy, cons
   float sb0 = 0.f, sb1 = 0.f, sg0 = 0.f, sg1 = 0.f;
   if (c < n) {
     for (int r = r0 + rl; r < r1; r += 8) {
-      float2 d = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy + (long long)r * n + c));
+      float2 d = hx22f2(*reinterpret_cast<const hx2*>(dy + (long long)r * n + c));
       sb0 += d.x;
       sb1 += d.y;
       if (x) {
-        float2 xv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + (long long)r * n + c));
+        float2 xv = hx22f2(*reinterpret_cast<const hx2*>(x + (long long)r * n + c));
         float mu = mean[r], rs = rstd[r];
         sg0 += d.x * ((xv.x - mu) * rs);
         sg1 += d.y * ((xv.y - mu) * rs);
@@ -352,8 +352,8 @@ int colsum_chunks(int rows) { return (rows + CR_ROWCHUNK - 1) / CR_ROWCHUNK; }
 // Single-pass column sums: a block owns 32 columns (4 groups of 8, 16-byte loads) and all
 // rows, split over 64 row lanes; partials are combined in shared memory in a fixed order
 // (bitwise reproducible).  out_b[c] (+)= sum_r dy[r][c];  out_g[c] (+)= sum_r dy * xhat.
-__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ dy,
-                                                     const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(256) colsum_kernel(const hx* __restrict__ dy,
+                                                     const hx* __restrict__ x,
                                                      const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, int rows,
                                                      int n, float* __restrict__ out_b,
@@ -424,8 +424,8 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
 // adds the partials in ascending row-chunk order -> one launch, bitwise reproducible.
 // workspace: [0, 4 KB) zero-initialised tickets, then 2 x R x n fp32 partials.
 constexpr int CS2_ROWS = 256;
-__global__ void __launch_bounds__(256) colsum2_kernel(const __nv_bfloat16* __restrict__ dy,
-                                                      const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(256) colsum2_kernel(const hx* __restrict__ dy,
+                                                      const hx* __restrict__ x,
                                                       const float* __restrict__ mean,
                                                       const float* __restrict__ rstd, int rows,
                                                       int n, float* __restrict__ part,
@@ -524,7 +524,7 @@ int colsum(const void* dy, const void* x, const float* mean, const float* rstd, 
     dim3 grid((n + 63) / 64, (rows + CS2_ROWS - 1) / CS2_ROWS);
     unsigned* ticket = reinterpret_cast<unsigned*>(workspace);
     float* part = workspace + 1024;
-    colsum2_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean,
+    colsum2_kernel<<<grid, 256, 0, st>>>((const hx*)dy, (const hx*)x, mean,
                                          rstd, rows, n, part, ticket, out_b, out_g, accumulate);
     return ok();
   }
@@ -532,7 +532,7 @@ int colsum(const void* dy, const void* x, const float* mean, const float* rstd, 
   float* part_b = workspace + 1024;
   float* part_g = part_b + (long long)nch * n;
   dim3 grid((n + 63) / 64, nch);
-  colsum_partial_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+  colsum_partial_kernel<<<grid, 256, 0, st>>>((const hx*)dy, (const hx*)x,
                                               mean, rstd, rows, n, part_b, part_g);
   colsum_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(part_b, nch, n, out_b, accumulate);
   if (x) colsum_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(part_g, nch, n, out_g, accumulate);
@@ -543,7 +543,7 @@ int colsum(const void* dy, const void* x, const float* mean, const float* rstd, 
 // Row q of S (fp32, already scaled by 1/sqrt(d)): P[q, k] = exp(S - max) / sum for
 // k <= q, 0 for k > q (D-8).  One warp per row; rows of length s.
 __global__ void softmax_fwd_kernel(const float* __restrict__ S, long long nrows, int s,
-                                   __nv_bfloat16* __restrict__ P) {
+                                   hx* __restrict__ P) {
   const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (row >= nrows) return;
   const int lane = threadIdx.x % 32;
@@ -556,46 +556,46 @@ __global__ void softmax_fwd_kernel(const float* __restrict__ S, long long nrows,
   for (int k = lane; k <= q; k += 32) sum += __expf(sr[k] - mx);
   sum = warp_sum(sum);
   const float inv = 1.f / sum;
-  __nv_bfloat16* pr = P + row * s;
+  hx* pr = P + row * s;
   for (int k = lane * 2; k < s; k += 64) {
     float a = k <= q ? __expf(sr[k] - mx) * inv : 0.f;
     float b = k + 1 <= q ? __expf(sr[k + 1] - mx) * inv : 0.f;
-    *reinterpret_cast<__nv_bfloat162*>(pr + k) = __floats2bfloat162_rn(a, b);
+    *reinterpret_cast<hx2*>(pr + k) = f2hx2(a, b);
   }
 }
 
 int softmax_fwd(const float* S, long long nrows, int s, void* P, cudaStream_t st) {
   unsigned blocks = (unsigned)((nrows + 7) / 8);
-  softmax_fwd_kernel<<<blocks, 256, 0, st>>>(S, nrows, s, (__nv_bfloat16*)P);
+  softmax_fwd_kernel<<<blocks, 256, 0, st>>>(S, nrows, s, (hx*)P);
   return ok();
 }
 
 // dS[q, k] = scale * P[q, k] * (dP[q, k] - sum_k' P[q, k'] dP[q, k']), zero for k > q.
-__global__ void softmax_bwd_kernel(const __nv_bfloat16* __restrict__ P, const float* __restrict__ dP,
+__global__ void softmax_bwd_kernel(const hx* __restrict__ P, const float* __restrict__ dP,
                                    long long nrows, int s, float scale,
-                                   __nv_bfloat16* __restrict__ dS) {
+                                   hx* __restrict__ dS) {
   const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (row >= nrows) return;
   const int lane = threadIdx.x % 32;
   const int q = (int)(row % s);
-  const __nv_bfloat16* pr = P + row * s;
+  const hx* pr = P + row * s;
   const float* dr = dP + row * s;
   float dot = 0.f;
-  for (int k = lane; k <= q; k += 32) dot += __bfloat162float(pr[k]) * dr[k];
+  for (int k = lane; k <= q; k += 32) dot += hx2f(pr[k]) * dr[k];
   dot = warp_sum(dot);
-  __nv_bfloat16* o = dS + row * s;
+  hx* o = dS + row * s;
   for (int k = lane * 2; k < s; k += 64) {
-    float a = k <= q ? scale * __bfloat162float(pr[k]) * (dr[k] - dot) : 0.f;
-    float b = k + 1 <= q ? scale * __bfloat162float(pr[k + 1]) * (dr[k + 1] - dot) : 0.f;
-    *reinterpret_cast<__nv_bfloat162*>(o + k) = __floats2bfloat162_rn(a, b);
+    float a = k <= q ? scale * hx2f(pr[k]) * (dr[k] - dot) : 0.f;
+    float b = k + 1 <= q ? scale * hx2f(pr[k + 1]) * (dr[k + 1] - dot) : 0.f;
+    *reinterpret_cast<hx2*>(o + k) = f2hx2(a, b);
   }
 }
 
 int softmax_bwd(const void* P, const float* dP, long long nrows, int s, float scale, void* dS,
                 cudaStream_t st) {
   unsigned blocks = (unsigned)((nrows + 7) / 8);
-  softmax_bwd_kernel<<<blocks, 256, 0, st>>>((const __nv_bfloat16*)P, dP, nrows, s, scale,
-                                             (__nv_bfloat16*)dS);
+  softmax_bwd_kernel<<<blocks, 256, 0, st>>>((const hx*)P, dP, nrows, s, scale,
+                                             (hx*)dS);
   return ok();
 }
 
@@ -603,10 +603,10 @@ int softmax_bwd(const void* P, const float* dP, long long nrows, int s, float sc
 // Per row of logits z [V] (bf16): lse = log sum exp z; ce = lse - z_y;
 // dz = coef * (softmax(z) - onehot(y)) written in place (bf16);
 // row_loss[row] = ce (fp32, unscaled).  coef = S / (M_total * tokens_in_microbatch) (D-9).
-__global__ void xent_kernel(__nv_bfloat16* __restrict__ z, const int32_t* __restrict__ labels,
+__global__ void xent_kernel(hx* __restrict__ z, const int32_t* __restrict__ labels,
                             long long lab_ld, int s, int V, float coef, float* __restrict__ row_loss) {
   const int row = blockIdx.x;
-  __nv_bfloat16* zr = z + (long long)row * V;
+  hx* zr = z + (long long)row * V;
   const int y = labels[(row / s) * lab_ld + (row % s)];
   float mx = -FLT_MAX, sum = 0.f;
   for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
@@ -636,7 +636,7 @@ __global__ void xent_kernel(__nv_bfloat16* __restrict__ z, const int32_t* __rest
   float gs = 0.f;
   for (int w = 0; w < nw; ++w) gs += ssum[w] * __expf(smx[w] - gm);
   const float lse = logf(gs) + gm;
-  const float zy = __bfloat162float(zr[y]);
+  const float zy = hx2f(zr[y]);
   __syncthreads();
   for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
     float f[8];
@@ -654,7 +654,7 @@ __global__ void xent_kernel(__nv_bfloat16* __restrict__ z, const int32_t* __rest
 int xent(void* z, const int32_t* labels, long long lab_ld, int rows, int s, int V, float coef,
          float* row_loss, cudaStream_t st) {
   if (V % 8) return -2;
-  xent_kernel<<<rows, 512, 0, st>>>((__nv_bfloat16*)z, labels, lab_ld, s, V, coef, row_loss);
+  xent_kernel<<<rows, 512, 0, st>>>((hx*)z, labels, lab_ld, s, V, coef, row_loss);
   return ok();
 }
 
@@ -679,40 +679,73 @@ int reduce_sum(const float* x, int n, float scale, double* out, cudaStream_t st)
 }
 
 // ------------------------------------------------------------------ casts
-__global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+__global__ void cast_f32_hx_kernel(const float* __restrict__ in, hx* __restrict__ out,
                                      long long n) {
   long long nv = n / 4;
   long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
     float4 v = reinterpret_cast<const float4*>(in)[i];
-    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    hx2 a = f2hx2(v.x, v.y), b = f2hx2(v.z, v.w);
     uint2 u;
     u.x = *reinterpret_cast<uint32_t*>(&a);
     u.y = *reinterpret_cast<uint32_t*>(&b);
     reinterpret_cast<uint2*>(out)[i] = u;
   }
   for (long long i = nv * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = __float2bfloat16_rn(in[i]);
+    out[i] = f2hx(in[i]);
 }
 
-int cast_f32_bf16(const float* in, void* out, long long n, cudaStream_t st) {
+// Overflow test of loss-scaled mixed precision (reading D-12): flag = 1 if any of the n
+// 16-bit values is inf or NaN (exponent field all ones).  HBM-bound: 16-B loads, grid-stride,
+// one block-wide vote per iteration and a plain store of 1 (every writer writes the same value).
+__device__ __forceinline__ bool nonfinite2(uint32_t u) {
+  constexpr uint32_t M = kHalfExpMask;
+  return (u & M) == M || ((u >> 16) & M) == M;
+}
+__global__ void __launch_bounds__(256) nonfinite_kernel(const hx* __restrict__ x, long long n,
+                                                        int* __restrict__ flag) {
+  const long long nv = n / 8;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    uint4 u = __ldcs(reinterpret_cast<const uint4*>(x) + i);
+    bad |= nonfinite2(u.x) | nonfinite2(u.y) | nonfinite2(u.z) | nonfinite2(u.w);
+  }
+  for (long long i = nv * 8 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint16_t b = reinterpret_cast<const uint16_t*>(x)[i];
+    bad |= (b & kHalfExpMask) == kHalfExpMask;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+int nonfinite_scan(const void* x, long long n, int* flag, cudaStream_t st) {
+  if (n <= 0) return 0;
+  long long blocks = (n / 8 + 255) / 256;
+  long long cap = (long long)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  nonfinite_kernel<<<(unsigned)blocks, 256, 0, st>>>((const hx*)x, n, flag);
+  return ok();
+}
+
+int cast_f32_hx(const float* in, void* out, long long n, cudaStream_t st) {
   if (n <= 0) return 0;
   long long blocks = (n / 4 + 255) / 256;
   long long cap = (long long)num_sms() * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  cast_f32_bf16_kernel<<<(unsigned)blocks, 256, 0, st>>>(in, (__nv_bfloat16*)out, n);
+  cast_f32_hx_kernel<<<(unsigned)blocks, 256, 0, st>>>(in, (hx*)out, n);
   return ok();
 }
 
-__global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ in, float* __restrict__ out,
+__global__ void cast_hx_f32_kernel(const hx* __restrict__ in, float* __restrict__ out,
                                      long long n) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = __bfloat162float(in[i]);
+  if (i < n) out[i] = hx2f(in[i]);
 }
-int cast_bf16_f32(const void* in, float* out, long long n, cudaStream_t st) {
+int cast_hx_f32(const void* in, float* out, long long n, cudaStream_t st) {
   if (n <= 0) return 0;
-  cast_bf16_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((const __nv_bfloat16*)in, out, n);
+  cast_hx_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((const hx*)in, out, n);
   return ok();
 }
 
@@ -724,7 +757,7 @@ __device__ __forceinline__ uint64_t smix(uint64_t z) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
-__global__ void init_normal_kernel(__nv_bfloat16* __restrict__ out, float* __restrict__ master,
+__global__ void init_normal_kernel(hx* __restrict__ out, float* __restrict__ master,
                                    long long n, uint64_t seed, float mean, float stdv) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -732,15 +765,18 @@ __global__ void init_normal_kernel(__nv_bfloat16* __restrict__ out, float* __res
   float u1 = ((a >> 40) + 1) * (1.0f / 16777217.0f), u2 = (b >> 40) * (1.0f / 16777216.0f);
   float z = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
   float v = mean + stdv * z;
-  uint32_t bits = __float_as_uint(v) & 0xFFFF0000u;
-  float tv = __uint_as_float(bits);
-  out[i] = __float2bfloat16_rn(tv);
+#ifdef AXONN_HALF_FP16
+  float tv = hx2f(f2hx(v));                                // fp16-representable (RNE)
+#else
+  float tv = __uint_as_float(__float_as_uint(v) & 0xFFFF0000u);   // bf16 by truncation
+#endif
+  out[i] = f2hx(tv);
   if (master) master[i] = tv;
 }
 int init_normal(void* out, float* master, long long n, uint64_t seed, float mean, float stdv,
                 cudaStream_t st) {
   if (n <= 0) return 0;
-  init_normal_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((__nv_bfloat16*)out, master, n,
+  init_normal_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((hx*)out, master, n,
                                                                   seed, mean, stdv);
   return ok();
 }
@@ -759,8 +795,8 @@ int preload_ops() {
                        (const void*)colsum_final_kernel, (const void*)colsum_kernel, (const void*)colsum2_kernel,
                        (const void*)softmax_fwd_kernel,
                        (const void*)softmax_bwd_kernel, (const void*)xent_kernel,
-                       (const void*)reduce_sum_kernel, (const void*)cast_f32_bf16_kernel,
-                       (const void*)cast_bf16_f32_kernel, (const void*)init_normal_kernel};
+                       (const void*)reduce_sum_kernel, (const void*)cast_f32_hx_kernel, (const void*)nonfinite_kernel,
+                       (const void*)cast_hx_f32_kernel, (const void*)init_normal_kernel};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
   return 0;

@@ -4,7 +4,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
-#include <cuda_bf16.h>
+#include "half.cuh"
 
 namespace axonn {
 
@@ -70,7 +70,7 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 inputs, fp32 accumulate)
-__device__ __forceinline__ void mma_bf16_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+__device__ __forceinline__ void mma_f16_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -136,16 +136,15 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t
   return d;
 }
 
-// Instruction descriptor for kind::f16: bf16 x bf16 -> fp32, dense.
-__host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N, uint32_t a_mn_major,
+// Instruction descriptor for kind::f16: 16-bit x 16-bit (bf16 or fp16, half.cuh) -> fp32, dense.
+__host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t M, uint32_t N, uint32_t a_mn_major,
                                                        uint32_t b_mn_major) {
   return (1u << 4)            // D format f32
-         | (1u << 7)          // A format bf16
-         | (1u << 10)         // B format bf16
+         | (kUmmaFmt << 7)    // A format (1 bf16, 0 fp16)
+         | (kUmmaFmt << 10)   // B format
          | (a_mn_major << 15) | (b_mn_major << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
-__device__ __forceinline__ float bf16_to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
 
 // ------------------------------------------------------------------ CTA pair (cta_group::2)
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -189,7 +188,7 @@ template <uint32_t kCols>
 __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
 }
-__device__ __forceinline__ void mma_bf16_ss_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+__device__ __forceinline__ void mma_f16_ss_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                                  uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"

@@ -40,9 +40,12 @@ class AxoNN:
                  weight_decay: float = 0.01, loss_scale: float = 1.0, offload: bool = False,
                  bucket_elems: int = 4_000_000, coarsen_k: int = 4, pipeline_limit: int = 0,
                  overlap_next_batch: bool | None = None, checkpoint_interval: int = 0,
-                 rank: int = 0, world_size: int = 1, device: int = 0, nccl_id: bytes | None = None):
-        self.lib = _lib.load()
-        self.mc = _lib.ModelCfg(n_layers, hidden, heads, seq_len, vocab, init_seed)
+                 rank: int = 0, world_size: int = 1, device: int = 0, nccl_id: bytes | None = None,
+                 dtype: str = "bf16"):
+        # the half format picks the library build (include/axonn.h axonn_dtype)
+        self.lib = _lib.load(dtype)
+        self.dtype = dtype
+        self.mc = _lib.ModelCfg(n_layers, hidden, heads, seq_len, vocab, init_seed, _lib.DTYPES[dtype])
         self.oc = _lib.OptCfg(lr, beta1, beta2, eps, weight_decay, loss_scale, int(offload),
                               bucket_elems, coarsen_k, pipeline_limit, checkpoint_interval,
                               # default: overlap when the optimizer is host-link bound (offload);

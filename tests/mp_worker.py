@@ -22,11 +22,15 @@ def main():
     ap.add_argument("--cfg", default="tiny")
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--offload", type=int, default=0)
+    ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--loss-scale", type=float, default=1.0)
+    ap.add_argument("--inf-rank", type=int, default=-1,
+                    help="after step 0's run_batch this rank writes one inf gradient (D-12 skip)")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     import torch
     from paper_2110_13005_b200 import dist as D
-    from paper_2110_13005_b200.engine import T_GRAD, T_GRAD32, T_MASTER, AxoNN
+    from paper_2110_13005_b200.engine import T_GRAD, T_GRAD32, T_MASTER, AxoNN, AxoNNError
     from synth import init_params, markov_tokens
     cfgs = {"tiny": dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256),
             "tiny4": dict(n_layers=4, hidden=64, heads=2, seq_len=32, vocab=256),
@@ -39,7 +43,8 @@ def main():
     D.init_process_group(rank, world)
     nid = D.share_unique_id(rank, world, D.nccl_unique_id)
     eng = AxoNN(a.g_inter, a.g_data, a.mb, **cfg, rank=rank, world_size=world, device=local,
-                nccl_id=nid, offload=bool(a.offload), bucket_elems=5000, coarsen_k=2)
+                nccl_id=nid, offload=bool(a.offload), bucket_elems=5000, coarsen_k=2,
+                dtype=a.dtype, loss_scale=a.loss_scale)
     params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=42)
     names = [n for n, _, _ in eng.tensors()]
     eng.write_all(T_MASTER, {n: params[n] for n in names})
@@ -53,6 +58,20 @@ def main():
                 out["g32." + n] = v
             for n, v in eng.read_all(T_GRAD).items():
                 out["g16." + n] = v
+        if step == 0 and a.inf_rank >= 0:
+            before = eng.read_all(T_MASTER)
+            if rank == a.inf_rank:
+                g = eng.read(T_GRAD, 0)
+                g.reshape(-1)[g.size // 2] = np.inf
+                eng.write(T_GRAD, 0, g)
+            try:
+                eng.optimizer_step()
+                out["skipped"] = np.array(0)
+            except AxoNNError as e:
+                out["skipped"] = np.array(1 if e.status == "NONFINITE" else -1)
+            after = eng.read_all(T_MASTER)
+            out["unchanged"] = np.array(all(np.array_equal(before[n], after[n]) for n in before))
+            eng.run_batch(tok)   # the skipped step is redone on the same batch
         eng.optimizer_step()
     for n, v in eng.read_all(T_MASTER).items():
         out["theta." + n] = v

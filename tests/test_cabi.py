@@ -8,10 +8,14 @@ import subprocess
 import pytest
 
 
-def test_library_builds_and_exports_all_symbols():
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+def test_library_builds_and_exports_all_symbols(dtype):
+    """Both builds (bf16 libaxonn.so, fp16 libaxonn_fp16.so) export exactly the header's ABI
+    and report their half format."""
     from paper_2110_13005_b200 import _lib, build
-    path = build.build()
-    lib = C.CDLL(path)
+    build.build()
+    path = build.LIBS[dtype]
+    lib = C.CDLL(path, mode=C.RTLD_LOCAL)
     names = _lib.exported_symbols()
     assert len(names) >= 15
     for n in names:
@@ -20,6 +24,18 @@ def test_library_builds_and_exports_all_symbols():
     out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (axonn_\w+)", out))
     assert exported == set(names), exported ^ set(names)
+    assert _lib.load(dtype).axonn_half_dtype() == _lib.DTYPES[dtype]
+
+
+def test_dtype_mismatch_rejected_before_device():
+    """axonn_model_cfg.dtype must match the library build (INVALID_ARG before any device work)."""
+    from paper_2110_13005_b200 import _lib
+    for dtype, other in (("bf16", 1), ("fp16", 0)):
+        mc = _lib.ModelCfg(2, 64, 2, 32, 256, 42, other)
+        oc = _lib.OptCfg(1e-3, 0.9, 0.999, 1e-8, 0.01, 1.0, 0, 4000000, 4, 0, 0, 0)
+        ctx = C.c_void_p()
+        rc = _lib.load(dtype).axonn_init(1, 1, 2, C.byref(mc), C.byref(oc), None, C.byref(ctx))
+        assert rc == -1 and not ctx.value
 
 
 def test_header_declares_paper_boundary():

@@ -28,13 +28,13 @@ def free_port():
     return p
 
 
-def launch(tmp_path, gi, gd, cfg="tiny", mb=2, batch=8, steps=1, offload=0):
+def launch(tmp_path, gi, gd, cfg="tiny", mb=2, batch=8, steps=1, offload=0, extra=()):
     n = gi * gd
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            os.path.join(ROOT, "tests", "mp_worker.py"), "--g-inter", str(gi), "--g-data", str(gd),
            "--mb", str(mb), "--batch", str(batch), "--cfg", cfg, "--steps", str(steps),
-           "--offload", str(offload), "--out", str(tmp_path)]
+           "--offload", str(offload), "--out", str(tmp_path)] + list(extra)
     env = dict(os.environ, AXONN_WATCHDOG_S="60")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
@@ -48,16 +48,17 @@ def cos(a, b):
     return float((a * b).sum() / (na * nb))
 
 
-def oracle(cfgname, batch, seed=7):
+def oracle(cfgname, batch, seed=7, half="bf16"):
+    from oracle.bf16 import round_half
     cfg = CFGS[cfgname]
     p = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=42)
-    p64 = {k: v.astype(np.float64) for k, v in p.items()}
+    p64 = {k: round_half(v, half).astype(np.float64) for k, v in p.items()}   # the model runs on theta16
     tok = markov_tokens(batch, cfg["seq_len"], cfg["vocab"], seed=seed)
     return model.full_batch_loss_and_grads(p64, model.GPTConfig(**cfg), tok)
 
 
-def check(res, gi, gd, cfgname, batch):
-    loss_ref, g_ref = oracle(cfgname, batch)
+def check(res, gi, gd, cfgname, batch, half="bf16"):
+    loss_ref, g_ref = oracle(cfgname, batch, half=half)
     for r in res:   # C5: every rank reports the same batch loss
         assert abs(float(r["loss0"]) - loss_ref) <= 2e-2 * abs(loss_ref)
     assert len({float(r["loss0"]) for r in res}) == 1
@@ -107,3 +108,24 @@ def test_pipeline_offload_multi_step(tmp_path):
     losses = [float(res[0][f"loss{k}"]) for k in range(3)]
     assert all(np.isfinite(losses))
     assert len({float(r["loss2"]) for r in res}) == 1
+
+
+@pytest.mark.multigpu(2)
+@pytest.mark.parametrize("gi,gd", [(2, 1), (1, 2)])
+def test_two_gpus_fp16(tmp_path, gi, gd):
+    """§8(f) N2: the fp16 library (fp16 messages over NCCL P2P, fp16 column all-reduce) with a
+    static loss scale 1024 matches the oracle at theta16 = RNE_fp16(theta)."""
+    res = launch(tmp_path, gi, gd, "tiny", 2, 8, extra=("--dtype", "fp16", "--loss-scale", "1024"))
+    check(res, gi, gd, "tiny", 8, half="fp16")
+
+
+@pytest.mark.multigpu(2)
+@pytest.mark.parametrize("gi,gd", [(2, 1), (1, 2)])
+def test_two_gpus_fp16_overflow_skip_is_collective(tmp_path, gi, gd):
+    """Reading D-12: an inf gradient on ONE rank skips the step on EVERY rank (flag MAX-reduced
+    over the world); no weight changes anywhere; the redone step then matches the oracle."""
+    res = launch(tmp_path, gi, gd, "tiny", 2, 8,
+                 extra=("--dtype", "fp16", "--loss-scale", "1024", "--inf-rank", "1"))
+    for r in res:
+        assert int(r["skipped"]) == 1 and bool(r["unchanged"])
+    check(res, gi, gd, "tiny", 8, half="fp16")
