@@ -147,6 +147,101 @@ static int init_weights(Ctx* c) {
   return 0;
 }
 
+// ------------------------------------------------------------------ peer-copy links
+// Stream memory operations (driver API, resolved once through the runtime's entry-point query).
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static void* driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return p;
+}
+static int wait_flag(Ctx* c, cudaStream_t st, const uint32_t* flag, uint32_t v) {
+  static PFN_waitValue32 fn = (PFN_waitValue32)driver_fn("cuStreamWaitValue32");
+  if (!fn) return c->fail(AXONN_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  if (fn((CUstream)st, (CUdeviceptr)flag, v, CU_STREAM_WAIT_VALUE_EQ) != CUDA_SUCCESS)
+    return c->fail(AXONN_ERR_CUDA, "cuStreamWaitValue32");
+  return 0;
+}
+static int write_flag(Ctx* c, cudaStream_t st, uint32_t* flag, uint32_t v) {
+  static PFN_writeValue32 fn = (PFN_writeValue32)driver_fn("cuStreamWriteValue32");
+  if (!fn) return c->fail(AXONN_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  // default flags: the write is ordered after, and made visible after, the preceding copy
+  if (fn((CUstream)st, (CUdeviceptr)flag, v, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+    return c->fail(AXONN_ERR_CUDA, "cuStreamWriteValue32");
+  return 0;
+}
+
+// Exchange CUDA IPC handles of the receive slots and flags with both neighbours (over the
+// already-connected NCCL link comms, in ascending boundary order like the warm-up) and map
+// the neighbours' buffers.  After this a message is one copy-engine transfer + one flag store.
+static int ipc_links(Ctx* c) {
+  const int L = c->limit;
+  const size_t HB = sizeof(cudaIpcMemHandle_t);
+  const size_t pk = (size_t)(1 + L) * HB;
+  int rc;
+  c->flags = (uint32_t*)c->dalloc(2 * L * sizeof(uint32_t));
+  if (!c->flags) return c->fail(AXONN_ERR_OOM, "link flags");
+  if ((rc = c->check_cuda(cudaMemset(c->flags, 0, 2 * L * sizeof(uint32_t)), "flags"))) return rc;
+  std::vector<char> up(pk), down(pk), got(pk);   // up: to stage-1 (my act slots), down: to stage+1
+  if ((rc = c->check_cuda(cudaIpcGetMemHandle((cudaIpcMemHandle_t*)up.data(), c->flags), "ipc flags")))
+    return rc;
+  memcpy(down.data(), up.data(), HB);
+  for (int k = 0; k < L; ++k) {
+    if (!c->first &&
+        (rc = c->check_cuda(cudaIpcGetMemHandle((cudaIpcMemHandle_t*)(up.data() + (1 + k) * HB), c->slots[k].in),
+                            "ipc act slot")))
+      return rc;
+    if (!c->last &&
+        (rc = c->check_cuda(cudaIpcGetMemHandle((cudaIpcMemHandle_t*)(down.data() + (1 + k) * HB),
+                                                c->slots[k].grecv), "ipc grad slot")))
+      return rc;
+  }
+  char* dbuf = (char*)c->dalloc(pk);
+  if (!dbuf) return c->fail(AXONN_ERR_OOM, "ipc exchange buffer");
+  auto xfer = [&](bool send, std::vector<char>& host, ncclComm_t comm, int peer) -> int {
+    int r;
+    if (send) {
+      if ((r = c->check_cuda(cudaMemcpy(dbuf, host.data(), pk, cudaMemcpyHostToDevice), "ipc h2d"))) return r;
+      if ((r = c->check_nccl(ncclSend(dbuf, pk, ncclChar, peer, comm, c->s_comp), "ipc send"))) return r;
+      return c->check_cuda(cudaStreamSynchronize(c->s_comp), "ipc sync");
+    }
+    if ((r = c->check_nccl(ncclRecv(dbuf, pk, ncclChar, peer, comm, c->s_comp), "ipc recv"))) return r;
+    if ((r = c->check_cuda(cudaStreamSynchronize(c->s_comp), "ipc sync"))) return r;
+    return c->check_cuda(cudaMemcpy(host.data(), dbuf, pk, cudaMemcpyDeviceToHost), "ipc d2h");
+  };
+  auto open = [&](const char* h, void** ptr) -> int {
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, h, HB);
+    int r = c->check_cuda(cudaIpcOpenMemHandle(ptr, hd, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+    if (!r) c->ipc_opened.push_back(*ptr);
+    return r;
+  };
+  for (int kb = 0; kb < c->g_inter - 1; ++kb) {
+    if (kb == c->stage) {            // lower end: give my grad slots, map the upper's act slots
+      if ((rc = xfer(true, down, c->act_out, 1)) || (rc = xfer(false, got, c->grad_in, 1))) return rc;
+      void* p;
+      if ((rc = open(got.data(), &p))) return rc;
+      c->peer_flags_next = (uint32_t*)p;
+      c->peer_act.assign(L, nullptr);
+      for (int k = 0; k < L; ++k)
+        if ((rc = open(got.data() + (1 + k) * HB, &c->peer_act[k]))) return rc;
+    } else if (kb == c->stage - 1) {   // upper end
+      if ((rc = xfer(false, got, c->act_in, 0)) || (rc = xfer(true, up, c->grad_out, 0))) return rc;
+      void* p;
+      if ((rc = open(got.data(), &p))) return rc;
+      c->peer_flags_prev = (uint32_t*)p;
+      c->peer_grad.assign(L, nullptr);
+      for (int k = 0; k < L; ++k)
+        if ((rc = open(got.data() + (1 + k) * HB, &c->peer_grad[k]))) return rc;
+    }
+  }
+  return 0;
+}
+
 // ------------------------------------------------------------------ init
 static int split_comm(Ctx* c, ncclComm_t parent, int color, int key, ncclComm_t* out,
                       int max_ctas) {
@@ -353,6 +448,10 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   c->dp = (d + 7) / 8 * 8;            // e.g. 12B: d = 188 -> 192 (D-7: scale stays 1/sqrt(188))
   c->lq = 3LL * c->heads * c->dp;
   c->limit = g_inter == 1 ? 1 : (opt->pipeline_limit > 0 ? opt->pipeline_limit : g_inter);
+  {
+    const char* e = getenv("AXONN_P2P");   // must agree on all ranks (same launcher env)
+    c->p2p_ipc = !(e && strcmp(e, "nccl") == 0);
+  }
   if (opt->checkpoint_interval == -1) {   // factor of N / G_inter closest to sqrt(N)
     const double root = std::sqrt((double)model->n_layers);
     int best = 1;
@@ -402,8 +501,9 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
                             "ncclCommInitRank")))
       return bail(rc);
     c->owned_comms.push_back(c->world_comm);
+    if (const char* e = getenv("AXONN_DP_CTAS")) c->dp_ctas = atoi(e);
     if ((rc = split_comm(c, c->world_comm, g_data > 1 ? c->stage : NCCL_SPLIT_NOCOLOR, c->replica,
-                         &c->dp_comm, 0)))
+                         &c->dp_comm, c->dp_ctas)))
       return bail(rc);
     // links between stage k and k+1 of row j; even and odd boundaries in separate splits so
     // that every rank joins at most one comm per split.  P2P comms capped at 4 CTAs.
@@ -452,6 +552,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
       }
     }
   }
+  if (world > 1 && g_inter > 1 && c->p2p_ipc && (rc = ipc_links(c))) return bail(rc);
   if ((rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "init sync"))) return bail(rc);
   *out = c;
   return AXONN_OK;
@@ -465,6 +566,7 @@ AXONN_API void axonn_free(axonn_ctx* c) {
     if (c->sticky) ncclCommAbort(nc);
     else ncclCommDestroy(nc);
   }
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : c->allocs) cudaFree(p);
   if (c->oc.offload) {
     if (c->master) cudaFreeHost(c->master);
@@ -647,6 +749,37 @@ AXONN_API axonn_status axonn_stats(const axonn_ctx* c, double* out, int n) {
 namespace axonn {
 
 // Alg. 2 on this rank for microbatches 0..m-1.
+int Ctx::ar_ready(int64_t lo) {
+  if (lo >= ar_hi) return 0;
+  cudaEvent_t a = ev(), b = ev();
+  int rc;
+  if ((rc = check_cuda(cudaEventRecord(a, s_comp), "ar ev")) || (rc = check_cuda(cudaEventRecord(b, s_wg), "ar ev")) ||
+      (rc = check_cuda(cudaStreamWaitEvent(s_dp, a, 0), "ar wait")) ||
+      (rc = check_cuda(cudaStreamWaitEvent(s_dp, b, 0), "ar wait")))
+    return rc;
+  if (!ar_active && opt_pending &&   // grad16 is read by the still-running optimizer step
+      (rc = check_cuda(cudaStreamWaitEvent(s_dp, ev_opt_done, 0), "ar wait opt")))
+    return rc;
+  ar_active = true;
+  if (cast_f32_hx(grad32 + lo, static_cast<char*>(grad16) + lo * 2, ar_hi - lo, s_dp))
+    return fail(AXONN_ERR_CUDA, "cast");
+  ++launches;
+  ar_hi = lo;
+  const int64_t ch = (int64_t)oc.coarsen_k * oc.bucket_elems;
+  while (ar_next_chunk >= 0 && ar_next_chunk * ch >= lo) {
+    const int64_t c0 = ar_next_chunk * ch, n = std::min(ch, nflat - c0);
+    if ((rc = check_nccl(ncclAllReduce(static_cast<char*>(grad16) + c0 * 2, static_cast<char*>(grad16) + c0 * 2, n,
+                                       kNcclHalf, ncclSum, dp_comm, s_dp), "ncclAllReduce")))
+      return rc;
+    cudaEvent_t e = ev();
+    if ((rc = check_cuda(cudaEventRecord(e, s_dp), "ar ev"))) return rc;
+    ev_chunk[ar_next_chunk] = e;
+    stats[AXONN_STAT_ALLREDUCE_BYTES] += n * 2.0;
+    --ar_next_chunk;
+  }
+  return 0;
+}
+
 static int run_pipeline(Ctx* c, int m) {
   const size_t Mh = (size_t)c->M * c->h;
   const int P = c->g_inter, L = c->limit;
@@ -667,6 +800,11 @@ static int run_pipeline(Ctx* c, int m) {
   int done_b = 0;                              // backwards completed on this stage
   int popped = 0;                              // stage 0 injections
   auto slot_of = [&](int mb) -> Slot& { return c->slots[mb % L]; };
+  // message sequence number (peer-copy links): unique over the context's lifetime, so a flag
+  // left from an earlier batch never matches; every stage counts the same microbatches
+  const uint32_t base = c->msg_base;
+  auto seq = [&](int mb) -> uint32_t { return base + (uint32_t)mb + 1u; };
+  c->msg_base += (uint32_t)m;
   auto post = [&]() -> int {
     // pre-post receives into free slots, in microbatch order
     while (!c->first && next_act_post < m && next_act_post < done_b + L) {
@@ -674,8 +812,9 @@ static int run_pipeline(Ctx* c, int m) {
       ev_act[mb] = c->ev();
       // the slot's previous occupant (mb - L) must have finished its backward on the GPU
       if (mb >= L) cudaStreamWaitEvent(c->s_recv_act, ev_bdone[mb - L], 0);
-      int r = c->check_nccl(ncclRecv(slot_of(mb).in, Mh, kNcclHalf, 0, c->act_in, c->s_recv_act),
-                            "ncclRecv act");
+      int r = c->p2p_ipc ? wait_flag(c, c->s_recv_act, c->flags + mb % L, seq(mb))
+                         : c->check_nccl(ncclRecv(slot_of(mb).in, Mh, kNcclHalf, 0, c->act_in, c->s_recv_act),
+                                         "ncclRecv act");
       if (r) return r;
       if ((r = c->check_cuda(cudaEventRecord(ev_act[mb], c->s_recv_act), "rec"))) return r;
     }
@@ -683,8 +822,9 @@ static int run_pipeline(Ctx* c, int m) {
       int mb = next_grad_post++;
       ev_grad[mb] = c->ev();
       if (mb >= L) cudaStreamWaitEvent(c->s_recv_grad, ev_bdone[mb - L], 0);
-      int r = c->check_nccl(ncclRecv(slot_of(mb).grecv, Mh, kNcclHalf, 1, c->grad_in, c->s_recv_grad),
-                            "ncclRecv grad");
+      int r = c->p2p_ipc ? wait_flag(c, c->s_recv_grad, c->flags + L + mb % L, seq(mb))
+                         : c->check_nccl(ncclRecv(slot_of(mb).grecv, Mh, kNcclHalf, 1, c->grad_in,
+                                                  c->s_recv_grad), "ncclRecv grad");
       if (r) return r;
       if ((r = c->check_cuda(cudaEventRecord(ev_grad[mb], c->s_recv_grad), "rec"))) return r;
     }
@@ -697,7 +837,14 @@ static int run_pipeline(Ctx* c, int m) {
     cudaStreamWaitEvent(c->s_send_act, e, 0);
     const void* out = c->stage_out(sl);
     c->stats[AXONN_STAT_P2P_BYTES] += (double)Mh * 2;
-    int r = c->check_nccl(ncclSend(out, Mh, kNcclHalf, 1, c->act_out, c->s_send_act), "ncclSend act");
+    int r;
+    if (c->p2p_ipc) {   // copy engine over NVLink into stage+1's slot, then its flag
+      r = c->check_cuda(cudaMemcpyAsync(c->peer_act[mb % L], out, Mh * 2, cudaMemcpyDeviceToDevice,
+                                        c->s_send_act), "peer copy act");
+      if (!r) r = write_flag(c, c->s_send_act, c->peer_flags_next + mb % L, seq(mb));
+    } else {
+      r = c->check_nccl(ncclSend(out, Mh, kNcclHalf, 1, c->act_out, c->s_send_act), "ncclSend act");
+    }
     ev_sent_act[mb] = c->ev();
     cudaEventRecord(ev_sent_act[mb], c->s_send_act);
     return r;
@@ -708,8 +855,14 @@ static int run_pipeline(Ctx* c, int m) {
     cudaEventRecord(e, c->s_comp);
     cudaStreamWaitEvent(c->s_send_grad, e, 0);
     c->stats[AXONN_STAT_P2P_BYTES] += (double)Mh * 2;
-    int r = c->check_nccl(ncclSend(sl.gsend, Mh, kNcclHalf, 0, c->grad_out, c->s_send_grad),
-                          "ncclSend grad");
+    int r;
+    if (c->p2p_ipc) {
+      r = c->check_cuda(cudaMemcpyAsync(c->peer_grad[mb % L], sl.gsend, Mh * 2, cudaMemcpyDeviceToDevice,
+                                        c->s_send_grad), "peer copy grad");
+      if (!r) r = write_flag(c, c->s_send_grad, c->peer_flags_prev + L + mb % L, seq(mb));
+    } else {
+      r = c->check_nccl(ncclSend(sl.gsend, Mh, kNcclHalf, 0, c->grad_out, c->s_send_grad), "ncclSend grad");
+    }
     ev_sent_grad[mb] = c->ev();
     cudaEventRecord(ev_sent_grad[mb], c->s_send_grad);
     return r;
@@ -858,15 +1011,30 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
     if (!c->ph[par][k]) CU(cudaEventCreate(&c->ph[par][k]));
   c->busy_ev.clear();
   CU(cudaEventRecord(c->ph[par][0], c->s_comp));
+  const int64_t ch_elems = chunk_elems(c);
+  c->ar_overlap = c->g_data > 1 && !(getenv("AXONN_AR_OVERLAP") && getenv("AXONN_AR_OVERLAP")[0] == '0');
+  c->ar_active = false;
+  c->ev_chunk.clear();
+  if (c->ar_overlap) {
+    c->ar_hi = c->nflat;
+    c->ar_next_chunk = (c->nflat + ch_elems - 1) / ch_elems - 1;
+    c->ev_chunk.assign((size_t)(c->ar_next_chunk + 1), nullptr);
+  }
   int rc = run_pipeline(c, m);
   if (rc) return (axonn_status)rc;
   CU(cudaEventRecord(c->ph[par][1], c->s_comp));
-  // grad16 is still read by a pending optimizer step until it completes
-  if (c->opt_pending) CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
-  // half-precision gradients (D-20: fp32 accumulation, bf16 reduction)
-  if (cast_f32_hx(c->grad32, c->grad16, c->nflat, c->s_comp)) return (axonn_status)c->fail(AXONN_ERR_CUDA, "cast");
-  ++c->launches;
-  CU(cudaEventRecord(c->ev_grads_ready, c->s_comp));
+  if (c->ar_overlap) {
+    if ((rc = c->ar_ready(0))) return (axonn_status)rc;   // no-op unless a stage had no layers
+    c->ar_active = false;
+    CU(cudaEventRecord(c->ev_grads_ready, c->s_comp));
+  } else {
+    // grad16 is still read by a pending optimizer step until it completes
+    if (c->opt_pending) CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
+    // half-precision gradients (D-20: fp32 accumulation, half reduction)
+    if (cast_f32_hx(c->grad32, c->grad16, c->nflat, c->s_comp)) return (axonn_status)c->fail(AXONN_ERR_CUDA, "cast");
+    ++c->launches;
+    CU(cudaEventRecord(c->ev_grads_ready, c->s_comp));
+  }
   if (c->g_data == 1) CU(cudaEventRecord(c->ph[par][2], c->s_comp));
   CU(cudaEventRecord(c->ev_loss, c->s_comp));
   CU(cudaStreamWaitEvent(c->s_dp, c->ev_loss, 0));
@@ -876,8 +1044,9 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   cudaEvent_t ev_loss_host = c->ev();
   CU(cudaEventRecord(ev_loss_host, c->s_dp));
   // Alg. 1 l.13: SUM all-reduce over the column, chunks of k * bsize
-  c->ev_chunk.clear();
-  if (c->g_data > 1) {
+  if (c->ar_overlap) {
+    CU(cudaEventRecord(c->ph[par][2], c->s_dp));
+  } else if (c->g_data > 1) {
     CU(cudaStreamWaitEvent(c->s_dp, c->ev_grads_ready, 0));
     const int64_t ch = chunk_elems(c);
     for (int64_t lo = 0; lo < c->nflat; lo += ch) {
@@ -892,7 +1061,8 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
     CU(cudaEventRecord(c->ph[par][2], c->s_dp));
   }
   CU(cudaEventSynchronize(ev_loss_host));
-  if (loss_out) *loss_out = (float)(*c->h_loss / c->oc.loss_scale);
+  // the row losses are summed unscaled (the S of D-11 enters only the CE gradient): L/S
+  if (loss_out) *loss_out = (float)(*c->h_loss);
   c->grads_ready = true;
   {   // device-timed phase of this batch (every s_comp event has completed: loss synced)
     float ms = 0;

@@ -116,6 +116,19 @@ struct Ctx {
   ncclComm_t world_comm = nullptr, dp_comm = nullptr, act_out = nullptr, act_in = nullptr,
              grad_out = nullptr, grad_in = nullptr;
   std::vector<ncclComm_t> owned_comms;
+  // Pipeline link transport (Alg. 2 messages).  p2p_ipc = 1 (default): the
+  // sender's copy engine writes the message over NVLink straight into the neighbour's receive
+  // slot (CUDA IPC mapping), then a stream memop stores the message's sequence number into
+  // the receiver's flag; the receiver's stream waits on that flag (no SM is held by a
+  // pending receive).  p2p_ipc = 0 (AXONN_P2P=nccl): NCCL send/recv on 2-rank link comms.
+  int p2p_ipc = 0;
+  uint32_t* flags = nullptr;          // device [2 * limit]: act slot k, then grad slot k
+  std::vector<void*> peer_act;        // stage + 1's slot.in buffers, mapped here
+  std::vector<void*> peer_grad;       // stage - 1's slot.grecv buffers, mapped here
+  uint32_t* peer_flags_next = nullptr;   // stage + 1's flags
+  uint32_t* peer_flags_prev = nullptr;   // stage - 1's flags
+  std::vector<void*> ipc_opened;
+  uint32_t msg_base = 0;              // sequence number base: messages of earlier batches
   cudaEvent_t ev_grads_ready = nullptr, ev_opt_done = nullptr, ev_loss = nullptr;
   std::vector<cudaEvent_t> ev_chunk;
   cudaEvent_t ev_h2d[3] = {}, ev_adam[3] = {}, ev_d2h[3] = {};
@@ -140,6 +153,16 @@ struct Ctx {
   cudaEvent_t ph[2][4] = {};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_ev;
   void phase_stats_ar_opt(int par);
+  // Column all-reduce overlapped with the batch's last backward (G_data > 1, reading D-32):
+  // as each layer's gradients become final (reverse layer order = descending flat index) its
+  // range is cast to the half format on s_dp and every all-reduce chunk (k * bsize elements,
+  // PAPER.md:731-737) lying wholly above the frontier is issued, top chunk first.
+  bool ar_overlap = false;            // this batch reduces chunk by chunk during the last backward
+  bool ar_active = false;             // an overlapped all-reduce has been issued (SM reservation)
+  int dp_ctas = 0;                    // AXONN_DP_CTAS: cap of the column comm's CTAs, reserved
+  int64_t ar_hi = 0;                  // gradients [ar_hi, nflat) are cast and handed to s_dp
+  int64_t ar_next_chunk = -1;         // highest chunk not yet issued
+  int ar_ready(int64_t lo);           // gradients [lo, ar_hi) are final on s_comp / s_wg
   std::vector<cudaEvent_t> ev_bucket; // K9 of bucket b done (theta16 of the bucket written)
   std::vector<ProfRec> prof_opt;      // AdamW records of the pending step
   void wait_params(int64_t off_end);  // s_comp waits until theta16[0, off_end) is updated

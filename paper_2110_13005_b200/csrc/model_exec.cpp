@@ -46,8 +46,11 @@ int Ctx::gemm(GemmArgs g, double flops) {
   if (g.Z == 0) g.Z = 1;
   if (g.Z1 == 0) g.Z1 = 1;
   if (g.alpha == 0.f) g.alpha = 1.f;
-  // leave two TPCs to the posted one-CTA NCCL P2P kernels (receive act/grad, short sends)
-  if (g.max_ctas == 0 && g_inter > 1) g.max_ctas = num_sms - 4;
+  // NCCL links: leave two TPCs to the posted one-CTA NCCL P2P kernels (receive act/grad,
+  // short sends).  Peer-copy links run on the copy engines and need no SM.
+  if (g.max_ctas == 0 && g_inter > 1 && !p2p_ipc) g.max_ctas = num_sms - 4;
+  // overlapped column all-reduce running: optionally leave its CTAs their SMs
+  if (g.max_ctas == 0 && ar_active && dp_ctas > 0) g.max_ctas = num_sms - ((dp_ctas + 1) & ~1);
   // stream-K (cross-pair waits) only on s_comp: a weight-gradient GEMM on s_wg may hold SMs
   // concurrently, and two partially resident spinning kernels could starve each other
   if (st == s_wg) g.no_sk = 1;
@@ -397,6 +400,7 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
   const int b = microbatch;
   const int acc = bwd_count > 0 ? 1 : 0;
   const int32_t* tok = dtok + (size_t)mb * b * (s + 1);
+  const bool ar_last = ar_overlap && bwd_count == cur_m - 1;   // backwards run in ascending mb
   void* cur = dh0;
   void* nxt = dh1;
   if (last) {
@@ -408,6 +412,7 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
     TRY(gemm(lin_dgrad(logits, p16(head_w), M, V, h, du), 2.0 * M * V * h));
     KCHK(ln_bwd(du, xL, sl.meanf, sl.rstdf, M, h, p16(lnf_g), nullptr, cur, s_comp));
     KCHK(colsum(du, xL, sl.meanf, sl.rstdf, M, h, cs_ws_ln, g32(lnf_b), g32(lnf_g), acc, s_comp));
+    if (ar_last) TRY(ar_ready(lnf_g));
   } else {
     cur = const_cast<void*>(dout);
   }
@@ -429,6 +434,7 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
     }
     void* din = (li == 0 && !first) ? sl.gsend : nxt;
     TRY(layer_bwd(li, x, stash(sl, li), cur, din));
+    if (ar_last && !(first && li == 0)) TRY(ar_ready(loff[li].ln1_g));
     if (li == 0 && !first) {
       cur = din;
     } else {
@@ -440,6 +446,7 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
     // embedding gradients (fp32, zeroed at batch start): deterministic scatter-add
     KCHK(embed_bwd(tok, s + 1, b, s, h, V, cur, g32(tok_emb), g32(pos_emb), s_comp));
   }
+  if (ar_last) TRY(ar_ready(0));
   wg_join();   // stash, logits and gradient buffers are reused by the next microbatch
   ++bwd_count;
   return 0;

@@ -28,14 +28,14 @@ def free_port():
     return p
 
 
-def launch(tmp_path, gi, gd, cfg="tiny", mb=2, batch=8, steps=1, offload=0, extra=()):
+def launch(tmp_path, gi, gd, cfg="tiny", mb=2, batch=8, steps=1, offload=0, extra=(), env=None):
     n = gi * gd
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            os.path.join(ROOT, "tests", "mp_worker.py"), "--g-inter", str(gi), "--g-data", str(gd),
            "--mb", str(mb), "--batch", str(batch), "--cfg", cfg, "--steps", str(steps),
            "--offload", str(offload), "--out", str(tmp_path)] + list(extra)
-    env = dict(os.environ, AXONN_WATCHDOG_S="60")
+    env = dict(os.environ, AXONN_WATCHDOG_S="60", **(env or {}))
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp_path, f"rank{k}.npz"))) for k in range(n)]
@@ -129,3 +129,33 @@ def test_two_gpus_fp16_overflow_skip_is_collective(tmp_path, gi, gd):
     for r in res:
         assert int(r["skipped"]) == 1 and bool(r["unchanged"])
     check(res, gi, gd, "tiny", 8, half="fp16")
+
+
+@pytest.mark.multigpu(2)
+@pytest.mark.parametrize("gi,gd", [(1, 2)])
+def test_overlapped_allreduce_is_bitwise_neutral(tmp_path, gi, gd):
+    """The column all-reduce issued chunk by chunk during the last backward (AXONN_AR_OVERLAP,
+    default on) reduces the same chunks as the all-reduce after the pipeline: gradients and
+    the weights after 2 steps are bitwise equal (PAPER.md:731-737 chunking, reading D-32)."""
+    res = []
+    for ov in ("0", "1"):
+        d = tmp_path / f"ov{ov}"
+        d.mkdir()
+        res.append(launch(d, gi, gd, "mini", 2, 16, steps=2, env={"AXONN_AR_OVERLAP": ov}))
+    for r0, r1 in zip(*res):
+        for k in r0:
+            assert np.array_equal(r0[k], r1[k]), k
+
+
+@pytest.mark.multigpu(2)
+def test_nccl_and_peer_copy_links_agree_bitwise(tmp_path):
+    """Pipeline messages by NCCL P2P (AXONN_P2P=nccl) or by copy-engine peer copies (default)
+    carry the same bytes: losses, gradients and weights after 2 steps are bitwise equal."""
+    res = []
+    for t in ("nccl", "ipc"):
+        d = tmp_path / t
+        d.mkdir()
+        res.append(launch(d, 2, 1, "mini", 2, 16, steps=2, env={"AXONN_P2P": t}))
+    for r0, r1 in zip(*res):
+        for k in r0:
+            assert np.array_equal(r0[k], r1[k]), k
