@@ -501,6 +501,9 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
                             "ncclCommInitRank")))
       return bail(rc);
     c->owned_comms.push_back(c->world_comm);
+    // column comm capped at 16 CTAs, and those SMs left free by the GEMMs of the last
+    // backward while its all-reduce chunks run (1.3B 1x2: 936.8 vs 931.9 uncapped, 921.4 at 8)
+    c->dp_ctas = 16;
     if (const char* e = getenv("AXONN_DP_CTAS")) c->dp_ctas = atoi(e);
     if ((rc = split_comm(c, c->world_comm, g_data > 1 ? c->stage : NCCL_SPLIT_NOCOLOR, c->replica,
                          &c->dp_comm, c->dp_ctas)))
