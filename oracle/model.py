@@ -102,6 +102,13 @@ def gelu_grad(x):
     return 0.5 * (1.0 + t) + 0.5 * x * (1.0 - t * t) * GELU_C * (1.0 + 3.0 * GELU_A * x * x)
 
 
+def wgrad(dy, x):
+    """Weight gradient sum_{b,s} dy[b,s,:]^T x[b,s,:] of a linear layer y = x W^T, evaluated
+    as one matrix product (a library primitive; the same contraction as the einsum
+    'bsn,bsk->nk', which numpy evaluates without BLAS)."""
+    return dy.reshape(-1, dy.shape[-1]).T @ x.reshape(-1, x.shape[-1])
+
+
 # ---------------------------------------------------------------- one layer
 def layer_forward(p, L, cfg: GPTConfig, h):
     """Pre-LN transformer block (D-1): h [b, s, H] -> [b, s, H]."""
@@ -138,17 +145,17 @@ def layer_backward(p, L, cfg: GPTConfig, cache, dh2):
     red = (0, 1)
     gr = {}
     # h2 = h1 + act W2^T + b2
-    gr[n + "w_fc2"] = np.einsum("bsn,bsk->nk", dh2, act)
+    gr[n + "w_fc2"] = wgrad(dh2, act)
     gr[n + "b_fc2"] = dh2.sum(axis=red)
     dact = dh2 @ p[n + "w_fc2"]
     dpre = dact * gelu_grad(pre)
-    gr[n + "w_fc1"] = np.einsum("bsn,bsk->nk", dpre, w)
+    gr[n + "w_fc1"] = wgrad(dpre, w)
     gr[n + "b_fc1"] = dpre.sum(axis=red)
     dw = dpre @ p[n + "w_fc1"]
     dh1_ln, gr[n + "ln2_g"], gr[n + "ln2_b"] = ln_backward(dw, p[n + "ln2_g"], c2)
     dh1 = dh2 + dh1_ln
     # h1 = h + o Wo^T + bo
-    gr[n + "w_o"] = np.einsum("bsn,bsk->nk", dh1, o)
+    gr[n + "w_o"] = wgrad(dh1, o)
     gr[n + "b_o"] = dh1.sum(axis=red)
     do = (dh1 @ p[n + "w_o"]).reshape(b, s, a, d).transpose(0, 2, 1, 3)
     scale = 1.0 / np.sqrt(d)
@@ -160,7 +167,7 @@ def layer_backward(p, L, cfg: GPTConfig, cache, dh2):
     dk = dsc.transpose(0, 1, 3, 2) @ q
     merge = lambda t: t.transpose(0, 2, 1, 3).reshape(b, s, H)
     dqkv = np.concatenate([merge(dq), merge(dk), merge(dv)], axis=-1)
-    gr[n + "w_qkv"] = np.einsum("bsn,bsk->nk", dqkv, u)
+    gr[n + "w_qkv"] = wgrad(dqkv, u)
     gr[n + "b_qkv"] = dqkv.sum(axis=red)
     du = dqkv @ p[n + "w_qkv"]
     dh_ln, gr[n + "ln1_g"], gr[n + "ln1_b"] = ln_backward(du, p[n + "ln1_g"], c1)
@@ -219,7 +226,7 @@ def stage_backward(p, cfg: GPTConfig, stage: int, n_stages: int, caches, dout):
         np.put_along_axis(onehot, y[..., None], 1.0, axis=-1)
         coef = dout * caches["loss_scale"] / (caches["m_total"] * caches["ntok"])
         dz = coef * (soft - onehot)
-        gr["head_w"] = np.einsum("bsv,bsk->vk", dz, caches["hf"])
+        gr["head_w"] = wgrad(dz, caches["hf"])
         dhf = dz @ p["head_w"]
         dh, gr["lnf_g"], gr["lnf_b"] = ln_backward(dhf, p["lnf_g"], caches["cf"])
     else:
