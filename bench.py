@@ -52,6 +52,22 @@ CONFIGS = {
 }
 
 
+def memory_ledger(eng, offload):
+    """Model-state bytes of rank 0's stage: the paper's
+    ledger, 20 phi without offload and 4 phi + 16 bsize with it, beside this build's:
+    theta16 2 phi + fp32 gradient accumulator 4 phi (reading D-20) + half-precision
+    all-reduce buffer 2 phi, plus theta32 / m / v (12 phi) in HBM or a 3-slot device ring of
+    36 bsize (D-34) with 12 phi in pinned host memory.  Activations come on top."""
+    phi = sum(n for _, _, n in eng.tensors())
+    bsize = eng.oc.bucket_elems
+    ours = 8 * phi + (36 * bsize if offload else 12 * phi)
+    return {"phi_stage": phi, "bsize": bsize,
+            "paper_model_state_bytes": 4 * phi + 16 * bsize if offload else 20 * phi,
+            "ours_model_state_bytes": ours, "host_pinned_bytes": 12 * phi if offload else 0,
+            "note": "rank 0's stage; ours = 2phi theta16 + 4phi fp32 grad (D-20) + 2phi half grad"
+                    " + (36 bsize ring | 12 phi theta32/m/v); device_mem_gib adds activations"}
+
+
 def model_flops(b, s, l, h, V):
     """72 b s l h^2 (1 + s/6h) + 6 b s h V (reading D-25; Eq. 3 credits recompute)."""
     return 72 * b * s * l * h * h + 12 * b * s * s * l * h + 6 * b * s * h * V
@@ -350,6 +366,7 @@ def main():
                        "l2": "inputs larger than L2 (GBs of weights/activations per step)"},
             "per_gpu_tflops": value / world,
             "device_mem_gib": torch.cuda.mem_get_info()[1] / 2**30 - torch.cuda.mem_get_info()[0] / 2**30,
+            "memory": memory_ledger(eng, cfg["offload"]),
             "pct_bf16_peak": 100.0 * value / world / peaks["bf16"],
             "pct_bf16_peak_sustained": 100.0 * value / world / peaks["bf16_sus"],
             "eq3_tflops_per_gpu": eq3_flops(B, s, cfg["n_layers"], cfg["hidden"], V) / (ms_step / 1e3) / 1e12 / world,

@@ -1,0 +1,58 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (③).
+
+The oracle cannot run a whole 64-sequence 1.3B batch in seconds, so the batch is built from
+TWO distinct seeded sequences repeated alternately ([s0, s1, s0, s1, ...]): the batch-mean
+loss and the exact gradient of the full batch then equal those of the two-sequence batch,
+which the oracle computes in fp64 (two sequences keep every per-sample offset inside a
+microbatch observable: a wrong row or sample stride changes the result).
+
+* configs[1], GPT 1.3B-shaped (24 layers, h 2048, 16 heads, s 512, V 51200), G_inter 1,
+  b_m 8, m 8 microbatches (B 64): bench.py's default workload, same engine and kernels;
+* configs[2]'s layer shape: the paper's 12B layer (h 4512, 24 heads, d = 188 padded to 192,
+  s 512, V 51200; Table I) with b_m 8 (Table II), one layer on one
+  stage, two microbatches (gradient accumulation across microbatches, D-20).
+
+Bars (BASELINE.json north_star): loss rel <= 2e-2, per-tensor gradient cosine >= 0.999."""
+import numpy as np
+import pytest
+
+from oracle import model
+from synth import init_params, markov_tokens
+
+pytestmark = pytest.mark.gpu
+
+
+def cos(a, b):
+    na, nb = np.linalg.norm(a), np.linalg.norm(b)
+    if na < 1e-30 and nb < 1e-30:
+        return 1.0
+    return float((a * b).sum() / (na * nb))
+
+
+def run_case(cfg, b_m, B, **kw):
+    from paper_2110_13005_b200.engine import T_GRAD32, T_MASTER, AxoNN
+    two = markov_tokens(2, cfg["seq_len"], cfg["vocab"], seed=77)
+    tok = np.ascontiguousarray(np.tile(two, (B // 2, 1)))          # s0, s1, s0, s1, ...
+    params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=42)
+    eng = AxoNN(1, 1, b_m, **cfg, **kw)
+    eng.write_all(T_MASTER, params)
+    loss = eng.run_batch(tok)
+    g = eng.read_all(T_GRAD32)
+    eng.close()
+    p64 = {k: v.astype(np.float64) for k, v in params.items()}
+    del params
+    loss_ref, g_ref = model.full_batch_loss_and_grads(p64, model.GPTConfig(**cfg), two)
+    assert abs(loss - loss_ref) <= 2e-2 * abs(loss_ref), (loss, loss_ref)
+    worst = min((cos(g[k].astype(np.float64), g_ref[k]), k) for k in g_ref)
+    assert worst[0] >= 0.999, worst
+    return loss, loss_ref, worst
+
+
+def test_gpt1p3b_bench_configuration_vs_oracle():
+    cfg = dict(n_layers=24, hidden=2048, heads=16, seq_len=512, vocab=51200)
+    run_case(cfg, b_m=8, B=64)
+
+
+def test_gpt12b_layer_shape_vs_oracle():
+    cfg = dict(n_layers=1, hidden=4512, heads=24, seq_len=512, vocab=51200)
+    run_case(cfg, b_m=8, B=16)
