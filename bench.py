@@ -226,6 +226,8 @@ def main():
     ap.add_argument("--offload", type=int, default=None, help="1/0: override the config's offload")
     ap.add_argument("--checkpoint-interval", type=int, default=0,
                     help="activation checkpointing ac (PAPER.md:553-576): 0 off, -1 the paper's rule")
+    ap.add_argument("--overlap-next-batch", type=int, default=None,
+                    help="1/0: optimizer step t overlaps batch t+1 (default: on with offload only)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"],
                     help="half format (library build); fp16 runs with a static loss scale (D-11)")
     ap.add_argument("--loss-scale", type=float, default=None,
@@ -265,6 +267,7 @@ def main():
                 heads=cfg["heads"], seq_len=cfg["seq_len"], vocab=cfg["vocab"], init_seed=42,
                 offload=cfg["offload"], rank=rank, world_size=world, device=local, nccl_id=nid,
                 checkpoint_interval=args.checkpoint_interval, dtype=args.dtype,
+                overlap_next_batch=None if args.overlap_next_batch is None else bool(args.overlap_next_batch),
                 loss_scale=args.loss_scale or (1024.0 if args.dtype == "fp16" else 1.0))
     from synth import uniform_tokens
     s, V = cfg["seq_len"], cfg["vocab"]
