@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include "half.cuh"
+#include <cstring>
 #include <cstdint>
 #include <cstdlib>
 
@@ -54,6 +55,30 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 __device__ __forceinline__ void nbar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+// Store up to 8 16-bit values (v) at dst, nvalid of them valid (even).  Head widths that are
+// not a multiple of 8 (d = 188, 176) leave head bases only 8-byte aligned: 8-byte stores.
+__device__ __forceinline__ void store8h(hx* dst, const uint4 v, int nvalid) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+  if (nvalid >= 8 && (a & 15) == 0) {
+    *reinterpret_cast<uint4*>(dst) = v;
+    return;
+  }
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  if ((a & 7) == 0) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      if (4 * hh + 4 <= nvalid)
+        *reinterpret_cast<uint2*>(dst + 4 * hh) = make_uint2(w[2 * hh], w[2 * hh + 1]);
+      else if (4 * hh + 2 <= nvalid)
+        *reinterpret_cast<uint32_t*>(dst + 4 * hh) = w[2 * hh];
+    }
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (2 * e + 2 <= nvalid) *reinterpret_cast<uint32_t*>(dst + 2 * e) = w[e];
+}
+
 __device__ __forceinline__ uint32_t pack_hx2(float lo, float hi) {
   hx2 v = f2hx2(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -309,15 +334,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           const int col = oc + ch * 8;
           if (gr < p.s && col < p.d) {
             const uint4 v = stg[rr * 4 + (ch ^ (rr & 3))];
-            hx* dst = obase + (long long)gr * p.ldo + col;
-            if ((p.d & 7) == 0) {
-              *reinterpret_cast<uint4*>(dst) = v;
-            } else {   // unaligned head width (d = 188, 176): bf16 pairs
-              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (col + 2 * e < p.d) *reinterpret_cast<uint32_t*>(dst + 2 * e) = w[e];
-            }
+            store8h(obase + (long long)gr * p.ldo + col, v, p.d - col);
           }
         }
         __syncwarp();
@@ -353,6 +370,8 @@ struct AttnBwdParams {
   int s, heads, d, nv, nq, nk, total, stages, nbuf;
   int nfb, nab;        // row-operand smem buffers, accumulator TMEM buffers (1 or 2 each)
   int dbg;             // AXONN_ATTN_DBG experiments: 1 no epilogue math, 2 no accumulation MMAs
+  int ld_bulk;         // KA: the producer bulk-copies each query block's lse / D slice into the
+                       // ring stage (s % 64 == 0); else the epilogue loads them per block
   float c1, alpha;
   const float* lse;
   const float* D;
@@ -394,15 +413,7 @@ __device__ __forceinline__ void store_chunk32(uint4* stg, int lane, const uint32
     const int col = col0 + ch * 8;
     if (gr < rows_valid && col < dvalid) {
       const uint4 v = stg[rr * 4 + (ch ^ (rr & 3))];
-      hx* dst = gbase + (long long)gr * ld + col;
-      if ((dvalid & 7) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-        *reinterpret_cast<uint4*>(dst) = v;
-      } else {
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (col + 2 * e < dvalid) *reinterpret_cast<uint32_t*>(dst + 2 * e) = w[e];
-      }
+      store8h(gbase + (long long)gr * ld + col, v, dvalid - col);
     }
   }
   __syncwarp();
@@ -420,7 +431,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const int g_bytes = p.nv * GR * 2;         // one streamed operand
   uint8_t* sF = smem;                        // [nfb] x (F1, F2)
   uint8_t* sG = smem + p.nfb * 2 * f_bytes;  // ring: stage i holds G1, G2
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sG + p.stages * 2 * g_bytes);
+  float* sLD = reinterpret_cast<float*>(sG + p.stages * 2 * g_bytes);   // [stages][lse 64 | D 64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sG + p.stages * 2 * g_bytes + (KA ? p.stages * 512 : 0));
   uint64_t* f_full = bars;                   // [2]
   uint64_t* f_empty = bars + 2;              // [2]
   uint64_t* acc_full = bars + 4;             // [2]
@@ -485,8 +497,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (elect_one()) {
         uint8_t* f = sF + fb * 2 * f_bytes;
         mbar_arrive_expect_tx(&f_full[fb], 2 * f_bytes);
+        if (p.dbg >= 6) {
+          mbar_arrive(&f_full[fb]);   // experiment: no operand loads
+        } else {
         load_rows(f, KA ? &mapK : &mapQ, &f_full[fb], p.nv, FR, r0, z1, z2);
         load_rows(f + f_bytes, KA ? &mapV : &mapO, &f_full[fb], p.nv, FR, r0, z1, z2);
+        }
       }
       __syncwarp();
       for (int it = 0; it < ni; ++it) {
@@ -494,9 +510,18 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         mbar_wait(&g_empty[stage], phase ^ 1);
         if (elect_one()) {
           uint8_t* g = sG + stage * 2 * g_bytes;
-          mbar_arrive_expect_tx(&g_full[stage], 2 * g_bytes);
-          load_rows(g, KA ? &mapQ : &mapK, &g_full[stage], p.nv, GR, g0, z1, z2);
-          load_rows(g + g_bytes, KA ? &mapO : &mapV, &g_full[stage], p.nv, GR, g0, z1, z2);
+          const bool bulk = KA && p.ld_bulk;
+          if (p.dbg >= 6) {
+            mbar_arrive(&g_full[stage]);
+          } else {
+            mbar_arrive_expect_tx(&g_full[stage], 2 * g_bytes + (bulk ? 512 : 0));
+            load_rows(g, KA ? &mapQ : &mapK, &g_full[stage], p.nv, GR, g0, z1, z2);
+            load_rows(g + g_bytes, KA ? &mapO : &mapV, &g_full[stage], p.nv, GR, g0, z1, z2);
+          }
+          if (bulk && p.dbg < 6) {   // this block's 64 queries: lse2 and D (consumed by the epilogue)
+            bulk_g2s(sLD + stage * 128, p.lse + (long long)z * p.s + g0, 256, &g_full[stage]);
+            bulk_g2s(sLD + stage * 128 + 64, p.D + (long long)z * p.s + g0, 256, &g_full[stage]);
+          }
         }
         __syncwarp();
         if (++stage == p.stages) { stage = 0; phase ^= 1; }
@@ -517,7 +542,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);   // last TS-MMA read of b
       tc_fence_after();
       const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
-      if (p.dbg == 4) {   // experiment: no X / Y MMAs
+      if (p.dbg >= 4) {   // experiment: no X / Y MMAs
         if (elect_one()) mma_commit(&xy_full[b]);
         __syncwarp();
         return;
@@ -620,7 +645,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const int b = g % p.nbuf;
         const int g0 = (i0 + it) * GR;        // first query (KA) or key (!KA) of the block
         const int sb = g & 1;
-        if (KA) {
+        const float* Lblk = sL[sb];
+        const float* Dblk = sD[sb];
+        if (KA && p.ld_bulk) {   // the ring stage holds this block's slices (TMA-visible after g_full)
+          const int stg = g % p.stages;
+          mbar_wait(&g_full[stg], (uint32_t)((g / p.stages) & 1));
+          Lblk = sLD + stg * 128;
+          Dblk = Lblk + 64;
+        } else if (KA) {
           const int tid = threadIdx.x - 64;
           if (tid < GR) {
             const int i = g0 + tid;
@@ -631,7 +663,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
         mbar_wait(&xy_full[b], (uint32_t)((g / p.nbuf) & 1));
         tc_fence_after();
-        if (p.dbg == 1 || p.dbg == 3 || p.dbg == 4) {
+        if (p.dbg == 1 || p.dbg >= 3) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&pd_ready[b]);
@@ -652,8 +684,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
             float L, Dv;
             bool ok;
             if (KA) {   // row = key, col = query
-              L = sL[sb][c0 + i + e];
-              Dv = sD[sb][c0 + i + e];
+              L = Lblk[c0 + i + e];
+              Dv = Dblk[c0 + i + e];
               ok = col >= row && col < p.s;
             } else {    // row = query, col = key
               L = Lr;
@@ -681,7 +713,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tc_fence_after();
       hx* base = p.dq + (long long)z2 * p.s * p.ldq + (long long)z1 * p.d;
       const int r0w = r0 + q * 32;
-      for (int which = KA ? 0 : 1; which < 2; ++which) {
+      for (int which = KA ? 0 : 1; which < 2 && p.dbg < 5; ++which) {
         const uint32_t ca = which == 0 ? colA : colB;
         hx* gb = base + (KA ? (which == 0 ? 2 * p.h : p.h) : 0);
         for (int cc = 0; cc < p.nv / 2; cc += 32) {
@@ -737,6 +769,40 @@ __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, in
       for (int e = 0; e < 4; ++e) {
         const float2 xf = hx22f2(xh[e]), yf = hx22f2(yh[e]);
         a = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, a));
+      }
+      acc[u] = a;
+    }
+  } else if ((d & 3) == 0 && (dp & 3) == 0 && (ld_o & 3) == 0 && (ld_do & 3) == 0 && d <= 256) {
+    // head width a multiple of 4 but not 8 (d = 188, 176): 8-byte loads, every load of the
+    // DITEMS items issued before the math (16 lanes x 4 elements = 64 per pass, <= 4 passes)
+    uint2 x[DITEMS][4], y[DITEMS][4];
+#pragma unroll
+    for (int u = 0; u < DITEMS; ++u) {
+      const long long w = grp * DITEMS + u;
+      const long long tok = w / heads;
+      const int hd = (int)(w % heads);
+#pragma unroll
+      for (int ps = 0; ps < 4; ++ps) {
+        const int j = 4 * l + 64 * ps;
+        x[u][ps] = y[u][ps] = make_uint2(0, 0);
+        if (w < nitems && j < d) {
+          x[u][ps] = __ldg(reinterpret_cast<const uint2*>(dO + tok * ld_do + (long long)hd * dp + j));
+          y[u][ps] = __ldg(reinterpret_cast<const uint2*>(O + tok * ld_o + (long long)hd * d + j));
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < DITEMS; ++u) {
+      float a = 0.f;
+#pragma unroll
+      for (int ps = 0; ps < 4; ++ps) {
+        const hx2* xh = reinterpret_cast<const hx2*>(&x[u][ps]);
+        const hx2* yh = reinterpret_cast<const hx2*>(&y[u][ps]);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float2 xf = hx22f2(xh[e]), yf = hx22f2(yh[e]);
+          a = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, a));
+        }
       }
       acc[u] = a;
     }
@@ -822,7 +888,9 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   const int nv = (dp + 63) / 64 * 64;
   if (nv > 256) return -1;
   const long long ntok = (long long)b * s;
-  {
+  // AXONN_ATTN_ONLY (experiments): "d", "ka" or "q" runs only that kernel of the backward
+  const char* only = getenv("AXONN_ATTN_ONLY");
+  if (!only || !strcmp(only, "d")) {
     const long long nthreads = (ntok * heads + DITEMS - 1) / DITEMS * 16;
     attn_bwd_d_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(
         static_cast<const hx*>(dO), (long long)heads * dp, dp,
@@ -856,8 +924,13 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
     p.dbg = e ? atoi(e) : 0;
   }
   const int max_smem = 227 * 1024 - 1024 - 256 - 18 * 1024;   // dynamic budget beside static
+  {
+    const char* e = getenv("AXONN_ATTN_LDBULK");
+    p.ld_bulk = (s % GRB == 0) && !(e && e[0] == '0');
+  }
   for (int ka = 1; ka >= 0; --ka) {
-    const int f_bytes = nv * 128 * 2, g_bytes = nv * GRB * 2;
+    if (only && strcmp(only, ka ? "ka" : "q")) continue;
+    const int f_bytes = nv * 128 * 2, g_bytes = nv * GRB * 2 + (ka ? 256 : 0);   // + lse/D slices
     // prefer: double row-operand buffer (next unit's loads overlap this unit), then ring depth
     static int nfb_env = -1;
     if (nfb_env < 0) {
@@ -881,7 +954,7 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
     if (128 * p.nbuf + accw > 512) return -1;
     p.nab = (128 * p.nbuf + 2 * accw <= 512) ? 2 : 1;
     p.total = b * heads * (ka ? p.nk : p.nq);
-    const int smem = p.nfb * 2 * f_bytes + stages * 2 * g_bytes + 1024 + 256;
+    const int smem = p.nfb * 2 * f_bytes + stages * 2 * g_bytes + 1024 + 256;   // g_bytes counts the slices
     void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, AttnBwdParams) =
         ka ? attn_bwd_kernel<true> : attn_bwd_kernel<false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
