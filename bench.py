@@ -228,6 +228,8 @@ def main():
                     help="activation checkpointing ac (PAPER.md:553-576): 0 off, -1 the paper's rule")
     ap.add_argument("--overlap-next-batch", type=int, default=None,
                     help="1/0: optimizer step t overlaps batch t+1 (default: on with offload only)")
+    ap.add_argument("--stage-balance", type=int, default=0,
+                    help="1: half-layer stage boundaries balancing the LM head (reading D-21b)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"],
                     help="half format (library build); fp16 runs with a static loss scale (D-11)")
     ap.add_argument("--loss-scale", type=float, default=None,
@@ -267,6 +269,7 @@ def main():
                 heads=cfg["heads"], seq_len=cfg["seq_len"], vocab=cfg["vocab"], init_seed=42,
                 offload=cfg["offload"], rank=rank, world_size=world, device=local, nccl_id=nid,
                 checkpoint_interval=args.checkpoint_interval, dtype=args.dtype,
+                stage_balance=bool(args.stage_balance),
                 overlap_next_batch=None if args.overlap_next_batch is None else bool(args.overlap_next_batch),
                 loss_scale=args.loss_scale or (1024.0 if args.dtype == "fp16" else 1.0))
     from synth import uniform_tokens
@@ -366,6 +369,7 @@ def main():
                        "microbatch": b_m, "microbatches_per_replica": m,
                        "parallelism": f"G_inter{g_inter} x G_data{g_data}",
                        "offload": cfg["offload"], "checkpoint_interval": args.checkpoint_interval,
+                       "stage_balance": args.stage_balance,
                        "l2": "inputs larger than L2 (GBs of weights/activations per step)"},
             "per_gpu_tflops": value / world,
             "device_mem_gib": torch.cuda.mem_get_info()[1] / 2**30 - torch.cuda.mem_get_info()[0] / 2**30,

@@ -89,6 +89,13 @@ typedef struct {
                                                  each layer's forward waits only for the buckets that
                                                  hold its parameters (results are identical; reading
                                                  D-32).  0: the step completes before returning. */
+  int stage_balance;                          /* 0: l / G_inter whole layers per stage (PAPER.md:615-617,
+                                                 D-21).  1: stage boundaries at half-layer granularity
+                                                 (after a layer's attention block or after its MLP
+                                                 block) chosen to minimise the largest stage cost in
+                                                 forward FLOPs including the last stage's LM head
+                                                 (reading D-21b); G_inter need not divide n_layers.
+                                                 Values are unchanged; requires checkpoint_interval <= 1. */
 } axonn_opt_cfg;
 
 /* Process placement in the G_inter x G_data grid: world_rank = j * G_inter + i

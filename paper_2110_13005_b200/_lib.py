@@ -41,7 +41,8 @@ class OptCfg(C.Structure):
                 ("eps", C.c_double), ("weight_decay", C.c_double), ("loss_scale", C.c_double),
                 ("offload", C.c_int),
                 ("bucket_elems", C.c_int64), ("coarsen_k", C.c_int), ("pipeline_limit", C.c_int),
-                ("checkpoint_interval", C.c_int), ("overlap_next_batch", C.c_int)]
+                ("checkpoint_interval", C.c_int), ("overlap_next_batch", C.c_int),
+                ("stage_balance", C.c_int)]
 
 
 class Dist(C.Structure):

@@ -98,19 +98,23 @@ static void build_tensors(Ctx* c) {
   }
   for (int li = 0; li < c->nl; ++li) {
     std::string p = "l" + std::to_string(c->layer0 + li) + ".";
-    LayerOff o;
-    o.ln1_g = add(p + "ln1_g", 1, h);
-    o.ln1_b = add(p + "ln1_b", 1, h);
-    o.w_qkv = add(p + "w_qkv", 3 * h, h);
-    o.b_qkv = add(p + "b_qkv", 1, 3 * h);
-    o.w_o = add(p + "w_o", h, h);
-    o.b_o = add(p + "b_o", 1, h);
-    o.ln2_g = add(p + "ln2_g", 1, h);
-    o.ln2_b = add(p + "ln2_b", 1, h);
-    o.w_fc1 = add(p + "w_fc1", 4 * h, h);
-    o.b_fc1 = add(p + "b_fc1", 1, 4 * h);
-    o.w_fc2 = add(p + "w_fc2", h, 4 * h);
-    o.b_fc2 = add(p + "b_fc2", 1, h);
+    LayerOff o{-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+    if (c->lhalf[li] & 1) {   // attention block
+      o.ln1_g = add(p + "ln1_g", 1, h);
+      o.ln1_b = add(p + "ln1_b", 1, h);
+      o.w_qkv = add(p + "w_qkv", 3 * h, h);
+      o.b_qkv = add(p + "b_qkv", 1, 3 * h);
+      o.w_o = add(p + "w_o", h, h);
+      o.b_o = add(p + "b_o", 1, h);
+    }
+    if (c->lhalf[li] & 2) {   // MLP block
+      o.ln2_g = add(p + "ln2_g", 1, h);
+      o.ln2_b = add(p + "ln2_b", 1, h);
+      o.w_fc1 = add(p + "w_fc1", 4 * h, h);
+      o.b_fc1 = add(p + "b_fc1", 1, 4 * h);
+      o.w_fc2 = add(p + "w_fc2", h, 4 * h);
+      o.b_fc2 = add(p + "b_fc2", 1, h);
+    }
     c->loff.push_back(o);
   }
   if (c->last) {
@@ -240,6 +244,36 @@ static int ipc_links(Ctx* c) {
     }
   }
   return 0;
+}
+
+// Reading D-21b (stage_balance): the 2l residual blocks (attention block of layer L = block
+// 2L, its MLP block = 2L + 1) are cut into G_inter contiguous ranges minimising the largest
+// stage cost, cost = forward FLOPs per token: attention block 8h^2 + 2sh (QKV, projection,
+// causal QK^T and PV), MLP block 16h^2, plus the LM head 2hV on the last stage (the embedding
+// gather is negligible).  Exact DP over (stage, boundary); ties go to the earliest boundary.
+// Returns G_inter + 1 boundaries (0 = b_0 < b_1 < ... < b_P = 2l).
+static std::vector<int> balanced_blocks(const axonn_model_cfg* m, int P) {
+  const int nb = 2 * m->n_layers;
+  const double h = m->hidden, s = m->seq_len, V = m->vocab;
+  std::vector<double> pre(nb + 1, 0.0);
+  for (int k = 0; k < nb; ++k) pre[k + 1] = pre[k] + ((k & 1) ? 16 * h * h : 8 * h * h + 2 * s * h);
+  const double head = 2 * h * V;
+  auto cost = [&](int i, int a, int b) { return pre[b] - pre[a] + (i == P - 1 ? head : 0.0); };
+  const double INF = 1e300;
+  std::vector<std::vector<double>> best(P + 1, std::vector<double>(nb + 1, INF));
+  std::vector<std::vector<int>> arg(P + 1, std::vector<int>(nb + 1, -1));
+  best[0][0] = 0;
+  for (int i = 1; i <= P; ++i)
+    for (int b = i; b <= nb; ++b)
+      for (int a = i - 1; a < b; ++a) {
+        if (best[i - 1][a] >= INF) continue;
+        const double v = std::max(best[i - 1][a], cost(i - 1, a, b));
+        if (v < best[i][b] * (1 - 1e-12)) { best[i][b] = v; arg[i][b] = a; }
+      }
+  std::vector<int> bb(P + 1, 0);
+  bb[P] = nb;
+  for (int i = P; i > 0; --i) bb[i - 1] = arg[i][bb[i]];
+  return bb;
 }
 
 // ------------------------------------------------------------------ init
@@ -415,7 +449,11 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   const int rank = dist ? dist->world_rank : 0;
   if (world != g_inter * g_data) return AXONN_ERR_GRID_MISMATCH;
   if (rank < 0 || rank >= world) return AXONN_ERR_INVALID_ARG;
-  if (model->n_layers < 1 || model->n_layers % g_inter) return AXONN_ERR_NONDIVISIBLE_LAYERS;
+  if (model->n_layers < 1 || (!opt->stage_balance && model->n_layers % g_inter) ||
+      2 * model->n_layers < g_inter)
+    return AXONN_ERR_NONDIVISIBLE_LAYERS;
+  if (opt->stage_balance && opt->checkpoint_interval != 0 && opt->checkpoint_interval != 1)
+    return AXONN_ERR_INVALID_ARG;   // checkpoint segments are whole layers
   if (model->hidden < 8 || model->heads < 1 || model->hidden % model->heads ||
       model->hidden % 8 || model->seq_len < 8 || model->seq_len % 8 || model->vocab < 2 ||
       model->vocab % 8)
@@ -441,8 +479,20 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   c->replica = rank / g_inter;
   c->first = c->stage == 0;
   c->last = c->stage == g_inter - 1;
-  c->nl = model->n_layers / g_inter;
-  c->layer0 = c->stage * c->nl;
+  if (opt->stage_balance) {
+    const std::vector<int> bb = balanced_blocks(model, g_inter);   // block boundaries
+    const int b0 = bb[c->stage], b1 = bb[c->stage + 1];            // blocks [b0, b1)
+    c->layer0 = b0 / 2;
+    c->nl = (b1 + 1) / 2 - b0 / 2;
+    for (int li = 0; li < c->nl; ++li) {
+      const int L = c->layer0 + li;
+      c->lhalf.push_back(((2 * L >= b0 && 2 * L < b1) ? 1 : 0) | ((2 * L + 1 >= b0 && 2 * L + 1 < b1) ? 2 : 0));
+    }
+  } else {
+    c->nl = model->n_layers / g_inter;
+    c->layer0 = c->stage * c->nl;
+    c->lhalf.assign(c->nl, 3);
+  }
   c->h = model->hidden; c->heads = model->heads; c->d = d; c->s = model->seq_len;
   c->V = model->vocab; c->M = microbatch * model->seq_len;
   c->dp = (d + 7) / 8 * 8;            // e.g. 12B: d = 188 -> 192 (D-7: scale stays 1/sqrt(188))

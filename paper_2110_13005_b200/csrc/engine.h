@@ -79,6 +79,9 @@ struct Ctx {
   int64_t nflat = 0;
   int64_t tok_emb = -1, pos_emb = -1, lnf_g = -1, lnf_b = -1, head_w = -1;
   std::vector<LayerOff> loff;
+  // per local layer: bit 0 its attention block, bit 1 its MLP block lives on this stage (3 =
+  // whole layer; a balanced split, stage_balance, may cut a layer after its attention block)
+  std::vector<int> lhalf;
   void* theta16 = nullptr;            // bf16 [nflat]
   float* grad32 = nullptr;            // fp32 accumulation (D-20)
   void* grad16 = nullptr;             // bf16 all-reduce / optimizer input
@@ -214,13 +217,16 @@ struct Ctx {
   int ac = 1;
   std::vector<LayerStash> ck;
   LayerStash& stash(Slot& sl, int li) { return ac > 1 ? ck[li % ac] : sl.L[li]; }
+  // output of local layer li: x1 when the stage ends after the layer's attention block
+  const void* layer_out(const LayerStash& st, int li) const { return (lhalf[li] & 2) ? st.out : st.x1; }
   const void* stage_out(const Slot& sl) const {
     if (ac > 1) return sl.seg[nl / ac];
-    return nl > 0 ? sl.L[nl - 1].out : sl.in;
+    return nl > 0 ? layer_out(sl.L[nl - 1], nl - 1) : sl.in;
   }
-  int64_t layer_end(int li) const {   // one past the last flat element of layer li
-    return loff[li].b_fc2 + ((int64_t)h + 63) / 64 * 64;
+  int64_t layer_end(int li) const {   // one past the last flat element of layer li on this stage
+    return ((lhalf[li] & 2) ? loff[li].b_fc2 : loff[li].b_o) + ((int64_t)h + 63) / 64 * 64;
   }
+  int64_t layer_begin(int li) const { return (lhalf[li] & 1) ? loff[li].ln1_g : loff[li].ln2_g; }
   int layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void* din);
   void wg_fork();                       // s_wg waits for everything enqueued on s_comp so far
   void wg_note(const void* buf);        // s_wg reads buf (recorded after its last enqueued read)

@@ -154,6 +154,8 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
   const LayerOff& o = loff[li];
   const int b = microbatch;
   const double dM = M, dh = h;
+  const int hm = lhalf[li];   // attention block (bit 0) and / or MLP block (bit 1) on this stage
+  if (hm & 1) {
   KCHK(ln_fwd(x, M, h, p16(o.ln1_g), p16(o.ln1_b), st.u, st.mean1, st.rstd1, s_comp));
   {
     GemmArgs g = lin_fwd(st.u, p16(o.w_qkv), M, 3 * h, h, st.qkv);
@@ -201,7 +203,10 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
     g.resid = x; g.ld_resid = h;
     TRY(gemm(g, 2 * dM * dh * dh));
   }
-  KCHK(ln_fwd(st.x1, M, h, p16(o.ln2_g), p16(o.ln2_b), st.w, st.mean2, st.rstd2, s_comp));
+  }   // attention block
+  if (!(hm & 2)) return 0;
+  const void* x1 = (hm & 1) ? st.x1 : x;   // a stage starting at the MLP block receives x1
+  KCHK(ln_fwd(x1, M, h, p16(o.ln2_g), p16(o.ln2_b), st.w, st.mean2, st.rstd2, s_comp));
   {
     GemmArgs g = lin_fwd(st.w, p16(o.w_fc1), M, 4 * h, h, st.act);
     g.bias = p16(o.b_fc1);
@@ -211,7 +216,7 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
   {
     GemmArgs g = lin_fwd(st.act, p16(o.w_fc2), M, h, 4 * h, st.out);
     g.bias = p16(o.b_fc2);
-    g.resid = st.x1; g.ld_resid = h;
+    g.resid = x1; g.ld_resid = h;
     TRY(gemm(g, 2 * dM * 4 * dh * dh));
   }
   return 0;
@@ -225,6 +230,12 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   // Weight gradients (dW GEMM + bias column sum) go to s_wg, concurrent with the
   // data-gradient chain on s_comp; wg_guard() orders any later overwrite of a buffer
   // s_wg still reads.
+  const int hm = lhalf[li];
+  // gradient w.r.t. x1: from the MLP block, or (stage cut after the attention block) dout
+  const void* gx1 = dout;
+  if (hm & 2) {
+  const void* x1 = (hm & 1) ? st.x1 : x;
+  void* dx1o = (hm & 1) ? dx1 : din;   // MLP-only layer: dx1 is the stage's input gradient
   // FC2: dpre = (dout W2) * GeLU'(pre);  dW2 += dout^T act;  db2 += colsum(dout)
   wg_fork();
   gst = wgs();
@@ -247,18 +258,21 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   wg_note(dpre);
   TRY(gemm(lin_dgrad(dpre, p16(o.w_fc1), M, 4 * h, h, du), 2 * dM * 4 * dh * dh));
   // LN2: dx1 = dout + LN2'(du);  dg2, db2
-  wg_guard(dx1);
-  KCHK(ln_bwd(du, st.x1, st.mean2, st.rstd2, M, h, p16(o.ln2_g), dout, dx1, s_comp));
-  KCHK(colsum(du, st.x1, st.mean2, st.rstd2, M, h, cs_ws_ln, g32(o.ln2_b), g32(o.ln2_g), acc, s_comp));
+  wg_guard(dx1o);
+  KCHK(ln_bwd(du, x1, st.mean2, st.rstd2, M, h, p16(o.ln2_g), dout, dx1o, s_comp));
+  KCHK(colsum(du, x1, st.mean2, st.rstd2, M, h, cs_ws_ln, g32(o.ln2_b), g32(o.ln2_g), acc, s_comp));
+  gx1 = dx1o;
+  }   // MLP block
+  if (!(hm & 1)) return 0;
   // proj: dO = dx1 Wo;  dWo += dx1^T o;  dbo += colsum(dx1)
   wg_fork();
   gst = wgs();
-  TRY(gemm(lin_wgrad(dx1, st.o, M, h, h, g32(o.w_o), acc), 2 * dM * dh * dh));
+  TRY(gemm(lin_wgrad(gx1, st.o, M, h, h, g32(o.w_o), acc), 2 * dM * dh * dh));
   gst = s_comp;
-  KCHK(colsum(dx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, wgs()));
-  wg_note(dx1);
+  KCHK(colsum(gx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, wgs()));
+  wg_note(gx1);
   {
-    GemmArgs g = lin_dgrad(dx1, p16(o.w_o), M, h, h, dO);
+    GemmArgs g = lin_dgrad(gx1, p16(o.w_o), M, h, h, dO);
     g.ldc = (long long)heads * dp;   // dO per head, padded like q/k/v
     if (dp != d) { g.col_group_in = d; g.col_group_out = dp; }
     TRY(gemm(g, 2 * dM * dh * dh));
@@ -333,7 +347,7 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   TRY(gemm(lin_dgrad(dqkv, p16(o.w_qkv), M, 3 * h, h, du), 2 * dM * 3 * dh * dh));
   // LN1: din = dx1 + LN1'(du)   (din is the buffer the layer above read as dout)
   wg_guard(din);
-  KCHK(ln_bwd(du, x, st.mean1, st.rstd1, M, h, p16(o.ln1_g), dx1, din, s_comp));
+  KCHK(ln_bwd(du, x, st.mean1, st.rstd1, M, h, p16(o.ln1_g), gx1, din, s_comp));
   KCHK(colsum(du, x, st.mean1, st.rstd1, M, h, cs_ws_ln, g32(o.ln1_b), g32(o.ln1_g), acc, s_comp));
   return 0;
 }
@@ -370,7 +384,7 @@ int Ctx::forward_impl(Slot& sl, int mb) {
       x = st.out;
     } else {
       TRY(layer_fwd(li, x, sl.L[li]));
-      x = sl.L[li].out;
+      x = layer_out(sl.L[li], li);
     }
   }
   if (!last) return 0;
@@ -430,11 +444,11 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
       }
       x = li % ac == 0 ? sl.seg[sg] : stash(sl, li - 1).out;
     } else {
-      x = li > 0 ? sl.L[li - 1].out : sl.in;
+      x = li > 0 ? layer_out(sl.L[li - 1], li - 1) : sl.in;
     }
     void* din = (li == 0 && !first) ? sl.gsend : nxt;
     TRY(layer_bwd(li, x, stash(sl, li), cur, din));
-    if (ar_last && !(first && li == 0)) TRY(ar_ready(loff[li].ln1_g));
+    if (ar_last && !(first && li == 0)) TRY(ar_ready(layer_begin(li)));
     if (li == 0 && !first) {
       cur = din;
     } else {

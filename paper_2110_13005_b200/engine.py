@@ -40,6 +40,7 @@ class AxoNN:
                  weight_decay: float = 0.01, loss_scale: float = 1.0, offload: bool = False,
                  bucket_elems: int = 4_000_000, coarsen_k: int = 4, pipeline_limit: int = 0,
                  overlap_next_batch: bool | None = None, checkpoint_interval: int = 0,
+                 stage_balance: bool = False,
                  rank: int = 0, world_size: int = 1, device: int = 0, nccl_id: bytes | None = None,
                  dtype: str = "bf16"):
         # the half format picks the library build (include/axonn.h axonn_dtype)
@@ -50,7 +51,8 @@ class AxoNN:
                               bucket_elems, coarsen_k, pipeline_limit, checkpoint_interval,
                               # default: overlap when the optimizer is host-link bound (offload);
                               # in HBM the AdamW kernels only compete with the GEMMs for SMs
-                              int(offload if overlap_next_batch is None else overlap_next_batch))
+                              int(offload if overlap_next_batch is None else overlap_next_batch),
+                              int(stage_balance))
         self._id = C.create_string_buffer(nccl_id if nccl_id else b"\0" * 128, 128)
         self.dist = _lib.Dist(rank, world_size, C.cast(self._id, C.c_void_p), device)
         self.ctx = C.c_void_p()

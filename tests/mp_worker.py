@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--loss-scale", type=float, default=1.0)
     ap.add_argument("--inf-rank", type=int, default=-1,
                     help="after step 0's run_batch this rank writes one inf gradient (D-12 skip)")
+    ap.add_argument("--balance", action="store_true", help="stage_balance (reading D-21b)")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     import torch
@@ -34,7 +35,9 @@ def main():
     from synth import init_params, markov_tokens
     cfgs = {"tiny": dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256),
             "tiny4": dict(n_layers=4, hidden=64, heads=2, seq_len=32, vocab=256),
-            "mini": dict(n_layers=4, hidden=256, heads=4, seq_len=128, vocab=1024)}
+            "mini": dict(n_layers=4, hidden=256, heads=4, seq_len=128, vocab=1024),
+            "tinyv": dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=1024),
+            "tiny4v": dict(n_layers=4, hidden=64, heads=2, seq_len=32, vocab=2048)}
     cfg = cfgs[a.cfg]
     rank, world, local = D.env_rank_world()
     if "AXONN_WATCHDOG_S" in os.environ:   # stagger so every rank reports its own state
@@ -44,7 +47,7 @@ def main():
     nid = D.share_unique_id(rank, world, D.nccl_unique_id)
     eng = AxoNN(a.g_inter, a.g_data, a.mb, **cfg, rank=rank, world_size=world, device=local,
                 nccl_id=nid, offload=bool(a.offload), bucket_elems=5000, coarsen_k=2,
-                dtype=a.dtype, loss_scale=a.loss_scale)
+                dtype=a.dtype, loss_scale=a.loss_scale, stage_balance=a.balance)
     params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=42)
     names = [n for n, _, _ in eng.tensors()]
     eng.write_all(T_MASTER, {n: params[n] for n in names})

@@ -17,7 +17,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CFGS = {"tiny": dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256),
         "tiny4": dict(n_layers=4, hidden=64, heads=2, seq_len=32, vocab=256),
-        "mini": dict(n_layers=4, hidden=256, heads=4, seq_len=128, vocab=1024)}
+        "mini": dict(n_layers=4, hidden=256, heads=4, seq_len=128, vocab=1024),
+        "tinyv": dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=1024),
+        "tiny4v": dict(n_layers=4, hidden=64, heads=2, seq_len=32, vocab=2048)}
 
 
 def free_port():
@@ -159,3 +161,22 @@ def test_nccl_and_peer_copy_links_agree_bitwise(tmp_path):
     for r0, r1 in zip(*res):
         for k in r0:
             assert np.array_equal(r0[k], r1[k]), k
+
+
+@pytest.mark.multigpu(2)
+def test_two_gpus_balanced_split(tmp_path):
+    """Reading D-21b (stage_balance): with an LM head heavier than a layer the stage boundary
+    falls after layer 1's attention block — stage 0 owns l1's attention tensors, stage 1 its
+    MLP tensors, the message is x1 — and the result still matches the plain full-batch oracle
+    (2 steps)."""
+    res = launch(tmp_path, 2, 1, "tinyv", 2, 8, steps=2, extra=("--balance",))
+    assert "g16.l1.w_qkv" in res[0] and "g16.l1.w_fc1" not in res[0]
+    assert "g16.l1.w_fc1" in res[1] and "g16.l1.w_qkv" not in res[1]
+    check(res, 2, 1, "tinyv", 8)
+
+
+@pytest.mark.multigpu(4)
+@pytest.mark.parametrize("gi,gd,cfg", [(4, 1, "tiny4v"), (2, 2, "tinyv")])
+def test_four_gpus_balanced_split(tmp_path, gi, gd, cfg):
+    res = launch(tmp_path, gi, gd, cfg, 2, 8 * gd, extra=("--balance",))
+    check(res, gi, gd, cfg, 8 * gd)
