@@ -228,8 +228,9 @@ def main():
                     help="activation checkpointing ac (PAPER.md:553-576): 0 off, -1 the paper's rule")
     ap.add_argument("--overlap-next-batch", type=int, default=None,
                     help="1/0: optimizer step t overlaps batch t+1 (default: on with offload only)")
-    ap.add_argument("--stage-balance", type=int, default=0,
-                    help="1: half-layer stage boundaries balancing the LM head (reading D-21b)")
+    ap.add_argument("--stage-balance", type=int, default=None,
+                    help="1: half-layer stage boundaries balancing the LM head (reading D-21b); "
+                         "default on unless activation checkpointing is requested")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"],
                     help="half format (library build); fp16 runs with a static loss scale (D-11)")
     ap.add_argument("--loss-scale", type=float, default=None,
@@ -237,6 +238,8 @@ def main():
     ap.add_argument("--g-inter", type=int, default=None,
                     help="pipeline stages (pipeline configs; G_data = N / G_inter)")
     args = ap.parse_args()
+    if args.stage_balance is None:
+        args.stage_balance = int(args.checkpoint_interval in (0, 1))
     cfg = dict(CONFIGS[args.config])
     if args.layers:
         cfg["n_layers"] = args.layers
