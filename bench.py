@@ -305,10 +305,15 @@ def main():
         losses = []
         for step in range(args.steps):
             prof = step == args.steps - 1
+            nvtx = prof and os.environ.get("AXONN_NVTX") == "1"   # ncu --nvtx-include timed_step/
             if prof:
                 eng.set_profiling(True)
+            if nvtx:
+                torch.cuda.nvtx.range_push("timed_step")
             losses.append(eng.run_batch_device(d_tok.data_ptr(), B))
             eng.optimizer_step()
+            if nvtx:
+                torch.cuda.nvtx.range_pop()
             st = eng.stats()
             launches += int(st["kernel_launches"])
             for k in ph:

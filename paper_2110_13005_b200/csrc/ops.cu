@@ -187,7 +187,23 @@ int embed_bwd(const int32_t* tok, long long tok_ld, int b, int s, int h, int voc
 }
 
 // ------------------------------------------------------------------ LayerNorm
-// y = (x - mean) * rstd * g + b, two-pass statistics in fp32 (D-6).  Warp per row.
+// raw 16-byte row chunk (8 halves) and its conversion, so a pass keeps LN_U chunks of every
+// operand in flight as packed registers (4 per chunk) and converts only in the math
+__device__ __forceinline__ uint4 ldraw(const hx* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ void cvt8(const uint4& u, float (&f)[8]) {
+  const hx2* h2 = reinterpret_cast<const hx2*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = hx22f2(h2[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+// y = (x - mean) * rstd * g + b, two-pass statistics in fp32 (D-6).  Warp per row; every
+// pass walks the row LN_U 16-byte chunks per lane at a time with all loads issued first
+// (memory-level parallelism of a latency-bound warp-per-row kernel).
+constexpr int LN_U = 4;
 __global__ void ln_fwd_kernel(const hx* __restrict__ x, int rows, int h,
                               const hx* __restrict__ g, const hx* __restrict__ bta,
                               hx* __restrict__ y, float* __restrict__ mean_out,
@@ -197,33 +213,58 @@ __global__ void ln_fwd_kernel(const hx* __restrict__ x, int rows, int h,
   const int lane = threadIdx.x % 32;
   const hx* xr = x + (long long)row * h;
   float s = 0.f;
-  for (int c = lane * 8; c < h; c += 256) {
-    float f[8];
-    load8(xr + c, f);
+  for (int c0 = lane * 8; c0 < h; c0 += 256 * LN_U) {
+    uint4 r[LN_U];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) s += f[i];
+    for (int u = 0; u < LN_U; ++u) r[u] = c0 + 256 * u < h ? ldraw(xr + c0 + 256 * u) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < LN_U; ++u) {
+      float f[8];
+      cvt8(r[u], f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += f[i];
+    }
   }
   const float mean = warp_sum(s) / h;
   float v = 0.f;
-  for (int c = lane * 8; c < h; c += 256) {
-    float f[8];
-    load8(xr + c, f);
+  for (int c0 = lane * 8; c0 < h; c0 += 256 * LN_U) {
+    uint4 r[LN_U];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float d = f[i] - mean;
-      v += d * d;
+    for (int u = 0; u < LN_U; ++u) r[u] = c0 + 256 * u < h ? ldraw(xr + c0 + 256 * u) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < LN_U; ++u) {
+      if (c0 + 256 * u >= h) continue;
+      float f[8];
+      cvt8(r[u], f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float d = f[i] - mean;
+        v += d * d;
+      }
     }
   }
   const float rstd = rsqrtf(warp_sum(v) / h + 1e-5f);
   hx* yr = y + (long long)row * h;
-  for (int c = lane * 8; c < h; c += 256) {
-    float f[8], gg[8], bb[8];
-    load8(xr + c, f);
-    load8(g + c, gg);
-    load8(bta + c, bb);
+  for (int c0 = lane * 8; c0 < h; c0 += 256 * LN_U) {
+    uint4 rx[LN_U], rg[LN_U], rb[LN_U];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) f[i] = (f[i] - mean) * rstd * gg[i] + bb[i];
-    store8(yr + c, f);
+    for (int u = 0; u < LN_U; ++u)
+      if (c0 + 256 * u < h) {
+        rx[u] = ldraw(xr + c0 + 256 * u);
+        rg[u] = ldraw(g + c0 + 256 * u);
+        rb[u] = ldraw(bta + c0 + 256 * u);
+      }
+#pragma unroll
+    for (int u = 0; u < LN_U; ++u)
+      if (c0 + 256 * u < h) {
+        float f[8], gg[8], bb[8];
+        cvt8(rx[u], f);
+        cvt8(rg[u], gg);
+        cvt8(rb[u], bb);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = (f[i] - mean) * rstd * gg[i] + bb[i];
+        store8(yr + c0 + 256 * u, f);
+      }
   }
   if (lane == 0) {
     mean_out[row] = mean;
@@ -251,36 +292,66 @@ __global__ void ln_bwd_kernel(const hx* __restrict__ dy, const hx* __restrict__ 
   const hx* xr = x + (long long)row * h;
   const hx* dyr = dy + (long long)row * h;
   float s1 = 0.f, s2 = 0.f;
-  for (int c = lane * 8; c < h; c += 256) {
-    float xf[8], df[8], gf[8];
-    load8(xr + c, xf);
-    load8(dyr + c, df);
-    load8(g + c, gf);
+  for (int c0 = lane * 8; c0 < h; c0 += 256 * LN_U) {
+    uint4 rx[LN_U], rd[LN_U], rg[LN_U];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float dxh = df[i] * gf[i];
-      float xh = (xf[i] - mu) * rs;
-      s1 += dxh;
-      s2 += dxh * xh;
+    for (int u = 0; u < LN_U; ++u) {
+      const int c = c0 + 256 * u;
+      if (c < h) {
+        rx[u] = ldraw(xr + c);
+        rd[u] = ldraw(dyr + c);
+        rg[u] = ldraw(g + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < LN_U; ++u) {
+      if (c0 + 256 * u >= h) continue;
+      float xf[8], df[8], gf[8];
+      cvt8(rx[u], xf);
+      cvt8(rd[u], df);
+      cvt8(rg[u], gf);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float dxh = df[i] * gf[i];
+        float xh = (xf[i] - mu) * rs;
+        s1 += dxh;
+        s2 += dxh * xh;
+      }
     }
   }
   s1 = warp_sum(s1) / h;
   s2 = warp_sum(s2) / h;
   hx* o = dx + (long long)row * h;
   const hx* rr = dres ? dres + (long long)row * h : nullptr;
-  for (int c = lane * 8; c < h; c += 256) {
-    float xf[8], df[8], gf[8], rf[8];
-    load8(xr + c, xf);
-    load8(dyr + c, df);
-    load8(g + c, gf);
-    if (rr) load8(rr + c, rf);
+  for (int c0 = lane * 8; c0 < h; c0 += 256 * LN_U) {
+    uint4 rx[LN_U], rd[LN_U], rg[LN_U], rres[LN_U];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float xh = (xf[i] - mu) * rs;
-      float v = rs * (df[i] * gf[i] - s1 - xh * s2);
-      rf[i] = rr ? rf[i] + v : v;
+    for (int u = 0; u < LN_U; ++u) {
+      const int c = c0 + 256 * u;
+      if (c < h) {
+        rx[u] = ldraw(xr + c);
+        rd[u] = ldraw(dyr + c);
+        rg[u] = ldraw(g + c);
+        rres[u] = rr ? ldraw(rr + c) : make_uint4(0, 0, 0, 0);
+      }
     }
-    store8(o + c, rf);
+#pragma unroll
+    for (int u = 0; u < LN_U; ++u) {
+      const int c = c0 + 256 * u;
+      if (c < h) {
+        float xf[8], df[8], gf[8], rf[8];
+        cvt8(rx[u], xf);
+        cvt8(rd[u], df);
+        cvt8(rg[u], gf);
+        cvt8(rres[u], rf);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float xh = (xf[i] - mu) * rs;
+          rf[i] += rs * (df[i] * gf[i] - s1 - xh * s2);
+        }
+        store8(o + c, rf);
+      }
+    }
   }
 }
 

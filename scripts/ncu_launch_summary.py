@@ -2,6 +2,8 @@
 `bench.py --steps 1 --warmup 1 --e2e-steps 1` (G_inter 1): keep the launches of the timed step
 (from the (m+1)-th to just before the (2m+1)-th embed_fwd launch, m = microbatches per step),
 write them to OUT.csv and a per-kernel share summary to OUT.json.
+m = 0: the log already holds only the timed step (bench.py with AXONN_NVTX=1 under
+ncu --nvtx --nvtx-include timed_step/).
 Usage: python scripts/ncu_launch_summary.py LOG.csv OUT_PREFIX [m]"""
 import csv
 import io
@@ -28,11 +30,14 @@ def main(log, out, m=8):
             continue
         v = float(r[col["Metric Value"]].replace(",", ""))
         unit = r[col["Metric Unit"]]
-        us = v / 1e3 if unit == "nsecond" else v * 1e3 if unit == "msecond" else v
+        us = v / 1e3 if unit in ("nsecond", "ns") else v * 1e3 if unit in ("msecond", "ms") else v
         launches.append((int(r[col["ID"]]), r[col["Kernel Name"]], us))
-    emb = [i for i, (_, n, _) in enumerate(launches) if "embed_fwd" in n]
-    lo, hi = emb[m], emb[2 * m] if len(emb) > 2 * m else len(launches)
-    step = launches[lo:hi]
+    if m == 0:   # the log holds only the timed step (ncu --nvtx-include timed_step/)
+        step = launches
+    else:
+        emb = [i for i, (_, n, _) in enumerate(launches) if "embed_fwd" in n]
+        lo, hi = emb[m], emb[2 * m] if len(emb) > 2 * m else len(launches)
+        step = launches[lo:hi]
     total = sum(t for _, _, t in step)
     by = {}
     for _, n, t in step:
