@@ -277,7 +277,8 @@ AXONN_API int axonn_k_attn_fwd(const void* qkv, int64_t lq, int b, int heads, in
  * [b*s][ldq]): dQ at columns [n*d, ...), dK at h + n*d, dV at 2h + n*d (h = heads*d), with
  * dS = alpha * P * (dP - D), D_i = dO_i . o_i.  P is recomputed from S and lse (never stored);
  * every output element has one writer (no atomics: bitwise reproducible).  dbuf: fp32
- * workspace of b*heads*s elements (receives D).  Same limits as axonn_k_attn_fwd. */
+ * workspace of b*heads*s elements (receives D).  Same limits as axonn_k_attn_fwd, and
+ * s % 4 == 0 (D is written 4 rows per 16-byte store); else returns -1. */
 AXONN_API int axonn_k_attn_bwd(const void* qkv, int64_t lq, const void* dO, const void* o, int64_t ldo,
                                const float* lse, float* dbuf, int b, int heads, int s, int d, int dp,
                                float alpha, void* dqkv, int64_t ldq, void* stream);

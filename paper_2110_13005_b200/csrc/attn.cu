@@ -739,25 +739,31 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 // D[z * s + i] = sum_j dO[i, head, j] * O[i, head * d + j]   (fp32); 16 lanes per (token, head),
 // DITEMS (token, head) items per 16-lane group with every load issued before the math
 constexpr int DITEMS = 4;
+// Group g of 16 lanes handles DITEMS = 4 consecutive query rows i..i+3 of one (sample, head)
+// z: g = z * (s / 4) + i / 4.  Lane l holds 8 (or 4) head-dim columns of each row; after the
+// 16-lane reduction lane 0 writes the 4 results as one 16-byte store D[z * s + i .. + 3].
 __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, int dp,
                                   const hx* __restrict__ O, long long ld_o, int d,
                                   int s, int heads, long long ntok, float* __restrict__ D) {
   const long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 16;
   const int l = threadIdx.x & 15;
-  const long long nitems = ntok * heads;
+  const long long ngrp = ntok * heads / DITEMS;
+  const bool live = grp < ngrp;
+  const long long z = live ? grp / (s / DITEMS) : 0;
+  const int i0 = live ? (int)(grp % (s / DITEMS)) * DITEMS : 0;
+  const long long sample = z / heads;
+  const int hd = (int)(z % heads);
+  const long long tok0 = sample * s + i0;
   float acc[DITEMS];
   if ((d & 7) == 0 && (dp & 7) == 0 && d <= 128) {
     uint4 x[DITEMS], y[DITEMS];
 #pragma unroll
     for (int u = 0; u < DITEMS; ++u) {
-      const long long w = grp * DITEMS + u;
       const int j = 8 * l;
       x[u] = y[u] = make_uint4(0, 0, 0, 0);
-      if (w < nitems && j < d) {
-        const long long tok = w / heads;
-        const int hd = (int)(w % heads);
-        x[u] = __ldg(reinterpret_cast<const uint4*>(dO + tok * ld_do + (long long)hd * dp + j));
-        y[u] = __ldg(reinterpret_cast<const uint4*>(O + tok * ld_o + (long long)hd * d + j));
+      if (live && j < d) {
+        x[u] = __ldg(reinterpret_cast<const uint4*>(dO + (tok0 + u) * ld_do + (long long)hd * dp + j));
+        y[u] = __ldg(reinterpret_cast<const uint4*>(O + (tok0 + u) * ld_o + (long long)hd * d + j));
       }
     }
 #pragma unroll
@@ -774,20 +780,17 @@ __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, in
     }
   } else if ((d & 3) == 0 && (dp & 3) == 0 && (ld_o & 3) == 0 && (ld_do & 3) == 0 && d <= 256) {
     // head width a multiple of 4 but not 8 (d = 188, 176): 8-byte loads, every load of the
-    // DITEMS items issued before the math (16 lanes x 4 elements = 64 per pass, <= 4 passes)
+    // DITEMS rows issued before the math (16 lanes x 4 elements = 64 per pass, <= 4 passes)
     uint2 x[DITEMS][4], y[DITEMS][4];
 #pragma unroll
     for (int u = 0; u < DITEMS; ++u) {
-      const long long w = grp * DITEMS + u;
-      const long long tok = w / heads;
-      const int hd = (int)(w % heads);
 #pragma unroll
       for (int ps = 0; ps < 4; ++ps) {
         const int j = 4 * l + 64 * ps;
         x[u][ps] = y[u][ps] = make_uint2(0, 0);
-        if (w < nitems && j < d) {
-          x[u][ps] = __ldg(reinterpret_cast<const uint2*>(dO + tok * ld_do + (long long)hd * dp + j));
-          y[u][ps] = __ldg(reinterpret_cast<const uint2*>(O + tok * ld_o + (long long)hd * d + j));
+        if (live && j < d) {
+          x[u][ps] = __ldg(reinterpret_cast<const uint2*>(dO + (tok0 + u) * ld_do + (long long)hd * dp + j));
+          y[u][ps] = __ldg(reinterpret_cast<const uint2*>(O + (tok0 + u) * ld_o + (long long)hd * d + j));
         }
       }
     }
@@ -809,13 +812,10 @@ __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, in
   } else {
 #pragma unroll
     for (int u = 0; u < DITEMS; ++u) {
-      const long long w = grp * DITEMS + u;
       float a = 0.f;
-      if (w < nitems) {
-        const long long tok = w / heads;
-        const int hd = (int)(w % heads);
-        const hx* xa = dO + tok * ld_do + (long long)hd * dp;
-        const hx* ya = O + tok * ld_o + (long long)hd * d;
+      if (live) {
+        const hx* xa = dO + (tok0 + u) * ld_do + (long long)hd * dp;
+        const hx* ya = O + (tok0 + u) * ld_o + (long long)hd * d;
         for (int j = 2 * l; j < d; j += 32) {
           const float2 xf = hx22f2(*reinterpret_cast<const hx2*>(xa + j));
           const float2 yf = hx22f2(*reinterpret_cast<const hx2*>(ya + j));
@@ -830,14 +830,10 @@ __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, in
     float a = acc[u];
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    const long long w = grp * DITEMS + u;
-    if (l == 0 && w < nitems) {
-      const long long tok = w / heads;
-      const int hd = (int)(w % heads);
-      const long long sample = tok / s, i = tok % s;
-      D[(sample * heads + hd) * s + i] = a;
-    }
+    acc[u] = a;
   }
+  if (l == 0 && live)
+    *reinterpret_cast<float4*>(D + z * s + i0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
 }
 
 }  // namespace
@@ -884,7 +880,7 @@ int attn_fwd(const void* qkv, long long lq, int b, int heads, int s, int d, int 
 int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long long ldo,
              const float* lse, float* Dbuf, int b, int heads, int s, int d, int dp, float alpha,
              void* dqkv, long long ldq, cudaStream_t st) {
-  if (s <= 0 || s > 512 || d <= 0 || dp < d || dp % 2 || (d & 1) || (ldq & 1)) return -1;
+  if (s <= 0 || s > 512 || s % 4 || d <= 0 || dp < d || dp % 2 || (d & 1) || (ldq & 1)) return -1;
   const int nv = (dp + 63) / 64 * 64;
   if (nv > 256) return -1;
   const long long ntok = (long long)b * s;
