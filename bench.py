@@ -228,6 +228,8 @@ def main():
                     help="activation checkpointing ac (PAPER.md:553-576): 0 off, -1 the paper's rule")
     ap.add_argument("--overlap-next-batch", type=int, default=None,
                     help="1/0: optimizer step t overlaps batch t+1 (default: on with offload only)")
+    ap.add_argument("--pipeline-limit", type=int, default=0,
+                    help="microbatches in flight per pipeline (0: G_inter, PAPER.md:467-470)")
     ap.add_argument("--stage-balance", type=int, default=None,
                     help="1: half-layer stage boundaries balancing the LM head (reading D-21b); "
                          "default on unless activation checkpointing is requested")
@@ -272,7 +274,7 @@ def main():
                 heads=cfg["heads"], seq_len=cfg["seq_len"], vocab=cfg["vocab"], init_seed=42,
                 offload=cfg["offload"], rank=rank, world_size=world, device=local, nccl_id=nid,
                 checkpoint_interval=args.checkpoint_interval, dtype=args.dtype,
-                stage_balance=bool(args.stage_balance),
+                stage_balance=bool(args.stage_balance), pipeline_limit=args.pipeline_limit,
                 overlap_next_batch=None if args.overlap_next_batch is None else bool(args.overlap_next_batch),
                 loss_scale=args.loss_scale or (1024.0 if args.dtype == "fp16" else 1.0))
     from synth import uniform_tokens
@@ -335,7 +337,8 @@ def main():
     eng.set_profiling(False)
     dev_ms = D.max_over_ranks(dev_ms, world)
     bubble = 1.0 - ph["t_busy_ms"] / ph["t_pipe_ms"] if ph["t_pipe_ms"] > 0 else 0.0
-    bubble_max = D.max_over_ranks(bubble, world)   # every rank joins the collective
+    bubble_ranks = D.gather_to_all(bubble, world)   # every rank joins the collective
+    bubble_max = max(bubble_ranks)
     ms_step = dev_ms / args.steps
     fl = model_flops(B, s, cfg["n_layers"], cfg["hidden"], V)
     value = fl / (ms_step / 1e3) / 1e12                       # whole-job model TFLOP/s
@@ -377,7 +380,7 @@ def main():
                        "microbatch": b_m, "microbatches_per_replica": m,
                        "parallelism": f"G_inter{g_inter} x G_data{g_data}",
                        "offload": cfg["offload"], "checkpoint_interval": args.checkpoint_interval,
-                       "stage_balance": args.stage_balance,
+                       "stage_balance": args.stage_balance, "pipeline_limit": args.pipeline_limit,
                        "l2": "inputs larger than L2 (GBs of weights/activations per step)"},
             "per_gpu_tflops": value / world,
             "device_mem_gib": torch.cuda.mem_get_info()[1] / 2**30 - torch.cuda.mem_get_info()[0] / 2**30,
@@ -392,6 +395,7 @@ def main():
             # column all-reduce after it, optimizer time after the all-reduce
             "phases": {"pipeline_ms": ph["t_pipe_ms"], "compute_busy_ms": ph["t_busy_ms"],
                        "bubble_frac": bubble, "bubble_frac_max_over_ranks": bubble_max,
+                       "bubble_frac_per_rank": bubble_ranks,
                        "predicted_bubble_frac": (g_inter - 1) / (m + g_inter - 1),
                        "allreduce_exposed_ms": ph["t_allreduce_ms"],
                        "optimizer_exposed_ms": ph["t_opt_exposed_ms"],

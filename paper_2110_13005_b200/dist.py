@@ -88,6 +88,17 @@ def max_over_ranks(value: float, world: int) -> float:
     return float(t.item())
 
 
+def gather_to_all(value: float, world: int) -> list[float]:
+    """Every rank's value, in rank order (gloo all_gather)."""
+    if world == 1:
+        return [value]
+    import torch
+    import torch.distributed as dist
+    out = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(out, torch.tensor([value], dtype=torch.float64))
+    return [float(t.item()) for t in out]
+
+
 def barrier(world: int):
     if world > 1:
         import torch.distributed as dist

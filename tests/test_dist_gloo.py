@@ -61,6 +61,7 @@ def _worker(rank, world, port, q):
     flat = torch.tensor(np.concatenate([grads[k].ravel() for k in sorted(grads)] + [[loss]]))
     dist.all_reduce(flat)                      # Alg. 1 l.13 SUM
     t = D.max_over_ranks(float(rank + 1), world)
+    t = (t, D.gather_to_all(10.0 * rank + 0.5, world))
     q.put((rank, nid, flat.numpy(), t))
     dist.barrier()
     dist.destroy_process_group()
@@ -81,7 +82,8 @@ def test_two_process_data_parallel_gloo():
         pr.join(timeout=60)
         assert pr.exitcode == 0
     assert out[0][1] == out[1][1] == bytes(range(128))   # rank 0's id reached rank 1
-    assert out[0][3] == out[1][3] == 2.0                 # max over ranks
+    assert out[0][3][0] == out[1][3][0] == 2.0           # max over ranks
+    assert out[0][3][1] == out[1][3][1] == [0.5, 10.5]   # gathered in rank order
     assert np.array_equal(out[0][2], out[1][2])          # both replicas hold the same sum
     cfg = model.GPTConfig(n_layers=2, hidden=32, heads=2, seq_len=16, vocab=64)
     p = {k: v.astype(np.float64) for k, v in init_params(2, 32, 16, 64, seed=42).items()}
