@@ -248,15 +248,20 @@ static int ipc_links(Ctx* c) {
 
 // Reading D-21b (stage_balance): the 2l residual blocks (attention block of layer L = block
 // 2L, its MLP block = 2L + 1) are cut into G_inter contiguous ranges minimising the largest
-// stage cost, cost = forward FLOPs per token: attention block 8h^2 + 2sh (QKV, projection,
-// causal QK^T and PV), MLP block 16h^2, plus the LM head 2hV on the last stage (the embedding
-// gather is negligible).  Exact DP over (stage, boundary); ties go to the earliest boundary.
+// stage cost, cost = forward FLOPs per token weighted by the measured relative speed of the
+// kernels that execute them: attention block 8h^2 + W * 2sh (QKV and projection GEMMs; the
+// causal QK^T and PV of the fused attention kernel, which runs at ~1/4 of the GEMMs' TFLOP/s:
+// W = 4, AXONN_BAL_ATTN_W overrides), MLP block 16h^2, plus the LM head 2hV on the last stage
+// (the embedding gather is negligible).  Exact DP over (stage, boundary); ties go to the
+// earliest boundary.
 // Returns G_inter + 1 boundaries (0 = b_0 < b_1 < ... < b_P = 2l).
 static std::vector<int> balanced_blocks(const axonn_model_cfg* m, int P) {
   const int nb = 2 * m->n_layers;
   const double h = m->hidden, s = m->seq_len, V = m->vocab;
   std::vector<double> pre(nb + 1, 0.0);
-  for (int k = 0; k < nb; ++k) pre[k + 1] = pre[k] + ((k & 1) ? 16 * h * h : 8 * h * h + 2 * s * h);
+  double w_att = 4.0;
+  if (const char* e = getenv("AXONN_BAL_ATTN_W")) w_att = atof(e);
+  for (int k = 0; k < nb; ++k) pre[k + 1] = pre[k] + ((k & 1) ? 16 * h * h : 8 * h * h + w_att * 2 * s * h);
   const double head = 2 * h * V;
   auto cost = [&](int i, int a, int b) { return pre[b] - pre[a] + (i == P - 1 ? head : 0.0); };
   const double INF = 1e300;
@@ -870,6 +875,7 @@ static int run_pipeline(Ctx* c, int m) {
                                          "ncclRecv act");
       if (r) return r;
       if ((r = c->check_cuda(cudaEventRecord(ev_act[mb], c->s_recv_act), "rec"))) return r;
+      c->msg_ev.emplace_back(2 * mb, ev_act[mb]);
     }
     while (!c->last && next_grad_post < m && next_grad_post < done_b + L) {
       int mb = next_grad_post++;
@@ -880,6 +886,7 @@ static int run_pipeline(Ctx* c, int m) {
                                                   c->s_recv_grad), "ncclRecv grad");
       if (r) return r;
       if ((r = c->check_cuda(cudaEventRecord(ev_grad[mb], c->s_recv_grad), "rec"))) return r;
+      c->msg_ev.emplace_back(2 * mb + 1, ev_grad[mb]);
     }
     return 0;
   };
@@ -1063,6 +1070,8 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   for (int k = 0; k < 4; ++k)
     if (!c->ph[par][k]) CU(cudaEventCreate(&c->ph[par][k]));
   c->busy_ev.clear();
+  c->busy_tag.clear();
+  c->msg_ev.clear();
   CU(cudaEventRecord(c->ph[par][0], c->s_comp));
   const int64_t ch_elems = chunk_elems(c);
   c->ar_overlap = c->g_data > 1 && !(getenv("AXONN_AR_OVERLAP") && getenv("AXONN_AR_OVERLAP")[0] == '0');
@@ -1128,6 +1137,24 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
       busy += b;
     }
     c->stats[AXONN_STAT_T_BUSY_MS] = busy;
+    if (const char* tl = getenv("AXONN_TIMELINE")) {   // per-op timeline of this batch (diagnostics)
+      std::string path = std::string(tl) + ".rank" + std::to_string(c->rank) + ".csv";
+      if (FILE* f = fopen(path.c_str(), "w")) {
+        fprintf(f, "stage,kind,mb,start_ms,end_ms\n");
+        for (size_t k = 0; k < c->busy_ev.size() && k < c->busy_tag.size(); ++k) {
+          float a = 0, b = 0;
+          cudaEventElapsedTime(&a, c->ph[par][0], c->busy_ev[k].first);
+          cudaEventElapsedTime(&b, c->ph[par][0], c->busy_ev[k].second);
+          fprintf(f, "%d,%c,%d,%.4f,%.4f\n", c->stage, (c->busy_tag[k] & 1) ? 'B' : 'F', c->busy_tag[k] / 2, a, b);
+        }
+        for (auto& me : c->msg_ev) {
+          float a = 0;
+          if (cudaEventElapsedTime(&a, c->ph[par][0], me.second) == cudaSuccess)
+            fprintf(f, "%d,%s,%d,%.4f,%.4f\n", c->stage, (me.first & 1) ? "msg_grad" : "msg_act", me.first / 2, a, a);
+        }
+        fclose(f);
+      }
+    }
   }
   if (c->opt_pending) {   // the previous step has completed (the cast above waited for it)
     c->opt_pending = false;

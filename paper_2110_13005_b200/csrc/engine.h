@@ -155,6 +155,8 @@ struct Ctx {
   // done, [3] optimizer done; busy spans = (start, end) event pairs around Forward/Backward
   cudaEvent_t ph[2][4] = {};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_ev;
+  std::vector<int> busy_tag;          // 2 mb (+1 for a Backward) per busy span
+  std::vector<std::pair<int, cudaEvent_t>> msg_ev;   // message landed: (2 mb (+1 grad), event)
   void phase_stats_ar_opt(int par);
   // Column all-reduce overlapped with the batch's last backward (G_data > 1, reading D-32):
   // as each layer's gradients become final (reverse layer order = descending flat index) its

@@ -360,6 +360,7 @@ int Ctx::forward(Slot& sl, int mb) {
   const int rc = forward_impl(sl, mb);
   cudaEventRecord(b1, s_comp);
   busy_ev.emplace_back(b0, b1);
+  busy_tag.push_back(2 * mb);
   return rc;
 }
 
@@ -406,6 +407,7 @@ int Ctx::backward(Slot& sl, int mb, const void* dout) {
   const int rc = backward_impl(sl, mb, dout);
   cudaEventRecord(b1, s_comp);
   busy_ev.emplace_back(b0, b1);
+  busy_tag.push_back(2 * mb + 1);
   return rc;
 }
 
