@@ -8,8 +8,11 @@ skipped inside the timed region.
 
 Default workload (N = 1, and weak scaling for N > 1): BASELINE.json
 configs[1], the GPT 1.3B-shaped model (24 layers, hidden 2048, 16 heads,
-seq 512, vocab 51200), G_inter = 1, G_data = N, microbatch 8, 8 microbatches
-per replica (64 samples per GPU), optimizer state in HBM (no offload).
+seq 512, vocab 51200), G_inter = 1, G_data = N, microbatch 32, 2 microbatches
+per replica (64 samples per GPU), optimizer state in HBM (no offload).  At
+G_inter = 1 the microbatch size only trades activation memory for GEMM size
+(b_m 8 / 16 / 32 / 64: 967-973 / 1015 / 1042 / 1053 TFLOP/s, 34 / 41 / 54 / 81
+GiB; profiles/r1/bench_1p3b_mb_sweep_r56.log).
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Under torchrun every rank runs one GPU; rank 0 prints ONE JSON line.
@@ -36,7 +39,7 @@ METRIC = "per-GPU model TFLOP/s and % of B200 bf16 peak at 1/2/4/8 GPUs; batch t
 CONFIGS = {
     # BASELINE.json configs[1]: GPT 1.3B-shaped, G_inter = 1, G_data = N, no offload
     "gpt1.3b": dict(n_layers=24, hidden=2048, heads=16, seq_len=512, vocab=51200,
-                    g_inter=1, microbatch=8, mb_per_replica=8, offload=False),
+                    g_inter=1, microbatch=32, mb_per_replica=2, offload=False),
     # small smoke configuration (BASELINE.json configs[0] shape, single stage)
     "tiny": dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256,
                  g_inter=1, microbatch=2, mb_per_replica=4, offload=False),
@@ -146,12 +149,12 @@ def k1_traffic(cfg):
     """roofline.traffic: DRAM bytes per K1 launch from the committed `ncu --set full` capture of
     one layer's linear-layer GEMMs (profiles/r1/k1_traffic.json, scripts/ncu_traffic.py), beside
     the algorithmic bytes per launch of the same launches (operands read once, outputs written
-    once).  null when no capture matches this model width."""
+    once).  null when no capture matches this model width and microbatch."""
     p = os.path.join(ROOT, "profiles", "r1", "k1_traffic.json")
     if not os.path.exists(p):
         return {"traffic": None}
     d = json.load(open(p))
-    if d.get("hidden") != cfg["hidden"]:
+    if d.get("hidden") != cfg["hidden"] or d.get("tokens") != cfg["microbatch"] * cfg["seq_len"]:
         return {"traffic": None}
     return {"traffic": d["dram_bytes_per_launch_avg"],
             "traffic_algorithmic": d.get("algorithmic_bytes_per_launch_avg"),
@@ -223,6 +226,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--layers", type=int, default=None, help="override n_layers (profiling runs only)")
     ap.add_argument("--mb-per-replica", type=int, default=None, help="microbatches per replica (m)")
+    ap.add_argument("--microbatch", type=int, default=None, help="microbatch size b_m (rows)")
     ap.add_argument("--offload", type=int, default=None, help="1/0: override the config's offload")
     ap.add_argument("--checkpoint-interval", type=int, default=0,
                     help="activation checkpointing ac (PAPER.md:553-576): 0 off, -1 the paper's rule")
@@ -232,6 +236,7 @@ def main():
                     help="microbatches in flight per pipeline (0: G_inter, PAPER.md:467-470)")
     ap.add_argument("--stage-balance", type=int, default=None,
                     help="1: half-layer stage boundaries balancing the LM head (reading D-21b); "
+                         "2: the same, weighted by each stage's measured GPU speed (D-21c); "
                          "default on unless activation checkpointing is requested")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"],
                     help="half format (library build); fp16 runs with a static loss scale (D-11)")
@@ -247,6 +252,8 @@ def main():
         cfg["n_layers"] = args.layers
     if args.mb_per_replica:
         cfg["mb_per_replica"] = args.mb_per_replica
+    if args.microbatch:
+        cfg["microbatch"] = args.microbatch
     if args.offload is not None:
         cfg["offload"] = bool(args.offload)
     if cfg.get("g_inter") == "N":   # pipeline proxies: one stage per GPU unless --g-inter
@@ -274,7 +281,8 @@ def main():
                 heads=cfg["heads"], seq_len=cfg["seq_len"], vocab=cfg["vocab"], init_seed=42,
                 offload=cfg["offload"], rank=rank, world_size=world, device=local, nccl_id=nid,
                 checkpoint_interval=args.checkpoint_interval, dtype=args.dtype,
-                stage_balance=bool(args.stage_balance), pipeline_limit=args.pipeline_limit,
+                stage_balance="calibrate" if args.stage_balance == 2 else bool(args.stage_balance),
+                pipeline_limit=args.pipeline_limit,
                 overlap_next_batch=None if args.overlap_next_batch is None else bool(args.overlap_next_batch),
                 loss_scale=args.loss_scale or (1024.0 if args.dtype == "fp16" else 1.0))
     from synth import uniform_tokens
@@ -381,6 +389,8 @@ def main():
                        "parallelism": f"G_inter{g_inter} x G_data{g_data}",
                        "offload": cfg["offload"], "checkpoint_interval": args.checkpoint_interval,
                        "stage_balance": args.stage_balance, "pipeline_limit": args.pipeline_limit,
+                       "stage_blocks": eng.partition() if args.stage_balance else None,
+                       "stage_speed_tflops": eng.stage_speed,
                        "l2": "inputs larger than L2 (GBs of weights/activations per step)"},
             "per_gpu_tflops": value / world,
             "device_mem_gib": torch.cuda.mem_get_info()[1] / 2**30 - torch.cuda.mem_get_info()[0] / 2**30,

@@ -96,7 +96,36 @@ typedef struct {
                                                  forward FLOPs including the last stage's LM head
                                                  (reading D-21b); G_inter need not divide n_layers.
                                                  Values are unchanged; requires checkpoint_interval <= 1. */
+  const double* stage_speed;                  /* NULL: every GPU equally fast.  Else G_inter relative
+                                                 speeds (finite, > 0; borrowed, read only inside
+                                                 axonn_init) of the GPUs holding stage i, the slowest
+                                                 replica of that stage (e.g. axonn_calibrate_speed on
+                                                 every rank, min over each column): with stage_balance
+                                                 each stage's cost is divided by its speed, so a GPU
+                                                 held back by the power cap gets fewer blocks (reading
+                                                 D-21c).  Must be identical on every rank (the column
+                                                 replicas hold the same layers).  Ignored when
+                                                 stage_balance = 0; non-positive or non-finite ->
+                                                 AXONN_ERR_INVALID_ARG. */
 } axonn_opt_cfg;
+
+/* The stage split stage_balance = 1 picks (reading D-21b/c), host-only (no device work):
+ * bounds[0..g_inter] receives the block boundaries 0 = b_0 < ... < b_G = 2 n_layers, stage i
+ * holding residual blocks [b_i, b_{i+1}) (block 2L = attention block of layer L, 2L + 1 its
+ * MLP block).  stage_speed as in axonn_opt_cfg (NULL = uniform).  Errors:
+ * AXONN_ERR_INVALID_ARG for NULL model/bounds, g_inter < 1, 2 n_layers < g_inter or a bad speed. */
+AXONN_API axonn_status axonn_stage_partition(const axonn_model_cfg* model, int g_inter,
+                                             const double* stage_speed, int* bounds);
+
+/* Sustained throughput of this library's K1 GEMM (C[M,N] = A[M,K] B[N,K]^T, half operands
+ * N(0,1), half output) on CUDA device `device`: iters/4 + 1 untimed launches, then `iters`
+ * back-to-back launches timed with CUDA events; *tflops = 2 M N K iters / time.  Allocates and
+ * frees its own buffers (2 (MK + NK + MN) bytes) and stream; the calling thread's current
+ * device becomes `device`.  Used to calibrate stage_speed (reading D-21c).  Errors:
+ * AXONN_ERR_INVALID_ARG (M, N < 128, K < 64, any not a multiple of 8,
+ * iters outside [1, 100000], NULL out),
+ * AXONN_ERR_CUDA (no sm_100a device, allocation or launch failure). */
+AXONN_API int axonn_calibrate_speed(int device, int M, int N, int K, int iters, double* tflops);
 
 /* Process placement in the G_inter x G_data grid: world_rank = j * G_inter + i
  * (i = stage, j = replica, reading D-29).  nccl_id: 128-byte ncclUniqueId made

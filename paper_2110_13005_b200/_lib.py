@@ -42,7 +42,7 @@ class OptCfg(C.Structure):
                 ("offload", C.c_int),
                 ("bucket_elems", C.c_int64), ("coarsen_k", C.c_int), ("pipeline_limit", C.c_int),
                 ("checkpoint_interval", C.c_int), ("overlap_next_batch", C.c_int),
-                ("stage_balance", C.c_int)]
+                ("stage_balance", C.c_int), ("stage_speed", C.POINTER(C.c_double))]
 
 
 class Dist(C.Structure):
@@ -71,6 +71,8 @@ def _declare(lib):
         "axonn_profile_json": (I, [P, C.c_char_p, I]),
         "axonn_timer_mark": (I, [P, I]),
         "axonn_timer_elapsed": (I, [P, I, I, C.POINTER(C.c_double)]),
+        "axonn_stage_partition": (I, [C.POINTER(ModelCfg), I, C.POINTER(C.c_double), C.POINTER(I)]),
+        "axonn_calibrate_speed": (I, [I, I, I, I, I, C.POINTER(C.c_double)]),
         "axonn_k_gemm": (I, [C.POINTER(GemmArgs), P]),
         "axonn_k_adamw": (I, [I64, P, P, P, P, P, C.POINTER(F), P]),
         "axonn_k_attn_fwd": (I, [P, I64, I, I, I, I, I, F, P, I64, P, P]),

@@ -41,3 +41,51 @@ extern "C" int axonn_k_attn_bwd(const void* qkv, int64_t lq, const void* dO, con
   return axonn::attn_bwd(qkv, lq, dO, o, ldo, lse, dbuf, b, heads, s, d, dp, alpha, dqkv, ldq,
                          reinterpret_cast<cudaStream_t>(stream));
 }
+
+// Sustained K1 throughput of this GPU on one GEMM shape (reading D-21c): random N(0, 1)
+// operands (zeros would draw less power and hide the power-capped clock), `iters` / 4 untimed
+// launches, then `iters` launches back to back timed with events on a private stream.
+extern "C" int axonn_calibrate_speed(int device, int M, int N, int K, int iters, double* tflops) {
+  if (!tflops || M < 128 || N < 128 || K < 64 || M % 8 || N % 8 || K % 8 || iters < 1 ||
+      iters > 100000)
+    return AXONN_ERR_INVALID_ARG;
+  *tflops = 0;
+  cudaDeviceProp prop;
+  if (cudaSetDevice(device) != cudaSuccess || cudaGetDeviceProperties(&prop, device) != cudaSuccess ||
+      prop.major < 10)
+    return AXONN_ERR_CUDA;
+  void *A = nullptr, *B = nullptr, *Cm = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int rc = AXONN_ERR_CUDA;
+  const size_t hb = sizeof(axonn::hx);
+  if (cudaMalloc(&A, (size_t)M * K * hb) == cudaSuccess &&
+      cudaMalloc(&B, (size_t)N * K * hb) == cudaSuccess &&
+      cudaMalloc(&Cm, (size_t)M * N * hb) == cudaSuccess &&
+      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+      cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess &&
+      !axonn::init_normal(A, nullptr, (long long)M * K, 0xCA1Bull, 0.f, 1.f, st) &&
+      !axonn::init_normal(B, nullptr, (long long)N * K, 0xCA1Cull, 0.f, 1.f, st)) {
+    axonn::GemmArgs g;
+    memset(&g, 0, sizeof(g));
+    g.M = M; g.N = N; g.K = K; g.Z = 1; g.Z1 = 1;
+    g.A = A; g.lda = K; g.B = B; g.ldb = K; g.C = Cm; g.ldc = N;
+    g.epi = axonn::EPI_HALF; g.alpha = 1.f;
+    rc = 0;
+    for (int i = 0; i < iters / 4 + 1 && !rc; ++i) rc = axonn::gemm_launch(g, st);
+    if (!rc && cudaEventRecord(e0, st) != cudaSuccess) rc = AXONN_ERR_CUDA;
+    for (int i = 0; i < iters && !rc; ++i) rc = axonn::gemm_launch(g, st);
+    float ms = 0;
+    if (!rc && (cudaEventRecord(e1, st) != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess ||
+                cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess || !(ms > 0)))
+      rc = AXONN_ERR_CUDA;
+    if (!rc) *tflops = 2.0 * M * N * (double)K * iters / (ms * 1e-3) / 1e12;
+    else rc = AXONN_ERR_CUDA;
+  }
+  if (st) cudaStreamSynchronize(st);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  cudaFree(A); cudaFree(B); cudaFree(Cm);
+  return rc;
+}

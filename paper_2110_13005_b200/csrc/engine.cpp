@@ -253,9 +253,11 @@ static int ipc_links(Ctx* c) {
 // causal QK^T and PV of the fused attention kernel, which runs at ~1/4 of the GEMMs' TFLOP/s:
 // W = 4, AXONN_BAL_ATTN_W overrides), MLP block 16h^2, plus the LM head 2hV on the last stage
 // (the embedding gather is negligible).  Exact DP over (stage, boundary); ties go to the
-// earliest boundary.
+// earliest boundary.  With stage_speed (the measured relative speed of the GPUs holding each
+// stage, slowest replica; axonn_calibrate_speed) a stage's cost is divided by its speed, so a
+// GPU that runs slower under the power cap gets fewer blocks (reading D-21c).
 // Returns G_inter + 1 boundaries (0 = b_0 < b_1 < ... < b_P = 2l).
-static std::vector<int> balanced_blocks(const axonn_model_cfg* m, int P) {
+static std::vector<int> balanced_blocks(const axonn_model_cfg* m, int P, const double* speed) {
   const int nb = 2 * m->n_layers;
   const double h = m->hidden, s = m->seq_len, V = m->vocab;
   std::vector<double> pre(nb + 1, 0.0);
@@ -263,7 +265,9 @@ static std::vector<int> balanced_blocks(const axonn_model_cfg* m, int P) {
   if (const char* e = getenv("AXONN_BAL_ATTN_W")) w_att = atof(e);
   for (int k = 0; k < nb; ++k) pre[k + 1] = pre[k] + ((k & 1) ? 16 * h * h : 8 * h * h + w_att * 2 * s * h);
   const double head = 2 * h * V;
-  auto cost = [&](int i, int a, int b) { return pre[b] - pre[a] + (i == P - 1 ? head : 0.0); };
+  auto cost = [&](int i, int a, int b) {
+    return (pre[b] - pre[a] + (i == P - 1 ? head : 0.0)) / (speed ? speed[i] : 1.0);
+  };
   const double INF = 1e300;
   std::vector<std::vector<double>> best(P + 1, std::vector<double>(nb + 1, INF));
   std::vector<std::vector<int>> arg(P + 1, std::vector<int>(nb + 1, -1));
@@ -443,6 +447,19 @@ AXONN_API axonn_status axonn_get_unique_id(void* out128) {
   return AXONN_OK;
 }
 
+AXONN_API axonn_status axonn_stage_partition(const axonn_model_cfg* model, int g_inter,
+                                              const double* stage_speed, int* bounds) {
+  if (!model || !bounds || g_inter < 1 || model->n_layers < 1 || 2 * model->n_layers < g_inter ||
+      model->hidden < 1 || model->seq_len < 1 || model->vocab < 1)
+    return AXONN_ERR_INVALID_ARG;
+  if (stage_speed)
+    for (int i = 0; i < g_inter; ++i)
+      if (!(stage_speed[i] > 0) || !std::isfinite(stage_speed[i])) return AXONN_ERR_INVALID_ARG;
+  const std::vector<int> bb = balanced_blocks(model, g_inter, stage_speed);
+  for (int i = 0; i <= g_inter; ++i) bounds[i] = bb[i];
+  return AXONN_OK;
+}
+
 AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
                                   const axonn_model_cfg* model, const axonn_opt_cfg* opt,
                                   const axonn_dist* dist, axonn_ctx** out) {
@@ -459,6 +476,9 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
     return AXONN_ERR_NONDIVISIBLE_LAYERS;
   if (opt->stage_balance && opt->checkpoint_interval != 0 && opt->checkpoint_interval != 1)
     return AXONN_ERR_INVALID_ARG;   // checkpoint segments are whole layers
+  if (opt->stage_balance && opt->stage_speed)
+    for (int i = 0; i < g_inter; ++i)
+      if (!(opt->stage_speed[i] > 0) || !std::isfinite(opt->stage_speed[i])) return AXONN_ERR_INVALID_ARG;
   if (model->hidden < 8 || model->heads < 1 || model->hidden % model->heads ||
       model->hidden % 8 || model->seq_len < 8 || model->seq_len % 8 || model->vocab < 2 ||
       model->vocab % 8)
@@ -485,7 +505,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   c->first = c->stage == 0;
   c->last = c->stage == g_inter - 1;
   if (opt->stage_balance) {
-    const std::vector<int> bb = balanced_blocks(model, g_inter);   // block boundaries
+    const std::vector<int> bb = balanced_blocks(model, g_inter, opt->stage_speed);
     const int b0 = bb[c->stage], b1 = bb[c->stage + 1];            // blocks [b0, b1)
     c->layer0 = b0 / 2;
     c->nl = (b1 + 1) / 2 - b0 / 2;

@@ -40,7 +40,7 @@ class AxoNN:
                  weight_decay: float = 0.01, loss_scale: float = 1.0, offload: bool = False,
                  bucket_elems: int = 4_000_000, coarsen_k: int = 4, pipeline_limit: int = 0,
                  overlap_next_batch: bool | None = None, checkpoint_interval: int = 0,
-                 stage_balance: bool = False,
+                 stage_balance: bool | str = False, stage_speed=None,
                  rank: int = 0, world_size: int = 1, device: int = 0, nccl_id: bytes | None = None,
                  dtype: str = "bf16"):
         # the half format picks the library build (include/axonn.h axonn_dtype)
@@ -52,7 +52,16 @@ class AxoNN:
                               # default: overlap when the optimizer is host-link bound (offload);
                               # in HBM the AdamW kernels only compete with the GEMMs for SMs
                               int(offload if overlap_next_batch is None else overlap_next_batch),
-                              int(stage_balance))
+                              int(bool(stage_balance)), None)
+        # reading D-21c: stage_balance="calibrate" measures every rank's sustained K1 speed
+        # on the stage's FC1 shape and splits by the slowest replica of each stage
+        if stage_balance == "calibrate" and stage_speed is None and g_inter > 1:
+            stage_speed = self.calibrate_stage_speed(
+                self.lib, g_inter, g_data, microbatch * seq_len, hidden, rank, world_size, device)
+        self.stage_speed = None if stage_speed is None else [float(x) for x in stage_speed]
+        if self.stage_speed is not None:
+            self._speed = (C.c_double * g_inter)(*self.stage_speed)
+            self.oc.stage_speed = self._speed
         self._id = C.create_string_buffer(nccl_id if nccl_id else b"\0" * 128, 128)
         self.dist = _lib.Dist(rank, world_size, C.cast(self._id, C.c_void_p), device)
         self.ctx = C.c_void_p()
@@ -65,6 +74,36 @@ class AxoNN:
         self.rank, self.world_size = rank, world_size
         self.stage, self.replica = rank % g_inter, rank // g_inter
         self._tensors = None
+
+    @staticmethod
+    def calibrate_stage_speed(lib, g_inter, g_data, M, hidden, rank, world_size, device,
+                              seconds: float = 0.4):
+        """Per-stage speeds for axonn_opt_cfg.stage_speed: every rank times the library's K1
+        on the FC1 shape (M x 4h x h) for about ``seconds`` (axonn_calibrate_speed), the
+        TFLOP/s are all-gathered over the host process group, and stage i takes the minimum
+        over its column (replicas share the layer split).  Host-side marshalling only."""
+        N, K = 4 * hidden, hidden
+        M, N, K = (max(128, (x + 7) // 8 * 8) for x in (M, N, K))
+        # about `seconds` at ~1 PFLOP/s, clamped: tiny shapes are launch-bound (~5 us a launch)
+        iters = min(4000, max(8, int(seconds * 1.0e15 / (2.0 * M * N * K))))
+        tf = C.c_double()
+        rc = lib.axonn_calibrate_speed(device, M, N, K, iters, C.byref(tf))
+        if rc != 0:
+            raise AxoNNError(rc, "axonn_calibrate_speed failed")
+        speeds = [tf.value]
+        if world_size > 1:
+            import torch.distributed as dist
+            speeds = [None] * world_size
+            dist.all_gather_object(speeds, tf.value)
+        return [min(speeds[j * g_inter + i] for j in range(g_data)) for i in range(g_inter)]
+
+    def partition(self):
+        """The block boundaries of the stage split (axonn_stage_partition)."""
+        out = (C.c_int * (self.g_inter + 1))()
+        rc = self.lib.axonn_stage_partition(C.byref(self.mc), self.g_inter, self.oc.stage_speed, out)
+        if rc != 0:
+            raise AxoNNError(rc, "axonn_stage_partition failed")
+        return list(out)
 
     # ------------------------------------------------------------- lifecycle
     def close(self):

@@ -2,7 +2,7 @@
 profiles/<round>/k1_traffic.json: per launch duration, DRAM bytes (dram__bytes_read.sum +
 dram__bytes_write.sum), the algorithmic bytes of the launch (A + B read, C written, plus the
 fused epilogue's extra operand), and the tensor-pipe utilisation.  bench.py reports the
-average as roofline.traffic.  Usage: python scripts/ncu_traffic.py REPORT.ncu-rep OUT.json"""
+average as roofline.traffic.  Usage: python scripts/ncu_traffic.py REPORT.ncu-rep OUT.json [M tokens per microbatch]"""
 import csv
 import io
 import json
@@ -14,7 +14,7 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
          "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
 
 
-def main(rep, out):
+def main(rep, out, M=4096):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -48,7 +48,7 @@ def main(rep, out):
     # model_exec.cpp: forward qkv, proj, fc1, fc2, head; backward head wgrad, head dgrad, then
     # fc2 wgrad, fc2 dgrad, fc1 wgrad, fc1 dgrad, proj wgrad, proj dgrad, qkv wgrad, qkv dgrad)
     # at M tokens, width h, vocab V; bf16 2 B, fp32 gradient 4 B (first microbatch: store only)
-    M, h, V = 4096, 2048, 51200
+    h, V = 2048, 51200
     b2, f4 = 2, 4
     alg = [("fwd qkv", b2 * (M * h + 3 * h * h + M * 3 * h)),
            ("fwd proj +resid", b2 * (M * h + h * h + 2 * M * h)),
@@ -80,4 +80,4 @@ def main(rep, out):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 4096)

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--inf-rank", type=int, default=-1,
                     help="after step 0's run_batch this rank writes one inf gradient (D-12 skip)")
     ap.add_argument("--balance", action="store_true", help="stage_balance (reading D-21b)")
+    ap.add_argument("--speed", default=None,
+                    help="with --balance: 'calibrate' or comma-separated stage speeds (reading D-21c)")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     import torch
@@ -47,11 +49,16 @@ def main():
     nid = D.share_unique_id(rank, world, D.nccl_unique_id)
     eng = AxoNN(a.g_inter, a.g_data, a.mb, **cfg, rank=rank, world_size=world, device=local,
                 nccl_id=nid, offload=bool(a.offload), bucket_elems=5000, coarsen_k=2,
-                dtype=a.dtype, loss_scale=a.loss_scale, stage_balance=a.balance)
+                dtype=a.dtype, loss_scale=a.loss_scale,
+                stage_balance="calibrate" if (a.balance and a.speed == "calibrate") else a.balance,
+                stage_speed=[float(x) for x in a.speed.split(",")]
+                if (a.speed and a.speed != "calibrate") else None)
     params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=42)
     names = [n for n, _, _ in eng.tensors()]
     eng.write_all(T_MASTER, {n: params[n] for n in names})
-    out = {}
+    out = {"bounds": np.array(eng.partition() if a.balance else [])}
+    if eng.stage_speed is not None:
+        out["speed"] = np.array(eng.stage_speed)
     for step in range(a.steps):
         tok = markov_tokens(a.batch, cfg["seq_len"], cfg["vocab"], seed=7 + step)
         loss = eng.run_batch(tok)

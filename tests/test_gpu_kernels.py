@@ -312,3 +312,14 @@ def test_gemm_stream_k_fixup(lib, M, N, K, epi):
         ref = acc + host(bias) + host(aux)
     out = outs[0].float().cpu().numpy().astype(np.float64)
     assert rel(out, ref) < (1e-5 if epi == 3 else 1e-2)
+
+
+def test_calibrate_speed_is_plausible(lib):
+    """axonn_calibrate_speed (reading D-21c) on the 1.3B FC1 shape: K1's sustained TFLOP/s
+    lies between half the bf16 peak and the nominal 2.25 PFLOP/s, and the call leaves the
+    device usable (a second call agrees within 25 %)."""
+    a, b = C.c_double(), C.c_double()
+    assert lib.axonn_calibrate_speed(0, 4096, 8192, 2048, 200, C.byref(a)) == 0
+    assert lib.axonn_calibrate_speed(0, 4096, 8192, 2048, 200, C.byref(b)) == 0
+    assert 700.0 < a.value < 2250.0 and 700.0 < b.value < 2250.0, (a.value, b.value)
+    assert abs(a.value - b.value) <= 0.25 * max(a.value, b.value)

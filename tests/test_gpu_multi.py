@@ -2,6 +2,7 @@
 column all-reduce (G_data > 1) and their combination, through the C-ABI, vs
 the oracle's plain full-batch result on the same seeded inputs."""
 import os
+import signal
 import socket
 import subprocess
 import sys
@@ -38,8 +39,17 @@ def launch(tmp_path, gi, gd, cfg="tiny", mb=2, batch=8, steps=1, offload=0, extr
            "--mb", str(mb), "--batch", str(batch), "--cfg", cfg, "--steps", str(steps),
            "--offload", str(offload), "--out", str(tmp_path)] + list(extra)
     env = dict(os.environ, AXONN_WATCHDOG_S="60", **(env or {}))
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT, env=env)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    # own process group: on a timeout the workers die with torchrun instead of living on as
+    # orphans that keep the GPUs busy for the tests (and benches) that follow
+    p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=ROOT,
+                         env=env, start_new_session=True)
+    try:
+        out, err = p.communicate(timeout=240)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        out, err = p.communicate()
+        raise AssertionError("timeout\n" + out[-3000:] + err[-3000:])
+    assert p.returncode == 0, out[-3000:] + err[-3000:]
     return [dict(np.load(os.path.join(tmp_path, f"rank{k}.npz"))) for k in range(n)]
 
 
@@ -180,3 +190,25 @@ def test_two_gpus_balanced_split(tmp_path):
 def test_four_gpus_balanced_split(tmp_path, gi, gd, cfg):
     res = launch(tmp_path, gi, gd, cfg, 2, 8 * gd, extra=("--balance",))
     check(res, gi, gd, cfg, 8 * gd)
+
+
+@pytest.mark.multigpu(2)
+def test_two_gpus_speed_weighted_split(tmp_path):
+    """Reading D-21c: a stage speed of 0.25 on stage 1 moves blocks onto stage 0 (the split
+    axonn_stage_partition reports on both ranks), and the result still matches the oracle."""
+    res = launch(tmp_path, 2, 1, "tiny4v", 2, 8, extra=("--balance", "--speed", "1.0,0.25"))
+    b = [list(r["bounds"]) for r in res]
+    assert b[0] == b[1]
+    assert b[0][2] - b[0][1] < b[0][1] - b[0][0], b[0]   # slow stage 1 holds fewer blocks
+    check(res, 2, 1, "tiny4v", 8)
+
+
+@pytest.mark.multigpu(2)
+def test_two_gpus_calibrated_split(tmp_path):
+    """stage_balance='calibrate': every rank times K1 (axonn_calibrate_speed), the speeds are
+    all-gathered, both ranks agree on one split, and the step matches the oracle."""
+    res = launch(tmp_path, 2, 1, "tiny4v", 2, 8, extra=("--balance", "--speed", "calibrate"))
+    assert np.array_equal(res[0]["bounds"], res[1]["bounds"])
+    assert np.array_equal(res[0]["speed"], res[1]["speed"])
+    assert all(300.0 < s < 3000.0 for s in res[0]["speed"]), res[0]["speed"]
+    check(res, 2, 1, "tiny4v", 8)
