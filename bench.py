@@ -156,10 +156,22 @@ def k1_traffic(cfg):
     d = json.load(open(p))
     if d.get("hidden") != cfg["hidden"] or d.get("tokens") != cfg["microbatch"] * cfg["seq_len"]:
         return {"traffic": None}
-    return {"traffic": d["dram_bytes_per_launch_avg"],
-            "traffic_algorithmic": d.get("algorithmic_bytes_per_launch_avg"),
-            "traffic_unit": "bytes per K1 launch (average over one layer's 13 linear GEMMs)",
-            "traffic_src": "profiles/r1/k1_traffic.json (ncu --set full)"}
+    # the capture is one 1-layer microbatch (12 layer GEMMs + 3 LM-head GEMMs); `achieved`
+    # averages over the K1 launches of one n_layers microbatch, so weight the layer launches
+    # by n_layers to average over the same population
+    ls = d.get("launches", [])
+    if ls and all("gemm" in l and "algorithmic_bytes" in l for l in ls):
+        L = cfg["n_layers"]
+        w = [1 if "head" in l["gemm"] else L for l in ls]
+        n = sum(w)
+        dram = sum(wi * l["dram_total"] for wi, l in zip(w, ls)) / n
+        alg = sum(wi * l["algorithmic_bytes"] for wi, l in zip(w, ls)) / n
+        unit = f"bytes per K1 launch (average over one microbatch: {L} x 12 layer GEMMs + 3 head)"
+    else:
+        dram, alg = d["dram_bytes_per_launch_avg"], d.get("algorithmic_bytes_per_launch_avg")
+        unit = "bytes per K1 launch (average over the captured launches)"
+    return {"traffic": dram, "traffic_algorithmic": alg, "traffic_unit": unit,
+            "traffic_src": "profiles/r1/k1_traffic.json (ncu --set full, 1-layer microbatch)"}
 
 
 def cpu_oracle_sample(cfg, steps: int = 1):
