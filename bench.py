@@ -33,10 +33,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")   # before any CUDA context
-# NCCL's "NCCL version ..." banner goes to stdout ahead of the JSON line; keep stdout to the
-# one line unless a caller asked for NCCL's INFO/TRACE output explicitly
-if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
-    os.environ["NCCL_DEBUG"] = "WARN"
+
+_JSON_FD = 1   # main() points fd 1 at stderr and keeps the real stdout here
+
+
+def emit(out: dict) -> None:
+    """Write the one JSON line to the real stdout (NCCL's native banner and any other
+    native prints land on stderr)."""
+    os.write(_JSON_FD, (json.dumps(out) + "\n").encode())
+
 
 METRIC = "per-GPU model TFLOP/s and % of B200 bf16 peak at 1/2/4/8 GPUs; batch time"
 
@@ -227,7 +232,7 @@ def run_reference(args, cfg, rank, world):
            "cpu_baseline": res,
            "e2e": {"value": v, "unit": "model TFLOP/s (all GPUs)", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
     _ = steps_total
 
 
@@ -451,9 +456,12 @@ def main():
                                    "launches": v[2]}
                                for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])},
         }
-        print(json.dumps(out), flush=True)
+        emit(out)
     eng.close()
 
 
 if __name__ == "__main__":
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     main()
