@@ -132,11 +132,39 @@ AXONN_API int axonn_calibrate_speed(int device, int M, int N, int K, int iters, 
  * by rank 0 with axonn_get_unique_id and broadcast by the caller (the Python
  * binding uses torch.distributed for that; PyTorch is plumbing only).
  * Ignored when world_size == 1. */
+typedef struct axonn_local_group axonn_local_group;
 typedef struct {
   int world_rank, world_size;
   const void* nccl_id;
   int device;   /* CUDA ordinal */
+  /* NULL (production): one process per GPU, NCCL communicators from nccl_id.
+   * Non-NULL: the test-only loopback transport below; nccl_id is ignored. */
+  axonn_local_group* local_group;
 } axonn_dist;
+
+/* Test-only loopback transport (SURVEY.md §4 "optional test-only loopback transport"):
+ * the G_inter stages of ONE pipeline (G_data = 1) as G_inter contexts in ONE process, each
+ * created and driven by its own host thread, on the same device or on different devices.
+ * The Alg. 2 scheduler runs unchanged: pre-posted receives into the
+ * `pipeline_limit` slots, backward-first dispatch among landed messages (D-19), stage-0
+ * injection after each backward (Alg. 2 l.24-26), and the production peer-copy link: a
+ * message for microbatch mb is a copy-engine copy into the neighbour's slot mb mod limit
+ * followed, on the same stream, by a stream-memop store of the message's sequence number
+ * into the neighbour's flag.  The only difference: the flag words live in host-mapped
+ * pinned memory and the receiving stage's host thread observes them (a stream wait per
+ * receive on G_inter contexts x 10 streams of one device could share a hardware queue with
+ * the sender's stream and deadlock).  Slot and flag pointers are exchanged through the
+ * group at axonn_init (a host rendezvous of all `size` contexts); the loss sum (C5) and the
+ * fp16 overflow flag (D-12) are reduced on the host through the group.  No NCCL call is
+ * made.  axonn_init with a group: world_size must equal `size`, g_data must be 1 (else
+ * AXONN_ERR_INVALID_ARG); every collective call (axonn_init, axonn_run_batch,
+ * axonn_optimizer_step) must be made by all `size` contexts concurrently, from different
+ * threads.  If one context fails inside a collective call the group is marked failed and
+ * the others return AXONN_ERR_STATE instead of waiting.  The caller frees the group after
+ * every context using it (axonn_free).  Errors: AXONN_ERR_INVALID_ARG (size < 1, NULL out),
+ * AXONN_ERR_OOM. */
+AXONN_API axonn_status axonn_local_group_create(int size, axonn_local_group** out);
+AXONN_API void axonn_local_group_free(axonn_local_group* group);
 
 /* Tensor kinds for inspection (canonical oracle layout, fp32 on the host). */
 typedef enum {

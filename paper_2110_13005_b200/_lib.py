@@ -47,7 +47,7 @@ class OptCfg(C.Structure):
 
 class Dist(C.Structure):
     _fields_ = [("world_rank", C.c_int), ("world_size", C.c_int), ("nccl_id", C.c_void_p),
-                ("device", C.c_int)]
+                ("device", C.c_int), ("local_group", C.c_void_p)]
 
 
 def _declare(lib):
@@ -73,6 +73,8 @@ def _declare(lib):
         "axonn_timer_elapsed": (I, [P, I, I, C.POINTER(C.c_double)]),
         "axonn_stage_partition": (I, [C.POINTER(ModelCfg), I, C.POINTER(C.c_double), C.POINTER(I)]),
         "axonn_calibrate_speed": (I, [I, I, I, I, I, C.POINTER(C.c_double)]),
+        "axonn_local_group_create": (I, [I, C.POINTER(C.c_void_p)]),
+        "axonn_local_group_free": (None, [P]),
         "axonn_k_gemm": (I, [C.POINTER(GemmArgs), P]),
         "axonn_k_adamw": (I, [I64, P, P, P, P, P, C.POINTER(F), P]),
         "axonn_k_attn_fwd": (I, [P, I64, I, I, I, I, I, F, P, I64, P, P]),

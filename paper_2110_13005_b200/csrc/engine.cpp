@@ -5,17 +5,76 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <mutex>
 #include <new>
 #include <map>
 #include <thread>
 
 #include "engine.h"
 
+// Test-only loopback group (include/axonn.h): a host rendezvous of `size` contexts in one
+// process, with a sum / max reduction riding on each rendezvous and a registry of the
+// stages' receive slots and flag words.
+struct axonn_local_group {
+  struct Reg {
+    uint32_t* flags = nullptr;          // device-visible address of the stage's flag words
+    std::vector<void*> act, grad;       // receive slots: activations (slot.in), gradients (slot.grecv)
+  };
+  int size = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool failed = false;
+  double acc_sum = 0, res_sum = 0;
+  int acc_max = 0, res_max = 0;
+  std::vector<Reg> reg;
+  std::mutex preload_mu;                // kernel preloading / attribute setup, one thread at a time
+
+  // Every member calls this; returns 0 with the sum of `*sum` and the max of `*mx` over the
+  // group written back (either may be NULL), or -1 if the group failed or timed out.
+  int rendezvous(double* sum, int* mx, double timeout_s) {
+    std::unique_lock<std::mutex> lk(mu);
+    if (failed) return -1;
+    acc_sum += sum ? *sum : 0.0;
+    acc_max = std::max(acc_max, mx ? *mx : 0);
+    const uint64_t g = gen;
+    if (++arrived == size) {
+      res_sum = acc_sum;
+      res_max = acc_max;
+      acc_sum = 0;
+      acc_max = 0;
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else if (!cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return gen != g || failed; }) ||
+               failed) {
+      failed = true;
+      cv.notify_all();
+      return -1;
+    }
+    if (sum) *sum = res_sum;
+    if (mx) *mx = res_max;
+    return 0;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    failed = true;
+    cv.notify_all();
+  }
+};
+
 namespace axonn {
+
+static double group_timeout_s() {
+  const char* e = getenv("AXONN_WATCHDOG_S");   // same bound as the Alg. 2 watchdog
+  return e ? atof(e) : 600.0;
+}
 
 // ------------------------------------------------------------------ helpers
 int Ctx::fail(int code, const std::string& msg) {
@@ -242,6 +301,44 @@ static int ipc_links(Ctx* c) {
       for (int k = 0; k < L; ++k)
         if ((rc = open(got.data() + (1 + k) * HB, &c->peer_grad[k]))) return rc;
     }
+  }
+  return 0;
+}
+
+// Loopback links (test-only local group): the flag words are host-mapped pinned memory
+// (written by the neighbours' stream memops, observed by this context's host thread); slot
+// and flag addresses are published in the group and read back after a rendezvous.
+static int local_links(Ctx* c) {
+  const int L = c->limit;
+  axonn_local_group* g = c->lg;
+  int rc;
+  uint32_t* hf = nullptr;
+  if ((rc = c->check_cuda(cudaHostAlloc((void**)&hf, 2 * L * sizeof(uint32_t),
+                                        cudaHostAllocMapped | cudaHostAllocPortable), "host flags")))
+    return rc;
+  memset(hf, 0, 2 * L * sizeof(uint32_t));
+  c->flags_host = hf;
+  if ((rc = c->check_cuda(cudaHostGetDevicePointer((void**)&c->flags, hf, 0), "host flags map"))) return rc;
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    axonn_local_group::Reg& r = g->reg[c->stage];
+    r.flags = c->flags;
+    r.act.assign(L, nullptr);
+    r.grad.assign(L, nullptr);
+    for (int k = 0; k < L; ++k) {
+      r.act[k] = c->slots[k].in;
+      r.grad[k] = c->slots[k].grecv;
+    }
+  }
+  if (g->rendezvous(nullptr, nullptr, group_timeout_s())) return c->fail(AXONN_ERR_STATE, "local group failed");
+  std::lock_guard<std::mutex> lk(g->mu);
+  if (!c->last) {
+    c->peer_flags_next = g->reg[c->stage + 1].flags;
+    c->peer_act = g->reg[c->stage + 1].act;
+  }
+  if (!c->first) {
+    c->peer_flags_prev = g->reg[c->stage - 1].flags;
+    c->peer_grad = g->reg[c->stage - 1].grad;
   }
   return 0;
 }
@@ -489,7 +586,9 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
       !(opt->eps > 0) || !(opt->loss_scale > 0) || opt->bucket_elems < 1 || opt->coarsen_k < 1 ||
       opt->pipeline_limit < 0)
     return AXONN_ERR_INVALID_ARG;
-  if (world > 1 && (!dist || !dist->nccl_id)) return AXONN_ERR_INVALID_ARG;
+  axonn_local_group* lg = (dist && world > 1) ? dist->local_group : nullptr;
+  if (lg && (lg->size != world || g_data != 1)) return AXONN_ERR_INVALID_ARG;
+  if (world > 1 && !lg && !dist->nccl_id) return AXONN_ERR_INVALID_ARG;
   if (opt->checkpoint_interval < -1 ||   // BadCheckpointInterval: ac must divide N / G_inter
       (opt->checkpoint_interval > 1 && (model->n_layers / g_inter) % opt->checkpoint_interval))
     return AXONN_ERR_INVALID_ARG;
@@ -500,6 +599,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   c->mc = *model; c->oc = *opt;
   if (c->oc.bucket_elems % 4) c->oc.bucket_elems += 4 - c->oc.bucket_elems % 4;   // 16-B aligned buckets
   c->rank = rank; c->world = world; c->device = dist ? dist->device : 0;
+  c->lg = lg;
   c->stage = rank % g_inter;            // world_rank = j * G_inter + i (D-29)
   c->replica = rank / g_inter;
   c->first = c->stage == 0;
@@ -538,6 +638,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   }
 
   auto bail = [&](int rc) {
+    if (c->lg) c->lg->abort();   // the other loopback stages must not wait for this one
     axonn_free(c);
     return (axonn_status)rc;
   };
@@ -550,8 +651,12 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   // CUDA lazy loading would load a kernel's module at its first launch and wait for the
   // device's running kernels — including a pre-posted ncclRecv spinning until the peer
   // sends, which the peer only does after our launch: load everything now.
-  if (preload_gemm() || preload_ops() || preload_adamw() || preload_attn())
-    return bail(c->fail(AXONN_ERR_CUDA, "kernel preload failed"));
+  {
+    std::unique_lock<std::mutex> lk;
+    if (c->lg) lk = std::unique_lock<std::mutex>(c->lg->preload_mu);
+    if (preload_gemm() || preload_ops() || preload_adamw() || preload_attn())
+      return bail(c->fail(AXONN_ERR_CUDA, "kernel preload failed"));
+  }
   for (cudaStream_t* st : {&c->s_comp, &c->s_send_act, &c->s_send_grad, &c->s_recv_act,
                            &c->s_recv_grad, &c->s_dp, &c->s_h2d, &c->s_d2h, &c->s_opt, &c->s_wg})
     if ((rc = c->check_cuda(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking), "stream")))
@@ -568,7 +673,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   if ((rc = init_weights(c))) return bail(rc);
 
   // NCCL: world, column (all-reduce) and per-direction neighbour links (2-rank comms).
-  if (world > 1) {
+  if (world > 1 && !c->lg) {
     ncclUniqueId id;
     memcpy(&id, dist->nccl_id, sizeof(id));
     ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
@@ -611,7 +716,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   // the peer also reaches it; in Alg. 2 the peer only does so after a message arrives, so
   // connect every link now, in ascending boundary order (no cycle: rank i finishes
   // boundary i-1 before boundary i).
-  if (world > 1 && g_inter > 1) {
+  if (world > 1 && g_inter > 1 && !c->lg) {
     void* tmp = c->dalloc(256);
     if (!tmp) return bail(c->fail(AXONN_ERR_OOM, "link warm-up buffer"));
     for (int k = 0; k < g_inter - 1; ++k) {
@@ -630,7 +735,12 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
       }
     }
   }
-  if (world > 1 && g_inter > 1 && c->p2p_ipc && (rc = ipc_links(c))) return bail(rc);
+  if (c->lg) {
+    c->p2p_ipc = 1;   // the loopback runs the peer-copy link protocol
+    if ((rc = local_links(c))) return bail(rc);
+  } else if (world > 1 && g_inter > 1 && c->p2p_ipc && (rc = ipc_links(c))) {
+    return bail(rc);
+  }
   if ((rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "init sync"))) return bail(rc);
   *out = c;
   return AXONN_OK;
@@ -652,6 +762,7 @@ AXONN_API void axonn_free(axonn_ctx* c) {
     if (c->adam_v) cudaFreeHost(c->adam_v);
   }
   if (c->h_loss) cudaFreeHost(c->h_loss);
+  if (c->flags_host) cudaFreeHost((void*)c->flags_host);
   if (c->dtok) cudaFree(c->dtok);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_pool_opt) cudaEventDestroy(e);
@@ -814,6 +925,20 @@ AXONN_API axonn_status axonn_set_profiling(axonn_ctx* c, int on) {
   return AXONN_OK;
 }
 
+AXONN_API axonn_status axonn_local_group_create(int size, axonn_local_group** out) {
+  if (!out) return AXONN_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (size < 1) return AXONN_ERR_INVALID_ARG;
+  axonn_local_group* g = new (std::nothrow) axonn_local_group();
+  if (!g) return AXONN_ERR_OOM;
+  g->size = size;
+  g->reg.resize(size);
+  *out = g;
+  return AXONN_OK;
+}
+
+AXONN_API void axonn_local_group_free(axonn_local_group* g) { delete g; }
+
 AXONN_API axonn_status axonn_stats(const axonn_ctx* c, double* out, int n) {
   if (!c || !out || n < 0) return AXONN_ERR_INVALID_ARG;
   for (int i = 0; i < n && i < AXONN_STAT_COUNT; ++i) out[i] = c->stats[i];
@@ -887,6 +1012,7 @@ static int run_pipeline(Ctx* c, int m) {
     // pre-post receives into free slots, in microbatch order
     while (!c->first && next_act_post < m && next_act_post < done_b + L) {
       int mb = next_act_post++;
+      if (c->flags_host) continue;   // loopback: the host thread observes the flag (landed())
       ev_act[mb] = c->ev();
       // the slot's previous occupant (mb - L) must have finished its backward on the GPU
       if (mb >= L) cudaStreamWaitEvent(c->s_recv_act, ev_bdone[mb - L], 0);
@@ -899,6 +1025,7 @@ static int run_pipeline(Ctx* c, int m) {
     }
     while (!c->last && next_grad_post < m && next_grad_post < done_b + L) {
       int mb = next_grad_post++;
+      if (c->flags_host) continue;
       ev_grad[mb] = c->ev();
       if (mb >= L) cudaStreamWaitEvent(c->s_recv_grad, ev_bdone[mb - L], 0);
       int r = c->p2p_ipc ? wait_flag(c, c->s_recv_grad, c->flags + L + mb % L, seq(mb))
@@ -950,7 +1077,7 @@ static int run_pipeline(Ctx* c, int m) {
   auto forward_of = [&](int mb) -> int {   // Forward (+ Backward(1) and grad send on the last stage)
     Slot& sl = slot_of(mb);
     sl.mb = mb;
-    if (!c->first) cudaStreamWaitEvent(c->s_comp, ev_act[mb], 0);
+    if (!c->first && ev_act[mb]) cudaStreamWaitEvent(c->s_comp, ev_act[mb], 0);
     // a slot's gradient-out buffer is reused only after its previous send finished
     if (!c->first && mb >= L && ev_sent_grad[mb - L]) cudaStreamWaitEvent(c->s_comp, ev_sent_grad[mb - L], 0);
     if (!c->last && mb >= L && ev_sent_act[mb - L]) cudaStreamWaitEvent(c->s_comp, ev_sent_act[mb - L], 0);
@@ -967,7 +1094,7 @@ static int run_pipeline(Ctx* c, int m) {
   };
   auto backward_of = [&](int mb) -> int {
     Slot& sl = slot_of(mb);
-    cudaStreamWaitEvent(c->s_comp, ev_grad[mb], 0);
+    if (ev_grad[mb]) cudaStreamWaitEvent(c->s_comp, ev_grad[mb], 0);
     int r = c->backward(sl, mb, sl.grecv);
     if (r) return r;
     ev_bdone[mb] = c->ev();
@@ -998,10 +1125,14 @@ static int run_pipeline(Ctx* c, int m) {
     bool need_grad = !c->last && next_grad < m;
     if (!need_act && !need_grad) break;
     if ((rc = post())) return rc;
-    bool grad_landed = need_grad && next_grad < next_grad_post &&
-                       cudaEventQuery(ev_grad[next_grad]) == cudaSuccess;
-    bool act_landed = !grad_landed && need_act && next_act < next_act_post &&
-                      cudaEventQuery(ev_act[next_act]) == cudaSuccess;
+    // a message has landed: its receive event completed, or (loopback) the flag word of its
+    // slot holds its sequence number (the store is ordered after the copy into the slot)
+    auto landed = [&](bool grad, int mb) -> bool {
+      if (c->flags_host) return c->flags_host[(grad ? L : 0) + mb % L] == seq(mb);
+      return cudaEventQuery(grad ? ev_grad[mb] : ev_act[mb]) == cudaSuccess;
+    };
+    bool grad_landed = need_grad && next_grad < next_grad_post && landed(true, next_grad);
+    bool act_landed = !grad_landed && need_act && next_act < next_act_post && landed(false, next_act);
     if (grad_landed) {   // backward-first among landed messages (D-19)
       int mb = next_grad++;
       if ((rc = backward_of(mb))) return rc;
@@ -1120,7 +1251,7 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   if (c->g_data == 1) CU(cudaEventRecord(c->ph[par][2], c->s_comp));
   CU(cudaEventRecord(c->ev_loss, c->s_comp));
   CU(cudaStreamWaitEvent(c->s_dp, c->ev_loss, 0));
-  if (c->world > 1)   // C5: loss sum over the last-stage ranks, seen by every rank
+  if (c->world > 1 && !c->lg)   // C5: loss sum over the last-stage ranks, seen by every rank
     NC(ncclAllReduce(c->d_loss, c->d_loss, 1, ncclFloat64, ncclSum, c->world_comm, c->s_dp));
   CU(cudaMemcpyAsync(c->h_loss, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->s_dp));
   cudaEvent_t ev_loss_host = c->ev();
@@ -1143,6 +1274,8 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
     CU(cudaEventRecord(c->ph[par][2], c->s_dp));
   }
   CU(cudaEventSynchronize(ev_loss_host));
+  if (c->lg && c->lg->rendezvous(c->h_loss, nullptr, group_timeout_s()))   // C5 on the host
+    return (axonn_status)c->fail(AXONN_ERR_STATE, "local group failed (loss)");
   // the row losses are summed unscaled (the S of D-11 enters only the CE gradient): L/S
   if (loss_out) *loss_out = (float)(*c->h_loss);
   c->grads_ready = true;
@@ -1192,17 +1325,28 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
 extern "C" {
 
 AXONN_API axonn_status axonn_run_batch(axonn_ctx* c, const int32_t* tokens, int batch, float* loss_out) {
-  return run_batch_impl(c, tokens, false, batch, loss_out);
+  const axonn_status rc = run_batch_impl(c, tokens, false, batch, loss_out);
+  if (rc && c && c->lg) c->lg->abort();   // loopback: the other stages must not wait for this one
+  return rc;
 }
 
 AXONN_API axonn_status axonn_run_batch_device(axonn_ctx* c, const int32_t* d_tokens, int batch,
                                               float* loss_out) {
-  return run_batch_impl(c, d_tokens, true, batch, loss_out);
+  const axonn_status rc = run_batch_impl(c, d_tokens, true, batch, loss_out);
+  if (rc && c && c->lg) c->lg->abort();
+  return rc;
 }
 
 // Alg. 1 l.7 with the memory optimisation and the
 // all-reduce / optimizer interleave.
+static axonn_status optimizer_step_impl(axonn_ctx* c);
 AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
+  const axonn_status rc = optimizer_step_impl(c);
+  if (rc && rc != AXONN_ERR_NONFINITE && c && c->lg) c->lg->abort();
+  return rc;
+}
+
+static axonn_status optimizer_step_impl(axonn_ctx* c) {
   if (!c) return AXONN_ERR_INVALID_ARG;
   if (c->sticky) return AXONN_ERR_STATE;
   if (!c->grads_ready) return (axonn_status)c->fail(AXONN_ERR_STATE, "optimizer_step without run_batch");
@@ -1232,11 +1376,13 @@ AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
     if (nonfinite_scan(c->grad16, c->nflat, c->d_flag, c->s_dp))
       return (axonn_status)c->fail(AXONN_ERR_CUDA, "nonfinite scan");
     ++c->launches;
-    if (c->world > 1) NC(ncclAllReduce(c->d_flag, c->d_flag, 1, ncclInt32, ncclMax, c->world_comm, c->s_dp));
+    if (c->world > 1 && !c->lg) NC(ncclAllReduce(c->d_flag, c->d_flag, 1, ncclInt32, ncclMax, c->world_comm, c->s_dp));
     CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->s_dp));
     cudaEvent_t e = c->ev();
     CU(cudaEventRecord(e, c->s_dp));
     CU(cudaEventSynchronize(e));
+    if (c->lg && c->lg->rendezvous(nullptr, c->h_flag, group_timeout_s()))
+      return (axonn_status)c->fail(AXONN_ERR_STATE, "local group failed (overflow flag)");
     if (*c->h_flag) {   // nothing was updated; t stays; run_batch may follow
       c->grads_ready = false;
       c->ev_chunk.clear();

@@ -131,6 +131,10 @@ struct Ctx {
   uint32_t* peer_flags_next = nullptr;   // stage + 1's flags
   uint32_t* peer_flags_prev = nullptr;   // stage - 1's flags
   std::vector<void*> ipc_opened;
+  // test-only loopback transport (axonn_local_group, include/axonn.h): flags are host-mapped
+  // and observed by this context's host thread; loss / overflow flag reduced through the group
+  axonn_local_group* lg = nullptr;
+  volatile uint32_t* flags_host = nullptr;
   uint32_t msg_base = 0;              // sequence number base: messages of earlier batches
   cudaEvent_t ev_grads_ready = nullptr, ev_opt_done = nullptr, ev_loss = nullptr;
   std::vector<cudaEvent_t> ev_chunk;

@@ -31,6 +31,47 @@ class AxoNNError(RuntimeError):
         self.status = STATUS.get(code, str(code))
 
 
+class LocalGroup:
+    """Test-only loopback transport (include/axonn.h axonn_local_group_create): the G_inter
+    stages of one pipeline as contexts of this process, each created and driven by its own
+    thread (ctypes releases the GIL during library calls).  See ``run_stages``."""
+
+    def __init__(self, size: int, dtype: str = "bf16"):
+        self.lib = _lib.load(dtype)
+        self.size = size
+        self.handle = C.c_void_p()
+        rc = self.lib.axonn_local_group_create(size, C.byref(self.handle))
+        if rc != 0:
+            raise AxoNNError(rc, "axonn_local_group_create failed")
+
+    def free(self):
+        if self.handle:
+            self.lib.axonn_local_group_free(self.handle)
+            self.handle = C.c_void_p()
+
+
+def run_stages(fn, n: int):
+    """Call fn(i) for i in range(n) on n threads at once (the loopback stages' collective
+    calls); returns the results in order and re-raises the first exception."""
+    import threading
+    out, err = [None] * n, [None] * n
+
+    def body(i):
+        try:
+            out[i] = fn(i)
+        except BaseException as e:   # noqa: BLE001 -- re-raised in the caller
+            err[i] = e
+    th = [threading.Thread(target=body, args=(i,)) for i in range(n)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
 class AxoNN:
     """One g^{i,j} of the G_inter x G_data grid."""
 
@@ -42,7 +83,7 @@ class AxoNN:
                  overlap_next_batch: bool | None = None, checkpoint_interval: int = 0,
                  stage_balance: bool | str = False, stage_speed=None,
                  rank: int = 0, world_size: int = 1, device: int = 0, nccl_id: bytes | None = None,
-                 dtype: str = "bf16"):
+                 dtype: str = "bf16", local_group: "LocalGroup | None" = None):
         # the half format picks the library build (include/axonn.h axonn_dtype)
         self.lib = _lib.load(dtype)
         self.dtype = dtype
@@ -63,7 +104,9 @@ class AxoNN:
             self._speed = (C.c_double * g_inter)(*self.stage_speed)
             self.oc.stage_speed = self._speed
         self._id = C.create_string_buffer(nccl_id if nccl_id else b"\0" * 128, 128)
-        self.dist = _lib.Dist(rank, world_size, C.cast(self._id, C.c_void_p), device)
+        self._group = local_group    # keeps the loopback group alive as long as this context
+        self.dist = _lib.Dist(rank, world_size, C.cast(self._id, C.c_void_p), device,
+                              local_group.handle if local_group is not None else None)
         self.ctx = C.c_void_p()
         rc = self.lib.axonn_init(g_inter, g_data, microbatch, C.byref(self.mc), C.byref(self.oc),
                                  C.byref(self.dist), C.byref(self.ctx))

@@ -125,3 +125,22 @@ def adam_test_state(n: int, seed: int = 11):
     m[:k] = np.array([0.0, 0.0, 0.0, 0.0, 0.0, 1e-3, 0.0, 0.0], dtype=np.float32)[:k]
     theta[:k] = np.array([0.5, -0.5, 0.0, 1.0, 0.02, 0.0, -1.0, 0.0], dtype=np.float32)[:k]
     return theta, m, v, g
+
+
+def mixed_batch(distinct: np.ndarray, batch: int, seed: int = 5):
+    """A full-size parity batch built from a few distinct sequences without a period.
+
+    Row r of the batch is ``distinct[assign[r]]`` with ``assign`` drawn uniformly (seeded),
+    every distinct sequence used at least once.  The exact batch gradient is then the
+    multiplicity-weighted sum of the per-sequence gradients, which the oracle computes from
+    the distinct sequences alone; because the assignment has no period, a row, sample or
+    microbatch offset error changes the multiset of rows the GPU reads and hence the result
+    (a tiled [s0, s1, s0, s1, ...] batch hides every offset error by an even count).
+    Returns (tokens int32 [batch, s + 1], counts int64 [n_distinct])."""
+    n = distinct.shape[0]
+    assert batch >= n
+    rng = np.random.default_rng(seed)
+    assign = np.concatenate([np.arange(n), rng.integers(0, n, size=batch - n)])
+    rng.shuffle(assign)
+    counts = np.bincount(assign, minlength=n).astype(np.int64)
+    return np.ascontiguousarray(distinct[assign]).astype(np.int32), counts
