@@ -6,13 +6,20 @@ all-reduce over the column) + axonn_optimizer_step (AdamW over every
 parameter, bucketed, overlapped with the all-reduce chunks).  Nothing is
 skipped inside the timed region.
 
-Default workload (N = 1, and weak scaling for N > 1): BASELINE.json
-configs[1], the GPT 1.3B-shaped model (24 layers, hidden 2048, 16 heads,
-seq 512, vocab 51200), G_inter = 1, G_data = N, microbatch 32, 2 microbatches
-per replica (64 samples per GPU), optimizer state in HBM (no offload).  At
-G_inter = 1 the microbatch size only trades activation memory for GEMM size
-(b_m 8 / 16 / 32 / 64: 967-973 / 1015 / 1042 / 1053 TFLOP/s, 34 / 41 / 54 / 81
-GiB; profiles/r1/bench_1p3b_mb_sweep_r56.log).
+Default workload (`--config auto`):
+* N = 1: BASELINE.json configs[1], the GPT 1.3B-shaped model (24 layers, hidden 2048,
+  16 heads, seq 512, vocab 51200), G_inter = 1, microbatch 32, 2 microbatches (64 samples),
+  optimizer state in HBM.  At G_inter = 1 the microbatch size only trades activation memory
+  for GEMM size (b_m 8 / 16 / 32 / 64: 967-973 / 1015 / 1042 / 1053 TFLOP/s, 34 / 41 / 54 / 81
+  GiB; profiles/r1/bench_1p3b_mb_sweep_r56.log).
+* N >= 2: the north-star target, BASELINE.json configs[2]: the paper's 12B transformer shape
+  (Table I: h 4512, 24 heads) on the grid G_inter = min(4, N) x G_data =
+  N / G_inter with 12 layers per stage (4 x 2 at N = 8 is the 48-layer 12B model; 4 x 1 at
+  N = 4 the same stages without the second replica; 2 x 1 at N = 2 the SURVEY's 24-layer
+  2-GPU proxy), microbatch 8 (Table II), 64 microbatches per replica, bsize 4M,
+  k 4 (PAPER.md:846-847).  Offload off by default (the 12-layer stage fits in 180 GB);
+  `--offload 1` selects the bucketed pinned-host optimizer.  Weak scaling: per-GPU work is
+  one 12-layer stage of 64 microbatches at every N.
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Under torchrun every rank runs one GPU; rank 0 prints ONE JSON line.
@@ -46,6 +53,10 @@ def emit(out: dict) -> None:
 METRIC = "per-GPU model TFLOP/s and % of B200 bf16 peak at 1/2/4/8 GPUs; batch time"
 
 CONFIGS = {
+    # BASELINE.json configs[2]: the 12B transformer shape on the G_inter = min(4, N) x
+    # G_data = N / G_inter grid, 12 layers per stage (the 48-layer model at G_inter = 4)
+    "gpt12b": dict(layers_per_stage=12, hidden=4512, heads=24, seq_len=512, vocab=51200,
+                   g_inter="grid", microbatch=8, mb_per_replica=64, offload=False),
     # BASELINE.json configs[1]: GPT 1.3B-shaped, G_inter = 1, G_data = N, no offload
     "gpt1.3b": dict(n_layers=24, hidden=2048, heads=16, seq_len=512, vocab=51200,
                     g_inter=1, microbatch=32, mb_per_replica=2, offload=False),
@@ -183,12 +194,20 @@ def k1_traffic(cfg):
             "traffic_src": "profiles/r1/k1_traffic.json (ncu --set full, 1-layer microbatch)"}
 
 
-def cpu_oracle_sample(cfg, steps: int = 1):
-    """Time the oracle (as it stands) on a bounded sample of the same workload:
-    one transformer layer of the configured shape as a middle pipeline stage
-    (nn_shard.Forward + Backward, no embedding / head) on one full-length
-    sequence, fp64 numpy on the host cores.  Unit: model TFLOP/s of that layer
-    (72 s h^2 (1 + s/6h) per sequence)."""
+def _blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        n = [d.get("num_threads", 0) for d in threadpool_info() if d.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:   # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def oracle_layer_sample(cfg, steps: int = 1):
+    """One timed oracle sample of the configured workload: one transformer layer of the
+    configured shape as a middle pipeline stage (nn_shard.Forward + Backward, no embedding /
+    head) on one full-length sequence, fp64 numpy on the host cores.  Returns (seconds per
+    sample, model FLOPs of the sample = 72 s h^2 (1 + s/6h), description)."""
     from oracle import model as om
     from synth import init_params
     c = om.GPTConfig(n_layers=3, hidden=cfg["hidden"], heads=cfg["heads"], seq_len=cfg["seq_len"],
@@ -206,43 +225,90 @@ def cpu_oracle_sample(cfg, steps: int = 1):
         om.stage_backward(p, c, 1, 3, cache, dy)
     dt = (time.perf_counter() - t0) / steps
     fl = 72 * c.seq_len * c.hidden ** 2 + 12 * c.seq_len ** 2 * c.hidden
-    return dict(value=fl / dt / 1e12, unit="model TFLOP/s", cores=os.cpu_count(), kind="oracle",
-                sample=f"numpy fp64 oracle nn_shard Forward+Backward of one layer (h {c.hidden}, "
-                       f"a {c.heads}, s {c.seq_len}) on 1 x {c.seq_len} tokens, {dt:.2f} s/step")
+    desc = (f"numpy fp64 oracle nn_shard Forward+Backward of one layer (h {c.hidden}, a {c.heads}, "
+            f"s {c.seq_len}) on 1 x {c.seq_len} tokens")
+    return dt, fl, desc
+
+
+def cpu_baseline(cfg, batch_flops: float):
+    """the oracle as it stands, timed on the host cores (never the target).
+    value = item 2, the oracle's model TFLOP/s on one layer of the configured shape; beside it
+    the EXTRAPOLATED oracle time of the whole configured batch (model FLOPs / that rate), item 3
+    (oracle AdamW over 2^26 parameters, GB/s at 28 B/param) and item 1 (the full tiny step:
+    Alg. 1 + Alg. 2 over 2 x 1 virtual workers, 4 microbatches, plus its AdamW).  About 10-30 s."""
+    from oracle import adamw as oa
+    from oracle import hybrid as oh
+    from oracle import model as om
+    from synth import init_params, markov_tokens
+    dt, fl, desc = oracle_layer_sample(cfg, 1)
+    rate = fl / dt
+    # item 3: AdamW over 2^26 fp32 parameters (in place), bf16 gradients
+    n = 1 << 26
+    rng = np.random.default_rng(3)
+    th = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    mm = np.zeros(n, np.float32)
+    vv = np.zeros(n, np.float32)
+    g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    t0 = time.perf_counter()
+    oa.adamw_step_fp32(th, mm, vv, g, oa.step_scalars(1))
+    t_adam = time.perf_counter() - t0
+    del th, mm, vv, g
+    # item 1: the full tiny step (BASELINE.json configs[0]) on 2 x 1 virtual workers
+    tc = om.GPTConfig(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=256)
+    tp = {k: v.astype(np.float64) for k, v in init_params(2, 64, 32, 256, seed=42).items()}
+    tok = markov_tokens(8, 32, 256, seed=7)
+    t0 = time.perf_counter()
+    _, tg = oh.hybrid_step(tp, tc, tok, 2, 1, 2)
+    sc = oa.step_scalars(1)
+    for k, v in tp.items():
+        t32 = v.astype(np.float32)
+        oa.adamw_step_fp32(t32, np.zeros_like(t32), np.zeros_like(t32), tg[k].astype(np.float32), sc)
+    t_tiny = time.perf_counter() - t0
+    return dict(value=rate / 1e12, unit="model TFLOP/s", cores=_blas_threads(), kind="oracle",
+                sample=f"{desc}, {dt:.2f} s/sample",
+                extrapolated_batch_s=batch_flops / rate,
+                adamw_gbs=28.0 * n / t_adam / 1e9, adamw_params=n,
+                tiny_step_s=t_tiny, host_cpus=os.cpu_count())
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the oracle (this tier's reference arm) on the host."""
+    """--impl reference: the oracle (this tier's reference arm) on the host, rank 0 only.
+    Every step is one bounded oracle sample of the configured workload (oracle_layer_sample);
+    W untimed + K timed samples, so steps x ms_per_step is the timed wall time."""
     if rank != 0:
         return
-    # bounded: one warm-up sample and at most 4 timed samples (a few minutes on 16 cores)
-    steps_total = min(args.warmup, 1) + min(args.steps, 4)
-    if args.warmup:
-        cpu_oracle_sample(cfg, 1)
-    res = cpu_oracle_sample(cfg, min(args.steps, 4))
-    v = res["value"]
-    sample_flops = 72 * cfg["seq_len"] * cfg["hidden"] ** 2 + 12 * cfg["seq_len"] ** 2 * cfg["hidden"]
-    ms = sample_flops / (v * 1e12) * 1e3
+    for _ in range(args.warmup):
+        oracle_layer_sample(cfg, 1)
+    t0 = time.perf_counter()
+    dts = []
+    for _ in range(args.steps):
+        dt, fl, desc = oracle_layer_sample(cfg, 1)
+        dts.append(dt)
+    wall = time.perf_counter() - t0
+    ms = wall * 1e3 / max(args.steps, 1)
+    v = fl / (ms / 1e3) / 1e12
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "model TFLOP/s (all GPUs)",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "timed_wall_s": wall,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic",
            "config": {"workload": args.config, "global_batch": 1, "seq_len": cfg["seq_len"],
-                      "parallelism": "cpu oracle", "sample": res["sample"]},
-           "cpu_baseline": res,
+                      "parallelism": "cpu oracle", "sample": desc},
+           "cpu_baseline": {"value": v, "unit": "model TFLOP/s", "cores": _blas_threads(),
+                            "kind": "oracle", "sample": f"{desc}, one sample per step"},
            "e2e": {"value": v, "unit": "model TFLOP/s (all GPUs)", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     emit(out)
-    _ = steps_total
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="gpt1.3b", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="auto", choices=["auto"] + sorted(CONFIGS),
+                    help="auto: gpt1.3b at N = 1, gpt12b (G_inter = min(4, N) grid) at N >= 2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--layers", type=int, default=None, help="override n_layers (profiling runs only)")
@@ -265,10 +331,25 @@ def main():
                     help="static loss scale S (default 1 for bf16, 1024 for fp16)")
     ap.add_argument("--g-inter", type=int, default=None,
                     help="pipeline stages (pipeline configs; G_data = N / G_inter)")
-    args = ap.parse_args()
+    ap.add_argument("--coarsen-k", type=int, default=4,
+                    help="all-reduce chunk = k * bsize elements (PAPER.md:731-737; paper 4)")
+    ap.add_argument("--bucket-elems", type=int, default=4_000_000,
+                    help="optimizer bucket bsize in elements (PAPER.md:683; paper 4M)")
+    args = ap.parse_args(argv)
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.stage_balance is None:
         args.stage_balance = int(args.checkpoint_interval in (0, 1))
-    cfg = dict(CONFIGS[args.config])
+    args.config, cfg = resolve_config(args, world_env)
+    return args, cfg
+
+
+def resolve_config(args, world: int):
+    """(workload name, config dict) the run measures: --config auto picks gpt1.3b at N = 1 and
+    the north-star 12B grid (G_inter = min(4, N) x G_data = N / G_inter) at N >= 2."""
+    name = args.config
+    if name == "auto":
+        name = "gpt1.3b" if world == 1 else "gpt12b"
+    cfg = dict(CONFIGS[name])
     if args.layers:
         cfg["n_layers"] = args.layers
     if args.mb_per_replica:
@@ -278,9 +359,16 @@ def main():
     if args.offload is not None:
         cfg["offload"] = bool(args.offload)
     if cfg.get("g_inter") == "N":   # pipeline proxies: one stage per GPU unless --g-inter
-        cfg["g_inter"] = args.g_inter or int(os.environ.get("WORLD_SIZE", "1"))
+        cfg["g_inter"] = args.g_inter or world
         cfg.setdefault("n_layers", cfg["layers_per_stage"] * cfg["g_inter"])
+    elif cfg.get("g_inter") == "grid":   # north-star grid: G_inter = min(4, N)
+        cfg["g_inter"] = args.g_inter or min(4, world)
+        cfg.setdefault("n_layers", cfg["layers_per_stage"] * cfg["g_inter"])
+    return name, cfg
 
+
+def main(argv=None):
+    args, cfg = parse_args(argv)
     from paper_2110_13005_b200 import dist as D
     rank, world, local = D.env_rank_world()
     if world == 1 and args.gpus > 1:
@@ -303,7 +391,8 @@ def main():
                 offload=cfg["offload"], rank=rank, world_size=world, device=local, nccl_id=nid,
                 checkpoint_interval=args.checkpoint_interval, dtype=args.dtype,
                 stage_balance="calibrate" if args.stage_balance == 2 else bool(args.stage_balance),
-                pipeline_limit=args.pipeline_limit,
+                pipeline_limit=args.pipeline_limit, coarsen_k=args.coarsen_k,
+                bucket_elems=args.bucket_elems,
                 overlap_next_batch=None if args.overlap_next_batch is None else bool(args.overlap_next_batch),
                 loss_scale=args.loss_scale or (1024.0 if args.dtype == "fp16" else 1.0))
     from synth import uniform_tokens
@@ -321,13 +410,8 @@ def main():
         eng.optimizer_step()
     torch.cuda.synchronize()
 
-    # timed region: K steps with device-resident inputs; the K1 / K2 / K9 launches of the
-    # LAST timed step are bracketed by CUDA events on their launching streams (roofline and
-    # per-shape numbers; the profiled microbatch runs its weight gradients in order, so only
-    # one step of the K pays for it)
-    gemm_ms = gemm_flop = adam_ms = adam_bytes = 0.0
+    # timed region: K plain steps with device-resident inputs (no instrumentation)
     ph = {"t_pipe_ms": 0.0, "t_busy_ms": 0.0, "t_allreduce_ms": 0.0, "t_opt_exposed_ms": 0.0}
-    breakdown = {}
     launches = 0
     D.barrier(world)
     torch.cuda.synchronize()
@@ -335,35 +419,16 @@ def main():
         eng.timer_mark(0)
         losses = []
         for step in range(args.steps):
-            prof = step == args.steps - 1
-            nvtx = prof and os.environ.get("AXONN_NVTX") == "1"   # ncu --nvtx-include timed_step/
-            if prof:
-                eng.set_profiling(True)
-            if nvtx:
-                torch.cuda.nvtx.range_push("timed_step")
             losses.append(eng.run_batch_device(d_tok.data_ptr(), B))
             eng.optimizer_step()
-            if nvtx:
-                torch.cuda.nvtx.range_pop()
             st = eng.stats()
             launches += int(st["kernel_launches"])
             for k in ph:
                 ph[k] += st[k] / args.steps
-            if prof:
-                gemm_ms += st["gemm_ms"]
-                gemm_flop += st["gemm_flop"]
-                adam_ms += st["adam_ms"]
-                adam_bytes += st["adam_bytes"]
-                for k, (kms, kw, kn) in eng.profile().items():
-                    acc = breakdown.setdefault(k, [0.0, 0.0, 0])
-                    acc[0] += kms
-                    acc[1] += kw
-                    acc[2] += kn
         eng.timer_mark(1)
         dev_ms = eng.timer_elapsed_ms(0, 1)
     torch.cuda.synchronize()
     D.barrier(world)
-    eng.set_profiling(False)
     dev_ms = D.max_over_ranks(dev_ms, world)
     bubble = 1.0 - ph["t_busy_ms"] / ph["t_pipe_ms"] if ph["t_pipe_ms"] > 0 else 0.0
     bubble_ranks = D.gather_to_all(bubble, world)   # every rank joins the collective
@@ -371,6 +436,34 @@ def main():
     ms_step = dev_ms / args.steps
     fl = model_flops(B, s, cfg["n_layers"], cfg["hidden"], V)
     value = fl / (ms_step / 1e3) / 1e12                       # whole-job model TFLOP/s
+
+    # one extra, instrumented step AFTER the timed region: the K1 / K2 launches of its last
+    # microbatch and its K9 launches are bracketed by CUDA events on their launching streams
+    # (roofline and per-shape numbers; the profiled microbatch runs its weight gradients in
+    # order on the compute stream so each event pair times one launch)
+    overlap = cfg["offload"] if args.overlap_next_batch is None else bool(args.overlap_next_batch)
+    eng.set_profiling(True)
+    nvtx = os.environ.get("AXONN_NVTX") == "1"   # ncu --nvtx-include profiled_step/
+    if nvtx:
+        torch.cuda.nvtx.range_push("profiled_step")
+    eng.run_batch_device(d_tok.data_ptr(), B)
+    eng.optimizer_step()
+    if nvtx:
+        torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
+    st = eng.stats()
+    gemm_ms, gemm_flop = st["gemm_ms"], st["gemm_flop"]
+    adam_ms, adam_bytes = st["adam_ms"], st["adam_bytes"]
+    breakdown = {k: list(v) for k, v in eng.profile().items()}
+    eng.set_profiling(False)
+    if overlap:   # the overlapped optimizer's records complete during the next batch
+        eng.run_batch_device(d_tok.data_ptr(), B)
+        eng.optimizer_step()
+        st2 = eng.stats()
+        adam_ms, adam_bytes = st2["adam_ms"], st2["adam_bytes"]
+        for k, v in eng.profile().items():
+            if k == "adamw":
+                breakdown[k] = list(v)
 
     # e2e: through the public C-ABI with HOST tokens; H2D of the shard + D2H of
     # the loss happen inside axonn_run_batch every step
@@ -388,7 +481,7 @@ def main():
     peaks = load_peaks()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:   # the CPU baseline is an N = 1 figure
-        cpu = cpu_oracle_sample(cfg, 1)
+        cpu = cpu_baseline(cfg, fl)
     if rank == 0:
         gemm_tf = gemm_flop / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
         out = {
@@ -442,7 +535,8 @@ def main():
                          "peak_src": peaks["src"] + " bf16_tflops_sustained (kernel timed inside a long step)",
                          # events bracket the K1 launches of the LAST microbatch of every
                          # timed step (same shapes each microbatch); share scaled by m
-                         "events": "K1 launches of the last microbatch of the last timed step",
+                         "events": "K1 launches of the last microbatch of one instrumented step "
+                                   "run after the timed region",
                          "gemm_share_of_step": gemm_ms * m / ms_step,
                          **k1_traffic(cfg)},
             "adam": {"achieved_gbs": adam_bytes / (adam_ms / 1e3) / 1e9 if adam_ms else None,

@@ -23,3 +23,31 @@ def test_reference_arm_prints_one_json_line():
     assert d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_reference_arm_reports_the_steps_it_ran():
+    """The reference line's steps x ms_per_step is its measured timed wall time (every step is
+    one oracle sample; nothing is extrapolated or skipped)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--config", "tiny", "--steps", "3", "--warmup", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["steps"] == 3 and d["warmup"] == 1
+    assert abs(d["steps"] * d["ms_per_step"] / 1e3 - d["timed_wall_s"]) <= 1e-6 * d["timed_wall_s"] + 1e-9
+
+
+def test_default_workload_per_gpu_count(monkeypatch):
+    """--config auto: gpt1.3b (configs[1]) at N = 1; the north-star 12B grid (configs[2]) at
+    N >= 2: 2 x 1 (24 layers), 4 x 1 (48), 4 x 2 (48) at N = 2, 4, 8 -- 12 layers per stage."""
+    sys.path.insert(0, ROOT)
+    import bench
+    want = {1: ("gpt1.3b", 1, 24, 1), 2: ("gpt12b", 2, 24, 1), 4: ("gpt12b", 4, 48, 1),
+            8: ("gpt12b", 4, 48, 2)}
+    for n, (name, gi, layers, gd) in want.items():
+        monkeypatch.setenv("WORLD_SIZE", str(n))
+        args, cfg = bench.parse_args([])
+        assert (args.config, cfg["g_inter"], cfg["n_layers"], n // cfg["g_inter"]) == (name, gi, layers, gd)
+        if name == "gpt12b":
+            assert cfg["hidden"] == 4512 and cfg["heads"] == 24 and cfg["microbatch"] == 8
+            assert cfg["mb_per_replica"] == 64
