@@ -658,7 +658,8 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
       return bail(c->fail(AXONN_ERR_CUDA, "kernel preload failed"));
   }
   for (cudaStream_t* st : {&c->s_comp, &c->s_send_act, &c->s_send_grad, &c->s_recv_act,
-                           &c->s_recv_grad, &c->s_dp, &c->s_h2d, &c->s_d2h, &c->s_opt, &c->s_wg})
+                           &c->s_recv_grad, &c->s_dp, &c->s_h2d, &c->s_d2h, &c->s_opt, &c->s_wg,
+                           &c->s_loss})
     if ((rc = c->check_cuda(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking), "stream")))
       return bail(rc);
   for (cudaEvent_t* e : {&c->ev_grads_ready, &c->ev_opt_done, &c->ev_loss})
@@ -778,7 +779,7 @@ AXONN_API void axonn_free(axonn_ctx* c) {
     for (cudaEvent_t e : {c->ev_h2d[r], c->ev_adam[r], c->ev_d2h[r]})
       if (e) cudaEventDestroy(e);
   for (cudaStream_t st : {c->s_comp, c->s_send_act, c->s_send_grad, c->s_recv_act, c->s_recv_grad,
-                          c->s_dp, c->s_h2d, c->s_d2h, c->s_opt, c->s_wg})
+                          c->s_dp, c->s_h2d, c->s_d2h, c->s_opt, c->s_wg, c->s_loss})
     if (st) cudaStreamDestroy(st);
   delete c;
 }
@@ -971,13 +972,15 @@ int Ctx::ar_ready(int64_t lo) {
   const int64_t ch = (int64_t)oc.coarsen_k * oc.bucket_elems;
   while (ar_next_chunk >= 0 && ar_next_chunk * ch >= lo) {
     const int64_t c0 = ar_next_chunk * ch, n = std::min(ch, nflat - c0);
-    if ((rc = check_nccl(ncclAllReduce(static_cast<char*>(grad16) + c0 * 2, static_cast<char*>(grad16) + c0 * 2, n,
-                                       kNcclHalf, ncclSum, dp_comm, s_dp), "ncclAllReduce")))
-      return rc;
+    if (g_data > 1) {   // Alg. 1 l.13: SUM over the column (pre-divided loss, D-10)
+      if ((rc = check_nccl(ncclAllReduce(static_cast<char*>(grad16) + c0 * 2, static_cast<char*>(grad16) + c0 * 2,
+                                         n, kNcclHalf, ncclSum, dp_comm, s_dp), "ncclAllReduce")))
+        return rc;
+      stats[AXONN_STAT_ALLREDUCE_BYTES] += n * 2.0;
+    }
     cudaEvent_t e = ev();
     if ((rc = check_cuda(cudaEventRecord(e, s_dp), "ar ev"))) return rc;
     ev_chunk[ar_next_chunk] = e;
-    stats[AXONN_STAT_ALLREDUCE_BYTES] += n * 2.0;
     --ar_next_chunk;
   }
   return 0;
@@ -1213,6 +1216,9 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
     c->stats[AXONN_STAT_H2D_BYTES] += need * 4.0;
   }
   CU(cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->s_comp));
+  // the batch loss is final after the last stage's last forward (recorded there); the other
+  // stages contribute 0 (C5)
+  if (!c->last) CU(cudaEventRecord(c->ev_loss, c->s_comp));
   if (c->first) {   // embedding gradients are scatter-added (K6)
     CU(cudaMemsetAsync(c->g32(c->tok_emb), 0, (size_t)c->V * c->h * 4, c->s_comp));
     CU(cudaMemsetAsync(c->g32(c->pos_emb), 0, (size_t)c->s * c->h * 4, c->s_comp));
@@ -1225,7 +1231,8 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   c->msg_ev.clear();
   CU(cudaEventRecord(c->ph[par][0], c->s_comp));
   const int64_t ch_elems = chunk_elems(c);
-  c->ar_overlap = c->g_data > 1 && !(getenv("AXONN_AR_OVERLAP") && getenv("AXONN_AR_OVERLAP")[0] == '0');
+  // AXONN_AR_OVERLAP=0: cast and reduce everything after the pipeline instead (same values)
+  c->ar_overlap = !(getenv("AXONN_AR_OVERLAP") && getenv("AXONN_AR_OVERLAP")[0] == '0');
   c->ar_active = false;
   c->ev_chunk.clear();
   if (c->ar_overlap) {
@@ -1239,7 +1246,7 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   if (c->ar_overlap) {
     if ((rc = c->ar_ready(0))) return (axonn_status)rc;   // no-op unless a stage had no layers
     c->ar_active = false;
-    CU(cudaEventRecord(c->ev_grads_ready, c->s_comp));
+    CU(cudaEventRecord(c->ev_grads_ready, c->s_dp));   // every chunk cast (and reduced)
   } else {
     // grad16 is still read by a pending optimizer step until it completes
     if (c->opt_pending) CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
@@ -1248,14 +1255,13 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
     ++c->launches;
     CU(cudaEventRecord(c->ev_grads_ready, c->s_comp));
   }
-  if (c->g_data == 1) CU(cudaEventRecord(c->ph[par][2], c->s_comp));
-  CU(cudaEventRecord(c->ev_loss, c->s_comp));
-  CU(cudaStreamWaitEvent(c->s_dp, c->ev_loss, 0));
+  if (c->g_data == 1 && !c->ar_overlap) CU(cudaEventRecord(c->ph[par][2], c->s_comp));
+  CU(cudaStreamWaitEvent(c->s_loss, c->ev_loss, 0));
   if (c->world > 1 && !c->lg)   // C5: loss sum over the last-stage ranks, seen by every rank
-    NC(ncclAllReduce(c->d_loss, c->d_loss, 1, ncclFloat64, ncclSum, c->world_comm, c->s_dp));
-  CU(cudaMemcpyAsync(c->h_loss, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->s_dp));
+    NC(ncclAllReduce(c->d_loss, c->d_loss, 1, ncclFloat64, ncclSum, c->world_comm, c->s_loss));
+  CU(cudaMemcpyAsync(c->h_loss, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->s_loss));
   cudaEvent_t ev_loss_host = c->ev();
-  CU(cudaEventRecord(ev_loss_host, c->s_dp));
+  CU(cudaEventRecord(ev_loss_host, c->s_loss));
   // Alg. 1 l.13: SUM all-reduce over the column, chunks of k * bsize
   if (c->ar_overlap) {
     CU(cudaEventRecord(c->ph[par][2], c->s_dp));
@@ -1279,37 +1285,9 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   // the row losses are summed unscaled (the S of D-11 enters only the CE gradient): L/S
   if (loss_out) *loss_out = (float)(*c->h_loss);
   c->grads_ready = true;
-  {   // device-timed phase of this batch (every s_comp event has completed: loss synced)
-    float ms = 0;
-    cudaEventElapsedTime(&ms, c->ph[par][0], c->ph[par][1]);
-    c->stats[AXONN_STAT_T_PIPE_MS] = ms;
-    double busy = 0;
-    for (auto& pr : c->busy_ev) {
-      float b = 0;
-      cudaEventElapsedTime(&b, pr.first, pr.second);
-      busy += b;
-    }
-    c->stats[AXONN_STAT_T_BUSY_MS] = busy;
-    if (const char* tl = getenv("AXONN_TIMELINE")) {   // per-op timeline of this batch (diagnostics)
-      std::string path = std::string(tl) + ".rank" + std::to_string(c->rank) + ".csv";
-      if (FILE* f = fopen(path.c_str(), "w")) {
-        fprintf(f, "stage,kind,mb,start_ms,end_ms\n");
-        for (size_t k = 0; k < c->busy_ev.size() && k < c->busy_tag.size(); ++k) {
-          float a = 0, b = 0;
-          cudaEventElapsedTime(&a, c->ph[par][0], c->busy_ev[k].first);
-          cudaEventElapsedTime(&b, c->ph[par][0], c->busy_ev[k].second);
-          fprintf(f, "%d,%c,%d,%.4f,%.4f\n", c->stage, (c->busy_tag[k] & 1) ? 'B' : 'F', c->busy_tag[k] / 2, a, b);
-        }
-        for (auto& me : c->msg_ev) {
-          float a = 0;
-          if (cudaEventElapsedTime(&a, c->ph[par][0], me.second) == cudaSuccess)
-            fprintf(f, "%d,%s,%d,%.4f,%.4f\n", c->stage, (me.first & 1) ? "msg_grad" : "msg_act", me.first / 2, a, a);
-        }
-        fclose(f);
-      }
-    }
-  }
-  if (c->opt_pending) {   // the previous step has completed (the cast above waited for it)
+  c->pipe_stats_par = par;   // phase statistics once the pipeline has drained (Ctx::pipe_stats)
+  if (c->opt_pending) {   // the previous step (every forward of this batch waited for it)
+    cudaEventSynchronize(c->ev_opt_done);
     c->opt_pending = false;
     c->collect_stats();
     c->prof_opt.clear();
@@ -1365,8 +1343,9 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
   sc[6] = (float)std::sqrt(1.0 - std::pow(b2, (double)t));
   sc[7] = (float)c->oc.eps;   // eps rounded once
   sc[8] = (float)(1.0 / c->oc.loss_scale);
-  // the optimizer may start only once the gradients exist
-  CU(cudaStreamWaitEvent(c->s_opt, c->ev_grads_ready, 0));
+  // the optimizer may start only once the gradients exist: per chunk (ev_chunk, A8) or, without
+  // chunk events, all of them
+  if (c->ev_chunk.empty()) CU(cudaStreamWaitEvent(c->s_opt, c->ev_grads_ready, 0));
   if (kHalfDtype == AXONN_FP16) {
     // Reading D-12: skip the whole step if any reduced gradient of any stage overflowed.
     // The flag needs the complete all-reduce (s_dp is past its last chunk), then one
@@ -1376,10 +1355,15 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
     if (nonfinite_scan(c->grad16, c->nflat, c->d_flag, c->s_dp))
       return (axonn_status)c->fail(AXONN_ERR_CUDA, "nonfinite scan");
     ++c->launches;
-    if (c->world > 1 && !c->lg) NC(ncclAllReduce(c->d_flag, c->d_flag, 1, ncclInt32, ncclMax, c->world_comm, c->s_dp));
-    CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->s_dp));
+    {   // the world comm's collectives all run on s_loss (issue order = the loss, then this)
+      cudaEvent_t es = c->ev();
+      CU(cudaEventRecord(es, c->s_dp));
+      CU(cudaStreamWaitEvent(c->s_loss, es, 0));
+    }
+    if (c->world > 1 && !c->lg) NC(ncclAllReduce(c->d_flag, c->d_flag, 1, ncclInt32, ncclMax, c->world_comm, c->s_loss));
+    CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->s_loss));
     cudaEvent_t e = c->ev();
-    CU(cudaEventRecord(e, c->s_dp));
+    CU(cudaEventRecord(e, c->s_loss));
     CU(cudaEventSynchronize(e));
     if (c->lg && c->lg->rendezvous(nullptr, c->h_flag, group_timeout_s()))
       return (axonn_status)c->fail(AXONN_ERR_STATE, "local group failed (overflow flag)");
@@ -1396,7 +1380,6 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
   const int64_t bs = c->oc.bucket_elems;
   const int64_t ch = chunk_elems(c);
   int64_t chunk_idx = -1;
-  int64_t bucket = 0;
   const bool overlap = c->oc.overlap_next_batch != 0;
   c->ev_next_opt = 0;
   if (overlap) {
@@ -1407,20 +1390,39 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
       c->ev_bucket.push_back(e);
     }
   }
-  int64_t pend_lo = 0;   // in-HBM: first element not yet handed to a launch
-  for (int64_t lo = 0; lo < c->nflat; lo += bs, ++bucket) {
+  // Bucket order (A8).  With chunk events and no next-batch overlap the
+  // buckets run in chunk-completion order: chunks are handed off top-first during the last
+  // backward (Ctx::ar_ready), so chunk c_max's buckets start first, each chunk's buckets in
+  // ascending order, each waiting only for its own chunk -- the update of the top layers runs
+  // while the rest of the backward and of the column all-reduce are still in flight.  With
+  // overlap_next_batch the next batch's forward needs layer 0 first: ascending order.
+  const int64_t nbk = (c->nflat + bs - 1) / bs;
+  std::vector<int64_t> order;
+  order.reserve(nbk);
+  const bool by_chunk = !overlap && !c->ev_chunk.empty();
+  if (by_chunk) {
+    const int64_t kpc = ch / bs;   // buckets per chunk (ch = k * bsize)
+    for (int64_t ci = (int64_t)c->ev_chunk.size() - 1; ci >= 0; --ci)
+      for (int64_t b = ci * kpc; b < std::min(nbk, (ci + 1) * kpc); ++b) order.push_back(b);
+  } else {
+    for (int64_t b = 0; b < nbk; ++b) order.push_back(b);
+  }
+  int64_t pend_lo = -1;   // in-HBM: first element of the run not yet handed to a launch
+  for (size_t q = 0; q < order.size(); ++q) {
+    const int64_t bucket = order[q];
+    const int64_t lo = bucket * bs;
     const int64_t n = std::min(bs, c->nflat - lo);
     const int64_t ci = lo / ch;
     if (ci != chunk_idx && ci < (int64_t)c->ev_chunk.size()) {   // bucket waits for its chunk
-      CU(cudaStreamWaitEvent(c->s_opt, c->ev_chunk[ci], 0));
+      if (c->ev_chunk[ci]) CU(cudaStreamWaitEvent(c->s_opt, c->ev_chunk[ci], 0));
       chunk_idx = ci;
     }
-    const void* g = static_cast<const char*>(c->grad16) + lo * 2;
     void* t16 = static_cast<char*>(c->theta16) + lo * 2;
+    const void* g = static_cast<const char*>(c->grad16) + lo * 2;
     ProfRec pr{};
     if (c->oc.offload) {   // fetch bucket, step, offload back; 3-slot ring
-      const int r = (int)(bucket % 3);
-      if (bucket >= 3) CU(cudaStreamWaitEvent(c->s_h2d, c->ev_d2h[r], 0));
+      const int r = (int)(q % 3);
+      if (q >= 3) CU(cudaStreamWaitEvent(c->s_h2d, c->ev_d2h[r], 0));
       CU(cudaMemcpyAsync(c->ring[r][0], c->master + lo, n * 4, cudaMemcpyHostToDevice, c->s_h2d));
       CU(cudaMemcpyAsync(c->ring[r][1], c->adam_m + lo, n * 4, cudaMemcpyHostToDevice, c->s_h2d));
       CU(cudaMemcpyAsync(c->ring[r][2], c->adam_v + lo, n * 4, cudaMemcpyHostToDevice, c->s_h2d));
@@ -1439,30 +1441,28 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
       CU(cudaEventRecord(c->ev_d2h[r], c->s_d2h));
       c->stats[AXONN_STAT_H2D_BYTES] += n * 12.0;
       c->stats[AXONN_STAT_D2H_BYTES] += n * 12.0;
-    } else {
-      // In HBM the bucket is only a scheduling unit: consecutive buckets that wait for the
-      // same all-reduce chunk (all of them when G_data = 1) run as one launch (same values;
-      // AdamW is elementwise), unless the next batch overlaps and needs per-bucket events.
-      const int64_t end = lo + n;
-      const bool chunk_ends = !c->ev_chunk.empty() && (end >= c->nflat || end / ch != ci);
-      if (overlap || end >= c->nflat || chunk_ends) {
-        const int64_t n2 = end - pend_lo;
-        const void* g2 = static_cast<const char*>(c->grad16) + pend_lo * 2;
-        void* t2 = static_cast<char*>(c->theta16) + pend_lo * 2;
-        if (c->profiling) { pr.a = c->ev_opt(); pr.b = c->ev_opt(); cudaEventRecord(pr.a, c->s_opt); }
-        if (adamw_launch(n2, g2, c->master + pend_lo, c->adam_m + pend_lo, c->adam_v + pend_lo, t2, sc,
-                         c->s_opt))
-          return (axonn_status)c->fail(AXONN_ERR_CUDA, "adamw launch");
-        if (c->profiling) { cudaEventRecord(pr.b, c->s_opt); pr.work = n2 * 28.0; pr.kind = 1; c->prof.push_back(pr); }
-        if (overlap) CU(cudaEventRecord(c->ev_bucket[bucket], c->s_opt));
-        pend_lo = end;
-        ++c->launches;
-      }
-      (void)g;
-      (void)t16;
+      ++c->launches;
       continue;
     }
-    ++c->launches;
+    // In HBM the bucket is only a scheduling unit: consecutive buckets that wait for the same
+    // chunk (all of them when there are no chunk events) run as one launch (same values;
+    // AdamW is elementwise), unless the next batch overlaps and needs per-bucket events.
+    if (pend_lo < 0) pend_lo = lo;
+    const int64_t end = lo + n;
+    const bool run_ends = q + 1 == order.size() || order[q + 1] != bucket + 1 ||
+                          (!c->ev_chunk.empty() && (order[q + 1] * bs) / ch != ci);
+    if (overlap || run_ends) {
+      const int64_t n2 = end - pend_lo;
+      const void* g2 = static_cast<const char*>(c->grad16) + pend_lo * 2;
+      void* t2 = static_cast<char*>(c->theta16) + pend_lo * 2;
+      if (c->profiling) { pr.a = c->ev_opt(); pr.b = c->ev_opt(); cudaEventRecord(pr.a, c->s_opt); }
+      if (adamw_launch(n2, g2, c->master + pend_lo, c->adam_m + pend_lo, c->adam_v + pend_lo, t2, sc, c->s_opt))
+        return (axonn_status)c->fail(AXONN_ERR_CUDA, "adamw launch");
+      if (c->profiling) { cudaEventRecord(pr.b, c->s_opt); pr.work = n2 * 28.0; pr.kind = 1; c->prof.push_back(pr); }
+      if (overlap) CU(cudaEventRecord(c->ev_bucket[bucket], c->s_opt));
+      pend_lo = -1;
+      ++c->launches;
+    }
   }
   if (c->oc.offload) {
     cudaEvent_t e = c->ev();
@@ -1476,6 +1476,7 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
   c->t_step = t;
   c->grads_ready = false;
   c->ev_chunk.clear();
+  c->pipe_stats(c->pipe_stats_par);
   if (overlap) {   // returns now; the next run_batch waits per layer (reading D-32)
     for (ProfRec& p : c->prof)
       if (p.kind == 1) c->prof_opt.push_back(p);
@@ -1498,6 +1499,44 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
 }  // extern "C"
 
 namespace axonn {
+
+// Device-timed Alg. 2 phase of batch `par` (PAPER.md:704-708 phase bars): waits until the
+// pipeline has drained on s_comp (run_batch returns once the loss is known, possibly before
+// its last backward has finished), then reads the phase and busy-span events.
+void Ctx::pipe_stats(int par) {
+  Ctx* c = this;
+  if (par < 0 || !c->ph[par][1]) return;
+  pipe_stats_par = -1;
+  cudaEventSynchronize(c->ph[par][1]);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c->ph[par][0], c->ph[par][1]);
+  c->stats[AXONN_STAT_T_PIPE_MS] = ms;
+  double busy = 0;
+  for (auto& pr : c->busy_ev) {
+    float b = 0;
+    cudaEventElapsedTime(&b, pr.first, pr.second);
+    busy += b;
+  }
+  c->stats[AXONN_STAT_T_BUSY_MS] = busy;
+  if (const char* tl = getenv("AXONN_TIMELINE")) {   // per-op timeline of this batch (diagnostics)
+    std::string path = std::string(tl) + ".rank" + std::to_string(c->rank) + ".csv";
+    if (FILE* f = fopen(path.c_str(), "w")) {
+      fprintf(f, "stage,kind,mb,start_ms,end_ms\n");
+      for (size_t k = 0; k < c->busy_ev.size() && k < c->busy_tag.size(); ++k) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, c->ph[par][0], c->busy_ev[k].first);
+        cudaEventElapsedTime(&b, c->ph[par][0], c->busy_ev[k].second);
+        fprintf(f, "%d,%c,%d,%.4f,%.4f\n", c->stage, (c->busy_tag[k] & 1) ? 'B' : 'F', c->busy_tag[k] / 2, a, b);
+      }
+      for (auto& me : c->msg_ev) {
+        float a = 0;
+        if (cudaEventElapsedTime(&a, c->ph[par][0], me.second) == cudaSuccess)
+          fprintf(f, "%d,%s,%d,%.4f,%.4f\n", c->stage, (me.first & 1) ? "msg_grad" : "msg_act", me.first / 2, a, a);
+      }
+      fclose(f);
+    }
+  }
+}
 
 void Ctx::phase_stats_ar_opt(int par) {
   if (!ph[par][1] || !ph[par][2] || !ph[par][3]) return;

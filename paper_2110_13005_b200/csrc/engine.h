@@ -111,6 +111,9 @@ struct Ctx {
   cudaStream_t s_comp = nullptr, s_send_act = nullptr, s_send_grad = nullptr,
                s_recv_act = nullptr, s_recv_grad = nullptr, s_dp = nullptr, s_h2d = nullptr,
                s_d2h = nullptr, s_opt = nullptr;
+  // batch loss (C5): its world all-reduce and D2H run here, off s_dp, so run_batch can return
+  // once the loss is known while the gradient chunks are still being reduced on s_dp
+  cudaStream_t s_loss = nullptr;
   // weight-gradient side stream: dW GEMMs and bias column sums of the backward run here,
   // concurrently with the data-gradient chain on s_comp (fills GEMM tail waves)
   cudaStream_t s_wg = nullptr;
@@ -162,11 +165,16 @@ struct Ctx {
   std::vector<int> busy_tag;          // 2 mb (+1 for a Backward) per busy span
   std::vector<std::pair<int, cudaEvent_t>> msg_ev;   // message landed: (2 mb (+1 grad), event)
   void phase_stats_ar_opt(int par);
-  // Column all-reduce overlapped with the batch's last backward (G_data > 1, reading D-32):
-  // as each layer's gradients become final (reverse layer order = descending flat index) its
-  // range is cast to the half format on s_dp and every all-reduce chunk (k * bsize elements,
-  // PAPER.md:731-737) lying wholly above the frontier is issued, top chunk first.
-  bool ar_overlap = false;            // this batch reduces chunk by chunk during the last backward
+  int pipe_stats_par = -1;            // batch whose pipeline phase statistics are pending
+  void pipe_stats(int par);
+  // Chunked gradient hand-off during the batch's last backward (reading D-32): as each layer's
+  // gradients become final (reverse layer order = descending flat index) its range is cast to
+  // the half format on s_dp and every chunk (k * bsize elements) lying wholly
+  // above the frontier is all-reduced over the column (G_data > 1) or just marked ready
+  // (G_data = 1), top chunk first, one event per chunk.  The optimizer step then runs its
+  // buckets in chunk-completion order, each waiting only for its chunk (A8),
+  // so K9 starts while the rest of the backward and of the all-reduce are still running.
+  bool ar_overlap = false;            // this batch hands gradients off chunk by chunk
   bool ar_active = false;             // an overlapped all-reduce has been issued (SM reservation)
   int dp_ctas = 0;                    // AXONN_DP_CTAS: cap of the column comm's CTAs, reserved
   int64_t ar_hi = 0;                  // gradients [ar_hi, nflat) are cast and handed to s_dp

@@ -395,6 +395,9 @@ int Ctx::forward_impl(Slot& sl, int mb) {
   const float coef = (float)(oc.loss_scale / ((double)cur_mtotal * (double)M));
   KCHK(xent(logits, tok + 1, s + 1, M, s, V, coef, row_loss, s_comp));
   KCHK(reduce_sum(row_loss, M, 1.0f / ((float)cur_mtotal * (float)M), d_loss, s_comp));
+  // the batch loss is final after the last microbatch's forward (forwards run in ascending mb)
+  if (mb == cur_m - 1 && cudaEventRecord(ev_loss, s_comp) != cudaSuccess)
+    return fail(AXONN_ERR_CUDA, "loss event");
   return 0;
 }
 

@@ -213,3 +213,31 @@ def test_activation_checkpointing_is_bitwise_neutral(ac):
     assert outs[0][0] == outs[1][0]
     for k in outs[0][1]:
         assert np.array_equal(outs[0][1][k].view(np.uint32), outs[1][1][k].view(np.uint32)), k
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_chunked_gradient_handoff_is_bitwise_neutral(monkeypatch, k):
+    """A8: the last backward hands the gradients off chunk by chunk (k * bsize
+    elements, cast to the half format as each layer becomes final) and the optimizer runs its
+    buckets in chunk-completion order, top chunk first, while the backward is still running.
+    Against the hand-off after the pipeline (AXONN_AR_OVERLAP=0, ascending buckets): losses,
+    theta32, v and theta16 after 3 steps bitwise equal (AdamW is elementwise, D-16/D-17)."""
+    from paper_2110_13005_b200.engine import T_ADAM_V, T_MASTER, T_PARAM16
+    cfg = MINI
+    params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=13)
+    toks = [markov_tokens(16, cfg["seq_len"], cfg["vocab"], seed=60 + i) for i in range(3)]
+    res = []
+    for ov in ("0", "1"):
+        monkeypatch.setenv("AXONN_AR_OVERLAP", ov)
+        eng = make(cfg, bucket_elems=50_000, coarsen_k=k, overlap_next_batch=False)
+        eng.write_all(T_MASTER, params)
+        losses = []
+        for tok in toks:
+            losses.append(eng.run_batch(tok))
+            eng.optimizer_step()
+        res.append((losses, eng.read_all(T_MASTER), eng.read_all(T_ADAM_V), eng.read_all(T_PARAM16)))
+        eng.close()
+    assert res[0][0] == res[1][0]
+    for a, b in zip(res[0][1:], res[1][1:]):
+        for name in a:
+            assert np.array_equal(a[name].view(np.uint32), b[name].view(np.uint32)), name
