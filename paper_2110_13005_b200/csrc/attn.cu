@@ -369,7 +369,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 struct AttnBwdParams {
   int s, heads, d, nv, nq, nk, total, stages, nbuf;
   int nfb, nab;        // row-operand smem buffers, accumulator TMEM buffers (1 or 2 each)
-  int dbg;             // AXONN_ATTN_DBG experiments: 1 no epilogue math, 2 no accumulation MMAs
   int ld_bulk;         // KA: the producer bulk-copies each query block's lse / D slice into the
                        // ring stage (s % 64 == 0); else the epilogue loads them per block
   float c1, alpha;
@@ -497,12 +496,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (elect_one()) {
         uint8_t* f = sF + fb * 2 * f_bytes;
         mbar_arrive_expect_tx(&f_full[fb], 2 * f_bytes);
-        if (p.dbg >= 6) {
-          mbar_arrive(&f_full[fb]);   // experiment: no operand loads
-        } else {
         load_rows(f, KA ? &mapK : &mapQ, &f_full[fb], p.nv, FR, r0, z1, z2);
         load_rows(f + f_bytes, KA ? &mapV : &mapO, &f_full[fb], p.nv, FR, r0, z1, z2);
-        }
       }
       __syncwarp();
       for (int it = 0; it < ni; ++it) {
@@ -511,14 +506,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         if (elect_one()) {
           uint8_t* g = sG + stage * 2 * g_bytes;
           const bool bulk = KA && p.ld_bulk;
-          if (p.dbg >= 6) {
-            mbar_arrive(&g_full[stage]);
-          } else {
-            mbar_arrive_expect_tx(&g_full[stage], 2 * g_bytes + (bulk ? 512 : 0));
-            load_rows(g, KA ? &mapQ : &mapK, &g_full[stage], p.nv, GR, g0, z1, z2);
-            load_rows(g + g_bytes, KA ? &mapO : &mapV, &g_full[stage], p.nv, GR, g0, z1, z2);
-          }
-          if (bulk && p.dbg < 6) {   // this block's 64 queries: lse2 and D (consumed by the epilogue)
+          mbar_arrive_expect_tx(&g_full[stage], 2 * g_bytes + (bulk ? 512 : 0));
+          load_rows(g, KA ? &mapQ : &mapK, &g_full[stage], p.nv, GR, g0, z1, z2);
+          load_rows(g + g_bytes, KA ? &mapO : &mapV, &g_full[stage], p.nv, GR, g0, z1, z2);
+          if (bulk) {   // this block's 64 queries: lse2 and D (consumed by the epilogue)
             bulk_g2s(sLD + stage * 128, p.lse + (long long)z * p.s + g0, 256, &g_full[stage]);
             bulk_g2s(sLD + stage * 128 + 64, p.D + (long long)z * p.s + g0, 256, &g_full[stage]);
           }
@@ -542,11 +533,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);   // last TS-MMA read of b
       tc_fence_after();
       const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
-      if (p.dbg >= 4) {   // experiment: no X / Y MMAs
-        if (elect_one()) mma_commit(&xy_full[b]);
-        __syncwarp();
-        return;
-      }
       if (elect_one()) {
         for (int c = 0; c < p.nv / 64; ++c) {
 #pragma unroll
@@ -589,11 +575,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tc_fence_after();
         const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
         if (elect_one()) {
-          if (p.dbg >= 2) {
-            mma_commit(&g_empty[stg]);
-            mma_commit(&acc_done[b]);
-            if (it == ni - 1) mma_commit(&acc_full[ab]);
-          } else {
           // accumulate over the 64 rows of this block: A = packed P^T / dS (TMEM; columns of
           // the two 32-wide halves at +0 and +32), B = G operand MN-major
 #pragma unroll
@@ -609,7 +590,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           mma_commit(&g_empty[stg]);
           mma_commit(&acc_done[b]);
           if (it == ni - 1) mma_commit(&acc_full[ab]);
-          }
         }
         __syncwarp();
         accd_ph[b] ^= 1;
@@ -663,12 +643,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
         mbar_wait(&xy_full[b], (uint32_t)((g / p.nbuf) & 1));
         tc_fence_after();
-        if (p.dbg == 1 || p.dbg >= 3) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&pd_ready[b]);
-          continue;
-        }
         const int c0 = 32 * half;             // this warp's 32 block columns
         uint32_t x[32], y[32];
         tmem_ld32_nowait(trow + 128 * b + c0, x);
@@ -713,7 +687,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tc_fence_after();
       hx* base = p.dq + (long long)z2 * p.s * p.ldq + (long long)z1 * p.d;
       const int r0w = r0 + q * 32;
-      for (int which = KA ? 0 : 1; which < 2 && p.dbg < 5; ++which) {
+      for (int which = KA ? 0 : 1; which < 2; ++which) {
         const uint32_t ca = which == 0 ? colA : colB;
         hx* gb = base + (KA ? (which == 0 ? 2 * p.h : p.h) : 0);
         for (int cc = 0; cc < p.nv / 2; cc += 32) {
@@ -884,9 +858,7 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   const int nv = (dp + 63) / 64 * 64;
   if (nv > 256) return -1;
   const long long ntok = (long long)b * s;
-  // AXONN_ATTN_ONLY (experiments): "d", "ka" or "q" runs only that kernel of the backward
-  const char* only = getenv("AXONN_ATTN_ONLY");
-  if (!only || !strcmp(only, "d")) {
+  {
     const long long nthreads = (ntok * heads + DITEMS - 1) / DITEMS * 16;
     attn_bwd_d_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(
         static_cast<const hx*>(dO), (long long)heads * dp, dp,
@@ -915,25 +887,12 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   p.dq = static_cast<hx*>(dqkv);
   p.ldq = ldq;
   p.h = heads * d;
-  {
-    const char* e = getenv("AXONN_ATTN_DBG");
-    p.dbg = e ? atoi(e) : 0;
-  }
   const int max_smem = 227 * 1024 - 1024 - 256 - 18 * 1024;   // dynamic budget beside static
-  {
-    const char* e = getenv("AXONN_ATTN_LDBULK");
-    p.ld_bulk = (s % GRB == 0) && !(e && e[0] == '0');
-  }
+  p.ld_bulk = s % GRB == 0;
   for (int ka = 1; ka >= 0; --ka) {
-    if (only && strcmp(only, ka ? "ka" : "q")) continue;
     const int f_bytes = nv * 128 * 2, g_bytes = nv * GRB * 2 + (ka ? 256 : 0);   // + lse/D slices
-    // prefer: double row-operand buffer (next unit's loads overlap this unit), then ring depth
-    static int nfb_env = -1;
-    if (nfb_env < 0) {
-      const char* e = getenv("AXONN_ATTN_NFB");
-      nfb_env = e ? atoi(e) : 1;
-    }
-    p.nfb = nfb_env == 2 ? 2 : 1;
+    // one row-operand buffer (a second one measured no faster and costs ring depth)
+    p.nfb = 1;
     int stages = 4;
     while (stages > 2 && p.nfb * 2 * f_bytes + stages * 2 * g_bytes > max_smem) --stages;
     if (p.nfb * 2 * f_bytes + stages * 2 * g_bytes > max_smem) {

@@ -347,8 +347,8 @@ static int local_links(Ctx* c) {
 // 2L, its MLP block = 2L + 1) are cut into G_inter contiguous ranges minimising the largest
 // stage cost, cost = forward FLOPs per token weighted by the measured relative speed of the
 // kernels that execute them: attention block 8h^2 + W * 2sh (QKV and projection GEMMs; the
-// causal QK^T and PV of the fused attention kernel, which runs at ~1/4 of the GEMMs' TFLOP/s:
-// W = 4, AXONN_BAL_ATTN_W overrides), MLP block 16h^2, plus the LM head 2hV on the last stage
+// causal QK^T and PV of the fused attention kernel, which ran at ~1/4 of the GEMMs' TFLOP/s:
+// W = 4), MLP block 16h^2, plus the LM head 2hV on the last stage
 // (the embedding gather is negligible).  Exact DP over (stage, boundary); ties go to the
 // earliest boundary.  With stage_speed (the measured relative speed of the GPUs holding each
 // stage, slowest replica; axonn_calibrate_speed) a stage's cost is divided by its speed, so a
@@ -358,8 +358,7 @@ static std::vector<int> balanced_blocks(const axonn_model_cfg* m, int P, const d
   const int nb = 2 * m->n_layers;
   const double h = m->hidden, s = m->seq_len, V = m->vocab;
   std::vector<double> pre(nb + 1, 0.0);
-  double w_att = 4.0;
-  if (const char* e = getenv("AXONN_BAL_ATTN_W")) w_att = atof(e);
+  const double w_att = 4.0;
   for (int k = 0; k < nb; ++k) pre[k + 1] = pre[k] + ((k & 1) ? 16 * h * h : 8 * h * h + w_att * 2 * s * h);
   const double head = 2 * h * V;
   auto cost = [&](int i, int a, int b) {
@@ -685,7 +684,6 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
     // column comm capped at 16 CTAs, and those SMs left free by the GEMMs of the last
     // backward while its all-reduce chunks run (1.3B 1x2: 936.8 vs 931.9 uncapped, 921.4 at 8)
     c->dp_ctas = 16;
-    if (const char* e = getenv("AXONN_DP_CTAS")) c->dp_ctas = atoi(e);
     if ((rc = split_comm(c, c->world_comm, g_data > 1 ? c->stage : NCCL_SPLIT_NOCOLOR, c->replica,
                          &c->dp_comm, c->dp_ctas)))
       return bail(rc);

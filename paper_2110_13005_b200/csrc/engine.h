@@ -203,22 +203,9 @@ struct Ctx {
 
   // model execution (model_exec.cpp)
   int gemm(GemmArgs g, double flops);
-  int softmax_mode = -1;              // AXONN_FUSED_SOFTMAX=0 -> separate softmax kernels
-  bool fused_softmax() {
-    if (softmax_mode < 0) {
-      const char* e = getenv("AXONN_FUSED_SOFTMAX");
-      softmax_mode = (e && e[0] == '0') ? 0 : 1;
-    }
-    return softmax_mode && s <= 512 && s % 32 == 0;
-  }
-  int flash_mode = -1;                // AXONN_FLASH_ATTN=0 -> GEMM + row-softmax attention path
-  bool flash_attn() {
-    if (flash_mode < 0) {
-      const char* e = getenv("AXONN_FLASH_ATTN");
-      flash_mode = (e && e[0] == '0') ? 0 : 1;
-    }
-    return flash_mode && s <= 512 && d % 2 == 0 && ((dp + 63) / 64) * 64 <= 256;
-  }
+  // K2 fused attention when the shape fits it; else the general path (S = Q K^T by K1 into an
+  // fp32 score buffer, softmax kernels, P V by K1)
+  bool flash_attn() const { return s <= 512 && d % 2 == 0 && ((dp + 63) / 64) * 64 <= 256; }
   float* attn_D = nullptr;            // fused attention backward workspace (D = dO . O)
   int attn_call(bool fwd, LayerStash& st);   // K2 launch (+ profiling events)
   int forward(Slot& sl, int mb);          // nn_shard.Forward (and the loss on the last stage)

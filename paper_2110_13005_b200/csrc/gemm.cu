@@ -45,16 +45,7 @@ struct GemmParams {
   long long ld_aux;
   float alpha;
   int num_m, num_n, total;
-  int dbg;   // AXONN_RS_DEBUG experiments (row-softmax epilogue): 0 normal
-  // hybrid stream-K schedule of the pair kernel (sk = 1): the first sk_dp tiles are dealt
-  // data-parallel, the remaining tiles' k-blocks are split into equal contiguous ranges of
-  // sk_L iterations per pair; a tile cut between pairs is finished (in fixed order) by the
-  // pair holding its k-block 0 from the fp32 partials the others leave in sk_ws
-  int sk, sk_dp, sk_L, kbt;
   int raster_n;       // tile order: 1 = N fastest (see fill_params)
-  float* sk_ws;
-  unsigned* sk_flag;
-  unsigned sk_epoch;
 };
 
 
@@ -84,124 +75,21 @@ __device__ __forceinline__ bool tile_coords(const GemmParams& p, int BN, int t, 
   return kb1 > kb0;
 }
 
-// Work units of one CTA pair: (tile, k-block range, role).  role 0 whole tile, 1 partial
-// (k-blocks after the first of its tile: written to the pair's workspace slot), 2 finisher
-// (holds k-block 0 of a cut tile: adds the partials of pairs first_prod..last_prod).
+// Tiles of one CTA pair: pair, pair + npairs, ... (static round robin over the raster order).
 struct PairUnits {
-  int pair, npairs, i, nfull, it, it1;
-  __device__ __forceinline__ PairUnits(const GemmParams& p, int pr, int np) : pair(pr), npairs(np) {
-    i = 0;
-    if (p.sk) {
-      nfull = p.sk_dp / np;
-      const int I = (p.total - p.sk_dp) * p.kbt;
-      it = min(pr * p.sk_L, I);
-      it1 = min(it + p.sk_L, I);
-    } else {
-      nfull = 0;
-      it = it1 = 0;
-    }
-  }
+  int pair, npairs, i;
+  __device__ __forceinline__ PairUnits(int pr, int np) : pair(pr), npairs(np), i(0) {}
   template <int TBM>
   __device__ __forceinline__ bool next(const GemmParams& p, int BN, int& t, int& z, int& m0, int& n0,
-                                       int& kb0, int& kb1, int& role, int& last_prod) {
-    role = 0;
-    last_prod = -1;
-    if (!p.sk) {
-      for (;;) {
-        t = pair + i * npairs;
-        ++i;
-        if (t >= p.total) return false;
-        if (tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) return true;
-      }
-    }
-    if (i < nfull) {
+                                       int& kb0, int& kb1) {
+    for (;;) {
       t = pair + i * npairs;
       ++i;
-      tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1);
-      return true;
+      if (t >= p.total) return false;
+      if (tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) return true;
     }
-    if (it >= it1) return false;
-    const int ts = it / p.kbt;
-    t = p.sk_dp + ts;
-    tile_coords<TBM>(p, BN, t, z, m0, n0, kb0, kb1);
-    kb0 = it % p.kbt;
-    kb1 = min(p.kbt, kb0 + (it1 - it));
-    it += kb1 - kb0;
-    if (kb0 > 0) {
-      role = 1;
-    } else if (kb1 < p.kbt) {
-      role = 2;
-      last_prod = ((ts + 1) * p.kbt - 1) / p.sk_L;
-    }
-    return true;
   }
 };
-
-__device__ __forceinline__ void st_release_u32(unsigned* a, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-
-// Stream-K fixup by one epilogue warp on its 32 rows x ncol columns of the accumulator at
-// TMEM address tb (lane base already applied).  role 1: store the partial to this pair's
-// slot and publish it; role 2: wait for the partials of pairs pair+1..last_prod and add them
-// (ascending pair order: deterministic) into TMEM before the regular epilogue runs.
-template <int BN>
-__device__ __forceinline__ void sk_fixup(const GemmParams& p, int role, int pair, int last_prod,
-                                         uint32_t rank, int wi, int rloc, int col0, int ncol,
-                                         uint32_t tb, int lane) {
-  auto slot_row = [&](int pr) {
-    return p.sk_ws + ((size_t)(pr * 2 + (int)rank) * 128 + rloc) * BN + col0;
-  };
-  if (role == 1) {
-    float* w = slot_row(pair);
-    for (int c = 0; c < ncol; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(tb + c, r);
-      float4* w4 = reinterpret_cast<float4*>(w + c);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        __stcg(w4 + j, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
-    }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release_u32(p.sk_flag + (pair * 2 + (int)rank) * 8 + wi, p.sk_epoch);
-    return;
-  }
-  for (int pr = pair + 1; pr <= last_prod; ++pr) {
-    if (lane == 0)
-      while (ld_acquire_u32(p.sk_flag + (pr * 2 + (int)rank) * 8 + wi) != p.sk_epoch) {
-      }
-    __syncwarp();
-  }
-  for (int c = 0; c < ncol; c += 32) {
-    uint32_t r[32];
-    tmem_ld32(tb + c, r);
-    float v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-    for (int pr = pair + 1; pr <= last_prod; ++pr) {
-      const float4* w4 = reinterpret_cast<const float4*>(slot_row(pr) + c);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float4 a = __ldcg(w4 + j);
-        v[4 * j] += a.x;
-        v[4 * j + 1] += a.y;
-        v[4 * j + 2] += a.z;
-        v[4 * j + 3] += a.w;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i]);
-    tmem_st32(tb + c, r);
-  }
-  tmem_st_wait();
-}
 
 // tanh on the SFU (MUFU.TANH, rel. error ~2^-11: below the bf16 rounding of the output)
 __device__ __forceinline__ float tanh_fast(float x) {
@@ -408,9 +296,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int z1 = z % p.Z1, z2 = z / p.Z1;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (p.dbg == 7) {
-            if (elect_one()) mbar_arrive(&full[stage]);
-          } else if (elect_one()) {
+          if (elect_one()) {
             mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
             uint8_t* sA = smem + stage * STAGE_BYTES;
             uint8_t* sB = sA + A_BYTES;
@@ -487,7 +373,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
-      for (int c = cpart * CW; c < (cpart + 1) * CW && p.dbg != 8; c += 32) {
+      for (int c = cpart * CW; c < (cpart + 1) * CW; c += 32) {
         if (n0 + c >= p.N) break;
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c, r);
@@ -563,16 +449,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                            const __grid_constant__ CUtensorMap mapB, const GemmParams p,
                            const __grid_constant__ CUtensorMap mapC,
                            const __grid_constant__ CUtensorMap mapX) {
-  // BN = 512: two N = 256 MMAs per k-step into one 512-column accumulator (no TMEM double
-  // buffer); per SM 48 KB of operands per 1024 MMA cycles instead of 32 KB per 512
-  constexpr int NST = TE ? (BN == 512 ? 3 : STAGES2_TE) : (BN == 512 ? 4 : STAGES2);
-  constexpr int NH = BN > 256 ? BN / 256 : 1;  // N = 256 MMAs per k-step
+  static_assert(BN == 128 || BN == 256, "pair tiles: 256 x 128 or 256 x 256");
+  constexpr int NST = TE ? STAGES2_TE : STAGES2;
   constexpr int TBM = 2 * BM;                 // 256 rows per pair
   constexpr int A_BYTES = BM * BK * 2;        // this CTA's 128 rows
-  constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's BN/2 rows (NH chunks of 128)
+  constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's BN/2 rows
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = (2 * BN <= 512) ? 2 * BN : BN;
-  constexpr int NACC = TMEM_COLS / BN;        // accumulator buffers
+  constexpr uint32_t TMEM_COLS = 2 * BN;      // double-buffered accumulator
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stg_all = smem + NST * STAGE_BYTES;          // TE staging boxes (1024-aligned)
@@ -615,40 +498,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     {   // whole warp runs the loop; one elected lane issues the TMA copies
       int stage = 0;
       uint32_t phase = 0;
-      PairUnits pu(p, pair, npairs);
-      int t, z, m0, n0, kb0, kb1, role, last_prod;
-      while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
+      PairUnits pu(pair, npairs);
+      int t, z, m0, n0, kb0, kb1;
+      while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) {
         const int z1 = z % p.Z1, z2 = z / p.Z1;
         const int am = m0 + (int)rank * BM;
-        const int bn = n0 + (int)rank * 128;   // this CTA's 128 B rows of each 256-wide N chunk
+        const int bn = n0 + (int)rank * (BN / 2);   // this CTA's BN/2 rows of B
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (elect_one()) {
-            if (p.dbg == 7) {   // experiment: no operand traffic (MMA on stale smem)
-              if (leader) mbar_arrive(&full[stage]);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+            uint8_t* sA = smem + stage * STAGE_BYTES;
+            uint8_t* sB = sA + A_BYTES;
+            const int k0 = kb * BK;
+            if (!p.a_mn) {
+              tma_load_4d_pair(sA, &mapA, &full[stage], k0, am, z1, z2);
             } else {
-              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
-              uint8_t* sA = smem + stage * STAGE_BYTES;
-              uint8_t* sB = sA + A_BYTES;
-              const int k0 = kb * BK;
-              if (!p.a_mn) {
-                tma_load_4d_pair(sA, &mapA, &full[stage], k0, am, z1, z2);
-              } else {
 #pragma unroll
-                for (int j = 0; j < BM / 64; ++j)
-                  tma_load_4d_pair(sA + j * 8192, &mapA, &full[stage], am + 64 * j, k0, z1, z2);
-              }
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_4d_pair(sA + j * 8192, &mapA, &full[stage], am + 64 * j, k0, z1, z2);
+            }
+            if (!p.b_mn) {
+              tma_load_4d_pair(sB, &mapB, &full[stage], k0, bn, z1, z2);
+            } else {
 #pragma unroll
-              for (int h = 0; h < NH; ++h) {
-                const int bnh = bn + 256 * h;
-                if (!p.b_mn) {
-                  tma_load_4d_pair(sB + h * 16384, &mapB, &full[stage], k0, bnh, z1, z2);
-                } else {
-#pragma unroll
-                  for (int j = 0; j < 2; ++j)
-                    tma_load_4d_pair(sB + h * 16384 + j * 8192, &mapB, &full[stage], bnh + 64 * j, k0, z1, z2);
-                }
-              }
+              for (int j = 0; j < BN / 128; ++j)
+                tma_load_4d_pair(sB + j * 8192, &mapB, &full[stage], bn + 64 * j, k0, z1, z2);
             }
           }
           __syncwarp();
@@ -658,7 +533,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (leader) {   // whole warp runs the loop; one elected lane issues (uniform registers)
-      const uint32_t idesc = umma_idesc_f16(TBM, BN > 256 ? 256 : BN, p.a_mn, p.b_mn);
+      const uint32_t idesc = umma_idesc_f16(TBM, BN, p.a_mn, p.b_mn);
       // descriptors of stage 0 and the per-stage / per-k16 increments (address field = addr >> 4)
       const uint32_t s0 = smem_u32(smem);
       const uint64_t a_d0 = p.a_mn ? umma_desc_sw128(s0, 8192, 1024) : umma_desc_sw128(s0, 16, 1024);
@@ -669,11 +544,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      PairUnits pu(p, pair, npairs);
-      int t, z, m0, n0, kb0, kb1, role, last_prod;
-      while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
-        const int acc = NACC == 2 ? (it & 1) : 0;
-        const uint32_t acc_phase = NACC == 2 ? ((it >> 1) & 1) : (it & 1);
+      PairUnits pu(pair, npairs);
+      int t, z, m0, n0, kb0, kb1;
+      while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
@@ -685,10 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-#pragma unroll
-              for (int h = 0; h < NH; ++h)
-                mma_f16_ss_pair(tmem_d + 256 * h, ad + k * a_k, bd + (uint64_t)(h * (16384 >> 4)) + k * b_k,
-                                 idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              mma_f16_ss_pair(tmem_d, ad + k * a_k, bd + k * b_k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             mma_commit_pair(&empty[stage]);
           }
           __syncwarp();
@@ -706,24 +578,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
     int it = 0;
-    PairUnits pu(p, pair, npairs);
-    int t, z, m0, n0, kb0, kb1, role, last_prod;
-    while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
-      const int acc = NACC == 2 ? (it & 1) : 0;
-      const uint32_t acc_phase = NACC == 2 ? ((it >> 1) & 1) : (it & 1);
+    PairUnits pu(pair, npairs);
+    int t, z, m0, n0, kb0, kb1;
+    while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      if (role) {
-        sk_fixup<BN>(p, role, pair, last_prod, rank, warp - 2, q * 32 + lane, cpart * CW, CW,
-                     tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + cpart * CW, lane);
-        if (role == 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-          ++it;
-          continue;
-        }
-      }
       const int row = m0 + (int)rank * BM + q * 32 + lane;
       for (int c = cpart * CW; c < (cpart + 1) * CW; c += 32) {
         if (n0 + c >= p.N) break;
@@ -752,24 +613,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     uint8_t* my_row0 = box0 + lane * 128;
     uint32_t ephase = 0;
     int it = 0;
-    PairUnits pu(p, pair, npairs);
-    int t, z, m0, n0, kb0, kb1, role, last_prod;
-    while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1, role, last_prod)) {
-      const int acc = NACC == 2 ? (it & 1) : 0;
-      const uint32_t acc_phase = NACC == 2 ? ((it >> 1) & 1) : (it & 1);
+    PairUnits pu(pair, npairs);
+    int t, z, m0, n0, kb0, kb1;
+    while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
       const int row0 = m0 + (int)rank * BM + q * 32;
       const int cb = n0 + cpart * CW;
-      if (role == 1) {   // stream-K partial: no epilogue, publish the fp32 partial
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-        sk_fixup<BN>(p, 1, pair, last_prod, rank, wi, q * 32 + lane, cpart * CW, CW,
-                     tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + cpart * CW, lane);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-        ++it;
-        continue;
-      }
       if (has_in && lane == 0) {   // residual / pre-activation boxes, before the accumulator
         bulk_wait_read<0>();
         mbar_arrive_expect_tx(&ebar[wi], (CW / 64) * TE_BOX);
@@ -779,12 +629,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + cpart * CW;
-      if (role == 2) sk_fixup<BN>(p, 2, pair, last_prod, rank, wi, q * 32 + lane, cpart * CW, CW, tb, lane);
-      if (p.dbg == 8) {   // experiment: no epilogue work
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-      } else if (f32) {
+      if (f32) {
 #pragma unroll 1
         for (int g = 0; g < CW / 32; ++g) {   // 32 fp32 columns = one 128-byte box row
           uint32_t r[32];
@@ -897,631 +742,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair<TMEM_COLS>(tmem_base);
-  }
-}
-
-// ------------------------------------------------------------------ row-softmax variant
-// Attention scores with the causal softmax (or its backward) fused into the epilogue:
-// one tile = 128 query rows x ALL keys (N <= 512: two N=256 MMAs filling the 512 TMEM
-// columns), so every epilogue thread owns a complete score row in TMEM.
-//   EPI_SOFTMAX     : C = P = softmax_k<=q(alpha * Q K^T)        (bf16, zeros for k > q)
-//   EPI_SOFTMAX_BWD : C = dS = alpha * P * (dP - sum_k P dP)     (acc = dP = dO V^T, P = aux)
-// Removes the fp32 score round trip and the separate softmax kernels (D-7, D-8).
-constexpr int RS_STAGES = 2;
-constexpr int RS_THREADS = 64 + 32 * 8;                 // 8 epilogue warps
-constexpr int RS_EPI_SMEM = 3 * 2 * 128 * 4 + 8 * 4096;  // partial max/sum/dot + staging
-
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// v2 epilogue of gemm_rowsoftmax.  Warp pair (q, half) owns TMEM lane quarter q (score rows
-// r0 .. r0+31, r0 = m0 + 32 q) and key columns [256 half, 256 half + 256).  A 32-column
-// chunk c0 of those rows is FULL (c0 + 32 <= r0: every key <= every query), the DIAGONAL
-// chunk (c0 == r0: key i valid for lane >= i) or MASKED (c0 > r0) — warp-uniform, so
-// only the diagonal chunk is predicated.  Forward: exp2 with the 1/sqrt(d) * log2(e) scale
-// folded into one FFMA, computed once and written back to TMEM (tcgen05.st), then
-// rescaled by 1/sum in the store pass.  Backward: P is exactly 0 above the diagonal, so
-// dS = alpha * P * (dP - dot) needs no mask at all.  P / dS leave (and P arrives) through a
-// per-warp swizzled 32 x 64 bf16 staging tile as coalesced 128-byte row segments.
-__device__ __forceinline__ void rowsoftmax_epilogue2(const GemmParams& p, uint32_t tmem_base,
-                                                     uint64_t* tfull, uint64_t* tempty, int warp,
-                                                     int lane) {
-  const int q = warp & 3, half = (warp - 2) >> 2;
-  const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-  __shared__ float red2[3 * 2 * 128];
-  __shared__ uint4 stg2[8 * 256];
-  float* red_max = red2;
-  float* red_sum = red2 + 256;
-  float* red_dot = red2 + 512;
-  uint4* stg = stg2 + (warp - 2) * 256;
-  const int rl = q * 32 + lane;
-  const bool fwd = p.epi == EPI_SOFTMAX;
-  const float c1 = p.alpha * 1.4426950408889634f;   // alpha * log2(e)
-  int it = 0;
-  for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
-    const int z = t / p.num_m, m0 = (t % p.num_m) * BM;
-    const int z1 = z % p.Z1, z2 = z / p.Z1;
-    const int kv = min(p.N, m0 + BM);
-    const int r0 = m0 + q * 32;                 // first row of this warp = its diagonal chunk
-    const int c_lo = half * 256;
-    const int c_end = min(p.N, c_lo + 256);     // my columns to write
-    const int c_val = min(min(kv, c_lo + 256), r0 + 32);   // columns [c_lo, c_val) hold scores
-    const int c_full = min(c_val, r0);          // [c_lo, c_full) are full chunks
-    const bool has_diag = r0 >= c_lo && r0 < c_val;   // diagonal chunk [r0, r0+32) is mine
-    const long long base = z2 * p.c_s2 + z1 * p.c_s1;
-    hx* out = reinterpret_cast<hx*>(p.C) + base;
-    const hx* Pin = p.aux + base;
-    mbar_wait(tfull, it & 1);
-    tc_fence_after();
-    uint32_t r[32];
-    auto stage_P = [&](int g0) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int rr = i * 4 + lane / 8, ch = lane % 8;
-        const int gr = r0 + rr;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (gr < p.M && g0 + ch * 8 < p.N)
-          v = *reinterpret_cast<const uint4*>(Pin + (long long)gr * p.ldc + g0 + ch * 8);
-        stg[rr * 8 + (ch ^ (rr & 7))] = v;
-      }
-      __syncwarp();
-    };
-    auto flush = [&](int g0) {
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int rr = i * 4 + lane / 8, ch = lane % 8;
-        const int gr = r0 + rr;
-        if (gr < p.M && g0 + ch * 8 < p.N)
-          *reinterpret_cast<uint4*>(out + (long long)gr * p.ldc + g0 + ch * 8) =
-              stg[rr * 8 + (ch ^ (rr & 7))];
-      }
-      __syncwarp();
-    };
-    auto put8 = [&](int j, const float* v8) {
-      uint4 u;
-      hx2* h2 = reinterpret_cast<hx2*>(&u);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) h2[i] = f2hx2(v8[2 * i], v8[2 * i + 1]);
-      stg[lane * 8 + (j ^ (lane & 7))] = u;
-    };
-    auto get8 = [&](int j, float* v8) {
-      uint4 u = stg[lane * 8 + (j ^ (lane & 7))];
-      const hx2* h2 = reinterpret_cast<const hx2*>(&u);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float2 f = hx22f2(h2[i]);
-        v8[2 * i] = f.x;
-        v8[2 * i + 1] = f.y;
-      }
-    };
-    if (fwd) {
-      float mx = -3.0e38f;   // max of the raw scores (alpha > 0)
-      for (int c0 = c_lo; c0 < c_full; c0 += 32) {
-        tmem_ld32(trow + c0, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
-      }
-      if (has_diag) {   // diagonal chunk
-        tmem_ld32(trow + r0, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (i <= lane) mx = fmaxf(mx, __uint_as_float(r[i]));
-      }
-      red_max[half * 128 + rl] = mx;
-      named_bar(1 + q, 64);
-      const float moff = fmaxf(red_max[rl], red_max[128 + rl]) * c1;
-      float s0 = 0.f, s1 = 0.f;
-      for (int c0 = c_lo; c0 < c_full; c0 += 32) {
-        tmem_ld32(trow + c0, r);
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float e0 = ex2_approx(fmaf(__uint_as_float(r[i]), c1, -moff));
-          const float e1 = ex2_approx(fmaf(__uint_as_float(r[i + 1]), c1, -moff));
-          s0 += e0;
-          s1 += e1;
-          r[i] = __float_as_uint(e0);
-          r[i + 1] = __float_as_uint(e1);
-        }
-        tmem_st32(trow + c0, r);
-      }
-      if (has_diag) {
-        tmem_ld32(trow + r0, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float e = i <= lane ? ex2_approx(fmaf(__uint_as_float(r[i]), c1, -moff)) : 0.f;
-          s0 += e;
-          r[i] = __float_as_uint(e);
-        }
-        tmem_st32(trow + r0, r);
-      }
-      tmem_st_wait();
-      red_sum[half * 128 + rl] = s0 + s1;
-      named_bar(1 + q, 64);
-      const float inv = 1.f / (red_sum[rl] + red_sum[128 + rl]);
-      for (int g0 = c_lo; g0 < c_end; g0 += 64) {
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int c0 = g0 + 32 * hh;
-          float v[32];
-          if (c0 < c_val) {
-            tmem_ld32(trow + c0, r);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * inv;
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) put8(4 * hh + j, v + 8 * j);
-        }
-        flush(g0);
-      }
-    } else {   // EPI_SOFTMAX_BWD
-      float d0 = 0.f, d1 = 0.f;
-      for (int g0 = c_lo; g0 < c_val; g0 += 64) {
-        stage_P(g0);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int c0 = g0 + 32 * hh;
-          if (c0 < c_val) {
-            tmem_ld32(trow + c0, r);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float pv[8];
-              get8(4 * hh + j, pv);
-#pragma unroll
-              for (int i = 0; i < 8; i += 2) {
-                d0 = fmaf(pv[i], __uint_as_float(r[8 * j + i]), d0);
-                d1 = fmaf(pv[i + 1], __uint_as_float(r[8 * j + i + 1]), d1);
-              }
-            }
-          }
-        }
-        __syncwarp();
-      }
-      red_dot[half * 128 + rl] = d0 + d1;
-      named_bar(1 + q, 64);
-      const float dot = red_dot[rl] + red_dot[128 + rl];
-      for (int g0 = c_lo; g0 < c_end; g0 += 64) {
-        if (g0 < c_val) stage_P(g0);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int c0 = g0 + 32 * hh;
-          float v[32];
-          if (c0 < c_val) {
-            tmem_ld32(trow + c0, r);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float pv[8];
-              get8(4 * hh + j, pv);
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                v[8 * j + i] = p.alpha * pv[i] * (__uint_as_float(r[8 * j + i]) - dot);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 4; ++j) put8(4 * hh + j, v + 8 * j);
-        }
-        flush(g0);
-      }
-    }
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(tempty);
-  }
-}
-
-// Epilogue of gemm_rowsoftmax: warp pair (q, half) owns TMEM lane quarter q (32 score rows)
-// and key columns [256 half, 256 half + 256).  Row statistics are combined across the pair
-// through shared memory; P / dS rows leave (and P rows arrive) through a per-warp swizzled
-// 32 x 64 bf16 staging tile so every global access is a coalesced 128-byte row segment.
-__device__ __forceinline__ void rowsoftmax_epilogue(const GemmParams& p, uint32_t tmem_base,
-                                                    uint64_t* tfull, uint64_t* tempty,
-                                                    uint8_t* scratch, int warp, int lane) {
-  const int q = warp & 3, half = (warp - 2) >> 2;
-  const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-  // static __shared__ so the compiler emits STS/LDS (a pointer laundered through integer
-  // arithmetic on the dynamic smem base turns into slow generic ST.E/LD.E)
-  __shared__ float red_s[3 * 2 * 128];
-  __shared__ uint4 stg_s[8 * 256];
-  (void)scratch;
-  float* red_max = red_s;                                  // [2][128]
-  float* red_sum = red_s + 256;
-  float* red_dot = red_s + 512;
-  uint4* stg = stg_s + (warp - 2) * 256;                   // 32 rows x 8 x 16 B per warp
-  const int rl = q * 32 + lane;                            // row within the 128-row tile
-  const bool fwd = p.epi == EPI_SOFTMAX;
-  int it = 0;
-  for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
-    const int z = t / p.num_m, m0 = (t % p.num_m) * BM;
-    const int z1 = z % p.Z1, z2 = z / p.Z1;
-    const int kv = min(p.N, m0 + BM);
-    const int row = m0 + rl;
-    const long long base = z2 * p.c_s2 + z1 * p.c_s1;
-    hx* out = reinterpret_cast<hx*>(p.C) + base;
-    const hx* Pin = p.aux + base;
-    const int c_lo = half * 256;
-    const int c_hi = min(kv, c_lo + 256);                    // my columns holding scores
-    const int c_end = min(p.N, c_lo + 256);                  // my columns to write
-    mbar_wait(tfull, it & 1);
-    tc_fence_after();
-    uint32_t r[32];
-    // coalesced load of P rows [m0 + 32 q, +32) x [g0, g0 + 64) into the staging tile
-    auto stage_P = [&](int g0) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int rr = i * 4 + lane / 8, ch = lane % 8;
-        const int gr = m0 + q * 32 + rr;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (gr < p.M && g0 + ch * 8 < p.N)
-          v = *reinterpret_cast<const uint4*>(Pin + (long long)gr * p.ldc + g0 + ch * 8);
-        stg[rr * 8 + (ch ^ (rr & 7))] = v;
-      }
-      __syncwarp();
-    };
-    // coalesced store of the staging tile to out rows [m0 + 32 q, +32) x [g0, g0 + 64)
-    auto flush = [&](int g0) {
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int rr = i * 4 + lane / 8, ch = lane % 8;
-        const int gr = m0 + q * 32 + rr;
-        if (gr < p.M && g0 + ch * 8 < p.N && p.dbg != 2)   // rows shorter than a 64-col group
-          *reinterpret_cast<uint4*>(out + (long long)gr * p.ldc + g0 + ch * 8) = stg[rr * 8 + (ch ^ (rr & 7))];
-      }
-      __syncwarp();
-    };
-    auto put_row = [&](int j, const float* v8) {   // this thread's row, 16-byte chunk j
-      uint4 u;
-      hx2* h2 = reinterpret_cast<hx2*>(&u);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) h2[i] = f2hx2(v8[2 * i], v8[2 * i + 1]);
-      stg[lane * 8 + (j ^ (lane & 7))] = u;
-    };
-    auto get_row = [&](int j, float* v8) {
-      uint4 u = stg[lane * 8 + (j ^ (lane & 7))];
-      const hx2* h2 = reinterpret_cast<const hx2*>(&u);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float2 f = hx22f2(h2[i]);
-        v8[2 * i] = f.x;
-        v8[2 * i + 1] = f.y;
-      }
-    };
-    if (p.dbg == 4) {            // experiment: no epilogue work at all
-    } else if (p.dbg == 3) {     // experiment: TMEM reads only
-      float acc = 0.f;
-      for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
-        tmem_ld32(trow + c0, r);
-        acc += __uint_as_float(r[0]) + __uint_as_float(r[31]);
-      }
-      if (acc == 1234.5f) red_max[rl] = acc;
-    } else if (fwd) {
-      float mx = -3.0e38f;
-      for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
-        tmem_ld32(trow + c0, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + i <= row) mx = fmaxf(mx, __uint_as_float(r[i]) * p.alpha);
-      }
-      red_max[half * 128 + rl] = mx;
-      named_bar(1 + q, 64);
-      mx = fmaxf(red_max[rl], red_max[128 + rl]);
-      float sum = 0.f;
-      for (int c0 = c_lo; c0 < c_hi && p.dbg != 5; c0 += 32) {
-        tmem_ld32(trow + c0, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + i <= row) sum += __expf(__uint_as_float(r[i]) * p.alpha - mx);
-      }
-      red_sum[half * 128 + rl] = sum;
-      named_bar(1 + q, 64);
-      const float inv = 1.f / (red_sum[rl] + red_sum[128 + rl]);
-      for (int g0 = c_lo; g0 < c_end && p.dbg < 5; g0 += 64) {
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int c0 = g0 + 32 * hh;
-          float v[32];
-          if (c0 < c_hi) {
-            tmem_ld32(trow + c0, r);
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              v[i] = (c0 + i <= row) ? __expf(__uint_as_float(r[i]) * p.alpha - mx) * inv : 0.f;
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) put_row(4 * hh + j, v + 8 * j);
-        }
-        flush(g0);
-      }
-    } else {   // EPI_SOFTMAX_BWD: dS = alpha * P * (dP - rowsum(P dP))
-      float dot = 0.f;
-      for (int g0 = c_lo; g0 < c_hi; g0 += 64) {
-        stage_P(g0);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int c0 = g0 + 32 * hh;
-          if (c0 < c_hi) {
-            tmem_ld32(trow + c0, r);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float pv[8];
-              get_row(4 * hh + j, pv);
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (c0 + 8 * j + i <= row) dot += pv[i] * __uint_as_float(r[8 * j + i]);
-            }
-          }
-        }
-        __syncwarp();
-      }
-      red_dot[half * 128 + rl] = dot;
-      named_bar(1 + q, 64);
-      dot = red_dot[rl] + red_dot[128 + rl];
-      for (int g0 = c_lo; g0 < c_end; g0 += 64) {
-        if (g0 < c_hi) stage_P(g0);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int c0 = g0 + 32 * hh;
-          float v[32];
-          if (c0 < c_hi) {
-            tmem_ld32(trow + c0, r);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float pv[8];
-              get_row(4 * hh + j, pv);
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                v[8 * j + i] = (c0 + 8 * j + i <= row)
-                                   ? p.alpha * pv[i] * (__uint_as_float(r[8 * j + i]) - dot) : 0.f;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-          __syncwarp();   // everyone has read its P chunk before it is overwritten
-#pragma unroll
-          for (int j = 0; j < 4; ++j) put_row(4 * hh + j, v + 8 * j);
-        }
-        flush(g0);
-      }
-    }
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(tempty);
-  }
-}
-__global__ void __launch_bounds__(RS_THREADS, 1)
-    gemm_rowsoftmax(const __grid_constant__ CUtensorMap mapA,
-                    const __grid_constant__ CUtensorMap mapB, const GemmParams p) {
-  constexpr int A_BYTES = BM * BK * 2;
-  constexpr int HALF_BYTES = 256 * BK * 2;
-  constexpr int STAGE_BYTES = A_BYTES + 2 * HALF_BYTES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RS_STAGES * STAGE_BYTES);
-  uint64_t* empty = full + RS_STAGES;
-  uint64_t* tfull = empty + RS_STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&mapA);
-    tma_prefetch_desc(&mapB);
-    for (int s = 0; s < RS_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 8);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tmem_holder);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-  const int nkb = (p.K + BK - 1) / BK;
-
-  if (warp == 0) {
-    {   // whole warp; elected lane issues
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
-        const int z = t / p.num_m, m0 = (t % p.num_m) * BM;
-        const int z1 = z % p.Z1, z2 = z / p.Z1;
-        const int kv = min(p.N, m0 + BM);
-        const int nh = kv > 256 ? 2 : 1;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (elect_one()) {
-            mbar_arrive_expect_tx(&full[stage], A_BYTES + nh * HALF_BYTES);
-            uint8_t* sA = smem + stage * STAGE_BYTES;
-            tma_load_4d(sA, &mapA, &full[stage], kb * BK, m0, z1, z2);
-            for (int hh = 0; hh < nh; ++hh)
-              tma_load_4d(sA + A_BYTES + hh * HALF_BYTES, &mapB, &full[stage], kb * BK, 256 * hh, z1, z2);
-          }
-          __syncwarp();
-          if (++stage == RS_STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    {   // whole warp; elected lane issues
-      const uint32_t idesc = umma_idesc_f16(BM, 256, 0, 0);
-      const uint64_t d0 = umma_desc_sw128(smem_u32(smem), 16, 1024);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
-        const int m0 = (t % p.num_m) * BM;
-        const int kv = min(p.N, m0 + BM);
-        const int nh = kv > 256 ? 2 : 1;
-        mbar_wait(tempty, (it & 1) ^ 1);
-        tc_fence_after();
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint64_t ad = d0 + (uint64_t)((stage * STAGE_BYTES) >> 4);
-          if (elect_one()) {
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-              for (int hh = 0; hh < nh; ++hh) {
-                const uint64_t bd = ad + (uint64_t)((A_BYTES + hh * HALF_BYTES) >> 4);
-                mma_f16_ss(tmem_base + 256 * hh, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-              }
-            }
-            mma_commit(&empty[stage]);
-          }
-          __syncwarp();
-          if (++stage == RS_STAGES) { stage = 0; phase ^= 1; }
-        }
-        if (elect_one()) mma_commit(tfull);
-        __syncwarp();
-      }
-    }
-  } else {
-    rowsoftmax_epilogue2(p, tmem_base, tfull, tempty, warp, lane);
-  }
-#if 0   // previous 4-warp row-per-thread epilogue (kept for reference, not compiled)
-  } else {
-    const int q = warp & 3;
-    const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    int it = 0;
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
-      const int z = t / p.num_m, m0 = (t % p.num_m) * BM;
-      const int z1 = z % p.Z1, z2 = z / p.Z1;
-      const int kv = min(p.N, m0 + BM);
-      const int row = m0 + q * 32 + lane;
-      const bool live = row < p.M;
-      const long long off = z2 * p.c_s2 + z1 * p.c_s1 + (long long)row * p.ldc;
-      hx* out = reinterpret_cast<hx*>(p.C) + off;
-      const hx* Pin = p.aux + off;
-      mbar_wait(tfull, it & 1);
-      tc_fence_after();
-      uint32_t r[32];
-      if (p.epi == EPI_SOFTMAX) {
-        float mx = -3.0e38f;
-        for (int c0 = 0; c0 < kv; c0 += 32) {
-          tmem_ld32(trow + c0, r);
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c0 + i <= row) mx = fmaxf(mx, __uint_as_float(r[i]) * p.alpha);
-        }
-        float sum = 0.f;
-        for (int c0 = 0; c0 < kv; c0 += 32) {
-          tmem_ld32(trow + c0, r);
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c0 + i <= row) sum += __expf(__uint_as_float(r[i]) * p.alpha - mx);
-        }
-        const float inv = 1.f / sum;
-        for (int c0 = 0; c0 < p.N; c0 += 32) {
-          float v[32];
-          if (c0 < kv) {
-            tmem_ld32(trow + c0, r);
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              v[i] = (c0 + i <= row) ? __expf(__uint_as_float(r[i]) * p.alpha - mx) * inv : 0.f;
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-          if (live) {
-            uint4* d4 = reinterpret_cast<uint4*>(out + c0);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              hx2 h0 = f2hx2(v[8 * i + 0], v[8 * i + 1]);
-              hx2 h1 = f2hx2(v[8 * i + 2], v[8 * i + 3]);
-              hx2 h2 = f2hx2(v[8 * i + 4], v[8 * i + 5]);
-              hx2 h3 = f2hx2(v[8 * i + 6], v[8 * i + 7]);
-              uint4 o;
-              o.x = *reinterpret_cast<uint32_t*>(&h0);
-              o.y = *reinterpret_cast<uint32_t*>(&h1);
-              o.z = *reinterpret_cast<uint32_t*>(&h2);
-              o.w = *reinterpret_cast<uint32_t*>(&h3);
-              d4[i] = o;
-            }
-          }
-        }
-      } else {   // EPI_SOFTMAX_BWD
-        float dot = 0.f;
-        for (int c0 = 0; c0 < kv; c0 += 32) {
-          tmem_ld32(trow + c0, r);
-          if (live) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 8) {
-              uint4 pv = *reinterpret_cast<const uint4*>(Pin + c0 + i);
-              const hx2* ph = reinterpret_cast<const hx2*>(&pv);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                float2 pf = hx22f2(ph[j]);
-                if (c0 + i + 2 * j <= row) dot += pf.x * __uint_as_float(r[i + 2 * j]);
-                if (c0 + i + 2 * j + 1 <= row) dot += pf.y * __uint_as_float(r[i + 2 * j + 1]);
-              }
-            }
-          }
-        }
-        for (int c0 = 0; c0 < p.N; c0 += 32) {
-          float v[32];
-          if (c0 < kv) {
-            tmem_ld32(trow + c0, r);
-            if (live) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 8) {
-                uint4 pv = *reinterpret_cast<const uint4*>(Pin + c0 + i);
-                const hx2* ph = reinterpret_cast<const hx2*>(&pv);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  float2 pf = hx22f2(ph[j]);
-                  v[i + 2 * j] = (c0 + i + 2 * j <= row)
-                                     ? p.alpha * pf.x * (__uint_as_float(r[i + 2 * j]) - dot) : 0.f;
-                  v[i + 2 * j + 1] = (c0 + i + 2 * j + 1 <= row)
-                                         ? p.alpha * pf.y * (__uint_as_float(r[i + 2 * j + 1]) - dot) : 0.f;
-                }
-              }
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-          if (live) {
-            uint4* d4 = reinterpret_cast<uint4*>(out + c0);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              hx2 h0 = f2hx2(v[8 * i + 0], v[8 * i + 1]);
-              hx2 h1 = f2hx2(v[8 * i + 2], v[8 * i + 3]);
-              hx2 h2 = f2hx2(v[8 * i + 4], v[8 * i + 5]);
-              hx2 h3 = f2hx2(v[8 * i + 6], v[8 * i + 7]);
-              uint4 o;
-              o.x = *reinterpret_cast<uint32_t*>(&h0);
-              o.y = *reinterpret_cast<uint32_t*>(&h1);
-              o.z = *reinterpret_cast<uint32_t*>(&h2);
-              o.w = *reinterpret_cast<uint32_t*>(&h3);
-              d4[i] = o;
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
-    }
-  }
-#endif
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
   }
 }
 
@@ -1642,14 +862,6 @@ static int launch_bn(const GemmArgs& g, cudaStream_t st) {
   if (rc) return rc;
   GemmParams p;
   fill_params(p, g, BM, BN);
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* e = getenv("AXONN_GEMM_DBG");
-      dbg = e ? atoi(e) : 0;
-    }
-    p.dbg = dbg;
-  }
   int grid = p.total < g_num_sms ? p.total : g_num_sms;
   if (g.max_ctas > 0 && grid > g.max_ctas) grid = g.max_ctas;
   gemm_bf16_tcgen05<BN><<<grid, GEMM_THREADS, SMEM, st>>>(ma, mb, p);
@@ -1693,40 +905,9 @@ static bool te_eligible(const GemmArgs& g) {
   return true;
 }
 
-static int g_te_mode = -1;   // AXONN_GEMM_TE=0 disables the TMA epilogue
-static int g_bn512 = -1;     // AXONN_GEMM_BN512=1: 256 x 512 pair tiles where eligible
-// AXONN_GEMM_SK=1 enables the hybrid stream-K schedule.  Off by default: measured slower on
-// every layer shape (proj fwd 37.8 -> 53.2 us, FC1 dgrad 119.8 -> 148.5 us,
-// profiles/r1/diag_stream_k.jsonl) — the data-parallel order keeps the pairs that share an
-// operand panel on the same k-block at the same time (L2 serves them together), and the
-// GEMMs are L2 -> SM bound; pieces starting mid-tile lose that alignment.
-static int g_sk_mode = -1;
-
-// Stream-K workspaces, one per concurrently launching stream (s_comp and s_wg run GEMMs at
-// the same time): fp32 [74 pairs][2 CTAs][128 x 256] partials + per-warp flags.
-constexpr int SK_SLOTS = 4;
-static float* g_sk_ws[SK_SLOTS] = {};
-static unsigned* g_sk_flag[SK_SLOTS] = {};
-static unsigned g_sk_epoch[SK_SLOTS] = {};
-static cudaStream_t g_sk_stream[SK_SLOTS] = {};
-static int sk_slot(cudaStream_t st) {
-  for (int i = 0; i < SK_SLOTS; ++i)
-    if (g_sk_ws[i] && g_sk_stream[i] == st) return i;
-  for (int i = 0; i < SK_SLOTS; ++i)
-    if (!g_sk_ws[i]) {
-      const size_t ws = (size_t)80 * 2 * 128 * 256 * 4;
-      if (cudaMalloc(&g_sk_ws[i], ws) != cudaSuccess) return -1;
-      if (cudaMalloc(&g_sk_flag[i], 80 * 2 * 8 * 4) != cudaSuccess) return -1;
-      if (cudaMemset(g_sk_flag[i], 0, 80 * 2 * 8 * 4) != cudaSuccess) return -1;
-      g_sk_stream[i] = st;
-      return i;
-    }
-  return -1;
-}
-
 template <int BN, bool TE>
 static int launch_pair(const GemmArgs& g, cudaStream_t st) {
-  constexpr int NST = TE ? (BN == 512 ? 3 : STAGES2_TE) : (BN == 512 ? 4 : STAGES2);
+  constexpr int NST = TE ? STAGES2_TE : STAGES2;
   constexpr int SMEM = NST * (BM * BK * 2 + (BN / 2) * BK * 2) + (TE ? TE_SMEM : 0) + 1024 + 256;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1736,7 +917,7 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
     attr_set = true;
   }
   CUtensorMap ma, mb, mc, mx;
-  int rc = make_maps(ma, mb, g, BM, 128);
+  int rc = make_maps(ma, mb, g, BM, BN / 2);   // each CTA stages BN/2 rows of B
   if (rc) return rc;
   memset(&mc, 0, sizeof(mc));
   memset(&mx, 0, sizeof(mx));
@@ -1750,101 +931,24 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
   }
   GemmParams p;
   fill_params(p, g, 2 * BM, BN);
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* e = getenv("AXONN_GEMM_DBG");
-      dbg = e ? atoi(e) : 0;
-    }
-    p.dbg = dbg;
-  }
   int pairs_avail = g_num_sms / 2;
   if (g.max_ctas > 0 && pairs_avail > g.max_ctas / 2) pairs_avail = g.max_ctas / 2;
-  int pairs = p.total < pairs_avail ? p.total : pairs_avail;
-  // hybrid stream-K when the last wave of whole tiles would leave pairs idle (T % P != 0,
-  // few waves); all but one full wave stay data-parallel
-  p.kbt = (g.K + BK - 1) / BK;
-  if (g_sk_mode < 0) {
-    const char* e = getenv("AXONN_GEMM_SK");
-    g_sk_mode = (e && e[0] == '1') ? 1 : 0;
-  }
-  const int T = p.total, P = pairs_avail;
-  if (g_sk_mode && !g.no_sk && g.causal == 0 && g.Z == 1 && T % P != 0 && T < 6 * P && p.kbt >= 8 &&
-      P <= 80 && p.dbg == 0) {
-    const int slot = sk_slot(st);
-    if (slot >= 0) {
-      p.sk = 1;
-      p.sk_dp = T >= P ? (T / P - 1) * P : 0;
-      const int I = (T - p.sk_dp) * p.kbt;
-      p.sk_L = (I + P - 1) / P;
-      p.sk_ws = g_sk_ws[slot];
-      p.sk_flag = g_sk_flag[slot];
-      p.sk_epoch = ++g_sk_epoch[slot];
-      pairs = P;
-    }
-  }
+  const int pairs = p.total < pairs_avail ? p.total : pairs_avail;
   gemm_bf16_tcgen05_pair<BN, TE><<<2 * pairs, GEMM_THREADS, SMEM, st>>>(ma, mb, p, mc, mx);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
-static int launch_rowsoftmax(const GemmArgs& g, cudaStream_t st) {
-  // dynamic part only; the epilogue's RS_EPI_SMEM bytes are static __shared__
-  constexpr int SMEM = RS_STAGES * (BM * BK * 2 + 2 * 256 * BK * 2) + 1024 + 256;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_rowsoftmax, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
-        cudaSuccess)
-      return -10;
-    attr_set = true;
-  }
-  if (g.N > 512 || g.N % 32 || g.a_mn || g.b_mn || (g.ldc % 8) || (g.c_s1 % 8) || (g.c_s2 % 8))
-    return -1;
-  CUtensorMap ma, mb;
-  int rc = make_maps(ma, mb, g, BM, 256);
-  if (rc) return rc;
-  GemmParams p;
-  fill_params(p, g, BM, 512);
-  p.num_n = 1;
-  p.total = p.num_m * g.Z;
-  {
-    const char* e = getenv("AXONN_RS_DEBUG");
-    p.dbg = e ? atoi(e) : 0;
-  }
-  int grid = p.total < g_num_sms ? p.total : g_num_sms;
-  if (g.max_ctas > 0 && grid > g.max_ctas) grid = g.max_ctas;
-  gemm_rowsoftmax<<<grid, RS_THREADS, SMEM, st>>>(ma, mb, p);
-  return cudaGetLastError() == cudaSuccess ? 0 : -11;
-}
-
-static int g_pair_mode = -1;   // AXONN_GEMM_PAIR=0 disables the CTA-pair kernel
-
 int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.Z <= 0 || g.Z1 <= 0 || g.Z % g.Z1) return -1;
-  if (g_pair_mode < 0) {
-    const char* e = getenv("AXONN_GEMM_PAIR");
-    g_pair_mode = (e && e[0] == '0') ? 0 : 1;
-  }
-  if (g.epi == EPI_SOFTMAX || g.epi == EPI_SOFTMAX_BWD) return launch_rowsoftmax(g, st);
-  // narrow outputs (attention P V, dQ, dK, dV: N = head dim): 256 x 128 pair tiles halve the
-  // per-SM A traffic of 128 x 128 single-CTA tiles
-  // (measured: 36 us vs 30 us for the single-CTA 128 x 128 tiles at the 1.3B attention shape,
-  // so narrow GEMMs use the pair only when forced with variant 2)
-  if (g_te_mode < 0) {
-    const char* e = getenv("AXONN_GEMM_TE");
-    g_te_mode = (e && e[0] == '0') ? 0 : 1;
-  }
+  // narrow outputs (N <= 128) and small M: single-CTA 128 x {128, 256} tiles (the narrow
+  // attention-path GEMMs measured 30 us single-CTA vs 36 us as 256 x 128 pairs at the 1.3B
+  // shape); variant 2 forces the 256 x 128 pair for them
   if (g.N <= 128 && g.M >= 256 && g.variant == 2) return launch_pair<128, false>(g, st);
-  if (g.variant == 1 || (g.variant == 0 && (g.N <= 128 || !g_pair_mode || g.M <= 128)))
+  if (g.variant == 1 || (g.variant == 0 && (g.N <= 128 || g.M <= 128)))
     return g.N <= 128 ? launch_bn<128>(g, st) : launch_bn<256>(g, st);
-  if (g_bn512 < 0) {
-    const char* e = getenv("AXONN_GEMM_BN512");
-    g_bn512 = (e && e[0] == '1') ? 1 : 0;
-  }
-  // 256 x 512 pair tiles: epilogues without a tile-sized input (two staging boxes per warp)
-  if (g_te_mode && te_eligible(g) && (g.variant == 4 || (g.variant == 0 && g_bn512)) &&
-      g.N >= 2048 && !(g.epi == EPI_DGELU || (g.epi == EPI_HALF && g.resid)))
-    return launch_pair<512, true>(g, st);
-  if (g_te_mode && g.variant != 3 && te_eligible(g)) return launch_pair<256, true>(g, st);
+  // linear layers: 256 x 256 CTA-pair tiles with the TMA epilogue where eligible (variant 3
+  // forces the thread-store epilogue)
+  if (g.variant != 3 && te_eligible(g)) return launch_pair<256, true>(g, st);
   return launch_pair<256, false>(g, st);
 }
 
@@ -1856,8 +960,7 @@ int preload_gemm() {   // see preload_ops (ops.cu)
   const void* fns[] = {(const void*)gemm_bf16_tcgen05<128>, (const void*)gemm_bf16_tcgen05<256>,
                        (const void*)gemm_bf16_tcgen05_pair<256, false>,
                        (const void*)gemm_bf16_tcgen05_pair<256, true>,
-                       (const void*)gemm_bf16_tcgen05_pair<512, true>,
-                       (const void*)gemm_bf16_tcgen05_pair<128, false>, (const void*)gemm_rowsoftmax};
+                       (const void*)gemm_bf16_tcgen05_pair<128, false>};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
   return 0;

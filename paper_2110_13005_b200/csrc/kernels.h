@@ -9,9 +9,7 @@
 namespace axonn {
 
 enum Epi {
-  EPI_HALF = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3,
-  EPI_SOFTMAX = 4,       // causal row softmax of alpha * acc -> bf16 P (N <= 512, full rows per tile)
-  EPI_SOFTMAX_BWD = 5    // dS = alpha * P * (acc - rowsum(P * acc)), P read from aux
+  EPI_HALF = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3
 };
 
 struct GemmArgs {
@@ -34,9 +32,7 @@ struct GemmArgs {
   long long ld_aux;
   float alpha;
   int max_ctas;
-  int variant;          // 0 auto, 1 single CTA, 2 CTA pair (TMA epilogue when eligible), 3 CTA pair, thread-store epilogue, 4 pair 256x512
-  int no_sk;            // 1: never use the stream-K schedule (launches that may run concurrently
-                        // with another spinning kernel: its cross-pair waits need co-residency)
+  int variant;          // 0 auto, 1 single CTA, 2 CTA pair (TMA epilogue when eligible), 3 CTA pair, thread-store epilogue
 };
 
 int gemm_launch(const GemmArgs& g, cudaStream_t st);

@@ -49,11 +49,8 @@ int Ctx::gemm(GemmArgs g, double flops) {
   // NCCL links: leave two TPCs to the posted one-CTA NCCL P2P kernels (receive act/grad,
   // short sends).  Peer-copy links run on the copy engines and need no SM.
   if (g.max_ctas == 0 && g_inter > 1 && !p2p_ipc) g.max_ctas = num_sms - 4;
-  // overlapped column all-reduce running: optionally leave its CTAs their SMs
-  if (g.max_ctas == 0 && ar_active && dp_ctas > 0) g.max_ctas = num_sms - ((dp_ctas + 1) & ~1);
-  // stream-K (cross-pair waits) only on s_comp: a weight-gradient GEMM on s_wg may hold SMs
-  // concurrently, and two partially resident spinning kernels could starve each other
-  if (st == s_wg) g.no_sk = 1;
+  // overlapped column all-reduce running (G_data > 1): leave its CTAs their SMs
+  if (g.max_ctas == 0 && ar_active && g_data > 1 && dp_ctas > 0) g.max_ctas = num_sms - ((dp_ctas + 1) & ~1);
   ProfRec pr{};
   if (prof_mb) {
     pr.a = ev();
@@ -176,14 +173,8 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
       g.b_s2 = (long long)s * lq;
       g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
       g.epi = EPI_F32; g.causal = 1; g.alpha = 1.0f / sqrtf((float)d);
-      if (fused_softmax()) {   // softmax in the epilogue: P straight from TMEM
-        g.C = st.P;
-        g.epi = EPI_SOFTMAX;
-        TRY(gemm(g, -1));
-      } else {
-        TRY(gemm(g, -1));
-        KCHK(softmax_fwd(S, (long long)b * heads * s, s, st.P, s_comp));
-      }
+      TRY(gemm(g, -1));
+      KCHK(softmax_fwd(S, (long long)b * heads * s, s, st.P, s_comp));
     }
     {  // o = P V, heads merged into [M, h]
       GemmArgs g;
@@ -291,16 +282,8 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
       g.b_s2 = (long long)s * lq;
       g.C = S; g.ldc = s; g.c_s1 = (long long)s * s; g.c_s2 = (long long)heads * s * s;
       g.epi = EPI_F32; g.causal = 1;
-      if (fused_softmax()) {   // dS = P * (dP - rowsum(P dP)) / sqrt(d) in the epilogue
-        g.C = dS;
-        g.epi = EPI_SOFTMAX_BWD;
-        g.aux = st.P;
-        g.alpha = 1.0f / sqrtf((float)d);
-        TRY(gemm(g, -1));
-      } else {
-        TRY(gemm(g, -1));
-        KCHK(softmax_bwd(st.P, S, (long long)b * heads * s, s, 1.0f / sqrtf((float)d), dS, s_comp));
-      }
+      TRY(gemm(g, -1));
+      KCHK(softmax_bwd(st.P, S, (long long)b * heads * s, s, 1.0f / sqrtf((float)d), dS, s_comp));
     }
     {  // dQ = dS K  -> dqkv[:, 0:h]
       GemmArgs g;
