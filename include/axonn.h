@@ -194,15 +194,25 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch, const
 /* Alg. 1 l.4-6: one data_parallel_step.  Collective (SPMD).
  * tokens: host int32 [batch][seq_len + 1], the FULL batch (inputs = [:, :s],
  * labels = [:, 1:]); replica j uses rows [j*batch/G_data, (j+1)*batch/G_data).
- * Runs Alg. 2 to completion on this rank, then the half-precision gradient
- * all-reduce over the column (chunked).  *loss_out (may be
- * NULL) = batch-mean token cross entropy, unscaled, identical on all ranks.
- * Errors: NONDIVISIBLE_BATCH, STATE (two run_batch without optimizer_step),
- * TIMEOUT, CUDA, NCCL. */
+ * Every token id must lie in [0, vocab): the whole batch is checked on the host
+ * before any device work, and a bad id returns AXONN_ERR_INVALID_ARG on every
+ * rank (not sticky).
+ * Runs Alg. 2 on this rank; during the last microbatch's backward each layer's
+ * gradients are cast to the half format and handed off in chunks of k * bsize
+ * elements -- all-reduced over the column when G_data > 1 --
+ * as soon as they are final.  Returns once the batch loss is known (the last
+ * backward and the all-reduce may still be running on the device; the next
+ * call orders after them).  *loss_out (may be NULL) = batch-mean token cross
+ * entropy, unscaled, identical on all ranks.
+ * Errors: NONDIVISIBLE_BATCH, INVALID_ARG (NULL tokens, token id out of range),
+ * STATE (two run_batch without optimizer_step), TIMEOUT, CUDA, NCCL. */
 AXONN_API axonn_status axonn_run_batch(axonn_ctx* ctx, const int32_t* tokens, int batch, float* loss_out);
 
 /* Same as axonn_run_batch with this replica's shard already resident on the
- * device: d_tokens = device int32 [batch/G_data][seq_len + 1]. */
+ * device: d_tokens = device int32 [batch/G_data][seq_len + 1].  The shard's ids
+ * are range-checked by a device kernel whose flag is MAX-reduced over the world
+ * (one small synchronisation per batch); a bad id returns AXONN_ERR_INVALID_ARG
+ * on every rank. */
 AXONN_API axonn_status axonn_run_batch_device(axonn_ctx* ctx, const int32_t* d_tokens, int batch,
                                     float* loss_out);
 

@@ -87,7 +87,6 @@ __global__ void __launch_bounds__(256) adamw_kernel(long long n, const hx* __res
   }
 }
 
-static int g_sms_adam = 0;
 
 int adamw_launch(long long n, const void* g16, float* theta, float* m, float* v, void* theta16,
                  const float* sc, cudaStream_t st) {
@@ -96,11 +95,7 @@ int adamw_launch(long long n, const void* g16, float* theta, float* m, float* v,
       (reinterpret_cast<uintptr_t>(m) & 15) || (reinterpret_cast<uintptr_t>(v) & 15) ||
       (reinterpret_cast<uintptr_t>(theta16) & 7))
     return -2;
-  if (!g_sms_adam) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms_adam, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int g_sms_adam = device_sms();
   AdamScalars s{sc[0], sc[1], sc[2], sc[3], sc[4], sc[5], sc[6], sc[7], sc[8]};
   long long nvec = (n + 3) / 4;
   long long blocks = (nvec + 255) / 256;

@@ -818,12 +818,13 @@ int attn_fwd(const void* qkv, long long lq, int b, int heads, int s, int d, int 
   const int nv = (dp + 63) / 64 * 64;
   if (nv > 256) return -1;
   constexpr int SMEM = ATT_STAGES * ATT_STAGE + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kMaxDevices] = {};
+  const int dev_ = cur_device();
+  if (!attr[dev_]) {
     if (cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
         cudaSuccess)
       return -10;
-    attr = true;
+    attr[dev_] = true;
   }
   const char* base = static_cast<const char*>(qkv);
   CUtensorMap mq, mk, mv;

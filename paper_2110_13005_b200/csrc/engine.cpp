@@ -196,8 +196,12 @@ static int init_weights(Ctx* c) {
     if (leaf.size() > 2 && leaf.compare(leaf.size() - 2, 2, "_g") == 0) { mean = 1.f; sd = 0.f; }
     else if ((leaf.size() > 2 && leaf.compare(leaf.size() - 2, 2, "_b") == 0) || leaf.rfind("b_", 0) == 0) sd = 0.f;
     else if (leaf == "w_o" || leaf == "w_fc2") sd = proj;
+    // the stream of a tensor depends only on its global name (not on the stage split), so
+    // every G_inter / stage_balance partition starts from the same model
+    uint64_t hname = 1469598103934665603ull;   // FNV-1a
+    for (char ch : t.name) hname = (hname ^ (uint8_t)ch) * 1099511628211ull;
     if (init_normal(c->p16(t.off), m32 ? m32 + t.off : nullptr, t.numel,
-                    seed * 1000003ull + (uint64_t)c->stage * 7919ull + i, mean, sd, c->s_comp))
+                    seed * 1000003ull + hname, mean, sd, c->s_comp))
       return c->fail(AXONN_ERR_CUDA, "init_normal");
   }
   if (c->oc.offload) {   // theta32 = theta16 exactly at step 0 (D-15)
@@ -1207,9 +1211,33 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   // (overlap_next_batch) per layer as its buckets complete (Ctx::wait_params)
   if (!c->opt_pending) CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
   const size_t row0 = (size_t)c->replica * shard * (c->s + 1);   // Alg. 1 l.5
+  // token ids must lie in [0, vocab): the kernels index embedding rows and logit columns with
+  // them.  Checked before any device work of the batch, identically on every rank (host: the
+  // whole batch; device: each shard, flag MAX-reduced over the world), so a bad batch returns
+  // AXONN_ERR_INVALID_ARG on every rank and leaves the context usable.
+  int bad = 0;
   if (on_device) {
     CU(cudaMemcpyAsync(c->dtok, tokens, need * 4, cudaMemcpyDeviceToDevice, c->s_comp));
+    int* d_bad = reinterpret_cast<int*>(reinterpret_cast<char*>(c->d_loss) + 40);
+    int* h_bad = reinterpret_cast<int*>(reinterpret_cast<char*>(c->h_loss) + 40);
+    CU(cudaMemsetAsync(d_bad, 0, sizeof(int), c->s_comp));
+    if (token_check(c->dtok, need, c->V, d_bad, c->s_comp)) return (axonn_status)c->fail(AXONN_ERR_CUDA, "token check");
+    ++c->launches;
+    cudaEvent_t e = c->ev();
+    CU(cudaEventRecord(e, c->s_comp));
+    CU(cudaStreamWaitEvent(c->s_loss, e, 0));
+    if (c->world > 1 && !c->lg) NC(ncclAllReduce(d_bad, d_bad, 1, ncclInt32, ncclMax, c->world_comm, c->s_loss));
+    CU(cudaMemcpyAsync(h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, c->s_loss));
+    CU(cudaStreamSynchronize(c->s_loss));
+    bad = *h_bad;
+    if (c->lg && c->lg->rendezvous(nullptr, &bad, group_timeout_s()))
+      return (axonn_status)c->fail(AXONN_ERR_STATE, "local group failed (token check)");
   } else {
+    const int64_t all = (int64_t)batch * (c->s + 1);
+    for (int64_t i = 0; i < all; ++i) bad |= (tokens[i] < 0) | (tokens[i] >= c->V);
+  }
+  if (bad) return (axonn_status)c->fail(AXONN_ERR_INVALID_ARG, "token id outside [0, vocab)");
+  if (!on_device) {
     CU(cudaMemcpyAsync(c->dtok, tokens + row0, need * 4, cudaMemcpyHostToDevice, c->s_comp));
     c->stats[AXONN_STAT_H2D_BYTES] += need * 4.0;
   }
@@ -1302,14 +1330,16 @@ extern "C" {
 
 AXONN_API axonn_status axonn_run_batch(axonn_ctx* c, const int32_t* tokens, int batch, float* loss_out) {
   const axonn_status rc = run_batch_impl(c, tokens, false, batch, loss_out);
-  if (rc && c && c->lg) c->lg->abort();   // loopback: the other stages must not wait for this one
+  // loopback: after a sticky failure the other stages must not wait for this one (argument
+  // errors are detected identically on every stage before any exchange)
+  if (rc && c && c->lg && c->sticky) c->lg->abort();
   return rc;
 }
 
 AXONN_API axonn_status axonn_run_batch_device(axonn_ctx* c, const int32_t* d_tokens, int batch,
                                               float* loss_out) {
   const axonn_status rc = run_batch_impl(c, d_tokens, true, batch, loss_out);
-  if (rc && c && c->lg) c->lg->abort();
+  if (rc && c && c->lg && c->sticky) c->lg->abort();
   return rc;
 }
 
@@ -1318,7 +1348,7 @@ AXONN_API axonn_status axonn_run_batch_device(axonn_ctx* c, const int32_t* d_tok
 static axonn_status optimizer_step_impl(axonn_ctx* c);
 AXONN_API axonn_status axonn_optimizer_step(axonn_ctx* c) {
   const axonn_status rc = optimizer_step_impl(c);
-  if (rc && rc != AXONN_ERR_NONFINITE && c && c->lg) c->lg->abort();
+  if (rc && c && c->lg && c->sticky) c->lg->abort();
   return rc;
 }
 

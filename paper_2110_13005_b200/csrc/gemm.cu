@@ -790,7 +790,6 @@ int make_tmap_4d(CUtensorMap* map, const void* base, long long inner, long long 
   return make_map(map, base, inner, outer, ld, Z1, s1, Z2, s2, box_outer);
 }
 
-static int g_num_sms = 0;
 
 static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
   memset(&p, 0, sizeof(p));
@@ -809,11 +808,7 @@ static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
   p.num_m = (g.M + tbm - 1) / tbm;
   p.num_n = (g.N + bn - 1) / bn;
   p.total = p.num_m * p.num_n * g.Z;
-  if (g_num_sms == 0) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int g_num_sms = device_sms();
   // M-fastest order re-reads A once per N column of tiles; when A is far larger than L2 and
   // B is small (LM-head weight gradient: A = dlogits^T 419 MB, B = 16.8 MB: 4.5x the
   // algorithmic DRAM bytes; FC1 weight gradient 2x, profiles/r1/k1_traffic.json), walk N
@@ -850,12 +845,14 @@ static int make_maps(CUtensorMap& ma, CUtensorMap& mb, const GemmArgs& g, int a_
 template <int BN>
 static int launch_bn(const GemmArgs& g, cudaStream_t st) {
   constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};
+  const int dev = cur_device();
+  const int g_num_sms = device_sms();
+  if (!attr_set[dev]) {
     if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM) != cudaSuccess)
       return -10;
-    attr_set = true;
+    attr_set[dev] = true;
   }
   CUtensorMap ma, mb;
   int rc = make_maps(ma, mb, g, BM, BN);
@@ -909,12 +906,14 @@ template <int BN, bool TE>
 static int launch_pair(const GemmArgs& g, cudaStream_t st) {
   constexpr int NST = TE ? STAGES2_TE : STAGES2;
   constexpr int SMEM = NST * (BM * BK * 2 + (BN / 2) * BK * 2) + (TE ? TE_SMEM : 0) + 1024 + 256;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};
+  const int dev = cur_device();
+  const int g_num_sms = device_sms();
+  if (!attr_set[dev]) {
     if (cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, TE>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
       return -10;
-    attr_set = true;
+    attr_set[dev] = true;
   }
   CUtensorMap ma, mb, mc, mx;
   int rc = make_maps(ma, mb, g, BM, BN / 2);   // each CTA stages BN/2 rows of B

@@ -8,6 +8,21 @@
 
 namespace axonn {
 
+// Per-device one-time state (kernel attributes and SM counts are per device; one process may
+// drive several devices, e.g. axonn_calibrate_speed or the loopback transport).
+constexpr int kMaxDevices = 64;
+inline int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDevices) ? d : 0;
+}
+inline int device_sms() {
+  static int cache[kMaxDevices] = {};
+  const int d = cur_device();
+  if (!cache[d]) cudaDeviceGetAttribute(&cache[d], cudaDevAttrMultiProcessorCount, d);
+  return cache[d];
+}
+
 enum Epi {
   EPI_HALF = 0, EPI_BIAS_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3
 };
@@ -76,6 +91,8 @@ int softmax_bwd(const void* P, const float* dP, long long nrows, int s, float sc
 int xent(void* z, const int32_t* labels, long long lab_ld, int rows, int s, int V, float coef,
          float* row_loss, cudaStream_t st);
 int reduce_sum(const float* x, int n, float scale, double* out, cudaStream_t st);
+// flag = 1 if any of the n int32 token ids is outside [0, vocab) (flag is not cleared)
+int token_check(const int32_t* tok, long long n, int vocab, int* flag, cudaStream_t st);
 int cast_f32_hx(const float* in, void* out, long long n, cudaStream_t st);
 // flag = 1 if any of the n 16-bit values is inf / NaN (flag is not cleared)
 int nonfinite_scan(const void* x, long long n, int* flag, cudaStream_t st);

@@ -13,6 +13,8 @@
 #include <cstdint>
 #include <cfloat>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace axonn {
@@ -46,15 +48,7 @@ __device__ __forceinline__ void store8(hx* p, const float (&f)[8]) {
   *reinterpret_cast<uint4*>(p) = u;
 }
 
-static int g_sms_ops = 0;
-static int num_sms() {
-  if (!g_sms_ops) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms_ops, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return g_sms_ops;
-}
+static int num_sms() { return device_sms(); }
 static inline int ok() { return cudaGetLastError() == cudaSuccess ? 0 : -11; }
 
 // ------------------------------------------------------------------ embedding
@@ -112,7 +106,7 @@ __global__ void embed_bwd_tok_kernel(const int32_t* __restrict__ tok, long long 
       bool hit = false;
       if (i0 + threadIdx.x < 1024 && i < rows) {
         int id = tok[(i / s) * tok_ld + (i % s)];
-        hit = id >= v0 && id < v0 + EMB_VROWS;
+        hit = id >= v0 && id < v0 + EMB_VROWS && id < vocab;   // last block may pass vocab
       }
       unsigned m = __ballot_sync(0xffffffffu, hit);
       // block-wide ordered prefix: warps in order
@@ -855,6 +849,27 @@ int init_normal(void* out, float* master, long long n, uint64_t seed, float mean
 }  // namespace axonn
 
 namespace axonn {
+namespace {
+// flag |= 1 if any token id of the [rows][cols] int32 block (row pitch ld) is outside [0, vocab)
+__global__ void token_check_kernel(const int32_t* __restrict__ tok, long long n, int vocab,
+                                   int* __restrict__ flag) {
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int id = tok[i];
+    bad |= id < 0 || id >= vocab;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+}  // namespace
+
+int token_check(const int32_t* tok, long long n, int vocab, int* flag, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const long long blocks = std::min<long long>((n + 255) / 256, 4LL * num_sms());
+  token_check_kernel<<<(unsigned)blocks, 256, 0, st>>>(tok, n, vocab, flag);
+  return ok();
+}
+
 // Force-load every kernel of this module now (CUDA lazy loading would otherwise load a
 // module at its first launch, which waits for running kernels — e.g. a pre-posted
 // ncclRecv spinning until the peer's message arrives — and deadlocks Alg. 2).
@@ -867,7 +882,8 @@ int preload_ops() {
                        (const void*)softmax_fwd_kernel,
                        (const void*)softmax_bwd_kernel, (const void*)xent_kernel,
                        (const void*)reduce_sum_kernel, (const void*)cast_f32_hx_kernel, (const void*)nonfinite_kernel,
-                       (const void*)cast_hx_f32_kernel, (const void*)init_normal_kernel};
+                       (const void*)cast_hx_f32_kernel, (const void*)init_normal_kernel,
+                       (const void*)token_check_kernel};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
   return 0;

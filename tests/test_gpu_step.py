@@ -241,3 +241,30 @@ def test_chunked_gradient_handoff_is_bitwise_neutral(monkeypatch, k):
     for a, b in zip(res[0][1:], res[1][1:]):
         for name in a:
             assert np.array_equal(a[name].view(np.uint32), b[name].view(np.uint32)), name
+
+
+def test_token_ids_out_of_range_are_rejected():
+    """Token ids index embedding rows and logit columns: an id outside [0, vocab) (host path:
+    the whole batch is scanned; device path: a check kernel) returns INVALID_ARG before any
+    device work and leaves the context usable; vocab 264 is not a multiple of the embedding
+    backward's 32-row blocks, so ids in [264, 288) would otherwise reach past dE_tok."""
+    import torch
+
+    from paper_2110_13005_b200.engine import AxoNNError
+    cfg = dict(TINY, vocab=264)
+    eng = make(cfg)
+    tok = markov_tokens(8, cfg["seq_len"], cfg["vocab"], seed=3)
+    for bad in (264, 287, -1):
+        t2 = tok.copy()
+        t2[5, 7] = bad
+        with pytest.raises(AxoNNError) as e:
+            eng.run_batch(t2)
+        assert e.value.status == "INVALID_ARG"
+        d = torch.from_numpy(t2).cuda()
+        with pytest.raises(AxoNNError) as e:
+            eng.run_batch_device(d.data_ptr(), 8)
+        assert e.value.status == "INVALID_ARG"
+    loss = eng.run_batch(tok)       # still usable
+    assert np.isfinite(loss)
+    eng.optimizer_step()
+    eng.close()
