@@ -352,6 +352,356 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ forward, streamed keys
+// K2 forward for any s (v2).  One work unit = 256 queries of one (sample, head) as two
+// 128-query tiles A (queries [256u, +128)) and B ([256u + 128, +128)) that share every key /
+// value block they both need.  Keys stream in blocks of KB (128 when the padded head width
+// NV <= 128, 64 when NV = 192, so that S_A, S_B (KB columns each) and O_A, O_B (NV each) fit
+// the 512 TMEM columns).  Online softmax in the log2 domain with a lazy rescale: a row keeps
+// its running max m until a block's max exceeds m + 8 (P <= 2^8 stays exact in bf16 / fp32),
+// and only then rescales l and its O row.  Ping-pong: the MMA warp issues PV_A(j), S_A(j+1),
+// then PV_B(j), S_B(j+1), so softmax A works on S_A(j+1) while the tensor core runs tile B's
+// MMAs and vice versa.  P overwrites its S block in TMEM (bf16 pairs, KB/2 columns) and feeds
+// PV as the TMEM A operand; tcgen05 MMAs execute in issue order, so S_X(j+1) (issued after
+// PV_X(j)) cannot overwrite P_X(j) before PV_X(j) has read it.
+// Warps: 0 TMA producer, 1 MMA issuer, 2-3 idle, 4-7 softmax + epilogue of tile A (TMEM lane
+// quarter = warp % 4), 8-11 of tile B.  Each softmax thread owns one query row and keeps the
+// row's KB scores of the block in registers (one TMEM read per score).
+constexpr int F2_THREADS = 12 * 32;
+constexpr float F2_RESCALE_TH = 8.0f;   // log2 units
+
+struct AttnFwd2Params {
+  int s, heads, d, nu, total;   // nu = units per (sample, head) = ceil(s / 256)
+  float c1;                     // alpha * log2(e)
+  hx* o;
+  long long ldo;
+  float* lse;
+};
+
+template <int NV, int KB>
+__global__ void __launch_bounds__(F2_THREADS, 1)
+    attn_fwd2_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
+                     const __grid_constant__ CUtensorMap mapV, const AttnFwd2Params p) {
+  constexpr int NC = NV / 64;                 // 64-wide head-dim chunks
+  constexpr int Q_BYTES = 128 * NV * 2;       // one 128-query tile
+  constexpr int KV_BYTES = KB * NV * 2;       // one key (or value) block
+  constexpr int KST = 2, VST = 2;
+  // TMEM columns: S / P of tile x at x * KB, O of tile x at 2 KB + x * NV
+#define S_COL(x) ((uint32_t)(x) * KB)
+#define O_COL(x) (2u * KB + (uint32_t)(x) * NV)
+  static_assert(2 * KB + 2 * NV <= 512, "TMEM budget");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                               // [2] tiles
+  uint8_t* sK = smem + 2 * Q_BYTES;                 // [KST]
+  uint8_t* sV = sK + KST * KV_BYTES;                // [VST]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * KV_BYTES);
+  uint64_t* q_full = bars;            // [2]
+  uint64_t* q_empty = bars + 2;       // [2]
+  uint64_t* k_full = bars + 4;        // [KST]
+  uint64_t* k_empty = k_full + KST;   // [KST]
+  uint64_t* v_full = k_empty + KST;   // [VST]
+  uint64_t* v_empty = v_full + VST;   // [VST]
+  uint64_t* s_full = v_empty + VST;   // [2]
+  uint64_t* p_ready = s_full + 2;     // [2], 4 warps
+  uint64_t* o_full = p_ready + 2;     // [2]
+  uint64_t* o_free = o_full + 2;      // [2], 4 warps
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_free + 2);
+  __shared__ uint4 stg_all[8][32 * 4];   // per softmax warp: 32 rows x 32 half values
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapQ);
+    tma_prefetch_desc(&mapK);
+    tma_prefetch_desc(&mapV);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_ready[i], 4);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_free[i], 4);
+    }
+    for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
+    for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const int nz = p.total / p.nu;
+  // key blocks needed by the tile whose queries end (exclusive) at qend
+  auto nblk = [&](int qend) { return (min(p.s, qend) + KB - 1) / KB; };
+
+  if (warp == 0) {
+    int ks = 0, vs = 0;
+    uint32_t kph = 0, vph = 0;
+    int uc = 0;   // units processed (q_empty parity)
+    for (int rnd = 0;; ++rnd, ++uc) {
+      const int t = snake_unit(rnd);
+      if (t >= p.total) break;
+      const int z = t % nz, u = p.nu - 1 - t / nz;
+      const int z1 = z % p.heads, z2 = z / p.heads;
+      const int nB = nblk(256 * u + 256);
+      for (int x = 0; x < 2; ++x) {
+        mbar_wait(&q_empty[x], (uint32_t)((uc & 1) ^ 1));
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&q_full[x], Q_BYTES);
+          for (int c = 0; c < NC; ++c)
+            tma_load_4d(sQ + x * Q_BYTES + c * 16384, &mapQ, &q_full[x], 64 * c, 256 * u + 128 * x, z1, z2);
+        }
+        __syncwarp();
+      }
+      for (int j = 0; j < nB; ++j) {
+        mbar_wait(&k_empty[ks], kph ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&k_full[ks], KV_BYTES);
+          for (int c = 0; c < NC; ++c)
+            tma_load_4d(sK + ks * KV_BYTES + c * KB * 128, &mapK, &k_full[ks], 64 * c, j * KB, z1, z2);
+        }
+        __syncwarp();
+        if (++ks == KST) { ks = 0; kph ^= 1; }
+        mbar_wait(&v_empty[vs], vph ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&v_full[vs], KV_BYTES);
+          for (int c = 0; c < NC; ++c)
+            tma_load_4d(sV + vs * KV_BYTES + c * KB * 128, &mapV, &v_full[vs], 64 * c, j * KB, z1, z2);
+        }
+        __syncwarp();
+        if (++vs == VST) { vs = 0; vph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idS = umma_idesc_f16(128, KB, 0, 0);
+    const uint32_t idO = umma_idesc_f16(128, NV, 0, 1);
+    const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV);
+    int ks = 0, vs = 0;
+    uint32_t kph = 0, vph = 0;
+    uint32_t pph[2] = {0, 0};   // p_ready parity per tile
+    int uc = 0;
+    auto issue_S = [&](int x, int kst) {   // S_x = Q_x K^T into TMEM columns S_COL(x)
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < NV / 16; ++kk) {
+          const int c = kk / 4, k = kk % 4;
+          mma_f16_ss(tmem + S_COL(x), umma_desc_sw128(q0 + x * Q_BYTES + c * 16384 + 32 * k, 16, 1024),
+                      umma_desc_sw128(k0 + kst * KV_BYTES + c * KB * 128 + 32 * k, 16, 1024), idS,
+                      kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[x]);
+      }
+      __syncwarp();
+    };
+    auto issue_PV = [&](int x, int vst, bool acc) {   // O_x (+)= P_x V (P from TMEM)
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < KB / 16; ++k)
+          mma_f16_ts(tmem + O_COL(x), tmem + S_COL(x) + 8 * k,
+                     umma_desc_sw128(v0 + vst * KV_BYTES + 2048 * k, KB * 128, 1024), idO,
+                     (acc || k > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+    };
+    for (int rnd = 0;; ++rnd, ++uc) {
+      const int t = snake_unit(rnd);
+      if (t >= p.total) break;
+      const int u = p.nu - 1 - t / nz;
+      const int nA = nblk(256 * u + 128), nB = nblk(256 * u + 256);
+      // S_A(0), S_B(0)
+      mbar_wait(&k_full[ks], kph);
+      tc_fence_after();
+      for (int x = 0; x < 2; ++x) {
+        mbar_wait(&q_full[x], (uint32_t)(uc & 1));
+        tc_fence_after();
+        issue_S(x, ks);
+        if ((x ? nB : nA) == 1 && elect_one()) mma_commit(&q_empty[x]);   // Q_x's last use
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(&k_empty[ks]);
+      __syncwarp();
+      if (++ks == KST) { ks = 0; kph ^= 1; }
+      for (int j = 0; j < nB; ++j) {
+        mbar_wait(&v_full[vs], vph);
+        tc_fence_after();
+        const bool knext = j + 1 < nB;
+        if (knext) {   // block j+1's keys (S_A(j+1) and / or S_B(j+1))
+          mbar_wait(&k_full[ks], kph);
+          tc_fence_after();
+        }
+        for (int x = 0; x < 2; ++x) {
+          const int nX = x ? nB : nA;
+          if (j >= nX) continue;
+          mbar_wait(&p_ready[x], pph[x]);
+          pph[x] ^= 1;
+          if (j == 0) mbar_wait(&o_free[x], (uint32_t)((uc & 1) ^ 1));   // previous unit drained
+          tc_fence_after();
+          issue_PV(x, vs, j > 0);
+          if (j + 1 < nX) {
+            issue_S(x, ks);
+            if (j + 2 == nX && elect_one()) mma_commit(&q_empty[x]);   // Q_x's last use
+          } else if (elect_one()) {
+            mma_commit(&o_full[x]);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) {
+          mma_commit(&v_empty[vs]);
+          if (knext) mma_commit(&k_empty[ks]);
+        }
+        __syncwarp();
+        if (++vs == VST) { vs = 0; vph ^= 1; }
+        if (knext && ++ks == KST) { ks = 0; kph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int x = (warp - 4) / 4;              // tile
+    const int q = warp & 3, wi = warp - 4;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    uint4* stg = stg_all[wi];
+    uint32_t sph = 0;
+    int uc = 0;
+    for (int rnd = 0;; ++rnd, ++uc) {
+      const int t = snake_unit(rnd);
+      if (t >= p.total) break;
+      const int z = t % nz, u = p.nu - 1 - t / nz;
+      const int z1 = z % p.heads, z2 = z / p.heads;
+      const int qt0 = 256 * u + 128 * x;      // first query of the tile
+      const int row = qt0 + q * 32 + lane;    // this thread's query
+      const int nX = nblk(qt0 + 128);
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nX; ++j) {
+        mbar_wait(&s_full[x], sph);
+        sph ^= 1;
+        tc_fence_after();
+        uint32_t sr[KB];
+#pragma unroll
+        for (int c = 0; c < KB / 32; ++c)
+          tmem_ld32_nowait(trow + S_COL(x) + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
+        tmem_ld_wait();
+        const int kb0 = j * KB;
+        if (kb0 + KB - 1 > qt0 || kb0 + KB > p.s) {   // diagonal or ragged block: mask
+#pragma unroll
+          for (int i = 0; i < KB; ++i)
+            if (kb0 + i > row || kb0 + i >= p.s) sr[i] = __float_as_uint(-INFINITY);
+        }
+        float bmax = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < KB; ++i) bmax = fmaxf(bmax, __uint_as_float(sr[i]));
+        const float bm = bmax * p.c1;
+        float mnew = m;
+        bool resc = false;
+        if (j == 0) {
+          mnew = bm;
+        } else if (bm > m + F2_RESCALE_TH) {
+          mnew = bm;
+          resc = true;
+        }
+        const float factor = resc ? ex2_approx(m - mnew) : 1.f;
+        float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < KB / 64; ++c) {   // 64 scores -> 32 packed P columns (already read)
+          uint32_t pk[32];
+#pragma unroll
+          for (int i = 0; i < 64; i += 2) {
+            const float e0 = ex2_approx(fmaf(__uint_as_float(sr[64 * c + i]), p.c1, -mnew));
+            const float e1 = ex2_approx(fmaf(__uint_as_float(sr[64 * c + i + 1]), p.c1, -mnew));
+            sum0 += e0;
+            sum1 += e1;
+            pk[i / 2] = pack_hx2(e0, e1);
+          }
+          tmem_st32(trow + S_COL(x) + 32 * c, pk);
+        }
+        l = l * factor + (sum0 + sum1);
+        m = mnew;
+        if (__any_sync(0xffffffffu, resc)) {   // rare: rescale this warp's O rows (PV_X(j-1) done)
+#pragma unroll 1
+          for (int c = 0; c < NV / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(trow + O_COL(x) + 32 * c, r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
+            tmem_st32(trow + O_COL(x) + 32 * c, r);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_ready[x]);
+      }
+      if (row < p.s) p.lse[(long long)z * p.s + row] = m + __log2f(l);
+      // epilogue: O / l -> half -> o[token][head * d + j]
+      mbar_wait(&o_full[x], (uint32_t)(uc & 1));
+      tc_fence_after();
+      const float inv = 1.f / l;
+      hx* obase = p.o + ((long long)z2 * p.s) * p.ldo + (long long)z1 * p.d;
+      const int r0 = qt0 + q * 32;
+#pragma unroll 1
+      for (int oc = 0; oc < NV && oc < p.d; oc += 32) {
+        uint32_t r[32];
+        tmem_ld32(trow + O_COL(x) + oc, r);
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          uint4 w;
+          w.x = pack_hx2(__uint_as_float(r[8 * jj + 0]) * inv, __uint_as_float(r[8 * jj + 1]) * inv);
+          w.y = pack_hx2(__uint_as_float(r[8 * jj + 2]) * inv, __uint_as_float(r[8 * jj + 3]) * inv);
+          w.z = pack_hx2(__uint_as_float(r[8 * jj + 4]) * inv, __uint_as_float(r[8 * jj + 5]) * inv);
+          w.w = pack_hx2(__uint_as_float(r[8 * jj + 6]) * inv, __uint_as_float(r[8 * jj + 7]) * inv);
+          stg[lane * 4 + (jj ^ (lane & 3))] = w;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = i * 8 + lane / 4, ch = lane & 3;
+          const int gr = r0 + rr;
+          const int col = oc + ch * 8;
+          if (gr < p.s && col < p.d) {
+            const uint4 v = stg[rr * 4 + (ch ^ (rr & 3))];
+            store8h(obase + (long long)gr * p.ldo + col, v, p.d - col);
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[x]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+#undef S_COL
+#undef O_COL
+
+template <int NV, int KB>
+constexpr int fwd2_smem() {
+  return 2 * 128 * NV * 2 + 4 * KB * NV * 2 + 16 * 8 + 64 + 1024;
+}
+
+template <int NV, int KB>
+int launch_fwd2(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                const AttnFwd2Params& p, cudaStream_t st) {
+  constexpr int SMEM = fwd2_smem<NV, KB>();
+  static bool attr[kMaxDevices] = {};
+  const int dev = cur_device();
+  if (!attr[dev]) {
+    if (cudaFuncSetAttribute(attn_fwd2_kernel<NV, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
+        cudaSuccess)
+      return -10;
+    attr[dev] = true;
+  }
+  const int nsm = device_sms();
+  const int grid = p.total < nsm ? p.total : nsm;
+  attn_fwd2_kernel<NV, KB><<<grid, F2_THREADS, SMEM, st>>>(mq, mk, mv, p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
 // ------------------------------------------------------------------ backward
 // dS = alpha * P * (dP - D),  D_i = sum_j P_ij dP_ij = dO_i . O_i (computed by attn_bwd_d),
 // P recomputed from S and the forward's lse2 (never stored).  Two kernels of one template:
@@ -814,42 +1164,30 @@ __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, in
 
 int attn_fwd(const void* qkv, long long lq, int b, int heads, int s, int d, int dp, float alpha,
              void* o, long long ldo, float* lse, cudaStream_t st) {
-  if (s <= 0 || s > 512 || d <= 0 || dp < d || dp % 2 || (d & 1)) return -1;
+  if (s <= 0 || d <= 0 || dp < d || dp % 2 || (d & 1)) return -1;
   const int nv = (dp + 63) / 64 * 64;
-  if (nv > 256) return -1;
-  constexpr int SMEM = ATT_STAGES * ATT_STAGE + 1024 + 256;
-  static bool attr[kMaxDevices] = {};
-  const int dev_ = cur_device();
-  if (!attr[dev_]) {
-    if (cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
-        cudaSuccess)
-      return -10;
-    attr[dev_] = true;
-  }
+  if (nv > 192) return -1;
   const char* base = static_cast<const char*>(qkv);
+  const int kb = nv <= 128 ? 128 : 64;
   CUtensorMap mq, mk, mv;
   const long long s2 = (long long)s * lq;
-  int rc = make_tmap_4d(&mq, base, dp, s, lq, heads, dp, b, s2, QT);
-  if (!rc) rc = make_tmap_4d(&mk, base + (size_t)heads * dp * 2, dp, s, lq, heads, dp, b, s2, 256);
-  if (!rc) rc = make_tmap_4d(&mv, base + (size_t)2 * heads * dp * 2, dp, s, lq, heads, dp, b, s2, 64);
+  int rc = make_tmap_4d(&mq, base, dp, s, lq, heads, dp, b, s2, 128);
+  if (!rc) rc = make_tmap_4d(&mk, base + (size_t)heads * dp * 2, dp, s, lq, heads, dp, b, s2, kb);
+  if (!rc) rc = make_tmap_4d(&mv, base + (size_t)2 * heads * dp * 2, dp, s, lq, heads, dp, b, s2, kb);
   if (rc) return rc;
-  AttnParams p;
+  AttnFwd2Params p;
   p.s = s;
   p.heads = heads;
   p.d = d;
-  p.nv = nv;
-  p.num_m = (s + QT - 1) / QT;
-  p.total = p.num_m * b * heads;
+  p.nu = (s + 255) / 256;
+  p.total = p.nu * b * heads;
   p.c1 = alpha * 1.4426950408889634f;
   p.o = static_cast<hx*>(o);
   p.ldo = ldo;
   p.lse = lse;
-  int nsm = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = p.total < nsm ? p.total : nsm;
-  attn_fwd_kernel<<<grid, ATT_THREADS, SMEM, st>>>(mq, mk, mv, p);
-  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+  if (nv == 64) return launch_fwd2<64, 128>(mq, mk, mv, p, st);
+  if (nv == 128) return launch_fwd2<128, 128>(mq, mk, mv, p, st);
+  return launch_fwd2<192, 64>(mq, mk, mv, p, st);
 }
 
 int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long long ldo,
@@ -924,7 +1262,9 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
 
 int preload_attn() {
   cudaFuncAttributes a;
-  if (cudaFuncGetAttributes(&a, attn_fwd_kernel) != cudaSuccess) return -1;
+  if (cudaFuncGetAttributes(&a, attn_fwd2_kernel<64, 128>) != cudaSuccess) return -1;
+  if (cudaFuncGetAttributes(&a, attn_fwd2_kernel<128, 128>) != cudaSuccess) return -1;
+  if (cudaFuncGetAttributes(&a, attn_fwd2_kernel<192, 64>) != cudaSuccess) return -1;
   if (cudaFuncGetAttributes(&a, attn_bwd_kernel<true>) != cudaSuccess) return -1;
   if (cudaFuncGetAttributes(&a, attn_bwd_kernel<false>) != cudaSuccess) return -1;
   return cudaFuncGetAttributes(&a, attn_bwd_d_kernel) == cudaSuccess ? 0 : -1;

@@ -46,10 +46,32 @@ def reference(x, d, alpha):
 
 @pytest.mark.parametrize("b,heads,s,d,dp", [(2, 2, 32, 32, 32), (1, 4, 512, 128, 128),
                                             (2, 3, 200, 64, 64), (1, 2, 512, 188, 192),
-                                            (1, 2, 384, 176, 176), (8, 2, 512, 128, 128)])
+                                            (1, 2, 384, 176, 176), (8, 2, 512, 128, 128),
+                                            (1, 2, 1024, 128, 128), (1, 2, 700, 10, 16),
+                                            (2, 1, 520, 188, 192)])
 def test_attn_fwd_matches_definition(lib, b, heads, s, d, dp):
+    """Streamed-key forward at any s: one, two and several 256-query units, ragged tails (the
+    second tile of the last unit partly or wholly past s), 64 / 128 / 192-wide padded heads."""
+    run_fwd(lib, b, heads, s, d, dp, make_qkv(b, heads, s, d, dp, seed=s + d))
+
+
+def test_attn_fwd_rescale_path(lib):
+    """Keys whose scores grow along the sequence (k_t scaled by 1 + 6 t / s): a row's running
+    max rises by far more than the lazy-rescale threshold (2^8) from block to block, so the
+    online softmax takes its rescale path (l and the O row multiplied by exp2(m - m'))."""
     import torch
-    qkv, x = make_qkv(b, heads, s, d, dp, seed=s + d)
+    b, heads, s, d, dp = 1, 2, 512, 128, 128
+    rng = np.random.default_rng(5)
+    x = np.zeros((b * s, 3, heads, dp), np.float32)
+    x[..., :d] = rng.standard_normal((b * s, 3, heads, d)) * 1.5
+    x[:, 1] *= (1.0 + 6.0 * np.arange(b * s) / s)[:, None, None]
+    t = torch.from_numpy(x.reshape(b * s, 3 * heads * dp)).to(torch.bfloat16).cuda()
+    run_fwd(lib, b, heads, s, d, dp, (t, t.float().cpu().numpy().astype(np.float64).reshape(b, s, 3, heads, dp)))
+
+
+def run_fwd(lib, b, heads, s, d, dp, made):
+    import torch
+    qkv, x = made
     h = heads * d
     o = torch.full((b * s, h), float("nan"), dtype=torch.bfloat16, device="cuda")
     lse = torch.zeros(b * heads * s, dtype=torch.float32, device="cuda")
