@@ -21,6 +21,12 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 LIBS = {"bf16": os.path.join(HERE, "libaxonn.so"), "fp16": os.path.join(HERE, "libaxonn_fp16.so")}
+# diagnostic builds only (never loaded by the package): extra -D defines into a separately
+# named library, e.g. AXONN_DIAG_DEFINES="-DAXONN_ATTN_EXP=1" AXONN_DIAG_TAG=_exp1
+DIAG_DEFINES = os.environ.get("AXONN_DIAG_DEFINES", "").split()
+DIAG_TAG = os.environ.get("AXONN_DIAG_TAG", "")
+if DIAG_TAG:
+    LIBS = {k: v.replace(".so", DIAG_TAG + ".so") for k, v in LIBS.items()}
 LIB = LIBS["bf16"]
 DEFINES = {"bf16": [], "fp16": ["-DAXONN_HALF_FP16"]}
 
@@ -41,7 +47,7 @@ def sources():
 
 
 def _digest(dtype: str):
-    h = hashlib.sha256(dtype.encode())
+    h = hashlib.sha256((dtype + " ".join(DIAG_DEFINES)).encode())
     for f in sources() + sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))) + [
             os.path.join(ROOT, "include", "axonn.h"), __file__]:
         with open(f, "rb") as fh:
@@ -61,11 +67,11 @@ def _build_one(dtype: str, force: bool, verbose: bool, pool: ThreadPoolExecutor)
     if not force and os.path.exists(lib_path) and os.path.exists(stamp) and open(stamp).read() == dig:
         return lib_path
     inc, lib = nccl_dirs()
-    objdir = os.path.join(HERE, "build", dtype)
+    objdir = os.path.join(HERE, "build", dtype + DIAG_TAG)
     os.makedirs(objdir, exist_ok=True)
     flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
              "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
-             "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc] + DEFINES[dtype]
+             "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc] + DEFINES[dtype] + DIAG_DEFINES
     if verbose:
         flags = ["-Xptxas=-v"] + flags
     objs, jobs = [], []

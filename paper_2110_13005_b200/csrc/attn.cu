@@ -368,6 +368,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 // quarter = warp % 4), 8-11 of tile B.  Each softmax thread owns one query row and keeps the
 // row's KB scores of the block in registers (one TMEM read per score).
 constexpr int F2_THREADS = 12 * 32;
+// Diagnostic builds only (scripts/attn_exp.sh; never the shipped library): AXONN_ATTN_EXP bit 0
+// skips the softmax math (P = 0), bit 1 skips the MMA instructions (commits only), bit 2 the
+// epilogue's global stores.
+#ifndef AXONN_ATTN_EXP
+#define AXONN_ATTN_EXP 0
+#endif
 constexpr float F2_RESCALE_TH = 8.0f;   // log2 units
 
 struct AttnFwd2Params {
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     auto issue_S = [&](int x, int kst) {   // S_x = Q_x K^T into TMEM columns S_COL(x)
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < NV / 16; ++kk) {
+        for (int kk = 0; kk < ((AXONN_ATTN_EXP & 2) ? 0 : NV / 16); ++kk) {
           const int c = kk / 4, k = kk % 4;
           mma_f16_ss(tmem + S_COL(x), umma_desc_sw128(q0 + x * Q_BYTES + c * 16384 + 32 * k, 16, 1024),
                       umma_desc_sw128(k0 + kst * KV_BYTES + c * KB * 128 + 32 * k, 16, 1024), idS,
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     auto issue_PV = [&](int x, int vst, bool acc) {   // O_x (+)= P_x V (P from TMEM)
       if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < KB / 16; ++k)
+        for (int k = 0; k < ((AXONN_ATTN_EXP & 2) ? 0 : KB / 16); ++k)
           mma_f16_ts(tmem + O_COL(x), tmem + S_COL(x) + 8 * k,
                      umma_desc_sw128(v0 + vst * KV_BYTES + 2048 * k, KB * 128, 1024), idO,
                      (acc || k > 0) ? 1u : 0u);
@@ -526,10 +532,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         mbar_wait(&v_full[vs], vph);
         tc_fence_after();
         const bool knext = j + 1 < nB;
-        if (knext) {   // block j+1's keys (S_A(j+1) and / or S_B(j+1))
-          mbar_wait(&k_full[ks], kph);
-          tc_fence_after();
-        }
+        bool kwaited = false;
         for (int x = 0; x < 2; ++x) {
           const int nX = x ? nB : nA;
           if (j >= nX) continue;
@@ -539,6 +542,11 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
           tc_fence_after();
           issue_PV(x, vs, j > 0);
           if (j + 1 < nX) {
+            if (!kwaited) {   // block j+1's keys: waited only here, after PV_x(j) is queued
+              mbar_wait(&k_full[ks], kph);
+              tc_fence_after();
+              kwaited = true;
+            }
             issue_S(x, ks);
             if (j + 2 == nX && elect_one()) mma_commit(&q_empty[x]);   // Q_x's last use
           } else if (elect_one()) {
@@ -605,8 +613,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
           uint32_t pk[32];
 #pragma unroll
           for (int i = 0; i < 64; i += 2) {
-            const float e0 = ex2_approx(fmaf(__uint_as_float(sr[64 * c + i]), p.c1, -mnew));
-            const float e1 = ex2_approx(fmaf(__uint_as_float(sr[64 * c + i + 1]), p.c1, -mnew));
+            const float e0 = (AXONN_ATTN_EXP & 1) ? 0.f : ex2_approx(fmaf(__uint_as_float(sr[64 * c + i]), p.c1, -mnew));
+            const float e1 = (AXONN_ATTN_EXP & 1) ? 0.f : ex2_approx(fmaf(__uint_as_float(sr[64 * c + i + 1]), p.c1, -mnew));
             sum0 += e0;
             sum1 += e1;
             pk[i / 2] = pack_hx2(e0, e1);
@@ -656,7 +664,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
           const int rr = i * 8 + lane / 4, ch = lane & 3;
           const int gr = r0 + rr;
           const int col = oc + ch * 8;
-          if (gr < p.s && col < p.d) {
+          if (gr < p.s && col < p.d && !(AXONN_ATTN_EXP & 4)) {
             const uint4 v = stg[rr * 4 + (ch ^ (rr & 3))];
             store8h(obase + (long long)gr * p.ldo + col, v, p.d - col);
           }

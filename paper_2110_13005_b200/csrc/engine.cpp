@@ -21,9 +21,11 @@
 // process, with a sum / max reduction riding on each rendezvous and a registry of the
 // stages' receive slots and flag words.
 struct axonn_local_group {
-  struct Reg {
+  struct Reg {   // indexed by world rank (= replica * G_inter + stage)
     uint32_t* flags = nullptr;          // device-visible address of the stage's flag words
     std::vector<void*> act, grad;       // receive slots: activations (slot.in), gradients (slot.grecv)
+    const void* g16 = nullptr;          // half gradients (fused column reduction, G_data > 1)
+    uint32_t* dp_flags = nullptr;       // device-visible address of its column flag words
   };
   int size = 0;
   std::mutex mu;
@@ -214,6 +216,10 @@ static int init_weights(Ctx* c) {
   return 0;
 }
 
+static int64_t chunk_elems(const Ctx* c) {
+  return (int64_t)c->oc.coarsen_k * c->oc.bucket_elems;
+}
+
 // ------------------------------------------------------------------ peer-copy links
 // Stream memory operations (driver API, resolved once through the runtime's entry-point query).
 typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
@@ -226,10 +232,11 @@ static void* driver_fn(const char* name) {
     return nullptr;
   return p;
 }
-static int wait_flag(Ctx* c, cudaStream_t st, const uint32_t* flag, uint32_t v) {
+static int wait_flag(Ctx* c, cudaStream_t st, const uint32_t* flag, uint32_t v, bool geq = false) {
   static PFN_waitValue32 fn = (PFN_waitValue32)driver_fn("cuStreamWaitValue32");
   if (!fn) return c->fail(AXONN_ERR_CUDA, "cuStreamWaitValue32 unavailable");
-  if (fn((CUstream)st, (CUdeviceptr)flag, v, CU_STREAM_WAIT_VALUE_EQ) != CUDA_SUCCESS)
+  if (fn((CUstream)st, (CUdeviceptr)flag, v, geq ? CU_STREAM_WAIT_VALUE_GEQ : CU_STREAM_WAIT_VALUE_EQ) !=
+      CUDA_SUCCESS)
     return c->fail(AXONN_ERR_CUDA, "cuStreamWaitValue32");
   return 0;
 }
@@ -309,6 +316,53 @@ static int ipc_links(Ctx* c) {
   return 0;
 }
 
+// Fused column reduction (reading D-35): exchange CUDA IPC handles of grad16 and of the column
+// flag words with the other replicas of this stage (all-gather over the column comm) and map
+// them.  K9 then reads the peers' half gradients over NVLink.
+static int dp_links(Ctx* c) {
+  const int G = c->g_data;
+  const size_t HB = sizeof(cudaIpcMemHandle_t);
+  int rc;
+  c->dp_flags = (uint32_t*)c->dalloc(2 * G * sizeof(uint32_t));
+  if (!c->dp_flags) return c->fail(AXONN_ERR_OOM, "dp flags");
+  if ((rc = c->check_cuda(cudaMemset(c->dp_flags, 0, 2 * G * sizeof(uint32_t)), "dp flags"))) return rc;
+  std::vector<char> mine(2 * HB), all(2 * HB * G);
+  if ((rc = c->check_cuda(cudaIpcGetMemHandle((cudaIpcMemHandle_t*)mine.data(), c->grad16), "ipc grad16")) ||
+      (rc = c->check_cuda(cudaIpcGetMemHandle((cudaIpcMemHandle_t*)(mine.data() + HB), c->dp_flags),
+                          "ipc dp flags")))
+    return rc;
+  char* dbuf = (char*)c->dalloc(2 * HB * (G + 1));
+  if (!dbuf) return c->fail(AXONN_ERR_OOM, "dp ipc exchange buffer");
+  if ((rc = c->check_cuda(cudaMemcpy(dbuf, mine.data(), 2 * HB, cudaMemcpyHostToDevice), "dp ipc h2d")) ||
+      (rc = c->check_nccl(ncclAllGather(dbuf, dbuf + 2 * HB, 2 * HB, ncclChar, c->dp_comm, c->s_comp),
+                          "dp ipc allgather")) ||
+      (rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "dp ipc sync")) ||
+      (rc = c->check_cuda(cudaMemcpy(all.data(), dbuf + 2 * HB, 2 * HB * G, cudaMemcpyDeviceToHost), "dp ipc d2h")))
+    return rc;
+  c->dp_g16.assign(G, nullptr);
+  c->dp_peer_flags.assign(G, nullptr);
+  for (int j = 0; j < G; ++j) {
+    if (j == c->replica) {
+      c->dp_g16[j] = c->grad16;
+      c->dp_peer_flags[j] = c->dp_flags;
+      continue;
+    }
+    void* p = nullptr;
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, all.data() + 2 * HB * j, HB);
+    if ((rc = c->check_cuda(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess), "ipc open grad16")))
+      return rc;
+    c->ipc_opened.push_back(p);
+    c->dp_g16[j] = p;
+    memcpy(&hd, all.data() + 2 * HB * j + HB, HB);
+    if ((rc = c->check_cuda(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess), "ipc open dp flags")))
+      return rc;
+    c->ipc_opened.push_back(p);
+    c->dp_peer_flags[j] = (uint32_t*)p;
+  }
+  return 0;
+}
+
 // Loopback links (test-only local group): the flag words are host-mapped pinned memory
 // (written by the neighbours' stream memops, observed by this context's host thread); slot
 // and flag addresses are published in the group and read back after a rendezvous.
@@ -323,9 +377,21 @@ static int local_links(Ctx* c) {
   memset(hf, 0, 2 * L * sizeof(uint32_t));
   c->flags_host = hf;
   if ((rc = c->check_cuda(cudaHostGetDevicePointer((void**)&c->flags, hf, 0), "host flags map"))) return rc;
+  uint32_t* dpf = nullptr;
+  if (c->dp_fused) {   // column flag words, host-mapped so this thread can observe them
+    if ((rc = c->check_cuda(cudaHostAlloc((void**)&dpf, 2 * c->g_data * sizeof(uint32_t),
+                                          cudaHostAllocMapped | cudaHostAllocPortable), "host dp flags")))
+      return rc;
+    memset(dpf, 0, 2 * c->g_data * sizeof(uint32_t));
+    c->dp_flags_host = dpf;
+    if ((rc = c->check_cuda(cudaHostGetDevicePointer((void**)&c->dp_flags, dpf, 0), "host dp flags map")))
+      return rc;
+  }
   {
     std::lock_guard<std::mutex> lk(g->mu);
-    axonn_local_group::Reg& r = g->reg[c->stage];
+    axonn_local_group::Reg& r = g->reg[c->rank];
+    r.g16 = c->grad16;
+    r.dp_flags = c->dp_flags;
     r.flags = c->flags;
     r.act.assign(L, nullptr);
     r.grad.assign(L, nullptr);
@@ -337,12 +403,20 @@ static int local_links(Ctx* c) {
   if (g->rendezvous(nullptr, nullptr, group_timeout_s())) return c->fail(AXONN_ERR_STATE, "local group failed");
   std::lock_guard<std::mutex> lk(g->mu);
   if (!c->last) {
-    c->peer_flags_next = g->reg[c->stage + 1].flags;
-    c->peer_act = g->reg[c->stage + 1].act;
+    c->peer_flags_next = g->reg[c->rank + 1].flags;
+    c->peer_act = g->reg[c->rank + 1].act;
   }
   if (!c->first) {
-    c->peer_flags_prev = g->reg[c->stage - 1].flags;
-    c->peer_grad = g->reg[c->stage - 1].grad;
+    c->peer_flags_prev = g->reg[c->rank - 1].flags;
+    c->peer_grad = g->reg[c->rank - 1].grad;
+  }
+  if (c->dp_fused) {   // the column: replicas j of this stage, rank j * G_inter + stage
+    c->dp_g16.assign(c->g_data, nullptr);
+    c->dp_peer_flags.assign(c->g_data, nullptr);
+    for (int j = 0; j < c->g_data; ++j) {
+      c->dp_g16[j] = g->reg[j * c->g_inter + c->stage].g16;
+      c->dp_peer_flags[j] = g->reg[j * c->g_inter + c->stage].dp_flags;
+    }
   }
   return 0;
 }
@@ -590,7 +664,9 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
       opt->pipeline_limit < 0)
     return AXONN_ERR_INVALID_ARG;
   axonn_local_group* lg = (dist && world > 1) ? dist->local_group : nullptr;
-  if (lg && (lg->size != world || g_data != 1)) return AXONN_ERR_INVALID_ARG;
+  // loopback: no NCCL, so G_data > 1 needs the fused column reduction (bf16 build, <= 8 replicas)
+  if (lg && (lg->size != world || (g_data > 1 && (kHalfDtype != AXONN_BF16 || g_data > kMaxReplicas))))
+    return AXONN_ERR_INVALID_ARG;
   if (world > 1 && !lg && !dist->nccl_id) return AXONN_ERR_INVALID_ARG;
   if (opt->checkpoint_interval < -1 ||   // BadCheckpointInterval: ac must divide N / G_inter
       (opt->checkpoint_interval > 1 && (model->n_layers / g_inter) % opt->checkpoint_interval))
@@ -603,6 +679,11 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   if (c->oc.bucket_elems % 4) c->oc.bucket_elems += 4 - c->oc.bucket_elems % 4;   // 16-B aligned buckets
   c->rank = rank; c->world = world; c->device = dist ? dist->device : 0;
   c->lg = lg;
+  {
+    const char* e = getenv("AXONN_DP");   // must agree on all ranks (same launcher env)
+    c->dp_fused = g_data > 1 && g_data <= kMaxReplicas && kHalfDtype == AXONN_BF16 &&
+                  (lg || !(e && strcmp(e, "nccl") == 0));
+  }
   c->stage = rank % g_inter;            // world_rank = j * G_inter + i (D-29)
   c->replica = rank / g_inter;
   c->first = c->stage == 0;
@@ -741,9 +822,11 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   if (c->lg) {
     c->p2p_ipc = 1;   // the loopback runs the peer-copy link protocol
     if ((rc = local_links(c))) return bail(rc);
-  } else if (world > 1 && g_inter > 1 && c->p2p_ipc && (rc = ipc_links(c))) {
-    return bail(rc);
+  } else {
+    if (world > 1 && g_inter > 1 && c->p2p_ipc && (rc = ipc_links(c))) return bail(rc);
+    if (c->dp_fused && (rc = dp_links(c))) return bail(rc);
   }
+  c->n_chunks = (c->nflat + chunk_elems(c) - 1) / chunk_elems(c);
   if ((rc = c->check_cuda(cudaStreamSynchronize(c->s_comp), "init sync"))) return bail(rc);
   *out = c;
   return AXONN_OK;
@@ -766,6 +849,7 @@ AXONN_API void axonn_free(axonn_ctx* c) {
   }
   if (c->h_loss) cudaFreeHost(c->h_loss);
   if (c->flags_host) cudaFreeHost((void*)c->flags_host);
+  if (c->dp_flags_host) cudaFreeHost((void*)c->dp_flags_host);
   if (c->dtok) cudaFree(c->dtok);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_pool_opt) cudaEventDestroy(e);
@@ -954,6 +1038,33 @@ AXONN_API axonn_status axonn_stats(const axonn_ctx* c, double* out, int n) {
 // ------------------------------------------------------------------ Alg. 2 + Alg. 1
 namespace axonn {
 
+// Column flag words of the fused reduction (reading D-35).  A stream waits (cuStreamWaitValue32,
+// cyclic >=) for every peer's word base + j; the loopback's host thread observes its
+// host-mapped words instead (no kernel or stream of one device waits on another context).
+int Ctx::dp_wait(cudaStream_t st, int base, uint32_t value) {
+  for (int j = 0; j < g_data; ++j) {
+    if (j == replica) continue;
+    if (dp_flags_host) {
+      const auto t0 = std::chrono::steady_clock::now();
+      while ((int32_t)(dp_flags_host[base + j] - value) < 0) {
+        if (lg && lg->failed) return fail(AXONN_ERR_STATE, "local group failed (column flags)");
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > group_timeout_s())
+          return fail(AXONN_ERR_TIMEOUT, "fused column reduction: peer flag never arrived");
+        std::this_thread::yield();
+      }
+    } else if (int rc = wait_flag(this, st, dp_flags + base + j, value, true)) {
+      return rc;
+    }
+  }
+  return 0;
+}
+int Ctx::dp_signal(cudaStream_t st, int slot, uint32_t value) {
+  for (int k = 0; k < g_data; ++k)
+    if (k != replica)
+      if (int rc = write_flag(this, st, dp_peer_flags[k] + slot, value)) return rc;
+  return 0;
+}
+
 // Alg. 2 on this rank for microbatches 0..m-1.
 int Ctx::ar_ready(int64_t lo) {
   if (lo >= ar_hi) return 0;
@@ -966,6 +1077,8 @@ int Ctx::ar_ready(int64_t lo) {
   if (!ar_active && opt_pending &&   // grad16 is read by the still-running optimizer step
       (rc = check_cuda(cudaStreamWaitEvent(s_dp, ev_opt_done, 0), "ar wait opt")))
     return rc;
+  // fused column reduction: the peers' K9 of the previous batch read this grad16
+  if (!ar_active && dp_fused && dp_epoch > 1 && (rc = dp_wait(s_dp, g_data, dp_epoch - 1))) return rc;
   ar_active = true;
   if (cast_f32_hx(grad32 + lo, static_cast<char*>(grad16) + lo * 2, ar_hi - lo, s_dp))
     return fail(AXONN_ERR_CUDA, "cast");
@@ -974,7 +1087,10 @@ int Ctx::ar_ready(int64_t lo) {
   const int64_t ch = (int64_t)oc.coarsen_k * oc.bucket_elems;
   while (ar_next_chunk >= 0 && ar_next_chunk * ch >= lo) {
     const int64_t c0 = ar_next_chunk * ch, n = std::min(ch, nflat - c0);
-    if (g_data > 1) {   // Alg. 1 l.13: SUM over the column (pre-divided loss, D-10)
+    if (dp_fused) {     // Alg. 1 l.13 fused into every replica's K9: tell the peers
+      if ((rc = dp_signal(s_dp, replica, dp_progress(ar_next_chunk)))) return rc;
+      stats[AXONN_STAT_ALLREDUCE_BYTES] += n * 2.0 * (g_data - 1);   // read by the peers' K9
+    } else if (g_data > 1) {   // Alg. 1 l.13: SUM over the column (pre-divided loss, D-10)
       if ((rc = check_nccl(ncclAllReduce(static_cast<char*>(grad16) + c0 * 2, static_cast<char*>(grad16) + c0 * 2,
                                          n, kNcclHalf, ncclSum, dp_comm, s_dp), "ncclAllReduce")))
         return rc;
@@ -1174,9 +1290,6 @@ static int run_pipeline(Ctx* c, int m) {
   return 0;
 }
 
-static int64_t chunk_elems(const Ctx* c) {
-  return (int64_t)c->oc.coarsen_k * c->oc.bucket_elems;
-}
 
 // Alg. 1 l.4-6 + l.11-14 on this rank.
 static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_device, int batch,
@@ -1258,7 +1371,8 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
   CU(cudaEventRecord(c->ph[par][0], c->s_comp));
   const int64_t ch_elems = chunk_elems(c);
   // AXONN_AR_OVERLAP=0: cast and reduce everything after the pipeline instead (same values)
-  c->ar_overlap = !(getenv("AXONN_AR_OVERLAP") && getenv("AXONN_AR_OVERLAP")[0] == '0');
+  c->ar_overlap = c->dp_fused || !(getenv("AXONN_AR_OVERLAP") && getenv("AXONN_AR_OVERLAP")[0] == '0');
+  if (c->dp_fused) ++c->dp_epoch;   // progress / read-done values of this batch
   c->ar_active = false;
   c->ev_chunk.clear();
   if (c->ar_overlap) {
@@ -1435,6 +1549,16 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
   } else {
     for (int64_t b = 0; b < nbk; ++b) order.push_back(b);
   }
+  // fused column reduction (reading D-35): K9 sums the replicas' half gradients itself
+  const bool sum_peers = c->dp_fused && !c->ev_chunk.empty();
+  std::vector<const void*> gp(c->g_data);
+  auto k9 = [&](int64_t lo0, int64_t n0, float* th, float* mm, float* vv) -> int {
+    void* t16 = static_cast<char*>(c->theta16) + lo0 * 2;
+    if (!sum_peers)
+      return adamw_launch(n0, static_cast<const char*>(c->grad16) + lo0 * 2, th, mm, vv, t16, sc, c->s_opt);
+    for (int j = 0; j < c->g_data; ++j) gp[j] = static_cast<const char*>(c->dp_g16[j]) + lo0 * 2;
+    return adamw_sum_launch(n0, gp.data(), c->g_data, th, mm, vv, t16, sc, c->s_opt);
+  };
   int64_t pend_lo = -1;   // in-HBM: first element of the run not yet handed to a launch
   for (size_t q = 0; q < order.size(); ++q) {
     const int64_t bucket = order[q];
@@ -1443,6 +1567,10 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
     const int64_t ci = lo / ch;
     if (ci != chunk_idx && ci < (int64_t)c->ev_chunk.size()) {   // bucket waits for its chunk
       if (c->ev_chunk[ci]) CU(cudaStreamWaitEvent(c->s_opt, c->ev_chunk[ci], 0));
+      if (sum_peers) {   // ... on every replica of the column
+        const int rc = c->dp_wait(c->s_opt, 0, c->dp_progress(ci));
+        if (rc) return (axonn_status)rc;
+      }
       chunk_idx = ci;
     }
     void* t16 = static_cast<char*>(c->theta16) + lo * 2;
@@ -1457,7 +1585,7 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
       CU(cudaEventRecord(c->ev_h2d[r], c->s_h2d));
       CU(cudaStreamWaitEvent(c->s_opt, c->ev_h2d[r], 0));
       if (c->profiling) { pr.a = c->ev_opt(); pr.b = c->ev_opt(); cudaEventRecord(pr.a, c->s_opt); }
-      if (adamw_launch(n, g, c->ring[r][0], c->ring[r][1], c->ring[r][2], t16, sc, c->s_opt))
+      if (k9(lo, n, c->ring[r][0], c->ring[r][1], c->ring[r][2]))
         return (axonn_status)c->fail(AXONN_ERR_CUDA, "adamw launch");
       if (c->profiling) { cudaEventRecord(pr.b, c->s_opt); pr.work = n * 28.0; pr.kind = 1; c->prof.push_back(pr); }
       CU(cudaEventRecord(c->ev_adam[r], c->s_opt));
@@ -1484,13 +1612,17 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
       const void* g2 = static_cast<const char*>(c->grad16) + pend_lo * 2;
       void* t2 = static_cast<char*>(c->theta16) + pend_lo * 2;
       if (c->profiling) { pr.a = c->ev_opt(); pr.b = c->ev_opt(); cudaEventRecord(pr.a, c->s_opt); }
-      if (adamw_launch(n2, g2, c->master + pend_lo, c->adam_m + pend_lo, c->adam_v + pend_lo, t2, sc, c->s_opt))
+      if (k9(pend_lo, n2, c->master + pend_lo, c->adam_m + pend_lo, c->adam_v + pend_lo))
         return (axonn_status)c->fail(AXONN_ERR_CUDA, "adamw launch");
       if (c->profiling) { cudaEventRecord(pr.b, c->s_opt); pr.work = n2 * 28.0; pr.kind = 1; c->prof.push_back(pr); }
       if (overlap) CU(cudaEventRecord(c->ev_bucket[bucket], c->s_opt));
       pend_lo = -1;
       ++c->launches;
     }
+  }
+  if (sum_peers) {   // every peer's grad16 has been read: they may overwrite it
+    const int rc = c->dp_signal(c->s_opt, c->g_data + c->replica, c->dp_epoch);
+    if (rc) return (axonn_status)rc;
   }
   if (c->oc.offload) {
     cudaEvent_t e = c->ev();

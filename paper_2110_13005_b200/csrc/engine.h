@@ -138,6 +138,27 @@ struct Ctx {
   // and observed by this context's host thread; loss / overflow flag reduced through the group
   axonn_local_group* lg = nullptr;
   volatile uint32_t* flags_host = nullptr;
+  // Fused column reduction (reading D-35; G_data > 1, bf16 build): there is
+  // no all-reduce call.  During the last backward each replica casts its gradient chunks to
+  // the half format (Ctx::ar_ready) and stores a progress value into every peer's flag word;
+  // each replica's K9 then waits for its chunk's flags and sums the G_data replicas' half
+  // gradients itself, reading the peers' grad16 over NVLink (CUDA IPC mappings; loopback:
+  // buffers of the other contexts on this device).  After its last K9 a replica stores a
+  // read-done value into every peer, and a replica's next cast waits for all of them.
+  // AXONN_DP=nccl selects ncclAllReduce instead (the fp16 build always does: its overflow
+  // scan needs the reduced gradient).
+  bool dp_fused = false;
+  std::vector<const void*> dp_g16;    // [G_data] grad16 of replica j (own one at [replica])
+  uint32_t* dp_flags = nullptr;       // device-visible [2 G_data]: progress of j, read-done of j
+  volatile uint32_t* dp_flags_host = nullptr;   // loopback: host view of dp_flags
+  std::vector<uint32_t*> dp_peer_flags;         // [G_data] replica k's dp_flags (mapped)
+  uint32_t dp_epoch = 0;              // batches reduced so far (1-based during a batch)
+  int64_t n_chunks = 0;
+  int dp_wait(cudaStream_t st, int base, uint32_t value);     // every peer's flag base + j >= value
+  int dp_signal(cudaStream_t st, int slot, uint32_t value);   // store value into every peer's slot
+  uint32_t dp_progress(int64_t chunk) const {                 // chunk ready in this epoch
+    return dp_epoch * (uint32_t)(n_chunks + 1) + (uint32_t)(n_chunks - chunk);
+  }
   uint32_t msg_base = 0;              // sequence number base: messages of earlier batches
   cudaEvent_t ev_grads_ready = nullptr, ev_opt_done = nullptr, ev_loss = nullptr;
   std::vector<cudaEvent_t> ev_chunk;

@@ -11,6 +11,7 @@ namespace axonn {
 // Per-device one-time state (kernel attributes and SM counts are per device; one process may
 // drive several devices, e.g. axonn_calibrate_speed or the loopback transport).
 constexpr int kMaxDevices = 64;
+constexpr int kMaxReplicas = 8;   // G_data limit of the fused column reduction (adamw_sum_launch)
 inline int cur_device() {
   int d = 0;
   cudaGetDevice(&d);
@@ -72,6 +73,9 @@ int preload_ops();
 int preload_adamw();
 int adamw_launch(long long n, const void* g16, float* theta, float* m, float* v, void* theta16,
                  const float* scalars9, cudaStream_t st);
+// AdamW on g = fp32 sum over j < ng (ascending) of g16s[j][0..n) (the column all-reduce fused in)
+int adamw_sum_launch(long long n, const void* const* g16s, int ng, float* theta, float* m, float* v,
+                     void* theta16, const float* scalars9, cudaStream_t st);
 
 // ops.cu
 int embed_fwd(const int32_t* tok, long long tok_ld, int b, int s, int h, const void* etok,

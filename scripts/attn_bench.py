@@ -11,10 +11,15 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
     from paper_2110_13005_b200 import _lib
-    lib = _lib.load()
+    if "--lib" in sys.argv:   # a diagnostic build (paper_2110_13005_b200/build.py AXONN_DIAG_TAG)
+        lib = _lib._declare(C.CDLL(sys.argv[sys.argv.index("--lib") + 1]))
+    else:
+        lib = _lib.load()
+    tag_arg = sys.argv[sys.argv.index("--tag") + 1] if "--tag" in sys.argv else ""
+    bs = int(sys.argv[sys.argv.index("--b") + 1]) if "--b" in sys.argv else 8
     st = torch.cuda.current_stream().cuda_stream
     only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
-    for tag, b, heads, s, d, dp in (("1.3B", 8, 16, 512, 128, 128), ("12B", 8, 24, 512, 188, 192)):
+    for tag, b, heads, s, d, dp in (("1.3B", bs, 16, 512, 128, 128), ("12B", bs, 24, 512, 188, 192)):
         if only and tag != only:
             continue
         lq = 3 * heads * dp
@@ -39,7 +44,8 @@ def main():
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) / n * 1e3
         fl = 4.0 * b * heads * s * s * dp / 2   # causal half of QK^T and PV
-        print(json.dumps({"kernel": "attn_fwd", "shape": tag, "us": us, "tflops_causal": fl / us / 1e6}),
+        print(json.dumps({"kernel": "attn_fwd", "shape": tag, "b": b, "variant": tag_arg, "us": us,
+                          "tflops_causal": fl / us / 1e6}),
               flush=True)
         dO = (torch.randn(b * s, heads * dp, device="cuda") * 0.1).to(torch.bfloat16)
         dbuf = torch.empty(b * heads * s, device="cuda", dtype=torch.float32)
@@ -59,7 +65,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) / n * 1e3
-        print(json.dumps({"kernel": "attn_bwd", "shape": tag, "us": us,
+        print(json.dumps({"kernel": "attn_bwd", "shape": tag, "b": b, "variant": tag_arg, "us": us,
                           "tflops_causal": 2.5 * fl / us / 1e6}), flush=True)
 
 

@@ -159,15 +159,103 @@ def test_loopback_12b_layer_shape_vs_oracle():
 
 
 def test_loopback_bad_group_arguments():
-    """A loopback group requires G_data = 1 and world_size == group size (INVALID_ARG)."""
+    """A loopback group needs world_size == group size, and G_data > 1 needs the bf16 build
+    (the fused column reduction; there is no NCCL in the loopback) (INVALID_ARG)."""
     from paper_2110_13005_b200.engine import AxoNN, AxoNNError, LocalGroup
-    grp = LocalGroup(2)
+    grp = LocalGroup(2, "fp16")
     try:
         with pytest.raises(AxoNNError) as e:
-            AxoNN(1, 2, 2, **TINY, rank=0, world_size=2, device=0, local_group=grp)
+            AxoNN(1, 2, 2, **TINY, rank=0, world_size=2, device=0, local_group=grp, dtype="fp16",
+                  loss_scale=1024.0)
         assert e.value.status == "INVALID_ARG"
         with pytest.raises(AxoNNError) as e:
             AxoNN(4, 1, 2, **MINI, rank=0, world_size=4, device=0, local_group=grp)
         assert e.value.status == "INVALID_ARG"
     finally:
         grp.free()
+
+
+def grid_run(cfg, gi, gd, mb, params, batches, steps, **kw):
+    """A G_inter x G_data grid of loopback contexts on cuda:0 (rank = j * G_inter + i): the
+    pipelines of the G_data replicas plus the fused column reduction (reading D-35).  Returns
+    per-rank dicts of the first batch's fp32 / half gradients (un-reduced, this replica's rows)
+    and the final theta32, and the losses."""
+    from paper_2110_13005_b200.engine import (T_GRAD, T_GRAD32, T_MASTER, AxoNN, LocalGroup,
+                                              run_stages)
+    n = gi * gd
+    grp = LocalGroup(n)
+    engs = run_stages(lambda r: AxoNN(gi, gd, mb, **cfg, rank=r, world_size=n, device=0,
+                                      local_group=grp, **kw), n)
+    try:
+        for e in engs:
+            e.write_all(T_MASTER, {k: params[k] for k, _, _ in e.tensors()})
+        losses, g32, g16, th_pre = [], None, None, None
+        for b, tok in enumerate(batches):
+            ls = run_stages(lambda r: engs[r].run_batch(tok), n)
+            assert len(set(ls)) == 1, ls
+            losses.append(ls[0])
+            if b == 0:
+                g32 = [e.read_all(T_GRAD32) for e in engs]
+                g16 = [e.read_all(T_GRAD) for e in engs]
+                th_pre = [e.read_all(T_MASTER) for e in engs]
+            if b < steps:
+                run_stages(lambda r: engs[r].optimizer_step(), n)
+            if b == 0:
+                th_post = [e.read_all(T_MASTER) for e in engs]
+        return losses, g32, g16, th_pre, th_post, [e.read_all(T_MASTER) for e in engs]
+    finally:
+        for e in engs:
+            e.close()
+        grp.free()
+
+
+@pytest.mark.parametrize("cfg,gi,gd,mb,B", [(TINY, 1, 2, 2, 8), (MINI, 2, 2, 2, 16), (TINY, 1, 4, 1, 8)])
+def test_loopback_fused_column_reduction_vs_oracle(cfg, gi, gd, mb, B):
+    """Alg. 1 l.13 as the fused column reduction of reading D-35, on one
+    GPU: G_inter x G_data contexts; replica j runs rows [j B / G_data, (j+1) B / G_data) (Alg. 1
+    l.5).  Bars: the column sum of the fp32 partial gradients vs the oracle's full-batch gradient
+    (cos, scale, elementwise); K9 on every replica equals the oracle's fp32 AdamW applied to the
+    fp32 sum (ascending j) of the replicas' half gradients, bit for bit; all replicas end with
+    identical weights."""
+    from oracle import adamw
+    params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=42)
+    distinct = markov_tokens(3, cfg["seq_len"], cfg["vocab"], seed=29)
+    tok, counts = mixed_batch(distinct, B, seed=B + gd)
+    losses, g32, g16, th_pre, th_post, _ = grid_run(cfg, gi, gd, mb, params, [tok], steps=1,
+                                                    bucket_elems=7_000, coarsen_k=2)
+    loss_ref, g_ref = oracle_mixed(params, cfg, distinct, counts)
+    assert abs(losses[0] - loss_ref) <= 2e-2 * abs(loss_ref), (losses[0], loss_ref)
+    sc = adamw.step_scalars(1)
+    for i in range(gi):
+        col = [j * gi + i for j in range(gd)]
+        names = list(g32[col[0]])
+        gsum = {k: sum(g32[r][k].astype(np.float64) for r in col) for k in names}
+        assert_grads_close(gsum, g_ref, names=names, where=f"stage {i} column sum")
+        for k in names:
+            g = np.zeros_like(g16[col[0]][k], dtype=np.float32)
+            for r in col:   # fp32 sum in replica order of the half gradients (K9's order)
+                g = (g + g16[r][k].astype(np.float32)).astype(np.float32)
+            th = th_pre[col[0]][k].copy()
+            m = np.zeros_like(th)
+            v = np.zeros_like(th)
+            adamw.adamw_step_fp32(th, m, v, g, sc)
+            for r in col:
+                assert np.array_equal(th_post[r][k].view(np.uint32), th.view(np.uint32)), (r, k)
+
+
+def test_loopback_fused_reduction_offload_three_steps():
+    """2 x 2 grid, offloaded optimizer overlapping the next batch (D-32), 3 steps: every replica
+    of a stage ends with bit-identical weights, and the losses follow the single-context run
+    within the bf16 tolerance (the reduction sums the replicas' half gradients in fp32, the
+    single context casts one fp32 sum: not bitwise)."""
+    cfg = MINI
+    params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=3)
+    toks = [markov_tokens(16, cfg["seq_len"], cfg["vocab"], seed=70 + k) for k in range(3)]
+    kw = dict(offload=True, bucket_elems=100_000, coarsen_k=2)
+    losses, _, _, _, _, th = grid_run(cfg, 2, 2, 2, params, toks, steps=3, **kw)
+    ref = single(cfg, 2, params, toks, steps=3, **kw)
+    for a, b in zip(losses, ref[0]):
+        assert abs(a - b) <= 2e-2 * abs(b), (losses, ref[0])
+    for i in range(2):
+        for k in th[i]:
+            assert np.array_equal(th[i][k].view(np.uint32), th[2 + i][k].view(np.uint32)), (i, k)
