@@ -1,17 +1,8 @@
-// Fused causal self-attention on tcgen05 (sm_100a) for the stage forward (SURVEY.md §8(a) A2:
-// "causal MHA"; readings D-7 scale 1/sqrt(d), D-8 causal mask).
-//
-// One CTA tile = 128 queries of one (sample, head); all keys of the tile (kv <= 512) fit in
-// TMEM, so the softmax is exact (no online rescaling):
-//   1. S = Q K^T                     SS-MMA into TMEM columns [0, 512)      (fp32)
-//   2. softmax rows in the epilogue:  e = exp2(alpha log2e S - m), P = bf16(e) written BACK into
-//      TMEM (packed bf16 pairs: keys [0,256) -> columns [0,128), keys [256,512) -> [384,512))
-//   3. O = P V                       TS-MMA (A = P from TMEM, B = V from smem) into [128, 128+NV)
-//   4. O / sum -> bf16 -> o[token][head * d + j]; lse2 = m + log2(sum) per row for the backward.
-// Neither S nor P touches HBM.  Warp roles (320 threads, 1 CTA / SM, persistent over tiles):
-//   warp 0 TMA producer (Q, K, then V blocks through a 2-stage ring), warp 1 MMA issuer,
-//   warps 2..9 epilogue: warp pair (q, half) owns TMEM lane quarter q (32 query rows) and the
-//   key half [256 half, 256 half + 256).
+// Fused causal self-attention on tcgen05 (sm_100a) for the stage forward and backward (SURVEY.md
+// §8(a) A2 / A4: "causal MHA"; readings D-7 scale 1/sqrt(d), D-8 causal mask).
+// Forward: attn_fwd2_kernel (streamed key blocks, online softmax, two query tiles ping-ponged on
+// the tensor core; S and P never leave TMEM).  Backward: attn_bwd_kernel<KA> (dK, dV) and
+// <!KA> (dQ) with P recomputed from S and the forward's log2-domain row normaliser.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include "half.cuh"
@@ -25,14 +16,6 @@
 namespace axonn {
 
 namespace {
-
-constexpr int QT = 128;                 // queries per tile
-constexpr int KB = 64;                  // head-dim block of the S = Q K^T mainloop
-constexpr int ATT_STAGES = 2;
-constexpr int Q_BYTES = QT * KB * 2;    // 16 KB
-constexpr int KH_BYTES = 256 * KB * 2;  // 32 KB (one key half)
-constexpr int ATT_STAGE = Q_BYTES + 2 * KH_BYTES;   // 80 KB: Q + K, or one V block (<= 32 KB)
-constexpr int ATT_THREADS = 64 + 8 * 32;
 
 __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
                                             uint32_t idesc, uint32_t accumulate) {
@@ -83,273 +66,12 @@ __device__ __forceinline__ uint32_t pack_hx2(float lo, float hi) {
   hx2 v = f2hx2(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-// TMEM column holding the packed P pair of key `key` (two keys per 32-bit column)
-__device__ __forceinline__ uint32_t p_col(int key) {
-  return key < 256 ? (uint32_t)(key >> 1) : (uint32_t)(256 + (key >> 1));
-}
-
 // Static "snake" schedule over work-sorted units: unit list ordered heaviest tile first
 // (all (sample, head) of the heaviest causal tile, then the next), dealt to the CTAs
 // boustrophedon (round r forward when r is even, backward when odd) so per-CTA work stays
 // within one unit of the mean even though causal tiles differ 4x in cost.
 __device__ __forceinline__ int snake_unit(int r) {
   return r * (int)gridDim.x + ((r & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
-}
-
-struct AttnParams {
-  int s, heads, d, nv, num_m, total;
-  float c1;               // alpha * log2(e)
-  hx* o;
-  long long ldo;
-  float* lse;
-};
-
-__global__ void __launch_bounds__(ATT_THREADS, 1)
-    attn_fwd_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
-                    const __grid_constant__ CUtensorMap mapV, const AttnParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ATT_STAGES * ATT_STAGE);
-  uint64_t* empty = full + ATT_STAGES;
-  uint64_t* s_full = empty + ATT_STAGES;
-  uint64_t* p_ready = s_full + 1;
-  uint64_t* o_full = p_ready + 1;
-  uint64_t* t_free = o_full + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_free + 1);
-  __shared__ float red[2][2][128];          // [max|sum][half][row]
-  __shared__ uint4 stg_all[8][32 * 4];      // per epilogue warp: 32 rows x 32 bf16
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int nkd = (p.nv + KB - 1) / KB;     // head-dim blocks (dp <= nv, OOB zero-filled)
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&mapQ);
-    tma_prefetch_desc(&mapK);
-    tma_prefetch_desc(&mapV);
-    for (int i = 0; i < ATT_STAGES; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    mbar_init(s_full, 1);
-    mbar_init(o_full, 1);
-    mbar_init(p_ready, 8);
-    mbar_init(t_free, 8);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tmem_holder);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
-
-  if (warp == 0) {
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int rnd = 0;; ++rnd) {
-      const int t = snake_unit(rnd);
-      if (t >= p.total) break;
-      const int nz = p.total / p.num_m;
-      const int z = t % nz, m0 = (p.num_m - 1 - t / nz) * QT;
-      const int z1 = z % p.heads, z2 = z / p.heads;
-      const int kv = min(p.s, m0 + QT);
-      const int nh = kv > 256 ? 2 : 1;
-      for (int kb = 0; kb < nkd; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&full[stage], Q_BYTES + nh * KH_BYTES);
-          uint8_t* sQ = smem + stage * ATT_STAGE;
-          tma_load_4d(sQ, &mapQ, &full[stage], kb * KB, m0, z1, z2);
-          for (int hh = 0; hh < nh; ++hh)
-            tma_load_4d(sQ + Q_BYTES + hh * KH_BYTES, &mapK, &full[stage], kb * KB, 256 * hh, z1, z2);
-        }
-        __syncwarp();
-        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
-      }
-      const int nvb = (kv + 63) / 64;
-      for (int j = 0; j < nvb; ++j) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&full[stage], (p.nv / 64) * 8192);
-          uint8_t* sV = smem + stage * ATT_STAGE;
-          for (int c = 0; c < p.nv / 64; ++c)
-            tma_load_4d(sV + c * 8192, &mapV, &full[stage], 64 * c, 64 * j, z1, z2);
-        }
-        __syncwarp();
-        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
-      }
-    }
-  } else if (warp == 1) {
-    const uint32_t idS = umma_idesc_f16(QT, 256, 0, 0);
-    const uint32_t idO = umma_idesc_f16(QT, p.nv, 0, 1);
-    const uint64_t d0 = umma_desc_sw128(smem_u32(smem), 16, 1024);          // K-major (Q, K)
-    const uint64_t v0 = umma_desc_sw128(smem_u32(smem), 8192, 1024);        // MN-major (V)
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int rnd = 0;; ++rnd, ++it) {
-      const int t = snake_unit(rnd);
-      if (t >= p.total) break;
-      const int nz = p.total / p.num_m;
-      const int m0 = (p.num_m - 1 - t / nz) * QT;
-      const int kv = min(p.s, m0 + QT);
-      const int nh = kv > 256 ? 2 : 1;
-      mbar_wait(t_free, (it & 1) ^ 1);
-      tc_fence_after();
-      for (int kb = 0; kb < nkd; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        const uint64_t ad = d0 + (uint64_t)((stage * ATT_STAGE) >> 4);
-        if (elect_one()) {
-#pragma unroll
-          for (int k = 0; k < KB / 16; ++k)
-            for (int hh = 0; hh < nh; ++hh)
-              mma_f16_ss(tmem + 256 * hh, ad + 2 * k, ad + ((Q_BYTES + hh * KH_BYTES) >> 4) + 2 * k,
-                          idS, (kb > 0 || k > 0) ? 1u : 0u);
-          mma_commit(&empty[stage]);
-        }
-        __syncwarp();
-        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
-      }
-      if (elect_one()) mma_commit(s_full);
-      __syncwarp();
-      mbar_wait(p_ready, it & 1);
-      tc_fence_after();
-      const int nvb = (kv + 63) / 64;
-      for (int j = 0; j < nvb; ++j) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        const uint64_t vd = v0 + (uint64_t)((stage * ATT_STAGE) >> 4);
-        if (elect_one()) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma_f16_ts(tmem + 128, tmem + p_col(64 * j + 16 * k), vd + k * (2048 >> 4), idO,
-                        (j > 0 || k > 0) ? 1u : 0u);
-          mma_commit(&empty[stage]);
-        }
-        __syncwarp();
-        if (++stage == ATT_STAGES) { stage = 0; phase ^= 1; }
-      }
-      if (elect_one()) mma_commit(o_full);
-      __syncwarp();
-    }
-  } else {
-    const int q = warp & 3, half = (warp - 2) >> 2, wi = warp - 2;
-    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const int rl = q * 32 + lane;
-    uint4* stg = stg_all[wi];
-    int it = 0;
-    for (int rnd = 0;; ++rnd, ++it) {
-      const int t = snake_unit(rnd);
-      if (t >= p.total) break;
-      const int nz = p.total / p.num_m;
-      const int z = t % nz, m0 = (p.num_m - 1 - t / nz) * QT;
-      const int z1 = z % p.heads, z2 = z / p.heads;
-      const int kv = min(p.s, m0 + QT);
-      const int kv64 = (kv + 63) / 64 * 64;
-      const int r0 = m0 + q * 32;                                 // first query row of the warp
-      const int c_lo = half * 256;
-      const int c_end = min(kv64, c_lo + 256);                    // P columns to write
-      const int c_val = min(min(kv, c_lo + 256), r0 + 32);        // columns holding scores
-      const int c_full = min(c_val, r0);                          // full chunks below
-      const bool has_diag = r0 >= c_lo && r0 < c_val;
-      mbar_wait(s_full, it & 1);
-      tc_fence_after();
-      uint32_t r[32];
-      // pass 1: row max of the raw scores (alpha > 0)
-      float mx = -3.0e38f;
-      for (int c0 = c_lo; c0 < c_full; c0 += 32) {
-        tmem_ld32(trow + c0, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
-      }
-      if (has_diag) {
-        tmem_ld32(trow + r0, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (i <= lane) mx = fmaxf(mx, __uint_as_float(r[i]));
-      }
-      red[0][half][rl] = mx;
-      nbar(1 + q, 64);
-      const float moff = fmaxf(red[0][0][rl], red[0][1][rl]) * p.c1;
-      // pass 2: e = exp2(c1 S - moff); P = bf16(e) into TMEM (half 1 walks downwards so its
-      // packed columns never overwrite unread scores); zeros above the diagonal up to kv64
-      float s0 = 0.f, s1 = 0.f;
-      const int nch = (c_end - c_lo + 31) / 32;
-      for (int ci = 0; ci < nch; ++ci) {
-        const int c0 = half ? c_lo + 32 * (nch - 1 - ci) : c_lo + 32 * ci;
-        uint32_t pk[16];
-        if (c0 < c_full || (has_diag && c0 == r0)) {
-          tmem_ld32(trow + c0, r);
-          const bool diag = c0 == r0;
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            float e0 = ex2_approx(fmaf(__uint_as_float(r[i]), p.c1, -moff));
-            float e1 = ex2_approx(fmaf(__uint_as_float(r[i + 1]), p.c1, -moff));
-            if (diag) {
-              e0 = i <= lane ? e0 : 0.f;
-              e1 = i + 1 <= lane ? e1 : 0.f;
-            }
-            s0 += e0;
-            s1 += e1;
-            pk[i / 2] = pack_hx2(e0, e1);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = 0u;
-        }
-        tmem_st16(trow + p_col(c0), pk);
-      }
-      red[1][half][rl] = s0 + s1;
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_ready);
-      nbar(1 + q, 64);
-      const float sum = red[1][0][rl] + red[1][1][rl];
-      const float inv = 1.f / sum;
-      const int row = r0 + lane;
-      if (half == 0 && row < p.s) p.lse[(long long)z * p.s + row] = moff + __log2f(sum);
-      // O = P V: this warp drains O columns [half * nv/2, +nv/2), scaled by 1/sum
-      mbar_wait(o_full, it & 1);
-      tc_fence_after();
-      const int ncol = p.nv / 2;
-      hx* obase = p.o + ((long long)z2 * p.s) * p.ldo + (long long)z1 * p.d;
-      for (int cc = 0; cc < ncol; cc += 32) {
-        const int oc = half * ncol + cc;                          // head-dim column
-        tmem_ld32(trow + 128 + oc, r);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint4 u;
-          u.x = pack_hx2(__uint_as_float(r[8 * j + 0]) * inv, __uint_as_float(r[8 * j + 1]) * inv);
-          u.y = pack_hx2(__uint_as_float(r[8 * j + 2]) * inv, __uint_as_float(r[8 * j + 3]) * inv);
-          u.z = pack_hx2(__uint_as_float(r[8 * j + 4]) * inv, __uint_as_float(r[8 * j + 5]) * inv);
-          u.w = pack_hx2(__uint_as_float(r[8 * j + 6]) * inv, __uint_as_float(r[8 * j + 7]) * inv);
-          stg[lane * 4 + (j ^ (lane & 3))] = u;
-        }
-        __syncwarp();
-        // 8 rows x 64 B per instruction: lane -> (row i * 8 + lane / 4, 16-byte chunk lane % 4)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int rr = i * 8 + lane / 4, ch = lane & 3;
-          const int gr = r0 + rr;
-          const int col = oc + ch * 8;
-          if (gr < p.s && col < p.d) {
-            const uint4 v = stg[rr * 4 + (ch ^ (rr & 3))];
-            store8h(obase + (long long)gr * p.ldo + col, v, p.d - col);
-          }
-        }
-        __syncwarp();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(t_free);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
-  }
 }
 
 // ------------------------------------------------------------------ forward, streamed keys
@@ -370,7 +92,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 constexpr int F2_THREADS = 12 * 32;
 // Diagnostic builds only (scripts/attn_exp.sh; never the shipped library): AXONN_ATTN_EXP bit 0
 // skips the softmax math (P = 0), bit 1 skips the MMA instructions (commits only), bit 2 the
-// epilogue's global stores.
+// epilogue's global stores of the forward; backward: bit 3 / 4 / 5 skip the KA / !KA / D
+// launch, bit 6 the P / dS math, bit 7 the MMA instructions.
 #ifndef AXONN_ATTN_EXP
 #define AXONN_ATTN_EXP 0
 #endif
@@ -437,7 +160,10 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  const int nz = p.total / p.nu;
+  // unit t = (z, u): the units of one (sample, head) are consecutive, heaviest (last) first, so
+  // the snake deal runs them on neighbouring CTAs at the same time and the key / value blocks
+  // they share are read from DRAM once (L2 hits for the second); consecutive rounds alternate
+  // each CTA between heavy and light units.
   // key blocks needed by the tile whose queries end (exclusive) at qend
   auto nblk = [&](int qend) { return (min(p.s, qend) + KB - 1) / KB; };
 
@@ -448,7 +174,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     for (int rnd = 0;; ++rnd, ++uc) {
       const int t = snake_unit(rnd);
       if (t >= p.total) break;
-      const int z = t % nz, u = p.nu - 1 - t / nz;
+      const int z = t / p.nu, u = p.nu - 1 - t % p.nu;
       const int z1 = z % p.heads, z2 = z / p.heads;
       const int nB = nblk(256 * u + 256);
       for (int x = 0; x < 2; ++x) {
@@ -513,7 +239,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     for (int rnd = 0;; ++rnd, ++uc) {
       const int t = snake_unit(rnd);
       if (t >= p.total) break;
-      const int u = p.nu - 1 - t / nz;
+      const int u = p.nu - 1 - t % p.nu;
       const int nA = nblk(256 * u + 128), nB = nblk(256 * u + 256);
       // S_A(0), S_B(0)
       mbar_wait(&k_full[ks], kph);
@@ -573,7 +299,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     for (int rnd = 0;; ++rnd, ++uc) {
       const int t = snake_unit(rnd);
       if (t >= p.total) break;
-      const int z = t % nz, u = p.nu - 1 - t / nz;
+      const int z = t / p.nu, u = p.nu - 1 - t % p.nu;
       const int z1 = z % p.heads, z2 = z / p.heads;
       const int qt0 = 256 * u + 128 * x;      // first query of the tile
       const int row = qt0 + q * 32 + lane;    // this thread's query
@@ -892,7 +618,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tc_fence_after();
       const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
       if (elect_one()) {
-        for (int c = 0; c < p.nv / 64; ++c) {
+        for (int c = 0; c < ((AXONN_ATTN_EXP & 128) ? 0 : p.nv / 64); ++c) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t acc = (c > 0 || k > 0) ? 1u : 0u;
@@ -936,7 +662,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           // accumulate over the 64 rows of this block: A = packed P^T / dS (TMEM; columns of
           // the two 32-wide halves at +0 and +32), B = G operand MN-major
 #pragma unroll
-          for (int k = 0; k < GR / 16; ++k) {
+          for (int k = 0; k < ((AXONN_ATTN_EXP & 128) ? 0 : GR / 16); ++k) {
             const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
             const uint32_t pc = 128 * b + (k >> 1) * 32 + (k & 1) * 8;
             if (KA)
@@ -1024,7 +750,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
               Dv = Dr;
               ok = col <= row;
             }
-            const float P = ok ? ex2_approx(fmaf(__uint_as_float(x[i + e]), p.c1, -L)) : 0.f;
+            const float P = (ok && !(AXONN_ATTN_EXP & 64)) ? ex2_approx(fmaf(__uint_as_float(x[i + e]), p.c1, -L)) : 0.f;
             P2[e] = P;
             S2[e] = P * (__uint_as_float(y[i + e]) - Dv) * p.alpha;
           }
@@ -1205,7 +931,7 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   const int nv = (dp + 63) / 64 * 64;
   if (nv > 256) return -1;
   const long long ntok = (long long)b * s;
-  {
+  if (!(AXONN_ATTN_EXP & 32)) {
     const long long nthreads = (ntok * heads + DITEMS - 1) / DITEMS * 16;
     attn_bwd_d_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(
         static_cast<const hx*>(dO), (long long)heads * dp, dp,
@@ -1237,6 +963,7 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   const int max_smem = 227 * 1024 - 1024 - 256 - 18 * 1024;   // dynamic budget beside static
   p.ld_bulk = s % GRB == 0;
   for (int ka = 1; ka >= 0; --ka) {
+    if ((ka && (AXONN_ATTN_EXP & 8)) || (!ka && (AXONN_ATTN_EXP & 16))) continue;
     const int f_bytes = nv * 128 * 2, g_bytes = nv * GRB * 2 + (ka ? 256 : 0);   // + lse/D slices
     // one row-operand buffer (a second one measured no faster and costs ring depth)
     p.nfb = 1;
