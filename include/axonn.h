@@ -247,6 +247,12 @@ AXONN_API axonn_status axonn_tensor_info(const axonn_ctx* ctx, int idx, char nam
 AXONN_API axonn_status axonn_read_tensor(axonn_ctx* ctx, int which, int idx, float* host_dst);
 AXONN_API axonn_status axonn_write_tensor(axonn_ctx* ctx, int which, int idx, const float* host_src);
 
+/* The activation checkpointing interval ac this context uses (checkpoint_interval resolved;
+ * 1 = off), or -1 for a NULL context.  For checkpoint_interval = -1 it is the paper's rule
+ * (PAPER.md:570-573): the factor of this stage's layer count closest to sqrt(n_layers), ties
+ * to the smaller factor. */
+AXONN_API int axonn_checkpoint_interval(const axonn_ctx* ctx);
+
 /* Statistics of the last batch; see AXONN_STAT_* for the index meaning. */
 enum {
   AXONN_STAT_T_BATCH_MS = 0,      /* run_batch wall time (host)                 */

@@ -75,6 +75,7 @@ def _declare(lib):
         "axonn_calibrate_speed": (I, [I, I, I, I, I, C.POINTER(C.c_double)]),
         "axonn_local_group_create": (I, [I, C.POINTER(C.c_void_p)]),
         "axonn_local_group_free": (None, [P]),
+        "axonn_checkpoint_interval": (I, [P]),
         "axonn_k_gemm": (I, [C.POINTER(GemmArgs), P]),
         "axonn_k_adamw": (I, [I64, P, P, P, P, P, C.POINTER(F), P]),
         "axonn_k_attn_fwd": (I, [P, I64, I, I, I, I, I, F, P, I64, P, P]),

@@ -1026,6 +1026,8 @@ AXONN_API axonn_status axonn_local_group_create(int size, axonn_local_group** ou
 
 AXONN_API void axonn_local_group_free(axonn_local_group* g) { delete g; }
 
+AXONN_API int axonn_checkpoint_interval(const axonn_ctx* c) { return c ? c->ac : -1; }
+
 AXONN_API axonn_status axonn_stats(const axonn_ctx* c, double* out, int n) {
   if (!c || !out || n < 0) return AXONN_ERR_INVALID_ARG;
   for (int i = 0; i < n && i < AXONN_STAT_COUNT; ++i) out[i] = c->stats[i];

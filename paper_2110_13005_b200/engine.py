@@ -222,6 +222,10 @@ class AxoNN:
         for i, (name, _, _) in enumerate(self.tensors()):
             self.write(which, i, values[name])
 
+    def checkpoint_interval(self) -> int:
+        """The activation checkpointing interval in use (axonn_checkpoint_interval)."""
+        return self.lib.axonn_checkpoint_interval(self.ctx)
+
     def timer_mark(self, i: int):
         self._check(self.lib.axonn_timer_mark(self.ctx, i), "timer_mark")
 
