@@ -452,6 +452,7 @@ int launch_fwd2(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap&
 // warp (q, half) owns TMEM lanes [32 q, +32) and block columns [32 half, +32).
 struct AttnBwdParams {
   int s, heads, d, nv, nq, nk, total, stages, nbuf;
+  int st_sh;           // log2(stages): stages is 2 or 4, so ring indices are masks and shifts
   int nfb, nab;        // row-operand smem buffers, accumulator TMEM buffers (1 or 2 each)
   int ld_bulk;         // KA: the producer bulk-copies each query block's lse / D slice into the
                        // ring stage (s % 64 == 0); else the epilogue loads them per block
@@ -502,6 +503,11 @@ __device__ __forceinline__ void store_chunk32(uint4* stg, int lane, const uint32
   __syncwarp();
 }
 
+// x mod n and x / n for n in {1, 2} (row-operand / TMEM buffer counts) without an integer
+// division in the per-block loops
+__device__ __forceinline__ int m12(int x, int n) { return n == 2 ? (x & 1) : 0; }
+__device__ __forceinline__ int d12(int x, int n) { return n == 2 ? (x >> 1) : x; }
+
 template <bool KA>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
@@ -549,10 +555,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   // unit t -> (z, tile): KA: key tile n ascending (most query blocks first); else query tile
   // m descending (most key blocks first)
   auto unit = [&](int t, int& z, int& r0, int& i0, int& ni) {
+    // the tiles of one (sample, head) are consecutive, heaviest first: the snake deal runs them
+    // on neighbouring CTAs at the same time, so the streamed blocks they share are read from
+    // DRAM once (L2 hits), and consecutive rounds alternate each CTA between heavy and light
+    // tiles (with per = 4 and 148 CTAs, CTA c gets tile c % 4, then 3 - c % 4, ...)
     const int per = KA ? p.nk : p.nq;
-    const int nz = p.total / per;
-    z = t % nz;
-    const int k = t / nz;                // heaviest tiles first (snake_unit deals them)
+    z = t / per;
+    const int k = t % per;
     if (KA) {
       r0 = k * 128;                     // keys [r0, r0 + 128)
       i0 = r0 / GR;                     // first query block touching the diagonal
@@ -575,8 +584,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       int z, r0, i0, ni;
       unit(t, z, r0, i0, ni);
       const int z1 = z % p.heads, z2 = z / p.heads;
-      const int fb = u % p.nfb;
-      mbar_wait(&f_empty[fb], (uint32_t)(((u / p.nfb) & 1) ^ 1));
+      const int fb = m12(u, p.nfb);
+      mbar_wait(&f_empty[fb], (uint32_t)(((d12(u, p.nfb)) & 1) ^ 1));
       if (elect_one()) {
         uint8_t* f = sF + fb * 2 * f_bytes;
         mbar_arrive_expect_tx(&f_full[fb], 2 * f_bytes);
@@ -612,8 +621,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     int u = 0;
     uint32_t sF0 = 0;                 // current unit's row operands
     auto issue_xy = [&](int gi) {     // X, Y of global block gi into buffer gi % nbuf
-      const int b = gi % p.nbuf, stg = gi % p.stages;
-      mbar_wait(&g_full[stg], (uint32_t)((gi / p.stages) & 1));
+      const int b = m12(gi, p.nbuf), stg = (gi & (p.stages - 1));
+      mbar_wait(&g_full[stg], (uint32_t)(((gi >> p.st_sh)) & 1));
       if (accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);   // last TS-MMA read of b
       tc_fence_after();
       const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
@@ -638,9 +647,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (t >= p.total) break;
       int z, r0, i0, ni;
       unit(t, z, r0, i0, ni);
-      const int fb = u % p.nfb, ab = u % p.nab;
+      const int fb = m12(u, p.nfb), ab = m12(u, p.nab);
       const uint32_t colA = 128 * p.nbuf + ab * acc_w, colB = colA + (KA ? p.nv : 0);
-      mbar_wait(&f_full[fb], (uint32_t)((u / p.nfb) & 1));
+      mbar_wait(&f_full[fb], (uint32_t)((d12(u, p.nfb)) & 1));
       tc_fence_after();
       sF0 = smem_u32(sF + fb * 2 * f_bytes);
       const int g_first = g;
@@ -648,14 +657,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (ni == 1 && elect_one()) mma_commit(&f_empty[fb]);
       __syncwarp();
       for (int it = 0; it < ni; ++it, ++g) {
-        const int b = g % p.nbuf, stg = g % p.stages;
+        const int b = m12(g, p.nbuf), stg = (g & (p.stages - 1));
         if (p.nbuf == 2 && it + 1 < ni) {
           issue_xy(g + 1);
           if (it + 2 == ni && elect_one()) mma_commit(&f_empty[fb]);
           __syncwarp();
         }
-        mbar_wait(&pd_ready[b], (uint32_t)(((g - (p.nbuf == 2 ? 0 : 0)) / p.nbuf) & 1));
-        if (it == 0) mbar_wait(&acc_free[ab], (uint32_t)(((u / p.nab) & 1) ^ 1));
+        mbar_wait(&pd_ready[b], (uint32_t)(d12(g, p.nbuf) & 1));
+        if (it == 0) mbar_wait(&acc_free[ab], (uint32_t)(((d12(u, p.nab)) & 1) ^ 1));
         tc_fence_after();
         const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
         if (elect_one()) {
@@ -706,14 +715,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         Dr = Dz[row];
       }
       for (int it = 0; it < ni; ++it, ++g) {
-        const int b = g % p.nbuf;
+        const int b = m12(g, p.nbuf);
         const int g0 = (i0 + it) * GR;        // first query (KA) or key (!KA) of the block
         const int sb = g & 1;
         const float* Lblk = sL[sb];
         const float* Dblk = sD[sb];
         if (KA && p.ld_bulk) {   // the ring stage holds this block's slices (TMA-visible after g_full)
-          const int stg = g % p.stages;
-          mbar_wait(&g_full[stg], (uint32_t)((g / p.stages) & 1));
+          const int stg = (g & (p.stages - 1));
+          mbar_wait(&g_full[stg], (uint32_t)(((g >> p.st_sh)) & 1));
           Lblk = sLD + stg * 128;
           Dblk = Lblk + 64;
         } else if (KA) {
@@ -725,7 +734,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           }
           nbar(1, 256);
         }
-        mbar_wait(&xy_full[b], (uint32_t)((g / p.nbuf) & 1));
+        mbar_wait(&xy_full[b], (uint32_t)(d12(g, p.nbuf) & 1));
         tc_fence_after();
         const int c0 = 32 * half;             // this warp's 32 block columns
         uint32_t x[32], y[32];
@@ -765,9 +774,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         if (lane == 0) mbar_arrive(&pd_ready[b]);
       }
       // drain the accumulators of the unit: KA -> dV (acc_a), dK (acc_b); else dQ (acc_b)
-      const int ab = u % p.nab;
+      const int ab = m12(u, p.nab);
       const uint32_t colA = 128 * p.nbuf + ab * acc_w, colB = colA + (KA ? p.nv : 0);
-      mbar_wait(&acc_full[ab], (uint32_t)((u / p.nab) & 1));
+      mbar_wait(&acc_full[ab], (uint32_t)((d12(u, p.nab)) & 1));
       tc_fence_after();
       hx* base = p.dq + (long long)z2 * p.s * p.ldq + (long long)z1 * p.d;
       const int r0w = r0 + q * 32;
@@ -797,9 +806,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 // D[z * s + i] = sum_j dO[i, head, j] * O[i, head * d + j]   (fp32); 16 lanes per (token, head),
 // DITEMS (token, head) items per 16-lane group with every load issued before the math
 constexpr int DITEMS = 4;
-// Group g of 16 lanes handles DITEMS = 4 consecutive query rows i..i+3 of one (sample, head)
-// z: g = z * (s / 4) + i / 4.  Lane l holds 8 (or 4) head-dim columns of each row; after the
-// 16-lane reduction lane 0 writes the 4 results as one 16-byte store D[z * s + i .. + 3].
+// Group g of 16 lanes handles DITEMS = 4 items; lane l holds 8 (or 4) head-dim columns of each
+// item's row and a 16-lane reduction finishes each dot product.
+//   TOK (heads % 4 == 0): the items are 4 consecutive heads of one token, g = token * heads / 4
+//     + head / 4 -- a group reads 4 * d contiguous elements of dO and of O, a warp two groups
+//     of the same or the next token: DRAM sees whole rows (the head-major order read 2 d-wide
+//     slices of rows 4 KB apart and ran at 2.3 TB/s);
+//   else: 4 consecutive query rows of one head (z = sample * heads + head), one 16-byte store.
+template <bool TOK>
 __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, int dp,
                                   const hx* __restrict__ O, long long ld_o, int d,
                                   int s, int heads, long long ntok, float* __restrict__ D) {
@@ -807,11 +821,30 @@ __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, in
   const int l = threadIdx.x & 15;
   const long long ngrp = ntok * heads / DITEMS;
   const bool live = grp < ngrp;
-  const long long z = live ? grp / (s / DITEMS) : 0;
-  const int i0 = live ? (int)(grp % (s / DITEMS)) * DITEMS : 0;
-  const long long sample = z / heads;
-  const int hd = (int)(z % heads);
-  const long long tok0 = sample * s + i0;
+  long long tok_u[DITEMS], out_u[DITEMS];
+  int hd_u[DITEMS];
+  if (TOK) {
+    const long long tok = live ? grp / (heads / DITEMS) : 0;
+    const int h0 = live ? (int)(grp % (heads / DITEMS)) * DITEMS : 0;
+    const long long sample = tok / s;
+    const int i = (int)(tok % s);
+#pragma unroll
+    for (int u = 0; u < DITEMS; ++u) {
+      tok_u[u] = tok;
+      hd_u[u] = h0 + u;
+      out_u[u] = (sample * heads + h0 + u) * s + i;
+    }
+  } else {
+    const long long z = live ? grp / (s / DITEMS) : 0;
+    const int i0 = live ? (int)(grp % (s / DITEMS)) * DITEMS : 0;
+    const long long sample = z / heads;
+#pragma unroll
+    for (int u = 0; u < DITEMS; ++u) {
+      tok_u[u] = sample * s + i0 + u;
+      hd_u[u] = (int)(z % heads);
+      out_u[u] = z * s + i0 + u;
+    }
+  }
   float acc[DITEMS];
   if ((d & 7) == 0 && (dp & 7) == 0 && d <= 128) {
     uint4 x[DITEMS], y[DITEMS];
@@ -820,8 +853,8 @@ __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, in
       const int j = 8 * l;
       x[u] = y[u] = make_uint4(0, 0, 0, 0);
       if (live && j < d) {
-        x[u] = __ldg(reinterpret_cast<const uint4*>(dO + (tok0 + u) * ld_do + (long long)hd * dp + j));
-        y[u] = __ldg(reinterpret_cast<const uint4*>(O + (tok0 + u) * ld_o + (long long)hd * d + j));
+        x[u] = __ldg(reinterpret_cast<const uint4*>(dO + tok_u[u] * ld_do + (long long)hd_u[u] * dp + j));
+        y[u] = __ldg(reinterpret_cast<const uint4*>(O + tok_u[u] * ld_o + (long long)hd_u[u] * d + j));
       }
     }
 #pragma unroll
@@ -847,8 +880,8 @@ __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, in
         const int j = 4 * l + 64 * ps;
         x[u][ps] = y[u][ps] = make_uint2(0, 0);
         if (live && j < d) {
-          x[u][ps] = __ldg(reinterpret_cast<const uint2*>(dO + (tok0 + u) * ld_do + (long long)hd * dp + j));
-          y[u][ps] = __ldg(reinterpret_cast<const uint2*>(O + (tok0 + u) * ld_o + (long long)hd * d + j));
+          x[u][ps] = __ldg(reinterpret_cast<const uint2*>(dO + tok_u[u] * ld_do + (long long)hd_u[u] * dp + j));
+          y[u][ps] = __ldg(reinterpret_cast<const uint2*>(O + tok_u[u] * ld_o + (long long)hd_u[u] * d + j));
         }
       }
     }
@@ -872,8 +905,8 @@ __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, in
     for (int u = 0; u < DITEMS; ++u) {
       float a = 0.f;
       if (live) {
-        const hx* xa = dO + (tok0 + u) * ld_do + (long long)hd * dp;
-        const hx* ya = O + (tok0 + u) * ld_o + (long long)hd * d;
+        const hx* xa = dO + tok_u[u] * ld_do + (long long)hd_u[u] * dp;
+        const hx* ya = O + tok_u[u] * ld_o + (long long)hd_u[u] * d;
         for (int j = 2 * l; j < d; j += 32) {
           const float2 xf = hx22f2(*reinterpret_cast<const hx2*>(xa + j));
           const float2 yf = hx22f2(*reinterpret_cast<const hx2*>(ya + j));
@@ -890,8 +923,14 @@ __global__ void attn_bwd_d_kernel(const hx* __restrict__ dO, long long ld_do, in
     for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     acc[u] = a;
   }
-  if (l == 0 && live)
-    *reinterpret_cast<float4*>(D + z * s + i0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  if (l == 0 && live) {
+    if (TOK) {
+#pragma unroll
+      for (int u = 0; u < DITEMS; ++u) D[out_u[u]] = acc[u];
+    } else {
+      *reinterpret_cast<float4*>(D + out_u[0]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    }
+  }
 }
 
 }  // namespace
@@ -933,7 +972,8 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   const long long ntok = (long long)b * s;
   if (!(AXONN_ATTN_EXP & 32)) {
     const long long nthreads = (ntok * heads + DITEMS - 1) / DITEMS * 16;
-    attn_bwd_d_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(
+    auto kd = heads % DITEMS == 0 ? attn_bwd_d_kernel<true> : attn_bwd_d_kernel<false>;
+    kd<<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(
         static_cast<const hx*>(dO), (long long)heads * dp, dp,
         static_cast<const hx*>(o), ldo, d, s, heads, ntok, Dbuf);
   }
@@ -968,14 +1008,10 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
     // one row-operand buffer (a second one measured no faster and costs ring depth)
     p.nfb = 1;
     int stages = 4;
-    while (stages > 2 && p.nfb * 2 * f_bytes + stages * 2 * g_bytes > max_smem) --stages;
-    if (p.nfb * 2 * f_bytes + stages * 2 * g_bytes > max_smem) {
-      p.nfb = 1;
-      stages = 4;
-      while (stages > 2 && 2 * f_bytes + stages * 2 * g_bytes > max_smem) --stages;
-    }
+    if (p.nfb * 2 * f_bytes + stages * 2 * g_bytes > max_smem) stages = 2;   // ring depth 4 or 2
     if (p.nfb * 2 * f_bytes + stages * 2 * g_bytes > max_smem) return -1;
     p.stages = stages;
+    p.st_sh = stages == 4 ? 2 : 1;
     // X / Y double buffer (256 TMEM columns) when the accumulators fit beside it; then
     // double-buffered accumulators (the drain of unit u overlaps unit u+1)
     const int accw = ka ? 2 * nv : nv;
@@ -1002,7 +1038,8 @@ int preload_attn() {
   if (cudaFuncGetAttributes(&a, attn_fwd2_kernel<192, 64>) != cudaSuccess) return -1;
   if (cudaFuncGetAttributes(&a, attn_bwd_kernel<true>) != cudaSuccess) return -1;
   if (cudaFuncGetAttributes(&a, attn_bwd_kernel<false>) != cudaSuccess) return -1;
-  return cudaFuncGetAttributes(&a, attn_bwd_d_kernel) == cudaSuccess ? 0 : -1;
+  if (cudaFuncGetAttributes(&a, attn_bwd_d_kernel<true>) != cudaSuccess) return -1;
+  return cudaFuncGetAttributes(&a, attn_bwd_d_kernel<false>) == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace axonn

@@ -114,7 +114,8 @@ def reference_grads(x, dout, d, alpha):
 
 @pytest.mark.parametrize("b,heads,s,d,dp", [(2, 2, 32, 32, 32), (1, 4, 512, 128, 128),
                                             (2, 3, 200, 64, 64), (1, 2, 512, 188, 192),
-                                            (1, 2, 384, 176, 176), (8, 2, 512, 128, 128)])
+                                            (1, 2, 384, 176, 176), (8, 2, 512, 128, 128),
+                                            (2, 4, 256, 188, 192), (1, 8, 96, 176, 176)])
 def test_attn_bwd_matches_definition(lib, b, heads, s, d, dp):
     import torch
     qkv, x = make_qkv(b, heads, s, d, dp, seed=3 * s + d)
