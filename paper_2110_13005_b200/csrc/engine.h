@@ -250,6 +250,7 @@ struct Ctx {
   }
   int64_t layer_begin(int li) const { return (lhalf[li] & 1) ? loff[li].ln1_g : loff[li].ln2_g; }
   int layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void* din);
+  bool dout_bias_fused = false;       // the next layer_bwd's dout column sum is already done
   void wg_fork();                       // s_wg waits for everything enqueued on s_comp so far
   void wg_note(const void* buf);        // s_wg reads buf (recorded after its last enqueued read)
   void wg_guard(const void* buf);       // s_comp waits before overwriting buf

@@ -87,6 +87,12 @@ int ln_fwd(const void* x, int rows, int h, const void* g, const void* b, void* y
 int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int h,
            const void* g, const void* dres, void* dx, cudaStream_t st);
 int colsum_chunks(int rows);
+// LayerNorm backward (as ln_bwd) with d gamma (+)= sum_r du xhat, d beta (+)= sum_r du and, if
+// out_s, out_s (+)= sum_r bf16(dx) fused; workspace >= 3 * ln_bwd_cs_parts(rows) * h floats
+int ln_bwd_cs(const void* du, const void* x, const float* mean, const float* rstd, int rows, int h,
+              const void* g, const void* dres, void* dx, float* out_g, float* out_b, float* out_s,
+              int accumulate, float* workspace, cudaStream_t st);
+int ln_bwd_cs_parts(int rows);
 int colsum(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int n,
            float* workspace, float* out_b, float* out_g, int accumulate, cudaStream_t st);
 int softmax_fwd(const float* S, long long nrows, int s, void* P, cudaStream_t st);

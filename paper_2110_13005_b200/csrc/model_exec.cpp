@@ -222,8 +222,14 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   // data-gradient chain on s_comp; wg_guard() orders any later overwrite of a buffer
   // s_wg still reads.
   const int hm = lhalf[li];
+  // the column sum of dout (this layer's first bias gradient) was fused into the LayerNorm
+  // backward that produced dout (LN1 of the layer above, or LN_f) -- see ln_bwd_cs
+  const bool dout_summed = dout_bias_fused;
+  dout_bias_fused = false;
+  float* const ws_ln = cs_ws_ln + 1024;   // ln_bwd_cs partials (past colsum2's tickets)
   // gradient w.r.t. x1: from the MLP block, or (stage cut after the attention block) dout
   const void* gx1 = dout;
+  bool gx1_summed = dout_summed;
   if (hm & 2) {
   const void* x1 = (hm & 1) ? st.x1 : x;
   void* dx1o = (hm & 1) ? dx1 : din;   // MLP-only layer: dx1 is the stage's input gradient
@@ -232,7 +238,8 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   gst = wgs();
   TRY(gemm(lin_wgrad(dout, st.act, M, h, 4 * h, g32(o.w_fc2), acc), 2 * dM * 4 * dh * dh));
   gst = s_comp;
-  KCHK(colsum(dout, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_fc2), nullptr, acc, wgs()));
+  if (!dout_summed)
+    KCHK(colsum(dout, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_fc2), nullptr, acc, wgs()));
   wg_note(dout);
   wg_guard(dpre);
   {
@@ -248,11 +255,12 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   KCHK(colsum(dpre, nullptr, nullptr, nullptr, M, 4 * h, cs_ws, g32(o.b_fc1), nullptr, acc, wgs()));
   wg_note(dpre);
   TRY(gemm(lin_dgrad(dpre, p16(o.w_fc1), M, 4 * h, h, du), 2 * dM * 4 * dh * dh));
-  // LN2: dx1 = dout + LN2'(du);  dg2, db2
+  // LN2: dx1 = dout + LN2'(du);  dg2, db2; and dbo = colsum(dx1) when the attention block follows
   wg_guard(dx1o);
-  KCHK(ln_bwd(du, x1, st.mean2, st.rstd2, M, h, p16(o.ln2_g), dout, dx1o, s_comp));
-  KCHK(colsum(du, x1, st.mean2, st.rstd2, M, h, cs_ws_ln, g32(o.ln2_b), g32(o.ln2_g), acc, s_comp));
+  KCHK(ln_bwd_cs(du, x1, st.mean2, st.rstd2, M, h, p16(o.ln2_g), dout, dx1o, g32(o.ln2_g), g32(o.ln2_b),
+                 (hm & 1) ? g32(o.b_o) : nullptr, acc, ws_ln, s_comp));
   gx1 = dx1o;
+  gx1_summed = (hm & 1) != 0;
   }   // MLP block
   if (!(hm & 1)) return 0;
   // proj: dO = dx1 Wo;  dWo += dx1^T o;  dbo += colsum(dx1)
@@ -260,7 +268,8 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   gst = wgs();
   TRY(gemm(lin_wgrad(gx1, st.o, M, h, h, g32(o.w_o), acc), 2 * dM * dh * dh));
   gst = s_comp;
-  KCHK(colsum(gx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, wgs()));
+  if (!gx1_summed)
+    KCHK(colsum(gx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, wgs()));
   wg_note(gx1);
   {
     GemmArgs g = lin_dgrad(gx1, p16(o.w_o), M, h, h, dO);
@@ -330,8 +339,13 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   TRY(gemm(lin_dgrad(dqkv, p16(o.w_qkv), M, 3 * h, h, du), 2 * dM * 3 * dh * dh));
   // LN1: din = dx1 + LN1'(du)   (din is the buffer the layer above read as dout)
   wg_guard(din);
-  KCHK(ln_bwd(du, x, st.mean1, st.rstd1, M, h, p16(o.ln1_g), gx1, din, s_comp));
-  KCHK(colsum(du, x, st.mean1, st.rstd1, M, h, cs_ws_ln, g32(o.ln1_b), g32(o.ln1_g), acc, s_comp));
+  // LN1, with the column sum of din fused when it is the output gradient of the layer below
+  // on this stage (whose first bias gradient is its FC2 bias: only a stage's top layer can
+  // lack its MLP block)
+  float* below = li > 0 ? g32(loff[li - 1].b_fc2) : nullptr;
+  KCHK(ln_bwd_cs(du, x, st.mean1, st.rstd1, M, h, p16(o.ln1_g), gx1, din, g32(o.ln1_g), g32(o.ln1_b), below,
+                 acc, ws_ln, s_comp));
+  dout_bias_fused = below != nullptr;
   return 0;
 }
 
@@ -403,6 +417,7 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
   const int acc = bwd_count > 0 ? 1 : 0;
   const int32_t* tok = dtok + (size_t)mb * b * (s + 1);
   const bool ar_last = ar_overlap && bwd_count == cur_m - 1;   // backwards run in ascending mb
+  dout_bias_fused = false;   // a received output gradient has no fused column sum
   void* cur = dh0;
   void* nxt = dh1;
   if (last) {
@@ -412,8 +427,12 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
     TRY(gemm(lin_wgrad(logits, sl.hf, M, V, h, g32(head_w), acc), 2.0 * M * V * h));
     gst = s_comp;
     TRY(gemm(lin_dgrad(logits, p16(head_w), M, V, h, du), 2.0 * M * V * h));
-    KCHK(ln_bwd(du, xL, sl.meanf, sl.rstdf, M, h, p16(lnf_g), nullptr, cur, s_comp));
-    KCHK(colsum(du, xL, sl.meanf, sl.rstdf, M, h, cs_ws_ln, g32(lnf_b), g32(lnf_g), acc, s_comp));
+    // LN_f, with the column sum of its output gradient (the top layer's first bias gradient)
+    float* top = nullptr;
+    if (nl > 0) top = (lhalf[nl - 1] & 2) ? g32(loff[nl - 1].b_fc2) : g32(loff[nl - 1].b_o);
+    KCHK(ln_bwd_cs(du, xL, sl.meanf, sl.rstdf, M, h, p16(lnf_g), nullptr, cur, g32(lnf_g), g32(lnf_b), top,
+                   acc, cs_ws_ln + 1024, s_comp));
+    dout_bias_fused = top != nullptr;
     if (ar_last) TRY(ar_ready(lnf_g));
   } else {
     cur = const_cast<void*>(dout);
