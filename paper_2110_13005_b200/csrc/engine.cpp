@@ -1054,9 +1054,10 @@ int Ctx::dp_wait(cudaStream_t st, int base, uint32_t value) {
           return fail(AXONN_ERR_TIMEOUT, "fused column reduction: peer flag never arrived");
         std::this_thread::yield();
       }
-    } else if (int rc = wait_flag(this, st, dp_flags + base + j, value, true)) {
-      return rc;
     }
+    // the stream wait (production; after the host spin of the loopback it is satisfied at once)
+    // orders the stream's later reads of the peer's buffer after the peer's writes
+    if (int rc = wait_flag(this, st, dp_flags + base + j, value, true)) return rc;
   }
   return 0;
 }
@@ -1201,6 +1202,13 @@ static int run_pipeline(Ctx* c, int m) {
     Slot& sl = slot_of(mb);
     sl.mb = mb;
     if (!c->first && ev_act[mb]) cudaStreamWaitEvent(c->s_comp, ev_act[mb], 0);
+    // loopback: the host has seen the flag; the same stream wait as production (satisfied at
+    // once, so it cannot block a shared hardware queue) orders this stream's reads of the slot
+    // after the copy for the GPU's memory model (generic loads must not hit stale L1 lines)
+    if (!c->first && c->flags_host) {
+      const int r = wait_flag(c, c->s_comp, c->flags + mb % L, seq(mb));
+      if (r) return r;
+    }
     // a slot's gradient-out buffer is reused only after its previous send finished
     if (!c->first && mb >= L && ev_sent_grad[mb - L]) cudaStreamWaitEvent(c->s_comp, ev_sent_grad[mb - L], 0);
     if (!c->last && mb >= L && ev_sent_act[mb - L]) cudaStreamWaitEvent(c->s_comp, ev_sent_act[mb - L], 0);
@@ -1218,6 +1226,10 @@ static int run_pipeline(Ctx* c, int m) {
   auto backward_of = [&](int mb) -> int {
     Slot& sl = slot_of(mb);
     if (ev_grad[mb]) cudaStreamWaitEvent(c->s_comp, ev_grad[mb], 0);
+    if (c->flags_host) {   // see forward_of
+      const int r0 = wait_flag(c, c->s_comp, c->flags + L + mb % L, seq(mb));
+      if (r0) return r0;
+    }
     int r = c->backward(sl, mb, sl.grecv);
     if (r) return r;
     ev_bdone[mb] = c->ev();
