@@ -708,8 +708,9 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   c->lq = 3LL * c->heads * c->dp;
   c->limit = g_inter == 1 ? 1 : (opt->pipeline_limit > 0 ? opt->pipeline_limit : g_inter);
   {
-    const char* e = getenv("AXONN_P2P");   // must agree on all ranks (same launcher env)
+    const char* e = getenv("AXONN_P2P");   // nccl | copy | (default) direct; same on all ranks
     c->p2p_ipc = !(e && strcmp(e, "nccl") == 0);
+    c->direct_send = c->p2p_ipc && !(e && strcmp(e, "copy") == 0);
   }
   if (opt->checkpoint_interval == -1) {   // factor of N / G_inter closest to sqrt(N)
     const double root = std::sqrt((double)model->n_layers);
@@ -720,6 +721,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   } else if (opt->checkpoint_interval > 1) {
     c->ac = opt->checkpoint_interval;
   }
+  if (c->ac > 1) c->direct_send = false;   // the message is a checkpoint segment boundary
 
   auto bail = [&](int rc) {
     if (c->lg) c->lg->abort();   // the other loopback stages must not wait for this one
@@ -820,6 +822,7 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
     }
   }
   if (c->lg) {
+    if (!c->p2p_ipc) c->direct_send = false;   // AXONN_P2P=nccl: the loopback copies
     c->p2p_ipc = 1;   // the loopback runs the peer-copy link protocol
     if ((rc = local_links(c))) return bail(rc);
   } else {
@@ -1169,6 +1172,12 @@ static int run_pipeline(Ctx* c, int m) {
     const void* out = c->stage_out(sl);
     c->stats[AXONN_STAT_P2P_BYTES] += (double)Mh * 2;
     int r;
+    if (c->direct_send) {   // the forward already stored into stage+1's slot: just the flag
+      r = write_flag(c, c->s_comp, c->peer_flags_next + mb % L, seq(mb));
+      ev_sent_act[mb] = c->ev();
+      cudaEventRecord(ev_sent_act[mb], c->s_comp);
+      return r;
+    }
     if (c->p2p_ipc) {   // copy engine over NVLink into stage+1's slot, then its flag
       r = c->check_cuda(cudaMemcpyAsync(c->peer_act[mb % L], out, Mh * 2, cudaMemcpyDeviceToDevice,
                                         c->s_send_act), "peer copy act");
@@ -1187,6 +1196,12 @@ static int run_pipeline(Ctx* c, int m) {
     cudaStreamWaitEvent(c->s_send_grad, e, 0);
     c->stats[AXONN_STAT_P2P_BYTES] += (double)Mh * 2;
     int r;
+    if (c->direct_send) {   // the backward already stored into stage-1's slot: just the flag
+      r = write_flag(c, c->s_comp, c->peer_flags_prev + L + mb % L, seq(mb));
+      ev_sent_grad[mb] = c->ev();
+      cudaEventRecord(ev_sent_grad[mb], c->s_comp);
+      return r;
+    }
     if (c->p2p_ipc) {
       r = c->check_cuda(cudaMemcpyAsync(c->peer_grad[mb % L], sl.gsend, Mh * 2, cudaMemcpyDeviceToDevice,
                                         c->s_send_grad), "peer copy grad");

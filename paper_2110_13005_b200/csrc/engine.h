@@ -159,6 +159,13 @@ struct Ctx {
   uint32_t dp_progress(int64_t chunk) const {                 // chunk ready in this epoch
     return dp_epoch * (uint32_t)(n_chunks + 1) + (uint32_t)(n_chunks - chunk);
   }
+  // Direct send: with peer-copy links and no activation checkpointing the
+  // kernel that produces a message writes it straight into the neighbour's mapped receive slot
+  // (the top layer's output GEMM through its TMA epilogue; the stage-input gradient's
+  // LayerNorm backward by P2P stores) and a stream memop then stores the sequence number into
+  // the neighbour's flag -- no copy-engine pass.  AXONN_P2P=copy keeps the copy.
+  bool direct_send = false;
+  void* out_redirect = nullptr;       // output of the top layer's last GEMM (during its forward)
   uint32_t msg_base = 0;              // sequence number base: messages of earlier batches
   cudaEvent_t ev_grads_ready = nullptr, ev_opt_done = nullptr, ev_loss = nullptr;
   std::vector<cudaEvent_t> ev_chunk;

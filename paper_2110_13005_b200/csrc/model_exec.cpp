@@ -189,7 +189,9 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
     }
   }
   {
-    GemmArgs g = lin_fwd(st.o, p16(o.w_o), M, h, h, st.x1);
+    // a stage cut after this attention block sends x1: written straight into the peer's slot
+    void* x1_dst = (!(hm & 2) && out_redirect) ? out_redirect : st.x1;
+    GemmArgs g = lin_fwd(st.o, p16(o.w_o), M, h, h, x1_dst);
     g.bias = p16(o.b_o);
     g.resid = x; g.ld_resid = h;
     TRY(gemm(g, 2 * dM * dh * dh));
@@ -205,7 +207,8 @@ int Ctx::layer_fwd(int li, const void* x, LayerStash& st) {
     TRY(gemm(g, 2 * dM * 4 * dh * dh));
   }
   {
-    GemmArgs g = lin_fwd(st.act, p16(o.w_fc2), M, h, 4 * h, st.out);
+    // the stage output: straight into the next stage's receive slot (direct send, §5 / N3)
+    GemmArgs g = lin_fwd(st.act, p16(o.w_fc2), M, h, 4 * h, out_redirect ? out_redirect : st.out);
     g.bias = p16(o.b_fc2);
     g.resid = x1; g.ld_resid = h;
     TRY(gemm(g, 2 * dM * 4 * dh * dh));
@@ -381,7 +384,11 @@ int Ctx::forward_impl(Slot& sl, int mb) {
       TRY(layer_fwd(li, x, st));
       x = st.out;
     } else {
-      TRY(layer_fwd(li, x, sl.L[li]));
+      // direct send: the top layer's output GEMM stores into the next stage's slot
+      out_redirect = (li == nl - 1 && !last && direct_send) ? peer_act[mb % limit] : nullptr;
+      const int rf = layer_fwd(li, x, sl.L[li]);
+      out_redirect = nullptr;
+      TRY(rf);
       x = layer_out(sl.L[li], li);
     }
   }
@@ -453,7 +460,8 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
     } else {
       x = li > 0 ? layer_out(sl.L[li - 1], li - 1) : sl.in;
     }
-    void* din = (li == 0 && !first) ? sl.gsend : nxt;
+    // direct send: the stage-input gradient goes straight into the previous stage's slot
+    void* din = (li == 0 && !first) ? (direct_send ? peer_grad[mb % limit] : sl.gsend) : nxt;
     TRY(layer_bwd(li, x, stash(sl, li), cur, din));
     if (ar_last && !(first && li == 0)) TRY(ar_ready(layer_begin(li)));
     if (li == 0 && !first) {

@@ -259,3 +259,22 @@ def test_loopback_fused_reduction_offload_three_steps():
     for i in range(2):
         for k in th[i]:
             assert np.array_equal(th[i][k].view(np.uint32), th[2 + i][k].view(np.uint32)), (i, k)
+
+
+@pytest.mark.parametrize("mode", ["copy", "direct"])
+def test_loopback_direct_send_equals_copy(monkeypatch, mode):
+    """N3: the producing kernels store each message straight into the neighbour's slot
+    (AXONN_P2P default 'direct': the top layer's output GEMM via its TMA epilogue, the stage-input
+    gradient's LayerNorm backward by plain stores) or the copy engine copies it (copy).  Both
+    equal the single-stage run bit for bit, with a balanced split whose top layer ends after
+    its attention block (the message is x1) and with whole layers."""
+    monkeypatch.setenv("AXONN_P2P", mode)
+    cfg = dict(n_layers=2, hidden=64, heads=2, seq_len=32, vocab=1024)   # balanced: cut after l1's attention
+    params = init_params(cfg["n_layers"], cfg["hidden"], cfg["seq_len"], cfg["vocab"], seed=8)
+    toks = [markov_tokens(8, cfg["seq_len"], cfg["vocab"], seed=90 + k) for k in range(2)]
+    for bal in (False, True):
+        a = pipeline(cfg, 2, 2, params, toks, steps=2, stage_balance=bal)
+        b = single(cfg, 2, params, toks, steps=2)
+        assert a[0] == b[0], (bal, a[0], b[0])
+        bitwise_equal(a[1], b[1], "grad32")
+        bitwise_equal(a[2], b[2], "theta32")

@@ -172,16 +172,19 @@ def test_overlapped_allreduce_is_bitwise_neutral(tmp_path, gi, gd):
 
 @pytest.mark.multigpu(2)
 def test_nccl_and_peer_copy_links_agree_bitwise(tmp_path):
-    """Pipeline messages by NCCL P2P (AXONN_P2P=nccl) or by copy-engine peer copies (default)
-    carry the same bytes: losses, gradients and weights after 2 steps are bitwise equal."""
+    """Pipeline messages by NCCL P2P (AXONN_P2P=nccl), by copy-engine peer copies into the
+    neighbour's slot (copy) or stored there directly by the producing kernels (direct, the
+    default; N3) carry the same bytes: losses, gradients and weights after 2 steps are bitwise
+    equal."""
     res = []
-    for t in ("nccl", "ipc"):
+    for t in ("nccl", "copy", "direct"):
         d = tmp_path / t
         d.mkdir()
         res.append(launch(d, 2, 1, "mini", 2, 16, steps=2, env={"AXONN_P2P": t}))
-    for r0, r1 in zip(*res):
-        for k in r0:
-            assert np.array_equal(r0[k], r1[k]), k
+    for other in res[1:]:
+        for r0, r1 in zip(res[0], other):
+            for k in r0:
+                assert np.array_equal(r0[k], r1[k]), k
 
 
 @pytest.mark.multigpu(2)
