@@ -9,6 +9,8 @@
 #include <cstring>
 #include <cstdint>
 #include <cstdlib>
+#include <string>
+#include <vector>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -462,7 +464,14 @@ struct AttnBwdParams {
   hx* dq;   // dqkv base; dQ at column z1*d, dK at h + z1*d, dV at 2h + z1*d
   long long ldq;
   int h;
+  unsigned long long* trace;   // diagnostic builds (AXONN_ATTN_EXP bit 8): CTA 0 event clocks
 };
+// diagnostic timeline (AXONN_ATTN_EXP & 256 only): event e of block / unit i of CTA 0
+#define BWD_TRACE(e, i)                                                                       \
+  do {                                                                                        \
+    if ((AXONN_ATTN_EXP & 256) && blockIdx.x == 0 && (i) < 512)                                \
+      p.trace[(e) * 512 + (i)] = clock64();                                                   \
+  } while (0)
 
 constexpr int BWD_THREADS = 64 + 8 * 32;
 constexpr int GRB = 64;   // rows of one streamed block (queries for KA, keys for !KA)
@@ -575,6 +584,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   };
 
   if (warp == 0) {
+    int gp_count = 0;
     int stage = 0;
     uint32_t phase = 0;
     int u = 0;
@@ -596,6 +606,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       for (int it = 0; it < ni; ++it) {
         const int g0 = (i0 + it) * GR;
         mbar_wait(&g_empty[stage], phase ^ 1);
+        if (lane == 0) BWD_TRACE(0, gp_count);
+        ++gp_count;
         if (elect_one()) {
           uint8_t* g = sG + stage * 2 * g_bytes;
           const bool bulk = KA && p.ld_bulk;
@@ -623,8 +635,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     auto issue_xy = [&](int gi) {     // X, Y of global block gi into buffer gi % nbuf
       const int b = m12(gi, p.nbuf), stg = (gi & (p.stages - 1));
       mbar_wait(&g_full[stg], (uint32_t)(((gi >> p.st_sh)) & 1));
+      if (lane == 0) BWD_TRACE(1, gi);
       if (accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);   // last TS-MMA read of b
       tc_fence_after();
+      if (lane == 0) BWD_TRACE(2, gi);
       const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
       if (elect_one()) {
         for (int c = 0; c < ((AXONN_ATTN_EXP & 128) ? 0 : p.nv / 64); ++c) {
@@ -664,7 +678,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           __syncwarp();
         }
         mbar_wait(&pd_ready[b], (uint32_t)(d12(g, p.nbuf) & 1));
+        if (lane == 0) BWD_TRACE(3, g);
         if (it == 0) mbar_wait(&acc_free[ab], (uint32_t)(((d12(u, p.nab)) & 1) ^ 1));
+        if (it == 0 && lane == 0) BWD_TRACE(9, u);
         tc_fence_after();
         const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
         if (elect_one()) {
@@ -682,6 +698,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           }
           mma_commit(&g_empty[stg]);
           mma_commit(&acc_done[b]);
+          BWD_TRACE(4, g);
           if (it == ni - 1) mma_commit(&acc_full[ab]);
         }
         __syncwarp();
@@ -735,6 +752,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           nbar(1, 256);
         }
         mbar_wait(&xy_full[b], (uint32_t)(d12(g, p.nbuf) & 1));
+        if (warp == 2 && lane == 0) BWD_TRACE(5, g);
         tc_fence_after();
         const int c0 = 32 * half;             // this warp's 32 block columns
         uint32_t x[32], y[32];
@@ -771,12 +789,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
+        if (warp == 2 && lane == 0) BWD_TRACE(6, g);
         if (lane == 0) mbar_arrive(&pd_ready[b]);
       }
       // drain the accumulators of the unit: KA -> dV (acc_a), dK (acc_b); else dQ (acc_b)
       const int ab = m12(u, p.nab);
       const uint32_t colA = 128 * p.nbuf + ab * acc_w, colB = colA + (KA ? p.nv : 0);
       mbar_wait(&acc_full[ab], (uint32_t)((d12(u, p.nab)) & 1));
+      if (warp == 2 && lane == 0) BWD_TRACE(7, u);
       tc_fence_after();
       hx* base = p.dq + (long long)z2 * p.s * p.ldq + (long long)z1 * p.d;
       const int r0w = r0 + q * 32;
@@ -792,6 +812,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
+      if (warp == 2 && lane == 0) BWD_TRACE(8, u);
       if (lane == 0) mbar_arrive(&acc_free[ab]);
     }
   }
@@ -1000,6 +1021,11 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
   p.dq = static_cast<hx*>(dqkv);
   p.ldq = ldq;
   p.h = heads * d;
+  p.trace = nullptr;
+#if AXONN_ATTN_EXP & 256
+  static unsigned long long* trace_buf = nullptr;
+  if (!trace_buf && cudaMalloc(&trace_buf, 2 * 10 * 512 * sizeof(unsigned long long)) != cudaSuccess) return -10;
+#endif
   const int max_smem = 227 * 1024 - 1024 - 256 - 18 * 1024;   // dynamic budget beside static
   p.ld_bulk = s % GRB == 0;
   for (int ka = 1; ka >= 0; --ka) {
@@ -1025,8 +1051,28 @@ int attn_bwd(const void* qkv, long long lq, const void* dO, const void* o, long 
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return -10;
     const int grid = p.total < nsm ? p.total : nsm;
+#if AXONN_ATTN_EXP & 256
+    p.trace = trace_buf + (ka ? 0 : 10 * 512);
+    cudaMemsetAsync(p.trace, 0, 10 * 512 * sizeof(unsigned long long), st);
+#endif
     kern<<<grid, BWD_THREADS, smem, st>>>(mq, mk, mv, mo, p);
     if (cudaGetLastError() != cudaSuccess) return -11;
+#if AXONN_ATTN_EXP & 256
+    if (const char* tf = getenv("AXONN_TRACE_FILE")) {   // diagnostic builds only
+      std::vector<unsigned long long> h(10 * 512);
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+      if (FILE* f = fopen((std::string(tf) + (ka ? ".ka.csv" : ".q.csv")).c_str(), "w")) {
+        fprintf(f, "i,prod_gempty,mma_gfull,mma_xy_issue,mma_pd,mma_acc_issue,epi_xyfull,epi_pd,drain_start,drain_end,mma_accfree\n");
+        for (int i = 0; i < 512; ++i) {
+          fprintf(f, "%d", i);
+          for (int e = 0; e < 10; ++e) fprintf(f, ",%llu", h[e * 512 + i]);
+          fprintf(f, "\n");
+        }
+        fclose(f);
+      }
+    }
+#endif
   }
   return 0;
 }
