@@ -70,7 +70,7 @@ def oracle(cfgname, batch, seed=7, half="bf16"):
     return model.full_batch_loss_and_grads(p64, model.GPTConfig(**cfg), tok)
 
 
-def check(res, gi, gd, cfgname, batch, half="bf16", fused=None):
+def check(res, gi, gd, cfgname, batch, half="bf16", fused=None, scale=1.0):
     """fused (default: G_data > 1 with the bf16 build, i.e. the fused column reduction of reading
     D-35): each replica's AXONN_T_GRAD is its own un-reduced half gradient and the reduction
     happens inside K9, so the column SUM of those is compared with the oracle; otherwise every
@@ -90,7 +90,7 @@ def check(res, gi, gd, cfgname, batch, half="bf16", fused=None):
             name = key[4:]
             seen.add(name)
             g = (sum(res[jj * gi + i][key].astype(np.float64) for jj in range(gd)) if fused
-                 else r[key].astype(np.float64))
+                 else r[key].astype(np.float64)) / scale   # fp16: the gradients carry S (D-11)
             c, nr, inf = grad_errors(g, g_ref[name])   # tests/parity.py bars
             assert c >= 0.999 and abs(nr) <= 1e-2 and inf <= 5e-2, (rank, name, c, nr, inf)
             # replicas of one stage hold the identical weights (and, unfused, reduced gradient)
@@ -102,7 +102,7 @@ def check(res, gi, gd, cfgname, batch, half="bf16", fused=None):
             for key in r:
                 if key.startswith("g32."):
                     name = key[4:]
-                    tot = sum(res[jj * gi + i][key].astype(np.float64) for jj in range(gd))
+                    tot = sum(res[jj * gi + i][key].astype(np.float64) for jj in range(gd)) / scale
                     c, nr, inf = grad_errors(tot, g_ref[name])
                     assert c >= 0.999 and abs(nr) <= 1e-2 and inf <= 5e-2, (rank, name, c, nr, inf)
     assert seen == set(g_ref), set(g_ref) ^ seen
@@ -139,7 +139,7 @@ def test_two_gpus_fp16(tmp_path, gi, gd):
     """§8(f) N2: the fp16 library (fp16 messages over NCCL P2P, fp16 column all-reduce) with a
     static loss scale 1024 matches the oracle at theta16 = RNE_fp16(theta)."""
     res = launch(tmp_path, gi, gd, "tiny", 2, 8, extra=("--dtype", "fp16", "--loss-scale", "1024"))
-    check(res, gi, gd, "tiny", 8, half="fp16")
+    check(res, gi, gd, "tiny", 8, half="fp16", scale=1024.0)
 
 
 @pytest.mark.multigpu(2)
@@ -151,7 +151,7 @@ def test_two_gpus_fp16_overflow_skip_is_collective(tmp_path, gi, gd):
                  extra=("--dtype", "fp16", "--loss-scale", "1024", "--inf-rank", "1"))
     for r in res:
         assert int(r["skipped"]) == 1 and bool(r["unchanged"])
-    check(res, gi, gd, "tiny", 8, half="fp16")
+    check(res, gi, gd, "tiny", 8, half="fp16", scale=1024.0)
 
 
 @pytest.mark.multigpu(2)
