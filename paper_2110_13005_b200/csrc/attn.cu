@@ -537,11 +537,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* acc_free = bars + 6;             // [2], 8 arrivals
   uint64_t* xy_full = bars + 8;              // [2]
   uint64_t* pd_ready = bars + 10;            // [2], 8 arrivals
-  uint64_t* acc_done = bars + 12;            // [2]
+  // bars + 12, + 13: unused (the accumulation-done handshake is implied by in-order MMA issue)
   uint64_t* g_full = bars + 14;              // [4]
   uint64_t* g_empty = bars + 18;             // [4]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 22);
-  __shared__ float sL[2][GR], sD[2][GR];
+  __shared__ __align__(16) float sL[2][GR], sD[2][GR];
   __shared__ uint4 stg_all[8][32 * 4];
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -628,15 +628,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const uint32_t idAcc = umma_idesc_f16(128, p.nv, 0, 1);
     const uint32_t sG0 = smem_u32(sG);
     int g = 0;                        // global block counter (stage / buffer / parity source)
-    uint32_t accd_ph[2] = {0, 0};     // acc_done uses per buffer
-    int accd_n[2] = {0, 0};
     int u = 0;
     uint32_t sF0 = 0;                 // current unit's row operands
     auto issue_xy = [&](int gi) {     // X, Y of global block gi into buffer gi % nbuf
       const int b = m12(gi, p.nbuf), stg = (gi & (p.stages - 1));
       mbar_wait(&g_full[stg], (uint32_t)(((gi >> p.st_sh)) & 1));
       if (lane == 0) BWD_TRACE(1, gi);
-      if (accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);   // last TS-MMA read of b
+      // no wait for the accumulation of block gi - nbuf, which reads P / dS from buffer b:
+      // it was issued before this (program order) and tcgen05 MMAs of one thread execute in
+      // issue order, so it has read its operands before these MMAs write b; the epilogue
+      // finished with b before that accumulation was issued (pd_ready)
       tc_fence_after();
       if (lane == 0) BWD_TRACE(2, gi);
       const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
@@ -697,13 +698,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                         idAcc, acc);
           }
           mma_commit(&g_empty[stg]);
-          mma_commit(&acc_done[b]);
           BWD_TRACE(4, g);
           if (it == ni - 1) mma_commit(&acc_full[ab]);
         }
         __syncwarp();
-        accd_ph[b] ^= 1;
-        ++accd_n[b];
         if (p.nbuf == 1 && it + 1 < ni) {
           issue_xy(g + 1);
           if (it + 2 == ni && elect_one()) mma_commit(&f_empty[fb]);
@@ -760,26 +758,34 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_ld32_nowait(trow + 128 * b + 64 + c0, y);
         tmem_ld_wait();
         uint32_t pp[16], pd[16];
+        // this warp's 32 columns: per-column (KA: query) or per-row (!KA) lse2 and D, masks only
+        // in blocks that cross the diagonal or s (warp-uniform test)
+        float nL[32], Da[32];
+        if (KA) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(Lblk + c0 + i);
+            const float4 d4 = *reinterpret_cast<const float4*>(Dblk + c0 + i);
+            nL[i] = -l4.x; nL[i + 1] = -l4.y; nL[i + 2] = -l4.z; nL[i + 3] = -l4.w;
+            Da[i] = d4.x; Da[i + 1] = d4.y; Da[i + 2] = d4.z; Da[i + 3] = d4.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) { nL[i] = -Lr; Da[i] = Dr; }
+        }
+        const int cb = g0 + c0;               // first column (query for KA, key for !KA)
+        const int rlo = r0 + q * 32;          // this warp's first row
+        const bool full = KA ? (cb >= rlo + 31 && cb + 31 < p.s) : (cb + 31 <= rlo);
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
           float P2[2], S2[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int col = g0 + c0 + i + e;
-            float L, Dv;
-            bool ok;
-            if (KA) {   // row = key, col = query
-              L = Lblk[c0 + i + e];
-              Dv = Dblk[c0 + i + e];
-              ok = col >= row && col < p.s;
-            } else {    // row = query, col = key
-              L = Lr;
-              Dv = Dr;
-              ok = col <= row;
-            }
-            const float P = (ok && !(AXONN_ATTN_EXP & 64)) ? ex2_approx(fmaf(__uint_as_float(x[i + e]), p.c1, -L)) : 0.f;
+            const int col = cb + i + e;
+            const bool ok = full || (KA ? (col >= row && col < p.s) : (col <= row));
+            const float P = (ok && !(AXONN_ATTN_EXP & 64)) ? ex2_approx(fmaf(__uint_as_float(x[i + e]), p.c1, nL[i + e])) : 0.f;
             P2[e] = P;
-            S2[e] = P * (__uint_as_float(y[i + e]) - Dv) * p.alpha;
+            S2[e] = P * ((__uint_as_float(y[i + e]) - Da[i + e]) * p.alpha);
           }
           pp[i / 2] = pack_hx2(P2[0], P2[1]);
           pd[i / 2] = pack_hx2(S2[0], S2[1]);

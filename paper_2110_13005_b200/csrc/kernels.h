@@ -93,6 +93,9 @@ int ln_bwd_cs(const void* du, const void* x, const float* mean, const float* rst
               const void* g, const void* dres, void* dx, float* out_g, float* out_b, float* out_s,
               int accumulate, float* workspace, cudaStream_t st);
 int ln_bwd_cs_parts(int rows);
+// out (+)= column sums of a bf16 [rows][h] tensor in ln_bwd_cs's summation order
+int colsum_lnc(const void* dy, int rows, int h, float* out, int accumulate, float* workspace,
+               cudaStream_t st);
 int colsum(const void* dy, const void* x, const float* mean, const float* rstd, int rows, int n,
            float* workspace, float* out_b, float* out_g, int accumulate, cudaStream_t st);
 int softmax_fwd(const float* S, long long nrows, int s, void* P, cudaStream_t st);

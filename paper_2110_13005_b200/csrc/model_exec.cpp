@@ -241,8 +241,8 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   gst = wgs();
   TRY(gemm(lin_wgrad(dout, st.act, M, h, 4 * h, g32(o.w_fc2), acc), 2 * dM * 4 * dh * dh));
   gst = s_comp;
-  if (!dout_summed)
-    KCHK(colsum(dout, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_fc2), nullptr, acc, wgs()));
+  if (!dout_summed)   // received output gradient: the fused sum's order (bitwise = G_inter 1)
+    KCHK(colsum_lnc(dout, M, h, g32(o.b_fc2), acc, cs_ws + 1024, wgs()));
   wg_note(dout);
   wg_guard(dpre);
   {
@@ -271,8 +271,8 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   gst = wgs();
   TRY(gemm(lin_wgrad(gx1, st.o, M, h, h, g32(o.w_o), acc), 2 * dM * dh * dh));
   gst = s_comp;
-  if (!gx1_summed)
-    KCHK(colsum(gx1, nullptr, nullptr, nullptr, M, h, cs_ws, g32(o.b_o), nullptr, acc, wgs()));
+  if (!gx1_summed)   // received gradient of x1 (stage cut after this attention block)
+    KCHK(colsum_lnc(gx1, M, h, g32(o.b_o), acc, cs_ws + 1024, wgs()));
   wg_note(gx1);
   {
     GemmArgs g = lin_dgrad(gx1, p16(o.w_o), M, h, h, dO);

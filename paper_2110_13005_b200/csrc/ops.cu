@@ -493,6 +493,47 @@ __global__ void lnc_final_kernel(const float* __restrict__ part, int nb, int h, 
   o[c] = accumulate ? o[c] + acc : acc;
 }
 
+// Column sum of a bf16 [rows][h] tensor in exactly ln_bwd_cs's order (blocks of LNC_ROWS rows,
+// rows in order per column, blocks in ascending order): the bias gradient of a layer whose
+// output gradient arrived from the next stage equals, bit for bit, the fused sum the same
+// layer gets when its output gradient is produced on this stage (pipelined == sequential).
+__global__ void __launch_bounds__(256) colsum_lnc_kernel(const hx* __restrict__ dy, int rows, int h,
+                                                         float* __restrict__ part) {
+  const int r0 = blockIdx.x * LNC_ROWS, r1 = min(rows, r0 + LNC_ROWS);
+  for (int c = threadIdx.x * 8; c < h; c += 256 * 8) {
+    float ss[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss[i] = 0.f;
+    for (int r = r0; r < r1; r += 4) {
+      uint4 rd[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r + u < r1) rd[u] = ldraw(dy + (long long)(r + u) * h + c);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (r + u >= r1) continue;
+        float rf[8];
+        cvt8(rd[u], rf);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss[i] += rf[i];
+      }
+    }
+    float* ps = part + (long long)blockIdx.x * h + c;
+    reinterpret_cast<float4*>(ps)[0] = make_float4(ss[0], ss[1], ss[2], ss[3]);
+    reinterpret_cast<float4*>(ps)[1] = make_float4(ss[4], ss[5], ss[6], ss[7]);
+  }
+}
+
+int colsum_lnc(const void* dy, int rows, int h, float* out, int accumulate, float* workspace,
+               cudaStream_t st) {
+  if (h % 8) return -1;
+  const int nb = (rows + LNC_ROWS - 1) / LNC_ROWS;
+  colsum_lnc_kernel<<<nb, 256, 0, st>>>((const hx*)dy, rows, h, workspace);
+  lnc_final_kernel<<<(unsigned)((h + 255) / 256), 256, 0, st>>>(workspace, nb, h, 1, out, nullptr, nullptr,
+                                                               accumulate);
+  return ok();
+}
+
 int ln_bwd_cs_parts(int rows) { return (rows + LNC_ROWS - 1) / LNC_ROWS; }
 
 int ln_bwd_cs(const void* du, const void* x, const float* mean, const float* rstd, int rows, int h,
@@ -1035,7 +1076,7 @@ int preload_ops() {
                        (const void*)reduce_sum_kernel, (const void*)cast_f32_hx_kernel, (const void*)nonfinite_kernel,
                        (const void*)cast_hx_f32_kernel, (const void*)init_normal_kernel,
                        (const void*)token_check_kernel, (const void*)ln_bwd_cs_kernel,
-                       (const void*)lnc_final_kernel};
+                       (const void*)lnc_final_kernel, (const void*)colsum_lnc_kernel};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
   return 0;
