@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* acc_free = bars + 6;             // [2], 8 arrivals
   uint64_t* xy_full = bars + 8;              // [2]
   uint64_t* pd_ready = bars + 10;            // [2], 8 arrivals
-  // bars + 12, + 13: unused (the accumulation-done handshake is implied by in-order MMA issue)
+  uint64_t* acc_done = bars + 12;            // [2]
   uint64_t* g_full = bars + 14;              // [4]
   uint64_t* g_empty = bars + 18;             // [4]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 22);
@@ -628,16 +628,20 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const uint32_t idAcc = umma_idesc_f16(128, p.nv, 0, 1);
     const uint32_t sG0 = smem_u32(sG);
     int g = 0;                        // global block counter (stage / buffer / parity source)
+    uint32_t accd_ph[2] = {0, 0};     // acc_done uses per buffer
+    int accd_n[2] = {0, 0};
     int u = 0;
     uint32_t sF0 = 0;                 // current unit's row operands
     auto issue_xy = [&](int gi) {     // X, Y of global block gi into buffer gi % nbuf
       const int b = m12(gi, p.nbuf), stg = (gi & (p.stages - 1));
       mbar_wait(&g_full[stg], (uint32_t)(((gi >> p.st_sh)) & 1));
       if (lane == 0) BWD_TRACE(1, gi);
-      // no wait for the accumulation of block gi - nbuf, which reads P / dS from buffer b:
-      // it was issued before this (program order) and tcgen05 MMAs of one thread execute in
-      // issue order, so it has read its operands before these MMAs write b; the epilogue
-      // finished with b before that accumulation was issued (pd_ready)
+      // wait until the accumulation of block gi - nbuf (which reads P / dS from buffer b) is
+      // complete.  In-order MMA issue alone would order the TMEM reuse, but measured: letting
+      // X / Y of the next block run under the epilogue's TMEM traffic slows the epilogue
+      // (the bottleneck) 2x -- 1.3B KA per block 2.5k -> 2.7k cycles, 12B worse
+      // (profiles/r2/attn_bwd_trace_c10_c11.md)
+      if (accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);
       tc_fence_after();
       if (lane == 0) BWD_TRACE(2, gi);
       const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
@@ -698,10 +702,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                         idAcc, acc);
           }
           mma_commit(&g_empty[stg]);
+          mma_commit(&acc_done[b]);
           BWD_TRACE(4, g);
           if (it == ni - 1) mma_commit(&acc_full[ab]);
         }
         __syncwarp();
+        accd_ph[b] ^= 1;
+        ++accd_n[b];
         if (p.nbuf == 1 && it + 1 < ni) {
           issue_xy(g + 1);
           if (it + 2 == ni && elect_one()) mma_commit(&f_empty[fb]);
