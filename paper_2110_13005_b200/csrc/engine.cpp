@@ -1649,7 +1649,9 @@ static axonn_status optimizer_step_impl(axonn_ctx* c) {
       ++c->launches;
     }
   }
-  if (sum_peers) {   // every peer's grad16 has been read: they may overwrite it
+  // every peer's grad16 has been read (or, gradients written by axonn_write_tensor, none was):
+  // the peers may overwrite theirs -- signalled after every step so no cast waits forever
+  if (c->dp_fused && c->dp_epoch > 0) {
     const int rc = c->dp_signal(c->s_opt, c->g_data + c->replica, c->dp_epoch);
     if (rc) return (axonn_status)rc;
   }
