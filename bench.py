@@ -170,8 +170,13 @@ def k1_traffic(cfg):
     one layer's linear-layer GEMMs (profiles/r1/k1_traffic.json, scripts/ncu_traffic.py), beside
     the algorithmic bytes per launch of the same launches (operands read once, outputs written
     once).  null when no capture matches this model width and microbatch."""
-    p = os.path.join(ROOT, "profiles", "r1", "k1_traffic.json")
-    if not os.path.exists(p):
+    p = None
+    for rnd in ("r2", "r1"):   # the latest round's capture
+        cand = os.path.join(ROOT, "profiles", rnd, "k1_traffic.json")
+        if os.path.exists(cand):
+            p = cand
+            break
+    if p is None:
         return {"traffic": None}
     d = json.load(open(p))
     if d.get("hidden") != cfg["hidden"] or d.get("tokens") != cfg["microbatch"] * cfg["seq_len"]:
@@ -191,7 +196,7 @@ def k1_traffic(cfg):
         dram, alg = d["dram_bytes_per_launch_avg"], d.get("algorithmic_bytes_per_launch_avg")
         unit = "bytes per K1 launch (average over the captured launches)"
     return {"traffic": dram, "traffic_algorithmic": alg, "traffic_unit": unit,
-            "traffic_src": "profiles/r1/k1_traffic.json (ncu --set full, 1-layer microbatch)"}
+            "traffic_src": os.path.relpath(p, ROOT) + " (ncu --set full, 1-layer microbatch)"}
 
 
 def _blas_threads() -> int:

@@ -366,7 +366,7 @@ int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, 
 // values the weight-gradient GEMM reads).  The partials [3][blocks][h] are then added in
 // ascending block order by lnc_final_kernel.  Replaces ln_bwd + two column-sum passes (du and
 // x read again, dx read again): 12 instead of 18 bytes per element.
-constexpr int LNC_ROWS = 32;
+constexpr int LNC_ROWS = 64;
 __global__ void __launch_bounds__(256) ln_bwd_cs_kernel(
     const hx* __restrict__ du, const hx* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, int rows, int h, const hx* __restrict__ g,
@@ -473,24 +473,39 @@ __global__ void __launch_bounds__(256) ln_bwd_cs_kernel(
   }
 }
 
-// out_a[c] (+)= sum over blocks k = 0..nb-1 (ascending) of part[a][k][c]; a = 0, 1, (2)
-__global__ void lnc_final_kernel(const float* __restrict__ part, int nb, int h, int na,
-                                 float* __restrict__ out_g, float* __restrict__ out_b,
-                                 float* __restrict__ out_s, int accumulate) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)na * h) return;
-  const int a = (int)(t / h), c = (int)(t % h);
+// out_a[c] (+)= sum over blocks k = 0..nb-1 of part[a][k][c]; a = 0, 1, (2).  Block = 32
+// columns x 8 groups of blocks: group r sums k in [r nb/8, (r+1) nb/8) in ascending order, the 8
+// group sums are added in ascending r (fixed order: bitwise reproducible); coalesced 128-byte
+// reads, 8 x 32 threads in flight per column slab instead of one thread walking all nb.
+__global__ void __launch_bounds__(256) lnc_final_kernel(const float* __restrict__ part, int nb, int h, int na,
+                                                        float* __restrict__ out_g, float* __restrict__ out_b,
+                                                        float* __restrict__ out_s, int accumulate) {
+  __shared__ float sh[8][33];
+  const int cl = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const long long t = (long long)blockIdx.x * 32 + cl;   // column over na * h
+  const bool live = t < (long long)na * h;
+  const int a = live ? (int)(t / h) : 0, c = live ? (int)(t % h) : 0;
   const float* pa = part + (long long)a * nb * h + c;
+  const int k0 = (int)((long long)rg * nb / 8), k1 = (int)((long long)(rg + 1) * nb / 8);
   float acc = 0.f;
-  for (int k0 = 0; k0 < nb; k0 += 8) {   // 8 loads in flight, then the ordered sum
-    float v[8];
+  if (live) {
+    for (int k = k0; k < k1; k += 8) {
+      float v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = k0 + i < nb ? pa[(long long)(k0 + i) * h] : 0.f;
+      for (int i = 0; i < 8; ++i) v[i] = k + i < k1 ? pa[(long long)(k + i) * h] : 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc += v[i];
+      for (int i = 0; i < 8; ++i) acc += v[i];
+    }
   }
-  float* o = a == 0 ? out_g : a == 1 ? out_b : out_s;
-  o[c] = accumulate ? o[c] + acc : acc;
+  sh[rg][cl] = acc;
+  __syncthreads();
+  if (rg == 0 && live) {
+    float s = 0.f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) s += sh[r][cl];
+    float* o = a == 0 ? out_g : a == 1 ? out_b : out_s;
+    o[c] = accumulate ? o[c] + s : s;
+  }
 }
 
 // Column sum of a bf16 [rows][h] tensor in exactly ln_bwd_cs's order (blocks of LNC_ROWS rows,
@@ -529,7 +544,7 @@ int colsum_lnc(const void* dy, int rows, int h, float* out, int accumulate, floa
   if (h % 8) return -1;
   const int nb = (rows + LNC_ROWS - 1) / LNC_ROWS;
   colsum_lnc_kernel<<<nb, 256, 0, st>>>((const hx*)dy, rows, h, workspace);
-  lnc_final_kernel<<<(unsigned)((h + 255) / 256), 256, 0, st>>>(workspace, nb, h, 1, out, nullptr, nullptr,
+  lnc_final_kernel<<<(unsigned)((h + 31) / 32), 256, 0, st>>>(workspace, nb, h, 1, out, nullptr, nullptr,
                                                                accumulate);
   return ok();
 }
@@ -544,7 +559,7 @@ int ln_bwd_cs(const void* du, const void* x, const float* mean, const float* rst
   ln_bwd_cs_kernel<<<nb, 256, 0, st>>>((const hx*)du, (const hx*)x, mean, rstd, rows, h, (const hx*)g,
                                        (const hx*)dres, (hx*)dx, workspace, out_s != nullptr);
   const int na = out_s ? 3 : 2;
-  lnc_final_kernel<<<(unsigned)(((long long)na * h + 255) / 256), 256, 0, st>>>(workspace, nb, h, na, out_g,
+  lnc_final_kernel<<<(unsigned)(((long long)na * h + 31) / 32), 256, 0, st>>>(workspace, nb, h, na, out_g,
                                                                               out_b, out_s, accumulate);
   return ok();
 }
