@@ -46,6 +46,10 @@ struct GemmParams {
   float alpha;
   int num_m, num_n, total;
   int raster_n;       // tile order: 1 = N fastest (see fill_params)
+  // L2 policies of the pair kernel (fill_params): the operand every wave of tiles sweeps again is
+  // loaded evict_last when it fits in L2, the other evict_normal; bf16 outputs are stored
+  // evict_first so a streamed output (the 1.68 GB of LM-head logits) cannot evict it
+  int keep_a, keep_b;
 };
 
 
@@ -500,6 +504,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       PairUnits pu(pair, npairs);
       int t, z, m0, n0, kb0, kb1;
+      const uint64_t pol_a = p.keep_a ? l2_policy_evict_last() : l2_policy_evict_normal();
+      const uint64_t pol_b = p.keep_b ? l2_policy_evict_last() : l2_policy_evict_normal();
       while (pu.next<TBM>(p, BN, t, z, m0, n0, kb0, kb1)) {
         const int z1 = z % p.Z1, z2 = z / p.Z1;
         const int am = m0 + (int)rank * BM;
@@ -512,18 +518,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             uint8_t* sB = sA + A_BYTES;
             const int k0 = kb * BK;
             if (!p.a_mn) {
-              tma_load_4d_pair(sA, &mapA, &full[stage], k0, am, z1, z2);
+              tma_load_4d_pair_hint(sA, &mapA, &full[stage], k0, am, z1, z2, pol_a);
             } else {
 #pragma unroll
               for (int j = 0; j < BM / 64; ++j)
-                tma_load_4d_pair(sA + j * 8192, &mapA, &full[stage], am + 64 * j, k0, z1, z2);
+                tma_load_4d_pair_hint(sA + j * 8192, &mapA, &full[stage], am + 64 * j, k0, z1, z2, pol_a);
             }
             if (!p.b_mn) {
-              tma_load_4d_pair(sB, &mapB, &full[stage], k0, bn, z1, z2);
+              tma_load_4d_pair_hint(sB, &mapB, &full[stage], k0, bn, z1, z2, pol_b);
             } else {
 #pragma unroll
               for (int j = 0; j < BN / 128; ++j)
-                tma_load_4d_pair(sB + j * 8192, &mapB, &full[stage], bn + 64 * j, k0, z1, z2);
+                tma_load_4d_pair_hint(sB + j * 8192, &mapB, &full[stage], bn + 64 * j, k0, z1, z2, pol_b);
             }
           }
           __syncwarp();
@@ -611,6 +617,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const bool has_in = p.epi == EPI_DGELU || (p.epi == EPI_HALF && p.resid != nullptr);
     const int sw = lane & 7;
     uint8_t* my_row0 = box0 + lane * 128;
+    const uint64_t pol_c = l2_policy_evict_first();
     uint32_t ephase = 0;
     int it = 0;
     PairUnits pu(pair, npairs);
@@ -652,7 +659,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
           if (lane == 0) {
             if (p.accumulate) tma_reduce_add_2d(&mapC, box0 + (g & 1) * TE_BOX, cb + 32 * g, row0);
-            else tma_store_2d(&mapC, box0 + (g & 1) * TE_BOX, cb + 32 * g, row0);
+            else tma_store_2d_hint(&mapC, box0 + (g & 1) * TE_BOX, cb + 32 * g, row0, pol_c);
             bulk_commit();
           }
         }
@@ -722,12 +729,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
           if (lane == 0) {
             if (gelu) {
-              tma_store_2d(&mapX, box0, cb + 64 * g, row0);            // pre-activation
+              tma_store_2d_hint(&mapX, box0, cb + 64 * g, row0, pol_c);            // pre-activation
               bulk_commit();
-              tma_store_2d(&mapC, box0 + TE_BOX, cb + 64 * g, row0);   // GeLU
+              tma_store_2d_hint(&mapC, box0 + TE_BOX, cb + 64 * g, row0, pol_c);   // GeLU
               bulk_commit();
             } else {
-              tma_store_2d(&mapC, box0 + (g & 1) * TE_BOX, cb + 64 * g, row0);
+              tma_store_2d_hint(&mapC, box0 + (g & 1) * TE_BOX, cb + 64 * g, row0, pol_c);
               bulk_commit();
             }
           }
@@ -823,6 +830,11 @@ static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
     const double cost_m = (a_bytes > big ? a_bytes * waves : a_bytes) + b_bytes;
     const double cost_n = (b_bytes > big ? b_bytes * waves : b_bytes) + a_bytes;
     p.raster_n = (g.Z == 1 && p.num_n > 1 && cost_n < 0.9 * cost_m) ? 1 : 0;
+    // the operand each later wave re-reads: A when M runs fastest, B when N does; keep it in
+    // L2 if it fits beside everything else (<= 80 MB of the 126 MB L2)
+    const double keep_max = 80e6;
+    p.keep_a = (waves > 1 && !p.raster_n && a_bytes <= keep_max) ? 1 : 0;
+    p.keep_b = (waves > 1 && p.raster_n && b_bytes <= keep_max) ? 1 : 0;
   }
 }
 
