@@ -47,9 +47,12 @@ struct GemmParams {
   int num_m, num_n, total;
   int raster_n;       // tile order: 1 = N fastest (see fill_params)
   // L2 policies of the pair kernel (fill_params): the operand every wave of tiles sweeps again is
-  // loaded evict_last when it fits in L2, the other evict_normal; bf16 outputs are stored
-  // evict_first so a streamed output (the 1.68 GB of LM-head logits) cannot evict it
-  int keep_a, keep_b;
+  // loaded evict_last when it fits in L2, the other evict_normal; a bf16 output larger than
+  // 100 MB (cannot stay in L2 anyway: the 1.68 GB of LM-head logits, FC1 activations, QKV) is
+  // stored evict_first so it does not evict the operands; smaller outputs stay evict_normal,
+  // the next kernel reads them at once (measured: evict_first on every output slowed the
+  // dgrads 1-2 % in the step)
+  int keep_a, keep_b, stream_c;
 };
 
 
@@ -617,7 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const bool has_in = p.epi == EPI_DGELU || (p.epi == EPI_HALF && p.resid != nullptr);
     const int sw = lane & 7;
     uint8_t* my_row0 = box0 + lane * 128;
-    const uint64_t pol_c = l2_policy_evict_first();
+    const uint64_t pol_c = p.stream_c ? l2_policy_evict_first() : l2_policy_evict_normal();
     uint32_t ephase = 0;
     int it = 0;
     PairUnits pu(pair, npairs);
@@ -835,6 +838,7 @@ static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
     const double keep_max = 80e6;
     p.keep_a = (waves > 1 && !p.raster_n && a_bytes <= keep_max) ? 1 : 0;
     p.keep_b = (waves > 1 && p.raster_n && b_bytes <= keep_max) ? 1 : 0;
+    p.stream_c = 2.0 * g.M * g.N * g.Z > 100e6 ? 1 : 0;
   }
 }
 
