@@ -553,8 +553,11 @@ static int plan_memory(Ctx* c) {
   c->dx1 = c->dalloc(Mh * 2);
   // column-sum workspaces (tickets + partials): one for the bias sums on s_wg, one for the
   // LayerNorm parameter sums on s_comp (the two streams run concurrently)
-  const size_t cs_bytes = 4096 + std::max((size_t)2 * colsum_chunks(c->M) * 4 * c->h * 4,
-                                          (size_t)2 * ((c->M + 7) / 8 + 32) * c->h * 4);
+  // 4 KB of colsum2 tickets, then partials: colsum / colsum2, or ln_bwd_cs's [3][blocks][h]
+  // (colsum_lnc needs [blocks][h]); all fp32
+  const size_t cs_bytes = 4096 + std::max({(size_t)2 * colsum_chunks(c->M) * 4 * c->h * 4,
+                                           (size_t)2 * ((c->M + 7) / 8 + 32) * c->h * 4,
+                                           (size_t)3 * ln_bwd_cs_parts(c->M) * c->h * 4});
   c->cs_ws = (float*)c->dalloc(cs_bytes);
   c->cs_ws_ln = (float*)c->dalloc(cs_bytes);
   if (c->cs_ws && c->cs_ws_ln &&

@@ -839,6 +839,7 @@ static void fill_params(GemmParams& p, const GemmArgs& g, int tbm, int bn) {
     p.keep_a = (waves > 1 && !p.raster_n && a_bytes <= keep_max) ? 1 : 0;
     p.keep_b = (waves > 1 && p.raster_n && b_bytes <= keep_max) ? 1 : 0;
     p.stream_c = 2.0 * g.M * g.N * g.Z > 100e6 ? 1 : 0;
+
   }
 }
 

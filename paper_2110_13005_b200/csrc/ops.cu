@@ -366,13 +366,22 @@ int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, 
 // values the weight-gradient GEMM reads).  The partials [3][blocks][h] are then added in
 // ascending block order by lnc_final_kernel.  Replaces ln_bwd + two column-sum passes (du and
 // x read again, dx read again): 12 instead of 18 bytes per element.
-constexpr int LNC_ROWS = 64;
+constexpr int LNC_ROWS = 64;   // most rows per block; lnc_rows() picks the block height
+// rows per block of ln_bwd_cs / colsum_lnc: a power of two in [8, 64] giving >= ~2 blocks per
+// SM (M = 4096 tokens -> 16 rows, 256 blocks; M = 16384 -> 64); both kernels use the same
+// function of M, so their column sums are added in the same order
+static int lnc_rows(int rows) {
+  const int target = rows / (2 * device_sms());
+  int r = 8;
+  while (r < LNC_ROWS && r < target) r *= 2;
+  return r;
+}
 __global__ void __launch_bounds__(256) ln_bwd_cs_kernel(
     const hx* __restrict__ du, const hx* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, int rows, int h, const hx* __restrict__ g,
-    const hx* __restrict__ dres, hx* __restrict__ dx, float* __restrict__ part, int want_s) {
+    const hx* __restrict__ dres, hx* __restrict__ dx, float* __restrict__ part, int want_s, int rpb) {
   __shared__ float sh_s1[LNC_ROWS], sh_s2[LNC_ROWS];
-  const int r0 = blockIdx.x * LNC_ROWS, r1 = min(rows, r0 + LNC_ROWS);
+  const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   for (int r = r0 + warp; r < r1; r += 8) {
     const float mu = mean[r], rs = rstd[r];
@@ -513,8 +522,8 @@ __global__ void __launch_bounds__(256) lnc_final_kernel(const float* __restrict_
 // output gradient arrived from the next stage equals, bit for bit, the fused sum the same
 // layer gets when its output gradient is produced on this stage (pipelined == sequential).
 __global__ void __launch_bounds__(256) colsum_lnc_kernel(const hx* __restrict__ dy, int rows, int h,
-                                                         float* __restrict__ part) {
-  const int r0 = blockIdx.x * LNC_ROWS, r1 = min(rows, r0 + LNC_ROWS);
+                                                         float* __restrict__ part, int rpb) {
+  const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
   for (int c = threadIdx.x * 8; c < h; c += 256 * 8) {
     float ss[8];
 #pragma unroll
@@ -542,22 +551,24 @@ __global__ void __launch_bounds__(256) colsum_lnc_kernel(const hx* __restrict__ 
 int colsum_lnc(const void* dy, int rows, int h, float* out, int accumulate, float* workspace,
                cudaStream_t st) {
   if (h % 8) return -1;
-  const int nb = (rows + LNC_ROWS - 1) / LNC_ROWS;
-  colsum_lnc_kernel<<<nb, 256, 0, st>>>((const hx*)dy, rows, h, workspace);
+  const int rpb = lnc_rows(rows);
+  const int nb = (rows + rpb - 1) / rpb;
+  colsum_lnc_kernel<<<nb, 256, 0, st>>>((const hx*)dy, rows, h, workspace, rpb);
   lnc_final_kernel<<<(unsigned)((h + 31) / 32), 256, 0, st>>>(workspace, nb, h, 1, out, nullptr, nullptr,
                                                                accumulate);
   return ok();
 }
 
-int ln_bwd_cs_parts(int rows) { return (rows + LNC_ROWS - 1) / LNC_ROWS; }
+int ln_bwd_cs_parts(int rows) { return (rows + lnc_rows(rows) - 1) / lnc_rows(rows); }
 
 int ln_bwd_cs(const void* du, const void* x, const float* mean, const float* rstd, int rows, int h,
               const void* g, const void* dres, void* dx, float* out_g, float* out_b, float* out_s,
               int accumulate, float* workspace, cudaStream_t st) {
   if (h % 8) return -1;
-  const int nb = ln_bwd_cs_parts(rows);
+  const int rpb = lnc_rows(rows);
+  const int nb = (rows + rpb - 1) / rpb;
   ln_bwd_cs_kernel<<<nb, 256, 0, st>>>((const hx*)du, (const hx*)x, mean, rstd, rows, h, (const hx*)g,
-                                       (const hx*)dres, (hx*)dx, workspace, out_s != nullptr);
+                                       (const hx*)dres, (hx*)dx, workspace, out_s != nullptr, rpb);
   const int na = out_s ? 3 : 2;
   lnc_final_kernel<<<(unsigned)(((long long)na * h + 31) / 32), 256, 0, st>>>(workspace, nb, h, na, out_g,
                                                                               out_b, out_s, accumulate);
