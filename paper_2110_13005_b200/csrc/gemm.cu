@@ -728,6 +728,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
               *slot = pack8(v);
             }
           }
+          if (p.col_group_in) {
+            // column remap (heads padded d -> dp, D-7): the warp copies the box out of the
+            // staging tile itself, 8 bytes per lane, 16 lanes per row (a TMA store cannot split
+            // the box at a group edge: it takes no negative coordinates and clips to 16 bytes)
+            __syncwarp();
+            const int c0 = cb + 64 * g, h0 = c0 / p.col_group_in, j0 = c0 - h0 * p.col_group_in;
+            const int u = lane & 15, cu = c0 + 4 * u;
+            const int hu = j0 + 4 * u >= p.col_group_in ? 1 : 0;
+            const long long coff = (long long)(h0 + hu) * p.col_group_out + j0 + 4 * u - hu * p.col_group_in;
+            hx* const Cb = reinterpret_cast<hx*>(p.C) + coff;
+#pragma unroll 4
+            for (int i = 0; i < 16; ++i) {
+              const int r = 2 * i + (lane >> 4), grow = row0 + r;
+              const uint2 val = *reinterpret_cast<const uint2*>(
+                  box0 + (g & 1) * TE_BOX + r * 128 + ((((u >> 1) ^ (r & 7)) << 4) | ((u & 1) << 3)));
+              if (cu < p.N && grow < p.M) *reinterpret_cast<uint2*>(Cb + (long long)grow * p.ldc) = val;
+            }
+            __syncwarp();
+            continue;
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -905,10 +925,16 @@ static bool al16h(const void* p, long long ld, int es) {
   return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * es) % 16 == 0;
 }
 
-// The TMA epilogue covers the linear layers: one batch, no column remap, every output
-// column valid, 16-byte aligned bases and row pitches.
+// The TMA epilogue covers the linear layers: one batch, every output column valid, 16-byte
+// aligned bases and row pitches; a column remap (QKV forward, attention-output dgrad at
+// d != dp) only for the plain bf16 epilogue, with groups of a multiple of 4 columns.
 static bool te_eligible(const GemmArgs& g) {
-  if (g.Z != 1 || g.col_group_in != 0 || (g.n_valid > 0 && g.n_valid < g.N)) return false;
+  if (g.Z != 1 || (g.n_valid > 0 && g.n_valid < g.N)) return false;
+  if (g.col_group_in != 0 &&
+      (g.epi != EPI_HALF || g.resid || g.accumulate || g.col_group_in > g.col_group_out ||
+       g.col_group_in < 64 || g.col_group_in % 4 || g.col_group_out % 4 || g.ldc % 4 ||
+       (long long)((g.N + g.col_group_in - 1) / g.col_group_in) * g.col_group_out > g.ldc))
+    return false;
   if (g.epi == EPI_F32) return al16h(g.C, g.ldc, 4);
   if (g.epi != EPI_HALF && g.epi != EPI_BIAS_GELU && g.epi != EPI_DGELU) return false;
   if (!al16h(g.C, g.ldc, 2)) return false;
@@ -938,7 +964,8 @@ static int launch_pair(const GemmArgs& g, cudaStream_t st) {
   memset(&mc, 0, sizeof(mc));
   memset(&mx, 0, sizeof(mx));
   if (TE) {
-    rc = make_map_epi(&mc, g.C, g.N, g.M, g.ldc, g.epi == EPI_F32);
+    // (a remapped output is stored by the epilogue warps; the map is only prefetched)
+    rc = make_map_epi(&mc, g.C, g.col_group_in ? g.ldc : g.N, g.M, g.ldc, g.epi == EPI_F32);
     if (!rc && (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU))
       rc = make_map_epi(&mx, g.aux, g.N, g.M, g.ld_aux, false);
     else if (!rc && g.resid)

@@ -1,0 +1,9 @@
+# 2 GPUs: column-remapped TMA epilogue (QKV forward / dO dgrad at d != dp): kernel + step +
+# loopback tests, 12B 2x1 and 1.3B bench
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/c20_build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_kernels.py -q -k "gemm" > gpurun_out/c20_tests_k.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_step.py tests/test_gpu_loopback.py tests/test_gpu_fullsize.py -q > gpurun_out/c20_tests.log 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29831 bench.py --gpus 2 > gpurun_out/c20_b12_2x1.jsonl 2> gpurun_out/c20_bench.err
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/c20_b13.jsonl 2>> gpurun_out/c20_bench.err
+echo done

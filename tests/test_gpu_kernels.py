@@ -198,6 +198,30 @@ def test_gemm_column_remap_and_nvalid(lib):
     assert np.all(o2[:, 37:] == 0) and rel(o2[:, :37], ref[:, :37]) < 1e-2
 
 
+@pytest.mark.parametrize("M,groups,d,dp,K", [(512, 12, 188, 192, 256), (300, 7, 120, 128, 64),
+                                              (4096, 72, 188, 192, 512)])
+def test_gemm_column_remap_tma_epilogue(lib, M, groups, d, dp, K):
+    """The remapped TMA-store epilogue (3-D map, two clipped stores where a 64-column box
+    crosses a group edge; the QKV forward / attention-output dgrad at d != dp, D-7): same bf16
+    values as the thread-store epilogue (variant 3), padding columns untouched, vs numpy."""
+    t = torch()
+    N = groups * d
+    A = dev_bf16(RNG.standard_normal((M, K)))
+    B = dev_bf16(RNG.standard_normal((N, K)) * 0.05)
+    bias = dev_bf16(RNG.standard_normal(N))
+    outs = []
+    for variant in (0, 3):
+        Cd = t.full((M, groups * dp), 7.0, dtype=t.bfloat16, device="cuda")
+        gemm(lib, M=M, N=N, K=K, A=A, lda=K, B=B, ldb=K, C=Cd, ldc=groups * dp, epi=0,
+             bias=bias, col_group_in=d, col_group_out=dp, variant=variant)
+        outs.append(host(Cd))
+    assert np.array_equal(outs[0], outs[1])
+    out = outs[0].reshape(M, groups, dp)
+    assert np.all(out[:, :, d:] == 7.0)
+    ref = (host(A) @ host(B).T + host(bias)).reshape(M, groups, d)
+    assert rel(out[:, :, :d], ref) < 1e-2
+
+
 @pytest.mark.parametrize("n", [1, 7, 4096, (1 << 20) + 3])
 def test_adamw_bit_exact_vs_oracle(lib, n):
     """K9 vs oracle AdamW (fp32, D-14 op order): bit-identical theta, m, v, theta16."""
