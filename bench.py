@@ -78,17 +78,22 @@ CONFIGS = {
 def memory_ledger(eng, offload):
     """Model-state bytes of rank 0's stage: the paper's
     ledger, 20 phi without offload and 4 phi + 16 bsize with it, beside this build's:
-    theta16 2 phi + fp32 gradient accumulator 4 phi (reading D-20) + half-precision
-    all-reduce buffer 2 phi, plus theta32 / m / v (12 phi) in HBM or a 3-slot device ring of
-    36 bsize (D-34) with 12 phi in pinned host memory.  Activations come on top."""
+    theta16 2 phi + half gradient 2 phi + fp32 gradient accumulators (4 phi, reading D-20; with
+    grad_accum_fp32 = 0 only the vectors and embedding tables, 4 phi32, reading D-38), plus
+    theta32 / m / v (12 phi) in HBM or a 3-slot device ring of 36 bsize (D-34) with 12 phi in
+    pinned host memory.  Activations come on top."""
+    mats = ("w_qkv", "w_o", "w_fc1", "w_fc2", "head_w")
     phi = sum(n for _, _, n in eng.tensors())
+    phi32 = phi if eng.oc.grad_accum_fp32 else \
+        sum(n for name, _, n in eng.tensors() if name.split(".")[-1] not in mats)
     bsize = eng.oc.bucket_elems
-    ours = 8 * phi + (36 * bsize if offload else 12 * phi)
-    return {"phi_stage": phi, "bsize": bsize,
+    ours = 4 * phi + 4 * phi32 + (36 * bsize if offload else 12 * phi)
+    return {"phi_stage": phi, "phi_fp32_accum": phi32, "bsize": bsize,
             "paper_model_state_bytes": 4 * phi + 16 * bsize if offload else 20 * phi,
             "ours_model_state_bytes": ours, "host_pinned_bytes": 12 * phi if offload else 0,
-            "note": "rank 0's stage; ours = 2phi theta16 + 4phi fp32 grad (D-20) + 2phi half grad"
-                    " + (36 bsize ring | 12 phi theta32/m/v); device_mem_gib adds activations"}
+            "note": "rank 0's stage; ours = 2phi theta16 + 2phi half grad + 4phi32 fp32 grad "
+                    "accumulators (D-20 / D-38) + (36 bsize ring | 12 phi theta32/m/v); "
+                    "device_mem_gib adds activations"}
 
 
 def model_flops(b, s, l, h, V):
@@ -340,6 +345,9 @@ def parse_args(argv=None):
                     help="all-reduce chunk = k * bsize elements (PAPER.md:731-737; paper 4)")
     ap.add_argument("--bucket-elems", type=int, default=4_000_000,
                     help="optimizer bucket bsize in elements (PAPER.md:683; paper 4M)")
+    ap.add_argument("--grad-accum-fp32", type=int, default=1,
+                    help="0: the paper's footprint, weight matrices accumulate in the half "
+                         "gradient (reading D-38)")
     args = ap.parse_args(argv)
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.stage_balance is None:
@@ -397,7 +405,7 @@ def main(argv=None):
                 checkpoint_interval=args.checkpoint_interval, dtype=args.dtype,
                 stage_balance="calibrate" if args.stage_balance == 2 else bool(args.stage_balance),
                 pipeline_limit=args.pipeline_limit, coarsen_k=args.coarsen_k,
-                bucket_elems=args.bucket_elems,
+                bucket_elems=args.bucket_elems, grad_accum_fp32=bool(args.grad_accum_fp32),
                 overlap_next_batch=None if args.overlap_next_batch is None else bool(args.overlap_next_batch),
                 loss_scale=args.loss_scale or (1024.0 if args.dtype == "fp16" else 1.0))
     from synth import uniform_tokens
@@ -507,6 +515,7 @@ def main(argv=None):
                        "microbatch": b_m, "microbatches_per_replica": m,
                        "parallelism": f"G_inter{g_inter} x G_data{g_data}",
                        "offload": cfg["offload"], "checkpoint_interval": args.checkpoint_interval,
+                       "grad_accum_fp32": args.grad_accum_fp32,
                        "stage_balance": args.stage_balance, "pipeline_limit": args.pipeline_limit,
                        "stage_blocks": eng.partition() if args.stage_balance else None,
                        "stage_speed_tflops": eng.stage_speed,

@@ -107,6 +107,17 @@ typedef struct {
                                                  replicas hold the same layers).  Ignored when
                                                  stage_balance = 0; non-positive or non-finite ->
                                                  AXONN_ERR_INVALID_ARG. */
+  int grad_accum_fp32;                        /* 1: weight gradients accumulate over the microbatches in
+                                                 fp32 and are rounded to half once per batch (reading
+                                                 D-20; 8 phi device bytes with offload).  0: the paper's
+                                                 footprint: the weight
+                                                 matrices (w_qkv, w_o, w_fc1, w_fc2, head_w) accumulate
+                                                 straight into the half gradient, grad <- RN(grad +
+                                                 RN(microbatch gradient)) (reading D-38); the bias /
+                                                 LayerNorm vectors and the embedding tables keep fp32
+                                                 accumulators (4 phi + 4 (V + s) h on the first stage +
+                                                 16 bsize with offload).  AXONN_T_GRAD32 of a matrix is
+                                                 then AXONN_ERR_INVALID_ARG. */
 } axonn_opt_cfg;
 
 /* The stage split stage_balance = 1 picks (reading D-21b/c), host-only (no device work):

@@ -15,6 +15,15 @@ virtual workers — oracle (test infrastructure only).
   (D-10), replicas summed in ascending j.
 * Weight gradients accumulate over microbatches in execution order, which
   the schedule guarantees is ascending microbatch id (D-19; asserted here).
+* grad_accum="half" (reading D-38, the memory optimisation of PAPER.md:675-680:
+  "only the half precision model parameters (theta16) and gradients
+  (grad theta16) reside on the GPU ... grad theta deleted"): the weight
+  matrices (``HALF_ACCUM``) accumulate in the half format, per microbatch
+  g <- RN(g + RN(dg_mu)); every other tensor accumulates exactly (as with
+  "fp32") and is rounded once by the caller's comparison.  The column SUM
+  then adds the replicas' half gradients.  Pinned by tests/test_oracle_hybrid.py
+  (one microbatch: RN of the exact gradient; bf16-exact increments: equal to
+  the exact sum; the deviation from the exact sum within m half-ulps).
 
 Pinned by tests/test_oracle_hybrid.py: equals ``model.full_batch_loss_and_grads``
 (the plain definition) to fp64 rounding for every valid
@@ -25,6 +34,14 @@ from __future__ import annotations
 import numpy as np
 
 from . import model, schedule
+from .bf16 import round_half
+
+# leaf names of the tensors that accumulate in the half format under grad_accum="half" (D-38)
+HALF_ACCUM = ("w_qkv", "w_o", "w_fc1", "w_fc2", "head_w")
+
+
+def accumulates_in_half(name: str) -> bool:
+    return name.split(".")[-1] in HALF_ACCUM
 
 
 class ConfigError(ValueError):
@@ -50,13 +67,15 @@ def split_stage_params(params: dict, cfg: model.GPTConfig, g_inter: int):
 
 def hybrid_step(params: dict, cfg: model.GPTConfig, tokens, g_inter: int, g_data: int,
                 microbatch: int, loss_scale: float = 1.0, policy: str = "backward_first",
-                seed: int | None = None):
+                seed: int | None = None, grad_accum: str = "fp32", half: str = "bf16"):
     """One data_parallel_step (Alg. 1 l.11-14) on every g^{i,j}.
 
     Returns (loss, grads) where loss = sum over all microbatches of the
     pre-divided loss (= S * batch-mean CE) and grads maps every parameter
     name to its column-summed gradient (what every replica holds after the
     all-reduce)."""
+    if grad_accum not in ("fp32", "half"):
+        raise ConfigError("InvalidArg: grad_accum")
     tokens = np.asarray(tokens)
     B = tokens.shape[0]
     validate(cfg, g_inter, g_data, microbatch, B)
@@ -92,7 +111,10 @@ def hybrid_step(params: dict, cfg: model.GPTConfig, tokens, g_inter: int, g_data
             c, _ = caches.pop((i, mu))
             dinp, g = model.stage_backward(shards[i], cfg, i, g_inter, c, dout)
             for n, v in g.items():
-                grads[i][n] += v
+                if grad_accum == "half" and accumulates_in_half(n):   # D-38
+                    grads[i][n] = round_half(grads[i][n] + round_half(v, half), half).astype(np.float64)
+                else:
+                    grads[i][n] += v
             if i > 0:
                 dacts[(i, mu)] = dinp
 

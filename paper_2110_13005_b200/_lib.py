@@ -42,7 +42,8 @@ class OptCfg(C.Structure):
                 ("offload", C.c_int),
                 ("bucket_elems", C.c_int64), ("coarsen_k", C.c_int), ("pipeline_limit", C.c_int),
                 ("checkpoint_interval", C.c_int), ("overlap_next_batch", C.c_int),
-                ("stage_balance", C.c_int), ("stage_speed", C.POINTER(C.c_double))]
+                ("stage_balance", C.c_int), ("stage_speed", C.POINTER(C.c_double)),
+                ("grad_accum_fp32", C.c_int)]
 
 
 class Dist(C.Structure):

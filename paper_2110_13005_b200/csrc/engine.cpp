@@ -184,6 +184,43 @@ static void build_tensors(Ctx* c) {
     c->head_w = add("head_w", V, h);
   }
   c->nflat = off;
+  // grad_accum_fp32 = 0 (reading D-38): the weight matrices accumulate in grad16; everything
+  // else keeps an fp32 accumulator in a compact grad32
+  c->n32 = 0;
+  for (TensorRec& t : c->tensors) {
+    const std::string leaf = t.name.substr(t.name.find('.') == std::string::npos ? 0 : t.name.find('.') + 1);
+    const bool matrix = leaf == "w_qkv" || leaf == "w_o" || leaf == "w_fc1" || leaf == "w_fc2" || leaf == "head_w";
+    if (!c->half_accum) {
+      t.off32 = t.off;
+    } else if (matrix) {
+      t.off32 = -1;
+    } else {
+      t.off32 = c->n32;
+      c->n32 += (t.numel + 63) / 64 * 64;
+    }
+  }
+  if (!c->half_accum) c->n32 = c->nflat;
+}
+
+// half gradients of [lo, hi) from the fp32 accumulators (D-20): the whole
+// range, or with half_accum (D-38) only the tensors that accumulate in fp32
+int Ctx::cast_grads(int64_t lo, int64_t hi, cudaStream_t st) {
+  if (hi <= lo) return 0;
+  if (!half_accum) {
+    if (cast_f32_hx(grad32 + lo, static_cast<char*>(grad16) + lo * 2, hi - lo, st))
+      return fail(AXONN_ERR_CUDA, "cast");
+    ++launches;
+    return 0;
+  }
+  for (const TensorRec& t : tensors) {
+    if (t.off32 < 0) continue;
+    const int64_t a = std::max(lo, t.off), b = std::min(hi, t.off + t.numel);
+    if (a >= b) continue;
+    if (cast_f32_hx(grad32 + t.off32 + (a - t.off), static_cast<char*>(grad16) + a * 2, b - a, st))
+      return fail(AXONN_ERR_CUDA, "cast");
+    ++launches;
+  }
+  return 0;
 }
 
 // D-22 initialisation on the device (bf16-representable by truncation, D-15).
@@ -574,11 +611,11 @@ static int plan_memory(Ctx* c) {
   c->h_flag = reinterpret_cast<int*>(reinterpret_cast<char*>(c->h_loss) + 32);
   // parameters, gradients, optimizer state
   c->theta16 = c->dalloc(c->nflat * 2);
-  c->grad32 = (float*)c->dalloc(c->nflat * 4);
+  c->grad32 = (float*)c->dalloc(std::max<int64_t>(c->n32, 64) * 4);
   c->grad16 = c->dalloc(c->nflat * 2);
   if (!c->theta16 || !c->grad32 || !c->grad16) return c->fail(AXONN_ERR_OOM, "parameter buffers");
   if (cudaMemsetAsync(c->theta16, 0, c->nflat * 2, c->s_comp) != cudaSuccess ||
-      cudaMemsetAsync(c->grad32, 0, c->nflat * 4, c->s_comp) != cudaSuccess ||
+      cudaMemsetAsync(c->grad32, 0, c->n32 * 4, c->s_comp) != cudaSuccess ||
       cudaMemsetAsync(c->grad16, 0, c->nflat * 2, c->s_comp) != cudaSuccess)
     return c->fail(AXONN_ERR_CUDA, "memset parameters");
   if (c->oc.offload) {
@@ -674,11 +711,13 @@ AXONN_API axonn_status axonn_init(int g_inter, int g_data, int microbatch,
   if (opt->checkpoint_interval < -1 ||   // BadCheckpointInterval: ac must divide N / G_inter
       (opt->checkpoint_interval > 1 && (model->n_layers / g_inter) % opt->checkpoint_interval))
     return AXONN_ERR_INVALID_ARG;
+  if (opt->grad_accum_fp32 != 0 && opt->grad_accum_fp32 != 1) return AXONN_ERR_INVALID_ARG;
 
   axonn_ctx* c = new (std::nothrow) axonn_ctx();
   if (!c) return AXONN_ERR_OOM;
   c->g_inter = g_inter; c->g_data = g_data; c->microbatch = microbatch;
   c->mc = *model; c->oc = *opt;
+  c->half_accum = opt->grad_accum_fp32 == 0;
   if (c->oc.bucket_elems % 4) c->oc.bucket_elems += 4 - c->oc.bucket_elems % 4;   // 16-B aligned buckets
   c->rank = rank; c->world = world; c->device = dist ? dist->device : 0;
   c->lg = lg;
@@ -915,7 +954,8 @@ AXONN_API axonn_status axonn_read_tensor(axonn_ctx* c, int which, int idx, float
       return AXONN_OK;
     }
     case AXONN_T_GRAD32:
-      CU(cudaMemcpy(dst, c->grad32 + t.off, t.numel * 4, cudaMemcpyDeviceToHost));
+      if (t.off32 < 0) return AXONN_ERR_INVALID_ARG;   // grad_accum_fp32 = 0: accumulates in half
+      CU(cudaMemcpy(dst, c->grad32 + t.off32, t.numel * 4, cudaMemcpyDeviceToHost));
       return AXONN_OK;
     case AXONN_T_MASTER:
     case AXONN_T_ADAM_M:
@@ -961,7 +1001,8 @@ AXONN_API axonn_status axonn_write_tensor(axonn_ctx* c, int which, int idx, cons
       }
       break;
     case AXONN_T_GRAD32:
-      rc = c->check_cuda(cudaMemcpy(c->grad32 + t.off, src, t.numel * 4, cudaMemcpyHostToDevice), "write32");
+      if (t.off32 < 0) return AXONN_ERR_INVALID_ARG;
+      rc = c->check_cuda(cudaMemcpy(c->grad32 + t.off32, src, t.numel * 4, cudaMemcpyHostToDevice), "write32");
       break;
     case AXONN_T_MASTER:
     case AXONN_T_ADAM_M:
@@ -1089,9 +1130,7 @@ int Ctx::ar_ready(int64_t lo) {
   // fused column reduction: the peers' K9 of the previous batch read this grad16
   if (!ar_active && dp_fused && dp_epoch > 1 && (rc = dp_wait(s_dp, g_data, dp_epoch - 1))) return rc;
   ar_active = true;
-  if (cast_f32_hx(grad32 + lo, static_cast<char*>(grad16) + lo * 2, ar_hi - lo, s_dp))
-    return fail(AXONN_ERR_CUDA, "cast");
-  ++launches;
+  if ((rc = cast_grads(lo, ar_hi, s_dp))) return rc;
   ar_hi = lo;
   const int64_t ch = (int64_t)oc.coarsen_k * oc.bucket_elems;
   while (ar_next_chunk >= 0 && ar_next_chunk * ch >= lo) {
@@ -1423,8 +1462,7 @@ static axonn_status run_batch_impl(axonn_ctx* c, const int32_t* tokens, bool on_
     // grad16 is still read by a pending optimizer step until it completes
     if (c->opt_pending) CU(cudaStreamWaitEvent(c->s_comp, c->ev_opt_done, 0));
     // half-precision gradients (D-20: fp32 accumulation, half reduction)
-    if (cast_f32_hx(c->grad32, c->grad16, c->nflat, c->s_comp)) return (axonn_status)c->fail(AXONN_ERR_CUDA, "cast");
-    ++c->launches;
+    if ((rc = c->cast_grads(0, c->nflat, c->s_comp))) return (axonn_status)rc;
     CU(cudaEventRecord(c->ev_grads_ready, c->s_comp));
   }
   if (c->g_data == 1 && !c->ar_overlap) CU(cudaEventRecord(c->ph[par][2], c->s_comp));

@@ -24,6 +24,7 @@ constexpr ncclDataType_t kNcclHalf = ncclBfloat16;
 struct TensorRec {
   std::string name;
   int64_t rows, cols, numel, off;   // off: element offset in every flat buffer
+  int64_t off32;                    // offset in grad32; -1: accumulates in grad16 (grad_accum_fp32 = 0)
 };
 
 // Element offsets of one layer's tensors in the flat buffers (D-2 layout).
@@ -83,7 +84,10 @@ struct Ctx {
   // whole layer; a balanced split, stage_balance, may cut a layer after its attention block)
   std::vector<int> lhalf;
   void* theta16 = nullptr;            // bf16 [nflat]
-  float* grad32 = nullptr;            // fp32 accumulation (D-20)
+  float* grad32 = nullptr;            // fp32 accumulation (D-20); with half_accum only the
+                                      // vectors and embedding tables (TensorRec::off32)
+  int64_t n32 = 0;                    // elements of grad32
+  bool half_accum = false;            // grad_accum_fp32 = 0: matrices accumulate in grad16 (D-38)
   void* grad16 = nullptr;             // bf16 all-reduce / optimizer input
   float *master = nullptr, *adam_m = nullptr, *adam_v = nullptr;   // device or pinned host
   float* ring[3][3] = {};             // offload ring: [slot][theta, m, v]
@@ -227,7 +231,22 @@ struct Ctx {
   int fail(int code, const std::string& msg);
 
   void* p16(int64_t off) const { return static_cast<char*>(theta16) + off * 2; }
-  float* g32(int64_t off) const { return grad32 + off; }
+  float* g32(int64_t off) const {   // fp32 accumulator of the tensor starting at off
+    if (!half_accum) return grad32 + off;
+    const TensorRec* t = tensor_at(off);
+    return t && t->off32 >= 0 ? grad32 + t->off32 : nullptr;
+  }
+  const TensorRec* tensor_at(int64_t off) const {   // tensors are in ascending off
+    size_t lo = 0, hi = tensors.size();
+    while (lo < hi) {
+      const size_t mid = (lo + hi) / 2;
+      if (tensors[mid].off < off) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo < tensors.size() && tensors[lo].off == off ? &tensors[lo] : nullptr;
+  }
+  int cast_grads(int64_t lo, int64_t hi, cudaStream_t st);   // grad32 -> grad16 over [lo, hi)
+  GemmArgs wgrad_args(const void* dY, const void* X, int M_, int Nout, int Kin, int64_t off, int acc) const;
 
   // model execution (model_exec.cpp)
   int gemm(GemmArgs g, double flops);

@@ -170,7 +170,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
     const hx* rsp = p.resid ? p.resid + row * p.ld_resid + col0 : nullptr;
     const hx* bp = p.bias ? p.bias + col0 : nullptr;
     if (ncols == 32 && p.col_group_in == 0 && al16(dst) && (!auxp || al16(auxp)) &&
-        (!rsp || al16(rsp)) && (!bp || al16(bp))) {
+        (!rsp || al16(rsp)) && (!bp || al16(bp)) && !p.accumulate) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float* w = v + 8 * j;
@@ -228,6 +228,13 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
       if (i < ncols) v[i] += hx2f(rs[i]);
   }
   hx* C = reinterpret_cast<hx*>(p.C) + z2 * p.c_s2 + z1 * p.c_s1 + row * p.ldc;
+  if (p.accumulate) {   // half weight gradient (D-38): C = RN(C + RN(v)), as the TMA reduce-add
+    hx* dst = C + col0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < ncols) dst[i] = f2hx(hx2f(dst[i]) + hx2f(f2hx(v[i])));
+    return;
+  }
   if (p.col_group_in == 0) {
     hx* dst = C + col0;
     if (ncols == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -756,6 +763,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
               bulk_commit();
               tma_store_2d_hint(&mapC, box0 + TE_BOX, cb + 64 * g, row0, pol_c);   // GeLU
               bulk_commit();
+            } else if (p.accumulate) {   // half weight gradient (D-38): C = RN(C + RN(acc)) in L2
+              tma_reduce_add_2d(&mapC, box0 + (g & 1) * TE_BOX, cb + 64 * g, row0);
+              bulk_commit();
             } else {
               tma_store_2d_hint(&mapC, box0 + (g & 1) * TE_BOX, cb + 64 * g, row0, pol_c);
               bulk_commit();
@@ -937,6 +947,7 @@ static bool te_eligible(const GemmArgs& g) {
     return false;
   if (g.epi == EPI_F32) return al16h(g.C, g.ldc, 4);
   if (g.epi != EPI_HALF && g.epi != EPI_BIAS_GELU && g.epi != EPI_DGELU) return false;
+  if (g.accumulate && (g.epi != EPI_HALF || g.bias || g.resid || g.col_group_in)) return false;
   if (!al16h(g.C, g.ldc, 2)) return false;
   if (g.bias && (reinterpret_cast<uintptr_t>(g.bias) & 15)) return false;
   if ((g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) && !al16h(g.aux, g.ld_aux, 2)) return false;

@@ -136,6 +136,17 @@ static GemmArgs lin_wgrad(const void* dY, const void* X, int M, int Nout, int Ki
   return g;
 }
 
+// dW[Nout, Kin] (+)= dY^T X into the tensor at flat offset off: fp32 (D-20), or with
+// grad_accum_fp32 = 0 straight into the half gradient, RN(dW + RN(dY^T X)) (reading D-38)
+GemmArgs Ctx::wgrad_args(const void* dY, const void* X, int M_, int Nout, int Kin, int64_t off, int acc) const {
+  GemmArgs g = lin_wgrad(dY, X, M_, Nout, Kin, half_accum ? nullptr : g32(off), acc);
+  if (half_accum) {
+    g.C = static_cast<char*>(grad16) + off * 2;
+    g.epi = EPI_HALF;
+  }
+  return g;
+}
+
 #define TRY(x)              \
   do {                      \
     int _rc = (x);          \
@@ -239,7 +250,7 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   // FC2: dpre = (dout W2) * GeLU'(pre);  dW2 += dout^T act;  db2 += colsum(dout)
   wg_fork();
   gst = wgs();
-  TRY(gemm(lin_wgrad(dout, st.act, M, h, 4 * h, g32(o.w_fc2), acc), 2 * dM * 4 * dh * dh));
+  TRY(gemm(wgrad_args(dout, st.act, M, h, 4 * h, o.w_fc2, acc), 2 * dM * 4 * dh * dh));
   gst = s_comp;
   if (!dout_summed)   // received output gradient: the fused sum's order (bitwise = G_inter 1)
     KCHK(colsum_lnc(dout, M, h, g32(o.b_fc2), acc, cs_ws + 1024, wgs()));
@@ -253,7 +264,7 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   // FC1: du = dpre W1;  dW1 += dpre^T w;  db1 += colsum(dpre)
   wg_fork();
   gst = wgs();
-  TRY(gemm(lin_wgrad(dpre, st.w, M, 4 * h, h, g32(o.w_fc1), acc), 2 * dM * 4 * dh * dh));
+  TRY(gemm(wgrad_args(dpre, st.w, M, 4 * h, h, o.w_fc1, acc), 2 * dM * 4 * dh * dh));
   gst = s_comp;
   KCHK(colsum(dpre, nullptr, nullptr, nullptr, M, 4 * h, cs_ws, g32(o.b_fc1), nullptr, acc, wgs()));
   wg_note(dpre);
@@ -269,7 +280,7 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   // proj: dO = dx1 Wo;  dWo += dx1^T o;  dbo += colsum(dx1)
   wg_fork();
   gst = wgs();
-  TRY(gemm(lin_wgrad(gx1, st.o, M, h, h, g32(o.w_o), acc), 2 * dM * dh * dh));
+  TRY(gemm(wgrad_args(gx1, st.o, M, h, h, o.w_o, acc), 2 * dM * dh * dh));
   gst = s_comp;
   if (!gx1_summed)   // received gradient of x1 (stage cut after this attention block)
     KCHK(colsum_lnc(gx1, M, h, g32(o.b_o), acc, cs_ws + 1024, wgs()));
@@ -335,7 +346,7 @@ int Ctx::layer_bwd(int li, const void* x, LayerStash& st, const void* dout, void
   // QKV: du = dqkv Wqkv;  dWqkv += dqkv^T u;  dbqkv += colsum(dqkv)
   wg_fork();
   gst = wgs();
-  TRY(gemm(lin_wgrad(dqkv, st.u, M, 3 * h, h, g32(o.w_qkv), acc), 2 * dM * 3 * dh * dh));
+  TRY(gemm(wgrad_args(dqkv, st.u, M, 3 * h, h, o.w_qkv, acc), 2 * dM * 3 * dh * dh));
   gst = s_comp;
   KCHK(colsum(dqkv, nullptr, nullptr, nullptr, M, 3 * h, cs_ws, g32(o.b_qkv), nullptr, acc, wgs()));
   wg_note(dqkv);
@@ -369,6 +380,14 @@ int Ctx::forward_impl(Slot& sl, int mb) {
   // batch (every microbatch runs the same GEMM shapes; bracketing all of them would
   // perturb the timed step by several percent).
   prof_mb = profiling && mb == cur_m - 1;
+  if (half_accum && bwd_count == 0) {   // the batch's first write of grad16 (D-38)
+    // the previous optimizer step (this rank's K9, and with the fused column reduction the
+    // peers' K9) must be done reading grad16
+    if (opt_pending)
+      if (int rc = check_cuda(cudaStreamWaitEvent(s_comp, ev_opt_done, 0), "half accum wait opt")) return rc;
+    if (dp_fused && dp_epoch > 1)
+      if (int rc = dp_wait(s_comp, g_data, dp_epoch - 1)) return rc;
+  }
   const int b = microbatch;
   const int32_t* tok = dtok + (size_t)mb * b * (s + 1);
   if (first) {
@@ -431,7 +450,7 @@ int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
     const void* xL = stage_out(sl);
     wg_fork();
     gst = wgs();
-    TRY(gemm(lin_wgrad(logits, sl.hf, M, V, h, g32(head_w), acc), 2.0 * M * V * h));
+    TRY(gemm(wgrad_args(logits, sl.hf, M, V, h, head_w, acc), 2.0 * M * V * h));
     gst = s_comp;
     TRY(gemm(lin_dgrad(logits, p16(head_w), M, V, h, du), 2.0 * M * V * h));
     // LN_f, with the column sum of its output gradient (the top layer's first bias gradient)

@@ -82,6 +82,7 @@ class AxoNN:
                  bucket_elems: int = 4_000_000, coarsen_k: int = 4, pipeline_limit: int = 0,
                  overlap_next_batch: bool | None = None, checkpoint_interval: int = 0,
                  stage_balance: bool | str = False, stage_speed=None,
+                 grad_accum_fp32: bool = True,
                  rank: int = 0, world_size: int = 1, device: int = 0, nccl_id: bytes | None = None,
                  dtype: str = "bf16", local_group: "LocalGroup | None" = None):
         # the half format picks the library build (include/axonn.h axonn_dtype)
@@ -93,7 +94,10 @@ class AxoNN:
                               # default: overlap when the optimizer is host-link bound (offload);
                               # in HBM the AdamW kernels only compete with the GEMMs for SMs
                               int(offload if overlap_next_batch is None else overlap_next_batch),
-                              int(bool(stage_balance)), None)
+                              int(bool(stage_balance)), None,
+                              # False: the paper's footprint, weight matrices accumulate in
+                              # the half gradient (reading D-38)
+                              int(bool(grad_accum_fp32)))
         # reading D-21c: stage_balance="calibrate" measures every rank's sustained K1 speed
         # on the stage's FC1 shape and splits by the slowest replica of each stage
         if stage_balance == "calibrate" and stage_speed is None and g_inter > 1:

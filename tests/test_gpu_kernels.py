@@ -222,6 +222,31 @@ def test_gemm_column_remap_tma_epilogue(lib, M, groups, d, dp, K):
     assert rel(out[:, :, :d], ref) < 1e-2
 
 
+@pytest.mark.parametrize("variant", [0, 3])
+@pytest.mark.parametrize("M,N,K", [(512, 768, 1024), (304, 200, 520), (2048, 4096, 512)])
+def test_gemm_wgrad_half_accumulate(lib, M, N, K, variant):
+    """grad_accum_fp32 = 0 (reading D-38): the wgrad GEMM adds its product into a half
+    gradient, C <- RN(C + RN(dY^T X)).  Bit for bit against that definition evaluated on the
+    host from the same kernel's fp32 product (epi 3 into a zeroed fp32 C), for the TMA
+    reduce-add epilogue (variant 0) and the thread-store one (variant 3)."""
+    from oracle.bf16 import round_bf16
+    t = torch()
+    dY = dev_bf16(RNG.standard_normal((K, M)))    # MN-major operands as in the engine's wgrad
+    X = dev_bf16(RNG.standard_normal((K, N)))
+    F = t.zeros((M, N), dtype=t.float32, device="cuda")
+    gemm(lib, M=M, N=N, K=K, A=dY, lda=M, a_mn=1, B=X, ldb=N, b_mn=1, C=F, ldc=N, epi=3,
+         accumulate=0, variant=variant)
+    v = F.cpu().numpy()
+    C0 = RNG.standard_normal((M, N)) * np.sqrt(K)
+    Cd = dev_bf16(C0)
+    c0 = Cd.float().cpu().numpy().astype(np.float64)
+    gemm(lib, M=M, N=N, K=K, A=dY, lda=M, a_mn=1, B=X, ldb=N, b_mn=1, C=Cd, ldc=N, epi=0,
+         accumulate=1, variant=variant)
+    want = round_bf16((c0 + round_bf16(v).astype(np.float64)).astype(np.float32))
+    got = Cd.float().cpu().numpy()
+    assert np.array_equal(got, want), int((got != want).sum())
+
+
 @pytest.mark.parametrize("n", [1, 7, 4096, (1 << 20) + 3])
 def test_adamw_bit_exact_vs_oracle(lib, n):
     """K9 vs oracle AdamW (fp32, D-14 op order): bit-identical theta, m, v, theta16."""

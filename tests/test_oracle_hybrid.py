@@ -86,3 +86,59 @@ def test_validation_errors():
         hybrid.hybrid_step(p, TINY, tok, 1, 3, 1)
     with pytest.raises(hybrid.ConfigError, match="NonDivisibleBatch"):
         hybrid.hybrid_step(p, TINY, tok, 1, 2, 3)
+
+
+@pytest.mark.parametrize("half", ["bf16", "fp16"])
+def test_half_accumulation_one_microbatch_is_rounded_exact_gradient(half):
+    """grad_accum="half" (reading D-38) with one microbatch per replica: every weight matrix is
+    RN(exact full-batch gradient) (a single rounding of the plain definition), every other
+    tensor the exact gradient."""
+    from oracle.bf16 import round_half
+    cfg = TINY
+    p, tok, (loss_ref, g_ref) = reference(cfg, 8)
+    loss, g = hybrid.hybrid_step(p, cfg, tok, 1, 1, 8, grad_accum="half", half=half)
+    assert abs(loss - loss_ref) <= 1e-12 * abs(loss_ref)
+    n_half = 0
+    for k in g_ref:
+        if hybrid.accumulates_in_half(k):
+            n_half += 1
+            assert np.array_equal(g[k], round_half(g_ref[k], half).astype(np.float64)), k
+        else:
+            assert rel(g[k], g_ref[k]) <= 1e-12, k
+    assert n_half == 4 * cfg.n_layers + 1   # w_qkv, w_o, w_fc1, w_fc2 per layer + head_w
+
+
+@pytest.mark.parametrize("gi,gd,bm", [(1, 1, 1), (2, 1, 2), (2, 2, 1)])
+def test_half_accumulation_error_bound(gi, gd, bm):
+    """m microbatches: each step g <- RN(g + RN(dg)) errs by at most u |dg| and u |partial sum|
+    (bf16: 8 significant bits, unit roundoff u = 2^-8), so |g_half - g_exact| <= sum over
+    steps u (|dg| + |partial|) elementwise.  A dropped, doubled or sign-flipped microbatch
+    breaks the bound by the size of a whole microbatch gradient."""
+    cfg = TINY
+    B = 8
+    p, tok, (loss_ref, g_ref) = reference(cfg, B)
+    _, g = hybrid.hybrid_step(p, cfg, tok, gi, gd, bm, grad_accum="half")
+    m = B // (gd * bm)
+    # per-step bound from the exact per-microbatch gradients of a replica's rows
+    for k in g_ref:
+        if not hybrid.accumulates_in_half(k):
+            assert rel(g[k], g_ref[k]) <= 1e-12, k
+            continue
+        bound = np.zeros_like(g_ref[k])
+        for j in range(gd):
+            part = np.zeros_like(g_ref[k])
+            for mu in range(m):
+                rows = tok[(j * m + mu) * bm:(j * m + mu + 1) * bm]
+                _, gm = model.full_batch_loss_and_grads(p, cfg, rows)
+                dg = gm[k] * bm / B          # pre-divided by M_total (D-9)
+                part = part + dg
+                bound += 2.0 ** -8 * (np.abs(dg) + np.abs(part))
+        err = np.abs(g[k] - g_ref[k])
+        assert np.all(err <= bound + 1e-30), (k, float((err - bound).max()))
+        assert not np.array_equal(g[k], g_ref[k]) or m == 1
+
+
+def test_half_accumulation_rejects_unknown_mode():
+    with pytest.raises(hybrid.ConfigError):
+        p, tok, _ = reference(TINY, 8)
+        hybrid.hybrid_step(p, TINY, tok, 1, 1, 8, grad_accum="fp8")
