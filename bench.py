@@ -450,8 +450,9 @@ def main(argv=None):
     fl = model_flops(B, s, cfg["n_layers"], cfg["hidden"], V)
     value = fl / (ms_step / 1e3) / 1e12                       # whole-job model TFLOP/s
 
-    # one extra, instrumented step AFTER the timed region: the K1 / K2 launches of its last
-    # microbatch and its K9 launches are bracketed by CUDA events on their launching streams
+    # one extra, instrumented step AFTER the timed region: the K1 / K2 launches of its middle
+    # microbatch ((m - 1) / 2, clear of the optimizer chunks of the last backward) and its K9
+    # launches are bracketed by CUDA events on their launching streams
     # (roofline and per-shape numbers; the profiled microbatch runs its weight gradients in
     # order on the compute stream so each event pair times one launch)
     overlap = cfg["offload"] if args.overlap_next_batch is None else bool(args.overlap_next_batch)
@@ -547,16 +548,16 @@ def main(argv=None):
                          "achieved": gemm_tf, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
                          "frac": (gemm_tf / peaks["bf16_sus"]) if gemm_tf else None,
                          "peak_src": peaks["src"] + " bf16_tflops_sustained (kernel timed inside a long step)",
-                         # events bracket the K1 launches of the LAST microbatch of every
-                         # timed step (same shapes each microbatch); share scaled by m
-                         "events": "K1 launches of the last microbatch of one instrumented step "
+                         # events bracket the K1 launches of one microbatch (same shapes
+                         # each microbatch); share scaled by m
+                         "events": "K1 launches of microbatch (m-1)/2 of one instrumented step "
                                    "run after the timed region",
                          "gemm_share_of_step": gemm_ms * m / ms_step,
                          **k1_traffic(cfg)},
             "adam": {"achieved_gbs": adam_bytes / (adam_ms / 1e3) / 1e9 if adam_ms else None,
                      "peak_gbs": peaks["hbm"], "bytes_per_param": 28},
             "cpu_baseline": cpu,
-            # per-shape K1 timing (last microbatch of each timed step): ms/launch, TFLOP/s
+            # per-shape K1 timing (microbatch (m-1)/2 of the instrumented step): ms/launch, TFLOP/s
             "gemm_breakdown": {k: {"ms_per_launch": v[0] / max(v[2], 1),
                                    ("tflops" if k != "adamw" else "GB/s"):
                                        v[1] / (v[0] / 1e3) / (1e12 if k != "adamw" else 1e9)

@@ -376,18 +376,11 @@ int Ctx::forward(Slot& sl, int mb) {
 }
 
 int Ctx::forward_impl(Slot& sl, int mb) {
-  // K1 launches are bracketed by CUDA events only for the last microbatch of the
-  // batch (every microbatch runs the same GEMM shapes; bracketing all of them would
-  // perturb the timed step by several percent).
-  prof_mb = profiling && mb == cur_m - 1;
-  if (half_accum && bwd_count == 0) {   // the batch's first write of grad16 (D-38)
-    // the previous optimizer step (this rank's K9, and with the fused column reduction the
-    // peers' K9) must be done reading grad16
-    if (opt_pending)
-      if (int rc = check_cuda(cudaStreamWaitEvent(s_comp, ev_opt_done, 0), "half accum wait opt")) return rc;
-    if (dp_fused && dp_epoch > 1)
-      if (int rc = dp_wait(s_comp, g_data, dp_epoch - 1)) return rc;
-  }
+  // K1 launches are bracketed by CUDA events only for one microbatch of the batch (every
+  // microbatch runs the same GEMM shapes; bracketing all of them would perturb the timed step
+  // by several percent): a middle one, (m - 1) / 2, whose kernels do not share the GPU with
+  // the optimizer chunks that start during the last backward (A8)
+  prof_mb = profiling && mb == (cur_m - 1) / 2;
   const int b = microbatch;
   const int32_t* tok = dtok + (size_t)mb * b * (s + 1);
   if (first) {
@@ -438,7 +431,15 @@ int Ctx::backward(Slot& sl, int mb, const void* dout) {
 }
 
 int Ctx::backward_impl(Slot& sl, int mb, const void* dout) {
-  prof_mb = profiling && mb == cur_m - 1;
+  prof_mb = profiling && mb == (cur_m - 1) / 2;
+  if (half_accum && bwd_count == 0) {   // the batch's first write of grad16 (D-38)
+    // the previous optimizer step (this rank's K9, and with the fused column reduction the
+    // peers' K9) must be done reading grad16
+    if (opt_pending)
+      if (int rc = check_cuda(cudaStreamWaitEvent(s_comp, ev_opt_done, 0), "half accum wait opt")) return rc;
+    if (dp_fused && dp_epoch > 1)
+      if (int rc = dp_wait(s_comp, g_data, dp_epoch - 1)) return rc;
+  }
   const int b = microbatch;
   const int acc = bwd_count > 0 ? 1 : 0;
   const int32_t* tok = dtok + (size_t)mb * b * (s + 1);

@@ -97,6 +97,15 @@ def gemm_sweep(variants=(0, 1, 2), only=None, iters=10):
                 g.epi, g.resid, g.ld_resid = 0, aux.data_ptr(), N    # bias + residual
             res["ours_fused_epilogue_tflops"] = fl / time_cuda(
                 lambda: lib.axonn_k_gemm(C.byref(g), C.c_void_p(st))) / 1e9
+        if kind == "dgrad" and name == "fc2":   # dgrad with GeLU' of the stored pre-activation
+            aux = torch.randn(M, N, device="cuda", dtype=torch.bfloat16)
+            g = _lib.GemmArgs()
+            g.M, g.N, g.K, g.Z, g.Z1 = M, N, K, 1, 1
+            g.A, g.lda, g.B, g.ldb, g.b_mn = A.data_ptr(), K, B.data_ptr(), N, 1
+            g.C, g.ldc, g.alpha = Cb.data_ptr(), N, 1.0
+            g.epi, g.aux, g.ld_aux = 2, aux.data_ptr(), N
+            res["ours_fused_epilogue_tflops"] = fl / time_cuda(
+                lambda: lib.axonn_k_gemm(C.byref(g), C.c_void_p(st))) / 1e9
         out.append(res)
         print(json.dumps(res), flush=True)
         del A, B, Cb
