@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--balance", action="store_true", help="stage_balance (reading D-21b)")
     ap.add_argument("--speed", default=None,
                     help="with --balance: 'calibrate' or comma-separated stage speeds (reading D-21c)")
+    ap.add_argument("--half-accum", action="store_true",
+                    help="grad_accum_fp32 = 0: weight matrices accumulate in the half gradient (D-38)")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     import torch
@@ -49,7 +51,7 @@ def main():
     nid = D.share_unique_id(rank, world, D.nccl_unique_id)
     eng = AxoNN(a.g_inter, a.g_data, a.mb, **cfg, rank=rank, world_size=world, device=local,
                 nccl_id=nid, offload=bool(a.offload), bucket_elems=5000, coarsen_k=2,
-                dtype=a.dtype, loss_scale=a.loss_scale,
+                dtype=a.dtype, loss_scale=a.loss_scale, grad_accum_fp32=not a.half_accum,
                 stage_balance="calibrate" if (a.balance and a.speed == "calibrate") else a.balance,
                 stage_speed=[float(x) for x in a.speed.split(",")]
                 if (a.speed and a.speed != "calibrate") else None)
@@ -64,8 +66,11 @@ def main():
         loss = eng.run_batch(tok)
         out[f"loss{step}"] = np.array(loss)
         if step == 0:
-            for n, v in eng.read_all(T_GRAD32).items():
-                out["g32." + n] = v
+            for idx, n in enumerate(names):
+                try:   # with --half-accum the weight matrices have no fp32 accumulator
+                    out["g32." + n] = eng.read(T_GRAD32, idx)
+                except AxoNNError:
+                    assert a.half_accum, n
             for n, v in eng.read_all(T_GRAD).items():
                 out["g16." + n] = v
         if step == 0 and a.inf_rank >= 0:

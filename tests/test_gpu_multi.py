@@ -251,3 +251,15 @@ def test_fused_column_reduction_vs_nccl(tmp_path, gi, gd):
             if k.startswith("theta."):
                 err = np.linalg.norm(a[k] - b[k]) / max(np.linalg.norm(b[k]), 1e-30)
                 assert err < 1e-2, (k, err)
+
+
+@pytest.mark.multigpu(2)
+@pytest.mark.parametrize("gi,gd", [(2, 1), (1, 2)])
+def test_two_gpus_half_accumulation(tmp_path, gi, gd):
+    """grad_accum_fp32 = 0 (reading D-38) over real peer links: 2 x 1 (direct-send messages)
+    and 1 x 2 (the fused column reduction reading the peer's half gradient over NVLink, whose
+    second batch must wait for the peer's optimizer to finish reading before its first
+    gradient write), 2 steps, every tensor within the parity bars of the exact gradient and
+    the replicas bit-identical."""
+    res = launch(tmp_path, gi, gd, "mini", 2, 16, steps=2, extra=("--half-accum",))
+    check(res, gi, gd, "mini", 16)
