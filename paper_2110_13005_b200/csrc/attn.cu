@@ -452,6 +452,9 @@ int launch_fwd2(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap&
 // (accumulation) descriptor.  X / Y are double-buffered in TMEM when the accumulators leave
 // room, so the epilogue of block i overlaps the MMAs of block i+1.  8 epilogue warps:
 // warp (q, half) owns TMEM lanes [32 q, +32) and block columns [32 half, +32).
+#ifndef AXONN_ATTN_NBUF1_WAIT
+#define AXONN_ATTN_NBUF1_WAIT 0   // diagnostic builds: the round-2 c19 behaviour (wait at nbuf 1 too)
+#endif
 struct AttnBwdParams {
   int s, heads, d, nv, nq, nk, total, stages, nbuf;
   int st_sh;           // log2(stages): stages is 2 or 4, so ring indices are masks and shifts
@@ -640,8 +643,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       // complete.  In-order MMA issue alone would order the TMEM reuse, but measured: letting
       // X / Y of the next block run under the epilogue's TMEM traffic slows the epilogue
       // (the bottleneck) 2x -- 1.3B KA per block 2.5k -> 2.7k cycles, 12B worse
-      // (profiles/r2/attn_bwd_trace_c10_c11.md)
-      if (accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);
+      // (profiles/r2/attn_bwd_trace_c10_c11.md).  With one X / Y buffer (KA at nv 192) X / Y of
+      // block gi is issued after the accumulation of gi - 1, which waited for that block's
+      // epilogue: nothing can overlap the epilogue, and the tensor pipe's in-order execution
+      // already orders the reuse, so the wait would only add its round trip to the chain
+      if ((p.nbuf == 2 || AXONN_ATTN_NBUF1_WAIT) && accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);
       tc_fence_after();
       if (lane == 0) BWD_TRACE(2, gi);
       const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
