@@ -453,7 +453,7 @@ int launch_fwd2(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap&
 // room, so the epilogue of block i overlaps the MMAs of block i+1.  8 epilogue warps:
 // warp (q, half) owns TMEM lanes [32 q, +32) and block columns [32 half, +32).
 #ifndef AXONN_ATTN_NBUF1_WAIT
-#define AXONN_ATTN_NBUF1_WAIT 0   // diagnostic builds: the round-2 c19 behaviour (wait at nbuf 1 too)
+#define AXONN_ATTN_NBUF1_WAIT 0   // diagnostic builds: the round-2 c19 behaviour (always wait)
 #endif
 struct AttnBwdParams {
   int s, heads, d, nv, nq, nk, total, stages, nbuf;
@@ -646,8 +646,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       // (profiles/r2/attn_bwd_trace_c10_c11.md).  With one X / Y buffer (KA at nv 192) X / Y of
       // block gi is issued after the accumulation of gi - 1, which waited for that block's
       // epilogue: nothing can overlap the epilogue, and the tensor pipe's in-order execution
-      // already orders the reuse, so the wait would only add its round trip to the chain
-      if ((p.nbuf == 2 || AXONN_ATTN_NBUF1_WAIT) && accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);
+      // already orders the reuse, so the wait would only add its round trip to the chain.  The dQ
+      // kernel (!KA: its epilogue writes only dS) measured 2196 -> 1941 cycles per block without
+      // the wait and an epilogue 6 % slower (c11 trace), so it skips the wait too
+      if (((KA && p.nbuf == 2) || AXONN_ATTN_NBUF1_WAIT) && accd_n[b] > 0) mbar_wait(&acc_done[b], accd_ph[b] ^ 1);
       tc_fence_after();
       if (lane == 0) BWD_TRACE(2, gi);
       const uint32_t g1 = sG0 + stg * 2 * g_bytes, g2 = g1 + g_bytes;
