@@ -51,3 +51,34 @@ def test_default_workload_per_gpu_count(monkeypatch):
         if name == "gpt12b":
             assert cfg["hidden"] == 4512 and cfg["heads"] == 24 and cfg["microbatch"] == 8
             assert cfg["mb_per_replica"] == 64
+
+
+def test_memory_ledger_half_accumulation():
+    """The bench line's `memory`: the paper's 20 phi / 4 phi +
+    16 bsize beside ours, 2 phi theta16 + 2 phi half grad + 4 phi32 fp32 accumulators + (12 phi
+    | 36 bsize ring); with grad_accum_fp32 = 0 (D-38) phi32 counts only the vectors and the
+    embedding tables."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    class Oc:
+        def __init__(self, fp32):
+            self.bucket_elems, self.grad_accum_fp32 = 1000, fp32
+
+    class Eng:
+        def __init__(self, fp32):
+            self.oc = Oc(fp32)
+
+        def tensors(self):
+            return [("tok_emb", (10, 4), 40), ("l0.ln1_g", (4,), 4), ("l0.w_qkv", (12, 4), 48),
+                    ("l0.b_qkv", (12,), 12), ("l0.w_fc2", (4, 16), 64), ("head_w", (10, 4), 40)]
+
+    phi = 40 + 4 + 48 + 12 + 64 + 40
+    full = bench.memory_ledger(Eng(1), offload=False)
+    assert full["phi_fp32_accum"] == phi
+    assert full["ours_model_state_bytes"] == 4 * phi + 4 * phi + 12 * phi == full["paper_model_state_bytes"]
+    half = bench.memory_ledger(Eng(0), offload=True)
+    phi32 = 40 + 4 + 12
+    assert half["phi_fp32_accum"] == phi32
+    assert half["ours_model_state_bytes"] == 4 * phi + 4 * phi32 + 36 * 1000
+    assert half["paper_model_state_bytes"] == 4 * phi + 16 * 1000

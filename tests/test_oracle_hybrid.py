@@ -108,16 +108,18 @@ def test_half_accumulation_one_microbatch_is_rounded_exact_gradient(half):
     assert n_half == 4 * cfg.n_layers + 1   # w_qkv, w_o, w_fc1, w_fc2 per layer + head_w
 
 
+@pytest.mark.parametrize("half,u,eta", [("bf16", 2.0 ** -8, 2.0 ** -134), ("fp16", 2.0 ** -11, 2.0 ** -25)])
 @pytest.mark.parametrize("gi,gd,bm", [(1, 1, 1), (2, 1, 2), (2, 2, 1)])
-def test_half_accumulation_error_bound(gi, gd, bm):
+def test_half_accumulation_error_bound(gi, gd, bm, half, u, eta):
     """m microbatches: each step g <- RN(g + RN(dg)) errs by at most u |dg| and u |partial sum|
-    (bf16: 8 significant bits, unit roundoff u = 2^-8), so |g_half - g_exact| <= sum over
-    steps u (|dg| + |partial|) elementwise.  A dropped, doubled or sign-flipped microbatch
+    (bf16: 8 significant bits, unit roundoff u = 2^-8; fp16: 11 bits, u = 2^-11) plus, for a
+    subnormal result, half the subnormal spacing eta (fp16 2^-25, bf16 2^-134), so
+    |g_half - g_exact| <= sum over steps (u (|dg| + |partial|) + 2 eta) elementwise.  A dropped, doubled or sign-flipped microbatch
     breaks the bound by the size of a whole microbatch gradient."""
     cfg = TINY
     B = 8
     p, tok, (loss_ref, g_ref) = reference(cfg, B)
-    _, g = hybrid.hybrid_step(p, cfg, tok, gi, gd, bm, grad_accum="half")
+    _, g = hybrid.hybrid_step(p, cfg, tok, gi, gd, bm, grad_accum="half", half=half)
     m = B // (gd * bm)
     # per-step bound from the exact per-microbatch gradients of a replica's rows
     for k in g_ref:
@@ -132,7 +134,7 @@ def test_half_accumulation_error_bound(gi, gd, bm):
                 _, gm = model.full_batch_loss_and_grads(p, cfg, rows)
                 dg = gm[k] * bm / B          # pre-divided by M_total (D-9)
                 part = part + dg
-                bound += 2.0 ** -8 * (np.abs(dg) + np.abs(part))
+                bound += u * (np.abs(dg) + np.abs(part)) + 2 * eta
         err = np.abs(g[k] - g_ref[k])
         assert np.all(err <= bound + 1e-30), (k, float((err - bound).max()))
         assert not np.array_equal(g[k], g_ref[k]) or m == 1
