@@ -331,7 +331,10 @@ typedef struct {
   const void* bias; const void* resid; int64_t ld_resid; void* aux; int64_t ld_aux;
   float alpha;
   int max_ctas;   /* cap on resident CTAs (0 = all SMs) */
-  int variant;    /* 0 auto, 1 single-CTA 128x256 tiles, 2 CTA-pair 256x256 tiles (cta_group::2; TMA-store epilogue when eligible), 3 CTA pair with the thread-store epilogue, 4 CTA-pair 256x512 tiles where the epilogue allows (else 2) */
+  int variant;    /* 0 auto (CTA pairs for the linear layers, single CTAs for N <= 128 or M <= 128),
+                     1 single-CTA 128 x {128, 256} tiles, 2 CTA-pair 256 x 256 tiles (cta_group::2; the
+                     TMA-store epilogue when eligible; 256 x 128 pairs for N <= 128), 3 CTA pairs with the
+                     thread-store epilogue; other values: as 2 but 256 x 256 pairs for N <= 128 too */
 } axonn_gemm_args;
 AXONN_API int axonn_k_gemm(const axonn_gemm_args* args, void* stream);
 

@@ -2,6 +2,7 @@
 (no compute calls: runs on CPU-only hosts), and the Python binding fails
 loudly instead of falling back when a call cannot run."""
 import ctypes as C
+import os
 import re
 import subprocess
 
@@ -81,3 +82,36 @@ def test_bad_checkpoint_interval_rejected_before_device():
     with pytest.raises(AxoNNError) as e:
         AxoNN(1, 1, 1, n_layers=4, hidden=64, heads=2, seq_len=32, vocab=256, checkpoint_interval=3)
     assert e.value.status == "INVALID_ARG"
+
+
+def _header_structs():
+    """field names, in order, of every `typedef struct { ... } name;` in include/axonn.h"""
+    import re
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "include", "axonn.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    hdr = re.sub(r"//[^\n]*", "", hdr)
+    out = {}
+    for body, name in re.findall(r"typedef struct\s*\{(.*?)\}\s*(\w+)\s*;", hdr, flags=re.S):
+        fields = []
+        for decl in body.split(";"):
+            decl = " ".join(decl.split())
+            if not decl:
+                continue
+            # "const double* stage_speed", "double lr, beta1", "int64_t bucket_elems"
+            m = re.match(r"(?:const\s+)?[\w]+(?:\s*\*)?\s+(.*)$", decl)
+            for part in m.group(1).split(","):
+                fields.append(part.strip().lstrip("*").strip())
+        out[name] = fields
+    return out
+
+
+def test_ctypes_structs_match_the_header():
+    """The binding's ctypes Structures list the header's fields in the header's order (a
+    missing or reordered field would shift every later one silently)."""
+    from paper_2110_13005_b200 import _lib
+    hs = _header_structs()
+    for cname, py in (("axonn_model_cfg", _lib.ModelCfg), ("axonn_opt_cfg", _lib.OptCfg),
+                      ("axonn_dist", _lib.Dist), ("axonn_gemm_args", _lib.GemmArgs)):
+        assert cname in hs, (cname, list(hs))
+        assert [f for f, _ in py._fields_] == hs[cname], (cname, [f for f, _ in py._fields_], hs[cname])
