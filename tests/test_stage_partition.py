@@ -15,12 +15,7 @@ import pytest
 
 from paper_2110_13005_b200 import _lib
 
-W_ATT = 4.0   # default attention-core weight (engine.cpp balanced_blocks; AXONN_BAL_ATTN_W unset)
-
-
-@pytest.fixture(autouse=True)
-def _no_weight_override(monkeypatch):
-    monkeypatch.delenv("AXONN_BAL_ATTN_W", raising=False)
+W_ATT = 4.0   # attention-core weight of the cost model (reading D-21b)
 
 
 def partition(n_layers, hidden, seq, vocab, P, speed=None):
